@@ -1,0 +1,102 @@
+"""O10 Algorithm 1 (PCG in low-rank format) and O11 report; plus the setup chain
+O1-O5 for a `synth.Problem`.  (Oracle: test-only.)
+
+Algorithm 1 [P:1825-1872], verbatim line by line, with the readings:
+A13 stop when ||R^{k+1}|| / ||B|| <= tol_stop (tol_stop = 10 eps), A14 X^0 = 0,
+A15 R^0 = B untruncated, A16 beta_k's denominator reuses <R^k, Z^k>, A17 k_max = 100.
+Scalars are named a_k, b_k so they cannot clash with the operator's alpha, beta.
+"""
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import cp as cpm
+from .cp import CP
+from .sturm import eigenpairs
+from .spectral import FC_F, FC_G, spectral_cp
+from .truncate import truncate
+
+
+@dataclass
+class Setup:
+    lams: list
+    V: list
+    F: CP
+    G: CP
+    info: dict = field(default_factory=dict)
+
+
+def setup(problem, F_rank=None, G_rank=None, eps_D=None) -> Setup:
+    """sl_setup: O2/O3 per mode, then O5 for F (eps_D-driven) and G (rank r_G, SPD guard)."""
+    lams, V = [], []
+    for l in range(3):
+        lam, Vl = eigenpairs(problem.a_mid[l], problem.boundary)
+        lams.append(lam)
+        V.append(Vl)
+    eps_D = problem.eps if eps_D is None else eps_D
+    infoF, infoG = {}, {}
+    F = spectral_cp(lams, FC_F, problem.alpha, problem.beta, eps_D, rank=F_rank, info=infoF)
+    G = spectral_cp(lams, FC_G, problem.alpha, problem.beta, eps_D,
+                    rank=problem.precond_rank if G_rank is None else G_rank,
+                    spd_guard=True, info=infoG)
+    return Setup(lams, V, F, G, {"F": infoF, "G": infoG})
+
+
+class NotSPD(RuntimeError):
+    pass
+
+
+def pcg(fun, precond, B: CP, eps: float, tol_stop: float, kmax: int = 100, trunc=None):
+    """Algorithm 1.  fun/precond: CP -> CP (untruncated applies); trunc(x, eps) -> CP."""
+    trunc = truncate if trunc is None else trunc
+    rep = {"rel_res": [], "rank_X": [], "rank_R": [], "rank_Z": [], "rank_P": [],
+           "rank_S": [], "t_iter": [], "converged": False, "iters": 0}
+    normB = cpm.norm(B)
+    X = cpm.zeros(B.shape)                                   # X^(0) = 0          (A14)
+    R = B.copy()                                             # line 1, R^0 = B    (A15)
+    Z = trunc(precond(R), eps)                               # lines 2-3
+    P = Z.copy()                                             # line 4
+    rz = cpm.dot(R, Z)
+    for k in range(kmax):                                    # lines 6..21
+        t0 = time.perf_counter()
+        S = trunc(fun(P), eps)                               # lines 7-8
+        ps = cpm.dot(P, S)
+        if not np.isfinite(ps) or ps <= 0:
+            raise NotSPD(f"<P,S> = {ps} at iteration {k}")
+        a_k = rz / ps                                        # line 9
+        X = trunc(cpm.axpy(X, a_k, P), eps)                  # lines 10-11
+        R = trunc(cpm.axpy(R, -a_k, S), eps)                 # lines 12-13
+        rel = np.sqrt(max(cpm.dot(R, R), 0.0)) / normB       # line 14 (A13)
+        rep["rel_res"].append(rel)
+        rep["rank_S"].append(S.rank); rep["rank_X"].append(X.rank); rep["rank_R"].append(R.rank)
+        rep["iters"] = k + 1
+        if rel <= tol_stop:
+            rep["converged"] = True
+            rep["rank_Z"].append(Z.rank); rep["rank_P"].append(P.rank)
+            rep["t_iter"].append(time.perf_counter() - t0)
+            return X, rep
+        Z = trunc(precond(R), eps)                           # lines 17-18
+        rz_new = cpm.dot(R, Z)
+        b_k = rz_new / rz                                    # line 19 (A16)
+        P = trunc(cpm.axpy(Z, b_k, P), eps)                  # lines 20-21
+        rz = rz_new
+        rep["rank_Z"].append(Z.rank); rep["rank_P"].append(P.rank)
+        rep["t_iter"].append(time.perf_counter() - t0)
+    return X, rep
+
+
+def solve(problem, st: Setup | None = None, kmax=None, with_true_residual=False):
+    """pcg_solve for a synth.Problem: returns (u, report, setup)."""
+    st = setup(problem) if st is None else st
+    B = cpm.normalized(problem.b_w, problem.b_U)
+    fun = lambda x: cpm.apply(st.V, st.F, x)
+    pre = lambda x: cpm.apply(st.V, st.G, x)
+    u, rep = pcg(fun, pre, B, problem.eps, problem.tol_stop,
+                 problem.kmax if kmax is None else kmax)
+    if with_true_residual:                                   # O11
+        from .measure import diff_norm
+        rep["true_residual"] = diff_norm(fun(u), B) / cpm.norm(B)
+    return u, rep, st
