@@ -1,0 +1,172 @@
+/*
+ * fraccontrol.h — C ABI of the B200-native (sm_100a, FP64) rank-truncated PCG for the
+ * 3D fractional control equation  (beta * A^alpha + A^-alpha) u = b.
+ *
+ * Paper: Schmitt, Khoromskij, Khoromskaia, Schulz, arXiv 2006.09314 (PAPER.md, cited
+ * [P:line]).  Readings of ambiguous passages are numbered A1..A25 in DESIGN.md.
+ *
+ * Conventions (all entry points):
+ *  - Every double* inside fc_cp, and every pointer documented "device", is a DEVICE
+ *    pointer allocated by the caller (e.g. with PyTorch).  The library never frees caller
+ *    memory; it owns only the context and its workspace.  Pointers documented "host" are
+ *    host memory.
+ *  - A canonical (CP) tensor  x = sum_{k<rank} w[k] U[0][:,k] (x) U[1][:,k] (x) U[2][:,k]
+ *    [P:1706-1712] is stored as fc_cp: factor l is column-major n[l] x cap with leading
+ *    dimension ld[l] >= n[l] (column k starts at U[l] + k*ld[l]); weights w[cap].
+ *    Columns have unit 2-norm and the weights carry magnitude and sign (reading A18).
+ *    rank == 0 is the zero tensor.
+ *  - All work is ordered on the context's CUDA stream.  Calls that return host scalars or
+ *    reports (cp_dot, pcg_solve, the *_info outputs) synchronise that stream first.
+ *  - Return value: FC_OK (0), a warning (> 0) or an error (< 0).  No exception or abort
+ *    crosses the ABI; fc_last_error(ctx) describes the last failure.
+ *  - Use one context per host thread.
+ */
+#ifndef FRACCONTROL_H
+#define FRACCONTROL_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (SPEC error semantics) ------------------------------ */
+#define FC_OK                 0
+#define FC_NOT_CONVERGED      1   /* pcg_solve hit kmax (warning)                           */
+#define FC_RANK_CAP_HIT       2   /* a truncation was clipped at rank_cap (warning)         */
+#define FC_ERR_INVALID_ARG   -1   /* n < 2, alpha not in (0,1], beta <= 0, eps <= 0, ...    */
+#define FC_ERR_SHAPE         -2   /* mode sizes disagree with the context                   */
+#define FC_ERR_CAPACITY      -3   /* output cap too small; *_info->required_rank is set     */
+#define FC_ERR_NONPOS_COEF   -4   /* a midpoint coefficient <= 0 or non-finite              */
+#define FC_ERR_NOT_SPD       -5   /* <P,S> <= 0 in PCG, or spectral CP of G not positive    */
+#define FC_ERR_NAN           -6
+#define FC_ERR_EIG_NOCONV    -7
+#define FC_ERR_CUDA          -8
+#define FC_ERR_NOT_READY     -9   /* sl_setup (or sl_set_eigen + op_set_spectral_cp) missing */
+
+/* spectral functions of A [P:640-648], mapped per reading A5 */
+#define FC_F          0   /* F(lam)  = beta*lam^alpha + lam^-alpha   (the operator F_2)     */
+#define FC_G          1   /* G(lam)  = 1/F(lam)                      (preconditioner F_3,B)  */
+#define FC_POW_PLUS   2   /* lam^alpha                                (F_1)                  */
+#define FC_POW_MINUS  3   /* lam^-alpha                               (state y = A^-alpha u) */
+
+#define FC_MAX_ITERS 256
+
+typedef struct fc_ctx_s* fc_ctx;
+
+typedef struct {
+    int n[3];        /* mode sizes (all equal to the context's n)                            */
+    int rank;        /* number of terms in use                                               */
+    int cap;         /* allocated columns (>= rank)                                          */
+    double* w;       /* device, [cap]                                                        */
+    double* U[3];    /* device, column-major n[l] x cap, leading dimension ld[l]             */
+    int ld[3];
+} fc_cp;
+
+typedef struct {
+    double alpha;        /* fractional order, (0, 1]                            [P:255]    */
+    double beta;         /* weight of A^alpha; A^-alpha has weight 1 (A5)        [P:436]    */
+    double eps;          /* truncation threshold (relative, A11/A12)             [P:989]    */
+    double tol_stop;     /* PCG stop ||R||/||B|| <= tol_stop (A13); <= 0 -> 10*eps         */
+    double eps_D;        /* tolerance of the spectral CP of F (A8); <= 0 -> eps            */
+    int kmax;            /* max PCG iterations (A17); <= 0 -> 100                           */
+    int precond_rank;    /* rank r_G of the preconditioner CP (A7); <= 0 -> 6    [P:990]    */
+    int op_rank;         /* > 0: fixed rank of the operator CP (C5 sweep); 0: eps_D-driven  */
+    int rank_cap;        /* max CP rank of any iterate (capacity); <= 0 -> 4096             */
+    int boundary;        /* 0: paper boundary rule [P:517-518] (A2); 1: standard            */
+} fc_params;
+
+typedef struct {
+    int tucker_rank[3];  /* RHOSVD ranks r_l                                                */
+    int out_rank;        /* canonical rank after Tucker-to-canonical                       */
+    int required_rank;   /* set with FC_ERR_CAPACITY                                        */
+    int in_rank;         /* terms after dropping zero terms                                 */
+    int basis_dim[3];    /* dimension of the reduced side-matrix basis per mode            */
+    int t2c_mode;        /* slicing mode of the T2C step                                    */
+    double energy;       /* sum xi^2 of the input                                           */
+    double min_cut_margin; /* min over cuts |tail(r) - thr| / thr (A23 noise band log)      */
+} fc_trunc_info;
+
+typedef struct {
+    int iters;
+    int converged;
+    int status;
+    double rel_res[FC_MAX_ITERS];
+    int rank_X[FC_MAX_ITERS], rank_R[FC_MAX_ITERS], rank_Z[FC_MAX_ITERS];
+    int rank_P[FC_MAX_ITERS], rank_S[FC_MAX_ITERS];
+    int tucker_S[FC_MAX_ITERS];     /* max_l r_l of the S truncation                         */
+    double t_iter_ms[FC_MAX_ITERS];
+    double t_total_ms;              /* whole pcg_solve (device events)                       */
+    double t_loop_ms;               /* loop only: iterations/s = iters / t_loop_ms * 1e3     */
+    double normB;
+} fc_pcg_report;
+
+/* ---- context -------------------------------------------------------------------------- */
+/* cuda_stream: a cudaStream_t (NULL = legacy default stream).  Binds the current device. */
+int fc_create(fc_ctx* ctx, void* cuda_stream);
+int fc_destroy(fc_ctx ctx);
+const char* fc_last_error(fc_ctx ctx);
+int fc_set_stream(fc_ctx ctx, void* cuda_stream);
+
+/* ---- setup: S1..S4 ------------------------------------------------------------------- */
+/* sl_setup  [P:443-561, P:688-722]
+ *   a_mid: HOST, 3 x (n+1) row-major; a_mid[l*(n+1)+i] = a_l((i+1/2)h), h = 1/(n+1) (A1).
+ *   Assembles the three 1D FD operators (A2, A3), computes their eigenpairs on the device
+ *   (Sturm bisection on the Golub-Kahan form of the bidiagonal factor + inverse iteration),
+ *   then the spectral CPs of F (eps_D-driven, or rank op_rank) and G (rank precond_rank,
+ *   raised until positive on the grid: SPD guard A7).  Errors: INVALID_ARG, NONPOS_COEF,
+ *   EIG_NOCONV, NOT_SPD, CUDA. */
+int sl_setup(fc_ctx ctx, int n, const double* a_mid, const fc_params* p);
+
+/* Eigenpairs of mode l: lam (device, n, ascending) and V (device, n x n column-major,
+ * column j = eigenvector j; sign: largest-magnitude entry positive, reading A4). */
+int sl_get_eigen(fc_ctx ctx, int mode, double* lam, double* V);
+/* Inject eigenpairs (shared-input parity).  Call for all 3 modes; n fixed by the first call
+ * (or by sl_setup).  Also stores alpha/beta/eps from p for later op_set_spectral_cp use. */
+int sl_set_eigen(fc_ctx ctx, int n, int mode, const double* lam, const double* V, const fc_params* p);
+
+/* Spectral CP of `which` (FC_F, FC_G, ...): D[i,j,k] ~ F(lam1_i + lam2_j + lam3_k) [P:693].
+ * get: out->cap must be >= its rank (else CAPACITY, out->rank = required).  set: copies. */
+int op_get_spectral_cp(fc_ctx ctx, int which, fc_cp* out);
+int op_set_spectral_cp(fc_ctx ctx, int which, const fc_cp* in);
+int op_spectral_rank(fc_ctx ctx, int which, int* rank, int* tucker_rank /* [3] or NULL */);
+
+/* ---- the operator: S5..S8 -------------------------------------------------------------- */
+/* fracop_apply  [P:597-623]:  y = F(A) x  =  sum_k sum_j (x)_l V_l (u_l^k . V_l^T x_l^j)
+ *   Term order t = k*x.rank + j (A19); y.rank = r_which * x.rank, untruncated; y's columns
+ *   normalised (norms folded into the weights).  y.cap >= r*x.rank else CAPACITY.
+ *   x and y must not alias. */
+int fracop_apply(fc_ctx ctx, int which, const fc_cp* x, fc_cp* y);
+/* precond_apply = fracop_apply(FC_G)  (case (B) preconditioner [P:956-959], A6). */
+int precond_apply(fc_ctx ctx, const fc_cp* x, fc_cp* y);
+
+/* ---- CP algebra: S9, S10 ----------------------------------------------------------------- */
+/* cp_dot [P:1748-1755]: *out_host = sum_{k,m} xi_k zeta_m prod_l <u_k^l, v_m^l>. */
+int cp_dot(fc_ctx ctx, const fc_cp* x, const fc_cp* y, double* out_host);
+/* z = x + a*y by concatenation [x terms ; a*y terms] (ranks add) [P:1845-1866]. */
+int cp_axpy(fc_ctx ctx, const fc_cp* x, double a, const fc_cp* y, fc_cp* z);
+
+/* ---- truncation: S11..S13 ---------------------------------------------------------------- */
+/* cp_truncate [P:187-190, P:1791-1816]: RHOSVD (C2T) at threshold eps, Tucker core, then
+ * Tucker-to-canonical (slice SVD along the min-rank mode).  Output is an orthogonal CP
+ * (mutually orthogonal terms).  y.cap too small -> CAPACITY with info->required_rank.
+ * info may be NULL.  x and y must not alias. */
+int cp_truncate(fc_ctx ctx, const fc_cp* x, double eps, fc_cp* y, fc_trunc_info* info);
+
+/* ---- the solver: S14 ------------------------------------------------------------------ */
+/* pcg_solve: Algorithm 1 [P:1825-1872] with fun = fracop_apply(FC_F), precond =
+ * fracop_apply(FC_G), trunc = cp_truncate(eps); X0 = 0 (A14), R0 = B untruncated (A15).
+ * Returns FC_OK, FC_NOT_CONVERGED, or an error; u (device CP, cap >= final rank, else
+ * CAPACITY) receives X; rep (host, may be NULL) the per-iteration history. */
+int pcg_solve(fc_ctx ctx, const fc_cp* b, const fc_params* p, fc_cp* u, fc_pcg_report* rep);
+
+/* ---- raw kernels exposed for tests/bench (same ABI rules) ------------------------------- */
+/* C = alpha*op(A)*op(B) + beta*C, FP64, column-major, DMMA tiles; all pointers device.   */
+int fc_dgemm(fc_ctx ctx, int transA, int transB, int M, int N, int K, double alpha,
+             const double* A, int lda, const double* B, int ldb, double beta, double* C, int ldc);
+/* Milliseconds of the last launch of the dominant kernel of the last API call (events on
+ * the context stream) and its algorithmic flop and byte counts (for the roofline line). */
+int fc_last_kernel_stats(fc_ctx ctx, double* ms, double* flops, double* bytes, int* launches);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FRACCONTROL_H */

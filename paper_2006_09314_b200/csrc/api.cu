@@ -1,0 +1,361 @@
+// C-ABI entry points (include/fraccontrol.h): context, eigen/spectral-CP injection,
+// fracop_apply (S5-S8), cp_dot (S10), cp_axpy (S9), raw DGEMM, kernel stats.
+#include <algorithm>
+#include <cmath>
+#include "cpops.cuh"
+#include "ctx.cuh"
+#include "solver.cuh"
+
+using namespace fc;
+
+namespace {
+
+template <class F>
+int guard(fc_ctx c, F&& f) {
+  try {
+    return f();
+  } catch (const Error& e) {
+    if (c) c->err = e.msg;
+    return e.code;
+  } catch (const std::exception& e) {
+    if (c) c->err = e.what();
+    return FC_ERR_CUDA;
+  }
+}
+
+void check_cp(fc_ctx c, const fc_cp* x, const char* name) {
+  require(x != nullptr, FC_ERR_INVALID_ARG, std::string(name) + " is NULL");
+  require(c->n > 0, FC_ERR_NOT_READY, "no eigenpairs: call sl_setup or sl_set_eigen first");
+  for (int l = 0; l < 3; ++l) {
+    require(x->n[l] == c->n, FC_ERR_SHAPE, std::string(name) + ": mode size differs from context n");
+    require(x->ld[l] >= x->n[l], FC_ERR_INVALID_ARG, std::string(name) + ": ld < n");
+    require(x->rank == 0 || x->U[l] != nullptr, FC_ERR_INVALID_ARG, std::string(name) + ": NULL factor");
+  }
+  require(x->rank >= 0 && x->rank <= x->cap, FC_ERR_INVALID_ARG, std::string(name) + ": rank > cap");
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------------------
+namespace fc {
+
+// y = F(A) x for a plain CP (S5-S8).  The dominant launch (inverse transform) is bracketed by
+// the context's events.
+void apply_plain(fc_ctx c, const SpecCP& sp, const fc_cp& x, fc_cp& y) {
+  const int n = c->n, r = sp.r, R = x.rank;
+  cudaStream_t st = c->st;
+  y.rank = r * R;
+  if (R == 0 || r == 0) {
+    y.rank = 0;
+    return;
+  }
+  Scratch s(st);
+  double* What = s.alloc<double>((size_t)3 * n * R);
+  double* Usq = s.alloc<double>((size_t)3 * n * r);
+  double* Wsq = s.alloc<double>((size_t)3 * n * R);
+  double* N2 = s.alloc<double>((size_t)3 * r * R);
+  double* cs = s.alloc<double>((size_t)3 * r * R);
+
+  // S5 forward transform  W_l = V_l^T X_l  (3 modes batched)
+  GemmArgs f;
+  f.transA = 1;
+  f.nbatch = 3;
+  for (int l = 0; l < 3; ++l)
+    f.b[l] = GemmBatch{n, R, n, c->V_l(l), n, x.U[l], x.ld[l], What + (size_t)l * n * R, n, nullptr, 0, nullptr};
+  gemm(f, st);
+
+  // S8 (moved ahead): column norms of u_k (.) w_j; ||V y|| = ||y|| since V is orthogonal
+  Mat3 a{}, as{}, b{}, bs{};
+  for (int l = 0; l < 3; ++l) {
+    a.p[l] = sp.Ul(n, l); a.ld[l] = n; a.rows[l] = n; a.cols[l] = r;
+    as.p[l] = Usq + (size_t)l * n * r; as.ld[l] = n; as.rows[l] = n; as.cols[l] = r;
+    b.p[l] = What + (size_t)l * n * R; b.ld[l] = n; b.rows[l] = n; b.cols[l] = R;
+    bs.p[l] = Wsq + (size_t)l * n * R; bs.ld[l] = n; bs.rows[l] = n; bs.cols[l] = R;
+  }
+  square3(a, as, st);
+  square3(b, bs, st);
+  GemmArgs g2;
+  g2.transA = 1;
+  g2.nbatch = 3;
+  for (int l = 0; l < 3; ++l)
+    g2.b[l] = GemmBatch{r, R, n, Usq + (size_t)l * n * r, n, Wsq + (size_t)l * n * R, n, N2 + (size_t)l * r * R, r,
+                        nullptr, 0, nullptr};
+  gemm(g2, st);
+  const double* N2p[3] = {N2, N2 + (size_t)r * R, N2 + (size_t)2 * r * R};
+  double* csp[3] = {cs, cs + (size_t)r * R, cs + (size_t)2 * r * R};
+  apply_weights(r, R, sp.w.p, x.w, N2p, y.w, csp, st);
+
+  // S6+S7 inverse transform with the Khatri-Rao operand fused: Y_l = V_l [u_k (.) w_j]_t
+  GemmArgs iv;
+  iv.nbatch = 3;
+  iv.krR = R;
+  for (int l = 0; l < 3; ++l)
+    iv.b[l] = GemmBatch{n, r * R, n, c->V_l(l), n, What + (size_t)l * n * R, n, y.U[l], y.ld[l],
+                        sp.Ul(n, l), n, csp[l]};
+  FC_CUDA_TRY(cudaEventRecord(c->e0, st));
+  gemm(iv, st);
+  FC_CUDA_TRY(cudaEventRecord(c->e1, st));
+  c->k_flops = 3.0 * 2.0 * (double)n * n * (double)r * R;
+  c->k_bytes = 3.0 * 8.0 * ((double)n * n + (double)n * R + (double)n * r + (double)n * r * R);
+  c->k_launches = 1;
+}
+
+// Cross Grams G_l = X_l^T Y_l (3 modes) into G (3 blocks of R1 x R2, ld R1).
+void cross_gram(cudaStream_t st, int n, int R1, const double* const X[3], const int ldx[3], int R2,
+                const double* const Y[3], const int ldy[3], double* G) {
+  size_t blk = (size_t)R1 * R2;
+  FC_CUDA_TRY(cudaMemsetAsync(G, 0, 3 * blk * sizeof(double), st));
+  GemmArgs g;
+  g.transA = 1;
+  g.nbatch = 3;
+  g.beta = 1.0;
+  int tiles = cdiv(R1, 64) * cdiv(R2, 64) * 3;
+  g.splitk = std::max(1, std::min(cdiv(n, 128), cdiv(148 * 4, tiles)));
+  for (int l = 0; l < 3; ++l) g.b[l] = GemmBatch{R1, R2, n, X[l], ldx[l], Y[l], ldy[l], G + l * blk, R1, nullptr, 0, nullptr};
+  gemm(g, st);
+}
+
+double dot_plain(fc_ctx c, const fc_cp& x, const fc_cp& y) {
+  if (x.rank == 0 || y.rank == 0) return 0.0;
+  Scratch s(c->st);
+  const int R1 = x.rank, R2 = y.rank;
+  double* G = s.alloc<double>((size_t)3 * R1 * R2 + 1);
+  double* out = G + (size_t)3 * R1 * R2;
+  const double* X[3] = {x.U[0], x.U[1], x.U[2]};
+  const double* Y[3] = {y.U[0], y.U[1], y.U[2]};
+  cross_gram(c->st, c->n, R1, X, x.ld, R2, Y, y.ld, G);
+  const double* Gp[3] = {G, G + (size_t)R1 * R2, G + (size_t)2 * R1 * R2};
+  dot_reduce(R1, R2, x.w, y.w, Gp, R1, out, c->st);
+  double h = 0;
+  FC_CUDA_TRY(cudaMemcpyAsync(&h, out, sizeof(double), cudaMemcpyDeviceToHost, c->st));
+  FC_CUDA_TRY(cudaStreamSynchronize(c->st));
+  return h;
+}
+
+void copy_cp_block(cudaStream_t st, int n, const fc_cp& src, fc_cp& dst, int col0, double scale) {
+  if (src.rank == 0) return;
+  Mat3 a{}, b{};
+  for (int l = 0; l < 3; ++l) {
+    a.p[l] = src.U[l]; a.ld[l] = src.ld[l]; a.rows[l] = n; a.cols[l] = src.rank;
+    b.p[l] = dst.U[l] + (size_t)col0 * dst.ld[l]; b.ld[l] = dst.ld[l]; b.rows[l] = n; b.cols[l] = src.rank;
+  }
+  copy_cols3(a, b, 1.0, st);
+  scale_copy(src.rank, src.w, scale, dst.w + col0, st);
+}
+
+}  // namespace fc
+
+// ======================================================================================
+extern "C" {
+
+int fc_create(fc_ctx* ctx, void* cuda_stream) {
+  if (!ctx) return FC_ERR_INVALID_ARG;
+  *ctx = nullptr;
+  fc_ctx c = new fc_ctx_s();
+  int rc = guard(c, [&]() {
+    FC_CUDA_TRY(cudaGetDevice(&c->dev));
+    c->st = (cudaStream_t)cuda_stream;
+    FC_CUDA_TRY(cudaEventCreate(&c->e0));
+    FC_CUDA_TRY(cudaEventCreate(&c->e1));
+    cudaMemPool_t pool;
+    FC_CUDA_TRY(cudaDeviceGetDefaultMemPool(&pool, c->dev));
+    uint64_t thr = UINT64_MAX;
+    FC_CUDA_TRY(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    return FC_OK;
+  });
+  if (rc != FC_OK) {
+    delete c;
+    return rc;
+  }
+  *ctx = c;
+  return FC_OK;
+}
+
+int fc_destroy(fc_ctx c) {
+  if (!c) return FC_OK;
+  cudaStreamSynchronize(c->st);
+  c->lam.release();
+  c->V.release();
+  for (auto& s : c->spec) {
+    s.w.release(); s.U.release(); s.W.release(); s.E.release();
+  }
+  if (c->e0) cudaEventDestroy(c->e0);
+  if (c->e1) cudaEventDestroy(c->e1);
+  delete c;
+  return FC_OK;
+}
+
+const char* fc_last_error(fc_ctx c) { return c ? c->err.c_str() : "NULL context"; }
+
+int fc_set_stream(fc_ctx c, void* s) {
+  if (!c) return FC_ERR_INVALID_ARG;
+  c->st = (cudaStream_t)s;
+  return FC_OK;
+}
+
+int sl_get_eigen(fc_ctx c, int mode, double* lam, double* V) {
+  return guard(c, [&]() {
+    require(mode >= 0 && mode < 3, FC_ERR_INVALID_ARG, "mode");
+    require(c->n > 0 && c->have_eig[mode], FC_ERR_NOT_READY, "no eigenpairs");
+    size_t n = c->n;
+    if (lam) FC_CUDA_TRY(cudaMemcpyAsync(lam, c->lam_l(mode), n * 8, cudaMemcpyDeviceToDevice, c->st));
+    if (V) FC_CUDA_TRY(cudaMemcpyAsync(V, c->V_l(mode), n * n * 8, cudaMemcpyDeviceToDevice, c->st));
+    FC_CUDA_TRY(cudaStreamSynchronize(c->st));
+    return FC_OK;
+  });
+}
+
+int sl_set_eigen(fc_ctx c, int n, int mode, const double* lam, const double* V, const fc_params* p) {
+  return guard(c, [&]() {
+    require(mode >= 0 && mode < 3 && n >= 2 && lam && V, FC_ERR_INVALID_ARG, "sl_set_eigen args");
+    if (c->n != n) {
+      c->n = n;
+      c->lam.ensure((size_t)3 * n);
+      c->V.ensure((size_t)3 * n * n);
+      for (auto& h : c->have_eig) h = false;
+      for (auto& s : c->spec) s.valid = false;
+    }
+    if (p) {
+      c->p = *p;
+      c->have_params = true;
+    }
+    FC_CUDA_TRY(cudaMemcpyAsync(c->lam_l(mode), lam, (size_t)n * 8, cudaMemcpyDeviceToDevice, c->st));
+    FC_CUDA_TRY(cudaMemcpyAsync(c->V_l(mode), V, (size_t)n * n * 8, cudaMemcpyDeviceToDevice, c->st));
+    FC_CUDA_TRY(cudaStreamSynchronize(c->st));
+    c->have_eig[mode] = true;
+    return FC_OK;
+  });
+}
+
+int op_set_spectral_cp(fc_ctx c, int which, const fc_cp* in) {
+  return guard(c, [&]() {
+    require(which >= 0 && which < 4, FC_ERR_INVALID_ARG, "which");
+    check_cp(c, in, "in");
+    SpecCP& s = c->spec[which];
+    const int n = c->n, r = in->rank;
+    s.r = r;
+    s.w.ensure(std::max(r, 1));
+    s.U.ensure((size_t)3 * n * std::max(r, 1));
+    fc_cp dst{};
+    for (int l = 0; l < 3; ++l) {
+      dst.n[l] = n; dst.U[l] = s.U.p + (size_t)l * n * r; dst.ld[l] = n;
+    }
+    dst.w = s.w.p; dst.rank = r; dst.cap = r;
+    copy_cp_block(c->st, n, *in, dst, 0, 1.0);
+    FC_CUDA_TRY(cudaStreamSynchronize(c->st));
+    s.valid = true;
+    s.has_basis = false;
+    return FC_OK;
+  });
+}
+
+int op_get_spectral_cp(fc_ctx c, int which, fc_cp* out) {
+  return guard(c, [&]() {
+    require(which >= 0 && which < 4, FC_ERR_INVALID_ARG, "which");
+    SpecCP& s = c->spec[which];
+    require(s.valid, FC_ERR_NOT_READY, "spectral CP not set");
+    check_cp(c, out, "out");
+    if (out->cap < s.r) {
+      out->rank = s.r;
+      throw Error(FC_ERR_CAPACITY, "out.cap < spectral rank");
+    }
+    fc_cp src{};
+    for (int l = 0; l < 3; ++l) {
+      src.n[l] = c->n; src.U[l] = s.U.p + (size_t)l * c->n * s.r; src.ld[l] = c->n;
+    }
+    src.w = s.w.p; src.rank = s.r; src.cap = s.r;
+    copy_cp_block(c->st, c->n, src, *out, 0, 1.0);
+    out->rank = s.r;
+    FC_CUDA_TRY(cudaStreamSynchronize(c->st));
+    return FC_OK;
+  });
+}
+
+int op_spectral_rank(fc_ctx c, int which, int* rank, int* tucker) {
+  return guard(c, [&]() {
+    require(which >= 0 && which < 4, FC_ERR_INVALID_ARG, "which");
+    SpecCP& s = c->spec[which];
+    require(s.valid, FC_ERR_NOT_READY, "spectral CP not set");
+    if (rank) *rank = s.r;
+    if (tucker)
+      for (int l = 0; l < 3; ++l) tucker[l] = s.tucker_rank[l];
+    return FC_OK;
+  });
+}
+
+int fracop_apply(fc_ctx c, int which, const fc_cp* x, fc_cp* y) {
+  return guard(c, [&]() {
+    require(which >= 0 && which < 4, FC_ERR_INVALID_ARG, "which");
+    check_cp(c, x, "x");
+    check_cp(c, y, "y");
+    require(c->have_eig[0] && c->have_eig[1] && c->have_eig[2], FC_ERR_NOT_READY, "eigenpairs missing");
+    const SpecCP& s = c->spec[which];
+    require(s.valid, FC_ERR_NOT_READY, "spectral CP not set");
+    long long need = (long long)s.r * x->rank;
+    if (y->cap < need) {
+      y->rank = (int)std::min<long long>(need, INT32_MAX);
+      throw Error(FC_ERR_CAPACITY, "y.cap < r * x.rank");
+    }
+    apply_plain(c, s, *x, *y);
+    return FC_OK;
+  });
+}
+
+int precond_apply(fc_ctx c, const fc_cp* x, fc_cp* y) { return fracop_apply(c, FC_G, x, y); }
+
+int cp_dot(fc_ctx c, const fc_cp* x, const fc_cp* y, double* out) {
+  return guard(c, [&]() {
+    check_cp(c, x, "x");
+    check_cp(c, y, "y");
+    require(out != nullptr, FC_ERR_INVALID_ARG, "out NULL");
+    *out = dot_plain(c, *x, *y);
+    return std::isfinite(*out) ? FC_OK : FC_ERR_NAN;
+  });
+}
+
+int cp_axpy(fc_ctx c, const fc_cp* x, double a, const fc_cp* y, fc_cp* z) {
+  return guard(c, [&]() {
+    check_cp(c, x, "x");
+    check_cp(c, y, "y");
+    check_cp(c, z, "z");
+    int need = x->rank + y->rank;
+    if (z->cap < need) {
+      z->rank = need;
+      throw Error(FC_ERR_CAPACITY, "z.cap < x.rank + y.rank");
+    }
+    copy_cp_block(c->st, c->n, *x, *z, 0, 1.0);
+    copy_cp_block(c->st, c->n, *y, *z, x->rank, a);
+    z->rank = need;
+    FC_CUDA_TRY(cudaStreamSynchronize(c->st));
+    return FC_OK;
+  });
+}
+
+int fc_dgemm(fc_ctx c, int transA, int transB, int M, int N, int K, double alpha, const double* A, int lda,
+             const double* B, int ldb, double beta, double* C, int ldc) {
+  return guard(c, [&]() {
+    require(M >= 0 && N >= 0 && K >= 0, FC_ERR_INVALID_ARG, "dims");
+    FC_CUDA_TRY(cudaEventRecord(c->e0, c->st));
+    dgemm(c->st, transA, transB, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+    FC_CUDA_TRY(cudaEventRecord(c->e1, c->st));
+    c->k_flops = 2.0 * M * (double)N * K;
+    c->k_bytes = 8.0 * ((double)M * K + (double)K * N + (double)M * N * (beta != 0 ? 2 : 1));
+    c->k_launches = 1;
+    return FC_OK;
+  });
+}
+
+int fc_last_kernel_stats(fc_ctx c, double* ms, double* flops, double* bytes, int* launches) {
+  return guard(c, [&]() {
+    float t = 0;
+    FC_CUDA_TRY(cudaEventSynchronize(c->e1));
+    FC_CUDA_TRY(cudaEventElapsedTime(&t, c->e0, c->e1));
+    if (ms) *ms = t;
+    if (flops) *flops = c->k_flops;
+    if (bytes) *bytes = c->k_bytes;
+    if (launches) *launches = c->k_launches;
+    return FC_OK;
+  });
+}
+
+}  // extern "C"

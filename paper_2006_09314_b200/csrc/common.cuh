@@ -1,0 +1,107 @@
+// Internal header of libfraccontrol (B200 / sm_100a, FP64).  Not part of the ABI.
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <cstdio>
+#include <string>
+#include <vector>
+#include "../../include/fraccontrol.h"
+
+#define FC_CUDA_TRY(expr)                                                            \
+  do {                                                                              \
+    cudaError_t _e = (expr);                                                        \
+    if (_e != cudaSuccess) {                                                        \
+      throw fc::Error(FC_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e)); \
+    }                                                                               \
+  } while (0)
+
+#define FC_CHECK_LAUNCH() FC_CUDA_TRY(cudaGetLastError())
+
+namespace fc {
+
+struct Error {
+  int code;
+  std::string msg;
+  Error(int c, std::string m) : code(c), msg(std::move(m)) {}
+};
+
+inline void require(bool cond, int code, const std::string& msg) {
+  if (!cond) throw Error(code, msg);
+}
+
+inline int cdiv(long long a, long long b) { return (int)((a + b - 1) / b); }
+
+// ---- stream-ordered device scratch (cudaMallocAsync from the device's default pool) ----
+struct Scratch {
+  cudaStream_t st;
+  std::vector<void*> ptrs;
+  explicit Scratch(cudaStream_t s) : st(s) {}
+  template <class T>
+  T* alloc(size_t count) {
+    void* p = nullptr;
+    size_t bytes = count * sizeof(T);
+    if (bytes == 0) bytes = 16;
+    bytes = (bytes + 255) & ~size_t(255);
+    FC_CUDA_TRY(cudaMallocAsync(&p, bytes, st));
+    ptrs.push_back(p);
+    return (T*)p;
+  }
+  template <class T>
+  T* zeros(size_t count) {
+    T* p = alloc<T>(count);
+    FC_CUDA_TRY(cudaMemsetAsync(p, 0, count * sizeof(T) ? count * sizeof(T) : 16, st));
+    return p;
+  }
+  ~Scratch() {
+    for (void* p : ptrs) cudaFreeAsync(p, st);
+  }
+};
+
+// ---- a device-resident buffer owned by the context (released in fc_destroy) -----------
+struct DBuf {
+  double* p = nullptr;
+  size_t n = 0;
+  void ensure(size_t count) {
+    if (count <= n && p) return;
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+    if (count == 0) return;
+    FC_CUDA_TRY(cudaMalloc(&p, count * sizeof(double)));
+    n = count;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+};
+
+// ---- batched FP64 GEMM on DMMA tiles (gemm.cu) ----------------------------------------
+// C_b = alpha * op(A_b) * op(B_b) + beta * C_b, column-major; op(A) is M x K, op(B) K x N.
+// KR-fused B operand (transB = 0 only): op(B)(k, c) = krU[k + (c / krR)*ldkr] * B[k + (c % krR)*ldb]
+// Column scale (epilogue): C(:, c) *= colscale[c] before alpha/beta.
+constexpr int kMaxBatch = 8;
+struct GemmBatch {
+  int M, N, K;
+  const double* A; int lda;
+  const double* B; int ldb;
+  double* C; int ldc;
+  const double* krU; int ldkr;
+  const double* colscale;
+};
+struct GemmArgs {
+  int transA = 0, transB = 0;
+  int krR = 0;           // > 0 enables the Khatri-Rao B operand
+  int splitk = 1;        // > 1: atomicAdd epilogue (beta must be 1, C pre-initialised)
+  double alpha = 1.0, beta = 0.0;
+  int nbatch = 0;
+  GemmBatch b[kMaxBatch];
+};
+void gemm(const GemmArgs& a, cudaStream_t st);
+// convenience single GEMM
+void dgemm(cudaStream_t st, int transA, int transB, int M, int N, int K, double alpha,
+           const double* A, int lda, const double* B, int ldb, double beta, double* C, int ldc,
+           int splitk = 1);
+
+}  // namespace fc

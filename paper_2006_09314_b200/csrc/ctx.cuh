@@ -1,0 +1,36 @@
+// Library context (opaque behind fc_ctx in the ABI).
+#pragma once
+#include "common.cuh"
+
+struct SpecCP {
+  int r = 0;          // CP rank
+  fc::DBuf w;         // [r]
+  fc::DBuf U;         // 3 blocks, mode l at U.p + l*n*r, column-major n x r, unit columns
+  // reduced (mixed Tucker-canonical) form U_l = W_l E_l, W_l orthonormal n x s_l [P:1804-1812]
+  int s[3] = {0, 0, 0};
+  fc::DBuf W;         // 3 blocks of n x s_l at W.p + l*n*smax
+  fc::DBuf E;         // 3 blocks of s_l x r at E.p + l*smax*r
+  int smax = 0;
+  bool valid = false;
+  bool has_basis = false;
+  int tucker_rank[3] = {0, 0, 0};
+  double* Ul(int n, int l) const { return U.p + (size_t)l * n * r; }
+};
+
+struct fc_ctx_s {
+  cudaStream_t st = nullptr;
+  int dev = 0;
+  int n = 0;
+  fc_params p{};
+  bool have_params = false;
+  fc::DBuf lam;       // 3 x n
+  fc::DBuf V;         // 3 x n x n (mode-major, each column-major)
+  bool have_eig[3] = {false, false, false};
+  SpecCP spec[4];
+  std::string err;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  double k_flops = 0, k_bytes = 0;
+  int k_launches = 0;
+  double* lam_l(int l) const { return lam.p + (size_t)l * n; }
+  double* V_l(int l) const { return V.p + (size_t)l * n * n; }
+};

@@ -1,0 +1,533 @@
+// Eigen machinery on the device.
+//
+// (a) S1-S3, the 1D Sturm-Liouville eigenpairs [P:466-542]: assembly of the bidiagonal factor
+//     C (T = C^T C, the paper's weak form [P:477]), Sturm-count bisection on the Golub-Kahan
+//     zero-diagonal tridiagonal of C (singular values to high relative accuracy, lam = s^2),
+//     inverse iteration per eigenvector on T, sign rule, Newton-Schulz orthogonality polish on
+//     DMMA GEMMs.  One thread per eigenvalue / eigenvector: n independent problems per mode.
+// (b) The small symmetric eigensolves of the truncation (S11): Householder tridiagonalisation
+//     (one CTA per matrix), bisection for all eigenvalues (thread per eigenvalue), inverse
+//     iteration for the leading r vectors, CGS2 re-orthonormalisation, back-transformation.
+#include <cfloat>
+#include "eig.cuh"
+
+namespace fc {
+namespace {
+
+constexpr double kEps = DBL_EPSILON;
+
+// ---------------------------------------------------------------------------------------
+// (a) 1D setup
+// ---------------------------------------------------------------------------------------
+// per mode: a~ (paper boundary rule A2), s_r = sqrt(a~_r)/h (r = 0..n), d, e of T = C^T C.
+__global__ void sl_assemble_kernel(int n, const double* __restrict__ a_mid, int boundary, double* s_out,
+                                   double* d_out, double* e_out, int* status) {
+  const int l = blockIdx.y;
+  const double* a = a_mid + (size_t)l * (n + 1);
+  double* s = s_out + (size_t)l * (n + 1);
+  double* d = d_out + (size_t)l * n;
+  double* e = e_out + (size_t)l * n;
+  const double h = 1.0 / (n + 1), ih2 = 1.0 / (h * h);
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r <= n; r += gridDim.x * blockDim.x) {
+    int src = r;
+    if (boundary == 0) {
+      if (r == 0) src = 1;
+      if (r == n) src = n - 1;
+    }
+    double ar = a[src];
+    if (!(ar > 0.0) || !isfinite(ar)) atomicExch(status, FC_ERR_NONPOS_COEF);
+    s[r] = sqrt(ar) / h;
+    if (r < n) {
+      int s0 = r, s1 = r + 1;
+      if (boundary == 0) {
+        if (s0 == 0) s0 = 1;
+        if (s1 == n) s1 = n - 1;
+      }
+      d[r] = (a[s0] + a[s1]) * ih2;
+      if (r < n - 1) e[r] = -a[s1] * ih2;
+    }
+  }
+}
+
+// #{ singular values of C < x } via the Sturm count of the (2n+1) zero-diagonal Golub-Kahan
+// tridiagonal with off-diagonals |f| = (s0, s1, s1, s2, s2, ..., s_{n-1}, s_n), x > 0.
+__device__ int gk_count(int n, const double* __restrict__ s, double x, double pivmin) {
+  double q = -x;
+  int cnt = 1;  // q0 = -x < 0
+  for (int k = 0; k < 2 * n; ++k) {
+    double f = s[(k + 1) >> 1];
+    q = -x - f * f / q;
+    if (fabs(q) < pivmin) q = -pivmin;
+    cnt += (q < 0.0);
+  }
+  return cnt - (n + 1);
+}
+
+__global__ void gk_bisect_kernel(int n, const double* __restrict__ s_all, double* lam_out) {
+  const int l = blockIdx.y;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double* s = s_all + (size_t)l * (n + 1);
+  double smax = 0.0;
+  for (int r = 0; r <= n; ++r) smax = fmax(smax, s[r]);
+  const double pivmin = DBL_MIN / kEps * fmax(1.0, smax * smax);
+  double lo = 0.0, hi = 2.0 * smax * (1.0 + 4 * kEps);
+  for (int it = 0; it < 200; ++it) {
+    double mid = 0.5 * (lo + hi);
+    if (mid <= lo || mid >= hi) break;
+    if (hi - lo <= 2.0 * kEps * hi) break;
+    if (gk_count(n, s, mid, pivmin) >= i + 1) hi = mid;
+    else lo = mid;
+  }
+  double sig = 0.5 * (lo + hi);
+  lam_out[(size_t)l * n + i] = sig * sig;
+}
+
+// ---- tridiagonal inverse iteration (shared by (a) and (b)) ---------------------------
+// T = tridiag(e, d, e) of size N.  Scratch arrays strided by `stride` (coalesced across
+// threads): 5 arrays of N entries.  Writes the unit vector into v[k*vstride].
+__device__ void tri_invit(int N, const double* __restrict__ d, const double* __restrict__ e, double lam,
+                          double tnorm, double* scr, size_t stride, double* v, size_t vstride, unsigned seed) {
+  double* u0 = scr;
+  double* u1 = scr + (size_t)N * stride;
+  double* u2 = scr + (size_t)2 * N * stride;
+  double* lm = scr + (size_t)3 * N * stride;
+  double* pv = scr + (size_t)4 * N * stride;
+  const double tiny = kEps * tnorm + DBL_MIN;
+#define S(a, k) a[(size_t)(k) * stride]
+  if (N == 1) {
+    v[0] = 1.0;
+    return;
+  }
+  // LU with partial pivoting of T - lam I (rows k, k+1 interact only)
+  double cd = d[0] - lam, cs = e[0], cs2 = 0.0;   // current row k: diag, sup, sup2
+  for (int k = 0; k < N - 1; ++k) {
+    double sub = e[k];                      // T[k+1, k]
+    double ad = d[k + 1] - lam;             // T[k+1, k+1]
+    double as = (k + 1 < N - 1) ? e[k + 1] : 0.0;
+    if (fabs(sub) > fabs(cd)) {
+      double m = cd / sub;
+      S(u0, k) = sub; S(u1, k) = ad; S(u2, k) = as;
+      S(lm, k) = m; S(pv, k) = 1.0;
+      double nd = cs - m * ad, ns = cs2 - m * as;
+      cd = nd; cs = ns; cs2 = 0.0;
+    } else {
+      if (fabs(cd) < tiny) cd = (cd >= 0 ? tiny : -tiny);
+      double m = sub / cd;
+      S(u0, k) = cd; S(u1, k) = cs; S(u2, k) = cs2;
+      S(lm, k) = m; S(pv, k) = 0.0;
+      cd = ad - m * cs; cs = as; cs2 = 0.0;
+    }
+  }
+  if (fabs(cd) < tiny) cd = (cd >= 0 ? tiny : -tiny);
+  S(u0, N - 1) = cd; S(u1, N - 1) = 0.0; S(u2, N - 1) = 0.0;
+  // start vector: deterministic hash in [0.5, 1.5)
+  for (int k = 0; k < N; ++k) {
+    unsigned h = (unsigned)k * 2654435761u ^ (seed * 2246822519u + 0x9E3779B9u);
+    h ^= h >> 15; h *= 2246822519u; h ^= h >> 13;
+    v[(size_t)k * vstride] = 0.5 + (h & 0xFFFFFF) / 16777216.0;
+  }
+  for (int it = 0; it < 3; ++it) {
+    // forward: apply P and L
+    for (int k = 0; k < N - 1; ++k) {
+      double bk = v[(size_t)k * vstride], bk1 = v[(size_t)(k + 1) * vstride];
+      if (S(pv, k) != 0.0) { double t = bk; bk = bk1; bk1 = t; }
+      bk1 -= S(lm, k) * bk;
+      v[(size_t)k * vstride] = bk;
+      v[(size_t)(k + 1) * vstride] = bk1;
+    }
+    // backward with U (3 diagonals)
+    double x2 = 0.0, x1 = 0.0, nrm = 0.0;
+    for (int k = N - 1; k >= 0; --k) {
+      double x = (v[(size_t)k * vstride] - S(u1, k) * x1 - S(u2, k) * x2) / S(u0, k);
+      v[(size_t)k * vstride] = x;
+      x2 = x1; x1 = x;
+      nrm = fmax(nrm, fabs(x));
+    }
+    // rescale by the max-abs entry (keeps the next solve in range), then 2-norm at the end
+    double inv = 1.0 / nrm;
+    for (int k = 0; k < N; ++k) v[(size_t)k * vstride] *= inv;
+  }
+  double s2 = 0.0;
+  for (int k = 0; k < N; ++k) { double x = v[(size_t)k * vstride]; s2 += x * x; }
+  double inv = 1.0 / sqrt(s2);
+  for (int k = 0; k < N; ++k) v[(size_t)k * vstride] *= inv;
+#undef S
+}
+
+// sign rule (reading A4): entry of largest magnitude positive, ties -> lowest index
+__device__ void sign_rule(int N, double* v, size_t vstride) {
+  double best = -1.0, sgn = 1.0;
+  for (int k = 0; k < N; ++k) {
+    double x = v[(size_t)k * vstride];
+    if (fabs(x) > best) { best = fabs(x); sgn = x < 0 ? -1.0 : 1.0; }
+  }
+  if (sgn < 0)
+    for (int k = 0; k < N; ++k) v[(size_t)k * vstride] = -v[(size_t)k * vstride];
+}
+
+__global__ void sl_invit_kernel(int n, const double* __restrict__ d_all, const double* __restrict__ e_all,
+                                const double* __restrict__ lam_all, double* V_all, double* scratch) {
+  const int l = blockIdx.y;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double* d = d_all + (size_t)l * n;
+  const double* e = e_all + (size_t)l * n;
+  const double lam = lam_all[(size_t)l * n + i];
+  double tnorm = 0.0;
+  for (int k = 0; k < n; ++k) tnorm = fmax(tnorm, fabs(d[k]) + 2.0 * (k < n - 1 ? fabs(e[k]) : 0.0));
+  const size_t stride = (size_t)3 * n;
+  double* scr = scratch + (size_t)l * n + i;
+  double* v = V_all + (size_t)l * n * n + (size_t)i * n;
+  tri_invit(n, d, e, lam, tnorm, scr, stride, v, 1, (unsigned)i);
+  sign_rule(n, v, 1);
+}
+
+// G <- 1.5 I - 0.5 G  (Newton-Schulz step V <- V (3I - V^T V)/2)
+__global__ void ns_matrix_kernel(int n, double* G) {
+  const int l = blockIdx.y;
+  double* g = G + (size_t)l * n * n;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < (long long)n * n;
+       idx += (long long)gridDim.x * blockDim.x) {
+    int i = (int)(idx % n), j = (int)(idx / n);
+    g[idx] = (i == j ? 1.5 : 0.0) - 0.5 * g[idx];
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// (b) small symmetric eigensolver
+// ---------------------------------------------------------------------------------------
+constexpr int kTriThreads = 512;
+constexpr int kSmemMaxN = 120;   // N*N*8 <= 115 KB in shared memory, else global (L2)
+
+__device__ double block_sum(double v, double* red) {
+  for (int s = 16; s > 0; s >>= 1) v += __shfl_down_sync(0xffffffffu, v, s);
+  const int w = threadIdx.x >> 5, ln = threadIdx.x & 31;
+  __syncthreads();
+  if (ln == 0) red[w] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (threadIdx.x < 32) {
+    t = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+    for (int s = 16; s > 0; s >>= 1) t += __shfl_down_sync(0xffffffffu, t, s);
+    if (threadIdx.x == 0) red[32] = t;
+  }
+  __syncthreads();
+  return red[32];
+}
+
+// Householder tridiagonalisation, lower part, in place: after return column k (rows k+1..)
+// holds the unit Householder vector u_k (H_k = I - 2 u u^T; zero column = identity).
+__global__ void __launch_bounds__(kTriThreads) tridiag_kernel(const __grid_constant__ SyevBatch B) {
+  extern __shared__ double sm[];
+  __shared__ double red[33];
+  const SyevEntry& E = B.e[blockIdx.x];
+  const int N = E.N;
+  if (N <= 0) return;
+  const bool use_sm = N <= kSmemMaxN;
+  double* M = use_sm ? sm : E.A;
+  const int ld = use_sm ? N : E.lda;
+  double* p = use_sm ? sm + N * N : E.e + 0;  // p needs N entries; e gets filled only at the end
+  double* uvec = use_sm ? sm + N * N + N : E.d;  // scratch (d filled at the end)
+  __shared__ double dk_s[1];
+  const int tid = threadIdx.x, nt = blockDim.x;
+  if (use_sm)
+    for (int idx = tid; idx < N * N; idx += nt) M[idx] = E.A[(idx % N) + (size_t)(idx / N) * E.lda];
+  __syncthreads();
+  // keep d/e in registers of thread 0 is not possible (N values); store in shared scratch
+  // at the end we write d/e; during the sweep we record them into the diagonal/subdiagonal
+  // positions, which the algorithm no longer touches.
+  for (int k = 0; k + 2 < N; ++k) {
+    const int m = N - k - 1;          // length of x = M[k+1.., k]
+    double x0 = M[(k + 1) + (size_t)k * ld];
+    double part = 0.0;
+    for (int i = tid + 1; i < m; i += nt) {
+      double x = M[(k + 1 + i) + (size_t)k * ld];
+      part += x * x;
+    }
+    double sig = block_sum(part, red);
+    double alpha, unrm2;
+    bool skip = (sig == 0.0);
+    if (!skip) {
+      alpha = -copysign(sqrt(x0 * x0 + sig), x0);
+      double v0 = x0 - alpha;
+      unrm2 = sig + v0 * v0;
+      double inv = 1.0 / sqrt(unrm2);
+      for (int i = tid; i < m; i += nt) {
+        double x = (i == 0) ? v0 : M[(k + 1 + i) + (size_t)k * ld];
+        uvec[i] = x * inv;
+      }
+    } else {
+      alpha = x0;
+    }
+    __syncthreads();
+    if (!skip) {
+      // p = A22 u
+      for (int i = tid; i < m; i += nt) {
+        double acc = 0.0;
+        for (int j = 0; j < m; ++j) acc += M[(k + 1 + i) + (size_t)(k + 1 + j) * ld] * uvec[j];
+        p[i] = acc;
+      }
+      __syncthreads();
+      double kp = 0.0;
+      for (int i = tid; i < m; i += nt) kp += uvec[i] * p[i];
+      double K = block_sum(kp, red);
+      for (int i = tid; i < m; i += nt) p[i] -= K * uvec[i];   // q
+      __syncthreads();
+      // A22 -= 2 (u q^T + q u^T)
+      for (long long idx = tid; idx < (long long)m * m; idx += nt) {
+        int i = (int)(idx % m), j = (int)(idx / m);
+        M[(k + 1 + i) + (size_t)(k + 1 + j) * ld] -= 2.0 * (uvec[i] * p[j] + p[i] * uvec[j]);
+      }
+      __syncthreads();
+    }
+    // record: diagonal stays M[k,k]; store alpha on the super-diagonal slot M[k, k+1]
+    // (never read again) and u_k in column k below the diagonal.
+    if (tid == 0) dk_s[0] = alpha;
+    __syncthreads();
+    for (int i = tid; i < m; i += nt) M[(k + 1 + i) + (size_t)k * ld] = skip ? 0.0 : uvec[i];
+    if (tid == 0) M[k + (size_t)(k + 1) * ld] = dk_s[0];
+    __syncthreads();
+  }
+  // extract d, e; write back Householder vectors if computed in shared memory
+  if (tid == 0) {
+    for (int k = 0; k < N; ++k) E.d[k] = M[k + (size_t)k * ld];
+    for (int k = 0; k + 1 < N; ++k) E.e[k] = (k + 2 < N) ? M[k + (size_t)(k + 1) * ld] : M[(k + 1) + (size_t)k * ld];
+  }
+  __syncthreads();
+  if (use_sm)
+    for (int idx = tid; idx < N * N; idx += nt) E.A[(idx % N) + (size_t)(idx / N) * E.lda] = M[idx];
+}
+
+__device__ int tri_count(int N, const double* __restrict__ d, const double* __restrict__ e, double x,
+                         double pivmin) {
+  double q = d[0] - x;
+  int cnt = q < 0.0;
+  for (int k = 1; k < N; ++k) {
+    if (fabs(q) < pivmin) q = -pivmin;
+    q = d[k] - x - e[k - 1] * e[k - 1] / q;
+    cnt += (q < 0.0);
+  }
+  return cnt;
+}
+
+// thread per eigenvalue; lam[i] = i-th largest
+__global__ void tri_bisect_kernel(const __grid_constant__ SyevBatch B) {
+  const SyevEntry& E = B.e[blockIdx.y];
+  const int N = E.N;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  double lo = 1e300, hi = -1e300, emax = 0.0;
+  for (int k = 0; k < N; ++k) {
+    double r = (k > 0 ? fabs(E.e[k - 1]) : 0.0) + (k < N - 1 ? fabs(E.e[k]) : 0.0);
+    lo = fmin(lo, E.d[k] - r);
+    hi = fmax(hi, E.d[k] + r);
+    if (k < N - 1) emax = fmax(emax, fabs(E.e[k]));
+  }
+  const double tnorm = fmax(fabs(lo), fabs(hi));
+  const double pivmin = DBL_MIN / kEps * fmax(1.0, emax * emax);
+  lo -= 2 * kEps * tnorm + pivmin;
+  hi += 2 * kEps * tnorm + pivmin;
+  const int target = N - i;  // want the target-th smallest (1-based)
+  const double atol = 2.0 * kEps * tnorm + pivmin;
+  for (int it = 0; it < 200; ++it) {
+    double mid = 0.5 * (lo + hi);
+    if (hi - lo <= fmax(atol, 2.0 * kEps * fmax(fabs(lo), fabs(hi)))) break;
+    if (mid <= lo || mid >= hi) break;
+    if (tri_count(N, E.d, E.e, mid, pivmin) >= target) hi = mid;
+    else lo = mid;
+  }
+  E.lam[i] = 0.5 * (lo + hi);
+}
+
+// thread per wanted vector (i < r): inverse iteration on (d, e) into Y[:, i]
+__global__ void tri_invit_kernel(const __grid_constant__ SyevBatch B) {
+  const SyevEntry& E = B.e[blockIdx.y];
+  const int N = E.N;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int r = min(*E.r, N);
+  if (i >= r) return;
+  double tnorm = 0.0;
+  for (int k = 0; k < N; ++k) tnorm = fmax(tnorm, fabs(E.d[k]) + 2.0 * (k < N - 1 ? fabs(E.e[k]) : 0.0));
+  tri_invit(N, E.d, E.e, E.lam[i], tnorm, E.scratch + i, (size_t)N, E.Y + (size_t)i * E.ldy, 1, (unsigned)(i + 17));
+}
+
+// one CTA per matrix: CGS2 orthonormalisation of Y[:, 0..r) in order, then back-transform
+// with the Householder vectors stored in A: z = H_0 H_1 ... H_{N-3} y.
+__global__ void __launch_bounds__(256) orth_backtransform_kernel(const __grid_constant__ SyevBatch B) {
+  __shared__ double red[33];
+  extern __shared__ double coef[];   // r coefficients
+  const SyevEntry& E = B.e[blockIdx.x];
+  const int N = E.N;
+  const int r = min(*E.r, N);
+  const int tid = threadIdx.x, nt = blockDim.x;
+  double* Y = E.Y;
+  const int ldy = E.ldy;
+  for (int i = 0; i < r; ++i) {
+    double* yi = Y + (size_t)i * ldy;
+    for (int pass = 0; pass < 2; ++pass) {
+      // coef[j] = y_j . y_i for j < i (warp per j)
+      const int w = tid >> 5, ln = tid & 31;
+      for (int j = w; j < i; j += nt / 32) {
+        const double* yj = Y + (size_t)j * ldy;
+        double s = 0.0;
+        for (int k = ln; k < N; k += 32) s += yj[k] * yi[k];
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+        if (ln == 0) coef[j] = s;
+      }
+      __syncthreads();
+      for (int k = tid; k < N; k += nt) {
+        double acc = yi[k];
+        for (int j = 0; j < i; ++j) acc -= coef[j] * Y[(size_t)j * ldy + k];
+        yi[k] = acc;
+      }
+      __syncthreads();
+    }
+    double part = 0.0;
+    for (int k = tid; k < N; k += nt) part += yi[k] * yi[k];
+    double s2 = block_sum(part, red);
+    double inv = s2 > 0 ? 1.0 / sqrt(s2) : 0.0;
+    for (int k = tid; k < N; k += nt) yi[k] *= inv;
+    __syncthreads();
+  }
+  if (E.A == nullptr) return;   // orthonormalisation only
+  // back-transform: for k = N-3 .. 0: y[k+1:] -= 2 u_k (u_k . y[k+1:]); warp per vector
+  const int w = tid >> 5, ln = tid & 31;
+  for (int i = w; i < r; i += nt / 32) {
+    double* yi = Y + (size_t)i * ldy;
+    for (int k = N - 3; k >= 0; --k) {
+      const double* u = E.A + (k + 1) + (size_t)k * E.lda;
+      const int m = N - k - 1;
+      double s = 0.0;
+      for (int t = ln; t < m; t += 32) s += u[t] * yi[k + 1 + t];
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (s != 0.0)
+        for (int t = ln; t < m; t += 32) yi[k + 1 + t] -= 2.0 * s * u[t];
+      __syncwarp();
+    }
+  }
+}
+
+__global__ void rank_cut_kernel(int count, const double* __restrict__ s2, double factor,
+                                const double* __restrict__ energy, int* r_out, double* margin_out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const double thr = factor * (*energy);
+  // tails from the small end: tail(r) = sum_{k >= r} s2[k]
+  double acc = 0.0;
+  int r = count;                 // default: keep everything
+  double margin = 1e300;
+  for (int k = count - 1; k >= 1; --k) {
+    acc += fmax(s2[k], 0.0);
+    double m = fabs(acc - thr) / (thr > 0 ? thr : 1.0);
+    if (acc <= thr) {
+      r = k;                    // tail beyond index k-1 fits: keep k values
+      margin = fmin(margin, m);
+    } else {
+      margin = fmin(margin, m);
+      break;
+    }
+  }
+  if (count >= 1 && r < 1) r = 1;
+  while (r > 0 && r < count && s2[r] == s2[r - 1]) ++r;   // ties kept together (A23)
+  *r_out = count == 0 ? 0 : r;
+  if (margin_out) *margin_out = margin;
+}
+
+__global__ void basis_rank_kernel(int count, const double* __restrict__ lam, double tau, int* r_out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  int r = 0;
+  const double lim = tau * lam[0];
+  while (r < count && lam[r] > lim && lam[r] > 0.0) ++r;
+  *r_out = r;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------------------
+void sl_eigen_device(cudaStream_t st, int n, const double* a_mid_dev, int boundary, double* lam, double* V,
+                     int* status_dev) {
+  Scratch s(st);
+  double* sv = s.alloc<double>((size_t)3 * (n + 1));
+  double* d = s.alloc<double>((size_t)3 * n);
+  double* e = s.alloc<double>((size_t)3 * n);
+  sl_assemble_kernel<<<dim3(cdiv(n + 1, 256), 3), 256, 0, st>>>(n, a_mid_dev, boundary, sv, d, e, status_dev);
+  FC_CHECK_LAUNCH();
+  gk_bisect_kernel<<<dim3(cdiv(n, 64), 3), 64, 0, st>>>(n, sv, lam);
+  FC_CHECK_LAUNCH();
+  double* scr = s.alloc<double>((size_t)5 * 3 * n * n);
+  sl_invit_kernel<<<dim3(cdiv(n, 64), 3), 64, 0, st>>>(n, d, e, lam, V, scr);
+  FC_CHECK_LAUNCH();
+  // Newton-Schulz polish: 2 steps of V <- V (3I - V^T V)/2 on DMMA GEMMs
+  double* G = scr;                       // reuse: 3 n^2
+  double* V2 = scr + (size_t)3 * n * n;  // 3 n^2 (fits: scratch is 15 n^2)
+  for (int step = 0; step < 2; ++step) {
+    GemmArgs g;
+    g.transA = 1;
+    g.nbatch = 3;
+    for (int l = 0; l < 3; ++l)
+      g.b[l] = GemmBatch{n, n, n, V + (size_t)l * n * n, n, V + (size_t)l * n * n, n, G + (size_t)l * n * n, n,
+                         nullptr, 0, nullptr};
+    gemm(g, st);
+    ns_matrix_kernel<<<dim3(cdiv((long long)n * n, 256) > 1024 ? 1024 : cdiv((long long)n * n, 256), 3), 256, 0,
+                       st>>>(n, G);
+    FC_CHECK_LAUNCH();
+    GemmArgs h;
+    h.nbatch = 3;
+    for (int l = 0; l < 3; ++l)
+      h.b[l] = GemmBatch{n, n, n, V + (size_t)l * n * n, n, G + (size_t)l * n * n, n, V2 + (size_t)l * n * n, n,
+                         nullptr, 0, nullptr};
+    gemm(h, st);
+    FC_CUDA_TRY(cudaMemcpyAsync(V, V2, (size_t)3 * n * n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  }
+}
+
+void syev_values(const SyevBatch& b, cudaStream_t st) {
+  if (b.nb == 0) return;
+  int maxN = 0;
+  bool any_sm = false;
+  for (int i = 0; i < b.nb; ++i) {
+    maxN = std::max(maxN, b.e[i].N);
+    any_sm |= b.e[i].N <= kSmemMaxN && b.e[i].N > 0;
+  }
+  if (maxN == 0) return;
+  const int smem = any_sm ? (kSmemMaxN * kSmemMaxN + 2 * kSmemMaxN) * 8 : 0;
+  static bool attr = false;
+  if (!attr) {
+    FC_CUDA_TRY(cudaFuncSetAttribute(tridiag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (kSmemMaxN * kSmemMaxN + 2 * kSmemMaxN) * 8));
+    attr = true;
+  }
+  tridiag_kernel<<<b.nb, kTriThreads, smem, st>>>(b);
+  FC_CHECK_LAUNCH();
+  tri_bisect_kernel<<<dim3(cdiv(maxN, 64), b.nb), 64, 0, st>>>(b);
+  FC_CHECK_LAUNCH();
+}
+
+void syev_vectors(const SyevBatch& b, int maxN, cudaStream_t st) {
+  if (b.nb == 0 || maxN == 0) return;
+  tri_invit_kernel<<<dim3(cdiv(maxN, 64), b.nb), 64, 0, st>>>(b);
+  FC_CHECK_LAUNCH();
+  orth_backtransform_kernel<<<b.nb, 256, (size_t)maxN * 8, st>>>(b);
+  FC_CHECK_LAUNCH();
+}
+
+void orthonormalize_cols(int N, double* Y, int ldy, int* r_dev, int rmax, cudaStream_t st) {
+  SyevBatch b;
+  b.nb = 1;
+  b.e[0] = SyevEntry{N, nullptr, 0, nullptr, nullptr, nullptr, Y, ldy, r_dev, nullptr};
+  orth_backtransform_kernel<<<1, 256, (size_t)std::max(rmax, 1) * 8, st>>>(b);
+  FC_CHECK_LAUNCH();
+}
+
+void rank_cut_device(int count, const double* s2, double factor, const double* energy, int* r_out,
+                     double* margin_out, cudaStream_t st) {
+  rank_cut_kernel<<<1, 32, 0, st>>>(count, s2, factor, energy, r_out, margin_out);
+  FC_CHECK_LAUNCH();
+}
+
+void basis_rank_device(int count, const double* lam, double tau, int* r_out, cudaStream_t st) {
+  basis_rank_kernel<<<1, 32, 0, st>>>(count, lam, tau, r_out);
+  FC_CHECK_LAUNCH();
+}
+
+}  // namespace fc

@@ -1,0 +1,378 @@
+// cp_truncate (S11-S13 on a plain CP) and pcg_solve: Algorithm 1 [P:1825-1872] on mixed
+// Tucker-canonical iterates.
+//
+// The operator apply inside the solver is the factored apply of [P:614-623] written for an
+// iterate whose factors are Q_l C_l (Q_l orthonormal, from the previous T2C):
+//   forward transform   Zhat_l = V_l^T Q_l                     (S5, DMMA GEMM)
+//   Khatri-Rao basis    Khat_l[:, a*q+b] = W_l[:, a] (.) Zhat_l[:, b]   (S6; U_F = W_F E_F)
+//   coefficients        kron(E_l, C_l),  weights kron(w_F, w_x)
+// the truncation then runs on that eigen-coordinate tensor, and only the r_l surviving basis
+// columns are transformed back, Z_l <- V_l Z_l (S7, DMMA GEMM).  Because V_l is orthogonal,
+// singular values, ranks and the T2C output are those of the paper's physical-coordinate
+// apply followed by RHOSVD.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include "cpops.cuh"
+#include "eig.cuh"
+#include "solver.cuh"
+#include "tt.cuh"
+
+namespace fc {
+namespace {
+
+__global__ void hadamard_basis_kernel(int n, int s, const double* __restrict__ W, int q,
+                                      const double* __restrict__ Zh, double* K) {
+  const long long tot = (long long)n * s * q;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < tot;
+       idx += (long long)gridDim.x * blockDim.x) {
+    int i = (int)(idx % n);
+    int col = (int)(idx / n);          // col = a*q + b
+    int a = col / q, b = col % q;
+    K[idx] = W[i + (size_t)a * n] * Zh[i + (size_t)b * n];
+  }
+}
+
+// out[(a*q + b), (k*R + j)] = E[a, k] * C[b, j]   (kron(E, C)), out ld = s*q
+__global__ void kron_kernel(int s, int r, const double* __restrict__ E, int q, int R, const double* __restrict__ C,
+                            double* out) {
+  const long long rows = (long long)s * q, tot = rows * r * R;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < tot;
+       idx += (long long)gridDim.x * blockDim.x) {
+    int row = (int)(idx % rows);
+    long long col = idx / rows;
+    int a = row / q, b = row % q;
+    int k = (int)(col / R), j = (int)(col % R);
+    out[idx] = E[a + (size_t)k * s] * C[b + (size_t)j * q];
+  }
+}
+
+__global__ void kron_w_kernel(int r, const double* __restrict__ wF, int R, const double* __restrict__ w, double* out) {
+  int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < r * R) out[t] = wF[t / R] * w[t % R];
+}
+
+__global__ void inv_sqrt_cols_kernel(int n, int s, const double* __restrict__ lam, double* W) {
+  const long long tot = (long long)n * s;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < tot;
+       idx += (long long)gridDim.x * blockDim.x) {
+    int a = (int)(idx / n);
+    W[idx] *= 1.0 / sqrt(lam[a]);
+  }
+}
+
+int nblocks(long long tot) { return (int)std::min<long long>(std::max<long long>((tot + 255) / 256, 1), 148 * 8); }
+
+}  // namespace
+
+// Reduced basis of the spectral CP: U_l = W_l E_l with W_l orthonormal (n x s_l).
+void ensure_spec_basis(fc_ctx c, SpecCP& sp) {
+  if (sp.has_basis) return;
+  cudaStream_t st = c->st;
+  const int n = c->n, r = sp.r;
+  Scratch s(st);
+  int sdim[3];
+  double* Wt[3];
+  for (int l = 0; l < 3; ++l) {
+    double* G = s.zeros<double>((size_t)r * r);
+    dgemm(st, 1, 0, r, r, n, 1.0, sp.Ul(n, l), n, sp.Ul(n, l), n, 1.0, G, r, std::max(1, std::min(cdiv(n, 256), 16)));
+    SyevBatch eb;
+    double* lam = s.alloc<double>(r);
+    double* Y = s.alloc<double>((size_t)r * r);
+    int* rr = s.alloc<int>(1);
+    eb.nb = 1;
+    eb.e[0] = SyevEntry{r, G, r, s.alloc<double>(r), s.alloc<double>(r), lam, Y, r, rr, s.alloc<double>((size_t)5 * r * r)};
+    syev_values(eb, st);
+    basis_rank_device(r, lam, 1e-20, rr, st);
+    syev_vectors(eb, r, st);
+    int h = 0;
+    FC_CUDA_TRY(cudaMemcpyAsync(&h, rr, sizeof(int), cudaMemcpyDeviceToHost, st));
+    FC_CUDA_TRY(cudaStreamSynchronize(st));
+    require(h >= 1, FC_ERR_NOT_SPD, "spectral CP has a zero factor matrix");
+    sdim[l] = h;
+    Wt[l] = s.alloc<double>((size_t)n * h);
+    dgemm(st, 0, 0, n, h, r, 1.0, sp.Ul(n, l), n, Y, r, 0.0, Wt[l], n);
+    inv_sqrt_cols_kernel<<<nblocks((long long)n * h), 256, 0, st>>>(n, h, lam, Wt[l]);
+    FC_CHECK_LAUNCH();
+    orthonormalize_cols(n, Wt[l], n, rr, h, st);
+  }
+  sp.smax = std::max(sdim[0], std::max(sdim[1], sdim[2]));
+  sp.W.ensure((size_t)3 * n * sp.smax);
+  sp.E.ensure((size_t)3 * sp.smax * r);
+  for (int l = 0; l < 3; ++l) {
+    sp.s[l] = sdim[l];
+    double* Wl = sp.W.p + (size_t)l * n * sp.smax;
+    double* El = sp.E.p + (size_t)l * sp.smax * r;
+    FC_CUDA_TRY(cudaMemcpyAsync(Wl, Wt[l], (size_t)n * sdim[l] * 8, cudaMemcpyDeviceToDevice, st));
+    FC_CUDA_TRY(cudaMemsetAsync(El, 0, (size_t)sdim[l] * r * 8, st));
+    dgemm(st, 1, 0, sdim[l], r, n, 1.0, Wl, n, sp.Ul(n, l), n, 1.0, El, sdim[l],
+          std::max(1, std::min(cdiv(n, 256), 16)));
+  }
+  FC_CUDA_TRY(cudaStreamSynchronize(st));
+  sp.has_basis = true;
+}
+
+// S = trunc(F x) for a TT iterate x (physical coordinates, orthonormal bases).
+TT apply_truncate_tt(fc_ctx c, SpecCP& sp, const TT& x, double eps, int rank_cap, TruncStats* stats) {
+  cudaStream_t st = c->st;
+  const int n = c->n, r = sp.r, R = x.R;
+  if (R == 0) {
+    TT z;
+    z.n = n;
+    return z;
+  }
+  ensure_spec_basis(c, sp);
+  TT y;   // eigen-coordinate Hadamard tensor (view over scratch-owned memory)
+  y.n = n;
+  y.R = r * R;
+  size_t need = (size_t)y.R;
+  for (int l = 0; l < 3; ++l) {
+    y.q[l] = sp.s[l] * x.q[l];
+    need += (size_t)n * x.q[l] + (size_t)n * y.q[l] + (size_t)y.q[l] * y.R;
+  }
+  y.mem.emplace_back(need * 8, st);
+  double* p = y.mem.back().d();
+  y.w = p;
+  p += y.R;
+  kron_w_kernel<<<cdiv(y.R, 256), 256, 0, st>>>(r, sp.w.p, R, x.w, y.w);
+  FC_CHECK_LAUNCH();
+  GemmArgs fwd;   // S5: Zhat_l = V_l^T Q_l
+  fwd.transA = 1;
+  fwd.nbatch = 3;
+  double* Zh[3];
+  for (int l = 0; l < 3; ++l) {
+    Zh[l] = p;
+    p += (size_t)n * x.q[l];
+    fwd.b[l] = GemmBatch{n, x.q[l], n, c->V_l(l), n, x.Q[l], n, Zh[l], n, nullptr, 0, nullptr};
+  }
+  gemm(fwd, st);
+  for (int l = 0; l < 3; ++l) {   // S6: Khatri-Rao basis and Kronecker coefficients
+    const double* Wl = sp.W.p + (size_t)l * n * sp.smax;
+    const double* El = sp.E.p + (size_t)l * sp.smax * r;
+    y.Q[l] = p;
+    p += (size_t)n * y.q[l];
+    y.C[l] = p;
+    p += (size_t)y.q[l] * y.R;
+    hadamard_basis_kernel<<<nblocks((long long)n * y.q[l]), 256, 0, st>>>(n, sp.s[l], Wl, x.q[l], Zh[l], y.Q[l]);
+    FC_CHECK_LAUNCH();
+    kron_kernel<<<nblocks((long long)y.q[l] * y.R), 256, 0, st>>>(sp.s[l], r, El, x.q[l], R, x.C[l], y.C[l]);
+    FC_CHECK_LAUNCH();
+    y.orth[l] = false;
+  }
+  TT out = truncate_tt(c, y, eps, rank_cap, stats);
+  // S7: back to physical coordinates, only the surviving basis columns
+  GemmArgs inv;
+  inv.nbatch = 0;
+  std::vector<DevMem> newQ;
+  for (int l = 0; l < 3; ++l) {
+    if (out.R == 0) break;
+    newQ.emplace_back((size_t)n * out.q[l] * 8, st);
+    inv.b[inv.nbatch++] = GemmBatch{n, out.q[l], n, c->V_l(l), n, out.Q[l], n, newQ.back().d(), n, nullptr, 0, nullptr};
+  }
+  if (inv.nbatch) {
+    gemm(inv, st);
+    for (int l = 0; l < 3; ++l)
+      FC_CUDA_TRY(cudaMemcpyAsync(out.Q[l], newQ[l].d(), (size_t)n * out.q[l] * 8, cudaMemcpyDeviceToDevice, st));
+  }
+  return out;
+}
+
+}  // namespace fc
+
+using namespace fc;
+
+namespace {
+template <class F>
+int guard2(fc_ctx c, F&& f) {
+  try {
+    return f();
+  } catch (const Error& e) {
+    if (c) c->err = e.msg;
+    return e.code;
+  } catch (const std::exception& e) {
+    if (c) c->err = e.what();
+    return FC_ERR_CUDA;
+  }
+}
+
+void check_cp2(fc_ctx c, const fc_cp* x, const char* name) {
+  require(x != nullptr, FC_ERR_INVALID_ARG, std::string(name) + " is NULL");
+  require(c->n > 0, FC_ERR_NOT_READY, "no eigenpairs: call sl_setup or sl_set_eigen first");
+  for (int l = 0; l < 3; ++l) {
+    require(x->n[l] == c->n, FC_ERR_SHAPE, std::string(name) + ": mode size differs from context n");
+    require(x->ld[l] >= x->n[l], FC_ERR_INVALID_ARG, std::string(name) + ": ld < n");
+  }
+  require(x->rank >= 0 && x->rank <= x->cap, FC_ERR_INVALID_ARG, std::string(name) + ": rank > cap");
+}
+
+void fill_info(fc_trunc_info* info, const TruncStats& S) {
+  if (!info) return;
+  for (int l = 0; l < 3; ++l) {
+    info->tucker_rank[l] = S.tucker[l];
+    info->basis_dim[l] = S.basis[l];
+  }
+  info->out_rank = S.out_rank;
+  info->in_rank = S.in_rank;
+  info->t2c_mode = S.t2c_mode;
+  info->energy = S.energy;
+  info->min_cut_margin = S.min_margin;
+}
+
+void store_tt(fc_ctx c, const TT& x, fc_cp* y) {
+  if (y->cap < x.R) {
+    y->rank = x.R;
+    throw Error(FC_ERR_CAPACITY, "output cap below the result rank");
+  }
+  tt_expand(c->st, x, y->U, y->ld, y->w);
+  y->rank = x.R;
+  FC_CUDA_TRY(cudaStreamSynchronize(c->st));
+}
+}  // namespace
+
+extern "C" {
+
+int cp_truncate(fc_ctx c, const fc_cp* x, double eps, fc_cp* y, fc_trunc_info* info) {
+  return guard2(c, [&]() {
+    check_cp2(c, x, "x");
+    check_cp2(c, y, "y");
+    require(eps > 0 && std::isfinite(eps), FC_ERR_INVALID_ARG, "eps must be > 0");
+    TruncStats S;
+    TT xt = tt_from_cp(c->st, c->n, x->rank, x->w, x->U, x->ld);
+    TT out;
+    try {
+      out = truncate_tt(c, xt, eps, 0, &S);
+    } catch (const Error& e) {
+      fill_info(info, S);
+      if (info && e.code == FC_ERR_CAPACITY) info->required_rank = S.out_rank;
+      throw;
+    }
+    fill_info(info, S);
+    if (y->cap < out.R) {
+      if (info) info->required_rank = out.R;
+    }
+    store_tt(c, out, y);
+    return FC_OK;
+  });
+}
+
+int pcg_solve(fc_ctx c, const fc_cp* b, const fc_params* prm, fc_cp* u, fc_pcg_report* rep) {
+  return guard2(c, [&]() {
+    check_cp2(c, b, "b");
+    check_cp2(c, u, "u");
+    require(prm != nullptr, FC_ERR_INVALID_ARG, "params NULL");
+    const double eps = prm->eps;
+    require(eps > 0, FC_ERR_INVALID_ARG, "eps must be > 0");
+    const double tol = prm->tol_stop > 0 ? prm->tol_stop : 10.0 * eps;     // A13
+    const int kmax = std::min(prm->kmax > 0 ? prm->kmax : 100, FC_MAX_ITERS);  // A17
+    const int cap = prm->rank_cap > 0 ? prm->rank_cap : 4096;
+    require(c->spec[FC_F].valid && c->spec[FC_G].valid, FC_ERR_NOT_READY, "spectral CPs missing");
+    cudaStream_t st = c->st;
+    fc_pcg_report local{};
+    fc_pcg_report& RP = rep ? *rep : local;
+    RP = fc_pcg_report{};
+    cudaEvent_t t0, t1, ti0, ti1;
+    FC_CUDA_TRY(cudaEventCreate(&t0));
+    FC_CUDA_TRY(cudaEventCreate(&t1));
+    FC_CUDA_TRY(cudaEventCreate(&ti0));
+    FC_CUDA_TRY(cudaEventCreate(&ti1));
+    struct EvGuard {
+      cudaEvent_t a, b, c2, d;
+      ~EvGuard() { cudaEventDestroy(a); cudaEventDestroy(b); cudaEventDestroy(c2); cudaEventDestroy(d); }
+    } evg{t0, t1, ti0, ti1};
+    FC_CUDA_TRY(cudaEventRecord(t0, st));
+    SpecCP& F = c->spec[FC_F];
+    SpecCP& G = c->spec[FC_G];
+    ensure_spec_basis(c, F);
+    ensure_spec_basis(c, G);
+
+    TT B = tt_from_cp(st, c->n, b->rank, b->w, b->U, b->ld);
+    const double normB = std::sqrt(std::max(tt_dot(c, B, B), 0.0));
+    RP.normB = normB;
+    require(std::isfinite(normB), FC_ERR_NAN, "non-finite right-hand side");
+    TT X;                                             // X0 = 0 (A14)
+    X.n = c->n;
+    if (normB == 0.0) {
+      RP.converged = 1;
+      u->rank = 0;
+      return FC_OK;
+    }
+    // line 1: R0 = B (A15, untruncated); lines 2-3: Z0 = trunc(precond(R0)); line 4: P0 = Z0
+    TT R = tt_copy(st, B);
+    // (B's basis need not be orthonormal: the truncation handles any Khatri-Rao basis)
+    TruncStats sZ;
+    TT Z = apply_truncate_tt(c, G, R, eps, cap, &sZ);
+    TT P = tt_copy(st, Z);
+    double rz = tt_dot(c, R, Z);
+    int status = FC_NOT_CONVERGED;
+    cudaEvent_t loop0;
+    FC_CUDA_TRY(cudaEventCreate(&loop0));
+    FC_CUDA_TRY(cudaEventRecord(loop0, st));
+    for (int k = 0; k < kmax; ++k) {
+      FC_CUDA_TRY(cudaEventRecord(ti0, st));
+      TruncStats sS, sX, sR;
+      TT S = apply_truncate_tt(c, F, P, eps, cap, &sS);            // lines 7-8
+      const double ps = tt_dot(c, P, S);
+      if (!std::isfinite(ps)) { cudaEventDestroy(loop0); throw Error(FC_ERR_NAN, "<P,S> is not finite"); }
+      if (ps <= 0) { cudaEventDestroy(loop0); throw Error(FC_ERR_NOT_SPD, "<P,S> <= 0"); }
+      const double a_k = rz / ps;                                   // line 9
+      {
+        TT XP = tt_axpy(st, X, a_k, P);                             // lines 10-11
+        X = truncate_tt(c, XP, eps, cap, &sX);
+      }
+      {
+        TT RS = tt_axpy(st, R, -a_k, S);                            // lines 12-13
+        R = truncate_tt(c, RS, eps, cap, &sR);
+      }
+      const double rr = tt_dot(c, R, R);
+      const double rel = std::sqrt(std::max(rr, 0.0)) / normB;      // line 14 (A13)
+      RP.rel_res[k] = rel;
+      RP.rank_S[k] = S.R;
+      RP.rank_X[k] = X.R;
+      RP.rank_R[k] = R.R;
+      RP.tucker_S[k] = std::max(sS.tucker[0], std::max(sS.tucker[1], sS.tucker[2]));
+      RP.iters = k + 1;
+      if (!std::isfinite(rel)) { cudaEventDestroy(loop0); throw Error(FC_ERR_NAN, "residual is not finite"); }
+      if (rel <= tol) {
+        RP.rank_Z[k] = Z.R;
+        RP.rank_P[k] = P.R;
+        FC_CUDA_TRY(cudaEventRecord(ti1, st));
+        FC_CUDA_TRY(cudaEventSynchronize(ti1));
+        float ms;
+        cudaEventElapsedTime(&ms, ti0, ti1);
+        RP.t_iter_ms[k] = ms;
+        status = FC_OK;
+        break;
+      }
+      TruncStats sZ2, sP;
+      Z = apply_truncate_tt(c, G, R, eps, cap, &sZ2);               // lines 17-18
+      const double rz_new = tt_dot(c, R, Z);
+      const double b_k = rz_new / rz;                               // line 19 (A16)
+      {
+        TT ZP = tt_axpy(st, Z, b_k, P);                             // lines 20-21
+        P = truncate_tt(c, ZP, eps, cap, &sP);
+      }
+      rz = rz_new;
+      RP.rank_Z[k] = Z.R;
+      RP.rank_P[k] = P.R;
+      FC_CUDA_TRY(cudaEventRecord(ti1, st));
+      FC_CUDA_TRY(cudaEventSynchronize(ti1));
+      float ms;
+      cudaEventElapsedTime(&ms, ti0, ti1);
+      RP.t_iter_ms[k] = ms;
+    }
+    FC_CUDA_TRY(cudaEventRecord(t1, st));
+    FC_CUDA_TRY(cudaEventSynchronize(t1));
+    float tl, tt;
+    cudaEventElapsedTime(&tl, loop0, t1);
+    cudaEventElapsedTime(&tt, t0, t1);
+    cudaEventDestroy(loop0);
+    RP.t_loop_ms = tl;
+    RP.t_total_ms = tt;
+    RP.converged = status == FC_OK;
+    RP.status = status;
+    store_tt(c, X, u);
+    return status;
+  });
+}
+
+}  // extern "C"

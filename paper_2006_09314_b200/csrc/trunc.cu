@@ -1,0 +1,718 @@
+// The rank truncation trunc(x, eps) = RHOSVD (C2T) + Tucker core + Tucker-to-canonical
+// [P:187-190, P:1791-1816], readings A10/A11/A12/A23, on mixed Tucker-canonical
+// tensors (tt.cuh).
+//
+// Per mode l (batched over the 3 modes), with K = Q_l the basis and the factor columns
+// y_t = K c_t, n_t = ||y_t||, xi_t = w_t prod_l n_{l,t}:
+//   side matrix  A_l = [xi_t y_t / n_t]_t = K C D,  D = diag(xi_t / n_{l,t})          (S11)
+//   K^T K = U Lam U^T,  F = Lam^1/2 U^T  (so F^T F = K^T K;  F = I for orthonormal K)
+//   B = F C D,  B B^T = Y diag(s^2) Y^T   ->  the singular values of A_l are s (no inverse)
+//   r_l = min{r : sum_{k>r} s_k^2 <= (eps/2)^2 sum xi^2}   (tails from the small end)
+//   Z_l = K H F^T Y_r diag(1/s^2)  with H = C D^2 C^T  (left singular vectors), CGS2-polished
+//   Chat_l = Z_l^T (K C diag(1/n_l))                                               (unit factors)
+//   core beta = sum_t xi_t Chat_1[:,t] (x) Chat_2[:,t] (x) Chat_3[:,t]                (S12)
+//   T2C: slice SVDs along the min-rank mode, pooled cut at (eps/2)^2 ||beta||^2        (S13)
+#include <algorithm>
+#include <cmath>
+#include "cpops.cuh"
+#include "eig.cuh"
+#include "tt.cuh"
+
+namespace fc {
+namespace {
+
+// n2[l][t] = sum_a C_l[a,t] * QC_l[a,t]   (QC = (Q^T Q) C, or C itself if orthonormal)
+struct TermArgs {
+  const double* C[3];
+  const double* QC[3];
+  int q[3];
+  double* n2[3];
+};
+__global__ void term_norms_kernel(int R, TermArgs a) {
+  const int l = blockIdx.y;
+  const int t = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  const int ln = threadIdx.x & 31;
+  if (t >= R) return;
+  const int q = a.q[l];
+  const double* c = a.C[l] + (size_t)t * q;
+  const double* qc = a.QC[l] + (size_t)t * q;
+  double s = 0.0;
+  for (int k = ln; k < q; k += 32) s += c[k] * qc[k];
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+  if (ln == 0) a.n2[l][t] = fmax(s, 0.0);
+}
+
+// xi_t, d_l[t] = xi_t / n_l[t], inv_n_l[t] = 1/n_l[t], energy += xi^2 (single block reduction)
+__global__ void term_weights_kernel(int R, const double* __restrict__ w, const double* n2a, const double* n2b,
+                                    const double* n2c, double* xi, double* da, double* db, double* dc,
+                                    double* ia, double* ib, double* ic, double* energy) {
+  __shared__ double red[32];
+  double acc = 0.0;
+  for (int t = threadIdx.x; t < R; t += blockDim.x) {
+    double na = sqrt(n2a[t]), nb = sqrt(n2b[t]), nc = sqrt(n2c[t]);
+    double x = w[t] * na * nb * nc;
+    bool zero = (x == 0.0);
+    xi[t] = x;
+    da[t] = zero ? 0.0 : w[t] * nb * nc;
+    db[t] = zero ? 0.0 : w[t] * na * nc;
+    dc[t] = zero ? 0.0 : w[t] * na * nb;
+    ia[t] = zero ? 0.0 : 1.0 / na;
+    ib[t] = zero ? 0.0 : 1.0 / nb;
+    ic[t] = zero ? 0.0 : 1.0 / nc;
+    acc += x * x;
+  }
+  for (int s = 16; s > 0; s >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+    for (int s = 16; s > 0; s >>= 1) v += __shfl_down_sync(0xffffffffu, v, s);
+    if (threadIdx.x == 0) *energy = v;
+  }
+}
+
+// F = Lam^1/2 U^T from the (descending) eigenpairs of K^T K; lam < 0 clamped to 0.
+__global__ void sqrt_factor_kernel(int q, const double* lam, const double* U, double* F) {
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < q * q; idx += gridDim.x * blockDim.x) {
+    int i = idx % q, j = idx / q;                 // F[i, j] = sqrt(lam_i) * U[j, i]
+    F[idx] = sqrt(fmax(lam[i], 0.0)) * U[j + (size_t)i * q];
+  }
+}
+
+__global__ void scale_rows_kernel(int rows, int cols, const double* __restrict__ in, int ldi,
+                                  const double* __restrict__ s, double* out, int ldo) {
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < (long long)rows * cols;
+       idx += (long long)gridDim.x * blockDim.x) {
+    int i = (int)(idx % rows), j = (int)(idx / rows);
+    out[i + (size_t)j * ldo] = s[i] * in[i + (size_t)j * ldi];
+  }
+}
+
+__global__ void inv_sq_kernel(int r, const double* __restrict__ s2, double* out) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < r) out[i] = s2[i] > 0 ? 1.0 / s2[i] : 0.0;
+}
+
+// KR12[(a + r1*b), t] = xi_t * C1[a,t] * C2[b,t]
+__global__ void kr12_kernel(int r1, int r2, int R, const double* __restrict__ xi, const double* __restrict__ C1,
+                            const double* __restrict__ C2, double* out) {
+  const long long tot = (long long)r1 * r2 * R;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < tot;
+       idx += (long long)gridDim.x * blockDim.x) {
+    int ab = (int)(idx % (r1 * r2));
+    int t = (int)(idx / (r1 * r2));
+    int a = ab % r1, b = ab / r1;
+    out[idx] = xi[t] * C1[a + (size_t)t * r1] * C2[b + (size_t)t * r2];
+  }
+}
+
+// slices: S_nu[x, y] = core[ia, ib, ic] with (mode a index x, mode b index y, mode c index nu)
+__global__ void extract_slices_kernel(const double* __restrict__ core, int r0, int r1, int r2, int ma, int mb,
+                                      int mc, double* S) {
+  const int r[3] = {r0, r1, r2};
+  const int ra = r[ma], rb = r[mb], rc = r[mc];
+  const long long tot = (long long)ra * rb * rc;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < tot;
+       idx += (long long)gridDim.x * blockDim.x) {
+    int x = (int)(idx % ra);
+    int y = (int)((idx / ra) % rb);
+    int nu = (int)(idx / ((long long)ra * rb));
+    int id[3];
+    id[ma] = x; id[mb] = y; id[mc] = nu;
+    S[idx] = core[id[0] + (size_t)r0 * (id[1] + (size_t)r1 * id[2])];
+  }
+}
+
+// One-sided Jacobi SVD of each slice (ra x rb, column-major) in shared memory; one CTA per
+// slice.  Outputs k = min(ra, rb) triples sorted by s descending: s[nu*k + m],
+// Ua[nu*ra*k + m*ra + x], Vb[nu*rb*k + m*rb + y].
+constexpr int kSliceMax = 96;
+__global__ void __launch_bounds__(256) slice_svd_kernel(int ra, int rb, const double* __restrict__ S, double* s_out,
+                                                        double* Ua, double* Vb) {
+  extern __shared__ double sm[];
+  const int nu = blockIdx.x;
+  const bool tr = ra < rb;                     // work on S^T when wide
+  const int rows = tr ? rb : ra, cols = tr ? ra : rb;
+  const int k = cols;                          // = min(ra, rb)
+  double* A = sm;                              // rows x cols
+  double* W = sm + rows * cols;                // cols x cols rotations
+  double* nrm = W + cols * cols;               // cols
+  int* order = (int*)(nrm + cols);             // cols
+  const double* src = S + (size_t)nu * ra * rb;
+  const int tid = threadIdx.x, nt = blockDim.x, warp = tid >> 5, ln = tid & 31, nw = nt >> 5;
+  for (int idx = tid; idx < rows * cols; idx += nt) {
+    int i = idx % rows, j = idx / rows;
+    A[idx] = tr ? src[j + (size_t)i * ra] : src[i + (size_t)j * ra];
+  }
+  for (int idx = tid; idx < cols * cols; idx += nt) W[idx] = (idx % cols == idx / cols) ? 1.0 : 0.0;
+  __shared__ int changed;
+  __syncthreads();
+  const int p = cols + (cols & 1);
+  for (int sweep = 0; sweep < 40; ++sweep) {
+    if (tid == 0) changed = 0;
+    __syncthreads();
+    for (int rd = 0; rd < p - 1; ++rd) {
+      for (int pi = warp; pi < p / 2; pi += nw) {
+        int a, b;
+        if (pi == 0) { a = rd % (p - 1); b = p - 1; }
+        else { a = (rd + pi) % (p - 1); b = (rd - pi + p - 1) % (p - 1); }
+        if (a > b) { int t = a; a = b; b = t; }
+        if (b >= cols) continue;
+        double al = 0, be = 0, ga = 0;
+        for (int i = ln; i < rows; i += 32) {
+          double x = A[i + a * rows], y = A[i + b * rows];
+          al += x * x; be += y * y; ga += x * y;
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+          al += __shfl_xor_sync(0xffffffffu, al, o);
+          be += __shfl_xor_sync(0xffffffffu, be, o);
+          ga += __shfl_xor_sync(0xffffffffu, ga, o);
+        }
+        if (ga == 0.0 || fabs(ga) <= 1e-15 * sqrt(al * be)) continue;
+        double zeta = (be - al) / (2.0 * ga);
+        double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+        double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
+        for (int i = ln; i < rows; i += 32) {
+          double x = A[i + a * rows], y = A[i + b * rows];
+          A[i + a * rows] = c * x - s * y;
+          A[i + b * rows] = s * x + c * y;
+        }
+        for (int i = ln; i < cols; i += 32) {
+          double x = W[i + a * cols], y = W[i + b * cols];
+          W[i + a * cols] = c * x - s * y;
+          W[i + b * cols] = s * x + c * y;
+        }
+        if (ln == 0) changed = 1;
+      }
+      __syncthreads();
+    }
+    if (!changed) break;
+    __syncthreads();
+  }
+  for (int j = warp; j < cols; j += nw) {
+    double s2 = 0;
+    for (int i = ln; i < rows; i += 32) s2 += A[i + j * rows] * A[i + j * rows];
+    for (int o = 16; o > 0; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+    if (ln == 0) nrm[j] = sqrt(s2);
+  }
+  __syncthreads();
+  for (int j = tid; j < cols; j += nt) {     // rank by (s desc, index asc)
+    int rk = 0;
+    for (int i = 0; i < cols; ++i) rk += (nrm[i] > nrm[j]) || (nrm[i] == nrm[j] && i < j);
+    order[rk] = j;
+  }
+  __syncthreads();
+  // outputs: left vectors u (ra), right v (rb)
+  for (int idx = tid; idx < k * (ra + rb); idx += nt) {
+    int m = idx / (ra + rb), e = idx % (ra + rb);
+    int j = order[m];
+    double sj = nrm[j];
+    double inv = sj > 0 ? 1.0 / sj : 0.0;
+    if (e < ra) {
+      int x = e;   // left vector component
+      double v = tr ? W[x + j * cols] : A[x + j * rows] * inv;
+      Ua[(size_t)nu * ra * k + (size_t)m * ra + x] = v;
+    } else {
+      int y = e - ra;
+      double v = tr ? A[y + j * rows] * inv : W[y + j * cols];
+      Vb[(size_t)nu * rb * k + (size_t)m * rb + y] = v;
+    }
+  }
+  for (int m = tid; m < k; m += nt) s_out[(size_t)nu * k + m] = nrm[order[m]];
+}
+
+// pool all (s, nu, m), sort by s desc, ties (nu, m) asc; s2 sorted, keys, energy = sum s^2
+__global__ void __launch_bounds__(1024) pool_sort_kernel(int K, const double* __restrict__ s, double* s2_sorted,
+                                                         int* key_sorted, double* energy) {
+  __shared__ double red[32];
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < K; i += blockDim.x) {
+    double si = s[i];
+    int rk = 0;
+    for (int j = 0; j < K; ++j) {
+      double sj = s[j];
+      rk += (sj > si) || (sj == si && j < i);
+    }
+    s2_sorted[rk] = si * si;
+    key_sorted[rk] = i;
+    acc += si * si;
+  }
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    if (threadIdx.x == 0) *energy = v;
+  }
+}
+
+// output coefficients for the first R terms
+__global__ void t2c_scatter_kernel(int R, int k, int ra, int rb, int rc, const int* __restrict__ keys,
+                                   const double* __restrict__ s2, const double* __restrict__ Ua,
+                                   const double* __restrict__ Vb, double* w, double* Ca, double* Cb, double* Cc) {
+  const int m2 = blockIdx.x;
+  if (m2 >= R) return;
+  const int key = keys[m2];
+  const int nu = key / k, m = key % k;
+  for (int x = threadIdx.x; x < ra; x += blockDim.x) Ca[x + (size_t)m2 * ra] = Ua[(size_t)nu * ra * k + (size_t)m * ra + x];
+  for (int y = threadIdx.x; y < rb; y += blockDim.x) Cb[y + (size_t)m2 * rb] = Vb[(size_t)nu * rb * k + (size_t)m * rb + y];
+  for (int z = threadIdx.x; z < rc; z += blockDim.x) Cc[z + (size_t)m2 * rc] = (z == nu) ? 1.0 : 0.0;
+  if (threadIdx.x == 0) w[m2] = sqrt(s2[m2]);
+}
+
+__global__ void identity_kernel(int n, double* I) {
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < (long long)n * n;
+       idx += (long long)gridDim.x * blockDim.x)
+    I[idx] = (idx % n == idx / n) ? 1.0 : 0.0;
+}
+
+__global__ void blockdiag_kernel(int q1, int R1, const double* __restrict__ C1, int q2, int R2,
+                                 const double* __restrict__ C2, double* out) {
+  const int q = q1 + q2, R = R1 + R2;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < (long long)q * R;
+       idx += (long long)gridDim.x * blockDim.x) {
+    int i = (int)(idx % q), t = (int)(idx / q);
+    double v = 0.0;
+    if (t < R1 && i < q1) v = C1[i + (size_t)t * q1];
+    else if (t >= R1 && i >= q1) v = C2[(i - q1) + (size_t)(t - R1) * q2];
+    out[idx] = v;
+  }
+}
+
+int blocks_for(long long total) {
+  long long b = (total + 255) / 256;
+  return (int)std::min<long long>(std::max<long long>(b, 1), 148 * 8);
+}
+
+int read_int(const int* d, cudaStream_t st) {
+  int h = 0;
+  FC_CUDA_TRY(cudaMemcpyAsync(&h, d, sizeof(int), cudaMemcpyDeviceToHost, st));
+  FC_CUDA_TRY(cudaStreamSynchronize(st));
+  return h;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------------------
+TT tucker_to_canonical(fc_ctx c, const double* core, const int r[3], double* const Z[3], int n, double eps,
+                       int keep, int rank_cap, TruncStats* stats) {
+  cudaStream_t st = c->st;
+  int mc = 0;
+  for (int l = 1; l < 3; ++l)
+    if (r[l] < r[mc]) mc = l;                       // ties -> lowest mode
+  int ma = (mc == 0) ? 1 : 0, mb = (mc == 2) ? 1 : 2;
+  const int ra = r[ma], rb = r[mb], rc = r[mc];
+  const int k = std::min(ra, rb);
+  require(std::max(ra, rb) <= kSliceMax, FC_ERR_CAPACITY, "Tucker rank above the T2C slice limit (96)");
+  const int K = rc * k;
+  Scratch s(st);
+  double* S = s.alloc<double>((size_t)ra * rb * rc);
+  double* sv = s.alloc<double>((size_t)K);
+  double* Ua = s.alloc<double>((size_t)rc * ra * k);
+  double* Vb = s.alloc<double>((size_t)rc * rb * k);
+  double* s2s = s.alloc<double>((size_t)K);
+  int* keys = s.alloc<int>((size_t)K);
+  double* energy = s.alloc<double>(2);
+  int* rdev = s.alloc<int>(2);
+  extract_slices_kernel<<<blocks_for((long long)ra * rb * rc), 256, 0, st>>>(core, r[0], r[1], r[2], ma, mb, mc, S);
+  FC_CHECK_LAUNCH();
+  const int rows = std::max(ra, rb), cols = k;
+  size_t smem = ((size_t)rows * cols + (size_t)cols * cols + cols) * 8 + (size_t)cols * 4 + 16;
+  static bool attr = false;
+  if (!attr) {
+    FC_CUDA_TRY(cudaFuncSetAttribute(slice_svd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    attr = true;
+  }
+  slice_svd_kernel<<<rc, 256, smem, st>>>(ra, rb, S, sv, Ua, Vb);
+  FC_CHECK_LAUNCH();
+  pool_sort_kernel<<<1, 1024, 0, st>>>(K, sv, s2s, keys, energy);
+  FC_CHECK_LAUNCH();
+  int R;
+  if (keep > 0) {
+    R = std::min(keep, K);
+  } else {
+    rank_cut_device(K, s2s, 0.25 * eps * eps, energy, rdev, energy + 1, st);
+    R = read_int(rdev, st);
+  }
+  if (stats) {
+    stats->t2c_mode = mc;
+    stats->out_rank = R;
+  }
+  if (rank_cap > 0 && R > rank_cap) throw Error(FC_ERR_CAPACITY, "truncation output rank above the rank cap");
+  TT out;
+  out.n = n;
+  out.R = R;
+  out.q[0] = r[0]; out.q[1] = r[1]; out.q[2] = r[2];
+  size_t need = (size_t)R + (size_t)R * (r[0] + r[1] + r[2]) + (size_t)n * (r[0] + r[1] + r[2]);
+  out.mem.emplace_back(need * 8, st);
+  double* base = out.mem.back().d();
+  out.w = base;
+  double* p = base + R;
+  for (int l = 0; l < 3; ++l) {
+    out.C[l] = p;
+    p += (size_t)R * r[l];
+  }
+  for (int l = 0; l < 3; ++l) {
+    out.Q[l] = p;
+    p += (size_t)n * r[l];
+    FC_CUDA_TRY(cudaMemcpyAsync(out.Q[l], Z[l], (size_t)n * r[l] * 8, cudaMemcpyDeviceToDevice, st));
+    out.orth[l] = true;
+  }
+  if (R > 0) {
+    t2c_scatter_kernel<<<R, 64, 0, st>>>(R, k, ra, rb, rc, keys, s2s, Ua, Vb, out.w, out.C[ma], out.C[mb], out.C[mc]);
+    FC_CHECK_LAUNCH();
+  }
+  return out;
+}
+
+TT truncate_tt(fc_ctx c, const TT& x, double eps, int rank_cap, TruncStats* stats) {
+  cudaStream_t st = c->st;
+  const int n = x.n, R = x.R;
+  TruncStats local;
+  TruncStats& S = stats ? *stats : local;
+  S.in_rank = R;
+  if (R == 0) {
+    TT z;
+    z.n = n;
+    return z;
+  }
+  int q[3];
+  for (int l = 0; l < 3; ++l) {
+    q[l] = x.q[l];
+    S.basis[l] = q[l];
+    require(q[l] >= 1 && q[l] <= 2048, FC_ERR_CAPACITY, "side-matrix basis dimension above 2048");
+  }
+  Scratch s(st);
+  // ---- term norms and weights -----------------------------------------------------------
+  double* GQ[3];
+  double* QC[3];
+  double* n2[3];
+  double* dl[3];
+  double* inv[3];
+  for (int l = 0; l < 3; ++l) {
+    GQ[l] = x.orth[l] ? nullptr : s.alloc<double>((size_t)q[l] * q[l]);
+    QC[l] = x.orth[l] ? x.C[l] : s.alloc<double>((size_t)q[l] * R);
+    n2[l] = s.alloc<double>(R);
+    dl[l] = s.alloc<double>(R);
+    inv[l] = s.alloc<double>(R);
+  }
+  double* xi = s.alloc<double>(R);
+  double* energy = s.alloc<double>(4);
+  {
+    GemmArgs g;  // GQ = Q^T Q (split-K over n)
+    g.transA = 1;
+    g.beta = 1.0;
+    int nb = 0;
+    for (int l = 0; l < 3; ++l)
+      if (!x.orth[l]) {
+        FC_CUDA_TRY(cudaMemsetAsync(GQ[l], 0, (size_t)q[l] * q[l] * 8, st));
+        g.b[nb++] = GemmBatch{q[l], q[l], n, x.Q[l], n, x.Q[l], n, GQ[l], q[l], nullptr, 0, nullptr};
+      }
+    g.nbatch = nb;
+    g.splitk = std::max(1, std::min(cdiv(n, 256), 16));
+    gemm(g, st);
+    GemmArgs h;  // QC = GQ C
+    nb = 0;
+    for (int l = 0; l < 3; ++l)
+      if (!x.orth[l]) h.b[nb++] = GemmBatch{q[l], R, q[l], GQ[l], q[l], x.C[l], q[l], QC[l], q[l], nullptr, 0, nullptr};
+    h.nbatch = nb;
+    gemm(h, st);
+  }
+  TermArgs ta;
+  for (int l = 0; l < 3; ++l) {
+    ta.C[l] = x.C[l]; ta.QC[l] = QC[l]; ta.q[l] = q[l]; ta.n2[l] = n2[l];
+  }
+  term_norms_kernel<<<dim3(cdiv(R, 8), 3), 256, 0, st>>>(R, ta);
+  FC_CHECK_LAUNCH();
+  term_weights_kernel<<<1, 1024, 0, st>>>(R, x.w, n2[0], n2[1], n2[2], xi, dl[0], dl[1], dl[2], inv[0], inv[1],
+                                          inv[2], energy);
+  FC_CHECK_LAUNCH();
+
+  // ---- F = Lam^1/2 U^T of K^T K (non-orthonormal bases) -----------------------------------
+  double* F[3] = {nullptr, nullptr, nullptr};
+  {
+    SyevBatch eb;
+    int maxq = 0;
+    double* Ueig[3];
+    int* rfull[3];
+    for (int l = 0; l < 3; ++l) {
+      if (x.orth[l]) continue;
+      const int ql = q[l];
+      double* A = s.alloc<double>((size_t)ql * ql);
+      FC_CUDA_TRY(cudaMemcpyAsync(A, GQ[l], (size_t)ql * ql * 8, cudaMemcpyDeviceToDevice, st));
+      Ueig[l] = s.alloc<double>((size_t)ql * ql);
+      rfull[l] = s.alloc<int>(1);
+      int hq = ql;
+      FC_CUDA_TRY(cudaMemcpyAsync(rfull[l], &hq, sizeof(int), cudaMemcpyHostToDevice, st));
+      eb.e[eb.nb++] = SyevEntry{ql, A, ql, s.alloc<double>(ql), s.alloc<double>(ql), s.alloc<double>(ql), Ueig[l], ql,
+                                rfull[l], s.alloc<double>((size_t)5 * ql * ql)};
+      maxq = std::max(maxq, ql);
+    }
+    if (eb.nb) {
+      syev_values(eb, st);
+      syev_vectors(eb, maxq, st);
+      int b = 0;
+      for (int l = 0; l < 3; ++l) {
+        if (x.orth[l]) continue;
+        F[l] = s.alloc<double>((size_t)q[l] * q[l]);
+        sqrt_factor_kernel<<<blocks_for((long long)q[l] * q[l]), 256, 0, st>>>(q[l], eb.e[b].lam, Ueig[l], F[l]);
+        FC_CHECK_LAUNCH();
+        ++b;
+      }
+    }
+  }
+  // ---- B = F C D (q x R), M = B B^T ---------------------------------------------------
+  double* Bm[3];
+  double* M[3];
+  {
+    // B = F C diag(d) (F = I for an orthonormal basis); the diag(d) is the GEMM column scale
+    GemmArgs g;
+    int nb = 0;
+    for (int l = 0; l < 3; ++l) {
+      Bm[l] = s.alloc<double>((size_t)q[l] * R);
+      const double* Fl = F[l];
+      if (x.orth[l]) {
+        double* I = s.alloc<double>((size_t)q[l] * q[l]);
+        identity_kernel<<<blocks_for((long long)q[l] * q[l]), 256, 0, st>>>(q[l], I);
+        FC_CHECK_LAUNCH();
+        Fl = I;
+      }
+      g.b[nb++] = GemmBatch{q[l], R, q[l], Fl, q[l], x.C[l], q[l], Bm[l], q[l], nullptr, 0, dl[l]};
+    }
+    g.nbatch = nb;
+    gemm(g, st);
+    GemmArgs m;
+    m.transB = 1;
+    m.beta = 1.0;
+    m.nbatch = 3;
+    int tiles = 0;
+    for (int l = 0; l < 3; ++l) {
+      M[l] = s.alloc<double>((size_t)q[l] * q[l]);
+      FC_CUDA_TRY(cudaMemsetAsync(M[l], 0, (size_t)q[l] * q[l] * 8, st));
+      m.b[l] = GemmBatch{q[l], q[l], R, Bm[l], q[l], Bm[l], q[l], M[l], q[l], nullptr, 0, nullptr};
+      tiles += cdiv(q[l], 64) * cdiv(q[l], 64);
+    }
+    m.splitk = std::max(1, std::min(cdiv(R, 128), std::max(1, 148 * 3 / std::max(tiles, 1))));
+    gemm(m, st);
+  }
+  // ---- eigen of M: singular values s^2 (descending), cut, leading vectors --------------
+  SyevBatch eb;
+  double* lam[3];
+  double* Y[3];
+  int* rl = s.alloc<int>(4);
+  double* margins = s.alloc<double>(3);
+  int maxq = 0;
+  for (int l = 0; l < 3; ++l) {
+    const int ql = q[l];
+    lam[l] = s.alloc<double>(ql);
+    Y[l] = s.alloc<double>((size_t)ql * ql);
+    eb.e[eb.nb++] = SyevEntry{ql, M[l], ql, s.alloc<double>(ql), s.alloc<double>(ql), lam[l], Y[l], ql, rl + l,
+                              s.alloc<double>((size_t)5 * ql * ql)};
+    maxq = std::max(maxq, ql);
+  }
+  syev_values(eb, st);
+  for (int l = 0; l < 3; ++l) rank_cut_device(q[l], lam[l], 0.25 * eps * eps, energy, rl + l, margins + l, st);
+  syev_vectors(eb, maxq, st);
+  int r[3];
+  double hm[3];
+  FC_CUDA_TRY(cudaMemcpyAsync(r, rl, 3 * sizeof(int), cudaMemcpyDeviceToHost, st));
+  FC_CUDA_TRY(cudaMemcpyAsync(hm, margins, 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
+  FC_CUDA_TRY(cudaMemcpyAsync(&S.energy, energy, sizeof(double), cudaMemcpyDeviceToHost, st));
+  FC_CUDA_TRY(cudaStreamSynchronize(st));
+  for (int l = 0; l < 3; ++l) {
+    S.tucker[l] = r[l];
+    S.min_margin = std::min(S.min_margin, hm[l]);
+  }
+  if (S.energy == 0.0) {
+    TT z;
+    z.n = n;
+    return z;
+  }
+  // ---- Z_l and unit-factor coefficients Chat_l --------------------------------------------
+  double* Z[3];
+  double* Chat[3];
+  for (int l = 0; l < 3; ++l) {
+    const int ql = q[l], rr = r[l];
+    Z[l] = s.alloc<double>((size_t)n * rr);
+    Chat[l] = s.alloc<double>((size_t)rr * R);
+    if (x.orth[l]) {
+      // Z = Q Y_r ; Chat = Y_r^T C diag(1/n)
+      dgemm(st, 0, 0, n, rr, ql, 1.0, x.Q[l], n, Y[l], ql, 0.0, Z[l], n);
+      GemmArgs g;
+      g.transA = 1;
+      g.nbatch = 1;
+      g.b[0] = GemmBatch{rr, R, ql, Y[l], ql, x.C[l], ql, Chat[l], rr, nullptr, 0, inv[l]};
+      gemm(g, st);
+    } else {
+      // T1 = B^T Y_r (R x r); T1 <- diag(d) T1; G_Z = C T1 diag(1/s^2); Z = K G_Z; CGS2
+      double* T1 = s.alloc<double>((size_t)R * rr);
+      GemmArgs g;
+      g.transA = 1;
+      g.nbatch = 1;
+      g.b[0] = GemmBatch{R, rr, ql, Bm[l], ql, Y[l], ql, T1, R, nullptr, 0, nullptr};
+      gemm(g, st);
+      scale_rows_kernel<<<blocks_for((long long)R * rr), 256, 0, st>>>(R, rr, T1, R, dl[l], T1, R);
+      FC_CHECK_LAUNCH();
+      double* is2 = s.alloc<double>(rr);
+      inv_sq_kernel<<<cdiv(rr, 64), 64, 0, st>>>(rr, lam[l], is2);
+      FC_CHECK_LAUNCH();
+      double* GZ = s.alloc<double>((size_t)ql * rr);
+      GemmArgs h;
+      h.nbatch = 1;
+      h.b[0] = GemmBatch{ql, rr, R, x.C[l], ql, T1, R, GZ, ql, nullptr, 0, is2};
+      gemm(h, st);
+      dgemm(st, 0, 0, n, rr, ql, 1.0, x.Q[l], n, GZ, ql, 0.0, Z[l], n);
+      orthonormalize_cols(n, Z[l], n, rl + l, rr, st);
+      // Chat = (Z^T Q) C diag(1/n)
+      double* ZQ = s.alloc<double>((size_t)rr * ql);
+      FC_CUDA_TRY(cudaMemsetAsync(ZQ, 0, (size_t)rr * ql * 8, st));
+      dgemm(st, 1, 0, rr, ql, n, 1.0, Z[l], n, x.Q[l], n, 1.0, ZQ, rr, std::max(1, std::min(cdiv(n, 256), 16)));
+      GemmArgs k2;
+      k2.nbatch = 1;
+      k2.b[0] = GemmBatch{rr, R, ql, ZQ, rr, x.C[l], ql, Chat[l], rr, nullptr, 0, inv[l]};
+      gemm(k2, st);
+    }
+  }
+  // ---- core beta (r1 r2 x r3) = KR12 * Chat_3^T -----------------------------------------
+  const size_t r12 = (size_t)r[0] * r[1];
+  double* KR = s.alloc<double>(r12 * R);
+  kr12_kernel<<<blocks_for((long long)r12 * R), 256, 0, st>>>(r[0], r[1], R, xi, Chat[0], Chat[1], KR);
+  FC_CHECK_LAUNCH();
+  double* core = s.alloc<double>(r12 * r[2]);
+  FC_CUDA_TRY(cudaMemsetAsync(core, 0, r12 * r[2] * 8, st));
+  {
+    int tiles = cdiv((long long)r12, 64) * cdiv(r[2], 64);
+    dgemm(st, 0, 1, (int)r12, r[2], R, 1.0, KR, (int)r12, Chat[2], r[2], 1.0, core, (int)r12,
+          std::max(1, std::min(cdiv(R, 64), std::max(1, 296 / std::max(tiles, 1)))));
+  }
+  return tucker_to_canonical(c, core, r, Z, n, eps, 0, rank_cap, &S);
+}
+
+TT tt_axpy(cudaStream_t st, const TT& x, double a, const TT& y) {
+  TT z;
+  z.n = x.n;
+  z.R = x.R + y.R;
+  size_t need = (size_t)z.R;
+  for (int l = 0; l < 3; ++l) {
+    z.q[l] = x.q[l] + y.q[l];
+    need += (size_t)x.n * z.q[l] + (size_t)z.q[l] * z.R;
+  }
+  z.mem.emplace_back(need * 8, st);
+  double* p = z.mem.back().d();
+  z.w = p;
+  p += z.R;
+  if (x.R) FC_CUDA_TRY(cudaMemcpyAsync(z.w, x.w, (size_t)x.R * 8, cudaMemcpyDeviceToDevice, st));
+  if (y.R) scale_copy(y.R, y.w, a, z.w + x.R, st);
+  for (int l = 0; l < 3; ++l) {
+    z.Q[l] = p;
+    p += (size_t)x.n * z.q[l];
+    z.C[l] = p;
+    p += (size_t)z.q[l] * z.R;
+    if (x.q[l]) FC_CUDA_TRY(cudaMemcpyAsync(z.Q[l], x.Q[l], (size_t)x.n * x.q[l] * 8, cudaMemcpyDeviceToDevice, st));
+    if (y.q[l])
+      FC_CUDA_TRY(cudaMemcpyAsync(z.Q[l] + (size_t)x.n * x.q[l], y.Q[l], (size_t)x.n * y.q[l] * 8,
+                                  cudaMemcpyDeviceToDevice, st));
+    blockdiag_kernel<<<blocks_for((long long)z.q[l] * z.R), 256, 0, st>>>(x.q[l], x.R, x.C[l], y.q[l], y.R, y.C[l],
+                                                                            z.C[l]);
+    FC_CHECK_LAUNCH();
+    z.orth[l] = (x.R == 0 && y.orth[l]) || (y.R == 0 && x.orth[l]);
+  }
+  return z;
+}
+
+double tt_dot(fc_ctx c, const TT& x, const TT& y) {
+  if (x.R == 0 || y.R == 0) return 0.0;
+  cudaStream_t st = c->st;
+  Scratch s(st);
+  double* H = s.alloc<double>((size_t)3 * x.R * y.R + 1);
+  for (int l = 0; l < 3; ++l) {
+    // G = Q_x^T Q_y (qx x qy), T = G C_y (qx x Ry), H_l = C_x^T T (Rx x Ry)
+    double* G = s.zeros<double>((size_t)x.q[l] * y.q[l]);
+    dgemm(st, 1, 0, x.q[l], y.q[l], x.n, 1.0, x.Q[l], x.n, y.Q[l], y.n, 1.0, G, x.q[l],
+          std::max(1, std::min(cdiv(x.n, 256), 16)));
+    double* T = s.alloc<double>((size_t)x.q[l] * y.R);
+    dgemm(st, 0, 0, x.q[l], y.R, y.q[l], 1.0, G, x.q[l], y.C[l], y.q[l], 0.0, T, x.q[l]);
+    dgemm(st, 1, 0, x.R, y.R, x.q[l], 1.0, x.C[l], x.q[l], T, x.q[l], 0.0, H + (size_t)l * x.R * y.R, x.R);
+  }
+  const double* Hp[3] = {H, H + (size_t)x.R * y.R, H + (size_t)2 * x.R * y.R};
+  double* out = H + (size_t)3 * x.R * y.R;
+  dot_reduce(x.R, y.R, x.w, y.w, Hp, x.R, out, st);
+  double h = 0;
+  FC_CUDA_TRY(cudaMemcpyAsync(&h, out, sizeof(double), cudaMemcpyDeviceToHost, st));
+  FC_CUDA_TRY(cudaStreamSynchronize(st));
+  return h;
+}
+
+void tt_expand(cudaStream_t st, const TT& x, double* const U[3], const int ld[3], double* w) {
+  if (x.R == 0) return;
+  for (int l = 0; l < 3; ++l) dgemm(st, 0, 0, x.n, x.R, x.q[l], 1.0, x.Q[l], x.n, x.C[l], x.q[l], 0.0, U[l], ld[l]);
+  FC_CUDA_TRY(cudaMemcpyAsync(w, x.w, (size_t)x.R * 8, cudaMemcpyDeviceToDevice, st));
+}
+
+TT tt_from_cp(cudaStream_t st, int n, int R, const double* w, double* const U[3], const int ld[3]) {
+  TT x;
+  x.n = n;
+  x.R = R;
+  if (R == 0) return x;
+  const bool wide = R > n;   // basis = I_n, coefficients = U
+  size_t need = (size_t)R;
+  for (int l = 0; l < 3; ++l) need += wide ? (size_t)n * n + (size_t)n * R : (size_t)n * R + (size_t)R * R;
+  x.mem.emplace_back(need * 8, st);
+  double* p = x.mem.back().d();
+  x.w = p;
+  p += R;
+  FC_CUDA_TRY(cudaMemcpyAsync(x.w, w, (size_t)R * 8, cudaMemcpyDeviceToDevice, st));
+  for (int l = 0; l < 3; ++l) {
+    x.Q[l] = p;
+    if (wide) {
+      x.q[l] = n;
+      identity_kernel<<<blocks_for((long long)n * n), 256, 0, st>>>(n, x.Q[l]);
+      FC_CHECK_LAUNCH();
+      p += (size_t)n * n;
+      x.C[l] = p;
+      FC_CUDA_TRY(cudaMemcpy2DAsync(x.C[l], (size_t)n * 8, U[l], (size_t)ld[l] * 8, (size_t)n * 8, R,
+                                    cudaMemcpyDeviceToDevice, st));
+      p += (size_t)n * R;
+      x.orth[l] = true;
+    } else {
+      x.q[l] = R;
+      FC_CUDA_TRY(cudaMemcpy2DAsync(x.Q[l], (size_t)n * 8, U[l], (size_t)ld[l] * 8, (size_t)n * 8, R,
+                                    cudaMemcpyDeviceToDevice, st));
+      p += (size_t)n * R;
+      x.C[l] = p;
+      identity_kernel<<<blocks_for((long long)R * R), 256, 0, st>>>(R, x.C[l]);
+      FC_CHECK_LAUNCH();
+      p += (size_t)R * R;
+      x.orth[l] = false;
+    }
+  }
+  return x;
+}
+
+TT tt_copy(cudaStream_t st, const TT& x) {
+  TT y;
+  y.n = x.n;
+  y.R = x.R;
+  size_t need = (size_t)x.R;
+  for (int l = 0; l < 3; ++l) need += (size_t)x.n * x.q[l] + (size_t)x.q[l] * x.R;
+  y.mem.emplace_back(need * 8, st);
+  double* p = y.mem.back().d();
+  y.w = p;
+  p += x.R;
+  if (x.R) FC_CUDA_TRY(cudaMemcpyAsync(y.w, x.w, (size_t)x.R * 8, cudaMemcpyDeviceToDevice, st));
+  for (int l = 0; l < 3; ++l) {
+    y.q[l] = x.q[l];
+    y.orth[l] = x.orth[l];
+    y.Q[l] = p;
+    p += (size_t)x.n * x.q[l];
+    y.C[l] = p;
+    p += (size_t)x.q[l] * x.R;
+    if (x.q[l]) FC_CUDA_TRY(cudaMemcpyAsync(y.Q[l], x.Q[l], (size_t)x.n * x.q[l] * 8, cudaMemcpyDeviceToDevice, st));
+    if (x.q[l] && x.R)
+      FC_CUDA_TRY(cudaMemcpyAsync(y.C[l], x.C[l], (size_t)x.q[l] * x.R * 8, cudaMemcpyDeviceToDevice, st));
+  }
+  return y;
+}
+
+}  // namespace fc

@@ -1,0 +1,73 @@
+// Mixed Tucker-canonical tensors [P:1804-1812] used inside the solver:
+//   x = sum_t w_t (Q_1 C_1[:,t]) (x) (Q_2 C_2[:,t]) (x) (Q_3 C_3[:,t])
+// Q_l: n x q_l (orthonormal when orth[l]); C_l: q_l x R (column-major, ld = q_l); w: R.
+// A plain CP is the special case Q_l = U_l, C_l = I (or Q_l = I_n, C_l = U_l).  T2C outputs
+// have Q_l = Z_l orthonormal and unit coefficient columns (an orthogonal CP).
+#pragma once
+#include <utility>
+#include "ctx.cuh"
+
+namespace fc {
+
+struct DevMem {               // move-only stream-ordered allocation
+  void* p = nullptr;
+  cudaStream_t st = nullptr;
+  DevMem() = default;
+  DevMem(size_t bytes, cudaStream_t s) : st(s) {
+    if (bytes == 0) bytes = 16;
+    FC_CUDA_TRY(cudaMallocAsync(&p, (bytes + 255) & ~size_t(255), s));
+  }
+  DevMem(const DevMem&) = delete;
+  DevMem& operator=(const DevMem&) = delete;
+  DevMem(DevMem&& o) noexcept : p(o.p), st(o.st) { o.p = nullptr; }
+  DevMem& operator=(DevMem&& o) noexcept {
+    if (this != &o) {
+      reset();
+      p = o.p; st = o.st; o.p = nullptr;
+    }
+    return *this;
+  }
+  void reset() {
+    if (p) cudaFreeAsync(p, st);
+    p = nullptr;
+  }
+  ~DevMem() { reset(); }
+  double* d() const { return (double*)p; }
+};
+
+struct TT {
+  int n = 0, R = 0;
+  int q[3] = {0, 0, 0};
+  double* Q[3] = {nullptr, nullptr, nullptr};
+  double* C[3] = {nullptr, nullptr, nullptr};
+  double* w = nullptr;
+  bool orth[3] = {false, false, false};
+  std::vector<DevMem> mem;    // owned storage (may be empty for views)
+};
+
+struct TruncStats {
+  int tucker[3] = {0, 0, 0};
+  int basis[3] = {0, 0, 0};
+  int in_rank = 0, out_rank = 0, t2c_mode = 0;
+  double energy = 0.0, min_margin = 1e300;
+};
+
+// RHOSVD -> core -> T2C (S11-S13).  Output: orthonormal Q (n x r_l), orthogonal CP terms.
+// rank_cap > 0: output rank limit (FC_ERR_CAPACITY with stats.out_rank = required).
+TT truncate_tt(fc_ctx c, const TT& x, double eps, int rank_cap, TruncStats* stats);
+// T2C of a dense core (r1 x r2 x r3, column-major) with bases Z (n x r_l, orthonormal):
+// eps-cut (keep <= 0) or top-`keep` triples.  Used by the truncation and the spectral CP.
+TT tucker_to_canonical(fc_ctx c, const double* core, const int r[3], double* const Z[3], int n, double eps,
+                       int keep, int rank_cap, TruncStats* stats);
+// x + a*y (concatenation; bases concatenated, coefficients block-diagonal)
+TT tt_axpy(cudaStream_t st, const TT& x, double a, const TT& y);
+// <x, y>  (result in device scalar `out`, and returned on the host when sync)
+double tt_dot(fc_ctx c, const TT& x, const TT& y);
+// expand to plain CP factors U_l = Q_l C_l into dst (n x R, ld) and weights
+void tt_expand(cudaStream_t st, const TT& x, double* const U[3], const int ld[3], double* w);
+// view of a plain CP as TT (Q_l = U_l, C_l = I_R)
+TT tt_from_cp(cudaStream_t st, int n, int R, const double* w, double* const U[3], const int ld[3]);
+// copy
+TT tt_copy(cudaStream_t st, const TT& x);
+
+}  // namespace fc

@@ -1,0 +1,133 @@
+"""GPU parity: DMMA GEMM, fracop_apply (S5-S8) and cp_dot (S10) against the oracle, with
+shared inputs (eigenpairs and spectral CP injected through sl_set_eigen/op_set_spectral_cp)."""
+import numpy as np
+import pytest
+
+from oracle import cp as cpm
+from oracle import spectral as sp
+from oracle import sturm
+from synth import make_problem, random_cp
+
+pytestmark = pytest.mark.gpu
+
+
+def _shared_setup(ctx, p, F_eps=1e-6, r_fixed=None):
+    from paper_2006_09314_b200.binding import DeviceCP, make_params, FC_F, FC_G
+    lams, V = [], []
+    for l in range(3):
+        lam, Vl = sturm.eigenpairs(p.a_mid[l])
+        lams.append(lam)
+        V.append(Vl)
+    prm = make_params(p.alpha, p.beta, p.eps)
+    for l in range(3):
+        ctx.sl_set_eigen(p.n, l, lams[l], V[l], prm)
+    if p.n <= 64:
+        F = sp.spectral_cp(lams, sp.FC_F, p.alpha, p.beta, F_eps, rank=r_fixed)
+        G = sp.spectral_cp(lams, sp.FC_G, p.alpha, p.beta, F_eps, rank=6, spd_guard=True)
+    else:   # random spectral CPs of the C5 shape (the apply kernel does not care)
+        w, U = random_cp(p.n, r_fixed or 8, 77)
+        F = cpm.CP(w, U)
+        w, U = random_cp(p.n, 6, 78)
+        G = cpm.CP(w, U)
+    ctx.op_set_spectral_cp(FC_F, DeviceCP.from_numpy(F.w, F.U))
+    ctx.op_set_spectral_cp(FC_G, DeviceCP.from_numpy(G.w, G.U))
+    return lams, V, F, G
+
+
+@pytest.mark.parametrize("tA,tB,M,N,K", [(0, 0, 64, 64, 64), (1, 0, 37, 129, 200), (0, 1, 130, 3, 17),
+                                         (1, 1, 1, 77, 65), (0, 0, 300, 260, 1)])
+def test_dgemm(lib, tA, tB, M, N, K):
+    import torch
+    ctx = lib.context()
+    rng = np.random.default_rng(M * 7 + N)
+    A = rng.standard_normal((K, M) if tA == 0 else (M, K))   # stored row-major == col-major transposed
+    B = rng.standard_normal((N, K) if tB == 0 else (K, N))
+    Cm = rng.standard_normal((N, M))
+    At, Bt, Ct = (torch.tensor(v, device="cuda") for v in (A, B, Cm))
+    # column-major views: colmajor(X) = X_rowmajor.T
+    opA = A.T if tA == 0 else A
+    opB = B.T if tB == 0 else B
+    ref = 0.5 * opA @ opB + 0.25 * Cm.T
+    lda = A.shape[1]
+    ldb = B.shape[1]
+    ctx.dgemm(tA, tB, M, N, K, 0.5, At, lda, Bt, ldb, 0.25, Ct, M)
+    got = Ct.cpu().numpy().T
+    assert np.max(np.abs(got - ref)) <= 1e-13 * max(1.0, np.max(np.abs(ref))) * np.sqrt(K)
+
+
+@pytest.mark.parametrize("n,R", [(32, 5), (37, 1), (64, 13)])
+def test_fracop_apply_parity(lib, n, R):
+    from paper_2006_09314_b200.binding import DeviceCP, FC_F, FC_G
+    p = make_problem("C1", n=n)
+    ctx = lib.context()
+    lams, V, F, G = _shared_setup(ctx, p)
+    w, U = random_cp(n, R, 5)
+    x = cpm.CP(np.linspace(0.5, 2.0, R), U)
+    for which, spec in ((FC_F, F), (FC_G, G)):
+        y = ctx.fracop_apply(which, DeviceCP.from_numpy(x.w, x.U))
+        yw, yU = y.to_numpy()
+        ref = cpm.apply(V, spec, x)
+        assert y.rank == ref.rank == spec.rank * R
+        assert np.max(np.abs(yw - ref.w) / np.abs(ref.w)) < 1e-12
+        for l in range(3):
+            assert np.max(np.abs(yU[l] - ref.U[l])) < 1e-12
+
+
+def test_fracop_apply_zero_rank_and_capacity(lib):
+    from paper_2006_09314_b200.binding import DeviceCP, FC_F, FCError
+    p = make_problem("C1", n=16)
+    ctx = lib.context()
+    _shared_setup(ctx, p)
+    x = DeviceCP(16, 4, rank=0)
+    assert ctx.fracop_apply(FC_F, x).rank == 0
+    w, U = random_cp(16, 3, 1)
+    xs = DeviceCP.from_numpy(w, U)
+    with pytest.raises(FCError) as e:
+        ctx.fracop_apply(FC_F, xs, DeviceCP(16, 2))
+    assert e.value.code == -3
+
+
+@pytest.mark.parametrize("n,R,r", [(256, 16, 8), (1024, 64, 16), (2048, 256, 32)])
+def test_fracop_apply_c5_sampled(lib, n, R, r):
+    """BJ configs[4] sizes in the bench's launch configuration; 64 sampled columns per mode
+    are recomputed by the oracle's formula y = V (u_k . V^T x_j) / ||.||."""
+    from paper_2006_09314_b200.binding import DeviceCP, FC_F
+    p = make_problem("C1", n=n)
+    ctx = lib.context()
+    lams, V, F, _ = _shared_setup(ctx, p, r_fixed=r)
+    w, U = random_cp(n, R, 5)
+    y = ctx.fracop_apply(FC_F, DeviceCP.from_numpy(w, U))
+    assert y.rank == r * R
+    rng = np.random.default_rng(0)
+    cols = rng.choice(r * R, size=64, replace=False)
+    yw = y.w[:r * R].cpu().numpy()
+    wref = np.ones(64)
+    for l in range(3):
+        got = y.U[l][cols].cpu().numpy().T
+        k, j = cols // R, cols % R
+        Yh = F.U[l][:, k] * (V[l].T @ U[l][:, j])
+        ref = V[l] @ Yh
+        nrm = np.linalg.norm(ref, axis=0)
+        wref *= nrm
+        assert np.max(np.abs(got - ref / nrm)) < 1e-12
+    wref *= F.w[cols // R] * w[cols % R]
+    assert np.max(np.abs(yw[cols] - wref) / np.abs(wref)) < 1e-12
+
+
+@pytest.mark.parametrize("n,R1,R2", [(32, 3, 4), (129, 17, 1), (1024, 64, 200)])
+def test_cp_dot_parity(lib, n, R1, R2):
+    from paper_2006_09314_b200.binding import DeviceCP
+    p = make_problem("C1", n=n)
+    ctx = lib.context()
+    _shared_setup(ctx, p)
+    x = cpm.CP(*random_cp(n, R1, 1))
+    y = cpm.CP(*random_cp(n, R2, 2))
+    x.w = np.linspace(-1, 2, R1)
+    got = ctx.cp_dot(DeviceCP.from_numpy(x.w, x.U), DeviceCP.from_numpy(y.w, y.U))
+    ref = cpm.dot(x, y)
+    scale = cpm.norm(x) * cpm.norm(y)
+    assert abs(got - ref) <= 1e-13 * scale
+    z = ctx.cp_axpy(DeviceCP.from_numpy(x.w, x.U), -0.3, DeviceCP.from_numpy(y.w, y.U))
+    zw, zU = z.to_numpy()
+    ref = cpm.axpy(x, -0.3, y)
+    assert np.array_equal(zw, ref.w) and all(np.array_equal(zU[l], ref.U[l]) for l in range(3))
