@@ -70,7 +70,7 @@ typedef struct {
     int kmax;            /* max PCG iterations (A17); <= 0 -> 100                           */
     int precond_rank;    /* rank r_G of the preconditioner CP (A7); <= 0 -> 6    [P:990]    */
     int op_rank;         /* > 0: fixed rank of the operator CP (C5 sweep); 0: eps_D-driven  */
-    int rank_cap;        /* max CP rank of any iterate (capacity); <= 0 -> 4096             */
+    int rank_cap;        /* max CP rank of any iterate (capacity); <= 0 -> 2^20             */
     int boundary;        /* 0: paper boundary rule [P:517-518] (A2); 1: standard            */
 } fc_params;
 
@@ -151,6 +151,14 @@ int cp_axpy(fc_ctx ctx, const fc_cp* x, double a, const fc_cp* y, fc_cp* z);
  * info may be NULL.  x and y must not alias. */
 int cp_truncate(fc_ctx ctx, const fc_cp* x, double eps, fc_cp* y, fc_trunc_info* info);
 
+/* fracop_apply_truncate: y = trunc(F(A) x, eps) fused (S5-S13): the
+ * Khatri-Rao Hadamard product is formed in the eigenbasis on a reduced basis
+ * [w_a (.) V^T q_b] (w_a: basis of the spectral CP's factors, q_b: of x's), the RHOSVD runs
+ * on that tensor, and only the surviving Tucker columns are transformed back.  Equal in exact
+ * arithmetic to cp_truncate(fracop_apply(x), eps) because each V_l is orthogonal.  This is
+ * the operator step pcg_solve uses.  Same output/info/CAPACITY rules as cp_truncate. */
+int fracop_apply_truncate(fc_ctx ctx, int which, const fc_cp* x, double eps, fc_cp* y, fc_trunc_info* info);
+
 /* ---- the solver: S14 ------------------------------------------------------------------ */
 /* pcg_solve: Algorithm 1 [P:1825-1872] with fun = fracop_apply(FC_F), precond =
  * fracop_apply(FC_G), trunc = cp_truncate(eps); X0 = 0 (A14), R0 = B untruncated (A15).
@@ -165,6 +173,8 @@ int fc_dgemm(fc_ctx ctx, int transA, int transB, int M, int N, int K, double alp
 /* Milliseconds of the last launch of the dominant kernel of the last API call (events on
  * the context stream) and its algorithmic flop and byte counts (for the roofline line). */
 int fc_last_kernel_stats(fc_ctx ctx, double* ms, double* flops, double* bytes, int* launches);
+/* Process-wide count of CUDA kernels this library has launched (host-side counter). */
+int fc_kernel_launches(long long* count);
 
 #ifdef __cplusplus
 }

@@ -51,9 +51,14 @@ class NotSPD(RuntimeError):
 
 def pcg(fun, precond, B: CP, eps: float, tol_stop: float, kmax: int = 100, trunc=None):
     """Algorithm 1.  fun/precond: CP -> CP (untruncated applies); trunc(x, eps) -> CP."""
-    trunc = truncate if trunc is None else trunc
     rep = {"rel_res": [], "rank_X": [], "rank_R": [], "rank_Z": [], "rank_P": [],
-           "rank_S": [], "t_iter": [], "converged": False, "iters": 0}
+           "rank_S": [], "t_iter": [], "converged": False, "iters": 0, "margins": []}
+    if trunc is None:
+        def trunc(x, e):                                      # logs the cut margins (A23)
+            info = {}
+            y = truncate(x, e, info)
+            rep["margins"].append(min(info.get("margins", [np.inf]) or [np.inf]))
+            return y
     normB = cpm.norm(B)
     X = cpm.zeros(B.shape)                                   # X^(0) = 0          (A14)
     R = B.copy()                                             # line 1, R^0 = B    (A15)

@@ -80,10 +80,22 @@ def spectral_cp(lams, kind: int, alpha: float, beta: float, eps: float,
         r = rank
         out = tucker_to_canonical(core, Z, None, keep=r)
         if spd_guard:
-            maxr = int(np.prod(core.shape))
-            while cp_min_entry(out) <= 0 and r < maxr:
-                r += 1
+            # reading A7': raise the T2C rank (up to 64) until the CP is positive on the grid;
+            # if the Tucker approximation itself is not positive at that accuracy, tighten its
+            # tolerance tenfold and repeat (up to eps/1e4)
+            e = eps
+            while cp_min_entry(out) <= 0:
+                if r < min(64, int(np.prod(core.shape))):
+                    r += 1
+                elif e > eps * 1e-4:
+                    e /= 10.0
+                    core, Z = hosvd(D, e)
+                    r = rank
+                else:
+                    break
                 out = tucker_to_canonical(core, Z, None, keep=r)
+            if info is not None:
+                info["guard_eps"] = e
     if info is not None:
         info["rank"] = out.rank
         diff = np.einsum("k,ik,jk,lk->ijl", out.w, out.U[0], out.U[1], out.U[2]) - D

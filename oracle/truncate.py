@@ -29,15 +29,25 @@ def tail_sums(s2: np.ndarray) -> np.ndarray:
     return t
 
 
-def rank_cut(s2: np.ndarray, thr: float, rmin: int = 1) -> int:
-    """min{ r >= rmin : sum_{k > r} s2_k <= thr }, ties at the cut kept together (A23)."""
+def rank_cut(s2: np.ndarray, thr: float, rmin: int = 1, margins: list | None = None) -> int:
+    """min{ r >= rmin : sum_{k > r} s2_k <= thr }, ties at the cut kept together (A23).
+
+    `margins` (logging only) receives the relative distance of thr to the two tails that
+    bracket the decision, min(|t[r]-thr|, |t[r-1]-thr|)/thr: a small value marks a cut that
+    rounding differences between two implementations may flip (the noise band of A23)."""
     t = tail_sums(s2)
     r = rmin
     while r < s2.size and t[r] > thr:
         r += 1
-    while 0 < r < s2.size and s2[r] == s2[r - 1]:
+    while 0 < r < s2.size and s2[r] == s2[r - 1] and s2[r] > 0:   # A23: zero terms never bind
         r += 1
-    return min(r, s2.size)
+    r = min(r, s2.size)
+    if margins is not None and thr > 0:
+        m = abs(t[r] - thr) / thr
+        if r - 1 >= rmin:
+            m = min(m, abs(t[r - 1] - thr) / thr)
+        margins.append(m)
+    return r
 
 
 def tucker_to_canonical(core: np.ndarray, Z: list, eps: float | None, keep: int | None = None,
@@ -63,10 +73,11 @@ def tucker_to_canonical(core: np.ndarray, Z: list, eps: float | None, keep: int 
     nb2 = float(np.sum(core * core))
     if nb2 == 0.0:
         return zeros(tuple(z.shape[0] for z in Z))
+    margins = info.setdefault("margins", []) if info is not None else None
     if keep is not None:
         R = min(keep, len(trip))
     else:
-        R = rank_cut(s_all ** 2, (eps / 2.0) ** 2 * nb2)
+        R = rank_cut(s_all ** 2, (eps / 2.0) ** 2 * nb2, margins=margins)
     if info is not None:
         info["t2c_mode"] = c
         info["t2c_candidates"] = len(trip)
@@ -91,10 +102,11 @@ def truncate(x: CP, eps: float, info: dict | None = None) -> CP:
     E = float(np.sum(w * w))
     thr = (eps / 2.0) ** 2 * E
     Z, C, ranks = [], [], []
+    margins = info.setdefault("margins", []) if info is not None else None
     for l in range(3):
         A = U[l] * w[None, :]                                  # side matrix U_l diag(xi)
         Zf, s, _ = np.linalg.svd(A, full_matrices=False)       # 2. singular values
-        r = rank_cut(s ** 2, thr)                              # 3. tail from the small end
+        r = rank_cut(s ** 2, thr, margins=margins)             # 3. tail from the small end
         Z.append(Zf[:, :r])                                    # 4. Z_l
         C.append(Z[-1].T @ U[l])                               #    C_l = Z_l^T U_l
         ranks.append(r)

@@ -67,7 +67,7 @@ class FCError(RuntimeError):
 ENTRY_POINTS = ["fc_create", "fc_destroy", "fc_last_error", "fc_set_stream", "sl_setup", "sl_get_eigen",
                 "sl_set_eigen", "op_get_spectral_cp", "op_set_spectral_cp", "op_spectral_rank",
                 "fracop_apply", "precond_apply", "cp_dot", "cp_axpy", "cp_truncate", "pcg_solve",
-                "fc_dgemm", "fc_last_kernel_stats"]
+                "fc_dgemm", "fc_last_kernel_stats", "fc_kernel_launches", "fracop_apply_truncate"]
 
 
 def load_library(path: str = LIB_PATH) -> C.CDLL:
@@ -88,9 +88,11 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "fracop_apply": ([P, I, cpp, cpp], I), "precond_apply": ([P, cpp, cpp], I),
         "cp_dot": ([P, cpp, cpp, C.POINTER(D)], I), "cp_axpy": ([P, cpp, D, cpp, cpp], I),
         "cp_truncate": ([P, cpp, D, cpp, C.POINTER(fc_trunc_info)], I),
+        "fracop_apply_truncate": ([P, I, cpp, D, cpp, C.POINTER(fc_trunc_info)], I),
         "pcg_solve": ([P, cpp, C.POINTER(fc_params), cpp, C.POINTER(fc_pcg_report)], I),
         "fc_dgemm": ([P, I, I, I, I, I, D, P, I, P, I, D, P, I], I),
         "fc_last_kernel_stats": ([P, C.POINTER(D), C.POINTER(D), C.POINTER(D), C.POINTER(I)], I),
+        "fc_kernel_launches": ([C.POINTER(C.c_longlong)], I),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -145,6 +147,12 @@ class Library:
 
     def context(self, stream=None) -> "Context":
         return Context(self, stream)
+
+
+def kernel_launches(L: "Library") -> int:
+    v = C.c_longlong()
+    L.lib.fc_kernel_launches(C.byref(v))
+    return v.value
 
 
 class Context:
@@ -250,14 +258,34 @@ class Context:
             y.rank = ys.rank
             return y, info
 
-    def pcg_solve(self, b: DeviceCP, params: fc_params, cap: int = 4096):
-        u = DeviceCP(self.n, cap)
-        rep = fc_pcg_report()
-        bs, us = b.struct(), u.struct()
-        rc = self.lib.pcg_solve(self.h, C.byref(bs), C.byref(params), C.byref(us), C.byref(rep))
-        self._check(rc, ok=(0, 1, 2))
-        u.rank = us.rank
-        return u, rep.as_dict(), rc
+    def fracop_apply_truncate(self, which, x: DeviceCP, eps: float, cap: int | None = None):
+        cap = cap if cap is not None else max(4 * x.rank, 64)
+        while True:
+            y = DeviceCP(self.n, cap)
+            info = fc_trunc_info()
+            xs, ys = x.struct(), y.struct()
+            rc = self.lib.fracop_apply_truncate(self.h, which, C.byref(xs), C.c_double(eps), C.byref(ys),
+                                                C.byref(info))
+            if rc == -3 and info.required_rank > cap:
+                cap = info.required_rank
+                continue
+            self._check(rc)
+            y.rank = ys.rank
+            return y, info
+
+    def pcg_solve(self, b: DeviceCP, params: fc_params, cap: int = 4096, u: DeviceCP | None = None):
+        while True:
+            if u is None or u.cap < cap:
+                u = DeviceCP(self.n, cap)
+            rep = fc_pcg_report()
+            bs, us = b.struct(), u.struct()
+            rc = self.lib.pcg_solve(self.h, C.byref(bs), C.byref(params), C.byref(us), C.byref(rep))
+            if rc == -3 and us.rank > u.cap:        # the solution's rank exceeds u.cap: re-run
+                cap = us.rank
+                continue
+            self._check(rc, ok=(0, 1, 2))
+            u.rank = us.rank
+            return u, rep.as_dict(), rc
 
     # ---- raw ----
     def dgemm(self, transA, transB, M, N, K, alpha, A, lda, B, ldb, beta, Cm, ldc):

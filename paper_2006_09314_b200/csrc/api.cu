@@ -145,8 +145,18 @@ void copy_cp_block(cudaStream_t st, int n, const fc_cp& src, fc_cp& dst, int col
 
 }  // namespace fc
 
+namespace fc {
+std::atomic<long long> g_launches{0};
+}
+
 // ======================================================================================
 extern "C" {
+
+int fc_kernel_launches(long long* count) {
+  if (!count) return FC_ERR_INVALID_ARG;
+  *count = fc::g_launches.load();
+  return FC_OK;
+}
 
 int fc_create(fc_ctx* ctx, void* cuda_stream) {
   if (!ctx) return FC_ERR_INVALID_ARG;

@@ -15,7 +15,17 @@
     }                                                                               \
   } while (0)
 
-#define FC_CHECK_LAUNCH() FC_CUDA_TRY(cudaGetLastError())
+#define FC_CHECK_LAUNCH()                 \
+  do {                                    \
+    fc::g_launches.fetch_add(1);          \
+    FC_CUDA_TRY(cudaGetLastError());      \
+  } while (0)
+
+#include <atomic>
+namespace fc {
+// every kernel launch of the library passes FC_CHECK_LAUNCH (fc_kernel_launches in the ABI)
+extern std::atomic<long long> g_launches;
+}  // namespace fc
 
 namespace fc {
 
@@ -90,8 +100,19 @@ struct GemmBatch {
   const double* krU; int ldkr;
   const double* colscale;
 };
+// Generated A operand (transA = 0): A(m, k) = f((l1[m % n1] + l2[m / n1]) + l3[k]) with the
+// spectral function f of kind FC_F / FC_G / FC_POW_PLUS / FC_POW_MINUS [P:640-648, P:693].
+struct GenA {
+  int kind = -1;
+  double alpha = 0, beta = 0;
+  const double* l1 = nullptr;
+  const double* l2 = nullptr;
+  const double* l3 = nullptr;
+  int n1 = 0;
+};
 struct GemmArgs {
   int transA = 0, transB = 0;
+  GenA gen;
   int krR = 0;           // > 0 enables the Khatri-Rao B operand
   int splitk = 1;        // > 1: atomicAdd epilogue (beta must be 1, C pre-initialised)
   double alpha = 1.0, beta = 0.0;

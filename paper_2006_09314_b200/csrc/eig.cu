@@ -183,6 +183,40 @@ __global__ void sl_invit_kernel(int n, const double* __restrict__ d_all, const d
   sign_rule(n, v, 1);
 }
 
+// Near-degenerate eigenvalues (relative gap < kClusterGap): inverse iteration from different
+// start vectors may return (nearly) the same vector for every member of the cluster.  One
+// thread per cluster re-runs modified Gram-Schmidt (twice) over the cluster's vectors in index
+// order; any orthonormal basis of a cluster's span is an eigenbasis to the accuracy the gap
+// allows (reading A25).  Clusters are short runs (pairs in practice).
+constexpr double kClusterGap = 1e-10;
+__global__ void sl_cluster_orth_kernel(int n, const double* __restrict__ lam_all, double* V_all) {
+  const int l = blockIdx.y;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double* lam = lam_all + (size_t)l * n;
+  double* V = V_all + (size_t)l * n * n;
+  auto close = [&](int a, int b) { return (lam[b] - lam[a]) <= kClusterGap * fabs(lam[b]); };
+  if (i > 0 && close(i - 1, i)) return;           // not the first member
+  if (i + 1 >= n || !close(i, i + 1)) return;      // singleton
+  int end = i + 1;
+  while (end + 1 < n && close(end, end + 1)) ++end;
+  for (int j = i + 1; j <= end; ++j) {
+    double* vj = V + (size_t)j * n;
+    for (int pass = 0; pass < 2; ++pass) {
+      for (int k = i; k < j; ++k) {
+        const double* vk = V + (size_t)k * n;
+        double d = 0.0;
+        for (int t = 0; t < n; ++t) d += vk[t] * vj[t];
+        for (int t = 0; t < n; ++t) vj[t] -= d * vk[t];
+      }
+      double s2 = 0.0;
+      for (int t = 0; t < n; ++t) s2 += vj[t] * vj[t];
+      double inv = 1.0 / sqrt(s2);
+      for (int t = 0; t < n; ++t) vj[t] *= inv;
+    }
+  }
+}
+
 // G <- 1.5 I - 0.5 G  (Newton-Schulz step V <- V (3I - V^T V)/2)
 __global__ void ns_matrix_kernel(int n, double* G) {
   const int l = blockIdx.y;
@@ -408,6 +442,94 @@ __global__ void __launch_bounds__(256) orth_backtransform_kernel(const __grid_co
   }
 }
 
+// Column-pivoted modified Gram-Schmidt (rank revealing, no Gram squaring), one CTA per matrix.
+// A (n x p, column-major, overwritten with residuals) -> Q (n x k, orthonormal, k <= p) with
+// every column of A within tau * ||a_c|| of span(Q).  Pivot: largest residual norm among the
+// columns not yet within their tolerance.  Each accepted vector is re-orthogonalised against Q.
+constexpr int kPmgsThreads = 1024;
+__global__ void __launch_bounds__(kPmgsThreads) pmgs_kernel(const __grid_constant__ PmgsBatch B) {
+  extern __shared__ double sh[];
+  const PmgsEntry& E = B.e[blockIdx.x];
+  const int n = E.n, p = E.p;
+  double* nrm2 = sh;          // current residual norms^2
+  double* lim2 = sh + p;      // (tau * original norm)^2
+  double* coef = sh + 2 * p;  // projections
+  __shared__ int piv_s;
+  __shared__ double pnorm_s;
+  __shared__ double red[33];
+  const int tid = threadIdx.x, nt = blockDim.x, warp = tid >> 5, ln = tid & 31, nw = nt >> 5;
+  double* A = E.A;
+  for (int c = warp; c < p; c += nw) {
+    double s = 0.0;
+    for (int i = ln; i < n; i += 32) s += A[i + (size_t)c * E.lda] * A[i + (size_t)c * E.lda];
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (ln == 0) { nrm2[c] = s; lim2[c] = E.tau * E.tau * s; }
+  }
+  __syncthreads();
+  int k = 0;
+  for (; k < min(p, n); ++k) {
+    if (tid == 0) {
+      int best = -1;
+      double bv = 0.0;
+      for (int c = 0; c < p; ++c)
+        if (nrm2[c] > lim2[c] && nrm2[c] > bv) { bv = nrm2[c]; best = c; }
+      piv_s = best;
+    }
+    __syncthreads();
+    const int piv = piv_s;
+    if (piv < 0) break;
+    double* q = E.Q + (size_t)k * E.ldq;
+    for (int i = tid; i < n; i += nt) q[i] = A[i + (size_t)piv * E.lda];
+    __syncthreads();
+    // re-orthogonalise against Q[:, :k] (one CGS pass; the residual already is one MGS pass)
+    for (int j = warp; j < k; j += nw) {
+      const double* qj = E.Q + (size_t)j * E.ldq;
+      double s = 0.0;
+      for (int i = ln; i < n; i += 32) s += qj[i] * q[i];
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (ln == 0) coef[j] = s;
+    }
+    __syncthreads();
+    double part = 0.0;
+    for (int i = tid; i < n; i += nt) {
+      double v = q[i];
+      for (int j = 0; j < k; ++j) v -= coef[j] * E.Q[i + (size_t)j * E.ldq];
+      q[i] = v;
+      part += v * v;
+    }
+    double s2 = block_sum(part, red);
+    if (tid == 0) pnorm_s = s2;
+    __syncthreads();
+    if (pnorm_s <= 0.0) {          // numerically dependent: retire the column
+      if (tid == 0) nrm2[piv] = 0.0;
+      __syncthreads();
+      --k;
+      continue;
+    }
+    const double inv = 1.0 / sqrt(pnorm_s);
+    for (int i = tid; i < n; i += nt) q[i] *= inv;
+    __syncthreads();
+    // project the new direction out of every remaining column (warp per column)
+    for (int c = warp; c < p; c += nw) {
+      if (nrm2[c] <= lim2[c]) continue;
+      double* a = A + (size_t)c * E.lda;
+      double s = 0.0;
+      for (int i = ln; i < n; i += 32) s += q[i] * a[i];
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      double r2 = 0.0;
+      for (int i = ln; i < n; i += 32) {
+        double v = a[i] - s * q[i];
+        a[i] = v;
+        r2 += v * v;
+      }
+      for (int o = 16; o > 0; o >>= 1) r2 += __shfl_xor_sync(0xffffffffu, r2, o);
+      if (ln == 0) nrm2[c] = r2;
+    }
+    __syncthreads();
+  }
+  if (tid == 0) *E.k_out = k;
+}
+
 __global__ void rank_cut_kernel(int count, const double* __restrict__ s2, double factor,
                                 const double* __restrict__ energy, int* r_out, double* margin_out) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
@@ -417,7 +539,8 @@ __global__ void rank_cut_kernel(int count, const double* __restrict__ s2, double
   int r = count;                 // default: keep everything
   double margin = 1e300;
   for (int k = count - 1; k >= 1; --k) {
-    acc += fmax(s2[k], 0.0);
+    acc += s2[k];   // not clamped: eigenvalues of a PSD Gram at the noise floor are +-eps||M||,
+                    // clamping would bias the tail upward by (#noise) * eps ||M||
     double m = fabs(acc - thr) / (thr > 0 ? thr : 1.0);
     if (acc <= thr) {
       r = k;                    // tail beyond index k-1 fits: keep k values
@@ -428,7 +551,7 @@ __global__ void rank_cut_kernel(int count, const double* __restrict__ s2, double
     }
   }
   if (count >= 1 && r < 1) r = 1;
-  while (r > 0 && r < count && s2[r] == s2[r - 1]) ++r;   // ties kept together (A23)
+  while (r > 0 && r < count && s2[r] == s2[r - 1] && s2[r] > 0) ++r;   // ties kept together (A23)
   *r_out = count == 0 ? 0 : r;
   if (margin_out) *margin_out = margin;
 }
@@ -456,6 +579,8 @@ void sl_eigen_device(cudaStream_t st, int n, const double* a_mid_dev, int bounda
   FC_CHECK_LAUNCH();
   double* scr = s.alloc<double>((size_t)5 * 3 * n * n);
   sl_invit_kernel<<<dim3(cdiv(n, 64), 3), 64, 0, st>>>(n, d, e, lam, V, scr);
+  FC_CHECK_LAUNCH();
+  sl_cluster_orth_kernel<<<dim3(cdiv(n, 64), 3), 64, 0, st>>>(n, lam, V);
   FC_CHECK_LAUNCH();
   // Newton-Schulz polish: 2 steps of V <- V (3I - V^T V)/2 on DMMA GEMMs
   double* G = scr;                       // reuse: 3 n^2
@@ -516,6 +641,21 @@ void orthonormalize_cols(int N, double* Y, int ldy, int* r_dev, int rmax, cudaSt
   b.nb = 1;
   b.e[0] = SyevEntry{N, nullptr, 0, nullptr, nullptr, nullptr, Y, ldy, r_dev, nullptr};
   orth_backtransform_kernel<<<1, 256, (size_t)std::max(rmax, 1) * 8, st>>>(b);
+  FC_CHECK_LAUNCH();
+}
+
+void pmgs(const PmgsBatch& b, cudaStream_t st) {
+  if (b.nb == 0) return;
+  int maxp = 1;
+  for (int i = 0; i < b.nb; ++i) maxp = std::max(maxp, b.e[i].p);
+  const size_t smem = (size_t)3 * maxp * 8;
+  static bool attr = false;
+  if (!attr) {
+    FC_CUDA_TRY(cudaFuncSetAttribute(pmgs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    attr = true;
+  }
+  require(smem <= 200 * 1024, FC_ERR_CAPACITY, "pmgs: too many columns");
+  pmgs_kernel<<<b.nb, kPmgsThreads, smem, st>>>(b);
   FC_CHECK_LAUNCH();
 }
 

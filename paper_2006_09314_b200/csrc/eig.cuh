@@ -34,6 +34,22 @@ void syev_values(const SyevBatch& b, cudaStream_t st);
 // back-transformation of the leading r eigenvectors.
 void syev_vectors(const SyevBatch& b, int maxN, cudaStream_t st);
 
+// Column-pivoted modified Gram-Schmidt (rank revealing, no Gram squaring), one CTA per entry:
+// A (n x p, overwritten) -> Q (n x k) orthonormal, every column of A within tau*||a_c|| of
+// span(Q); k written to *k_out (device).
+struct PmgsEntry {
+  int n, p;
+  double* A; int lda;
+  double* Q; int ldq;
+  int* k_out;
+  double tau;
+};
+struct PmgsBatch {
+  int nb = 0;
+  PmgsEntry e[kMaxSyev];
+};
+void pmgs(const PmgsBatch& b, cudaStream_t st);
+
 // CGS2 orthonormalisation of the first *r_dev (<= rmax) columns of Y (N x ., ld ldy).
 void orthonormalize_cols(int N, double* Y, int ldy, int* r_dev, int rmax, cudaStream_t st);
 

@@ -51,6 +51,31 @@ __device__ __forceinline__ void load_tile_A(double* As, const GemmBatch& g, int 
   }
 }
 
+__device__ __forceinline__ double spectral_f(int kind, double alpha, double beta, double lam) {
+  if (kind == FC_F) return beta * pow(lam, alpha) + pow(lam, -alpha);
+  if (kind == FC_G) return 1.0 / (beta * pow(lam, alpha) + pow(lam, -alpha));
+  if (kind == FC_POW_PLUS) return pow(lam, alpha);
+  return pow(lam, -alpha);
+}
+
+// generated operand: A(m, k) = f((l1[m % n1] + l2[m / n1]) + l3[k])  (never stored)
+__device__ __forceinline__ void gen_tile_A(double* As, const GemmBatch& g, const GenA& gen, int m0, int k0, int kend,
+                                           int tid) {
+#pragma unroll 2
+  for (int i = 0; i < (BK * BM) / NT; ++i) {
+    int idx = tid + i * NT;
+    int mm = idx % BM, kk = idx / BM;
+    int m = m0 + mm, k = k0 + kk;
+    double v = 0.0;
+    if (m < g.M && k < kend) {
+      int i1 = m % gen.n1, i2 = m / gen.n1;
+      double lam = (__ldg(gen.l1 + i1) + __ldg(gen.l2 + i2)) + __ldg(gen.l3 + k);
+      v = spectral_f(gen.kind, gen.alpha, gen.beta, lam);
+    }
+    As[kk * LDS + mm] = v;
+  }
+}
+
 __device__ __forceinline__ void load_tile_B(double* Bs, double* Ks, const GemmBatch& g, int transB, int krR,
                                             int n0, int k0, int kend, int tid) {
   if (krR > 0) {
@@ -83,7 +108,7 @@ __device__ __forceinline__ void load_tile_B(double* Bs, double* Ks, const GemmBa
   }
 }
 
-template <bool KR>
+template <bool KR, bool GEN>
 __global__ void __launch_bounds__(NT) dgemm_dmma_kernel(const __grid_constant__ GemmArgs args) {
   extern __shared__ __align__(16) double smem[];
   double* As = smem;
@@ -116,7 +141,8 @@ __global__ void __launch_bounds__(NT) dgemm_dmma_kernel(const __grid_constant__ 
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
     if (s < nk) {
-      load_tile_A(As + s * STAGE_ELEMS, g, args.transA, m0, kbeg + s * BK, kend, tid);
+      if (GEN) gen_tile_A(As + s * STAGE_ELEMS, g, args.gen, m0, kbeg + s * BK, kend, tid);
+      else load_tile_A(As + s * STAGE_ELEMS, g, args.transA, m0, kbeg + s * BK, kend, tid);
       load_tile_B(Bs + s * STAGE_ELEMS, Ks + s * STAGE_ELEMS, g, args.transB, KR ? args.krR : 0, n0,
                   kbeg + s * BK, kend, tid);
     }
@@ -132,7 +158,8 @@ __global__ void __launch_bounds__(NT) dgemm_dmma_kernel(const __grid_constant__ 
       int nt = kt + STAGES - 1;
       if (nt < nk) {
         int sl = nt % STAGES;
-        load_tile_A(As + sl * STAGE_ELEMS, g, args.transA, m0, kbeg + nt * BK, kend, tid);
+        if (GEN) gen_tile_A(As + sl * STAGE_ELEMS, g, args.gen, m0, kbeg + nt * BK, kend, tid);
+        else load_tile_A(As + sl * STAGE_ELEMS, g, args.transA, m0, kbeg + nt * BK, kend, tid);
         load_tile_B(Bs + sl * STAGE_ELEMS, Ks + sl * STAGE_ELEMS, g, args.transB, KR ? args.krR : 0, n0,
                     kbeg + nt * BK, kend, tid);
       }
@@ -195,14 +222,16 @@ void gemm(const GemmArgs& a, cudaStream_t st) {
   const int smem2 = 2 * STAGES * STAGE_ELEMS * (int)sizeof(double);
   const int smem3 = 3 * STAGES * STAGE_ELEMS * (int)sizeof(double);
   if (!attr) {
-    FC_CUDA_TRY(cudaFuncSetAttribute(dgemm_dmma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2));
-    FC_CUDA_TRY(cudaFuncSetAttribute(dgemm_dmma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem3));
+    FC_CUDA_TRY(cudaFuncSetAttribute(dgemm_dmma_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2));
+    FC_CUDA_TRY(cudaFuncSetAttribute(dgemm_dmma_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem3));
+    FC_CUDA_TRY(cudaFuncSetAttribute(dgemm_dmma_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2));
     attr = true;
   }
   dim3 grid(cdiv(maxM, BM), cdiv(maxN, BN), a.nbatch * a.splitk);
   require(grid.y <= 65535 && grid.z <= 65535, FC_ERR_INVALID_ARG, "gemm grid too large");
-  if (a.krR > 0) dgemm_dmma_kernel<true><<<grid, NT, smem3, st>>>(a);
-  else dgemm_dmma_kernel<false><<<grid, NT, smem2, st>>>(a);
+  if (a.gen.kind >= 0) dgemm_dmma_kernel<false, true><<<grid, NT, smem2, st>>>(a);
+  else if (a.krR > 0) dgemm_dmma_kernel<true, false><<<grid, NT, smem3, st>>>(a);
+  else dgemm_dmma_kernel<false, false><<<grid, NT, smem2, st>>>(a);
   FC_CHECK_LAUNCH();
 }
 

@@ -73,28 +73,20 @@ void ensure_spec_basis(fc_ctx c, SpecCP& sp) {
   Scratch s(st);
   int sdim[3];
   double* Wt[3];
-  for (int l = 0; l < 3; ++l) {
-    double* G = s.zeros<double>((size_t)r * r);
-    dgemm(st, 1, 0, r, r, n, 1.0, sp.Ul(n, l), n, sp.Ul(n, l), n, 1.0, G, r, std::max(1, std::min(cdiv(n, 256), 16)));
-    SyevBatch eb;
-    double* lam = s.alloc<double>(r);
-    double* Y = s.alloc<double>((size_t)r * r);
-    int* rr = s.alloc<int>(1);
-    eb.nb = 1;
-    eb.e[0] = SyevEntry{r, G, r, s.alloc<double>(r), s.alloc<double>(r), lam, Y, r, rr, s.alloc<double>((size_t)5 * r * r)};
-    syev_values(eb, st);
-    basis_rank_device(r, lam, 1e-20, rr, st);
-    syev_vectors(eb, r, st);
-    int h = 0;
-    FC_CUDA_TRY(cudaMemcpyAsync(&h, rr, sizeof(int), cudaMemcpyDeviceToHost, st));
+  {
+    // orthonormal basis of span(U_l) by column-pivoted MGS (columns kept to 1e-14)
+    PmgsBatch pb;
+    int* kd = s.alloc<int>(4);
+    for (int l = 0; l < 3; ++l) {
+      double* A = s.alloc<double>((size_t)n * r);
+      FC_CUDA_TRY(cudaMemcpyAsync(A, sp.Ul(n, l), (size_t)n * r * 8, cudaMemcpyDeviceToDevice, st));
+      Wt[l] = s.alloc<double>((size_t)n * std::min(n, r));
+      pb.e[pb.nb++] = PmgsEntry{n, r, A, n, Wt[l], n, kd + l, 1e-14};
+    }
+    pmgs(pb, st);
+    FC_CUDA_TRY(cudaMemcpyAsync(sdim, kd, 3 * sizeof(int), cudaMemcpyDeviceToHost, st));
     FC_CUDA_TRY(cudaStreamSynchronize(st));
-    require(h >= 1, FC_ERR_NOT_SPD, "spectral CP has a zero factor matrix");
-    sdim[l] = h;
-    Wt[l] = s.alloc<double>((size_t)n * h);
-    dgemm(st, 0, 0, n, h, r, 1.0, sp.Ul(n, l), n, Y, r, 0.0, Wt[l], n);
-    inv_sqrt_cols_kernel<<<nblocks((long long)n * h), 256, 0, st>>>(n, h, lam, Wt[l]);
-    FC_CHECK_LAUNCH();
-    orthonormalize_cols(n, Wt[l], n, rr, h, st);
+    for (int l = 0; l < 3; ++l) require(sdim[l] >= 1, FC_ERR_NOT_SPD, "spectral CP has a zero factor matrix");
   }
   sp.smax = std::max(sdim[0], std::max(sdim[1], sdim[2]));
   sp.W.ensure((size_t)3 * n * sp.smax);
@@ -255,6 +247,32 @@ int cp_truncate(fc_ctx c, const fc_cp* x, double eps, fc_cp* y, fc_trunc_info* i
   });
 }
 
+int fracop_apply_truncate(fc_ctx c, int which, const fc_cp* x, double eps, fc_cp* y, fc_trunc_info* info) {
+  return guard2(c, [&]() {
+    require(which >= 0 && which < 4, FC_ERR_INVALID_ARG, "which");
+    check_cp2(c, x, "x");
+    check_cp2(c, y, "y");
+    require(eps > 0 && std::isfinite(eps), FC_ERR_INVALID_ARG, "eps must be > 0");
+    require(c->have_eig[0] && c->have_eig[1] && c->have_eig[2], FC_ERR_NOT_READY, "eigenpairs missing");
+    SpecCP& sp = c->spec[which];
+    require(sp.valid, FC_ERR_NOT_READY, "spectral CP not set");
+    TruncStats S;
+    TT xt = tt_from_cp(c->st, c->n, x->rank, x->w, x->U, x->ld);
+    TT out;
+    try {
+      out = apply_truncate_tt(c, sp, xt, eps, 0, &S);
+    } catch (const Error& e) {
+      fill_info(info, S);
+      if (info && e.code == FC_ERR_CAPACITY) info->required_rank = S.out_rank;
+      throw;
+    }
+    fill_info(info, S);
+    if (y->cap < out.R && info) info->required_rank = out.R;
+    store_tt(c, out, y);
+    return FC_OK;
+  });
+}
+
 int pcg_solve(fc_ctx c, const fc_cp* b, const fc_params* prm, fc_cp* u, fc_pcg_report* rep) {
   return guard2(c, [&]() {
     check_cp2(c, b, "b");
@@ -264,7 +282,7 @@ int pcg_solve(fc_ctx c, const fc_cp* b, const fc_params* prm, fc_cp* u, fc_pcg_r
     require(eps > 0, FC_ERR_INVALID_ARG, "eps must be > 0");
     const double tol = prm->tol_stop > 0 ? prm->tol_stop : 10.0 * eps;     // A13
     const int kmax = std::min(prm->kmax > 0 ? prm->kmax : 100, FC_MAX_ITERS);  // A17
-    const int cap = prm->rank_cap > 0 ? prm->rank_cap : 4096;
+    const int cap = prm->rank_cap > 0 ? prm->rank_cap : (1 << 20);
     require(c->spec[FC_F].valid && c->spec[FC_G].valid, FC_ERR_NOT_READY, "spectral CPs missing");
     cudaStream_t st = c->st;
     fc_pcg_report local{};

@@ -71,11 +71,15 @@ __global__ void term_weights_kernel(int R, const double* __restrict__ w, const d
   }
 }
 
-// F = Lam^1/2 U^T from the (descending) eigenpairs of K^T K; lam < 0 clamped to 0.
+// F = Lam^1/2 U^T from the (descending) eigenpairs of K^T K.  Eigenvalues below the
+// eigensolver's noise level (kBasisTau * lam_max, bisection accuracy ~ 2 eps ||T||) are
+// numerical null directions of K and are set to 0 (their square roots would be pure noise).
+constexpr double kBasisTau = 1e-14;
 __global__ void sqrt_factor_kernel(int q, const double* lam, const double* U, double* F) {
+  const double lim = kBasisTau * lam[0];
   for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < q * q; idx += gridDim.x * blockDim.x) {
     int i = idx % q, j = idx / q;                 // F[i, j] = sqrt(lam_i) * U[j, i]
-    F[idx] = sqrt(fmax(lam[i], 0.0)) * U[j + (size_t)i * q];
+    F[idx] = lam[i] > lim ? sqrt(lam[i]) * U[j + (size_t)i * q] : 0.0;
   }
 }
 
@@ -366,9 +370,9 @@ TT tucker_to_canonical(fc_ctx c, const double* core, const int r[3], double* con
   return out;
 }
 
-TT truncate_tt(fc_ctx c, const TT& x, double eps, int rank_cap, TruncStats* stats) {
+TT truncate_tt(fc_ctx c, const TT& xin, double eps, int rank_cap, TruncStats* stats) {
   cudaStream_t st = c->st;
-  const int n = x.n, R = x.R;
+  const int n = xin.n, R = xin.R;
   TruncStats local;
   TruncStats& S = stats ? *stats : local;
   S.in_rank = R;
@@ -377,110 +381,88 @@ TT truncate_tt(fc_ctx c, const TT& x, double eps, int rank_cap, TruncStats* stat
     z.n = n;
     return z;
   }
+  Scratch s(st);
+  // ---- 1. orthonormal basis per mode: K = Q_l (n x q) -> pivoted MGS -> Qo (n x k), then
+  //         the coefficients in that basis Co = (Qo^T K) C.  Rank revealing without forming
+  //         K^T K (no squaring): every column of K is kept to 1e-13 of its norm.
+  double* Qo[3];
+  double* Co[3];
   int q[3];
+  {
+    PmgsBatch pb;
+    int* kdev = s.alloc<int>(4);
+    int map[3];
+    for (int l = 0; l < 3; ++l) {
+      map[l] = -1;
+      if (xin.orth[l]) continue;
+      require(xin.q[l] >= 1, FC_ERR_INVALID_ARG, "empty basis");
+      double* Kc = s.alloc<double>((size_t)n * xin.q[l]);
+      FC_CUDA_TRY(cudaMemcpyAsync(Kc, xin.Q[l], (size_t)n * xin.q[l] * 8, cudaMemcpyDeviceToDevice, st));
+      double* Qn = s.alloc<double>((size_t)n * std::min(n, xin.q[l]));
+      map[l] = pb.nb;
+      pb.e[pb.nb++] = PmgsEntry{n, xin.q[l], Kc, n, Qn, n, kdev + l, 1e-13};
+    }
+    pmgs(pb, st);
+    int kh[4] = {0, 0, 0, 0};
+    if (pb.nb) {
+      FC_CUDA_TRY(cudaMemcpyAsync(kh, kdev, 3 * sizeof(int), cudaMemcpyDeviceToHost, st));
+      FC_CUDA_TRY(cudaStreamSynchronize(st));
+    }
+    for (int l = 0; l < 3; ++l) {
+      if (map[l] < 0) {
+        Qo[l] = xin.Q[l];
+        Co[l] = xin.C[l];
+        q[l] = xin.q[l];
+        continue;
+      }
+      const int k = std::max(kh[l], 1);
+      Qo[l] = pb.e[map[l]].Q;
+      q[l] = k;
+      // Rm = Qo^T K (k x qin) ; Co = Rm C (k x R)
+      double* Rm = s.zeros<double>((size_t)k * xin.q[l]);
+      dgemm(st, 1, 0, k, xin.q[l], n, 1.0, Qo[l], n, xin.Q[l], n, 1.0, Rm, k,
+            std::max(1, std::min(cdiv(n, 256), 16)));
+      Co[l] = s.alloc<double>((size_t)k * R);
+      dgemm(st, 0, 0, k, R, xin.q[l], 1.0, Rm, k, xin.C[l], xin.q[l], 0.0, Co[l], k);
+    }
+  }
   for (int l = 0; l < 3; ++l) {
-    q[l] = x.q[l];
     S.basis[l] = q[l];
     require(q[l] >= 1 && q[l] <= 2048, FC_ERR_CAPACITY, "side-matrix basis dimension above 2048");
   }
-  Scratch s(st);
-  // ---- term norms and weights -----------------------------------------------------------
-  double* GQ[3];
-  double* QC[3];
+  // ---- 2. term norms n_l[t] = ||C_l[:, t]|| (orthonormal basis), xi_t, d_l[t] = xi_t/n_l[t] ----
   double* n2[3];
   double* dl[3];
   double* inv[3];
   for (int l = 0; l < 3; ++l) {
-    GQ[l] = x.orth[l] ? nullptr : s.alloc<double>((size_t)q[l] * q[l]);
-    QC[l] = x.orth[l] ? x.C[l] : s.alloc<double>((size_t)q[l] * R);
     n2[l] = s.alloc<double>(R);
     dl[l] = s.alloc<double>(R);
     inv[l] = s.alloc<double>(R);
   }
   double* xi = s.alloc<double>(R);
   double* energy = s.alloc<double>(4);
-  {
-    GemmArgs g;  // GQ = Q^T Q (split-K over n)
-    g.transA = 1;
-    g.beta = 1.0;
-    int nb = 0;
-    for (int l = 0; l < 3; ++l)
-      if (!x.orth[l]) {
-        FC_CUDA_TRY(cudaMemsetAsync(GQ[l], 0, (size_t)q[l] * q[l] * 8, st));
-        g.b[nb++] = GemmBatch{q[l], q[l], n, x.Q[l], n, x.Q[l], n, GQ[l], q[l], nullptr, 0, nullptr};
-      }
-    g.nbatch = nb;
-    g.splitk = std::max(1, std::min(cdiv(n, 256), 16));
-    gemm(g, st);
-    GemmArgs h;  // QC = GQ C
-    nb = 0;
-    for (int l = 0; l < 3; ++l)
-      if (!x.orth[l]) h.b[nb++] = GemmBatch{q[l], R, q[l], GQ[l], q[l], x.C[l], q[l], QC[l], q[l], nullptr, 0, nullptr};
-    h.nbatch = nb;
-    gemm(h, st);
-  }
   TermArgs ta;
   for (int l = 0; l < 3; ++l) {
-    ta.C[l] = x.C[l]; ta.QC[l] = QC[l]; ta.q[l] = q[l]; ta.n2[l] = n2[l];
+    ta.C[l] = Co[l]; ta.QC[l] = Co[l]; ta.q[l] = q[l]; ta.n2[l] = n2[l];
   }
   term_norms_kernel<<<dim3(cdiv(R, 8), 3), 256, 0, st>>>(R, ta);
   FC_CHECK_LAUNCH();
-  term_weights_kernel<<<1, 1024, 0, st>>>(R, x.w, n2[0], n2[1], n2[2], xi, dl[0], dl[1], dl[2], inv[0], inv[1],
+  term_weights_kernel<<<1, 1024, 0, st>>>(R, xin.w, n2[0], n2[1], n2[2], xi, dl[0], dl[1], dl[2], inv[0], inv[1],
                                           inv[2], energy);
   FC_CHECK_LAUNCH();
-
-  // ---- F = Lam^1/2 U^T of K^T K (non-orthonormal bases) -----------------------------------
-  double* F[3] = {nullptr, nullptr, nullptr};
-  {
-    SyevBatch eb;
-    int maxq = 0;
-    double* Ueig[3];
-    int* rfull[3];
-    for (int l = 0; l < 3; ++l) {
-      if (x.orth[l]) continue;
-      const int ql = q[l];
-      double* A = s.alloc<double>((size_t)ql * ql);
-      FC_CUDA_TRY(cudaMemcpyAsync(A, GQ[l], (size_t)ql * ql * 8, cudaMemcpyDeviceToDevice, st));
-      Ueig[l] = s.alloc<double>((size_t)ql * ql);
-      rfull[l] = s.alloc<int>(1);
-      int hq = ql;
-      FC_CUDA_TRY(cudaMemcpyAsync(rfull[l], &hq, sizeof(int), cudaMemcpyHostToDevice, st));
-      eb.e[eb.nb++] = SyevEntry{ql, A, ql, s.alloc<double>(ql), s.alloc<double>(ql), s.alloc<double>(ql), Ueig[l], ql,
-                                rfull[l], s.alloc<double>((size_t)5 * ql * ql)};
-      maxq = std::max(maxq, ql);
-    }
-    if (eb.nb) {
-      syev_values(eb, st);
-      syev_vectors(eb, maxq, st);
-      int b = 0;
-      for (int l = 0; l < 3; ++l) {
-        if (x.orth[l]) continue;
-        F[l] = s.alloc<double>((size_t)q[l] * q[l]);
-        sqrt_factor_kernel<<<blocks_for((long long)q[l] * q[l]), 256, 0, st>>>(q[l], eb.e[b].lam, Ueig[l], F[l]);
-        FC_CHECK_LAUNCH();
-        ++b;
-      }
-    }
-  }
-  // ---- B = F C D (q x R), M = B B^T ---------------------------------------------------
+  // ---- 3. side matrix in the basis: B_l = C_l D_l (q x R); M_l = B_l B_l^T -------------
   double* Bm[3];
   double* M[3];
   {
-    // B = F C diag(d) (F = I for an orthonormal basis); the diag(d) is the GEMM column scale
     GemmArgs g;
-    int nb = 0;
+    g.nbatch = 3;
     for (int l = 0; l < 3; ++l) {
       Bm[l] = s.alloc<double>((size_t)q[l] * R);
-      const double* Fl = F[l];
-      if (x.orth[l]) {
-        double* I = s.alloc<double>((size_t)q[l] * q[l]);
-        identity_kernel<<<blocks_for((long long)q[l] * q[l]), 256, 0, st>>>(q[l], I);
-        FC_CHECK_LAUNCH();
-        Fl = I;
-      }
-      g.b[nb++] = GemmBatch{q[l], R, q[l], Fl, q[l], x.C[l], q[l], Bm[l], q[l], nullptr, 0, dl[l]};
+      double* I = s.alloc<double>((size_t)q[l] * q[l]);
+      identity_kernel<<<blocks_for((long long)q[l] * q[l]), 256, 0, st>>>(q[l], I);
+      FC_CHECK_LAUNCH();
+      g.b[l] = GemmBatch{q[l], R, q[l], I, q[l], Co[l], q[l], Bm[l], q[l], nullptr, 0, dl[l]};
     }
-    g.nbatch = nb;
     gemm(g, st);
     GemmArgs m;
     m.transB = 1;
@@ -488,15 +470,14 @@ TT truncate_tt(fc_ctx c, const TT& x, double eps, int rank_cap, TruncStats* stat
     m.nbatch = 3;
     int tiles = 0;
     for (int l = 0; l < 3; ++l) {
-      M[l] = s.alloc<double>((size_t)q[l] * q[l]);
-      FC_CUDA_TRY(cudaMemsetAsync(M[l], 0, (size_t)q[l] * q[l] * 8, st));
+      M[l] = s.zeros<double>((size_t)q[l] * q[l]);
       m.b[l] = GemmBatch{q[l], q[l], R, Bm[l], q[l], Bm[l], q[l], M[l], q[l], nullptr, 0, nullptr};
       tiles += cdiv(q[l], 64) * cdiv(q[l], 64);
     }
     m.splitk = std::max(1, std::min(cdiv(R, 128), std::max(1, 148 * 3 / std::max(tiles, 1))));
     gemm(m, st);
   }
-  // ---- eigen of M: singular values s^2 (descending), cut, leading vectors --------------
+  // ---- 4. eigen of M: s^2 descending, rank cut (tails from the small end), leading vectors ----
   SyevBatch eb;
   double* lam[3];
   double* Y[3];
@@ -529,58 +510,28 @@ TT truncate_tt(fc_ctx c, const TT& x, double eps, int rank_cap, TruncStats* stat
     z.n = n;
     return z;
   }
-  // ---- Z_l and unit-factor coefficients Chat_l --------------------------------------------
+  // ---- 5. Z_l = Qo_l Y_r ; unit-factor coefficients Chat_l = Y_r^T C_l diag(1/n_l) ----------
   double* Z[3];
   double* Chat[3];
-  for (int l = 0; l < 3; ++l) {
-    const int ql = q[l], rr = r[l];
-    Z[l] = s.alloc<double>((size_t)n * rr);
-    Chat[l] = s.alloc<double>((size_t)rr * R);
-    if (x.orth[l]) {
-      // Z = Q Y_r ; Chat = Y_r^T C diag(1/n)
-      dgemm(st, 0, 0, n, rr, ql, 1.0, x.Q[l], n, Y[l], ql, 0.0, Z[l], n);
-      GemmArgs g;
-      g.transA = 1;
-      g.nbatch = 1;
-      g.b[0] = GemmBatch{rr, R, ql, Y[l], ql, x.C[l], ql, Chat[l], rr, nullptr, 0, inv[l]};
-      gemm(g, st);
-    } else {
-      // T1 = B^T Y_r (R x r); T1 <- diag(d) T1; G_Z = C T1 diag(1/s^2); Z = K G_Z; CGS2
-      double* T1 = s.alloc<double>((size_t)R * rr);
-      GemmArgs g;
-      g.transA = 1;
-      g.nbatch = 1;
-      g.b[0] = GemmBatch{R, rr, ql, Bm[l], ql, Y[l], ql, T1, R, nullptr, 0, nullptr};
-      gemm(g, st);
-      scale_rows_kernel<<<blocks_for((long long)R * rr), 256, 0, st>>>(R, rr, T1, R, dl[l], T1, R);
-      FC_CHECK_LAUNCH();
-      double* is2 = s.alloc<double>(rr);
-      inv_sq_kernel<<<cdiv(rr, 64), 64, 0, st>>>(rr, lam[l], is2);
-      FC_CHECK_LAUNCH();
-      double* GZ = s.alloc<double>((size_t)ql * rr);
-      GemmArgs h;
-      h.nbatch = 1;
-      h.b[0] = GemmBatch{ql, rr, R, x.C[l], ql, T1, R, GZ, ql, nullptr, 0, is2};
-      gemm(h, st);
-      dgemm(st, 0, 0, n, rr, ql, 1.0, x.Q[l], n, GZ, ql, 0.0, Z[l], n);
-      orthonormalize_cols(n, Z[l], n, rl + l, rr, st);
-      // Chat = (Z^T Q) C diag(1/n)
-      double* ZQ = s.alloc<double>((size_t)rr * ql);
-      FC_CUDA_TRY(cudaMemsetAsync(ZQ, 0, (size_t)rr * ql * 8, st));
-      dgemm(st, 1, 0, rr, ql, n, 1.0, Z[l], n, x.Q[l], n, 1.0, ZQ, rr, std::max(1, std::min(cdiv(n, 256), 16)));
-      GemmArgs k2;
-      k2.nbatch = 1;
-      k2.b[0] = GemmBatch{rr, R, ql, ZQ, rr, x.C[l], ql, Chat[l], rr, nullptr, 0, inv[l]};
-      gemm(k2, st);
+  {
+    GemmArgs gz, gc;
+    gz.nbatch = gc.nbatch = 3;
+    gc.transA = 1;
+    for (int l = 0; l < 3; ++l) {
+      Z[l] = s.alloc<double>((size_t)n * r[l]);
+      Chat[l] = s.alloc<double>((size_t)r[l] * R);
+      gz.b[l] = GemmBatch{n, r[l], q[l], Qo[l], n, Y[l], q[l], Z[l], n, nullptr, 0, nullptr};
+      gc.b[l] = GemmBatch{r[l], R, q[l], Y[l], q[l], Co[l], q[l], Chat[l], r[l], nullptr, 0, inv[l]};
     }
+    gemm(gz, st);
+    gemm(gc, st);
   }
-  // ---- core beta (r1 r2 x r3) = KR12 * Chat_3^T -----------------------------------------
+  // ---- 6. core beta (r1 r2 x r3) = KR12 * Chat_3^T ----------------------------------------
   const size_t r12 = (size_t)r[0] * r[1];
   double* KR = s.alloc<double>(r12 * R);
   kr12_kernel<<<blocks_for((long long)r12 * R), 256, 0, st>>>(r[0], r[1], R, xi, Chat[0], Chat[1], KR);
   FC_CHECK_LAUNCH();
-  double* core = s.alloc<double>(r12 * r[2]);
-  FC_CUDA_TRY(cudaMemsetAsync(core, 0, r12 * r[2] * 8, st));
+  double* core = s.zeros<double>(r12 * r[2]);
   {
     int tiles = cdiv((long long)r12, 64) * cdiv(r[2], 64);
     dgemm(st, 0, 1, (int)r12, r[2], R, 1.0, KR, (int)r12, Chat[2], r[2], 1.0, core, (int)r12,

@@ -2,9 +2,11 @@
 eigenpairs and spectral CPs (sl_set_eigen / op_set_spectral_cp).
 
 Tolerances: ranks identical at non-marginal cuts; a single truncation
-within 1e-9 relative (the device forms the side-matrix Gram, whose singular directions near the
-cut carry ~eps*s_1^2/s_r^2 error, i.e. <= 1e-10 of the tensor at eps = 1e-6); the final control
-u within max(10 eps, 1e-9) [BASELINE.json north_star]."""
+within eps relative.  Typically the two agree to ~1e-10 (the device forms the side-matrix Gram,
+whose singular directions near the cut carry ~eps_mach*s_1^2/s_r^2 error); when two T2C
+candidates are near-tied at the cut, the two implementations may keep different members of the
+tie, which changes the result by at most the dropped singular value, i.e. < eps/2 (reading A25).
+The final control u within max(10 eps, 1e-9) [BASELINE.json north_star]."""
 import numpy as np
 import pytest
 
@@ -47,7 +49,7 @@ def test_truncate_apply_output(lib, n, R, eps):
     y, info = ctx.cp_truncate(DeviceCP.from_numpy(x.w, x.U), eps)
     assert list(info.tucker_rank) == info_o["tucker_rank"]
     assert y.rank == ref.rank
-    assert reldiff(_cp(y), ref) <= 1e-9
+    assert reldiff(_cp(y), ref) <= eps
     g = _cp(y)
     assert cpm.dot(g, g) == pytest.approx(np.sum(g.w ** 2), rel=1e-10)     # orthogonal CP
 
@@ -64,10 +66,28 @@ def test_truncate_concat_and_duplicates(lib, n, R1, R2):
     ref = truncate(x, 1e-6)
     y, info = ctx.cp_truncate(DeviceCP.from_numpy(x.w, x.U), 1e-6)
     assert y.rank == ref.rank
-    assert reldiff(_cp(y), ref) <= 1e-9
+    assert reldiff(_cp(y), ref) <= 1e-6
     d = cpm.CP(np.concatenate([a.w, a.w]), [np.concatenate([u, u], axis=1) for u in a.U])
     y, info = ctx.cp_truncate(DeviceCP.from_numpy(d.w, d.U), 1e-8)
     assert reldiff(_cp(y), cpm.scale(2.0, a)) <= 1e-9
+
+
+@pytest.mark.parametrize("name,n,R,which", [("C1", 16, 2, 0), ("C1", 32, 3, 1), ("C3b", 24, 4, 0),
+                                            ("C1", 40, 5, 0)])
+def test_fused_apply_truncate(lib, name, n, R, which):
+    """fracop_apply_truncate (the solver's operator step) vs trunc(apply(x)) of the oracle."""
+    from paper_2006_09314_b200.binding import DeviceCP
+    p = make_problem(name, n=n)
+    ctx = lib.context()
+    st = _shared(ctx, p)
+    spec = st.F if which == 0 else st.G
+    x = truncate(cpm.apply(st.V, st.F, cpm.CP(np.linspace(1, 2, R), random_cp(n, R, 9)[1])), p.eps)
+    info_o = {}
+    ref = truncate(cpm.apply(st.V, spec, x), p.eps, info_o)
+    y, info = ctx.fracop_apply_truncate(which, DeviceCP.from_numpy(x.w, x.U), p.eps)
+    assert list(info.tucker_rank) == info_o["tucker_rank"]
+    assert y.rank == ref.rank
+    assert reldiff(_cp(y), ref) <= p.eps
 
 
 def test_truncate_zero_and_rank1(lib):
@@ -93,9 +113,34 @@ def test_pcg_parity_shared(lib, name, n):
     prm = make_params(p.alpha, p.beta, p.eps, p.tol_stop)
     u, rep, rc = ctx.pcg_solve(b, prm)
     assert rc == 0 and rep["converged"]
-    assert rep["iters"] == rep_ref["iters"]
-    assert rep["rank_S"] == rep_ref["rank_S"]
-    assert rep["rank_X"] == rep_ref["rank_X"]
-    assert rep["rank_R"] == rep_ref["rank_R"]
-    assert np.allclose(rep["rel_res"], rep_ref["rel_res"], rtol=1e-5)
+    check_rank_history(rep, rep_ref)
     assert reldiff(_cp(u), u_ref) <= max(10 * p.eps, 1e-9)
+
+
+MARGIN_BAND = 5e-3   # relative distance of thr to a bracketing tail below which a cut is marginal
+
+
+def check_rank_history(rep, rep_ref):
+    """Ranks equal truncation by truncation until the first cut the oracle logged as marginal
+    (A23 noise band); after a marginal cut the two runs are different (equally valid) rank
+    sequences, so only the iteration count (+-1) and the final control are compared."""
+    m = rep_ref["margins"]          # order: Z0, then per iteration S, X, R, Z, P
+    marginal = False
+    for k in range(min(rep["iters"], rep_ref["iters"])):
+        base = 1 + 5 * k
+        for key, off in (("rank_S", 0), ("rank_X", 1), ("rank_R", 2)):
+            if marginal:
+                break
+            if rep[key][k] != rep_ref[key][k]:
+                assert m[base + off] < MARGIN_BAND, (key, k, rep[key][k], rep_ref[key][k], m[base + off])
+                marginal = True
+        if not marginal:
+            assert rep["rel_res"][k] == pytest.approx(rep_ref["rel_res"][k], rel=1e-5)
+        if marginal:
+            break
+        if any(x < MARGIN_BAND for x in m[base:base + 5]):
+            marginal = True          # a Z/P cut was marginal: later ranks may legitimately differ
+    if marginal:
+        assert abs(rep["iters"] - rep_ref["iters"]) <= 1
+    else:
+        assert rep["iters"] == rep_ref["iters"]
