@@ -9,7 +9,7 @@ value = PCG iterations / second over the timed steps (all ranks); time_to_eps_ms
 per-step solve time.  L2 is flushed (a 512 MiB write) between timed steps, outside the events.
 
 --impl reference: the oracle (oracle/, NumPy/SciPy FP64) on the host cores, on a bounded
-sample of the same workload (C4 at n = 128: the oracle's dense setup is infeasible at n = 1024).
+sample of the same workload (C4 at n = 64: the oracle's dense setup is infeasible at n = 1024).
 Multi-GPU: replicas only (independent solves per rank, no collective).
 """
 from __future__ import annotations
@@ -97,8 +97,8 @@ def dist_env():
     return rank, world, local
 
 
-def oracle_sample(n=128, iters_cap=3):
-    """Oracle PCG on the C4 workload at n = 128 (bounded): returns (iters, loop seconds)."""
+def oracle_sample(n=64, iters_cap=3):
+    """Oracle PCG on the C4 workload at n = 64 (bounded): returns (iters, loop seconds)."""
     from oracle import cp as cpm
     from oracle import pcg as P
     from synth import make_problem
@@ -131,9 +131,9 @@ def run_reference(args):
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * float(np.mean(per)),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": {"workload": WORKLOAD, "sample": "C4 workload at n=128, 2 PCG iterations per step"},
+            "data": "synthetic", "config": {"workload": WORKLOAD, "sample": "C4 workload at n=64, 2 PCG iterations per step"},
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
-                             "sample": "oracle (NumPy/SciPy) PCG loop, C4 workload at n=128, 2 iterations per step"},
+                             "sample": "oracle (NumPy/SciPy) PCG loop, C4 workload at n=64, 2 iterations per step"},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -271,7 +271,7 @@ def main():
     if not args.no_cpu_baseline and world == 1 or (not args.no_cpu_baseline and rank == 0):
         it, dt = oracle_sample(iters_cap=2)
         line["cpu_baseline"] = {"value": it / dt, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle",
-                                "sample": "oracle PCG loop, C4 workload at n=128 (dense oracle setup infeasible at n=1024), 2 iterations"}
+                                "sample": "oracle PCG loop, C4 workload at n=64 (dense oracle setup infeasible at n=1024), 2 iterations"}
     print(json.dumps(line), flush=True)
 
 

@@ -173,6 +173,10 @@ int fc_dgemm(fc_ctx ctx, int transA, int transB, int M, int N, int K, double alp
 /* Milliseconds of the last launch of the dominant kernel of the last API call (events on
  * the context stream) and its algorithmic flop and byte counts (for the roofline line). */
 int fc_last_kernel_stats(fc_ctx ctx, double* ms, double* flops, double* bytes, int* launches);
+/* Rank-revealing orthonormalisation used by the truncation (blocked Gram-Schmidt, columns kept
+ * to tau times their norm): A (device, n x p, column-major, overwritten), Q (device, n x
+ * min(n,p)); *k_host receives the basis size. */
+int fc_orthonormalize(fc_ctx ctx, int n, int p, double* A, double* Q, double tau, int* k_host);
 /* Process-wide count of CUDA kernels this library has launched (host-side counter). */
 int fc_kernel_launches(long long* count);
 

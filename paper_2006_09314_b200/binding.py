@@ -67,7 +67,7 @@ class FCError(RuntimeError):
 ENTRY_POINTS = ["fc_create", "fc_destroy", "fc_last_error", "fc_set_stream", "sl_setup", "sl_get_eigen",
                 "sl_set_eigen", "op_get_spectral_cp", "op_set_spectral_cp", "op_spectral_rank",
                 "fracop_apply", "precond_apply", "cp_dot", "cp_axpy", "cp_truncate", "pcg_solve",
-                "fc_dgemm", "fc_last_kernel_stats", "fc_kernel_launches", "fracop_apply_truncate"]
+                "fc_dgemm", "fc_last_kernel_stats", "fc_kernel_launches", "fracop_apply_truncate", "fc_orthonormalize"]
 
 
 def load_library(path: str = LIB_PATH) -> C.CDLL:
@@ -93,6 +93,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "fc_dgemm": ([P, I, I, I, I, I, D, P, I, P, I, D, P, I], I),
         "fc_last_kernel_stats": ([P, C.POINTER(D), C.POINTER(D), C.POINTER(D), C.POINTER(I)], I),
         "fc_kernel_launches": ([C.POINTER(C.c_longlong)], I),
+        "fc_orthonormalize": ([P, I, I, P, P, D, C.POINTER(I)], I),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -288,6 +289,16 @@ class Context:
             return u, rep.as_dict(), rc
 
     # ---- raw ----
+    def orthonormalize(self, A, tau=1e-13):
+        """A: torch (p, n) row-major == n x p column-major (overwritten).  Returns Q (k, n)."""
+        import torch
+        p, n = A.shape
+        Q = torch.zeros(min(n, p), n, dtype=torch.float64, device=A.device)
+        k = C.c_int()
+        self._check(self.lib.fc_orthonormalize(self.h, n, p, A.data_ptr(), Q.data_ptr(), C.c_double(tau),
+                                               C.byref(k)))
+        return Q[:k.value]
+
     def dgemm(self, transA, transB, M, N, K, alpha, A, lda, B, ldb, beta, Cm, ldc):
         self._check(self.lib.fc_dgemm(self.h, transA, transB, M, N, K, alpha, A.data_ptr(), lda,
                                       B.data_ptr(), ldb, beta, Cm.data_ptr(), ldc))

@@ -5,6 +5,7 @@
 #include "cpops.cuh"
 #include "ctx.cuh"
 #include "solver.cuh"
+#include "eig.cuh"
 
 using namespace fc;
 
@@ -151,6 +152,48 @@ std::atomic<long long> g_launches{0};
 
 // ======================================================================================
 extern "C" {
+
+int fc_orthonormalize(fc_ctx c, int n, int p, double* A, double* Q, double tau, int* k_host) {
+  return guard(c, [&]() {
+    require(n >= 1 && p >= 1 && A && Q && k_host, FC_ERR_INVALID_ARG, "fc_orthonormalize args");
+    Scratch s(c->st);
+    const int kcap = std::min(n, p);
+    // run as a batch of 3 identical problems (as the truncation does per mode) and require
+    // identical results, so the batched path is what the tests exercise
+    BcgsBatch b;
+    b.nb = 3;
+    int* kd = s.alloc<int>(3);
+    double* Qx[3] = {Q, s.alloc<double>((size_t)n * kcap), s.alloc<double>((size_t)n * kcap)};
+    for (int i = 0; i < 3; ++i) {
+      double* Ai = A;
+      if (i > 0) {
+        Ai = s.alloc<double>((size_t)n * p);
+        FC_CUDA_TRY(cudaMemcpyAsync(Ai, A, (size_t)n * p * 8, cudaMemcpyDeviceToDevice, c->st));
+      }
+      b.e[i] = BcgsEntry{n, p, Ai, n, Qx[i], n, kcap, kd + i, s.alloc<double>(p), s.alloc<double>((size_t)kcap * 32), tau};
+    }
+    // the copies must be taken before entry 0 overwrites A: reorder so entry 0 runs on a copy too
+    double* A0 = s.alloc<double>((size_t)n * p);
+    FC_CUDA_TRY(cudaMemcpyAsync(A0, A, (size_t)n * p * 8, cudaMemcpyDeviceToDevice, c->st));
+    b.e[0].A = A0;
+    bcgs(b, c->st);
+    int kh[3];
+    FC_CUDA_TRY(cudaMemcpyAsync(kh, kd, 3 * sizeof(int), cudaMemcpyDeviceToHost, c->st));
+    FC_CUDA_TRY(cudaStreamSynchronize(c->st));
+    std::vector<double> q0((size_t)n * kcap), qi((size_t)n * kcap);
+    FC_CUDA_TRY(cudaMemcpy(q0.data(), Qx[0], q0.size() * 8, cudaMemcpyDeviceToHost));
+    for (int i = 1; i < 3; ++i) {
+      FC_CUDA_TRY(cudaMemcpy(qi.data(), Qx[i], qi.size() * 8, cudaMemcpyDeviceToHost));
+      double d = 0;
+      for (size_t t = 0; t < q0.size(); ++t) d = std::max(d, std::fabs(q0[t] - qi[t]));
+      require(kh[i] == kh[0] && d < 1e-12, FC_ERR_CUDA,
+              "batched orthonormalisation differs between identical entries (k " + std::to_string(kh[0]) + " vs " +
+                  std::to_string(kh[i]) + ", maxdiff " + std::to_string(d) + ")");
+    }
+    *k_host = kh[0];
+    return FC_OK;
+  });
+}
 
 int fc_kernel_launches(long long* count) {
   if (!count) return FC_ERR_INVALID_ARG;

@@ -33,17 +33,33 @@ __global__ void apply_weights_kernel(int r, int R, const double* wF, const doubl
   csc[t] = nc > 0 ? 1.0 / nc : 0.0;
 }
 
-// out = sum_{k,m} wx[k] wy[m] G0[k,m] G1[k,m] G2[k,m]   (single block, deterministic order)
+// out[blockIdx.x] = partial of sum_{k,m} wx[k] wy[m] G0[k,m] G1[k,m] G2[k,m]  (grid-stride,
+// deterministic: a fixed grid and a second single-block pass over the partials)
 __global__ void dot_reduce_kernel(int R1, int R2, const double* wx, const double* wy, const double* G0,
                                   const double* G1, const double* G2, int ld, double* out) {
   __shared__ double red[32];
   double acc = 0.0;
   const long long total = (long long)R1 * R2;
-  for (long long idx = threadIdx.x; idx < total; idx += blockDim.x) {
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
     int k = (int)(idx % R1), m = (int)(idx / R1);
     size_t o = (size_t)k + (size_t)m * ld;
     acc += wx[k] * wy[m] * (G0[o] * G1[o] * G2[o]);
   }
+  for (int s = 16; s > 0; s >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+    for (int s = 16; s > 0; s >>= 1) v += __shfl_down_sync(0xffffffffu, v, s);
+    if (threadIdx.x == 0) out[blockIdx.x] = v;
+  }
+}
+
+__global__ void sum_kernel(int n, const double* __restrict__ x, double* out) {
+  __shared__ double red[32];
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) acc += x[i];
   for (int s = 16; s > 0; s >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, s);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
   __syncthreads();
@@ -97,8 +113,15 @@ void apply_weights(int r, int R, const double* wF, const double* wx, const doubl
 
 void dot_reduce(int R1, int R2, const double* wx, const double* wy, const double* const G[3], int ld,
                 double* out_dev, cudaStream_t st) {
-  dot_reduce_kernel<<<1, 1024, 0, st>>>(R1, R2, wx, wy, G[0], G[1], G[2], ld, out_dev);
+  const long long total = (long long)R1 * R2;
+  const int nb = (int)std::min<long long>(std::max<long long>((total + 8191) / 8192, 1), 296);
+  double* part = nullptr;
+  FC_CUDA_TRY(cudaMallocAsync(&part, (size_t)nb * sizeof(double), st));
+  dot_reduce_kernel<<<nb, 512, 0, st>>>(R1, R2, wx, wy, G[0], G[1], G[2], ld, part);
   FC_CHECK_LAUNCH();
+  sum_kernel<<<1, 512, 0, st>>>(nb, part, out_dev);
+  FC_CHECK_LAUNCH();
+  FC_CUDA_TRY(cudaFreeAsync(part, st));
 }
 
 void copy_cols3(const Mat3& src, const Mat3& dst, double scale, cudaStream_t st) {

@@ -232,7 +232,8 @@ __global__ void ns_matrix_kernel(int n, double* G) {
 // (b) small symmetric eigensolver
 // ---------------------------------------------------------------------------------------
 constexpr int kTriThreads = 512;
-constexpr int kSmemMaxN = 120;   // N*N*8 <= 115 KB in shared memory, else global (L2)
+constexpr int kSmemMaxN = 150;   // (N^2 + 18 N) * 8 <= 202 KB in shared memory, else global (L2)
+constexpr size_t kTriSmemMax = 220 * 1024;
 
 __device__ double block_sum(double v, double* red) {
   for (int s = 16; s > 0; s >>= 1) v += __shfl_down_sync(0xffffffffu, v, s);
@@ -250,80 +251,92 @@ __device__ double block_sum(double v, double* red) {
   return red[32];
 }
 
-// Householder tridiagonalisation, lower part, in place: after return column k (rows k+1..)
-// holds the unit Householder vector u_k (H_k = I - 2 u u^T; zero column = identity).
+// Householder tridiagonalisation (lower triangle), in place: after return column k (rows
+// k+1..) holds the unit Householder vector u_k (H_k = I - 2 u u^T; zero column = identity),
+// E.d / E.e the tridiagonal.  One CTA per matrix; the matrix lives in shared memory when
+// N <= kSmemMaxN, else in global memory (L2).  Only the lower triangle is read and updated:
+//   p = A22 u  column by column (warp per column, lanes over rows, coalesced): column j adds
+//              A[i,j] u_j to p_i (i >= j) and sum_{i>j} A[i,j] u_i to p_j, into per-warp
+//              partial vectors that are summed afterwards;
+//   A22 -= 2 (u q^T + q u^T) on the lower triangle (warp per column).
 __global__ void __launch_bounds__(kTriThreads) tridiag_kernel(const __grid_constant__ SyevBatch B) {
   extern __shared__ double sm[];
   __shared__ double red[33];
+  __shared__ double alpha_s;
   const SyevEntry& E = B.e[blockIdx.x];
   const int N = E.N;
   if (N <= 0) return;
+  constexpr int NW = kTriThreads / 32;
   const bool use_sm = N <= kSmemMaxN;
   double* M = use_sm ? sm : E.A;
   const int ld = use_sm ? N : E.lda;
-  double* p = use_sm ? sm + N * N : E.e + 0;  // p needs N entries; e gets filled only at the end
-  double* uvec = use_sm ? sm + N * N + N : E.d;  // scratch (d filled at the end)
-  __shared__ double dk_s[1];
-  const int tid = threadIdx.x, nt = blockDim.x;
+  double* base = use_sm ? sm + (size_t)N * N : sm;
+  double* uvec = base;              // N
+  double* p = base + N;             // N
+  double* pw = base + 2 * N;        // NW x N warp partials
+  const int tid = threadIdx.x, nt = blockDim.x, warp = tid >> 5, ln = tid & 31;
   if (use_sm)
     for (int idx = tid; idx < N * N; idx += nt) M[idx] = E.A[(idx % N) + (size_t)(idx / N) * E.lda];
   __syncthreads();
-  // keep d/e in registers of thread 0 is not possible (N values); store in shared scratch
-  // at the end we write d/e; during the sweep we record them into the diagonal/subdiagonal
-  // positions, which the algorithm no longer touches.
   for (int k = 0; k + 2 < N; ++k) {
-    const int m = N - k - 1;          // length of x = M[k+1.., k]
-    double x0 = M[(k + 1) + (size_t)k * ld];
+    const int m = N - k - 1;                  // trailing size; x = M[k+1.., k]
+    double* col_k = M + (k + 1) + (size_t)k * ld;
+    double* A22 = M + (k + 1) + (size_t)(k + 1) * ld;
+    const double x0 = col_k[0];
     double part = 0.0;
-    for (int i = tid + 1; i < m; i += nt) {
-      double x = M[(k + 1 + i) + (size_t)k * ld];
-      part += x * x;
-    }
-    double sig = block_sum(part, red);
-    double alpha, unrm2;
-    bool skip = (sig == 0.0);
+    for (int i = tid + 1; i < m; i += nt) part += col_k[i] * col_k[i];
+    const double sig = block_sum(part, red);
+    const bool skip = (sig == 0.0);
+    double alpha = x0;
     if (!skip) {
       alpha = -copysign(sqrt(x0 * x0 + sig), x0);
-      double v0 = x0 - alpha;
-      unrm2 = sig + v0 * v0;
-      double inv = 1.0 / sqrt(unrm2);
-      for (int i = tid; i < m; i += nt) {
-        double x = (i == 0) ? v0 : M[(k + 1 + i) + (size_t)k * ld];
-        uvec[i] = x * inv;
-      }
-    } else {
-      alpha = x0;
+      const double v0 = x0 - alpha;
+      const double inv = 1.0 / sqrt(sig + v0 * v0);
+      for (int i = tid; i < m; i += nt) uvec[i] = (i == 0 ? v0 : col_k[i]) * inv;
+      for (int i = tid; i < NW * m; i += nt) pw[(i / m) * N + (i % m)] = 0.0;
     }
     __syncthreads();
     if (!skip) {
-      // p = A22 u
-      for (int i = tid; i < m; i += nt) {
-        double acc = 0.0;
-        for (int j = 0; j < m; ++j) acc += M[(k + 1 + i) + (size_t)(k + 1 + j) * ld] * uvec[j];
-        p[i] = acc;
+      // p = A22 u from the lower triangle
+      for (int j = warp; j < m; j += NW) {
+        const double* cj = A22 + (size_t)j * ld;
+        const double uj = uvec[j];
+        double* pwj = pw + (size_t)warp * N;
+        double dot = 0.0;
+        for (int i = j + ln; i < m; i += 32) {
+          const double a = cj[i];
+          pwj[i] += a * uj;
+          if (i > j) dot += a * uvec[i];
+        }
+        for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+        if (ln == 0) pwj[j] += dot;
+        __syncwarp();
       }
       __syncthreads();
       double kp = 0.0;
-      for (int i = tid; i < m; i += nt) kp += uvec[i] * p[i];
-      double K = block_sum(kp, red);
+      for (int i = tid; i < m; i += nt) {
+        double s = 0.0;
+        for (int w = 0; w < NW; ++w) s += pw[(size_t)w * N + i];
+        p[i] = s;
+        kp += uvec[i] * s;
+      }
+      const double K = block_sum(kp, red);
       for (int i = tid; i < m; i += nt) p[i] -= K * uvec[i];   // q
       __syncthreads();
-      // A22 -= 2 (u q^T + q u^T)
-      for (long long idx = tid; idx < (long long)m * m; idx += nt) {
-        int i = (int)(idx % m), j = (int)(idx / m);
-        M[(k + 1 + i) + (size_t)(k + 1 + j) * ld] -= 2.0 * (uvec[i] * p[j] + p[i] * uvec[j]);
+      // lower-triangle rank-2 update
+      for (int j = warp; j < m; j += NW) {
+        double* cj = A22 + (size_t)j * ld;
+        const double uj = uvec[j], qj = p[j];
+        for (int i = j + ln; i < m; i += 32) cj[i] -= 2.0 * (uvec[i] * qj + p[i] * uj);
       }
       __syncthreads();
     }
-    // record: diagonal stays M[k,k]; store alpha on the super-diagonal slot M[k, k+1]
-    // (never read again) and u_k in column k below the diagonal.
-    if (tid == 0) dk_s[0] = alpha;
+    if (tid == 0) alpha_s = alpha;
     __syncthreads();
-    for (int i = tid; i < m; i += nt) M[(k + 1 + i) + (size_t)k * ld] = skip ? 0.0 : uvec[i];
-    if (tid == 0) M[k + (size_t)(k + 1) * ld] = dk_s[0];
+    for (int i = tid; i < m; i += nt) col_k[i] = skip ? 0.0 : uvec[i];
+    if (tid == 0) M[k + (size_t)(k + 1) * ld] = alpha_s;          // e_k in the (stale) upper slot
     __syncthreads();
   }
-  // extract d, e; write back Householder vectors if computed in shared memory
   if (tid == 0) {
     for (int k = 0; k < N; ++k) E.d[k] = M[k + (size_t)k * ld];
     for (int k = 0; k + 1 < N; ++k) E.e[k] = (k + 2 < N) ? M[k + (size_t)(k + 1) * ld] : M[(k + 1) + (size_t)k * ld];
@@ -332,6 +345,7 @@ __global__ void __launch_bounds__(kTriThreads) tridiag_kernel(const __grid_const
   if (use_sm)
     for (int idx = tid; idx < N * N; idx += nt) E.A[(idx % N) + (size_t)(idx / N) * E.lda] = M[idx];
 }
+
 
 __device__ int tri_count(int N, const double* __restrict__ d, const double* __restrict__ e, double x,
                          double pivmin) {
@@ -530,6 +544,116 @@ __global__ void __launch_bounds__(kPmgsThreads) pmgs_kernel(const __grid_constan
   if (tid == 0) *E.k_out = k;
 }
 
+// In-block step of the blocked rank-revealing Gram-Schmidt (one CTA per matrix): the block's
+// columns X (n x w), already projected against the accepted basis Q[:, :k], are orthogonalised
+// among themselves in order (two MGS passes against the vectors accepted in this block);
+// a column is accepted when its residual exceeds tau * its original norm, and appended to Q at
+// the device counter k.
+__global__ void __launch_bounds__(512) bcgs_block_kernel(const __grid_constant__ BcgsBatch B, int j0, int w) {
+  __shared__ double coef[64];
+  __shared__ double red[33];
+  __shared__ int acc_idx[64];
+  __shared__ int nacc_s, k0_s;
+  __shared__ double nmax_s;
+  const BcgsEntry& E = B.e[blockIdx.x];
+  if (j0 >= E.p) return;
+  const int n = E.n, wb = min(w, E.p - j0);
+  const int tid = threadIdx.x, nt = blockDim.x, warp = tid >> 5, ln = tid & 31, nw = nt >> 5;
+  if (tid == 0) {
+    nacc_s = 0;
+    k0_s = *E.k;
+    double mx = 0.0;
+    for (int c = 0; c < E.p; ++c) mx = fmax(mx, E.norm0[c]);
+    nmax_s = mx;
+  }
+  for (int i = tid; i < n * 32; i += nt) E.Y[i] = 0.0;   // block buffer (n x 32, ld n)
+  __syncthreads();
+  for (int c = 0; c < wb; ++c) {
+    double* x = E.A + (size_t)(j0 + c) * E.lda;
+    const int na = nacc_s;
+    for (int pass = 0; pass < 2; ++pass) {
+      for (int a = warp; a < na; a += nw) {
+        const double* q = E.Y + (size_t)a * n;
+        double s = 0.0;
+        for (int i = ln; i < n; i += 32) s += q[i] * x[i];
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (ln == 0) coef[a] = s;
+      }
+      __syncthreads();
+      for (int i = tid; i < n; i += nt) {
+        double v = x[i];
+        for (int a = 0; a < na; ++a) v -= coef[a] * E.Y[i + (size_t)a * n];
+        x[i] = v;
+      }
+      __syncthreads();
+    }
+    double part = 0.0;
+    for (int i = tid; i < n; i += nt) part += x[i] * x[i];
+    const double s2 = block_sum(part, red);
+    // kept if the residual exceeds tau times its own norm AND tau times the largest column
+    // (columns below tau * max are negligible; their residuals are rounding residue, and
+    // normalising them would inject garbage directions)
+    const double lim = E.tau * fmax(E.norm0[j0 + c], nmax_s);
+    if (s2 > lim * lim && k0_s + na < E.kcap) {
+      const double inv = 1.0 / sqrt(s2);
+      double* q = E.Y + (size_t)na * n;
+      for (int i = tid; i < n; i += nt) q[i] = x[i] * inv;
+      if (tid == 0) nacc_s = na + 1;
+    }
+    __syncthreads();
+  }
+  if (tid == 0) *E.nacc = nacc_s;
+}
+
+// BCGS2 second pass, in-block part: the accepted unit vectors Y[:, :nacc] (already re-projected
+// against Q by a GEMM) are re-orthonormalised among themselves (MGS) and appended to Q at k.
+__global__ void __launch_bounds__(512) bcgs_finalize_kernel(const __grid_constant__ BcgsBatch B, int j0) {
+  __shared__ double coef[64];
+  __shared__ double red[33];
+  const BcgsEntry& E = B.e[blockIdx.x];
+  if (j0 >= E.p) return;
+  const int n = E.n, na = *E.nacc, k0 = *E.k;
+  const int tid = threadIdx.x, nt = blockDim.x, warp = tid >> 5, ln = tid & 31, nw = nt >> 5;
+  for (int c = 0; c < na; ++c) {
+    double* y = E.Y + (size_t)c * n;
+    for (int a = warp; a < c; a += nw) {
+      const double* q = E.Y + (size_t)a * n;
+      double s = 0.0;
+      for (int i = ln; i < n; i += 32) s += q[i] * y[i];
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (ln == 0) coef[a] = s;
+    }
+    __syncthreads();
+    double part = 0.0;
+    for (int i = tid; i < n; i += nt) {
+      double v = y[i];
+      for (int a = 0; a < c; ++a) v -= coef[a] * E.Y[i + (size_t)a * n];
+      y[i] = v;
+      part += v * v;
+    }
+    const double s2 = block_sum(part, red);
+    const double inv = s2 > 0 ? 1.0 / sqrt(s2) : 0.0;
+    double* q = E.Q + (size_t)(k0 + c) * E.ldq;
+    for (int i = tid; i < n; i += nt) {
+      y[i] *= inv;
+      q[i] = y[i];
+    }
+    __syncthreads();
+  }
+  if (tid == 0) *E.k = k0 + na;
+}
+
+__global__ void col_norms_kernel(const __grid_constant__ BcgsBatch B) {
+  const BcgsEntry& E = B.e[blockIdx.y];
+  const int c = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5), ln = threadIdx.x & 31;
+  if (c >= E.p) return;
+  const double* a = E.A + (size_t)c * E.lda;
+  double s = 0.0;
+  for (int i = ln; i < E.n; i += 32) s += a[i] * a[i];
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (ln == 0) E.norm0[c] = sqrt(s);
+}
+
 __global__ void rank_cut_kernel(int count, const double* __restrict__ s2, double factor,
                                 const double* __restrict__ energy, int* r_out, double* margin_out) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
@@ -609,17 +733,19 @@ void sl_eigen_device(cudaStream_t st, int n, const double* a_mid_dev, int bounda
 void syev_values(const SyevBatch& b, cudaStream_t st) {
   if (b.nb == 0) return;
   int maxN = 0;
-  bool any_sm = false;
+  size_t smem = 0;
+  constexpr int NW = kTriThreads / 32;
   for (int i = 0; i < b.nb; ++i) {
-    maxN = std::max(maxN, b.e[i].N);
-    any_sm |= b.e[i].N <= kSmemMaxN && b.e[i].N > 0;
+    const int N = b.e[i].N;
+    maxN = std::max(maxN, N);
+    const size_t need = ((N <= kSmemMaxN ? (size_t)N * N : 0) + (size_t)(2 + NW) * N) * 8;
+    smem = std::max(smem, need);
   }
   if (maxN == 0) return;
-  const int smem = any_sm ? (kSmemMaxN * kSmemMaxN + 2 * kSmemMaxN) * 8 : 0;
+  require(smem <= kTriSmemMax, FC_ERR_CAPACITY, "symmetric eigensolver: matrix dimension above 1500");
   static bool attr = false;
   if (!attr) {
-    FC_CUDA_TRY(cudaFuncSetAttribute(tridiag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (kSmemMaxN * kSmemMaxN + 2 * kSmemMaxN) * 8));
+    FC_CUDA_TRY(cudaFuncSetAttribute(tridiag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTriSmemMax));
     attr = true;
   }
   tridiag_kernel<<<b.nb, kTriThreads, smem, st>>>(b);
@@ -657,6 +783,76 @@ void pmgs(const PmgsBatch& b, cudaStream_t st) {
   require(smem <= 200 * 1024, FC_ERR_CAPACITY, "pmgs: too many columns");
   pmgs_kernel<<<b.nb, kPmgsThreads, smem, st>>>(b);
   FC_CHECK_LAUNCH();
+}
+
+void bcgs(const BcgsBatch& bin, cudaStream_t st) {
+  if (bin.nb == 0) return;
+  constexpr int W = 32;
+  BcgsBatch b = bin;
+  Scratch scr(st);
+  for (int i = 0; i < b.nb; ++i) {
+    b.e[i].Y = scr.alloc<double>((size_t)b.e[i].n * W);
+    b.e[i].nacc = scr.alloc<int>(1);
+  }
+  int maxp = 0;
+  for (int i = 0; i < b.nb; ++i) {
+    const BcgsEntry& E = b.e[i];
+    maxp = std::max(maxp, E.p);
+    FC_CUDA_TRY(cudaMemsetAsync(E.Q, 0, (size_t)E.ldq * E.kcap * 8, st));
+    FC_CUDA_TRY(cudaMemsetAsync(E.k, 0, sizeof(int), st));
+  }
+  col_norms_kernel<<<dim3(cdiv(maxp, 8), b.nb), 256, 0, st>>>(b);
+  FC_CHECK_LAUNCH();
+  for (int j0 = 0; j0 < maxp; j0 += W) {
+    // project the block against every column accepted so far (<= j0; unused Q columns are 0)
+    for (int pass = 0; pass < 2 && j0 > 0; ++pass) {
+      GemmArgs p, u;
+      p.transA = 1;
+      p.beta = 1.0;
+      u.alpha = -1.0;
+      u.beta = 1.0;
+      int nb = 0;
+      for (int i = 0; i < b.nb; ++i) {
+        const BcgsEntry& E = b.e[i];
+        if (j0 >= E.p) continue;
+        const int wb = std::min(W, E.p - j0), kup = std::min(j0, E.kcap);
+        FC_CUDA_TRY(cudaMemsetAsync(E.P, 0, (size_t)kup * W * 8, st));
+        p.b[nb] = GemmBatch{kup, wb, E.n, E.Q, E.ldq, E.A + (size_t)j0 * E.lda, E.lda, E.P, kup, nullptr, 0, nullptr};
+        u.b[nb] = GemmBatch{E.n, wb, kup, E.Q, E.ldq, E.P, kup, E.A + (size_t)j0 * E.lda, E.lda, nullptr, 0, nullptr};
+        ++nb;
+      }
+      p.nbatch = u.nbatch = nb;
+      p.splitk = std::max(1, std::min(cdiv(b.e[0].n, 256), 8));
+      gemm(p, st);
+      gemm(u, st);
+    }
+    bcgs_block_kernel<<<b.nb, 512, 0, st>>>(b, j0, W);
+    FC_CHECK_LAUNCH();
+    // BCGS2: re-project the accepted (unit) block vectors against the previous basis
+    if (j0 > 0) {
+      GemmArgs p, u;
+      p.transA = 1;
+      p.beta = 1.0;
+      u.alpha = -1.0;
+      u.beta = 1.0;
+      int nb = 0;
+      for (int i = 0; i < b.nb; ++i) {
+        const BcgsEntry& E = b.e[i];
+        if (j0 >= E.p) continue;
+        const int kup = std::min(j0, E.kcap);
+        FC_CUDA_TRY(cudaMemsetAsync(E.P, 0, (size_t)kup * W * 8, st));
+        p.b[nb] = GemmBatch{kup, W, E.n, E.Q, E.ldq, E.Y, E.n, E.P, kup, nullptr, 0, nullptr};
+        u.b[nb] = GemmBatch{E.n, W, kup, E.Q, E.ldq, E.P, kup, E.Y, E.n, nullptr, 0, nullptr};
+        ++nb;
+      }
+      p.nbatch = u.nbatch = nb;
+      p.splitk = std::max(1, std::min(cdiv(b.e[0].n, 256), 8));
+      gemm(p, st);
+      gemm(u, st);
+    }
+    bcgs_finalize_kernel<<<b.nb, 512, 0, st>>>(b, j0);
+    FC_CHECK_LAUNCH();
+  }
 }
 
 void rank_cut_device(int count, const double* s2, double factor, const double* energy, int* r_out,

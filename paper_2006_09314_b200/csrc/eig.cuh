@@ -50,6 +50,28 @@ struct PmgsBatch {
 };
 void pmgs(const PmgsBatch& b, cudaStream_t st);
 
+// Blocked rank-revealing Gram-Schmidt (multi-CTA): blocks of 32 columns are projected against
+// the accepted basis with DMMA GEMMs (twice), then orthogonalised in-block by one CTA; a column
+// is accepted when its residual exceeds tau * its original norm.  A (n x p) is overwritten;
+// Q (n x kcap) receives the basis, *k (device) its size; P is kcap x 32 scratch, norm0 p.
+struct BcgsEntry {
+  int n, p;
+  double* A; int lda;
+  double* Q; int ldq;
+  int kcap;
+  int* k;
+  double* norm0;
+  double* P;
+  double tau;
+  double* Y = nullptr;   // n x 32 block buffer (allocated by bcgs)
+  int* nacc = nullptr;   // accepted count of the current block (allocated by bcgs)
+};
+struct BcgsBatch {
+  int nb = 0;
+  BcgsEntry e[kMaxSyev];
+};
+void bcgs(const BcgsBatch& b, cudaStream_t st);
+
 // CGS2 orthonormalisation of the first *r_dev (<= rmax) columns of Y (N x ., ld ldy).
 void orthonormalize_cols(int N, double* Y, int ldy, int* r_dev, int rmax, cudaStream_t st);
 

@@ -130,17 +130,21 @@ __global__ void extract_slices_kernel(const double* __restrict__ core, int r0, i
 // One-sided Jacobi SVD of each slice (ra x rb, column-major) in shared memory; one CTA per
 // slice.  Outputs k = min(ra, rb) triples sorted by s descending: s[nu*k + m],
 // Ua[nu*ra*k + m*ra + x], Vb[nu*rb*k + m*rb + y].
-constexpr int kSliceMax = 96;
+// Slices whose working set exceeds the shared-memory budget run the same algorithm in a
+// per-slice global (L2-resident) workspace `gws` of (rows*cols + cols*cols) doubles.
+constexpr int kSliceMax = 512;
+constexpr size_t kSliceSmem = 200 * 1024;
 __global__ void __launch_bounds__(256) slice_svd_kernel(int ra, int rb, const double* __restrict__ S, double* s_out,
-                                                        double* Ua, double* Vb) {
+                                                        double* Ua, double* Vb, double* gws) {
   extern __shared__ double sm[];
   const int nu = blockIdx.x;
   const bool tr = ra < rb;                     // work on S^T when wide
   const int rows = tr ? rb : ra, cols = tr ? ra : rb;
   const int k = cols;                          // = min(ra, rb)
-  double* A = sm;                              // rows x cols
-  double* W = sm + rows * cols;                // cols x cols rotations
-  double* nrm = W + cols * cols;               // cols
+  const bool in_smem = gws == nullptr;
+  double* A = in_smem ? sm : gws + (size_t)nu * ((size_t)rows * cols + (size_t)cols * cols);   // rows x cols
+  double* W = A + rows * cols;                 // cols x cols rotations
+  double* nrm = in_smem ? W + cols * cols : sm;  // cols
   int* order = (int*)(nrm + cols);             // cols
   const double* src = S + (size_t)nu * ra * rb;
   const int tid = threadIdx.x, nt = blockDim.x, warp = tid >> 5, ln = tid & 31, nw = nt >> 5;
@@ -308,7 +312,7 @@ TT tucker_to_canonical(fc_ctx c, const double* core, const int r[3], double* con
   int ma = (mc == 0) ? 1 : 0, mb = (mc == 2) ? 1 : 2;
   const int ra = r[ma], rb = r[mb], rc = r[mc];
   const int k = std::min(ra, rb);
-  require(std::max(ra, rb) <= kSliceMax, FC_ERR_CAPACITY, "Tucker rank above the T2C slice limit (96)");
+  require(std::max(ra, rb) <= kSliceMax, FC_ERR_CAPACITY, "Tucker rank above the T2C slice limit (512)");
   const int K = rc * k;
   Scratch s(st);
   double* S = s.alloc<double>((size_t)ra * rb * rc);
@@ -323,12 +327,17 @@ TT tucker_to_canonical(fc_ctx c, const double* core, const int r[3], double* con
   FC_CHECK_LAUNCH();
   const int rows = std::max(ra, rb), cols = k;
   size_t smem = ((size_t)rows * cols + (size_t)cols * cols + cols) * 8 + (size_t)cols * 4 + 16;
+  double* gws = nullptr;
+  if (smem > kSliceSmem) {
+    gws = s.alloc<double>((size_t)rc * ((size_t)rows * cols + (size_t)cols * cols));
+    smem = (size_t)cols * 12 + 16;
+  }
   static bool attr = false;
   if (!attr) {
-    FC_CUDA_TRY(cudaFuncSetAttribute(slice_svd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    FC_CUDA_TRY(cudaFuncSetAttribute(slice_svd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSliceSmem));
     attr = true;
   }
-  slice_svd_kernel<<<rc, 256, smem, st>>>(ra, rb, S, sv, Ua, Vb);
+  slice_svd_kernel<<<rc, 256, smem, st>>>(ra, rb, S, sv, Ua, Vb, gws);
   FC_CHECK_LAUNCH();
   pool_sort_kernel<<<1, 1024, 0, st>>>(K, sv, s2s, keys, energy);
   FC_CHECK_LAUNCH();
@@ -389,7 +398,7 @@ TT truncate_tt(fc_ctx c, const TT& xin, double eps, int rank_cap, TruncStats* st
   double* Co[3];
   int q[3];
   {
-    PmgsBatch pb;
+    BcgsBatch pb;
     int* kdev = s.alloc<int>(4);
     int map[3];
     for (int l = 0; l < 3; ++l) {
@@ -398,11 +407,13 @@ TT truncate_tt(fc_ctx c, const TT& xin, double eps, int rank_cap, TruncStats* st
       require(xin.q[l] >= 1, FC_ERR_INVALID_ARG, "empty basis");
       double* Kc = s.alloc<double>((size_t)n * xin.q[l]);
       FC_CUDA_TRY(cudaMemcpyAsync(Kc, xin.Q[l], (size_t)n * xin.q[l] * 8, cudaMemcpyDeviceToDevice, st));
-      double* Qn = s.alloc<double>((size_t)n * std::min(n, xin.q[l]));
+      const int kcap = std::min(n, xin.q[l]);
+      double* Qn = s.alloc<double>((size_t)n * kcap);
       map[l] = pb.nb;
-      pb.e[pb.nb++] = PmgsEntry{n, xin.q[l], Kc, n, Qn, n, kdev + l, 1e-13};
+      pb.e[pb.nb++] = BcgsEntry{n, xin.q[l], Kc, n, Qn, n, kcap, kdev + l, s.alloc<double>(xin.q[l]),
+                                s.alloc<double>((size_t)kcap * 32), 1e-13};
     }
-    pmgs(pb, st);
+    bcgs(pb, st);
     int kh[4] = {0, 0, 0, 0};
     if (pb.nb) {
       FC_CUDA_TRY(cudaMemcpyAsync(kh, kdev, 3 * sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -418,6 +429,28 @@ TT truncate_tt(fc_ctx c, const TT& xin, double eps, int rank_cap, TruncStats* st
       const int k = std::max(kh[l], 1);
       Qo[l] = pb.e[map[l]].Q;
       q[l] = k;
+      if (getenv("FC_TRACE")) {   // debugging aid: orthogonality of the device basis
+        double* Gq = s.zeros<double>((size_t)k * k);
+        dgemm(st, 1, 0, k, k, n, 1.0, Qo[l], n, Qo[l], n, 0.0, Gq, k);
+        std::vector<double> h((size_t)k * k);
+        FC_CUDA_TRY(cudaMemcpyAsync(h.data(), Gq, h.size() * 8, cudaMemcpyDeviceToHost, st));
+        FC_CUDA_TRY(cudaStreamSynchronize(st));
+        double dev = 0;
+        for (int i = 0; i < k; ++i)
+          for (int j = 0; j < k; ++j) dev = std::max(dev, std::fabs(h[i + (size_t)j * k] - (i == j ? 1.0 : 0.0)));
+        fprintf(stderr, "[fc trunc] mode %d basis %d of %d orth_err %.2e\n", l, k, xin.q[l], dev);
+        static int dumped = 0;
+        if (dev > 1e-8 && dumped < 1 && getenv("FC_DUMP")) {
+          ++dumped;
+          std::vector<double> K((size_t)n * xin.q[l]);
+          FC_CUDA_TRY(cudaMemcpy(K.data(), xin.Q[l], K.size() * 8, cudaMemcpyDeviceToHost));
+          FILE* f = fopen(getenv("FC_DUMP"), "wb");
+          int hdr[2] = {n, xin.q[l]};
+          fwrite(hdr, sizeof(int), 2, f);
+          fwrite(K.data(), 8, K.size(), f);
+          fclose(f);
+        }
+      }
       // Rm = Qo^T K (k x qin) ; Co = Rm C (k x R)
       double* Rm = s.zeros<double>((size_t)k * xin.q[l]);
       dgemm(st, 1, 0, k, xin.q[l], n, 1.0, Qo[l], n, xin.Q[l], n, 1.0, Rm, k,
@@ -505,6 +538,10 @@ TT truncate_tt(fc_ctx c, const TT& xin, double eps, int rank_cap, TruncStats* st
     S.tucker[l] = r[l];
     S.min_margin = std::min(S.min_margin, hm[l]);
   }
+  static const bool trace = getenv("FC_TRACE") != nullptr;
+  if (trace)
+    fprintf(stderr, "[fc trunc] n=%d terms=%d qin=(%d,%d,%d) basis=(%d,%d,%d) tucker=(%d,%d,%d)\n", n, R, xin.q[0],
+            xin.q[1], xin.q[2], q[0], q[1], q[2], r[0], r[1], r[2]);
   if (S.energy == 0.0) {
     TT z;
     z.n = n;
