@@ -114,13 +114,21 @@ TT apply_truncate_tt(fc_ctx c, SpecCP& sp, const TT& x, double eps, int rank_cap
     return z;
   }
   ensure_spec_basis(c, sp);
-  TT y;   // eigen-coordinate Hadamard tensor (view over scratch-owned memory)
+  // x's Tucker core (T2C outputs carry it; otherwise form it once from the CP coefficients)
+  TT xc;
+  const double* core_x = x.core;
+  if (!core_x) {
+    xc = tt_copy(st, x);
+    tt_compute_core(st, xc);
+    core_x = xc.core;
+  }
+  TT y;   // eigen-coordinate Hadamard tensor: basis K_l, weights kron(w_F, w_x); no coefficients
   y.n = n;
   y.R = r * R;
   size_t need = (size_t)y.R;
   for (int l = 0; l < 3; ++l) {
     y.q[l] = sp.s[l] * x.q[l];
-    need += (size_t)n * x.q[l] + (size_t)n * y.q[l] + (size_t)y.q[l] * y.R;
+    need += (size_t)n * x.q[l] + (size_t)n * y.q[l];
   }
   y.mem.emplace_back(need * 8, st);
   double* p = y.mem.back().d();
@@ -138,20 +146,25 @@ TT apply_truncate_tt(fc_ctx c, SpecCP& sp, const TT& x, double eps, int rank_cap
     fwd.b[l] = GemmBatch{n, x.q[l], n, c->V_l(l), n, x.Q[l], n, Zh[l], n, nullptr, 0, nullptr};
   }
   gemm(fwd, st);
-  for (int l = 0; l < 3; ++l) {   // S6: Khatri-Rao basis and Kronecker coefficients
+  StructuredS ss;
+  ss.r = r;
+  ss.Rx = R;
+  ss.wF = sp.w.p;
+  ss.core_x = core_x;
+  for (int l = 0; l < 3; ++l) {   // S6: the Khatri-Rao basis [w_a (.) xhat_b]
     const double* Wl = sp.W.p + (size_t)l * n * sp.smax;
-    const double* El = sp.E.p + (size_t)l * sp.smax * r;
+    ss.s[l] = sp.s[l];
+    ss.t[l] = x.q[l];
+    ss.E[l] = sp.E.p + (size_t)l * sp.smax * r;
+    ss.Cx[l] = x.C[l];
     y.Q[l] = p;
     p += (size_t)n * y.q[l];
-    y.C[l] = p;
-    p += (size_t)y.q[l] * y.R;
+    y.C[l] = nullptr;
     hadamard_basis_kernel<<<nblocks((long long)n * y.q[l]), 256, 0, st>>>(n, sp.s[l], Wl, x.q[l], Zh[l], y.Q[l]);
-    FC_CHECK_LAUNCH();
-    kron_kernel<<<nblocks((long long)y.q[l] * y.R), 256, 0, st>>>(sp.s[l], r, El, x.q[l], R, x.C[l], y.C[l]);
     FC_CHECK_LAUNCH();
     y.orth[l] = false;
   }
-  TT out = truncate_tt(c, y, eps, rank_cap, stats);
+  TT out = truncate_tt(c, y, eps, rank_cap, stats, &ss);
   // S7: back to physical coordinates, only the surviving basis columns
   GemmArgs inv;
   inv.nbatch = 0;

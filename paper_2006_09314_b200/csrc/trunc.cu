@@ -288,6 +288,58 @@ __global__ void blockdiag_kernel(int q1, int R1, const double* __restrict__ C1, 
   }
 }
 
+// number of kept T2C triples per slice (the kept set of each slice is a prefix of its
+// descending singular values)
+__global__ void slice_counts_kernel(int R, int k, const int* __restrict__ keys, int* counts) {
+  int m = blockIdx.x * blockDim.x + threadIdx.x;
+  if (m < R) atomicAdd(counts + keys[m] / k, 1);
+}
+
+// T2C output core in mode order: core[id] = sum_{m < cnt[nu]} s[nu,m] Ua[nu][x,m] Vb[nu][y,m]
+// with id[ma] = x, id[mb] = y, id[mc] = nu
+__global__ void t2c_core_kernel(int ra, int rb, int rc, int k, const int* __restrict__ cnt,
+                                const double* __restrict__ s, const double* __restrict__ Ua,
+                                const double* __restrict__ Vb, int ma, int mb, int mc, int r0, int r1, double* core) {
+  const long long tot = (long long)ra * rb * rc;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < tot;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int x = (int)(idx % ra), y = (int)((idx / ra) % rb), nu = (int)(idx / ((long long)ra * rb));
+    const int km = cnt[nu];
+    const double* u = Ua + (size_t)nu * ra * k;
+    const double* v = Vb + (size_t)nu * rb * k;
+    const double* sv = s + (size_t)nu * k;
+    double acc = 0.0;
+    for (int m = 0; m < km; ++m) acc += sv[m] * u[x + (size_t)m * ra] * v[y + (size_t)m * rb];
+    int id[3];
+    id[ma] = x; id[mb] = y; id[mc] = nu;
+    core[id[0] + (size_t)r0 * (id[1] + (size_t)r1 * id[2])] = acc;
+  }
+}
+
+// X2 [x + r0 (b + t1 z)] -> X2p [b + t1 (x + r0 z)], batched over nb blocks of size r0*t1*r2
+__global__ void permute_xbz_kernel(int nb, int r0, int t1, int r2, const double* __restrict__ X, double* Y) {
+  const long long per = (long long)r0 * t1 * r2, tot = per * nb;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < tot;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const long long bI = idx / per, e = idx % per;
+    const int x = (int)(e % r0), b = (int)((e / r0) % t1), z = (int)(e / ((long long)r0 * t1));
+    Y[bI * per + b + (size_t)t1 * (x + (size_t)r0 * z)] = X[idx];
+  }
+}
+
+// core[x + r0 (y + r1 z)] += sum_i wF[kk0 + i] * X3_i[y + r1 (x + r0 z)]
+__global__ void accumulate_core_kernel(int nb, int r0, int r1, int r2, const double* __restrict__ wF, int kk0,
+                                       const double* __restrict__ X3, double* core) {
+  const long long per = (long long)r0 * r1 * r2;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < per;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int x = (int)(idx % r0), y = (int)((idx / r0) % r1), z = (int)(idx / ((long long)r0 * r1));
+    double acc = core[idx];
+    for (int i = 0; i < nb; ++i) acc += wF[kk0 + i] * X3[i * per + y + (size_t)r1 * (x + (size_t)r0 * z)];
+    core[idx] = acc;
+  }
+}
+
 int blocks_for(long long total) {
   long long b = (total + 255) / 256;
   return (int)std::min<long long>(std::max<long long>(b, 1), 148 * 8);
@@ -357,10 +409,12 @@ TT tucker_to_canonical(fc_ctx c, const double* core, const int r[3], double* con
   out.n = n;
   out.R = R;
   out.q[0] = r[0]; out.q[1] = r[1]; out.q[2] = r[2];
-  size_t need = (size_t)R + (size_t)R * (r[0] + r[1] + r[2]) + (size_t)n * (r[0] + r[1] + r[2]);
+  const size_t csz = (size_t)r[0] * r[1] * r[2];
+  size_t need = (size_t)R + (size_t)R * (r[0] + r[1] + r[2]) + (size_t)n * (r[0] + r[1] + r[2]) + csz;
   out.mem.emplace_back(need * 8, st);
   double* base = out.mem.back().d();
   out.w = base;
+  out.core = base + need - csz;
   double* p = base + R;
   for (int l = 0; l < 3; ++l) {
     out.C[l] = p;
@@ -375,11 +429,41 @@ TT tucker_to_canonical(fc_ctx c, const double* core, const int r[3], double* con
   if (R > 0) {
     t2c_scatter_kernel<<<R, 64, 0, st>>>(R, k, ra, rb, rc, keys, s2s, Ua, Vb, out.w, out.C[ma], out.C[mb], out.C[mc]);
     FC_CHECK_LAUNCH();
+    // Tucker core of the output (kept triples of each slice are a prefix of that slice)
+    int* cnt = s.zeros<int>(rc);
+    slice_counts_kernel<<<cdiv(R, 256), 256, 0, st>>>(R, k, keys, cnt);
+    FC_CHECK_LAUNCH();
+    t2c_core_kernel<<<blocks_for((long long)ra * rb * rc), 256, 0, st>>>(ra, rb, rc, k, cnt, sv, Ua, Vb, ma, mb, mc,
+                                                                         r[0], r[1], out.core);
+    FC_CHECK_LAUNCH();
+  } else {
+    FC_CUDA_TRY(cudaMemsetAsync(out.core, 0, csz * 8, st));
   }
   return out;
 }
 
-TT truncate_tt(fc_ctx c, const TT& xin, double eps, int rank_cap, TruncStats* stats) {
+void tt_compute_core(cudaStream_t st, TT& x) {
+  const size_t csz = (size_t)x.q[0] * x.q[1] * x.q[2];
+  x.mem.emplace_back(std::max<size_t>(csz, 1) * 8, st);
+  x.core = x.mem.back().d();
+  FC_CUDA_TRY(cudaMemsetAsync(x.core, 0, std::max<size_t>(csz, 1) * 8, st));
+  if (x.R == 0 || csz == 0) return;
+  const size_t r12 = (size_t)x.q[0] * x.q[1];
+  // chunk the terms so that the Khatri-Rao operand stays below ~128M doubles
+  const int chunk = (int)std::max<size_t>(1, std::min<size_t>((size_t)x.R, (size_t)(1 << 27) / std::max<size_t>(r12, 1)));
+  Scratch s(st);
+  double* KR = s.alloc<double>(r12 * chunk);
+  for (int t0 = 0; t0 < x.R; t0 += chunk) {
+    const int m = std::min(chunk, x.R - t0);
+    kr12_kernel<<<blocks_for((long long)r12 * m), 256, 0, st>>>(x.q[0], x.q[1], m, x.w + t0, x.C[0] + (size_t)t0 * x.q[0],
+                                                                 x.C[1] + (size_t)t0 * x.q[1], KR);
+    FC_CHECK_LAUNCH();
+    dgemm(st, 0, 1, (int)r12, x.q[2], m, 1.0, KR, (int)r12, x.C[2] + (size_t)t0 * x.q[2], x.q[2], 1.0, x.core,
+          (int)r12, std::max(1, std::min(cdiv(m, 64), 8)));
+  }
+}
+
+TT truncate_tt(fc_ctx c, const TT& xin, double eps, int rank_cap, TruncStats* stats, const StructuredS* ss) {
   cudaStream_t st = c->st;
   const int n = xin.n, R = xin.R;
   TruncStats local;
@@ -396,7 +480,9 @@ TT truncate_tt(fc_ctx c, const TT& xin, double eps, int rank_cap, TruncStats* st
   //         K^T K (no squaring): every column of K is kept to 1e-13 of its norm.
   double* Qo[3];
   double* Co[3];
+  double* RmE[3] = {nullptr, nullptr, nullptr};
   int q[3];
+  require(!ss || (!xin.orth[0] && !xin.orth[1] && !xin.orth[2]), FC_ERR_INVALID_ARG, "structured input basis");
   {
     BcgsBatch pb;
     int* kdev = s.alloc<int>(4);
@@ -456,7 +542,24 @@ TT truncate_tt(fc_ctx c, const TT& xin, double eps, int rank_cap, TruncStats* st
       dgemm(st, 1, 0, k, xin.q[l], n, 1.0, Qo[l], n, xin.Q[l], n, 1.0, Rm, k,
             std::max(1, std::min(cdiv(n, 256), 16)));
       Co[l] = s.alloc<double>((size_t)k * R);
-      dgemm(st, 0, 0, k, R, xin.q[l], 1.0, Rm, k, xin.C[l], xin.q[l], 0.0, Co[l], k);
+      if (!ss) {
+        dgemm(st, 0, 0, k, R, xin.q[l], 1.0, Rm, k, xin.C[l], xin.q[l], 0.0, Co[l], k);
+      } else {
+        // structured Hadamard: K columns a*t + b; Rm viewed (k t) x s times E (s x r) gives
+        // RmE = [Rm_1 | ... | Rm_r], Rm_kk = sum_a E[a,kk] Rm[:, a*t:(a+1)*t] (k x t);
+        // term (kk, j) has coefficient Rm_kk C_x[:, j]  ->  Co[:, kk*Rx + j]
+        const int t = ss->t[l], sl = ss->s[l], r = ss->r, Rx = ss->Rx;
+        RmE[l] = s.alloc<double>((size_t)k * t * r);
+        dgemm(st, 0, 0, k * t, r, sl, 1.0, Rm, k * t, ss->E[l], sl, 0.0, RmE[l], k * t);
+        for (int k0 = 0; k0 < r; k0 += kMaxBatch) {
+          GemmArgs g;
+          g.nbatch = std::min(kMaxBatch, r - k0);
+          for (int b = 0; b < g.nbatch; ++b)
+            g.b[b] = GemmBatch{k, Rx, t, RmE[l] + (size_t)(k0 + b) * k * t, k, ss->Cx[l], t,
+                               Co[l] + (size_t)(k0 + b) * k * Rx, k, nullptr, 0, nullptr};
+          gemm(g, st);
+        }
+      }
     }
   }
   for (int l = 0; l < 3; ++l) {
@@ -547,32 +650,83 @@ TT truncate_tt(fc_ctx c, const TT& xin, double eps, int rank_cap, TruncStats* st
     z.n = n;
     return z;
   }
-  // ---- 5. Z_l = Qo_l Y_r ; unit-factor coefficients Chat_l = Y_r^T C_l diag(1/n_l) ----------
+  // ---- 5. Z_l = Qo_l Y_r -----------------------------------------------------------------
   double* Z[3];
-  double* Chat[3];
   {
-    GemmArgs gz, gc;
-    gz.nbatch = gc.nbatch = 3;
-    gc.transA = 1;
+    GemmArgs gz;
+    gz.nbatch = 3;
     for (int l = 0; l < 3; ++l) {
       Z[l] = s.alloc<double>((size_t)n * r[l]);
-      Chat[l] = s.alloc<double>((size_t)r[l] * R);
       gz.b[l] = GemmBatch{n, r[l], q[l], Qo[l], n, Y[l], q[l], Z[l], n, nullptr, 0, nullptr};
-      gc.b[l] = GemmBatch{r[l], R, q[l], Y[l], q[l], Co[l], q[l], Chat[l], r[l], nullptr, 0, inv[l]};
     }
     gemm(gz, st);
-    gemm(gc, st);
   }
-  // ---- 6. core beta (r1 r2 x r3) = KR12 * Chat_3^T ----------------------------------------
+  // ---- 6. core beta = x x_l Z_l^T (r0 x r1 x r2) ---------------------------------------------
   const size_t r12 = (size_t)r[0] * r[1];
-  double* KR = s.alloc<double>(r12 * R);
-  kr12_kernel<<<blocks_for((long long)r12 * R), 256, 0, st>>>(r[0], r[1], R, xi, Chat[0], Chat[1], KR);
-  FC_CHECK_LAUNCH();
   double* core = s.zeros<double>(r12 * r[2]);
-  {
-    int tiles = cdiv((long long)r12, 64) * cdiv(r[2], 64);
-    dgemm(st, 0, 1, (int)r12, r[2], R, 1.0, KR, (int)r12, Chat[2], r[2], 1.0, core, (int)r12,
-          std::max(1, std::min(cdiv(R, 64), std::max(1, 296 / std::max(tiles, 1)))));
+  if (ss) {
+    // Tucker route: beta = sum_kk wF[kk] core_x x_1 H1_kk x_2 H2_kk x_3 H3_kk,
+    // H_l,kk = Z_l^T diag(u_l,kk) xhat_l = Y_r^T Rm_kk (r_l x t_l): Hall_l = Y_r^T RmE_l
+    double* Hall[3];
+    for (int l = 0; l < 3; ++l) {
+      Hall[l] = s.alloc<double>((size_t)r[l] * ss->t[l] * ss->r);
+      dgemm(st, 1, 0, r[l], ss->t[l] * ss->r, q[l], 1.0, Y[l], q[l], RmE[l], q[l], 0.0, Hall[l], r[l]);
+    }
+    const int t0 = ss->t[0], t1 = ss->t[1], t2 = ss->t[2], r0 = r[0], r1 = r[1], r2 = r[2];
+    const int NB = kMaxBatch;
+    double* X1 = s.alloc<double>((size_t)NB * r0 * t1 * t2);
+    double* X2 = s.alloc<double>((size_t)NB * r0 * t1 * r2);
+    double* X2p = s.alloc<double>((size_t)NB * r0 * t1 * r2);
+    double* X3 = s.alloc<double>((size_t)NB * r0 * r1 * r2);
+    for (int k0 = 0; k0 < ss->r; k0 += NB) {
+      const int nb = std::min(NB, ss->r - k0);
+      GemmArgs a, b, d;
+      a.nbatch = b.nbatch = d.nbatch = nb;
+      b.transB = 1;
+      for (int i = 0; i < nb; ++i) {
+        const int kk = k0 + i;
+        // X1 = H1_kk (r0 x t0) * core_x_(1) (t0 x t1 t2)
+        a.b[i] = GemmBatch{r0, t1 * t2, t0, Hall[0] + (size_t)kk * r0 * t0, r0, ss->core_x, t0,
+                           X1 + (size_t)i * r0 * t1 * t2, r0, nullptr, 0, nullptr};
+        // X2 = X1 ((r0 t1) x t2) * H3_kk^T (t2 x r2)
+        b.b[i] = GemmBatch{r0 * t1, r2, t2, X1 + (size_t)i * r0 * t1 * t2, r0 * t1, Hall[2] + (size_t)kk * r2 * t2, r2,
+                           X2 + (size_t)i * r0 * t1 * r2, r0 * t1, nullptr, 0, nullptr};
+        // X3 = H2_kk (r1 x t1) * X2p (t1 x r0 r2)
+        d.b[i] = GemmBatch{r1, r0 * r2, t1, Hall[1] + (size_t)kk * r1 * t1, r1, X2p + (size_t)i * r0 * t1 * r2, t1,
+                           X3 + (size_t)i * r0 * r1 * r2, r1, nullptr, 0, nullptr};
+      }
+      gemm(a, st);
+      gemm(b, st);
+      permute_xbz_kernel<<<blocks_for((long long)nb * r0 * t1 * r2), 256, 0, st>>>(nb, r0, t1, r2, X2, X2p);
+      FC_CHECK_LAUNCH();
+      gemm(d, st);
+      accumulate_core_kernel<<<blocks_for((long long)r0 * r1 * r2), 256, 0, st>>>(nb, r0, r1, r2, ss->wF, k0, X3,
+                                                                                  core);
+      FC_CHECK_LAUNCH();
+    }
+  } else {
+    // CP route: beta = sum_t xi_t Chat_1[:,t] (x) Chat_2[:,t] (x) Chat_3[:,t] with the
+    // unit-factor coefficients Chat_l = Y_r^T Co_l diag(1/n_l), chunked over the terms
+    double* Chat[3];
+    GemmArgs gc;
+    gc.nbatch = 3;
+    gc.transA = 1;
+    for (int l = 0; l < 3; ++l) {
+      Chat[l] = s.alloc<double>((size_t)r[l] * R);
+      gc.b[l] = GemmBatch{r[l], R, q[l], Y[l], q[l], Co[l], q[l], Chat[l], r[l], nullptr, 0, inv[l]};
+    }
+    gemm(gc, st);
+    const int chunk = (int)std::max<size_t>(1, std::min<size_t>((size_t)R, (size_t)(1 << 27) / std::max<size_t>(r12, 1)));
+    double* KR = s.alloc<double>(r12 * chunk);
+    for (int tt0 = 0; tt0 < R; tt0 += chunk) {
+      const int m = std::min(chunk, R - tt0);
+      kr12_kernel<<<blocks_for((long long)r12 * m), 256, 0, st>>>(r[0], r[1], m, xi + tt0, Chat[0] + (size_t)tt0 * r[0],
+                                                                   Chat[1] + (size_t)tt0 * r[1], KR);
+      FC_CHECK_LAUNCH();
+      int tiles = cdiv((long long)r12, 64) * cdiv(r[2], 64);
+      dgemm(st, 0, 1, (int)r12, r[2], m, 1.0, KR, (int)r12, Chat[2] + (size_t)tt0 * r[2], r[2], 1.0, core, (int)r12,
+            std::max(1, std::min(cdiv(m, 64), std::max(1, 296 / std::max(tiles, 1)))));
+    }
   }
   return tucker_to_canonical(c, core, r, Z, n, eps, 0, rank_cap, &S);
 }
@@ -699,6 +853,12 @@ TT tt_copy(cudaStream_t st, const TT& x) {
     if (x.q[l]) FC_CUDA_TRY(cudaMemcpyAsync(y.Q[l], x.Q[l], (size_t)x.n * x.q[l] * 8, cudaMemcpyDeviceToDevice, st));
     if (x.q[l] && x.R)
       FC_CUDA_TRY(cudaMemcpyAsync(y.C[l], x.C[l], (size_t)x.q[l] * x.R * 8, cudaMemcpyDeviceToDevice, st));
+  }
+  if (x.core) {
+    const size_t csz = (size_t)x.q[0] * x.q[1] * x.q[2];
+    y.mem.emplace_back(std::max<size_t>(csz, 1) * 8, st);
+    y.core = y.mem.back().d();
+    FC_CUDA_TRY(cudaMemcpyAsync(y.core, x.core, csz * 8, cudaMemcpyDeviceToDevice, st));
   }
   return y;
 }

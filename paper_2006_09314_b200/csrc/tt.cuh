@@ -42,7 +42,20 @@ struct TT {
   double* C[3] = {nullptr, nullptr, nullptr};
   double* w = nullptr;
   bool orth[3] = {false, false, false};
+  double* core = nullptr;     // optional Tucker core q0 x q1 x q2 (x = core x_l Q_l), column-major
   std::vector<DevMem> mem;    // owned storage (may be empty for views)
+};
+
+// Structured input of the Hadamard truncation S = F (.) x in eigen coordinates (pcg.cu): the
+// basis is K_l = [w_a (.) xhat_b], the coefficient of term (k, j) is E_l[:, k] (x) C_l[:, j];
+// neither kron(E, C) nor the KR core operand is ever formed.
+struct StructuredS {
+  int s[3], t[3];             // spectral basis size, x basis size per mode (q_l = s_l t_l)
+  int r, Rx;                  // spectral rank, x rank (terms = r * Rx, order k*Rx + j)
+  const double* E[3];         // s_l x r
+  const double* Cx[3];        // t_l x Rx
+  const double* wF;           // r
+  const double* core_x;       // t0 x t1 x t2 (x's Tucker core in its basis)
 };
 
 struct TruncStats {
@@ -54,7 +67,10 @@ struct TruncStats {
 
 // RHOSVD -> core -> T2C (S11-S13).  Output: orthonormal Q (n x r_l), orthogonal CP terms.
 // rank_cap > 0: output rank limit (FC_ERR_CAPACITY with stats.out_rank = required).
-TT truncate_tt(fc_ctx c, const TT& x, double eps, int rank_cap, TruncStats* stats);
+TT truncate_tt(fc_ctx c, const TT& x, double eps, int rank_cap, TruncStats* stats,
+               const StructuredS* ss = nullptr);
+// Tucker core of a TT from its CP coefficients (sum_t w_t (x)_l C_l[:, t]), chunked over terms
+void tt_compute_core(cudaStream_t st, TT& x);
 // T2C of a dense core (r1 x r2 x r3, column-major) with bases Z (n x r_l, orthonormal):
 // eps-cut (keep <= 0) or top-`keep` triples.  Used by the truncation and the spectral CP.
 TT tucker_to_canonical(fc_ctx c, const double* core, const int r[3], double* const Z[3], int n, double eps,
