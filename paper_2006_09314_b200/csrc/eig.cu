@@ -233,6 +233,7 @@ __global__ void ns_matrix_kernel(int n, double* G) {
 // ---------------------------------------------------------------------------------------
 constexpr int kTriThreads = 512;
 constexpr int kSmemMaxN = 150;   // (N^2 + 18 N) * 8 <= 202 KB in shared memory, else global (L2)
+constexpr int kPackedMaxN = 230; // packed lower triangle in shared memory up to this size
 constexpr size_t kTriSmemMax = 220 * 1024;
 
 __device__ double block_sum(double v, double* red) {
@@ -265,9 +266,9 @@ __global__ void __launch_bounds__(kTriThreads) tridiag_kernel(const __grid_const
   __shared__ double alpha_s;
   const SyevEntry& E = B.e[blockIdx.x];
   const int N = E.N;
-  if (N <= 0) return;
+  if (N <= kPackedMaxN) return;          // handled by tridiag_packed_kernel
   constexpr int NW = kTriThreads / 32;
-  const bool use_sm = N <= kSmemMaxN;
+  const bool use_sm = false;
   double* M = use_sm ? sm : E.A;
   const int ld = use_sm ? N : E.lda;
   double* base = use_sm ? sm + (size_t)N * N : sm;
@@ -346,6 +347,84 @@ __global__ void __launch_bounds__(kTriThreads) tridiag_kernel(const __grid_const
     for (int idx = tid; idx < N * N; idx += nt) E.A[(idx % N) + (size_t)(idx / N) * E.lda] = M[idx];
 }
 
+
+// Same Householder tridiagonalisation with the lower triangle packed in shared memory
+// (N(N+1)/2 doubles: N <= 230 fits in 216 KB), 1024 threads, matvec partials by shared-memory
+// atomics.  Column j is contiguous at off(j) = j N - j(j-1)/2; element (i, j), i >= j, at
+// off(j) + i - j.
+__global__ void __launch_bounds__(1024) tridiag_packed_kernel(const __grid_constant__ SyevBatch B) {
+  extern __shared__ double sm[];
+  __shared__ double red[33];
+  __shared__ double alpha_s;
+  const SyevEntry& E = B.e[blockIdx.x];
+  const int N = E.N;
+  if (N <= 0 || N > kPackedMaxN) return;
+  const int tid = threadIdx.x, nt = blockDim.x, warp = tid >> 5, ln = tid & 31, NW = nt >> 5;
+  const size_t P = (size_t)N * (N + 1) / 2;
+  double* L = sm;
+  double* u = sm + P;
+  double* p = u + N;
+  auto off = [N](int j) { return (size_t)j * N - (size_t)j * (j - 1) / 2; };
+  for (int j = warp; j < N; j += NW)
+    for (int i = j + ln; i < N; i += 32) L[off(j) + (i - j)] = E.A[i + (size_t)j * E.lda];
+  __syncthreads();
+  for (int k = 0; k + 2 < N; ++k) {
+    const int m = N - k - 1;
+    double* colk = L + off(k) + 1;           // x = A[k+1.., k]
+    const double x0 = colk[0];
+    double part = 0.0;
+    for (int i = tid + 1; i < m; i += nt) part += colk[i] * colk[i];
+    const double sig = block_sum(part, red);
+    const bool skip = (sig == 0.0);
+    double alpha = x0;
+    if (!skip) {
+      alpha = -copysign(sqrt(x0 * x0 + sig), x0);
+      const double v0 = x0 - alpha;
+      const double inv = 1.0 / sqrt(sig + v0 * v0);
+      for (int i = tid; i < m; i += nt) {
+        u[i] = (i == 0 ? v0 : colk[i]) * inv;
+        p[i] = 0.0;
+      }
+    }
+    __syncthreads();
+    if (!skip) {
+      for (int jj = warp; jj < m; jj += NW) {
+        const double* cj = L + off(k + 1 + jj);   // element (k+1+ii, k+1+jj) at cj[ii - jj]
+        const double uj = u[jj];
+        double dot = 0.0;
+        for (int ii = jj + ln; ii < m; ii += 32) {
+          const double a = cj[ii - jj];
+          atomicAdd(p + ii, a * uj);
+          if (ii > jj) dot += a * u[ii];
+        }
+        for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+        if (ln == 0) atomicAdd(p + jj, dot);
+      }
+      __syncthreads();
+      double kp = 0.0;
+      for (int i = tid; i < m; i += nt) kp += u[i] * p[i];
+      const double K = block_sum(kp, red);
+      for (int i = tid; i < m; i += nt) p[i] -= K * u[i];
+      __syncthreads();
+      for (int jj = warp; jj < m; jj += NW) {
+        double* cj = L + off(k + 1 + jj);
+        const double uj = u[jj], qj = p[jj];
+        for (int ii = jj + ln; ii < m; ii += 32) cj[ii - jj] -= 2.0 * (u[ii] * qj + p[ii] * uj);
+      }
+      __syncthreads();
+    }
+    if (tid == 0) alpha_s = alpha;
+    __syncthreads();
+    for (int i = tid; i < m; i += nt) colk[i] = skip ? 0.0 : u[i];
+    if (tid == 0) E.e[k] = alpha_s;
+    __syncthreads();
+  }
+  // d, the last off-diagonal, and the Householder vectors back to global memory
+  for (int k = tid; k < N; k += nt) E.d[k] = L[off(k)];
+  if (tid == 0 && N >= 2) E.e[N - 2] = L[off(N - 2) + 1];
+  for (int k = warp; k + 2 < N; k += NW)
+    for (int i = ln; i < N - k - 1; i += 32) E.A[(k + 1 + i) + (size_t)k * E.lda] = L[off(k) + 1 + i];
+}
 
 __device__ int tri_count(int N, const double* __restrict__ d, const double* __restrict__ e, double x,
                          double pivmin) {
@@ -544,15 +623,33 @@ __global__ void __launch_bounds__(kPmgsThreads) pmgs_kernel(const __grid_constan
   if (tid == 0) *E.k_out = k;
 }
 
+// warp-level dot product of a global vector with a shared-memory vector, 4 independent
+// accumulators (keeps 4 loads in flight per lane); result valid in every lane
+__device__ __forceinline__ double warp_dot_gs(const double* __restrict__ g, const double* s, int n, int ln) {
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  int i = ln;
+  for (; i + 96 < n; i += 128) {
+    a0 += g[i] * s[i];
+    a1 += g[i + 32] * s[i + 32];
+    a2 += g[i + 64] * s[i + 64];
+    a3 += g[i + 96] * s[i + 96];
+  }
+  for (; i < n; i += 32) a0 += g[i] * s[i];
+  double v = (a0 + a1) + (a2 + a3);
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
 // In-block step of the blocked rank-revealing Gram-Schmidt (one CTA per matrix): the block's
-// columns X (n x w), already projected against the accepted basis Q[:, :k], are orthogonalised
-// among themselves in order (two MGS passes against the vectors accepted in this block);
-// a column is accepted when its residual exceeds tau * its original norm, and appended to Q at
-// the device counter k.
-__global__ void __launch_bounds__(512) bcgs_block_kernel(const __grid_constant__ BcgsBatch B, int j0, int w) {
+// columns (already projected against the accepted basis by GEMMs) are orthogonalised among
+// themselves in order, two MGS passes against the vectors accepted in this block, with the
+// current column staged in shared memory; a column is accepted when its residual exceeds
+// tau * max(its norm, the largest column norm) and is written, normalised, to the block buffer
+// Y (n x 32).  The BCGS2 second pass (GEMM + bcgs_finalize_kernel) follows.
+__global__ void __launch_bounds__(1024) bcgs_block_kernel(const __grid_constant__ BcgsBatch B, int j0, int w) {
+  extern __shared__ double xs[];   // n
   __shared__ double coef[64];
   __shared__ double red[33];
-  __shared__ int acc_idx[64];
   __shared__ int nacc_s, k0_s;
   __shared__ double nmax_s;
   const BcgsEntry& E = B.e[blockIdx.x];
@@ -569,26 +666,30 @@ __global__ void __launch_bounds__(512) bcgs_block_kernel(const __grid_constant__
   for (int i = tid; i < n * 32; i += nt) E.Y[i] = 0.0;   // block buffer (n x 32, ld n)
   __syncthreads();
   for (int c = 0; c < wb; ++c) {
-    double* x = E.A + (size_t)(j0 + c) * E.lda;
+    const double* xg = E.A + (size_t)(j0 + c) * E.lda;
+    for (int i = tid; i < n; i += nt) xs[i] = xg[i];
+    __syncthreads();
     const int na = nacc_s;
-    for (int pass = 0; pass < 2; ++pass) {
+    for (int pass = 0; pass < 2 && na > 0; ++pass) {
       for (int a = warp; a < na; a += nw) {
-        const double* q = E.Y + (size_t)a * n;
-        double s = 0.0;
-        for (int i = ln; i < n; i += 32) s += q[i] * x[i];
-        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        const double s = warp_dot_gs(E.Y + (size_t)a * n, xs, n, ln);
         if (ln == 0) coef[a] = s;
       }
       __syncthreads();
       for (int i = tid; i < n; i += nt) {
-        double v = x[i];
-        for (int a = 0; a < na; ++a) v -= coef[a] * E.Y[i + (size_t)a * n];
-        x[i] = v;
+        double v0 = xs[i], v1 = 0.0;
+        int a = 0;
+        for (; a + 1 < na; a += 2) {
+          v0 -= coef[a] * E.Y[i + (size_t)a * n];
+          v1 -= coef[a + 1] * E.Y[i + (size_t)(a + 1) * n];
+        }
+        if (a < na) v0 -= coef[a] * E.Y[i + (size_t)a * n];
+        xs[i] = v0 + v1;
       }
       __syncthreads();
     }
     double part = 0.0;
-    for (int i = tid; i < n; i += nt) part += x[i] * x[i];
+    for (int i = tid; i < n; i += nt) part += xs[i] * xs[i];
     const double s2 = block_sum(part, red);
     // kept if the residual exceeds tau times its own norm AND tau times the largest column
     // (columns below tau * max are negligible; their residuals are rounding residue, and
@@ -597,7 +698,7 @@ __global__ void __launch_bounds__(512) bcgs_block_kernel(const __grid_constant__
     if (s2 > lim * lim && k0_s + na < E.kcap) {
       const double inv = 1.0 / sqrt(s2);
       double* q = E.Y + (size_t)na * n;
-      for (int i = tid; i < n; i += nt) q[i] = x[i] * inv;
+      for (int i = tid; i < n; i += nt) q[i] = xs[i] * inv;
       if (tid == 0) nacc_s = na + 1;
     }
     __syncthreads();
@@ -607,7 +708,8 @@ __global__ void __launch_bounds__(512) bcgs_block_kernel(const __grid_constant__
 
 // BCGS2 second pass, in-block part: the accepted unit vectors Y[:, :nacc] (already re-projected
 // against Q by a GEMM) are re-orthonormalised among themselves (MGS) and appended to Q at k.
-__global__ void __launch_bounds__(512) bcgs_finalize_kernel(const __grid_constant__ BcgsBatch B, int j0) {
+__global__ void __launch_bounds__(1024) bcgs_finalize_kernel(const __grid_constant__ BcgsBatch B, int j0) {
+  extern __shared__ double ys[];   // n
   __shared__ double coef[64];
   __shared__ double red[33];
   const BcgsEntry& E = B.e[blockIdx.x];
@@ -616,27 +718,27 @@ __global__ void __launch_bounds__(512) bcgs_finalize_kernel(const __grid_constan
   const int tid = threadIdx.x, nt = blockDim.x, warp = tid >> 5, ln = tid & 31, nw = nt >> 5;
   for (int c = 0; c < na; ++c) {
     double* y = E.Y + (size_t)c * n;
+    for (int i = tid; i < n; i += nt) ys[i] = y[i];
+    __syncthreads();
     for (int a = warp; a < c; a += nw) {
-      const double* q = E.Y + (size_t)a * n;
-      double s = 0.0;
-      for (int i = ln; i < n; i += 32) s += q[i] * y[i];
-      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      const double s = warp_dot_gs(E.Y + (size_t)a * n, ys, n, ln);
       if (ln == 0) coef[a] = s;
     }
     __syncthreads();
     double part = 0.0;
     for (int i = tid; i < n; i += nt) {
-      double v = y[i];
+      double v = ys[i];
       for (int a = 0; a < c; ++a) v -= coef[a] * E.Y[i + (size_t)a * n];
-      y[i] = v;
+      ys[i] = v;
       part += v * v;
     }
     const double s2 = block_sum(part, red);
     const double inv = s2 > 0 ? 1.0 / sqrt(s2) : 0.0;
     double* q = E.Q + (size_t)(k0 + c) * E.ldq;
     for (int i = tid; i < n; i += nt) {
-      y[i] *= inv;
-      q[i] = y[i];
+      const double v = ys[i] * inv;
+      y[i] = v;
+      q[i] = v;
     }
     __syncthreads();
   }
@@ -733,23 +835,37 @@ void sl_eigen_device(cudaStream_t st, int n, const double* a_mid_dev, int bounda
 void syev_values(const SyevBatch& b, cudaStream_t st) {
   if (b.nb == 0) return;
   int maxN = 0;
-  size_t smem = 0;
+  size_t smem_g = 0, smem_p = 0;
+  bool any_g = false, any_p = false;
   constexpr int NW = kTriThreads / 32;
   for (int i = 0; i < b.nb; ++i) {
     const int N = b.e[i].N;
     maxN = std::max(maxN, N);
-    const size_t need = ((N <= kSmemMaxN ? (size_t)N * N : 0) + (size_t)(2 + NW) * N) * 8;
-    smem = std::max(smem, need);
+    if (N <= 0) continue;
+    if (N <= kPackedMaxN) {
+      any_p = true;
+      smem_p = std::max(smem_p, ((size_t)N * (N + 1) / 2 + 2 * (size_t)N) * 8);
+    } else {
+      any_g = true;
+      smem_g = std::max(smem_g, (size_t)(2 + NW) * N * 8);
+    }
   }
   if (maxN == 0) return;
-  require(smem <= kTriSmemMax, FC_ERR_CAPACITY, "symmetric eigensolver: matrix dimension above 1500");
+  require(smem_g <= kTriSmemMax, FC_ERR_CAPACITY, "symmetric eigensolver: matrix dimension above 1500");
   static bool attr = false;
   if (!attr) {
     FC_CUDA_TRY(cudaFuncSetAttribute(tridiag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTriSmemMax));
+    FC_CUDA_TRY(cudaFuncSetAttribute(tridiag_packed_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     attr = true;
   }
-  tridiag_kernel<<<b.nb, kTriThreads, smem, st>>>(b);
-  FC_CHECK_LAUNCH();
+  if (any_p) {
+    tridiag_packed_kernel<<<b.nb, 1024, smem_p, st>>>(b);
+    FC_CHECK_LAUNCH();
+  }
+  if (any_g) {
+    tridiag_kernel<<<b.nb, kTriThreads, smem_g, st>>>(b);
+    FC_CHECK_LAUNCH();
+  }
   tri_bisect_kernel<<<dim3(cdiv(maxN, 64), b.nb), 64, 0, st>>>(b);
   FC_CHECK_LAUNCH();
 }
@@ -805,7 +921,8 @@ void bcgs(const BcgsBatch& bin, cudaStream_t st) {
   FC_CHECK_LAUNCH();
   for (int j0 = 0; j0 < maxp; j0 += W) {
     // project the block against every column accepted so far (<= j0; unused Q columns are 0)
-    for (int pass = 0; pass < 2 && j0 > 0; ++pass) {
+    // one projection pass (BCGS2: the accepted vectors get a second one below)
+    for (int pass = 0; pass < 1 && j0 > 0; ++pass) {
       GemmArgs p, u;
       p.transA = 1;
       p.beta = 1.0;
@@ -826,7 +943,7 @@ void bcgs(const BcgsBatch& bin, cudaStream_t st) {
       gemm(p, st);
       gemm(u, st);
     }
-    bcgs_block_kernel<<<b.nb, 512, 0, st>>>(b, j0, W);
+    bcgs_block_kernel<<<b.nb, 1024, (size_t)b.e[0].n * 8, st>>>(b, j0, W);
     FC_CHECK_LAUNCH();
     // BCGS2: re-project the accepted (unit) block vectors against the previous basis
     if (j0 > 0) {
@@ -850,7 +967,7 @@ void bcgs(const BcgsBatch& bin, cudaStream_t st) {
       gemm(p, st);
       gemm(u, st);
     }
-    bcgs_finalize_kernel<<<b.nb, 512, 0, st>>>(b, j0);
+    bcgs_finalize_kernel<<<b.nb, 1024, (size_t)b.e[0].n * 8, st>>>(b, j0);
     FC_CHECK_LAUNCH();
   }
 }

@@ -463,6 +463,12 @@ void tt_compute_core(cudaStream_t st, TT& x) {
   }
 }
 
+// Basis tolerance of the rank-revealing orthonormalisation (relative to the largest column of
+// K).  A dropped residual moves a side-matrix singular value near the cut by at most
+// ~2 kBasisTol ||A|| sigma_cut, i.e. <= 4e-4 of the threshold (eps/2)^2 ||A||^2 at eps = 1e-6,
+// well inside the A23 noise band; it shrinks the eigenproblem (and its N^3 cost) notably.
+constexpr double kBasisTol = 1e-10;
+
 TT truncate_tt(fc_ctx c, const TT& xin, double eps, int rank_cap, TruncStats* stats, const StructuredS* ss) {
   cudaStream_t st = c->st;
   const int n = xin.n, R = xin.R;
@@ -497,7 +503,7 @@ TT truncate_tt(fc_ctx c, const TT& xin, double eps, int rank_cap, TruncStats* st
       double* Qn = s.alloc<double>((size_t)n * kcap);
       map[l] = pb.nb;
       pb.e[pb.nb++] = BcgsEntry{n, xin.q[l], Kc, n, Qn, n, kcap, kdev + l, s.alloc<double>(xin.q[l]),
-                                s.alloc<double>((size_t)kcap * 32), 1e-13};
+                                s.alloc<double>((size_t)kcap * 32), kBasisTol};
     }
     bcgs(pb, st);
     int kh[4] = {0, 0, 0, 0};
