@@ -248,8 +248,22 @@ def main():
         dist.all_reduce(tt[1:], op=dist.ReduceOp.SUM)
         e2e_value = float(tt[1]) / float(tmax[0])
 
-    # ---- dominant-kernel roofline: the fused Khatri-Rao inverse transform (DMMA) ---------
-    roof = apply_roofline(ctx, L, p.n)
+    # ---- dominant kernel class of the step: the DMMA GEMMs (one extra, untimed solve with every
+    # GEMM launch bracketed by events on the library stream; algorithmic flops 2MNK) ----------
+    ctx.profile_gemm(True)
+    flush.fill_(1.0)
+    _, rep_p, _ = ctx.pcg_solve(b, prm)
+    gp = ctx.profile_gemm(False)
+    step_ms = float(np.median(times))
+    ach = gp["flops"] / (gp["ms"] * 1e-3) / 1e12 if gp["ms"] > 0 else 0.0
+    roof = {"kernel": "dgemm_dmma_kernel / dgemm_big_kernel (all DMMA GEMM launches of one pcg_solve)",
+            "bound": "tensor", "achieved": ach, "peak": FP64_DMMA_TFLOPS, "unit": "TFLOP/s",
+            "frac": ach / FP64_DMMA_TFLOPS, "traffic": None,
+            "peak_source": "measured DMMA m8n8k4 FP64 peak (tools/peak_fp64.cu); MEASURED_PEAKS.json has no FP64 entry",
+            "launches_per_step": gp["launches"], "gemm_ms_per_step": gp["ms"],
+            "share_of_step": gp["ms"] / step_ms if step_ms > 0 else None}
+    # the north-star's mode-transform kernel at a C5 cell (fused Khatri-Rao inverse transform)
+    roof_apply = apply_roofline(ctx, L, p.n)
     if rank != 0:
         return
     line = {
@@ -266,6 +280,7 @@ def main():
         "gpu_launches": int(launches),
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
         "roofline": roof,
+        "roofline_apply": roof_apply,
         "clocks": clk.summary(),
     }
     if not args.no_cpu_baseline and world == 1 or (not args.no_cpu_baseline and rank == 0):

@@ -177,6 +177,10 @@ int fc_last_kernel_stats(fc_ctx ctx, double* ms, double* flops, double* bytes, i
  * to tau times their norm): A (device, n x p, column-major, overwritten), Q (device, n x
  * min(n,p)); *k_host receives the basis size. */
 int fc_orthonormalize(fc_ctx ctx, int n, int p, double* A, double* Q, double tau, int* k_host);
+/* Opt-in accounting of every DMMA GEMM launch (events around each launch; for the bench's
+ * roofline line).  enable=1 starts recording; enable=0 stops and returns the summed device
+ * time (ms), the summed algorithmic flops (2 M N K per batch entry) and the launch count. */
+int fc_profile_gemm(fc_ctx ctx, int enable, double* ms, double* flops, long long* launches);
 /* Process-wide count of CUDA kernels this library has launched (host-side counter). */
 int fc_kernel_launches(long long* count);
 

@@ -67,7 +67,8 @@ class FCError(RuntimeError):
 ENTRY_POINTS = ["fc_create", "fc_destroy", "fc_last_error", "fc_set_stream", "sl_setup", "sl_get_eigen",
                 "sl_set_eigen", "op_get_spectral_cp", "op_set_spectral_cp", "op_spectral_rank",
                 "fracop_apply", "precond_apply", "cp_dot", "cp_axpy", "cp_truncate", "pcg_solve",
-                "fc_dgemm", "fc_last_kernel_stats", "fc_kernel_launches", "fracop_apply_truncate", "fc_orthonormalize"]
+                "fc_dgemm", "fc_last_kernel_stats", "fc_kernel_launches", "fracop_apply_truncate", "fc_orthonormalize",
+                "fc_profile_gemm"]
 
 
 def load_library(path: str = LIB_PATH) -> C.CDLL:
@@ -94,6 +95,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "fc_last_kernel_stats": ([P, C.POINTER(D), C.POINTER(D), C.POINTER(D), C.POINTER(I)], I),
         "fc_kernel_launches": ([C.POINTER(C.c_longlong)], I),
         "fc_orthonormalize": ([P, I, I, P, P, D, C.POINTER(I)], I),
+        "fc_profile_gemm": ([P, I, C.POINTER(D), C.POINTER(D), C.POINTER(C.c_longlong)], I),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -289,6 +291,11 @@ class Context:
             return u, rep.as_dict(), rc
 
     # ---- raw ----
+    def profile_gemm(self, enable: bool):
+        ms, fl, nl = C.c_double(), C.c_double(), C.c_longlong()
+        self._check(self.lib.fc_profile_gemm(self.h, 1 if enable else 0, C.byref(ms), C.byref(fl), C.byref(nl)))
+        return {"ms": ms.value, "flops": fl.value, "launches": nl.value}
+
     def orthonormalize(self, A, tau=1e-13):
         """A: torch (p, n) row-major == n x p column-major (overwritten).  Returns Q (k, n)."""
         import torch

@@ -93,6 +93,16 @@ void apply_plain(fc_ctx c, const SpecCP& sp, const fc_cp& x, fc_cp& y) {
   for (int l = 0; l < 3; ++l)
     iv.b[l] = GemmBatch{n, r * R, n, c->V_l(l), n, What + (size_t)l * n * R, n, y.U[l], y.ld[l],
                         sp.Ul(n, l), n, csp[l]};
+  // wave balance: with one 128x128 CTA per SM, split K until the grid covers >= 3 waves
+  const long long tiles = 3LL * cdiv(n, 128) * cdiv((long long)r * R, 128);
+  int sk = 1;
+  while (tiles * sk < 3LL * 148 && n / (sk * 2) >= 256 && sk < 4) sk *= 2;
+  if (sk > 1) {
+    iv.splitk = sk;
+    iv.beta = 1.0;
+    for (int l = 0; l < 3; ++l)
+      FC_CUDA_TRY(cudaMemset2DAsync(y.U[l], (size_t)y.ld[l] * 8, 0, (size_t)n * 8, (size_t)r * R, st));
+  }
   FC_CUDA_TRY(cudaEventRecord(c->e0, st));
   gemm(iv, st);
   FC_CUDA_TRY(cudaEventRecord(c->e1, st));
@@ -191,6 +201,13 @@ int fc_orthonormalize(fc_ctx c, int n, int p, double* A, double* Q, double tau, 
                   std::to_string(kh[i]) + ", maxdiff " + std::to_string(d) + ")");
     }
     *k_host = kh[0];
+    return FC_OK;
+  });
+}
+
+int fc_profile_gemm(fc_ctx c, int enable, double* ms, double* flops, long long* launches) {
+  return guard(c, [&]() {
+    gemm_profile(enable != 0, ms, flops, launches);
     return FC_OK;
   });
 }

@@ -120,6 +120,8 @@ struct GemmArgs {
   GemmBatch b[kMaxBatch];
 };
 void gemm(const GemmArgs& a, cudaStream_t st);
+// fc_profile_gemm: enable -> start recording; disable -> totals of the recorded launches
+void gemm_profile(bool enable, double* ms, double* flops, long long* launches);
 // convenience single GEMM
 void dgemm(cudaStream_t st, int transA, int transB, int M, int N, int K, double alpha,
            const double* A, int lda, const double* B, int ldb, double beta, double* C, int ldc,

@@ -208,9 +208,256 @@ __global__ void __launch_bounds__(NT) dgemm_dmma_kernel(const __grid_constant__ 
   }
 }
 
+// ---------------------------------------------------------------------------------------
+// Big-tile variant: CTA 128x128, BK = 16, 16 warps (4 x 4) each owning 32x32 (4x4 DMMA
+// fragments, 64 fp64 accumulators per thread), 3-stage cp.async ring.  Operand tiles are
+// stored k-major ([k][m], ld 136) when the operand is contiguous along m/n, and m/n-major
+// ([m][k], ld 20) when it is contiguous along k, so that 16-byte cp.async can be used for
+// K-contiguous operands and every fragment load is at most 2-way banked.
+namespace big {
+constexpr int BM = 128, BN = 128, BK = 16, NT = 512, STAGES = 3;
+constexpr int LDK = BM + 8;        // k-major row length (136)
+constexpr int LDM = BK + 4;        // m/n-major row length (20)
+constexpr int TILE = BM * LDM > BK * LDK ? BM * LDM : BK * LDK;   // 2560 doubles
+
+__device__ __forceinline__ void cp_async16(double* smem, const double* gmem, int bytes) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(bytes));
+}
+
+// load a ROWS x BK operand tile; `kcontig`: element (r, k) at base + k + r*ld (K contiguous),
+// else at base + r + k*ld.  Stored k-major if !kcontig, r-major if kcontig.
+template <bool KCONTIG>
+__device__ __forceinline__ void load_op(double* T, const double* base, int ld, int r0, int rmax, int k0, int kend,
+                                        int tid, bool vec) {
+  if (KCONTIG) {
+    // 128 rows x 16 k: 8 x 16-byte chunks per row -> 1024 chunks, 2 per thread
+#pragma unroll
+    for (int i = 0; i < 1024 / NT; ++i) {
+      const int idx = tid + i * NT;
+      const int rr = idx >> 3, kk = (idx & 7) * 2;
+      const int r = r0 + rr, k = k0 + kk;
+      double* dst = T + rr * LDM + kk;
+      if (vec) {
+        const int nk = (r < rmax) ? max(0, min(2, kend - k)) : 0;
+        cp_async16(dst, nk > 0 ? base + (size_t)k + (size_t)r * ld : base, nk * 8);
+      } else {
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const bool ok = (r < rmax) && (k + e < kend);
+          cp_async8(dst + e, ok ? base + (size_t)(k + e) + (size_t)r * ld : base, ok);
+        }
+      }
+    }
+  } else {
+    // 16 k x 128 rows: 64 x 16-byte chunks per k-row -> 1024 chunks, 2 per thread
+#pragma unroll
+    for (int i = 0; i < 1024 / NT; ++i) {
+      const int idx = tid + i * NT;
+      const int kk = idx >> 6, rr = (idx & 63) * 2;
+      const int r = r0 + rr, k = k0 + kk;
+      double* dst = T + kk * LDK + rr;
+      if (vec) {
+        const int nr = (k < kend) ? max(0, min(2, rmax - r)) : 0;
+        cp_async16(dst, nr > 0 ? base + (size_t)r + (size_t)k * ld : base, nr * 8);
+      } else {
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const bool ok = (r + e < rmax) && (k < kend);
+          cp_async8(dst + e, ok ? base + (size_t)(r + e) + (size_t)k * ld : base, ok);
+        }
+      }
+    }
+  }
+}
+
+// Khatri-Rao operand tile (K contiguous): column c -> W[:, c % R] and U[:, c / R]
+__device__ __forceinline__ void load_kr(double* T, double* TK, const GemmBatch& g, int krR, int n0, int k0, int kend,
+                                        int tid) {
+#pragma unroll
+  for (int i = 0; i < 2048 / NT; ++i) {
+    const int idx = tid + i * NT;
+    const int rr = idx >> 4, kk = idx & 15;
+    const int c = n0 + rr, k = k0 + kk;
+    const bool ok = (c < g.N) && (k < kend);
+    const int kf = ok ? c / krR : 0, j = ok ? c - kf * krR : 0;
+    cp_async8(T + rr * LDM + kk, ok ? g.B + (size_t)k + (size_t)j * g.ldb : g.B, ok);
+    cp_async8(TK + rr * LDM + kk, ok ? g.krU + (size_t)k + (size_t)kf * g.ldkr : g.krU, ok);
+  }
+}
+
+template <int TA, int TB, bool KR>
+__global__ void __launch_bounds__(NT, 1) dgemm_big_kernel(const __grid_constant__ GemmArgs args) {
+  extern __shared__ __align__(16) double smem[];
+  double* As = smem;
+  double* Bs = smem + STAGES * TILE;
+  double* Ks = smem + 2 * STAGES * TILE;
+  const int bz = blockIdx.z;
+  const int bi = bz / args.splitk, ks = bz - bi * args.splitk;
+  const GemmBatch& g = args.b[bi];
+  const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
+  if (m0 >= g.M || n0 >= g.N) return;
+  const int kchunk = ((g.K + args.splitk - 1) / args.splitk + BK - 1) / BK * BK;
+  const int kbeg = ks * kchunk, kend = min(g.K, kbeg + kchunk);
+  const int nk = kend > kbeg ? (kend - kbeg + BK - 1) / BK : 0;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = (warp & 3) * 32, wn = (warp >> 2) * 32;
+  const int fr = lane >> 2, fc4 = lane & 3;
+  // 16-byte transfers need an even leading dimension and 16-byte aligned base pointers
+  const bool vecA = ((g.lda & 1) == 0) && (((uintptr_t)g.A & 15) == 0);
+  const bool vecB = ((g.ldb & 1) == 0) && (((uintptr_t)g.B & 15) == 0);
+  constexpr bool AK = TA == 1;    // A contiguous along k
+  constexpr bool BKc = TB == 0;   // B contiguous along k
+
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  auto issue = [&](int s, int kt) {
+    const int k0 = kbeg + kt * BK;
+    load_op<AK>(As + s * TILE, g.A, g.lda, m0, g.M, k0, kend, tid, vecA);
+    if (KR) load_kr(Bs + s * TILE, Ks + s * TILE, g, args.krR, n0, k0, kend, tid);
+    else load_op<BKc>(Bs + s * TILE, g.B, g.ldb, n0, g.N, k0, kend, tid, vecB);
+  };
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < nk) issue(s, s);
+    cp_async_commit();
+  }
+  for (int kt = 0; kt < nk; ++kt) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    {
+      const int nt = kt + STAGES - 1;
+      if (nt < nk) issue(nt % STAGES, nt);
+      cp_async_commit();
+    }
+    const int st = kt % STAGES;
+    const double* a_s = As + st * TILE;
+    const double* b_s = Bs + st * TILE;
+    const double* k_s = Ks + st * TILE;
+#pragma unroll
+    for (int kq = 0; kq < BK; kq += 4) {
+      double af[4], bf[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int m = wm + i * 8 + fr, k = kq + fc4;
+        af[i] = AK ? a_s[m * LDM + k] : a_s[k * LDK + m];
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int nn = wn + j * 8 + fr, k = kq + fc4;
+        if (KR) {
+          const int o = nn * LDM + k;
+          bf[j] = b_s[o] * k_s[o];
+        } else {
+          bf[j] = (BKc || KR) ? b_s[nn * LDM + k] : b_s[k * LDK + nn];
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+  }
+  cp_async_wait<0>();
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int c = n0 + wn + j * 8 + 2 * fc4 + e;
+      if (c >= g.N) continue;
+      const double cs = g.colscale ? g.colscale[c] : 1.0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int r = m0 + wm + i * 8 + fr;
+        if (r >= g.M) continue;
+        const double v = args.alpha * cs * acc[i][j][e];
+        double* dst = g.C + (size_t)r + (size_t)c * g.ldc;
+        if (args.splitk > 1) atomicAdd(dst, v);
+        else if (args.beta == 0.0) *dst = v;
+        else *dst = v + args.beta * *dst;
+      }
+    }
+  }
+}
+
+template <int TA, int TB, bool KR>
+void launch_big(const GemmArgs& a, dim3 grid, cudaStream_t st) {
+  const int smem = (KR ? 3 : 2) * STAGES * TILE * (int)sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    FC_CUDA_TRY(cudaFuncSetAttribute(dgemm_big_kernel<TA, TB, KR>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr = true;
+  }
+  dgemm_big_kernel<TA, TB, KR><<<grid, NT, smem, st>>>(a);
+  FC_CHECK_LAUNCH();
+}
+}  // namespace big
+
 }  // namespace
 
+// ---- opt-in accounting of every GEMM launch (fc_profile_gemm): events around each launch and
+// the algorithmic flop count 2 M N K per batch entry ------------------------------------
+namespace {
+struct GemmProf {
+  bool on = false;
+  std::vector<cudaEvent_t> ev;   // pairs
+  std::vector<double> flops;
+  size_t used = 0;
+};
+GemmProf& gprof() {
+  static GemmProf p;
+  return p;
+}
+}  // namespace
+
+void gemm_profile(bool enable, double* ms, double* flops, long long* launches) {
+  GemmProf& P = gprof();
+  if (enable) {
+    P.on = true;
+    P.used = 0;
+    P.flops.clear();
+    return;
+  }
+  P.on = false;
+  double t = 0, f = 0;
+  for (size_t i = 0; i < P.used; ++i) {
+    float x = 0;
+    FC_CUDA_TRY(cudaEventSynchronize(P.ev[2 * i + 1]));
+    FC_CUDA_TRY(cudaEventElapsedTime(&x, P.ev[2 * i], P.ev[2 * i + 1]));
+    t += x;
+    f += P.flops[i];
+  }
+  if (ms) *ms = t;
+  if (flops) *flops = f;
+  if (launches) *launches = (long long)P.used;
+}
+
+static void gemm_dispatch(const GemmArgs& a, cudaStream_t st);
+
 void gemm(const GemmArgs& a, cudaStream_t st) {
+  GemmProf& P = gprof();
+  if (!P.on) return gemm_dispatch(a, st);
+  if (P.ev.size() < 2 * (P.used + 1)) {
+    for (int i = 0; i < 256; ++i) {
+      cudaEvent_t e;
+      FC_CUDA_TRY(cudaEventCreate(&e));
+      P.ev.push_back(e);
+    }
+  }
+  double f = 0;
+  for (int i = 0; i < a.nbatch; ++i) f += 2.0 * a.b[i].M * (double)a.b[i].N * a.b[i].K;
+  FC_CUDA_TRY(cudaEventRecord(P.ev[2 * P.used], st));
+  gemm_dispatch(a, st);
+  FC_CUDA_TRY(cudaEventRecord(P.ev[2 * P.used + 1], st));
+  P.flops.push_back(f);
+  ++P.used;
+}
+
+static void gemm_dispatch(const GemmArgs& a, cudaStream_t st) {
   if (a.nbatch <= 0) return;
   int maxM = 0, maxN = 0;
   for (int i = 0; i < a.nbatch; ++i) {
@@ -218,6 +465,22 @@ void gemm(const GemmArgs& a, cudaStream_t st) {
     maxN = std::max(maxN, a.b[i].N);
   }
   if (maxM == 0 || maxN == 0) return;
+  long long work = 0;
+  int minK = INT32_MAX;
+  for (int i = 0; i < a.nbatch; ++i) {
+    work += (long long)a.b[i].M * a.b[i].N * a.b[i].K;
+    minK = std::min(minK, a.b[i].K);
+  }
+  if (a.gen.kind < 0 && maxM >= 256 && maxN >= 256 && minK >= 64 && work >= (1LL << 27)) {
+    dim3 grid(cdiv(maxM, big::BM), cdiv(maxN, big::BN), a.nbatch * a.splitk);
+    require(grid.y <= 65535 && grid.z <= 65535, FC_ERR_INVALID_ARG, "gemm grid too large");
+    if (a.krR > 0) big::launch_big<0, 0, true>(a, grid, st);
+    else if (!a.transA && !a.transB) big::launch_big<0, 0, false>(a, grid, st);
+    else if (a.transA && !a.transB) big::launch_big<1, 0, false>(a, grid, st);
+    else if (!a.transA && a.transB) big::launch_big<0, 1, false>(a, grid, st);
+    else big::launch_big<1, 1, false>(a, grid, st);
+    return;
+  }
   static bool attr = false;
   const int smem2 = 2 * STAGES * STAGE_ELEMS * (int)sizeof(double);
   const int smem3 = 3 * STAGES * STAGE_ELEMS * (int)sizeof(double);

@@ -35,7 +35,10 @@ def _shared_setup(ctx, p, F_eps=1e-6, r_fixed=None):
 
 
 @pytest.mark.parametrize("tA,tB,M,N,K", [(0, 0, 64, 64, 64), (1, 0, 37, 129, 200), (0, 1, 130, 3, 17),
-                                         (1, 1, 1, 77, 65), (0, 0, 300, 260, 1)])
+                                         (1, 1, 1, 77, 65), (0, 0, 300, 260, 1),
+                                         # big-tile kernel (ragged edges, all transposes)
+                                         (0, 0, 1000, 700, 300), (1, 0, 513, 1030, 257),
+                                         (0, 1, 700, 900, 330), (1, 1, 400, 600, 1001)])
 def test_dgemm(lib, tA, tB, M, N, K):
     import torch
     ctx = lib.context()

@@ -120,18 +120,28 @@ def test_pcg_parity_shared(lib, name, n):
 MARGIN_BAND = 5e-3   # relative distance of thr to a bracketing tail below which a cut is marginal
 
 
+CANCEL_RES = 1e-4   # below this relative residual, R = R - a S is a cancellation of ~1/rel_res
+
+
 def check_rank_history(rep, rep_ref):
     """Ranks equal truncation by truncation until the first cut the oracle logged as marginal
     (A23 noise band); after a marginal cut the two runs are different (equally valid) rank
-    sequences, so only the iteration count (+-1) and the final control are compared."""
+    sequences, so only the iteration count (+-1) and the final control are compared.
+    Once the residual is below CANCEL_RES, the update R - a S cancels ~1/rel_res of its
+    magnitude, amplifying rounding differences by the same factor; there ranks may differ by
+    1% (or 2 terms) without being logged as marginal."""
     m = rep_ref["margins"]          # order: Z0, then per iteration S, X, R, Z, P
     marginal = False
     for k in range(min(rep["iters"], rep_ref["iters"])):
         base = 1 + 5 * k
+        cancel = k > 0 and rep_ref["rel_res"][k - 1] < CANCEL_RES
         for key, off in (("rank_S", 0), ("rank_X", 1), ("rank_R", 2)):
             if marginal:
                 break
             if rep[key][k] != rep_ref[key][k]:
+                if cancel and abs(rep[key][k] - rep_ref[key][k]) <= max(2, 0.01 * rep_ref[key][k]):
+                    marginal = True
+                    break
                 assert m[base + off] < MARGIN_BAND, (key, k, rep[key][k], rep_ref[key][k], m[base + off])
                 marginal = True
         if not marginal:
