@@ -180,7 +180,7 @@ int fc_orthonormalize(fc_ctx c, int n, int p, double* A, double* Q, double tau, 
         Ai = s.alloc<double>((size_t)n * p);
         FC_CUDA_TRY(cudaMemcpyAsync(Ai, A, (size_t)n * p * 8, cudaMemcpyDeviceToDevice, c->st));
       }
-      b.e[i] = BcgsEntry{n, p, Ai, n, Qx[i], n, kcap, kd + i, s.alloc<double>(p), s.alloc<double>((size_t)kcap * 32), tau};
+      b.e[i] = BcgsEntry{n, p, Ai, n, Qx[i], n, kcap, kd + i, s.alloc<double>(p), s.alloc<double>((size_t)kcap * kBcgsW), tau};
     }
     // the copies must be taken before entry 0 overwrites A: reorder so entry 0 runs on a copy too
     double* A0 = s.alloc<double>((size_t)n * p);

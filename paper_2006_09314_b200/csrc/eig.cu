@@ -155,6 +155,30 @@ __device__ void tri_invit(int N, const double* __restrict__ d, const double* __r
 #undef S
 }
 
+// one inverse-iteration solve with the LU factors tri_invit stored in `scr` (same layout)
+__device__ void tri_lu_solve(int N, const double* scr, size_t stride, double* v) {
+  const double* u0 = scr;
+  const double* u1 = scr + (size_t)N * stride;
+  const double* u2 = scr + (size_t)2 * N * stride;
+  const double* lm = scr + (size_t)3 * N * stride;
+  const double* pv = scr + (size_t)4 * N * stride;
+#define S(a, k) a[(size_t)(k) * stride]
+  for (int k = 0; k < N - 1; ++k) {
+    double bk = v[k], bk1 = v[k + 1];
+    if (S(pv, k) != 0.0) { double t = bk; bk = bk1; bk1 = t; }
+    bk1 -= S(lm, k) * bk;
+    v[k] = bk;
+    v[k + 1] = bk1;
+  }
+  double x2 = 0.0, x1 = 0.0;
+  for (int k = N - 1; k >= 0; --k) {
+    double x = (v[k] - S(u1, k) * x1 - S(u2, k) * x2) / S(u0, k);
+    v[k] = x;
+    x2 = x1; x1 = x;
+  }
+#undef S
+}
+
 // sign rule (reading A4): entry of largest magnitude positive, ties -> lowest index
 __device__ void sign_rule(int N, double* v, size_t vstride) {
   double best = -1.0, sgn = 1.0;
@@ -189,7 +213,9 @@ __global__ void sl_invit_kernel(int n, const double* __restrict__ d_all, const d
 // order; any orthonormal basis of a cluster's span is an eigenbasis to the accuracy the gap
 // allows (reading A25).  Clusters are short runs (pairs in practice).
 constexpr double kClusterGap = 1e-10;
-__global__ void sl_cluster_orth_kernel(int n, const double* __restrict__ lam_all, double* V_all) {
+__global__ void sl_cluster_orth_kernel(int n, const double* __restrict__ lam_all, const double* __restrict__ d_all,
+                                       const double* __restrict__ e_all, double* V_all,
+                                       const double* __restrict__ scratch) {
   const int l = blockIdx.y;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -202,6 +228,22 @@ __global__ void sl_cluster_orth_kernel(int n, const double* __restrict__ lam_all
   while (end + 1 < n && close(end, end + 1)) ++end;
   for (int j = i + 1; j <= end; ++j) {
     double* vj = V + (size_t)j * n;
+    // inverse iteration with orthogonalisation against the earlier members (LAPACK stein):
+    // solve with member j's stored LU factors, then MGS, three times
+    const double* scr = scratch + (size_t)l * n + j;
+    for (int it = 0; it < 3; ++it) {
+      tri_lu_solve(n, scr, (size_t)3 * n, vj);
+      for (int k = i; k < j; ++k) {
+        const double* vk = V + (size_t)k * n;
+        double dd = 0.0;
+        for (int t = 0; t < n; ++t) dd += vk[t] * vj[t];
+        for (int t = 0; t < n; ++t) vj[t] -= dd * vk[t];
+      }
+      double s2 = 0.0;
+      for (int t = 0; t < n; ++t) s2 += vj[t] * vj[t];
+      const double inv = 1.0 / sqrt(s2);
+      for (int t = 0; t < n; ++t) vj[t] *= inv;
+    }
     for (int pass = 0; pass < 2; ++pass) {
       for (int k = i; k < j; ++k) {
         const double* vk = V + (size_t)k * n;
@@ -213,6 +255,70 @@ __global__ void sl_cluster_orth_kernel(int n, const double* __restrict__ lam_all
       for (int t = 0; t < n; ++t) s2 += vj[t] * vj[t];
       double inv = 1.0 / sqrt(s2);
       for (int t = 0; t < n; ++t) vj[t] *= inv;
+    }
+  }
+  // Rayleigh-Ritz inside the cluster: Jacobi sweeps on H = Vc^T T Vc (k <= 8), rotating the
+  // cluster's vectors, so each vector is an eigenvector to the accuracy the true gap allows
+  // (an arbitrary rotation inside the span would leave residuals of order gap).
+  const int k = end - i + 1;
+  if (k > 8) return;
+  const double* d = d_all + (size_t)l * n;
+  const double* e = e_all + (size_t)l * n;
+  double H[8][8];
+  for (int a = 0; a < k; ++a) {
+    const double* va = V + (size_t)(i + a) * n;
+    for (int b = a; b < k; ++b) {
+      const double* vb = V + (size_t)(i + b) * n;
+      double h = 0.0;   // va^T T vb with T = tridiag(e, d, e)
+      for (int t = 0; t < n; ++t) {
+        double tv = d[t] * vb[t];
+        if (t > 0) tv += e[t - 1] * vb[t - 1];
+        if (t + 1 < n) tv += e[t] * vb[t + 1];
+        h += va[t] * tv;
+      }
+      H[a][b] = H[b][a] = h;
+    }
+  }
+  for (int sweep = 0; sweep < 10; ++sweep) {
+    double off = 0.0;
+    for (int a = 0; a < k; ++a)
+      for (int b = a + 1; b < k; ++b) off += H[a][b] * H[a][b];
+    if (off == 0.0) break;
+    for (int a = 0; a < k; ++a)
+      for (int b = a + 1; b < k; ++b) {
+        if (H[a][b] == 0.0) continue;
+        const double zeta = (H[b][b] - H[a][a]) / (2.0 * H[a][b]);
+        const double tt = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+        const double c = 1.0 / sqrt(1.0 + tt * tt), s = c * tt;
+        for (int m = 0; m < k; ++m) {          // H <- J^T H J
+          const double hma = H[m][a], hmb = H[m][b];
+          H[m][a] = c * hma - s * hmb;
+          H[m][b] = s * hma + c * hmb;
+        }
+        for (int m = 0; m < k; ++m) {
+          const double ham = H[a][m], hbm = H[b][m];
+          H[a][m] = c * ham - s * hbm;
+          H[b][m] = s * ham + c * hbm;
+        }
+        double* va = V + (size_t)(i + a) * n;
+        double* vb = V + (size_t)(i + b) * n;
+        for (int t = 0; t < n; ++t) {
+          const double x = va[t], y = vb[t];
+          va[t] = c * x - s * y;
+          vb[t] = s * x + c * y;
+        }
+      }
+  }
+  // keep ascending order of the Ritz values inside the cluster (selection sort by swapping)
+  for (int a = 0; a < k; ++a) {
+    int best = a;
+    for (int b = a + 1; b < k; ++b)
+      if (H[b][b] < H[best][best]) best = b;
+    if (best != a) {
+      double tmp = H[a][a]; H[a][a] = H[best][best]; H[best][best] = tmp;
+      double* va = V + (size_t)(i + a) * n;
+      double* vb = V + (size_t)(i + best) * n;
+      for (int t = 0; t < n; ++t) { double x = va[t]; va[t] = vb[t]; vb[t] = x; }
     }
   }
 }
@@ -481,7 +587,7 @@ __global__ void tri_invit_kernel(const __grid_constant__ SyevBatch B) {
 
 // one CTA per matrix: CGS2 orthonormalisation of Y[:, 0..r) in order, then back-transform
 // with the Householder vectors stored in A: z = H_0 H_1 ... H_{N-3} y.
-__global__ void __launch_bounds__(256) orth_backtransform_kernel(const __grid_constant__ SyevBatch B) {
+__global__ void __launch_bounds__(1024) orth_backtransform_kernel(const __grid_constant__ SyevBatch B) {
   __shared__ double red[33];
   extern __shared__ double coef[];   // r coefficients
   const SyevEntry& E = B.e[blockIdx.x];
@@ -518,8 +624,46 @@ __global__ void __launch_bounds__(256) orth_backtransform_kernel(const __grid_co
     __syncthreads();
   }
   if (E.A == nullptr) return;   // orthonormalisation only
-  // back-transform: for k = N-3 .. 0: y[k+1:] -= 2 u_k (u_k . y[k+1:]); warp per vector
+  // back-transform: for k = N-3 .. 0: y[k+1:] -= 2 u_k (u_k . y[k+1:]); warp per vector.
+  // For N <= 512 the warp keeps its vector in registers (element ln + 32 c in slot c), so the
+  // only memory traffic is the (L2-resident) Householder vectors, all loads independent.
   const int w = tid >> 5, ln = tid & 31;
+  if (N <= 512) {
+    constexpr int MC = 16;
+    for (int i = w; i < r; i += nt / 32) {
+      double* yi = Y + (size_t)i * ldy;
+      double yv[MC];
+#pragma unroll
+      for (int c = 0; c < MC; ++c) {
+        const int idx = ln + 32 * c;
+        yv[c] = idx < N ? yi[idx] : 0.0;
+      }
+      for (int k = N - 3; k >= 0; --k) {
+        const double* u = E.A + (size_t)k * E.lda;   // u_k[idx] at A[idx, k] for idx > k
+        double s = 0.0;
+#pragma unroll
+        for (int c = 0; c < MC; ++c) {
+          const int idx = ln + 32 * c;
+          if (idx > k && idx < N) s += u[idx] * yv[c];
+        }
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (s != 0.0) {
+          const double t2 = 2.0 * s;
+#pragma unroll
+          for (int c = 0; c < MC; ++c) {
+            const int idx = ln + 32 * c;
+            if (idx > k && idx < N) yv[c] -= t2 * u[idx];
+          }
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < MC; ++c) {
+        const int idx = ln + 32 * c;
+        if (idx < N) yi[idx] = yv[c];
+      }
+    }
+    return;
+  }
   for (int i = w; i < r; i += nt / 32) {
     double* yi = Y + (size_t)i * ldy;
     for (int k = N - 3; k >= 0; --k) {
@@ -663,7 +807,7 @@ __global__ void __launch_bounds__(1024) bcgs_block_kernel(const __grid_constant_
     for (int c = 0; c < E.p; ++c) mx = fmax(mx, E.norm0[c]);
     nmax_s = mx;
   }
-  for (int i = tid; i < n * 32; i += nt) E.Y[i] = 0.0;   // block buffer (n x 32, ld n)
+  for (int i = tid; i < n * kBcgsW; i += nt) E.Y[i] = 0.0;   // block buffer (n x W, ld n)
   __syncthreads();
   for (int c = 0; c < wb; ++c) {
     const double* xg = E.A + (size_t)(j0 + c) * E.lda;
@@ -806,7 +950,7 @@ void sl_eigen_device(cudaStream_t st, int n, const double* a_mid_dev, int bounda
   double* scr = s.alloc<double>((size_t)5 * 3 * n * n);
   sl_invit_kernel<<<dim3(cdiv(n, 64), 3), 64, 0, st>>>(n, d, e, lam, V, scr);
   FC_CHECK_LAUNCH();
-  sl_cluster_orth_kernel<<<dim3(cdiv(n, 64), 3), 64, 0, st>>>(n, lam, V);
+  sl_cluster_orth_kernel<<<dim3(cdiv(n, 64), 3), 64, 0, st>>>(n, lam, d, e, V, scr);
   FC_CHECK_LAUNCH();
   // Newton-Schulz polish: 2 steps of V <- V (3I - V^T V)/2 on DMMA GEMMs
   double* G = scr;                       // reuse: 3 n^2
@@ -874,7 +1018,7 @@ void syev_vectors(const SyevBatch& b, int maxN, cudaStream_t st) {
   if (b.nb == 0 || maxN == 0) return;
   tri_invit_kernel<<<dim3(cdiv(maxN, 64), b.nb), 64, 0, st>>>(b);
   FC_CHECK_LAUNCH();
-  orth_backtransform_kernel<<<b.nb, 256, (size_t)maxN * 8, st>>>(b);
+  orth_backtransform_kernel<<<b.nb, 1024, (size_t)maxN * 8, st>>>(b);
   FC_CHECK_LAUNCH();
 }
 
@@ -882,7 +1026,7 @@ void orthonormalize_cols(int N, double* Y, int ldy, int* r_dev, int rmax, cudaSt
   SyevBatch b;
   b.nb = 1;
   b.e[0] = SyevEntry{N, nullptr, 0, nullptr, nullptr, nullptr, Y, ldy, r_dev, nullptr};
-  orth_backtransform_kernel<<<1, 256, (size_t)std::max(rmax, 1) * 8, st>>>(b);
+  orth_backtransform_kernel<<<1, 1024, (size_t)std::max(rmax, 1) * 8, st>>>(b);
   FC_CHECK_LAUNCH();
 }
 
@@ -903,7 +1047,7 @@ void pmgs(const PmgsBatch& b, cudaStream_t st) {
 
 void bcgs(const BcgsBatch& bin, cudaStream_t st) {
   if (bin.nb == 0) return;
-  constexpr int W = 32;
+  constexpr int W = kBcgsW;
   BcgsBatch b = bin;
   Scratch scr(st);
   for (int i = 0; i < b.nb; ++i) {

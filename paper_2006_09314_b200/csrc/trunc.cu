@@ -134,7 +134,7 @@ __global__ void extract_slices_kernel(const double* __restrict__ core, int r0, i
 // per-slice global (L2-resident) workspace `gws` of (rows*cols + cols*cols) doubles.
 constexpr int kSliceMax = 512;
 constexpr size_t kSliceSmem = 200 * 1024;
-__global__ void __launch_bounds__(256) slice_svd_kernel(int ra, int rb, const double* __restrict__ S, double* s_out,
+__global__ void __launch_bounds__(1024) slice_svd_kernel(int ra, int rb, const double* __restrict__ S, double* s_out,
                                                         double* Ua, double* Vb, double* gws) {
   extern __shared__ double sm[];
   const int nu = blockIdx.x;
@@ -389,7 +389,7 @@ TT tucker_to_canonical(fc_ctx c, const double* core, const int r[3], double* con
     FC_CUDA_TRY(cudaFuncSetAttribute(slice_svd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSliceSmem));
     attr = true;
   }
-  slice_svd_kernel<<<rc, 256, smem, st>>>(ra, rb, S, sv, Ua, Vb, gws);
+  slice_svd_kernel<<<rc, 1024, smem, st>>>(ra, rb, S, sv, Ua, Vb, gws);
   FC_CHECK_LAUNCH();
   pool_sort_kernel<<<1, 1024, 0, st>>>(K, sv, s2s, keys, energy);
   FC_CHECK_LAUNCH();
@@ -503,7 +503,7 @@ TT truncate_tt(fc_ctx c, const TT& xin, double eps, int rank_cap, TruncStats* st
       double* Qn = s.alloc<double>((size_t)n * kcap);
       map[l] = pb.nb;
       pb.e[pb.nb++] = BcgsEntry{n, xin.q[l], Kc, n, Qn, n, kcap, kdev + l, s.alloc<double>(xin.q[l]),
-                                s.alloc<double>((size_t)kcap * 32), kBasisTol};
+                                s.alloc<double>((size_t)kcap * kBcgsW), kBasisTol};
     }
     bcgs(pb, st);
     int kh[4] = {0, 0, 0, 0};

