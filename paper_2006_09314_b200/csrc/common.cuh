@@ -99,6 +99,8 @@ struct GemmBatch {
   double* C; int ldc;
   const double* krU; int ldkr;
   const double* colscale;
+  // strides between the GemmArgs::rep repetitions of this entry (A, B, C, colscale, krU)
+  long long sA = 0, sB = 0, sC = 0, sS = 0, sK = 0;
 };
 // Generated A operand (transA = 0): A(m, k) = f((l1[m % n1] + l2[m / n1]) + l3[k]) with the
 // spectral function f of kind FC_F / FC_G / FC_POW_PLUS / FC_POW_MINUS [P:640-648, P:693].
@@ -117,6 +119,7 @@ struct GemmArgs {
   int splitk = 1;        // > 1: atomicAdd epilogue (beta must be 1, C pre-initialised)
   double alpha = 1.0, beta = 0.0;
   int nbatch = 0;
+  int rep = 1;           // every entry is repeated rep times with its strides (strided batch)
   GemmBatch b[kMaxBatch];
 };
 void gemm(const GemmArgs& a, cudaStream_t st);

@@ -34,8 +34,8 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
                : "d"(a), "d"(b));
 }
 
-__device__ __forceinline__ void load_tile_A(double* As, const GemmBatch& g, int transA, int m0, int k0,
-                                            int kend, int tid) {
+__device__ __forceinline__ void load_tile_A(double* As, const GemmBatch& g, const double* gA, int transA, int m0,
+                                            int k0, int kend, int tid) {
 #pragma unroll
   for (int i = 0; i < (BK * BM) / NT; ++i) {
     int idx = tid + i * NT;
@@ -44,9 +44,9 @@ __device__ __forceinline__ void load_tile_A(double* As, const GemmBatch& g, int 
     else         { kk = idx % BK; mm = idx / BK; }
     int m = m0 + mm, k = k0 + kk;
     bool ok = (m < g.M) && (k < kend);
-    const double* src = ok ? (transA ? g.A + (size_t)k + (size_t)m * g.lda
-                                     : g.A + (size_t)m + (size_t)k * g.lda)
-                           : g.A;
+    const double* src = ok ? (transA ? gA + (size_t)k + (size_t)m * g.lda
+                                     : gA + (size_t)m + (size_t)k * g.lda)
+                           : gA;
     cp_async8(As + kk * LDS + mm, src, ok);
   }
 }
@@ -76,8 +76,9 @@ __device__ __forceinline__ void gen_tile_A(double* As, const GemmBatch& g, const
   }
 }
 
-__device__ __forceinline__ void load_tile_B(double* Bs, double* Ks, const GemmBatch& g, int transB, int krR,
-                                            int n0, int k0, int kend, int tid) {
+__device__ __forceinline__ void load_tile_B(double* Bs, double* Ks, const GemmBatch& g, const double* gB,
+                                            const double* gK, int transB, int krR, int n0, int k0, int kend,
+                                            int tid) {
   if (krR > 0) {
     // Khatri-Rao operand: column c = k_F * R + j  ->  u_F[:, k_F] (.) W[:, j].  Both factors are
     // gathered by cp.async into two tiles; the product is formed at fragment-load time.
@@ -88,8 +89,8 @@ __device__ __forceinline__ void load_tile_B(double* Bs, double* Ks, const GemmBa
       int c = n0 + nn, k = k0 + kk;
       bool ok = (c < g.N) && (k < kend);
       int kf = ok ? c / krR : 0, j = ok ? c - kf * krR : 0;
-      cp_async8(Bs + kk * LDS + nn, ok ? g.B + (size_t)k + (size_t)j * g.ldb : g.B, ok);
-      cp_async8(Ks + kk * LDS + nn, ok ? g.krU + (size_t)k + (size_t)kf * g.ldkr : g.krU, ok);
+      cp_async8(Bs + kk * LDS + nn, ok ? gB + (size_t)k + (size_t)j * g.ldb : gB, ok);
+      cp_async8(Ks + kk * LDS + nn, ok ? gK + (size_t)k + (size_t)kf * g.ldkr : gK, ok);
     }
     return;
   }
@@ -101,9 +102,9 @@ __device__ __forceinline__ void load_tile_B(double* Bs, double* Ks, const GemmBa
     else         { nn = idx % BN; kk = idx / BN; }
     int c = n0 + nn, k = k0 + kk;
     bool ok = (c < g.N) && (k < kend);
-    const double* src = ok ? (transB ? g.B + (size_t)c + (size_t)k * g.ldb
-                                     : g.B + (size_t)k + (size_t)c * g.ldb)
-                           : g.B;
+    const double* src = ok ? (transB ? gB + (size_t)c + (size_t)k * g.ldb
+                                     : gB + (size_t)k + (size_t)c * g.ldb)
+                           : gB;
     cp_async8(Bs + kk * LDS + nn, src, ok);
   }
 }
@@ -118,7 +119,13 @@ __global__ void __launch_bounds__(NT) dgemm_dmma_kernel(const __grid_constant__ 
   const int bz = blockIdx.z;
   const int bi = bz / args.splitk;
   const int ks = bz - bi * args.splitk;
-  const GemmBatch& g = args.b[bi];
+  const int ei = bi / args.rep, ri = bi - ei * args.rep;
+  const GemmBatch& g = args.b[ei];
+  const double* gA = g.A + (size_t)ri * g.sA;
+  const double* gB = g.B + (size_t)ri * g.sB;
+  const double* gK = g.krU + (size_t)ri * g.sK;
+  double* gC = g.C + (size_t)ri * g.sC;
+  const double* gS = g.colscale ? g.colscale + (size_t)ri * g.sS : nullptr;
   const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
   if (m0 >= g.M || n0 >= g.N) return;
 
@@ -142,8 +149,8 @@ __global__ void __launch_bounds__(NT) dgemm_dmma_kernel(const __grid_constant__ 
   for (int s = 0; s < STAGES - 1; ++s) {
     if (s < nk) {
       if (GEN) gen_tile_A(As + s * STAGE_ELEMS, g, args.gen, m0, kbeg + s * BK, kend, tid);
-      else load_tile_A(As + s * STAGE_ELEMS, g, args.transA, m0, kbeg + s * BK, kend, tid);
-      load_tile_B(Bs + s * STAGE_ELEMS, Ks + s * STAGE_ELEMS, g, args.transB, KR ? args.krR : 0, n0,
+      else load_tile_A(As + s * STAGE_ELEMS, g, gA, args.transA, m0, kbeg + s * BK, kend, tid);
+      load_tile_B(Bs + s * STAGE_ELEMS, Ks + s * STAGE_ELEMS, g, gB, gK, args.transB, KR ? args.krR : 0, n0,
                   kbeg + s * BK, kend, tid);
     }
     cp_async_commit();
@@ -159,8 +166,8 @@ __global__ void __launch_bounds__(NT) dgemm_dmma_kernel(const __grid_constant__ 
       if (nt < nk) {
         int sl = nt % STAGES;
         if (GEN) gen_tile_A(As + sl * STAGE_ELEMS, g, args.gen, m0, kbeg + nt * BK, kend, tid);
-        else load_tile_A(As + sl * STAGE_ELEMS, g, args.transA, m0, kbeg + nt * BK, kend, tid);
-        load_tile_B(Bs + sl * STAGE_ELEMS, Ks + sl * STAGE_ELEMS, g, args.transB, KR ? args.krR : 0, n0,
+        else load_tile_A(As + sl * STAGE_ELEMS, g, gA, args.transA, m0, kbeg + nt * BK, kend, tid);
+        load_tile_B(Bs + sl * STAGE_ELEMS, Ks + sl * STAGE_ELEMS, g, gB, gK, args.transB, KR ? args.krR : 0, n0,
                     kbeg + nt * BK, kend, tid);
       }
       cp_async_commit();
@@ -193,13 +200,13 @@ __global__ void __launch_bounds__(NT) dgemm_dmma_kernel(const __grid_constant__ 
     for (int e = 0; e < 2; ++e) {
       int c = n0 + wn + j * 8 + 2 * fc4 + e;
       if (c >= g.N) continue;
-      double cs = g.colscale ? g.colscale[c] : 1.0;
+      double cs = gS ? gS[c] : 1.0;
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         int r = m0 + wm + i * 8 + fr;
         if (r >= g.M) continue;
         double v = args.alpha * cs * acc[i][j][e];
-        double* dst = g.C + (size_t)r + (size_t)c * g.ldc;
+        double* dst = gC + (size_t)r + (size_t)c * g.ldc;
         if (args.splitk > 1) atomicAdd(dst, v);
         else if (args.beta == 0.0) *dst = v;
         else *dst = v + args.beta * *dst;
@@ -272,8 +279,8 @@ __device__ __forceinline__ void load_op(double* T, const double* base, int ld, i
 }
 
 // Khatri-Rao operand tile (K contiguous): column c -> W[:, c % R] and U[:, c / R]
-__device__ __forceinline__ void load_kr(double* T, double* TK, const GemmBatch& g, int krR, int n0, int k0, int kend,
-                                        int tid) {
+__device__ __forceinline__ void load_kr(double* T, double* TK, const GemmBatch& g, const double* gB, const double* gK,
+                                        int krR, int n0, int k0, int kend, int tid) {
 #pragma unroll
   for (int i = 0; i < 2048 / NT; ++i) {
     const int idx = tid + i * NT;
@@ -281,8 +288,8 @@ __device__ __forceinline__ void load_kr(double* T, double* TK, const GemmBatch& 
     const int c = n0 + rr, k = k0 + kk;
     const bool ok = (c < g.N) && (k < kend);
     const int kf = ok ? c / krR : 0, j = ok ? c - kf * krR : 0;
-    cp_async8(T + rr * LDM + kk, ok ? g.B + (size_t)k + (size_t)j * g.ldb : g.B, ok);
-    cp_async8(TK + rr * LDM + kk, ok ? g.krU + (size_t)k + (size_t)kf * g.ldkr : g.krU, ok);
+    cp_async8(T + rr * LDM + kk, ok ? gB + (size_t)k + (size_t)j * g.ldb : gB, ok);
+    cp_async8(TK + rr * LDM + kk, ok ? gK + (size_t)k + (size_t)kf * g.ldkr : gK, ok);
   }
 }
 
@@ -294,7 +301,11 @@ __global__ void __launch_bounds__(NT, 1) dgemm_big_kernel(const __grid_constant_
   double* Ks = smem + 2 * STAGES * TILE;
   const int bz = blockIdx.z;
   const int bi = bz / args.splitk, ks = bz - bi * args.splitk;
-  const GemmBatch& g = args.b[bi];
+  const int ei = bi / args.rep, ri = bi - ei * args.rep;
+  const GemmBatch& g = args.b[ei];
+  const double* gA = g.A + (size_t)ri * g.sA;
+  const double* gB = g.B + (size_t)ri * g.sB;
+  const double* gK = g.krU + (size_t)ri * g.sK;
   const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
   if (m0 >= g.M || n0 >= g.N) return;
   const int kchunk = ((g.K + args.splitk - 1) / args.splitk + BK - 1) / BK * BK;
@@ -304,8 +315,8 @@ __global__ void __launch_bounds__(NT, 1) dgemm_big_kernel(const __grid_constant_
   const int wm = (warp & 3) * 32, wn = (warp >> 2) * 32;
   const int fr = lane >> 2, fc4 = lane & 3;
   // 16-byte transfers need an even leading dimension and 16-byte aligned base pointers
-  const bool vecA = ((g.lda & 1) == 0) && (((uintptr_t)g.A & 15) == 0);
-  const bool vecB = ((g.ldb & 1) == 0) && (((uintptr_t)g.B & 15) == 0);
+  const bool vecA = ((g.lda & 1) == 0) && (((uintptr_t)gA & 15) == 0);
+  const bool vecB = ((g.ldb & 1) == 0) && (((uintptr_t)gB & 15) == 0);
   constexpr bool AK = TA == 1;    // A contiguous along k
   constexpr bool BKc = TB == 0;   // B contiguous along k
 
@@ -317,9 +328,9 @@ __global__ void __launch_bounds__(NT, 1) dgemm_big_kernel(const __grid_constant_
 
   auto issue = [&](int s, int kt) {
     const int k0 = kbeg + kt * BK;
-    load_op<AK>(As + s * TILE, g.A, g.lda, m0, g.M, k0, kend, tid, vecA);
-    if (KR) load_kr(Bs + s * TILE, Ks + s * TILE, g, args.krR, n0, k0, kend, tid);
-    else load_op<BKc>(Bs + s * TILE, g.B, g.ldb, n0, g.N, k0, kend, tid, vecB);
+    load_op<AK>(As + s * TILE, gA, g.lda, m0, g.M, k0, kend, tid, vecA);
+    if (KR) load_kr(Bs + s * TILE, Ks + s * TILE, g, gB, gK, args.krR, n0, k0, kend, tid);
+    else load_op<BKc>(Bs + s * TILE, gB, g.ldb, n0, g.N, k0, kend, tid, vecB);
   };
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
@@ -369,13 +380,13 @@ __global__ void __launch_bounds__(NT, 1) dgemm_big_kernel(const __grid_constant_
     for (int e = 0; e < 2; ++e) {
       const int c = n0 + wn + j * 8 + 2 * fc4 + e;
       if (c >= g.N) continue;
-      const double cs = g.colscale ? g.colscale[c] : 1.0;
+      const double cs = g.colscale ? g.colscale[c + (size_t)ri * g.sS] : 1.0;
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const int r = m0 + wm + i * 8 + fr;
         if (r >= g.M) continue;
         const double v = args.alpha * cs * acc[i][j][e];
-        double* dst = g.C + (size_t)r + (size_t)c * g.ldc;
+        double* dst = g.C + (size_t)ri * g.sC + (size_t)r + (size_t)c * g.ldc;
         if (args.splitk > 1) atomicAdd(dst, v);
         else if (args.beta == 0.0) *dst = v;
         else *dst = v + args.beta * *dst;
@@ -449,7 +460,7 @@ void gemm(const GemmArgs& a, cudaStream_t st) {
     }
   }
   double f = 0;
-  for (int i = 0; i < a.nbatch; ++i) f += 2.0 * a.b[i].M * (double)a.b[i].N * a.b[i].K;
+  for (int i = 0; i < a.nbatch; ++i) f += 2.0 * a.rep * a.b[i].M * (double)a.b[i].N * a.b[i].K;
   FC_CUDA_TRY(cudaEventRecord(P.ev[2 * P.used], st));
   gemm_dispatch(a, st);
   FC_CUDA_TRY(cudaEventRecord(P.ev[2 * P.used + 1], st));
@@ -468,11 +479,11 @@ static void gemm_dispatch(const GemmArgs& a, cudaStream_t st) {
   long long work = 0;
   int minK = INT32_MAX;
   for (int i = 0; i < a.nbatch; ++i) {
-    work += (long long)a.b[i].M * a.b[i].N * a.b[i].K;
+    work += (long long)a.rep * a.b[i].M * a.b[i].N * a.b[i].K;
     minK = std::min(minK, a.b[i].K);
   }
   if (a.gen.kind < 0 && maxM >= 256 && maxN >= 256 && minK >= 64 && work >= (1LL << 27)) {
-    dim3 grid(cdiv(maxM, big::BM), cdiv(maxN, big::BN), a.nbatch * a.splitk);
+    dim3 grid(cdiv(maxM, big::BM), cdiv(maxN, big::BN), a.nbatch * a.rep * a.splitk);
     require(grid.y <= 65535 && grid.z <= 65535, FC_ERR_INVALID_ARG, "gemm grid too large");
     if (a.krR > 0) big::launch_big<0, 0, true>(a, grid, st);
     else if (!a.transA && !a.transB) big::launch_big<0, 0, false>(a, grid, st);
@@ -490,7 +501,7 @@ static void gemm_dispatch(const GemmArgs& a, cudaStream_t st) {
     FC_CUDA_TRY(cudaFuncSetAttribute(dgemm_dmma_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2));
     attr = true;
   }
-  dim3 grid(cdiv(maxM, BM), cdiv(maxN, BN), a.nbatch * a.splitk);
+  dim3 grid(cdiv(maxM, BM), cdiv(maxN, BN), a.nbatch * a.rep * a.splitk);
   require(grid.y <= 65535 && grid.z <= 65535, FC_ERR_INVALID_ARG, "gemm grid too large");
   if (a.gen.kind >= 0) dgemm_dmma_kernel<false, true><<<grid, NT, smem2, st>>>(a);
   else if (a.krR > 0) dgemm_dmma_kernel<true, false><<<grid, NT, smem3, st>>>(a);

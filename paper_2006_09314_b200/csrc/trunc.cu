@@ -42,6 +42,49 @@ __global__ void term_norms_kernel(int R, TermArgs a) {
   if (ln == 0) a.n2[l][t] = fmax(s, 0.0);
 }
 
+// Khatri-Rao structured input (f1): term T = kk*Rx + j has mode coefficient Rm_kk cx_j, so
+// n2[T] = cx_j^T (Rm_kk^T Rm_kk cx_j) = sum_a Cx[a, j] * P[a, T] with P[:, T] = Gm_kk cx_j.
+struct StructNormArgs {
+  const double* Cx[3];
+  const double* P[3];
+  int t[3];
+  double* n2[3];
+};
+__global__ void struct_norms_kernel(int R, int Rx, StructNormArgs a) {
+  const int l = blockIdx.y;
+  const int T = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  const int ln = threadIdx.x & 31;
+  if (T >= R) return;
+  const int t = a.t[l], j = T % Rx;
+  const double* c = a.Cx[l] + (size_t)j * t;
+  const double* p = a.P[l] + (size_t)T * t;
+  double s = 0.0;
+  for (int k = ln; k < t; k += 32) s += c[k] * p[k];
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+  if (ln == 0) a.n2[l][T] = fmax(s, 0.0);
+}
+
+// W[:, T] = Cx[:, T % Rx] * d[T]   (t x R): the structured side-matrix coefficients C_x D
+__global__ void struct_scale_kernel(int t, int R, int Rx, const double* __restrict__ Cx, const double* __restrict__ d,
+                                    double* W) {
+  const long long tot = (long long)t * R;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < tot;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int a = (int)(idx % t);
+    const int T = (int)(idx / t);
+    W[idx] = Cx[a + (size_t)(T % Rx) * t] * d[T];
+  }
+}
+
+// out[:, c] = in[:, c] * d[c]   (rows x cols, ld rows)
+__global__ void scale_cols_kernel(int rows, int cols, const double* __restrict__ in, const double* __restrict__ d,
+                                  double* out) {
+  const long long tot = (long long)rows * cols;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < tot;
+       idx += (long long)gridDim.x * blockDim.x)
+    out[idx] = in[idx] * d[idx / rows];
+}
+
 // xi_t, d_l[t] = xi_t / n_l[t], inv_n_l[t] = 1/n_l[t], energy += xi^2 (single block reduction)
 __global__ void term_weights_kernel(int R, const double* __restrict__ w, const double* n2a, const double* n2b,
                                     const double* n2c, double* xi, double* da, double* db, double* dc,
@@ -547,24 +590,18 @@ TT truncate_tt(fc_ctx c, const TT& xin, double eps, int rank_cap, TruncStats* st
       double* Rm = s.zeros<double>((size_t)k * xin.q[l]);
       dgemm(st, 1, 0, k, xin.q[l], n, 1.0, Qo[l], n, xin.Q[l], n, 1.0, Rm, k,
             std::max(1, std::min(cdiv(n, 256), 16)));
-      Co[l] = s.alloc<double>((size_t)k * R);
       if (!ss) {
+        Co[l] = s.alloc<double>((size_t)k * R);
         dgemm(st, 0, 0, k, R, xin.q[l], 1.0, Rm, k, xin.C[l], xin.q[l], 0.0, Co[l], k);
       } else {
         // structured Hadamard: K columns a*t + b; Rm viewed (k t) x s times E (s x r) gives
         // RmE = [Rm_1 | ... | Rm_r], Rm_kk = sum_a E[a,kk] Rm[:, a*t:(a+1)*t] (k x t);
-        // term (kk, j) has coefficient Rm_kk C_x[:, j]  ->  Co[:, kk*Rx + j]
-        const int t = ss->t[l], sl = ss->s[l], r = ss->r, Rx = ss->Rx;
+        // term (kk, j) has coefficient Rm_kk C_x[:, j] (never formed: norms and the side-matrix
+        // Gram are contracted through the t x t per-term Grams below)
+        const int t = ss->t[l], sl = ss->s[l], r = ss->r;
+        Co[l] = nullptr;
         RmE[l] = s.alloc<double>((size_t)k * t * r);
         dgemm(st, 0, 0, k * t, r, sl, 1.0, Rm, k * t, ss->E[l], sl, 0.0, RmE[l], k * t);
-        for (int k0 = 0; k0 < r; k0 += kMaxBatch) {
-          GemmArgs g;
-          g.nbatch = std::min(kMaxBatch, r - k0);
-          for (int b = 0; b < g.nbatch; ++b)
-            g.b[b] = GemmBatch{k, Rx, t, RmE[l] + (size_t)(k0 + b) * k * t, k, ss->Cx[l], t,
-                               Co[l] + (size_t)(k0 + b) * k * Rx, k, nullptr, 0, nullptr};
-          gemm(g, st);
-        }
       }
     }
   }
@@ -583,29 +620,83 @@ TT truncate_tt(fc_ctx c, const TT& xin, double eps, int rank_cap, TruncStats* st
   }
   double* xi = s.alloc<double>(R);
   double* energy = s.alloc<double>(4);
-  TermArgs ta;
-  for (int l = 0; l < 3; ++l) {
-    ta.C[l] = Co[l]; ta.QC[l] = Co[l]; ta.q[l] = q[l]; ta.n2[l] = n2[l];
+  if (!ss) {
+    TermArgs ta;
+    for (int l = 0; l < 3; ++l) {
+      ta.C[l] = Co[l]; ta.QC[l] = Co[l]; ta.q[l] = q[l]; ta.n2[l] = n2[l];
+    }
+    term_norms_kernel<<<dim3(cdiv(R, 8), 3), 256, 0, st>>>(R, ta);
+    FC_CHECK_LAUNCH();
+  } else {
+    // n2[kk*Rx + j] = cx_j^T Gm_kk cx_j with Gm_kk = Rm_kk^T Rm_kk (t x t), P_kk = Gm_kk Cx
+    const int r = ss->r, Rx = ss->Rx;
+    GemmArgs gg, gp;
+    gg.transA = 1;
+    gg.nbatch = gp.nbatch = 3;
+    gg.rep = gp.rep = r;
+    StructNormArgs na;
+    for (int l = 0; l < 3; ++l) {
+      const int t = ss->t[l], k = q[l];
+      double* Gm = s.alloc<double>((size_t)t * t * r);
+      double* P = s.alloc<double>((size_t)t * R);
+      gg.b[l] = GemmBatch{t, t, k, RmE[l], k, RmE[l], k, Gm, t, nullptr, 0, nullptr};
+      gg.b[l].sA = gg.b[l].sB = (long long)k * t;
+      gg.b[l].sC = (long long)t * t;
+      gp.b[l] = GemmBatch{t, Rx, t, Gm, t, ss->Cx[l], t, P, t, nullptr, 0, nullptr};
+      gp.b[l].sA = (long long)t * t;
+      gp.b[l].sC = (long long)t * Rx;
+      na.Cx[l] = ss->Cx[l]; na.P[l] = P; na.t[l] = t; na.n2[l] = n2[l];
+    }
+    gemm(gg, st);
+    gemm(gp, st);
+    struct_norms_kernel<<<dim3(cdiv(R, 8), 3), 256, 0, st>>>(R, Rx, na);
+    FC_CHECK_LAUNCH();
   }
-  term_norms_kernel<<<dim3(cdiv(R, 8), 3), 256, 0, st>>>(R, ta);
-  FC_CHECK_LAUNCH();
   term_weights_kernel<<<1, 1024, 0, st>>>(R, xin.w, n2[0], n2[1], n2[2], xi, dl[0], dl[1], dl[2], inv[0], inv[1],
                                           inv[2], energy);
   FC_CHECK_LAUNCH();
   // ---- 3. side matrix in the basis: B_l = C_l D_l (q x R); M_l = B_l B_l^T -------------
   double* Bm[3];
   double* M[3];
-  {
-    GemmArgs g;
-    g.nbatch = 3;
+  if (ss) {
+    // M_l = sum_kk Rm_kk H_kk Rm_kk^T,  H_kk = W_kk W_kk^T,  W_kk = Cx diag(d_l[kk*Rx + .])
+    // (t x t per spectral term): G_kk = Rm_kk H_kk, then M = [G_1 .. G_r] [Rm_1 .. Rm_r]^T
+    const int r = ss->r, Rx = ss->Rx;
+    GemmArgs gh, gq, m;
+    gh.transB = 1;
+    m.transB = 1;
+    gh.nbatch = gq.nbatch = m.nbatch = 3;
+    gh.rep = gq.rep = r;
+    int tiles = 0, minkd = INT32_MAX;
+    for (int l = 0; l < 3; ++l) {
+      const int t = ss->t[l], k = q[l];
+      double* W = s.alloc<double>((size_t)t * R);
+      struct_scale_kernel<<<blocks_for((long long)t * R), 256, 0, st>>>(t, R, Rx, ss->Cx[l], dl[l], W);
+      FC_CHECK_LAUNCH();
+      double* H = s.alloc<double>((size_t)t * t * r);
+      double* G = s.alloc<double>((size_t)k * t * r);
+      gh.b[l] = GemmBatch{t, t, Rx, W, t, W, t, H, t, nullptr, 0, nullptr};
+      gh.b[l].sA = gh.b[l].sB = (long long)t * Rx;
+      gh.b[l].sC = (long long)t * t;
+      gq.b[l] = GemmBatch{k, t, t, RmE[l], k, H, t, G, k, nullptr, 0, nullptr};
+      gq.b[l].sA = gq.b[l].sC = (long long)k * t;
+      gq.b[l].sB = (long long)t * t;
+      M[l] = s.zeros<double>((size_t)k * k);
+      m.b[l] = GemmBatch{k, k, t * r, G, k, RmE[l], k, M[l], k, nullptr, 0, nullptr};
+      tiles += cdiv(k, 64) * cdiv(k, 64);
+      minkd = std::min(minkd, t * r);
+    }
+    gemm(gh, st);
+    gemm(gq, st);
+    m.beta = 1.0;
+    m.splitk = std::max(1, std::min(cdiv(minkd, 128), std::max(1, 148 * 3 / std::max(tiles, 1))));
+    gemm(m, st);
+  } else {
     for (int l = 0; l < 3; ++l) {
       Bm[l] = s.alloc<double>((size_t)q[l] * R);
-      double* I = s.alloc<double>((size_t)q[l] * q[l]);
-      identity_kernel<<<blocks_for((long long)q[l] * q[l]), 256, 0, st>>>(q[l], I);
+      scale_cols_kernel<<<blocks_for((long long)q[l] * R), 256, 0, st>>>(q[l], R, Co[l], dl[l], Bm[l]);
       FC_CHECK_LAUNCH();
-      g.b[l] = GemmBatch{q[l], R, q[l], I, q[l], Co[l], q[l], Bm[l], q[l], nullptr, 0, dl[l]};
     }
-    gemm(g, st);
     GemmArgs m;
     m.transB = 1;
     m.beta = 1.0;
