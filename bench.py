@@ -58,7 +58,7 @@ class Clocks:
         try:
             self.f = open(self.path, "w")
             self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                          "--format=csv,noheader,nounits", "-lms", os.environ.get("FC_BENCH_CLOCK_MS", "200")],
                                          stdout=self.f, stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
@@ -274,6 +274,9 @@ def main():
                    "l2": "flushed (512 MiB write) between timed steps", "parallelism": "replicas",
                    "setup_ms": setup_ms},
         "time_to_eps_ms": float(np.median(times)),
+        "step_ms": [round(t, 2) for t in times],
+        "slowest_step_iter_ms": [round(t, 1) for t in reps[int(np.argmax(times))]["t_iter_ms"]] if reps else [],
+        "fastest_step_iter_ms": [round(t, 1) for t in reps[int(np.argmin(times))]["t_iter_ms"]] if reps else [],
         "iters_per_solve": reps[-1]["iters"] if reps else 0,
         "final_rel_res": reps[-1]["rel_res"][-1] if reps else None,
         "ranks_last_iter": {k: reps[-1][k][-1] for k in ("rank_X", "rank_R", "rank_S", "rank_Z", "rank_P")} if reps else {},

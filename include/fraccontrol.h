@@ -177,6 +177,13 @@ int fc_last_kernel_stats(fc_ctx ctx, double* ms, double* flops, double* bytes, i
  * to tau times their norm): A (device, n x p, column-major, overwritten), Q (device, n x
  * min(n,p)); *k_host receives the basis size. */
 int fc_orthonormalize(fc_ctx ctx, int n, int p, double* A, double* Q, double tau, int* k_host);
+/* Batched symmetric eigensolver of the truncation (S11: the side-matrix Gram eigenproblem),
+ * exposed for testing: nb <= 8 matrices; host arrays of length nb.  Entry i: A[i] (device,
+ * N[i] x N[i] symmetric, column-major, leading dimension lda[i], overwritten), lam[i] (device,
+ * N[i]: eigenvalues in DESCENDING order), Y[i] (device, N[i] x r[i], ld ldy[i]: orthonormal
+ * eigenvectors of the r[i] largest eigenvalues, 0 <= r[i] <= N[i]).  1 <= N[i] <= 1500. */
+int fc_syev(fc_ctx ctx, int nb, const int* N, double* const* A, const int* lda, double* const* lam,
+            double* const* Y, const int* ldy, const int* r);
 /* Opt-in accounting of every DMMA GEMM launch (events around each launch; for the bench's
  * roofline line).  enable=1 starts recording; enable=0 stops and returns the summed device
  * time (ms), the summed algorithmic flops (2 M N K per batch entry) and the launch count. */

@@ -68,7 +68,7 @@ ENTRY_POINTS = ["fc_create", "fc_destroy", "fc_last_error", "fc_set_stream", "sl
                 "sl_set_eigen", "op_get_spectral_cp", "op_set_spectral_cp", "op_spectral_rank",
                 "fracop_apply", "precond_apply", "cp_dot", "cp_axpy", "cp_truncate", "pcg_solve",
                 "fc_dgemm", "fc_last_kernel_stats", "fc_kernel_launches", "fracop_apply_truncate", "fc_orthonormalize",
-                "fc_profile_gemm"]
+                "fc_profile_gemm", "fc_syev"]
 
 
 def load_library(path: str = LIB_PATH) -> C.CDLL:
@@ -96,6 +96,8 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "fc_kernel_launches": ([C.POINTER(C.c_longlong)], I),
         "fc_orthonormalize": ([P, I, I, P, P, D, C.POINTER(I)], I),
         "fc_profile_gemm": ([P, I, C.POINTER(D), C.POINTER(D), C.POINTER(C.c_longlong)], I),
+        "fc_syev": ([P, I, C.POINTER(I), C.POINTER(P), C.POINTER(I), C.POINTER(P), C.POINTER(P), C.POINTER(I),
+                     C.POINTER(I)], I),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -305,6 +307,21 @@ class Context:
         self._check(self.lib.fc_orthonormalize(self.h, n, p, A.data_ptr(), Q.data_ptr(), C.c_double(tau),
                                                C.byref(k)))
         return Q[:k.value]
+
+    def syev(self, mats, rs):
+        """Batched symmetric eigensolver (fc_syev).  mats: list of symmetric torch (N, N) float64
+        CUDA tensors (overwritten); rs: wanted leading eigenvectors per matrix.  Returns
+        [(lam descending (N,), Y (r, N) row-major == N x r column-major)]."""
+        import torch
+        nb = len(mats)
+        Ns = [m.shape[0] for m in mats]
+        lams = [torch.zeros(N, dtype=torch.float64, device=m.device) for N, m in zip(Ns, mats)]
+        Ys = [torch.zeros(max(r, 1), N, dtype=torch.float64, device=m.device) for N, r, m in zip(Ns, rs, mats)]
+        IA, PA = C.c_int * nb, C.c_void_p * nb
+        self._check(self.lib.fc_syev(self.h, nb, IA(*Ns), PA(*[m.data_ptr() for m in mats]), IA(*Ns),
+                                     PA(*[x.data_ptr() for x in lams]), PA(*[y.data_ptr() for y in Ys]),
+                                     IA(*Ns), IA(*rs)))
+        return [(lam, Y[:r]) for lam, Y, r in zip(lams, Ys, rs)]
 
     def dgemm(self, transA, transB, M, N, K, alpha, A, lda, B, ldb, beta, Cm, ldc):
         self._check(self.lib.fc_dgemm(self.h, transA, transB, M, N, K, alpha, A.data_ptr(), lda,

@@ -205,6 +205,31 @@ int fc_orthonormalize(fc_ctx c, int n, int p, double* A, double* Q, double tau, 
   });
 }
 
+int fc_syev(fc_ctx c, int nb, const int* N, double* const* A, const int* lda, double* const* lam, double* const* Y,
+            const int* ldy, const int* r) {
+  return guard(c, [&]() {
+    require(nb >= 1 && nb <= kMaxSyev && N && A && lda && lam && Y && ldy && r, FC_ERR_INVALID_ARG, "fc_syev args");
+    Scratch s(c->st);
+    SyevBatch b;
+    b.nb = nb;
+    int* rd = s.alloc<int>(nb);
+    FC_CUDA_TRY(cudaMemcpyAsync(rd, r, nb * sizeof(int), cudaMemcpyHostToDevice, c->st));
+    int maxN = 0;
+    for (int i = 0; i < nb; ++i) {
+      require(N[i] >= 1 && N[i] <= 1500 && lda[i] >= N[i] && ldy[i] >= N[i] && r[i] >= 0 && r[i] <= N[i] && A[i] &&
+                  lam[i] && (Y[i] || r[i] == 0),
+              FC_ERR_INVALID_ARG, "fc_syev entry");
+      b.e[i] = SyevEntry{N[i], A[i], lda[i], s.alloc<double>(N[i]), s.alloc<double>(N[i]), lam[i], Y[i], ldy[i],
+                         rd + i, s.alloc<double>((size_t)5 * N[i] * N[i])};
+      maxN = std::max(maxN, N[i]);
+    }
+    syev_values(b, c->st);
+    syev_vectors(b, maxN, c->st);
+    FC_CUDA_TRY(cudaStreamSynchronize(c->st));
+    return FC_OK;
+  });
+}
+
 int fc_profile_gemm(fc_ctx c, int enable, double* ms, double* flops, long long* launches) {
   return guard(c, [&]() {
     gemm_profile(enable != 0, ms, flops, launches);
@@ -231,6 +256,22 @@ int fc_create(fc_ctx* ctx, void* cuda_stream) {
     FC_CUDA_TRY(cudaDeviceGetDefaultMemPool(&pool, c->dev));
     uint64_t thr = UINT64_MAX;
     FC_CUDA_TRY(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    // Pre-grow the pool once (the memory stays reserved): growing it inside a solve maps new
+    // physical memory, a stall of hundreds of ms when a large scratch request fits no free chunk.
+    // Default 16 GB (capped at half the free memory), FC_POOL_RESERVE_MB overrides (0 = off).
+    uint64_t cur = 0;
+    FC_CUDA_TRY(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &cur));
+    size_t fr = 0, tot = 0;
+    FC_CUDA_TRY(cudaMemGetInfo(&fr, &tot));
+    const char* env = getenv("FC_POOL_RESERVE_MB");
+    size_t want = env ? (size_t)atoll(env) << 20 : (size_t)16 << 30;
+    want = std::min(want, fr / 2);
+    if (want > cur) {
+      void* p = nullptr;
+      FC_CUDA_TRY(cudaMallocAsync(&p, want, c->st));
+      FC_CUDA_TRY(cudaFreeAsync(p, c->st));
+      FC_CUDA_TRY(cudaStreamSynchronize(c->st));
+    }
     return FC_OK;
   });
   if (rc != FC_OK) {

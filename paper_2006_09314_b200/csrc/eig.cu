@@ -9,6 +9,8 @@
 //     (one CTA per matrix), bisection for all eigenvalues (thread per eigenvalue), inverse
 //     iteration for the leading r vectors, CGS2 re-orthonormalisation, back-transformation.
 #include <cfloat>
+#include <cstdlib>
+#include <cooperative_groups.h>
 #include "eig.cuh"
 
 namespace fc {
@@ -366,13 +368,13 @@ __device__ double block_sum(double v, double* red) {
 //              A[i,j] u_j to p_i (i >= j) and sum_{i>j} A[i,j] u_i to p_j, into per-warp
 //              partial vectors that are summed afterwards;
 //   A22 -= 2 (u q^T + q u^T) on the lower triangle (warp per column).
-__global__ void __launch_bounds__(kTriThreads) tridiag_kernel(const __grid_constant__ SyevBatch B) {
+__global__ void __launch_bounds__(kTriThreads) tridiag_kernel(const __grid_constant__ SyevBatch B, int minN) {
   extern __shared__ double sm[];
   __shared__ double red[33];
   __shared__ double alpha_s;
   const SyevEntry& E = B.e[blockIdx.x];
   const int N = E.N;
-  if (N <= kPackedMaxN) return;          // handled by tridiag_packed_kernel
+  if (N <= minN) return;                 // handled by the packed / cluster kernels
   constexpr int NW = kTriThreads / 32;
   const bool use_sm = false;
   double* M = use_sm ? sm : E.A;
@@ -530,6 +532,194 @@ __global__ void __launch_bounds__(1024) tridiag_packed_kernel(const __grid_const
   if (tid == 0 && N >= 2) E.e[N - 2] = L[off(N - 2) + 1];
   for (int k = warp; k + 2 < N; k += NW)
     for (int i = ln; i < N - k - 1; i += 32) E.A[(k + 1 + i) + (size_t)k * E.lda] = L[off(k) + 1 + i];
+}
+
+// Same Householder tridiagonalisation on a thread-block cluster of CS CTAs (one cluster per
+// matrix): column j of the packed lower triangle lives in the shared memory of CTA j % CS.
+// Per step s (pivot column s, trailing block rows/cols >= s+1):
+//   every CTA holds the pivot column and computes the Householder vector u redundantly (same
+//   code, same data -> bit-identical in every CTA; no broadcast);
+//   partial matvec Y_c = A22[:, own cols] u (thread per row, lower part) + the own-column dots
+//   (warp per column, upper part by symmetry);
+//   cluster barrier; reduce-scatter: CTA c sums the CS partials of its index slice through DSMEM
+//   and fetches its slice of the (not yet updated) next pivot column from that column's owner;
+//   cluster barrier; all-gather of p and of the next pivot column; q = p - (u^T p) u; the next
+//   pivot column is updated and its Householder vector formed (redundantly); the rank-2 update
+//   of the own columns is fused with the next step's partial matvec.
+// Two cluster barriers per step; the owner of a slice serves only that slice (DSMEM reads are
+// paid by the owner's shared-memory port).
+constexpr int kCl8MaxN = 600;    // packed own columns + 5 N vectors fit 220 KB with 8 CTAs
+constexpr int kCl16MaxN = 840;   // ... with 16 CTAs (non-portable cluster size)
+
+template <int CS>
+__host__ __device__ constexpr bool cluster_class(int N) {
+  return CS == 8 ? (N > kPackedMaxN && N <= kCl8MaxN) : (N > kCl8MaxN && N <= kCl16MaxN);
+}
+
+template <int CS>
+__host__ __device__ inline size_t cluster_smem_doubles(int N) {
+  const int ncol0 = (N + CS - 1) / CS;                                 // CTA 0 owns the most
+  const size_t P = (size_t)ncol0 * N - (size_t)CS * ncol0 * (ncol0 - 1) / 2;
+  const int SL = (N + CS - 1) / CS;
+  return P + 4 * (size_t)N + (size_t)CS * SL + 2 * (size_t)SL;
+}
+
+// a - 2 (ui qj + qi uj) with explicit roundings (identical wherever it is evaluated)
+__device__ __forceinline__ double rank2(double a, double ui, double qi, double uj, double qj) {
+  return __fma_rn(-2.0, __fma_rn(ui, qj, __dmul_rn(qi, uj)), a);
+}
+
+template <int CS>
+__global__ void __launch_bounds__(1024, 1) tridiag_cluster_kernel(const __grid_constant__ SyevBatch B) {
+  namespace cg = cooperative_groups;
+  extern __shared__ double sm[];
+  __shared__ double red[33];
+  cg::cluster_group cl = cg::this_cluster();
+  const SyevEntry& E = B.e[blockIdx.y];
+  const int N = E.N;
+  if (!cluster_class<CS>(N)) return;                     // uniform over the cluster
+  const int c = (int)cl.block_rank();
+  const int tid = threadIdx.x, nt = blockDim.x, warp = tid >> 5, ln = tid & 31, NW = nt >> 5;
+  const int ncol = (N - c + CS - 1) / CS;                // own columns j = c + t CS
+  const int SL = (N + CS - 1) / CS;                      // index slice [c SL, (c+1) SL)
+  auto loff_of = [N](int o, int t) { return (size_t)t * (N - o) - (size_t)CS * t * (t - 1) / 2; };
+  // the same layout in every CTA (CTA 0 owns the most entries): map_shared_rank(ptr, r) maps
+  // to the same offset in CTA r
+  const size_t P = loff_of(0, SL);
+  double* L = sm;
+  double* u = L + P;          // Householder vector of the current step (absolute row index)
+  double* u1 = u + N;         // ... of the next step
+  double* col = u1 + N;       // current pivot column (absolute row index)
+  double* Y = col + N;        // partial matvec (read remotely)
+  double* q = Y + N;          // p / q (size CS*SL >= N; reduce-scatter scratch in phase 3)
+  double* ps = q + (size_t)CS * SL;   // my slice of p (read remotely)
+  double* ncs = ps + SL;              // my slice of the next pivot column (read remotely)
+
+  for (int t = warp; t < ncol; t += NW) {
+    const int j = c + t * CS;
+    double* dst = L + loff_of(c, t);
+    for (int i = j + ln; i < N; i += 32) dst[i - j] = E.A[i + (size_t)j * E.lda];
+  }
+  for (int i = tid; i < N; i += nt) col[i] = E.A[i];
+  __syncthreads();
+
+  // Householder vector of pivot column s (in col): uu[s+1..N), returns alpha (= e_s)
+  auto house = [&](int s, double* uu) -> double {
+    const double x0 = col[s + 1];
+    double part = 0.0;
+    for (int i = s + 2 + tid; i < N; i += nt) part += col[i] * col[i];
+    const double sig = block_sum(part, red);
+    double alpha = x0;
+    if (sig == 0.0) {
+      for (int i = s + 1 + tid; i < N; i += nt) uu[i] = 0.0;
+    } else {
+      alpha = -copysign(sqrt(x0 * x0 + sig), x0);
+      const double v0 = x0 - alpha;
+      const double inv = 1.0 / sqrt(sig + v0 * v0);
+      for (int i = s + 1 + tid; i < N; i += nt) uu[i] = (i == s + 1 ? v0 : col[i]) * inv;
+    }
+    __syncthreads();
+    return alpha;
+  };
+  // own columns j >= jupd get the rank-2 update of (u, q); partial matvec of step ssym with w
+  // over own columns j >= ssym+1 into Y (rows >= ssym+1)
+  auto pass = [&](int jupd, bool upd, int ssym, const double* w) {
+    const int jsym = ssym + 1;
+    const int lo = min(jupd, jsym);
+    for (int i = lo + tid; i < N; i += nt) {
+      const double ui = upd ? u[i] : 0.0, qi = upd ? q[i] : 0.0;
+      double acc = 0.0;
+      int t = max(0, (lo - c + CS - 1) / CS);
+      size_t off = loff_of(c, t);
+      for (int j = c + t * CS; j <= i; j += CS) {
+        double* a = L + off + (i - j);
+        double v = *a;
+        if (upd && j >= jupd) {
+          v = rank2(v, ui, qi, u[j], q[j]);
+          *a = v;
+        }
+        if (j >= jsym) acc = fma(v, w[j], acc);
+        off += (size_t)(N - j);
+      }
+      Y[i] = acc;
+    }
+    __syncthreads();
+    for (int t = max(0, (jsym - c + CS - 1) / CS) + warp; t < ncol; t += NW) {
+      const int j = c + t * CS;
+      const double* a = L + loff_of(c, t);
+      double dot = 0.0;
+      for (int i = j + 1 + ln; i < N; i += 32) dot = fma(a[i - j], w[i], dot);
+      for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+      if (ln == 0) Y[j] += dot;
+    }
+  };
+
+  double alpha = house(0, u);
+  if (c == 0 && tid == 0) {
+    E.d[0] = col[0];
+    E.e[0] = alpha;
+  }
+  pass(N, false, 0, u);
+  for (int s = 0; s + 2 < N; ++s) {
+    cl.sync();                                                           // (A) partials ready
+    // ---- phase 3: reduce-scatter of p(s) over my slice, my slice of the next pivot column ----
+    const int i0 = max(c * SL, s + 1), i1 = min(N, (c + 1) * SL);
+    const int cnt = max(0, i1 - i0);
+    for (int idx = tid; idx < cnt * CS; idx += nt) {
+      const int i = i0 + idx % cnt, src = idx / cnt;
+      q[idx] = cl.map_shared_rank(Y, src)[i];
+    }
+    {
+      const int jn = s + 1, o = jn % CS, tn = jn / CS;
+      const double* Lo = cl.map_shared_rank(L, o) + loff_of(o, tn);
+      for (int i = i0 + tid; i < i1; i += nt) ncs[i - c * SL] = Lo[i - jn];
+    }
+    if (c == 0)   // the Householder vector of step s into column s of A (all initial reads are done)
+      for (int i = s + 1 + tid; i < N; i += nt) E.A[i + (size_t)s * E.lda] = u[i];
+    __syncthreads();
+    for (int i = i0 + tid; i < i1; i += nt) {
+      double v = 0.0;
+      for (int src = 0; src < CS; ++src) v += q[(i - i0) + src * cnt];
+      ps[i - c * SL] = v;
+    }
+    cl.sync();                                                           // (B) slices ready
+    // ---- phase 4: all-gather; q = p - (u^T p) u; next pivot column and its Householder vector ----
+    for (int i = s + 1 + tid; i < N; i += nt) {
+      const int o = i / SL;
+      q[i] = cl.map_shared_rank(ps, o)[i - o * SL];
+      col[i] = cl.map_shared_rank(ncs, o)[i - o * SL];
+    }
+    __syncthreads();
+    double kp = 0.0;
+    for (int i = s + 1 + tid; i < N; i += nt) kp += u[i] * q[i];
+    const double K = block_sum(kp, red);
+    for (int i = s + 1 + tid; i < N; i += nt) q[i] -= K * u[i];
+    __syncthreads();
+    {
+      const double us = u[s + 1], qs = q[s + 1];
+      for (int i = s + 1 + tid; i < N; i += nt) col[i] = rank2(col[i], u[i], q[i], us, qs);
+    }
+    __syncthreads();
+    const bool more = (s + 3 < N);
+    if (more) {
+      alpha = house(s + 1, u1);
+      if (c == 0 && tid == 0) {
+        E.d[s + 1] = col[s + 1];
+        E.e[s + 1] = alpha;
+      }
+    } else if (c == 0 && tid == 0) {
+      E.d[s + 1] = col[s + 1];
+      E.e[s + 1] = col[s + 2];
+    }
+    // ---- rank-2 update of own columns >= s+2, fused with the partial matvec of step s+1 ----
+    pass(s + 2, true, more ? s + 1 : N, u1);
+    __syncthreads();
+    double* tmp = u;
+    u = u1;
+    u1 = tmp;
+  }
+  if (tid == 0 && (N - 1) % CS == c) E.d[N - 1] = L[loff_of(c, (N - 1) / CS)];
+  cl.sync();                                                             // smem stays alive for readers
 }
 
 __device__ int tri_count(int N, const double* __restrict__ d, const double* __restrict__ e, double x,
@@ -976,10 +1166,37 @@ void sl_eigen_device(cudaStream_t st, int n, const double* a_mid_dev, int bounda
   }
 }
 
+template <int CS>
+void launch_tridiag_cluster(const SyevBatch& b, size_t smem, cudaStream_t st) {
+  auto kern = tridiag_cluster_kernel<CS>;
+  static bool attr = false;
+  if (!attr) {
+    FC_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    if (CS > 8) FC_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    attr = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(CS, b.nb, 1);
+  cfg.blockDim = dim3(1024, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CS;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  FC_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, b));
+  FC_CHECK_LAUNCH();
+}
+
 void syev_values(const SyevBatch& b, cudaStream_t st) {
   if (b.nb == 0) return;
+  static const bool no_cluster = getenv("FC_NO_CLUSTER") != nullptr;
+  const int minG = no_cluster ? kPackedMaxN : kCl16MaxN;   // sizes above go to the global kernel
   int maxN = 0;
-  size_t smem_g = 0, smem_p = 0;
+  size_t smem_g = 0, smem_p = 0, smem_8 = 0, smem_16 = 0;
   bool any_g = false, any_p = false;
   constexpr int NW = kTriThreads / 32;
   for (int i = 0; i < b.nb; ++i) {
@@ -989,11 +1206,17 @@ void syev_values(const SyevBatch& b, cudaStream_t st) {
     if (N <= kPackedMaxN) {
       any_p = true;
       smem_p = std::max(smem_p, ((size_t)N * (N + 1) / 2 + 2 * (size_t)N) * 8);
-    } else {
+    } else if (N > minG) {
       any_g = true;
       smem_g = std::max(smem_g, (size_t)(2 + NW) * N * 8);
+    } else if (cluster_class<8>(N)) {
+      smem_8 = std::max(smem_8, cluster_smem_doubles<8>(N) * 8);
+    } else {
+      smem_16 = std::max(smem_16, cluster_smem_doubles<16>(N) * 8);
     }
   }
+  if (smem_8) launch_tridiag_cluster<8>(b, smem_8, st);
+  if (smem_16) launch_tridiag_cluster<16>(b, smem_16, st);
   if (maxN == 0) return;
   require(smem_g <= kTriSmemMax, FC_ERR_CAPACITY, "symmetric eigensolver: matrix dimension above 1500");
   static bool attr = false;
@@ -1007,7 +1230,7 @@ void syev_values(const SyevBatch& b, cudaStream_t st) {
     FC_CHECK_LAUNCH();
   }
   if (any_g) {
-    tridiag_kernel<<<b.nb, kTriThreads, smem_g, st>>>(b);
+    tridiag_kernel<<<b.nb, kTriThreads, smem_g, st>>>(b, minG);
     FC_CHECK_LAUNCH();
   }
   tri_bisect_kernel<<<dim3(cdiv(maxN, 64), b.nb), 64, 0, st>>>(b);
