@@ -1079,6 +1079,213 @@ __global__ void __launch_bounds__(1024) bcgs_finalize_kernel(const __grid_consta
   if (tid == 0) *E.k = k0 + na;
 }
 
+// ---- cluster versions of the two in-block steps --------------------------------------------
+// CTA r of a CS-CTA cluster owns rows [r RB, (r+1) RB) of the n x W block (RB = n / CS <= 128)
+// and keeps them in shared memory: the block X and the accepted unit vectors Yb.  Every dot
+// product and norm is a partial over the CTA's rows, all-reduced through DSMEM in a fixed order
+// (same value in every CTA, so the accept decisions agree).  3 cluster barriers per column
+// (2 projection passes + norm) in the in-block step, 2 in the finalisation.
+constexpr int kBcgsClusterThreads = 512;
+constexpr int kBcgsRB = 128;   // rows per CTA: n <= 8*128 with 8 CTAs, n <= 16*128 with 16
+
+template <int CS>
+struct BcgsClusterSmem {
+  double X[kBcgsRB * kBcgsW];     // column-major, ld RB
+  double Yb[kBcgsRB * kBcgsW];
+  double part[3][kBcgsW];         // per-phase partial dots (read remotely)
+  double coef[kBcgsW];
+  double nrm[2];                  // partial norm^2, double-buffered by column parity
+  double red[kBcgsClusterThreads / 32];
+};
+
+// all-reduce of v[0..cnt) (per-CTA partials in `buf`, read remotely) into out[0..cnt); every
+// CTA sums the CS partials in rank order (shuffle tree over groups of CS lanes)
+template <int CS>
+__device__ __forceinline__ void cluster_allreduce(cooperative_groups::cluster_group& cl, double* buf, int cnt,
+                                                  double* out) {
+  const int tid = threadIdx.x;
+  for (int base = 0; base < cnt * CS; base += blockDim.x) {
+    const int idx = base + tid;
+    const int a = idx / CS, src = idx % CS;
+    double v = (a < cnt) ? cl.map_shared_rank(buf, src)[a] : 0.0;
+#pragma unroll
+    for (int o = CS / 2; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o, CS);
+    if (src == 0 && a < cnt) out[a] = v;
+  }
+}
+
+template <int CS>
+__device__ __forceinline__ double cluster_sum_scalar(cooperative_groups::cluster_group& cl, double* slot,
+                                                     double* bcast) {
+  const int tid = threadIdx.x;
+  if (tid < 32) {
+    double v = tid < CS ? cl.map_shared_rank(slot, tid)[0] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    if (tid == 0) *bcast = v;
+  }
+  __syncthreads();
+  return *bcast;
+}
+
+// block-wide sum of v over all threads into red[]; result returned to every thread
+__device__ __forceinline__ double block_sum_small(double v, double* red) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5, ln = threadIdx.x & 31, nw = blockDim.x >> 5;
+  __syncthreads();
+  if (ln == 0) red[w] = v;
+  __syncthreads();
+  double t = 0.0;
+  for (int i = 0; i < nw; ++i) t += red[i];
+  return t;
+}
+
+template <int CS>
+__global__ void __launch_bounds__(kBcgsClusterThreads, 1)
+    bcgs_block_cluster_kernel(const __grid_constant__ BcgsBatch B, int j0, int w) {
+  namespace cg = cooperative_groups;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  BcgsClusterSmem<CS>& S = *reinterpret_cast<BcgsClusterSmem<CS>*>(smraw);
+  __shared__ double bcast;
+  __shared__ int nacc_s;
+  cg::cluster_group cl = cg::this_cluster();
+  const BcgsEntry& E = B.e[blockIdx.y];
+  if (j0 >= E.p) return;                                   // uniform over the cluster
+  const int n = E.n, wb = min(w, E.p - j0);
+  const int r = (int)cl.block_rank(), RB = (n + CS - 1) / CS;
+  const int r0 = r * RB, nr = max(0, min(n, r0 + RB) - r0);
+  const int tid = threadIdx.x, nt = blockDim.x, warp = tid >> 5, ln = tid & 31, NW = nt >> 5;
+  for (int idx = tid; idx < RB * wb; idx += nt) {
+    const int i = idx % RB, c = idx / RB;
+    S.X[idx] = i < nr ? E.A[(size_t)(r0 + i) + (size_t)(j0 + c) * E.lda] : 0.0;
+  }
+  double mx = 0.0;
+  for (int c = tid; c < E.p; c += nt) mx = fmax(mx, E.norm0[c]);
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  __syncthreads();
+  if (ln == 0) S.red[warp] = mx;
+  __syncthreads();
+  double nmax = 0.0;
+  for (int i = 0; i < NW; ++i) nmax = fmax(nmax, S.red[i]);
+  const int k0 = *E.k;
+  int na = 0;
+  __syncthreads();
+  for (int c = 0; c < wb; ++c) {
+    double* x = S.X + (size_t)c * RB;
+    for (int pass = 0; pass < 2 && na > 0; ++pass) {
+      for (int a = warp; a < na; a += NW) {
+        const double* y = S.Yb + (size_t)a * RB;
+        double s = 0.0;
+        for (int i = ln; i < nr; i += 32) s = fma(y[i], x[i], s);
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (ln == 0) S.part[pass][a] = s;
+      }
+      cl.sync();
+      cluster_allreduce<CS>(cl, S.part[pass], na, S.coef);
+      __syncthreads();
+      // x_i -= sum_a coef_a Yb[i, a]: 4 threads per row, each a quarter of the a-range
+      for (int base = 0; base < RB * 4; base += nt) {
+        const int idx = base + tid, i = idx >> 2, qd = idx & 3;
+        double v = 0.0;
+        if (i < nr)
+          for (int a = qd; a < na; a += 4) v = fma(S.coef[a], S.Yb[i + (size_t)a * RB], v);
+        v += __shfl_xor_sync(0xffffffffu, v, 1);
+        v += __shfl_xor_sync(0xffffffffu, v, 2);
+        if (qd == 0 && i < nr) x[i] -= v;
+      }
+      __syncthreads();
+    }
+    double part = 0.0;
+    for (int i = tid; i < nr; i += nt) part += x[i] * x[i];
+    part = block_sum_small(part, S.red);
+    if (tid == 0) S.nrm[c & 1] = part;
+    cl.sync();
+    const double s2 = cluster_sum_scalar<CS>(cl, &S.nrm[c & 1], &bcast);
+    const double lim = E.tau * fmax(E.norm0[j0 + c], nmax);
+    if (s2 > lim * lim && k0 + na < E.kcap) {
+      const double inv = 1.0 / sqrt(s2);
+      double* y = S.Yb + (size_t)na * RB;
+      for (int i = tid; i < RB; i += nt) y[i] = i < nr ? x[i] * inv : 0.0;
+      ++na;
+    }
+    __syncthreads();
+  }
+  for (int idx = tid; idx < nr * na; idx += nt) {
+    const int i = idx % nr, a = idx / nr;
+    E.Y[(size_t)(r0 + i) + (size_t)a * n] = S.Yb[i + (size_t)a * RB];
+  }
+  for (int idx = tid; idx < nr * (kBcgsW - na); idx += nt) {   // unused block columns stay 0
+    const int i = idx % nr, a = na + idx / nr;
+    E.Y[(size_t)(r0 + i) + (size_t)a * n] = 0.0;
+  }
+  if (r == 0 && tid == 0) *E.nacc = na;
+  cl.sync();                                                 // smem stays alive for readers
+}
+
+// BCGS2 second pass, in-block part, on the cluster: Y[:, :nacc] (re-projected against Q) are
+// re-orthonormalised among themselves (one MGS pass) and appended to Q at k.
+template <int CS>
+__global__ void __launch_bounds__(kBcgsClusterThreads, 1)
+    bcgs_finalize_cluster_kernel(const __grid_constant__ BcgsBatch B, int j0) {
+  namespace cg = cooperative_groups;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  BcgsClusterSmem<CS>& S = *reinterpret_cast<BcgsClusterSmem<CS>*>(smraw);
+  __shared__ double bcast;
+  cg::cluster_group cl = cg::this_cluster();
+  const BcgsEntry& E = B.e[blockIdx.y];
+  if (j0 >= E.p) return;
+  const int n = E.n, na = *E.nacc, k0 = *E.k;
+  const int r = (int)cl.block_rank(), RB = (n + CS - 1) / CS;
+  const int r0 = r * RB, nr = max(0, min(n, r0 + RB) - r0);
+  const int tid = threadIdx.x, nt = blockDim.x, warp = tid >> 5, ln = tid & 31, NW = nt >> 5;
+  for (int idx = tid; idx < RB * na; idx += nt) {
+    const int i = idx % RB, c = idx / RB;
+    S.Yb[idx] = i < nr ? E.Y[(size_t)(r0 + i) + (size_t)c * n] : 0.0;
+  }
+  __syncthreads();
+  for (int c = 0; c < na; ++c) {
+    double* y = S.Yb + (size_t)c * RB;
+    if (c > 0) {
+      for (int a = warp; a < c; a += NW) {
+        const double* ya = S.Yb + (size_t)a * RB;
+        double s = 0.0;
+        for (int i = ln; i < nr; i += 32) s = fma(ya[i], y[i], s);
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (ln == 0) S.part[c & 1][a] = s;
+      }
+      cl.sync();
+      cluster_allreduce<CS>(cl, S.part[c & 1], c, S.coef);
+      __syncthreads();
+      for (int base = 0; base < RB * 4; base += nt) {
+        const int idx = base + tid, i = idx >> 2, qd = idx & 3;
+        double v = 0.0;
+        if (i < nr)
+          for (int a = qd; a < c; a += 4) v = fma(S.coef[a], S.Yb[i + (size_t)a * RB], v);
+        v += __shfl_xor_sync(0xffffffffu, v, 1);
+        v += __shfl_xor_sync(0xffffffffu, v, 2);
+        if (qd == 0 && i < nr) y[i] -= v;
+      }
+      __syncthreads();
+    }
+    double part = 0.0;
+    for (int i = tid; i < nr; i += nt) part += y[i] * y[i];
+    part = block_sum_small(part, S.red);
+    if (tid == 0) S.nrm[c & 1] = part;
+    cl.sync();
+    const double s2 = cluster_sum_scalar<CS>(cl, &S.nrm[c & 1], &bcast);
+    const double inv = s2 > 0 ? 1.0 / sqrt(s2) : 0.0;
+    for (int i = tid; i < nr; i += nt) {
+      const double v = y[i] * inv;
+      y[i] = v;
+      E.Y[(size_t)(r0 + i) + (size_t)c * n] = v;
+      E.Q[(size_t)(r0 + i) + (size_t)(k0 + c) * E.ldq] = v;
+    }
+    __syncthreads();
+  }
+  cl.sync();
+  if (r == 0 && tid == 0) *E.k = k0 + na;
+}
+
 __global__ void col_norms_kernel(const __grid_constant__ BcgsBatch B) {
   const BcgsEntry& E = B.e[blockIdx.y];
   const int c = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5), ln = threadIdx.x & 31;
@@ -1268,9 +1475,69 @@ void pmgs(const PmgsBatch& b, cudaStream_t st) {
   FC_CHECK_LAUNCH();
 }
 
+template <typename K>
+void launch_cluster(K kern, int CS, int nb, size_t smem, cudaStream_t st, const BcgsBatch& b, int j0, int w,
+                    bool with_w) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(CS, nb, 1);
+  cfg.blockDim = dim3(kBcgsClusterThreads, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CS;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  if (with_w) FC_CUDA_TRY(cudaLaunchKernelEx(&cfg, (void (*)(BcgsBatch, int, int))kern, b, j0, w));
+  else FC_CUDA_TRY(cudaLaunchKernelEx(&cfg, (void (*)(BcgsBatch, int))kern, b, j0));
+  FC_CHECK_LAUNCH();
+}
+
+template <int CS>
+void bcgs_cluster_setup() {
+  static bool attr = false;
+  if (attr) return;
+  const int smem = (int)sizeof(BcgsClusterSmem<CS>);
+  FC_CUDA_TRY(cudaFuncSetAttribute(bcgs_block_cluster_kernel<CS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  FC_CUDA_TRY(cudaFuncSetAttribute(bcgs_finalize_cluster_kernel<CS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  if (CS > 8) {
+    FC_CUDA_TRY(cudaFuncSetAttribute(bcgs_block_cluster_kernel<CS>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    FC_CUDA_TRY(cudaFuncSetAttribute(bcgs_finalize_cluster_kernel<CS>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  }
+  attr = true;
+}
+
 void bcgs(const BcgsBatch& bin, cudaStream_t st) {
   if (bin.nb == 0) return;
   constexpr int W = kBcgsW;
+  static const bool no_cluster = getenv("FC_NO_CLUSTER") != nullptr;
+  int maxn = 0;
+  for (int i = 0; i < bin.nb; ++i) maxn = std::max(maxn, bin.e[i].n);
+  const int CS = no_cluster || maxn > 16 * kBcgsRB ? 0 : (maxn <= 8 * kBcgsRB ? 8 : 16);
+  if (CS == 8) bcgs_cluster_setup<8>();
+  if (CS == 16) bcgs_cluster_setup<16>();
+  auto block_step = [&](const BcgsBatch& bb, int j0) {
+    if (CS == 8)
+      launch_cluster(bcgs_block_cluster_kernel<8>, 8, bb.nb, sizeof(BcgsClusterSmem<8>), st, bb, j0, W, true);
+    else if (CS == 16)
+      launch_cluster(bcgs_block_cluster_kernel<16>, 16, bb.nb, sizeof(BcgsClusterSmem<16>), st, bb, j0, W, true);
+    else {
+      bcgs_block_kernel<<<bb.nb, 1024, (size_t)bb.e[0].n * 8, st>>>(bb, j0, W);
+      FC_CHECK_LAUNCH();
+    }
+  };
+  auto finalize_step = [&](const BcgsBatch& bb, int j0) {
+    if (CS == 8)
+      launch_cluster(bcgs_finalize_cluster_kernel<8>, 8, bb.nb, sizeof(BcgsClusterSmem<8>), st, bb, j0, 0, false);
+    else if (CS == 16)
+      launch_cluster(bcgs_finalize_cluster_kernel<16>, 16, bb.nb, sizeof(BcgsClusterSmem<16>), st, bb, j0, 0, false);
+    else {
+      bcgs_finalize_kernel<<<bb.nb, 1024, (size_t)bb.e[0].n * 8, st>>>(bb, j0);
+      FC_CHECK_LAUNCH();
+    }
+  };
   BcgsBatch b = bin;
   Scratch scr(st);
   for (int i = 0; i < b.nb; ++i) {
@@ -1310,8 +1577,7 @@ void bcgs(const BcgsBatch& bin, cudaStream_t st) {
       gemm(p, st);
       gemm(u, st);
     }
-    bcgs_block_kernel<<<b.nb, 1024, (size_t)b.e[0].n * 8, st>>>(b, j0, W);
-    FC_CHECK_LAUNCH();
+    block_step(b, j0);
     // BCGS2: re-project the accepted (unit) block vectors against the previous basis
     if (j0 > 0) {
       GemmArgs p, u;
@@ -1334,8 +1600,7 @@ void bcgs(const BcgsBatch& bin, cudaStream_t st) {
       gemm(p, st);
       gemm(u, st);
     }
-    bcgs_finalize_kernel<<<b.nb, 1024, (size_t)b.e[0].n * 8, st>>>(b, j0);
-    FC_CHECK_LAUNCH();
+    finalize_step(b, j0);
   }
 }
 
