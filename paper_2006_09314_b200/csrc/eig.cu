@@ -734,18 +734,25 @@ __device__ int tri_count(int N, const double* __restrict__ d, const double* __re
   return cnt;
 }
 
-// thread per eigenvalue; lam[i] = i-th largest
+// warp per eigenvalue (multisection); lam[i] = i-th largest.  Each round the 32 lanes count
+// the eigenvalues below 32 equispaced interior points of [lo, hi]; the interval shrinks 33x.
 __global__ void tri_bisect_kernel(const __grid_constant__ SyevBatch B) {
   const SyevEntry& E = B.e[blockIdx.y];
   const int N = E.N;
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int ln = threadIdx.x & 31;
   if (i >= N) return;
   double lo = 1e300, hi = -1e300, emax = 0.0;
-  for (int k = 0; k < N; ++k) {
+  for (int k = ln; k < N; k += 32) {
     double r = (k > 0 ? fabs(E.e[k - 1]) : 0.0) + (k < N - 1 ? fabs(E.e[k]) : 0.0);
     lo = fmin(lo, E.d[k] - r);
     hi = fmax(hi, E.d[k] + r);
     if (k < N - 1) emax = fmax(emax, fabs(E.e[k]));
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    emax = fmax(emax, __shfl_xor_sync(0xffffffffu, emax, o));
   }
   const double tnorm = fmax(fabs(lo), fabs(hi));
   const double pivmin = DBL_MIN / kEps * fmax(1.0, emax * emax);
@@ -753,14 +760,20 @@ __global__ void tri_bisect_kernel(const __grid_constant__ SyevBatch B) {
   hi += 2 * kEps * tnorm + pivmin;
   const int target = N - i;  // want the target-th smallest (1-based)
   const double atol = 2.0 * kEps * tnorm + pivmin;
-  for (int it = 0; it < 200; ++it) {
-    double mid = 0.5 * (lo + hi);
+  for (int it = 0; it < 60; ++it) {
     if (hi - lo <= fmax(atol, 2.0 * kEps * fmax(fabs(lo), fabs(hi)))) break;
-    if (mid <= lo || mid >= hi) break;
-    if (tri_count(N, E.d, E.e, mid, pivmin) >= target) hi = mid;
-    else lo = mid;
+    const double x = lo + (hi - lo) * ((double)(ln + 1) / 33.0);
+    const bool ge = (x > lo && x < hi) ? tri_count(N, E.d, E.e, x, pivmin) >= target : (x >= hi);
+    const unsigned m = __ballot_sync(0xffffffffu, ge);
+    // first lane whose point has >= target eigenvalues below it: new interval (x_{j-1}, x_j]
+    const int j = m ? __ffs(m) - 1 : 32;
+    const double xl = j > 0 ? __shfl_sync(0xffffffffu, x, j - 1) : lo;
+    const double xh = j < 32 ? __shfl_sync(0xffffffffu, x, j & 31) : hi;
+    if (xl <= lo && xh >= hi) break;   // no progress (interval at rounding resolution)
+    lo = xl;
+    hi = xh;
   }
-  E.lam[i] = 0.5 * (lo + hi);
+  if (ln == 0) E.lam[i] = 0.5 * (lo + hi);
 }
 
 // thread per wanted vector (i < r): inverse iteration on (d, e) into Y[:, i]
@@ -1081,25 +1094,31 @@ __global__ void __launch_bounds__(1024) bcgs_finalize_kernel(const __grid_consta
 
 // ---- cluster versions of the two in-block steps --------------------------------------------
 // CTA r of a CS-CTA cluster owns rows [r RB, (r+1) RB) of the n x W block (RB = n / CS <= 128)
-// and keeps them in shared memory: the block X and the accepted unit vectors Yb.  Every dot
-// product and norm is a partial over the CTA's rows, all-reduced through DSMEM in a fixed order
-// (same value in every CTA, so the accept decisions agree).  3 cluster barriers per column
-// (2 projection passes + norm) in the in-block step, 2 in the finalisation.
+// and keeps them in shared memory: the block X and the accepted unit vectors Yb (leading
+// dimension RB + 4: conflict-free row-parallel access).  Every dot product and norm is a partial
+// over the CTA's rows, all-reduced through DSMEM in a fixed order (the same value in every CTA,
+// so the accept decisions agree).
+//   in-block step: one all-reduce of all block column norms first (columns already below the
+//   threshold after the GEMM projection cannot be accepted later: skipped); then per remaining
+//   column: pass 1 (dots, all-reduce, update), pass 2 fused with the norm (dots and ||x'||^2 in
+//   one all-reduce, ||x''||^2 = ||x'||^2 - ||c2||^2: c2 = O(eps ||x||) after pass 1, far below
+//   the tau ||x|| decision level) -> at most 2 cluster barriers per column;
+//   finalisation: dots with the earlier block vectors and the norm in one all-reduce (1 barrier).
 constexpr int kBcgsClusterThreads = 512;
-constexpr int kBcgsRB = 128;   // rows per CTA: n <= 8*128 with 8 CTAs, n <= 16*128 with 16
+constexpr int kBcgsRB = 128;               // rows per CTA: n <= 8*128 with 8 CTAs, <= 16*128 with 16
+constexpr int kBcgsLd = kBcgsRB + 4;
 
-template <int CS>
 struct BcgsClusterSmem {
-  double X[kBcgsRB * kBcgsW];     // column-major, ld RB
-  double Yb[kBcgsRB * kBcgsW];
-  double part[3][kBcgsW];         // per-phase partial dots (read remotely)
-  double coef[kBcgsW];
-  double nrm[2];                  // partial norm^2, double-buffered by column parity
+  double X[kBcgsLd * kBcgsW];
+  double Yb[kBcgsLd * kBcgsW];
+  double part[2][kBcgsW + 2];     // partial dots (+ norm), double-buffered (read remotely)
+  double coef[kBcgsW + 2];
   double red[kBcgsClusterThreads / 32];
+  int alive[kBcgsW];
 };
 
-// all-reduce of v[0..cnt) (per-CTA partials in `buf`, read remotely) into out[0..cnt); every
-// CTA sums the CS partials in rank order (shuffle tree over groups of CS lanes)
+// all-reduce of buf[0..cnt) (per-CTA partials, read remotely) into out[0..cnt); every CTA sums
+// the CS partials in rank order (shuffle tree over groups of CS lanes)
 template <int CS>
 __device__ __forceinline__ void cluster_allreduce(cooperative_groups::cluster_group& cl, double* buf, int cnt,
                                                   double* out) {
@@ -1114,30 +1133,59 @@ __device__ __forceinline__ void cluster_allreduce(cooperative_groups::cluster_gr
   }
 }
 
-template <int CS>
-__device__ __forceinline__ double cluster_sum_scalar(cooperative_groups::cluster_group& cl, double* slot,
-                                                     double* bcast) {
-  const int tid = threadIdx.x;
-  if (tid < 32) {
-    double v = tid < CS ? cl.map_shared_rank(slot, tid)[0] : 0.0;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
-    if (tid == 0) *bcast = v;
+// partial dots part[a] = sum_{i < nr} V[i, a] x[i] for a < na (4 independent dots per warp)
+// and, if want_norm, part[na] = sum x[i]^2
+__device__ __forceinline__ void block_dots(const double* V, const double* x, int nr, int na, bool want_norm,
+                                           double* part, double* red) {
+  const int tid = threadIdx.x, warp = tid >> 5, ln = tid & 31, NW = blockDim.x >> 5;
+  for (int a0 = warp * 4; a0 < na; a0 += NW * 4) {
+    double s0 = 0, s1 = 0, s2 = 0, s3 = 0;
+    for (int i = ln; i < nr; i += 32) {
+      const double xi = x[i];
+      s0 = fma(V[i + (size_t)a0 * kBcgsLd], xi, s0);
+      if (a0 + 1 < na) s1 = fma(V[i + (size_t)(a0 + 1) * kBcgsLd], xi, s1);
+      if (a0 + 2 < na) s2 = fma(V[i + (size_t)(a0 + 2) * kBcgsLd], xi, s2);
+      if (a0 + 3 < na) s3 = fma(V[i + (size_t)(a0 + 3) * kBcgsLd], xi, s3);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+      s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+      s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+      s3 += __shfl_xor_sync(0xffffffffu, s3, o);
+    }
+    if (ln == 0) {
+      part[a0] = s0;
+      if (a0 + 1 < na) part[a0 + 1] = s1;
+      if (a0 + 2 < na) part[a0 + 2] = s2;
+      if (a0 + 3 < na) part[a0 + 3] = s3;
+    }
   }
-  __syncthreads();
-  return *bcast;
+  if (want_norm) {
+    double q = 0.0;
+    for (int i = tid; i < nr; i += blockDim.x) q = fma(x[i], x[i], q);
+    for (int o = 16; o > 0; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
+    if (ln == 0) red[warp] = q;
+    __syncthreads();
+    if (tid == 0) {
+      double t = 0.0;
+      for (int w = 0; w < NW; ++w) t += red[w];
+      part[na] = t;
+    }
+  }
 }
 
-// block-wide sum of v over all threads into red[]; result returned to every thread
-__device__ __forceinline__ double block_sum_small(double v, double* red) {
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  const int w = threadIdx.x >> 5, ln = threadIdx.x & 31, nw = blockDim.x >> 5;
-  __syncthreads();
-  if (ln == 0) red[w] = v;
-  __syncthreads();
-  double t = 0.0;
-  for (int i = 0; i < nw; ++i) t += red[i];
-  return t;
+// x[i] -= sum_{a < na} coef[a] V[i, a]  (4 threads per row)
+__device__ __forceinline__ void block_update(const double* V, double* x, int nr, int na, const double* coef) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  for (int base = 0; base < kBcgsRB * 4; base += nt) {
+    const int idx = base + tid, i = idx >> 2, qd = idx & 3;
+    double v = 0.0;
+    if (i < nr)
+      for (int a = qd; a < na; a += 4) v = fma(coef[a], V[i + (size_t)a * kBcgsLd], v);
+    v += __shfl_xor_sync(0xffffffffu, v, 1);
+    v += __shfl_xor_sync(0xffffffffu, v, 2);
+    if (qd == 0 && i < nr) x[i] -= v;
+  }
 }
 
 template <int CS>
@@ -1145,9 +1193,7 @@ __global__ void __launch_bounds__(kBcgsClusterThreads, 1)
     bcgs_block_cluster_kernel(const __grid_constant__ BcgsBatch B, int j0, int w) {
   namespace cg = cooperative_groups;
   extern __shared__ __align__(16) unsigned char smraw[];
-  BcgsClusterSmem<CS>& S = *reinterpret_cast<BcgsClusterSmem<CS>*>(smraw);
-  __shared__ double bcast;
-  __shared__ int nacc_s;
+  BcgsClusterSmem& S = *reinterpret_cast<BcgsClusterSmem*>(smraw);
   cg::cluster_group cl = cg::this_cluster();
   const BcgsEntry& E = B.e[blockIdx.y];
   if (j0 >= E.p) return;                                   // uniform over the cluster
@@ -1157,7 +1203,7 @@ __global__ void __launch_bounds__(kBcgsClusterThreads, 1)
   const int tid = threadIdx.x, nt = blockDim.x, warp = tid >> 5, ln = tid & 31, NW = nt >> 5;
   for (int idx = tid; idx < RB * wb; idx += nt) {
     const int i = idx % RB, c = idx / RB;
-    S.X[idx] = i < nr ? E.A[(size_t)(r0 + i) + (size_t)(j0 + c) * E.lda] : 0.0;
+    S.X[i + (size_t)c * kBcgsLd] = i < nr ? E.A[(size_t)(r0 + i) + (size_t)(j0 + c) * E.lda] : 0.0;
   }
   double mx = 0.0;
   for (int c = tid; c < E.p; c += nt) mx = fmax(mx, E.norm0[c]);
@@ -1168,111 +1214,104 @@ __global__ void __launch_bounds__(kBcgsClusterThreads, 1)
   double nmax = 0.0;
   for (int i = 0; i < NW; ++i) nmax = fmax(nmax, S.red[i]);
   const int k0 = *E.k;
-  int na = 0;
   __syncthreads();
+  // ---- pre-filter: all block column norms in one all-reduce ----
+  for (int c = warp; c < wb; c += NW) {
+    const double* x = S.X + (size_t)c * kBcgsLd;
+    double q = 0.0;
+    for (int i = ln; i < nr; i += 32) q = fma(x[i], x[i], q);
+    for (int o = 16; o > 0; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
+    if (ln == 0) S.part[0][c] = q;
+  }
+  cl.sync();
+  cluster_allreduce<CS>(cl, S.part[0], wb, S.coef);
+  __syncthreads();
+  for (int c = tid; c < wb; c += nt) {
+    const double lim = E.tau * fmax(E.norm0[j0 + c], nmax);
+    S.alive[c] = S.coef[c] > lim * lim;
+  }
+  __syncthreads();
+  int na = 0, ph = 1;                                      // ph: partial buffer of the next phase
   for (int c = 0; c < wb; ++c) {
-    double* x = S.X + (size_t)c * RB;
-    for (int pass = 0; pass < 2 && na > 0; ++pass) {
-      for (int a = warp; a < na; a += NW) {
-        const double* y = S.Yb + (size_t)a * RB;
-        double s = 0.0;
-        for (int i = ln; i < nr; i += 32) s = fma(y[i], x[i], s);
-        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-        if (ln == 0) S.part[pass][a] = s;
-      }
+    if (!S.alive[c]) continue;
+    double* x = S.X + (size_t)c * kBcgsLd;
+    double s2;
+    if (na == 0) {
+      block_dots(S.Yb, x, nr, 0, true, S.part[ph], S.red);
       cl.sync();
-      cluster_allreduce<CS>(cl, S.part[pass], na, S.coef);
+      cluster_allreduce<CS>(cl, S.part[ph], 1, S.coef);
       __syncthreads();
-      // x_i -= sum_a coef_a Yb[i, a]: 4 threads per row, each a quarter of the a-range
-      for (int base = 0; base < RB * 4; base += nt) {
-        const int idx = base + tid, i = idx >> 2, qd = idx & 3;
-        double v = 0.0;
-        if (i < nr)
-          for (int a = qd; a < na; a += 4) v = fma(S.coef[a], S.Yb[i + (size_t)a * RB], v);
-        v += __shfl_xor_sync(0xffffffffu, v, 1);
-        v += __shfl_xor_sync(0xffffffffu, v, 2);
-        if (qd == 0 && i < nr) x[i] -= v;
-      }
+      s2 = S.coef[0];
+      ph ^= 1;
+    } else {
+      block_dots(S.Yb, x, nr, na, false, S.part[ph], S.red);
+      cl.sync();
+      cluster_allreduce<CS>(cl, S.part[ph], na, S.coef);
       __syncthreads();
+      block_update(S.Yb, x, nr, na, S.coef);
+      __syncthreads();
+      ph ^= 1;
+      block_dots(S.Yb, x, nr, na, true, S.part[ph], S.red);
+      cl.sync();
+      cluster_allreduce<CS>(cl, S.part[ph], na + 1, S.coef);
+      __syncthreads();
+      block_update(S.Yb, x, nr, na, S.coef);
+      double c2 = 0.0;
+      for (int a = 0; a < na; ++a) c2 = fma(S.coef[a], S.coef[a], c2);
+      s2 = S.coef[na] - c2;
+      __syncthreads();
+      ph ^= 1;
     }
-    double part = 0.0;
-    for (int i = tid; i < nr; i += nt) part += x[i] * x[i];
-    part = block_sum_small(part, S.red);
-    if (tid == 0) S.nrm[c & 1] = part;
-    cl.sync();
-    const double s2 = cluster_sum_scalar<CS>(cl, &S.nrm[c & 1], &bcast);
     const double lim = E.tau * fmax(E.norm0[j0 + c], nmax);
     if (s2 > lim * lim && k0 + na < E.kcap) {
       const double inv = 1.0 / sqrt(s2);
-      double* y = S.Yb + (size_t)na * RB;
+      double* y = S.Yb + (size_t)na * kBcgsLd;
       for (int i = tid; i < RB; i += nt) y[i] = i < nr ? x[i] * inv : 0.0;
       ++na;
     }
     __syncthreads();
   }
-  for (int idx = tid; idx < nr * na; idx += nt) {
+  for (int idx = tid; idx < nr * kBcgsW; idx += nt) {      // unused block columns stay 0
     const int i = idx % nr, a = idx / nr;
-    E.Y[(size_t)(r0 + i) + (size_t)a * n] = S.Yb[i + (size_t)a * RB];
-  }
-  for (int idx = tid; idx < nr * (kBcgsW - na); idx += nt) {   // unused block columns stay 0
-    const int i = idx % nr, a = na + idx / nr;
-    E.Y[(size_t)(r0 + i) + (size_t)a * n] = 0.0;
+    E.Y[(size_t)(r0 + i) + (size_t)a * n] = a < na ? S.Yb[i + (size_t)a * kBcgsLd] : 0.0;
   }
   if (r == 0 && tid == 0) *E.nacc = na;
   cl.sync();                                                 // smem stays alive for readers
 }
 
 // BCGS2 second pass, in-block part, on the cluster: Y[:, :nacc] (re-projected against Q) are
-// re-orthonormalised among themselves (one MGS pass) and appended to Q at k.
+// re-orthonormalised among themselves (one MGS pass, dots and norm in one all-reduce) and
+// appended to Q at k.
 template <int CS>
 __global__ void __launch_bounds__(kBcgsClusterThreads, 1)
     bcgs_finalize_cluster_kernel(const __grid_constant__ BcgsBatch B, int j0) {
   namespace cg = cooperative_groups;
   extern __shared__ __align__(16) unsigned char smraw[];
-  BcgsClusterSmem<CS>& S = *reinterpret_cast<BcgsClusterSmem<CS>*>(smraw);
-  __shared__ double bcast;
+  BcgsClusterSmem& S = *reinterpret_cast<BcgsClusterSmem*>(smraw);
   cg::cluster_group cl = cg::this_cluster();
   const BcgsEntry& E = B.e[blockIdx.y];
   if (j0 >= E.p) return;
   const int n = E.n, na = *E.nacc, k0 = *E.k;
   const int r = (int)cl.block_rank(), RB = (n + CS - 1) / CS;
   const int r0 = r * RB, nr = max(0, min(n, r0 + RB) - r0);
-  const int tid = threadIdx.x, nt = blockDim.x, warp = tid >> 5, ln = tid & 31, NW = nt >> 5;
+  const int tid = threadIdx.x, nt = blockDim.x;
   for (int idx = tid; idx < RB * na; idx += nt) {
     const int i = idx % RB, c = idx / RB;
-    S.Yb[idx] = i < nr ? E.Y[(size_t)(r0 + i) + (size_t)c * n] : 0.0;
+    S.Yb[i + (size_t)c * kBcgsLd] = i < nr ? E.Y[(size_t)(r0 + i) + (size_t)c * n] : 0.0;
   }
   __syncthreads();
   for (int c = 0; c < na; ++c) {
-    double* y = S.Yb + (size_t)c * RB;
-    if (c > 0) {
-      for (int a = warp; a < c; a += NW) {
-        const double* ya = S.Yb + (size_t)a * RB;
-        double s = 0.0;
-        for (int i = ln; i < nr; i += 32) s = fma(ya[i], y[i], s);
-        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-        if (ln == 0) S.part[c & 1][a] = s;
-      }
-      cl.sync();
-      cluster_allreduce<CS>(cl, S.part[c & 1], c, S.coef);
-      __syncthreads();
-      for (int base = 0; base < RB * 4; base += nt) {
-        const int idx = base + tid, i = idx >> 2, qd = idx & 3;
-        double v = 0.0;
-        if (i < nr)
-          for (int a = qd; a < c; a += 4) v = fma(S.coef[a], S.Yb[i + (size_t)a * RB], v);
-        v += __shfl_xor_sync(0xffffffffu, v, 1);
-        v += __shfl_xor_sync(0xffffffffu, v, 2);
-        if (qd == 0 && i < nr) y[i] -= v;
-      }
-      __syncthreads();
-    }
-    double part = 0.0;
-    for (int i = tid; i < nr; i += nt) part += y[i] * y[i];
-    part = block_sum_small(part, S.red);
-    if (tid == 0) S.nrm[c & 1] = part;
+    double* y = S.Yb + (size_t)c * kBcgsLd;
+    double* part = S.part[c & 1];
+    block_dots(S.Yb, y, nr, c, true, part, S.red);
     cl.sync();
-    const double s2 = cluster_sum_scalar<CS>(cl, &S.nrm[c & 1], &bcast);
+    cluster_allreduce<CS>(cl, part, c + 1, S.coef);
+    __syncthreads();
+    if (c > 0) block_update(S.Yb, y, nr, c, S.coef);
+    double c2 = 0.0;
+    for (int a = 0; a < c; ++a) c2 = fma(S.coef[a], S.coef[a], c2);
+    const double s2 = S.coef[c] - c2;
+    __syncthreads();
     const double inv = s2 > 0 ? 1.0 / sqrt(s2) : 0.0;
     for (int i = tid; i < nr; i += nt) {
       const double v = y[i] * inv;
@@ -1440,7 +1479,7 @@ void syev_values(const SyevBatch& b, cudaStream_t st) {
     tridiag_kernel<<<b.nb, kTriThreads, smem_g, st>>>(b, minG);
     FC_CHECK_LAUNCH();
   }
-  tri_bisect_kernel<<<dim3(cdiv(maxN, 64), b.nb), 64, 0, st>>>(b);
+  tri_bisect_kernel<<<dim3(cdiv(maxN, 8), b.nb), 256, 0, st>>>(b);
   FC_CHECK_LAUNCH();
 }
 
@@ -1499,7 +1538,7 @@ template <int CS>
 void bcgs_cluster_setup() {
   static bool attr = false;
   if (attr) return;
-  const int smem = (int)sizeof(BcgsClusterSmem<CS>);
+  const int smem = (int)sizeof(BcgsClusterSmem);
   FC_CUDA_TRY(cudaFuncSetAttribute(bcgs_block_cluster_kernel<CS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   FC_CUDA_TRY(cudaFuncSetAttribute(bcgs_finalize_cluster_kernel<CS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   if (CS > 8) {
@@ -1520,9 +1559,9 @@ void bcgs(const BcgsBatch& bin, cudaStream_t st) {
   if (CS == 16) bcgs_cluster_setup<16>();
   auto block_step = [&](const BcgsBatch& bb, int j0) {
     if (CS == 8)
-      launch_cluster(bcgs_block_cluster_kernel<8>, 8, bb.nb, sizeof(BcgsClusterSmem<8>), st, bb, j0, W, true);
+      launch_cluster(bcgs_block_cluster_kernel<8>, 8, bb.nb, sizeof(BcgsClusterSmem), st, bb, j0, W, true);
     else if (CS == 16)
-      launch_cluster(bcgs_block_cluster_kernel<16>, 16, bb.nb, sizeof(BcgsClusterSmem<16>), st, bb, j0, W, true);
+      launch_cluster(bcgs_block_cluster_kernel<16>, 16, bb.nb, sizeof(BcgsClusterSmem), st, bb, j0, W, true);
     else {
       bcgs_block_kernel<<<bb.nb, 1024, (size_t)bb.e[0].n * 8, st>>>(bb, j0, W);
       FC_CHECK_LAUNCH();
@@ -1530,9 +1569,9 @@ void bcgs(const BcgsBatch& bin, cudaStream_t st) {
   };
   auto finalize_step = [&](const BcgsBatch& bb, int j0) {
     if (CS == 8)
-      launch_cluster(bcgs_finalize_cluster_kernel<8>, 8, bb.nb, sizeof(BcgsClusterSmem<8>), st, bb, j0, 0, false);
+      launch_cluster(bcgs_finalize_cluster_kernel<8>, 8, bb.nb, sizeof(BcgsClusterSmem), st, bb, j0, 0, false);
     else if (CS == 16)
-      launch_cluster(bcgs_finalize_cluster_kernel<16>, 16, bb.nb, sizeof(BcgsClusterSmem<16>), st, bb, j0, 0, false);
+      launch_cluster(bcgs_finalize_cluster_kernel<16>, 16, bb.nb, sizeof(BcgsClusterSmem), st, bb, j0, 0, false);
     else {
       bcgs_finalize_kernel<<<bb.nb, 1024, (size_t)bb.e[0].n * 8, st>>>(bb, j0);
       FC_CHECK_LAUNCH();

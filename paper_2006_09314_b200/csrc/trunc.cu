@@ -176,8 +176,9 @@ __global__ void extract_slices_kernel(const double* __restrict__ core, int r0, i
 // Slices whose working set exceeds the shared-memory budget run the same algorithm in a
 // per-slice global (L2-resident) workspace `gws` of (rows*cols + cols*cols) doubles.
 constexpr int kSliceMax = 512;
+__device__ int g_slice_sweeps_max = 0;   // diagnostics (FC_TRACE): most Jacobi sweeps of a slice
 constexpr size_t kSliceSmem = 200 * 1024;
-__global__ void __launch_bounds__(1024) slice_svd_kernel(int ra, int rb, const double* __restrict__ S, double* s_out,
+__global__ void __launch_bounds__(512) slice_svd_kernel(int ra, int rb, const double* __restrict__ S, double* s_out,
                                                         double* Ua, double* Vb, double* gws) {
   extern __shared__ double sm[];
   const int nu = blockIdx.x;
@@ -191,53 +192,97 @@ __global__ void __launch_bounds__(1024) slice_svd_kernel(int ra, int rb, const d
   int* order = (int*)(nrm + cols);             // cols
   const double* src = S + (size_t)nu * ra * rb;
   const int tid = threadIdx.x, nt = blockDim.x, warp = tid >> 5, ln = tid & 31, nw = nt >> 5;
+  // columns sorted by decreasing norm (de Rijk): column j of the slice goes to position
+  // order-rank(j); W starts as that permutation, so A_final = A_slice W holds throughout
+  for (int j = warp; j < cols; j += nw) {
+    double s2 = 0;
+    for (int i = ln; i < rows; i += 32) {
+      const double v = tr ? src[j + (size_t)i * ra] : src[i + (size_t)j * ra];
+      s2 = fma(v, v, s2);
+    }
+    for (int o = 16; o > 0; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+    if (ln == 0) nrm[j] = s2;
+  }
+  __syncthreads();
+  for (int j = tid; j < cols; j += nt) {
+    int rk = 0;
+    for (int i = 0; i < cols; ++i) rk += (nrm[i] > nrm[j]) || (nrm[i] == nrm[j] && i < j);
+    order[j] = rk;
+  }
+  __syncthreads();
   for (int idx = tid; idx < rows * cols; idx += nt) {
     int i = idx % rows, j = idx / rows;
-    A[idx] = tr ? src[j + (size_t)i * ra] : src[i + (size_t)j * ra];
+    A[i + (size_t)order[j] * rows] = tr ? src[j + (size_t)i * ra] : src[i + (size_t)j * ra];
   }
-  for (int idx = tid; idx < cols * cols; idx += nt) W[idx] = (idx % cols == idx / cols) ? 1.0 : 0.0;
+  for (int idx = tid; idx < cols * cols; idx += nt) {
+    const int i = idx % cols, j = idx / cols;
+    W[idx] = (order[i] == j) ? 1.0 : 0.0;
+  }
   __shared__ int changed;
+  __shared__ double fro2_s;
+  if (tid == 0) {
+    double f = 0.0;
+    for (int j = 0; j < cols; ++j) f += nrm[j];
+    fro2_s = f;
+  }
   __syncthreads();
+  // columns below 1e-12 ||slice||_F are numerical noise whose triples the pooled eps cut always
+  // drops (for eps >= 1e-9): pairs involving them count as converged
+  const double neg2 = 1e-24 * fro2_s;
   const int p = cols + (cols & 1);
+  // convergence: |a_i . a_j| <= tol ||a_i|| ||a_j|| with tol = 2 sqrt(rows) eps (the rounding
+  // level of the computed dot product; LAPACK dgesvj uses sqrt(m) eps)
+  const double tol = 2.0 * sqrt((double)rows) * 2.220446049250313e-16, tol2 = tol * tol;
+  // G lanes per column pair (power of two, 4..32): all p/2 pairs of a round in one wave
+  int G = 32;
+  while (G > 4 && nt / G < p / 2) G >>= 1;
+  const int gid = tid / G, gl = tid % G, ng = nt / G;
+  const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << ((ln / G) * G));
   for (int sweep = 0; sweep < 40; ++sweep) {
     if (tid == 0) changed = 0;
     __syncthreads();
     for (int rd = 0; rd < p - 1; ++rd) {
-      for (int pi = warp; pi < p / 2; pi += nw) {
+      for (int pi = gid; pi < p / 2; pi += ng) {
         int a, b;
         if (pi == 0) { a = rd % (p - 1); b = p - 1; }
         else { a = (rd + pi) % (p - 1); b = (rd - pi + p - 1) % (p - 1); }
         if (a > b) { int t = a; a = b; b = t; }
         if (b >= cols) continue;
         double al = 0, be = 0, ga = 0;
-        for (int i = ln; i < rows; i += 32) {
+        for (int i = gl; i < rows; i += G) {
           double x = A[i + a * rows], y = A[i + b * rows];
-          al += x * x; be += y * y; ga += x * y;
+          al = fma(x, x, al); be = fma(y, y, be); ga = fma(x, y, ga);
         }
-        for (int o = 16; o > 0; o >>= 1) {
-          al += __shfl_xor_sync(0xffffffffu, al, o);
-          be += __shfl_xor_sync(0xffffffffu, be, o);
-          ga += __shfl_xor_sync(0xffffffffu, ga, o);
+        for (int o = G >> 1; o > 0; o >>= 1) {
+          al += __shfl_xor_sync(gmask, al, o);
+          be += __shfl_xor_sync(gmask, be, o);
+          ga += __shfl_xor_sync(gmask, ga, o);
         }
-        if (ga == 0.0 || fabs(ga) <= 1e-15 * sqrt(al * be)) continue;
-        double zeta = (be - al) / (2.0 * ga);
-        double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-        double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
-        for (int i = ln; i < rows; i += 32) {
+        if (ga == 0.0 || ga * ga <= tol2 * (al * be) || al <= neg2 || be <= neg2) continue;
+        // Rutishauser's rotation, zeta = (be - al) / (2 ga), t = sign(zeta) / (|zeta| + sqrt(1 + zeta^2)),
+        // written with one square root and one division
+        const double dd = be - al, g2 = 2.0 * ga;
+        const double t = copysign(1.0, dd) * g2 / (fabs(dd) + sqrt(fma(dd, dd, g2 * g2)));
+        const double c = rsqrt(fma(t, t, 1.0)), s = c * t;
+        for (int i = gl; i < rows; i += G) {
           double x = A[i + a * rows], y = A[i + b * rows];
           A[i + a * rows] = c * x - s * y;
           A[i + b * rows] = s * x + c * y;
         }
-        for (int i = ln; i < cols; i += 32) {
+        for (int i = gl; i < cols; i += G) {
           double x = W[i + a * cols], y = W[i + b * cols];
           W[i + a * cols] = c * x - s * y;
           W[i + b * cols] = s * x + c * y;
         }
-        if (ln == 0) changed = 1;
+        if (gl == 0) changed = 1;
       }
       __syncthreads();
     }
-    if (!changed) break;
+    if (!changed) {
+      if (tid == 0) atomicMax(&g_slice_sweeps_max, sweep + 1);
+      break;
+    }
+    if (sweep == 39 && tid == 0) atomicMax(&g_slice_sweeps_max, 40);
     __syncthreads();
   }
   for (int j = warp; j < cols; j += nw) {
@@ -272,22 +317,35 @@ __global__ void __launch_bounds__(1024) slice_svd_kernel(int ra, int rb, const d
   for (int m = tid; m < k; m += nt) s_out[(size_t)nu * k + m] = nrm[order[m]];
 }
 
-// pool all (s, nu, m), sort by s desc, ties (nu, m) asc; s2 sorted, keys, energy = sum s^2
-__global__ void __launch_bounds__(1024) pool_sort_kernel(int K, const double* __restrict__ s, double* s2_sorted,
-                                                         int* key_sorted, double* energy) {
-  __shared__ double red[32];
-  double acc = 0.0;
-  for (int i = threadIdx.x; i < K; i += blockDim.x) {
-    double si = s[i];
-    int rk = 0;
-    for (int j = 0; j < K; ++j) {
-      double sj = s[j];
-      rk += (sj > si) || (sj == si && j < i);
+// pool all (s, nu, m), sort by s desc, ties (nu, m) asc: rank of each element by counting
+// (thread per element, candidates staged through shared-memory tiles); s2 sorted and keys
+__global__ void __launch_bounds__(256) pool_rank_kernel(int K, const double* __restrict__ s, double* s2_sorted,
+                                                        int* key_sorted) {
+  __shared__ double tile[1024];
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const double si = i < K ? s[i] : 0.0;
+  int rk = 0;
+  for (int j0 = 0; j0 < K; j0 += 1024) {
+    const int m = min(1024, K - j0);
+    __syncthreads();
+    for (int t = threadIdx.x; t < m; t += blockDim.x) tile[t] = s[j0 + t];
+    __syncthreads();
+    for (int t = 0; t < m; ++t) {
+      const double sj = tile[t];
+      rk += (sj > si) || (sj == si && j0 + t < i);
     }
+  }
+  if (i < K) {
     s2_sorted[rk] = si * si;
     key_sorted[rk] = i;
-    acc += si * si;
   }
+}
+
+// energy = sum s^2 (single block, fixed order)
+__global__ void __launch_bounds__(1024) pool_energy_kernel(int K, const double* __restrict__ s, double* energy) {
+  __shared__ double red[32];
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < K; i += blockDim.x) acc += s[i] * s[i];
   for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
   __syncthreads();
@@ -432,9 +490,18 @@ TT tucker_to_canonical(fc_ctx c, const double* core, const int r[3], double* con
     FC_CUDA_TRY(cudaFuncSetAttribute(slice_svd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSliceSmem));
     attr = true;
   }
-  slice_svd_kernel<<<rc, 1024, smem, st>>>(ra, rb, S, sv, Ua, Vb, gws);
+  slice_svd_kernel<<<rc, 512, smem, st>>>(ra, rb, S, sv, Ua, Vb, gws);
   FC_CHECK_LAUNCH();
-  pool_sort_kernel<<<1, 1024, 0, st>>>(K, sv, s2s, keys, energy);
+  if (getenv("FC_TRACE")) {
+    int sw = 0, zero = 0;
+    FC_CUDA_TRY(cudaMemcpyFromSymbolAsync(&sw, g_slice_sweeps_max, sizeof(int), 0, cudaMemcpyDeviceToHost, st));
+    FC_CUDA_TRY(cudaMemcpyToSymbolAsync(g_slice_sweeps_max, &zero, sizeof(int), 0, cudaMemcpyHostToDevice, st));
+    FC_CUDA_TRY(cudaStreamSynchronize(st));
+    fprintf(stderr, "[fc t2c] slices %d of %d x %d: max sweeps %d\n", rc, ra, rb, sw);
+  }
+  pool_rank_kernel<<<cdiv(K, 256), 256, 0, st>>>(K, sv, s2s, keys);
+  FC_CHECK_LAUNCH();
+  pool_energy_kernel<<<1, 1024, 0, st>>>(K, sv, energy);
   FC_CHECK_LAUNCH();
   int R;
   if (keep > 0) {

@@ -1,9 +1,5 @@
 mkdir -p gpurun_out
-timeout 300 python -m pytest tests/test_gpu_linalg.py -q --tb=short -x > gpurun_out/pytest_linalg.log 2>&1
-echo "linalg rc=$?"; tail -2 gpurun_out/pytest_linalg.log
-timeout 900 python -m pytest tests/test_gpu_truncate_pcg.py -q --tb=short -x > gpurun_out/pytest_gpu.log 2>&1
+python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/smoke.log 2>&1
+tail -1 gpurun_out/smoke.log
+timeout 1500 python -m pytest tests -m gpu -q --tb=short > gpurun_out/pytest_gpu.log 2>&1
 tail -2 gpurun_out/pytest_gpu.log
-timeout 600 python bench.py --steps 5 --no-cpu-baseline > gpurun_out/bench.jsonl 2> gpurun_out/bench.err
-python -c "
-import json;d=json.loads(open('gpurun_out/bench.jsonl').read().strip().splitlines()[-1])
-print(round(d['value'],2), d['step_ms'], round(d['e2e']['value'],2), d['iters_per_solve'], d['gpu_launches'])"
