@@ -97,6 +97,20 @@ def dist_env():
     return rank, world, local
 
 
+def aggregate_over_ranks(t_seconds: float, iters: int, world: int, device: str):
+    """Whole-job totals of a replicas run: the device time is the MAX over ranks (the job ends
+    when the slowest replica ends), the PCG iterations are SUMMED over ranks."""
+    if world <= 1:
+        return t_seconds, iters
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([t_seconds], dtype=torch.float64, device=device)
+    k = torch.tensor([float(iters)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dist.all_reduce(k, op=dist.ReduceOp.SUM)
+    return float(t.item()), int(round(k.item()))
+
+
 def oracle_sample(n=64, iters_cap=3):
     """Oracle PCG on the C4 workload at n = 64 (bounded): returns (iters, loop seconds)."""
     from oracle import cp as cpm
@@ -201,14 +215,7 @@ def main():
             reps.append(rep)
     barrier()
     launches = (kernel_launches(L) - l0) // max(args.steps, 1)
-    t_total = sum(times) / 1e3
-    if world > 1:
-        import torch.distributed as dist
-        tt = torch.tensor([t_total, float(iters)], dtype=torch.float64, device="cuda")
-        tmax = tt.clone()
-        dist.all_reduce(tmax[:1], op=dist.ReduceOp.MAX)
-        dist.all_reduce(tt[1:], op=dist.ReduceOp.SUM)
-        t_total, iters = float(tmax[0]), int(tt[1])
+    t_total, iters = aggregate_over_ranks(sum(times) / 1e3, iters, world, "cuda")
     value = iters / t_total
 
     # ---- end to end through the public API with HOST buffers ----------------------------
@@ -239,14 +246,8 @@ def main():
         e2e_iters += rep["iters"]
         h2d = 8 * (hw.numel() + 3 * hw.numel() * p.n)
         d2h = 8 * (R + 3 * R * p.n)
-    e2e_value = e2e_iters / (sum(e2e_times) / 1e3)
-    if world > 1:
-        import torch.distributed as dist
-        tt = torch.tensor([sum(e2e_times) / 1e3, float(e2e_iters)], dtype=torch.float64, device="cuda")
-        tmax = tt.clone()
-        dist.all_reduce(tmax[:1], op=dist.ReduceOp.MAX)
-        dist.all_reduce(tt[1:], op=dist.ReduceOp.SUM)
-        e2e_value = float(tt[1]) / float(tmax[0])
+    t_e2e, e2e_iters = aggregate_over_ranks(sum(e2e_times) / 1e3, e2e_iters, world, "cuda")
+    e2e_value = e2e_iters / t_e2e
 
     # ---- dominant kernel class of the step: the DMMA GEMMs (one extra, untimed solve with every
     # GEMM launch bracketed by events on the library stream; algorithmic flops 2MNK) ----------
