@@ -126,21 +126,39 @@ void cross_gram(cudaStream_t st, int n, int R1, const double* const X[3], const 
   gemm(g, st);
 }
 
+// <x, y> = sum_{k,m} xi_k zeta_m prod_l (U_l^T V_l)[k, m]  [P:1748-1755], tiled over (k, m) so
+// the three cross-Grams of a tile stay below ~48 Mi doubles whatever the ranks; the tile sums are
+// added on the host in tile order (deterministic).
 double dot_plain(fc_ctx c, const fc_cp& x, const fc_cp& y) {
   if (x.rank == 0 || y.rank == 0) return 0.0;
   Scratch s(c->st);
   const int R1 = x.rank, R2 = y.rank;
-  double* G = s.alloc<double>((size_t)3 * R1 * R2 + 1);
-  double* out = G + (size_t)3 * R1 * R2;
-  const double* X[3] = {x.U[0], x.U[1], x.U[2]};
-  const double* Y[3] = {y.U[0], y.U[1], y.U[2]};
-  cross_gram(c->st, c->n, R1, X, x.ld, R2, Y, y.ld, G);
-  const double* Gp[3] = {G, G + (size_t)R1 * R2, G + (size_t)2 * R1 * R2};
-  dot_reduce(R1, R2, x.w, y.w, Gp, R1, out, c->st);
-  double h = 0;
-  FC_CUDA_TRY(cudaMemcpyAsync(&h, out, sizeof(double), cudaMemcpyDeviceToHost, c->st));
+  constexpr int TILE = 4096;
+  const int T1 = std::min(R1, TILE), T2 = std::min(R2, TILE);
+  const int n1 = cdiv(R1, T1), n2 = cdiv(R2, T2);
+  double* G = s.alloc<double>((size_t)3 * T1 * T2);
+  double* out = s.alloc<double>((size_t)n1 * n2);
+  for (int a = 0; a < n1; ++a) {
+    const int k0 = a * T1, kr = std::min(T1, R1 - k0);
+    for (int b = 0; b < n2; ++b) {
+      const int m0 = b * T2, mr = std::min(T2, R2 - m0);
+      const double* X[3];
+      const double* Y[3];
+      for (int l = 0; l < 3; ++l) {
+        X[l] = x.U[l] + (size_t)k0 * x.ld[l];
+        Y[l] = y.U[l] + (size_t)m0 * y.ld[l];
+      }
+      cross_gram(c->st, c->n, kr, X, x.ld, mr, Y, y.ld, G);
+      const double* Gp[3] = {G, G + (size_t)kr * mr, G + (size_t)2 * kr * mr};
+      dot_reduce(kr, mr, x.w + k0, y.w + m0, Gp, kr, out + (size_t)a * n2 + b, c->st);
+    }
+  }
+  std::vector<double> h((size_t)n1 * n2);
+  FC_CUDA_TRY(cudaMemcpyAsync(h.data(), out, h.size() * sizeof(double), cudaMemcpyDeviceToHost, c->st));
   FC_CUDA_TRY(cudaStreamSynchronize(c->st));
-  return h;
+  double sum = 0.0;
+  for (double v : h) sum += v;
+  return sum;
 }
 
 void copy_cp_block(cudaStream_t st, int n, const fc_cp& src, fc_cp& dst, int col0, double scale) {

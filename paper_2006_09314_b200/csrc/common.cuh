@@ -39,6 +39,19 @@ inline void require(bool cond, int code, const std::string& msg) {
   if (!cond) throw Error(code, msg);
 }
 
+// stream-ordered allocation; a failure names the size and clears the (non-sticky) error so that
+// the next launch check does not report it again
+inline void* dev_alloc(size_t bytes, cudaStream_t st) {
+  void* p = nullptr;
+  const cudaError_t e = cudaMallocAsync(&p, bytes, st);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    throw Error(FC_ERR_CUDA, "device allocation of " + std::to_string(bytes >> 20) + " MiB failed: " +
+                                 cudaGetErrorString(e));
+  }
+  return p;
+}
+
 inline int cdiv(long long a, long long b) { return (int)((a + b - 1) / b); }
 
 // ---- stream-ordered device scratch (cudaMallocAsync from the device's default pool) ----
@@ -52,7 +65,7 @@ struct Scratch {
     size_t bytes = count * sizeof(T);
     if (bytes == 0) bytes = 16;
     bytes = (bytes + 255) & ~size_t(255);
-    FC_CUDA_TRY(cudaMallocAsync(&p, bytes, st));
+    p = dev_alloc(bytes, st);
     ptrs.push_back(p);
     return (T*)p;
   }

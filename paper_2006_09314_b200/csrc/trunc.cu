@@ -579,6 +579,14 @@ void tt_compute_core(cudaStream_t st, TT& x) {
 // well inside the A23 noise band; it shrinks the eigenproblem (and its N^3 cost) notably.
 constexpr double kBasisTol = 1e-10;
 
+// spectral terms per chunk of the structured norm / Gram pass: t x (Rx * chunk) <= 2^27 doubles
+constexpr size_t kStructChunk = (size_t)1 << 27;
+int struct_chunk(const StructuredS* ss) {
+  const int tmax = std::max(ss->t[0], std::max(ss->t[1], ss->t[2]));
+  const size_t per = (size_t)std::max(tmax, 1) * std::max(ss->Rx, 1);
+  return (int)std::max<size_t>(1, std::min<size_t>((size_t)ss->r, kStructChunk / per));
+}
+
 TT truncate_tt(fc_ctx c, const TT& xin, double eps, int rank_cap, TruncStats* stats, const StructuredS* ss) {
   cudaStream_t st = c->st;
   const int n = xin.n, R = xin.R;
@@ -695,29 +703,41 @@ TT truncate_tt(fc_ctx c, const TT& xin, double eps, int rank_cap, TruncStats* st
     term_norms_kernel<<<dim3(cdiv(R, 8), 3), 256, 0, st>>>(R, ta);
     FC_CHECK_LAUNCH();
   } else {
-    // n2[kk*Rx + j] = cx_j^T Gm_kk cx_j with Gm_kk = Rm_kk^T Rm_kk (t x t), P_kk = Gm_kk Cx
-    const int r = ss->r, Rx = ss->Rx;
-    GemmArgs gg, gp;
+    // n2[kk*Rx + j] = cx_j^T Gm_kk cx_j with Gm_kk = Rm_kk^T Rm_kk (t x t), P_kk = Gm_kk Cx,
+    // chunked over the spectral terms kk so that P stays below kStructChunk doubles per mode
+    const int r = ss->r, Rx = ss->Rx, kc = struct_chunk(ss);
+    GemmArgs gg;
     gg.transA = 1;
-    gg.nbatch = gp.nbatch = 3;
-    gg.rep = gp.rep = r;
-    StructNormArgs na;
+    gg.nbatch = 3;
+    gg.rep = r;
+    double* Gm[3];
+    double* P[3];
     for (int l = 0; l < 3; ++l) {
       const int t = ss->t[l], k = q[l];
-      double* Gm = s.alloc<double>((size_t)t * t * r);
-      double* P = s.alloc<double>((size_t)t * R);
-      gg.b[l] = GemmBatch{t, t, k, RmE[l], k, RmE[l], k, Gm, t, nullptr, 0, nullptr};
+      Gm[l] = s.alloc<double>((size_t)t * t * r);
+      P[l] = s.alloc<double>((size_t)t * Rx * kc);
+      gg.b[l] = GemmBatch{t, t, k, RmE[l], k, RmE[l], k, Gm[l], t, nullptr, 0, nullptr};
       gg.b[l].sA = gg.b[l].sB = (long long)k * t;
       gg.b[l].sC = (long long)t * t;
-      gp.b[l] = GemmBatch{t, Rx, t, Gm, t, ss->Cx[l], t, P, t, nullptr, 0, nullptr};
-      gp.b[l].sA = (long long)t * t;
-      gp.b[l].sC = (long long)t * Rx;
-      na.Cx[l] = ss->Cx[l]; na.P[l] = P; na.t[l] = t; na.n2[l] = n2[l];
     }
     gemm(gg, st);
-    gemm(gp, st);
-    struct_norms_kernel<<<dim3(cdiv(R, 8), 3), 256, 0, st>>>(R, Rx, na);
-    FC_CHECK_LAUNCH();
+    for (int k0 = 0; k0 < r; k0 += kc) {
+      const int nk = std::min(kc, r - k0);
+      GemmArgs gp;
+      gp.nbatch = 3;
+      gp.rep = nk;
+      StructNormArgs na;
+      for (int l = 0; l < 3; ++l) {
+        const int t = ss->t[l];
+        gp.b[l] = GemmBatch{t, Rx, t, Gm[l] + (size_t)k0 * t * t, t, ss->Cx[l], t, P[l], t, nullptr, 0, nullptr};
+        gp.b[l].sA = (long long)t * t;
+        gp.b[l].sC = (long long)t * Rx;
+        na.Cx[l] = ss->Cx[l]; na.P[l] = P[l]; na.t[l] = t; na.n2[l] = n2[l] + (size_t)k0 * Rx;
+      }
+      gemm(gp, st);
+      struct_norms_kernel<<<dim3(cdiv(nk * Rx, 8), 3), 256, 0, st>>>(nk * Rx, Rx, na);
+      FC_CHECK_LAUNCH();
+    }
   }
   term_weights_kernel<<<1, 1024, 0, st>>>(R, xin.w, n2[0], n2[1], n2[2], xi, dl[0], dl[1], dl[2], inv[0], inv[1],
                                           inv[2], energy);
@@ -727,33 +747,49 @@ TT truncate_tt(fc_ctx c, const TT& xin, double eps, int rank_cap, TruncStats* st
   double* M[3];
   if (ss) {
     // M_l = sum_kk Rm_kk H_kk Rm_kk^T,  H_kk = W_kk W_kk^T,  W_kk = Cx diag(d_l[kk*Rx + .])
-    // (t x t per spectral term): G_kk = Rm_kk H_kk, then M = [G_1 .. G_r] [Rm_1 .. Rm_r]^T
-    const int r = ss->r, Rx = ss->Rx;
-    GemmArgs gh, gq, m;
-    gh.transB = 1;
+    // (t x t per spectral term, W chunked over kk): G_kk = Rm_kk H_kk, then
+    // M = [G_1 .. G_r] [Rm_1 .. Rm_r]^T
+    const int r = ss->r, Rx = ss->Rx, kc = struct_chunk(ss);
+    double* W[3];
+    double* H[3];
+    double* G[3];
+    for (int l = 0; l < 3; ++l) {
+      W[l] = s.alloc<double>((size_t)ss->t[l] * Rx * kc);
+      H[l] = s.alloc<double>((size_t)ss->t[l] * ss->t[l] * r);
+      G[l] = s.alloc<double>((size_t)q[l] * ss->t[l] * r);
+    }
+    for (int k0 = 0; k0 < r; k0 += kc) {
+      const int nk = std::min(kc, r - k0);
+      GemmArgs gh;
+      gh.transB = 1;
+      gh.nbatch = 3;
+      gh.rep = nk;
+      for (int l = 0; l < 3; ++l) {
+        const int t = ss->t[l];
+        struct_scale_kernel<<<blocks_for((long long)t * Rx * nk), 256, 0, st>>>(t, nk * Rx, Rx, ss->Cx[l],
+                                                                                 dl[l] + (size_t)k0 * Rx, W[l]);
+        FC_CHECK_LAUNCH();
+        gh.b[l] = GemmBatch{t, t, Rx, W[l], t, W[l], t, H[l] + (size_t)k0 * t * t, t, nullptr, 0, nullptr};
+        gh.b[l].sA = gh.b[l].sB = (long long)t * Rx;
+        gh.b[l].sC = (long long)t * t;
+      }
+      gemm(gh, st);
+    }
+    GemmArgs gq, m;
     m.transB = 1;
-    gh.nbatch = gq.nbatch = m.nbatch = 3;
-    gh.rep = gq.rep = r;
+    gq.nbatch = m.nbatch = 3;
+    gq.rep = r;
     int tiles = 0, minkd = INT32_MAX;
     for (int l = 0; l < 3; ++l) {
       const int t = ss->t[l], k = q[l];
-      double* W = s.alloc<double>((size_t)t * R);
-      struct_scale_kernel<<<blocks_for((long long)t * R), 256, 0, st>>>(t, R, Rx, ss->Cx[l], dl[l], W);
-      FC_CHECK_LAUNCH();
-      double* H = s.alloc<double>((size_t)t * t * r);
-      double* G = s.alloc<double>((size_t)k * t * r);
-      gh.b[l] = GemmBatch{t, t, Rx, W, t, W, t, H, t, nullptr, 0, nullptr};
-      gh.b[l].sA = gh.b[l].sB = (long long)t * Rx;
-      gh.b[l].sC = (long long)t * t;
-      gq.b[l] = GemmBatch{k, t, t, RmE[l], k, H, t, G, k, nullptr, 0, nullptr};
+      gq.b[l] = GemmBatch{k, t, t, RmE[l], k, H[l], t, G[l], k, nullptr, 0, nullptr};
       gq.b[l].sA = gq.b[l].sC = (long long)k * t;
       gq.b[l].sB = (long long)t * t;
       M[l] = s.zeros<double>((size_t)k * k);
-      m.b[l] = GemmBatch{k, k, t * r, G, k, RmE[l], k, M[l], k, nullptr, 0, nullptr};
+      m.b[l] = GemmBatch{k, k, t * r, G[l], k, RmE[l], k, M[l], k, nullptr, 0, nullptr};
       tiles += cdiv(k, 64) * cdiv(k, 64);
       minkd = std::min(minkd, t * r);
     }
-    gemm(gh, st);
     gemm(gq, st);
     m.beta = 1.0;
     m.splitk = std::max(1, std::min(cdiv(minkd, 128), std::max(1, 148 * 3 / std::max(tiles, 1))));

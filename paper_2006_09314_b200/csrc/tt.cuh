@@ -15,7 +15,7 @@ struct DevMem {               // move-only stream-ordered allocation
   DevMem() = default;
   DevMem(size_t bytes, cudaStream_t s) : st(s) {
     if (bytes == 0) bytes = 16;
-    FC_CUDA_TRY(cudaMallocAsync(&p, (bytes + 255) & ~size_t(255), s));
+    p = dev_alloc((bytes + 255) & ~size_t(255), s);
   }
   DevMem(const DevMem&) = delete;
   DevMem& operator=(const DevMem&) = delete;

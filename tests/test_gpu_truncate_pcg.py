@@ -67,9 +67,12 @@ def test_truncate_concat_and_duplicates(lib, n, R1, R2):
     y, info = ctx.cp_truncate(DeviceCP.from_numpy(x.w, x.U), 1e-6)
     assert y.rank == ref.rank
     assert reldiff(_cp(y), ref) <= 1e-6
+    # duplicated terms [a; a] = 2a: the Tucker ranks are exact, so the RHOSVD tails vanish and
+    # the only loss is the T2C pooled cut of the recomputed core, <= (eps/2) ||2a|| (A10/A11)
     d = cpm.CP(np.concatenate([a.w, a.w]), [np.concatenate([u, u], axis=1) for u in a.U])
     y, info = ctx.cp_truncate(DeviceCP.from_numpy(d.w, d.U), 1e-8)
-    assert reldiff(_cp(y), cpm.scale(2.0, a)) <= 1e-9
+    assert reldiff(_cp(y), cpm.scale(2.0, a)) <= 0.5e-8 + 1e-12
+    assert y.rank <= 2 * a.rank
 
 
 @pytest.mark.parametrize("name,n,R,which", [("C1", 16, 2, 0), ("C1", 32, 3, 1), ("C3b", 24, 4, 0),
@@ -102,7 +105,7 @@ def test_truncate_zero_and_rank1(lib):
     assert y.rank == 0
 
 
-@pytest.mark.parametrize("name,n", [("C1", 32), ("C1", 16), ("C3b", 24)])
+@pytest.mark.parametrize("name,n", [("C1", 32), ("C1", 16), ("C3b", 24), ("C4", 32)])
 def test_pcg_parity_shared(lib, name, n):
     from paper_2006_09314_b200.binding import DeviceCP, make_params
     p = make_problem(name, n=n)
@@ -114,7 +117,22 @@ def test_pcg_parity_shared(lib, name, n):
     u, rep, rc = ctx.pcg_solve(b, prm)
     assert rc == 0 and rep["converged"]
     check_rank_history(rep, rep_ref)
-    assert reldiff(_cp(u), u_ref) <= max(10 * p.eps, 1e-9)
+    d = reldiff(_cp(u), u_ref)
+    assert d <= max(10 * p.eps, 1e-9)
+    # true residual ||B - F(u)||/||B|| (O11) on both sides: the two differ by at most
+    # ||F(u_gpu - u_oracle)|| / ||B|| <= F_max ||u_gpu - u_oracle|| / ||B||  (+ dot rounding)
+    from paper_2006_09314_b200.binding import FC_F
+    from oracle.measure import diff_norm
+    B = cpm.normalized(p.b_w, p.b_U)
+    fun = lambda x: cpm.apply(st.V, st.F, x)
+    true_ref = diff_norm(fun(u_ref), B) / cpm.norm(B)
+    Fu = ctx.fracop_apply(FC_F, u)
+    r = ctx.cp_axpy(b, -1.0, Fu)
+    true_gpu = np.sqrt(max(ctx.cp_dot(r, r), 0.0) / ctx.cp_dot(b, b))
+    f = sp.spectral_fn(sp.FC_F, p.alpha, p.beta)
+    fmax = max(f(sum(l[-1] for l in st.lams)), f(sum(l[0] for l in st.lams)))
+    slack = fmax * d * cpm.norm(u_ref) / cpm.norm(B) + 1e-7
+    assert abs(true_gpu - true_ref) <= slack, (true_gpu, true_ref, slack)
 
 
 MARGIN_BAND = 5e-3   # relative distance of thr to a bracketing tail below which a cut is marginal

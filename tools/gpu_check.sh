@@ -1,5 +1,3 @@
 mkdir -p gpurun_out
-python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/smoke.log 2>&1
-tail -1 gpurun_out/smoke.log
-timeout 1500 python -m pytest tests -m gpu -q --tb=short > gpurun_out/pytest_gpu.log 2>&1
-tail -2 gpurun_out/pytest_gpu.log
+timeout 1500 python -m pytest tests/test_gpu_fullsize.py tests/test_gpu_truncate_pcg.py tests/test_gpu_apply.py -q -s --tb=short > gpurun_out/pytest_gpu.log 2>&1
+tail -3 gpurun_out/pytest_gpu.log
