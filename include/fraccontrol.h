@@ -72,7 +72,15 @@ typedef struct {
     int op_rank;         /* > 0: fixed rank of the operator CP (C5 sweep); 0: eps_D-driven  */
     int rank_cap;        /* max CP rank of any iterate (capacity); <= 0 -> 2^20             */
     int boundary;        /* 0: paper boundary rule [P:517-518] (A2); 1: standard            */
+    int precond_case;    /* FC_PRECOND_B (0, default, A6) or FC_PRECOND_A (1)   [P:758-868] */
 } fc_params;
+
+/* preconditioner cases [P:758-768] */
+#define FC_PRECOND_B  0   /* direct low-rank G = 1/F(A) in the SL eigenbasis of A (reading A6)    */
+#define FC_PRECOND_A  1   /* G = B_0^-1, B_0 = F(B), B the anisotropic Laplacian with constant    */
+                          /* b0_l = (max a_l + min a_l)/2 [P:842-849, P:1462-1467], diagonal in   */
+                          /* the DST-I basis: lam_k = b0_l 4/h^2 sin^2(k pi h / 2) [P:778-785];    */
+                          /* cond(B_0^-1 F(A)) is bounded independently of n (Theorem [P:871-938]) */
 
 typedef struct {
     int tucker_rank[3];  /* RHOSVD ranks r_l                                                */
@@ -128,6 +136,13 @@ int sl_set_eigen(fc_ctx ctx, int n, int mode, const double* lam, const double* V
 int op_get_spectral_cp(fc_ctx ctx, int which, fc_cp* out);
 int op_set_spectral_cp(fc_ctx ctx, int which, const fc_cp* in);
 int op_spectral_rank(fc_ctx ctx, int which, int* rank, int* tucker_rank /* [3] or NULL */);
+/* Case-(A) preconditioner basis of mode `mode` (FC_PRECOND_A): lam (device, n, ascending
+ * b0-scaled Laplacian eigenvalues) and V (device, n x n column-major, the DST-I basis).
+ * get: NOT_READY unless sl_setup ran with precond_case = FC_PRECOND_A or a basis was set.
+ * set (shared-input parity): copies; once all 3 modes are set the FC_G spectral CP is applied
+ * in this basis (its CP must then be built on these lam, op_set_spectral_cp). */
+int op_get_precond_basis(fc_ctx ctx, int mode, double* lam, double* V);
+int op_set_precond_basis(fc_ctx ctx, int mode, const double* lam, const double* V);
 
 /* ---- the operator: S5..S8 -------------------------------------------------------------- */
 /* fracop_apply  [P:597-623]:  y = F(A) x  =  sum_k sum_j (x)_l V_l (u_l^k . V_l^T x_l^j)

@@ -15,7 +15,7 @@ import numpy as np
 
 from . import cp as cpm
 from .cp import CP
-from .sturm import eigenpairs
+from .sturm import dst1_basis, effective_midpoints, eigenpairs, laplace_eigenvalues
 from .spectral import FC_F, FC_G, spectral_cp
 from .truncate import truncate
 
@@ -27,10 +27,27 @@ class Setup:
     F: CP
     G: CP
     info: dict = field(default_factory=dict)
+    lamsG: list = None         # eigenvalues G is a function of (= lams in case (B))
+    VG: list = None            # basis G is applied in (= V in case (B))
+
+
+def precond_basis_A(problem):
+    """Case (A) [P:842-849]: b0_l = (max a_l + min a_l)/2 over the coefficient values the operator
+    uses (majorant / minorant on the grid, A2's effective midpoints); B = sum_l b0_l (1D Laplacian)
+    is diagonal in the DST-I basis [P:778-785]: lam_k = b0_l 4/h^2 sin^2(k pi h/2).
+    Returns (b0, lams, V)."""
+    b0, lams, V = [], [], []
+    for l in range(3):
+        a = effective_midpoints(problem.a_mid[l], problem.boundary)
+        b0.append(0.5 * (a.max() + a.min()))
+        lams.append(b0[-1] * laplace_eigenvalues(problem.n))
+        V.append(dst1_basis(problem.n))
+    return b0, lams, V
 
 
 def setup(problem, F_rank=None, G_rank=None, eps_D=None) -> Setup:
-    """sl_setup: O2/O3 per mode, then O5 for F (eps_D-driven) and G (rank r_G, SPD guard)."""
+    """sl_setup: O2/O3 per mode, then O5 for F (eps_D-driven) and G (rank r_G, SPD guard);
+    in case (A) G = 1/F over the b0-Laplacian's eigenvalues, applied in the DST-I basis."""
     lams, V = [], []
     for l in range(3):
         lam, Vl = eigenpairs(problem.a_mid[l], problem.boundary)
@@ -39,10 +56,13 @@ def setup(problem, F_rank=None, G_rank=None, eps_D=None) -> Setup:
     eps_D = problem.eps if eps_D is None else eps_D
     infoF, infoG = {}, {}
     F = spectral_cp(lams, FC_F, problem.alpha, problem.beta, eps_D, rank=F_rank, info=infoF)
-    G = spectral_cp(lams, FC_G, problem.alpha, problem.beta, eps_D,
+    lamsG, VG = lams, V
+    if getattr(problem, "precond", "B") == "A":
+        _, lamsG, VG = precond_basis_A(problem)
+    G = spectral_cp(lamsG, FC_G, problem.alpha, problem.beta, eps_D,
                     rank=problem.precond_rank if G_rank is None else G_rank,
                     spd_guard=True, info=infoG)
-    return Setup(lams, V, F, G, {"F": infoF, "G": infoG})
+    return Setup(lams, V, F, G, {"F": infoF, "G": infoG}, lamsG, VG)
 
 
 class NotSPD(RuntimeError):
@@ -98,7 +118,7 @@ def solve(problem, st: Setup | None = None, kmax=None, with_true_residual=False)
     st = setup(problem) if st is None else st
     B = cpm.normalized(problem.b_w, problem.b_U)
     fun = lambda x: cpm.apply(st.V, st.F, x)
-    pre = lambda x: cpm.apply(st.V, st.G, x)
+    pre = lambda x: cpm.apply(st.VG if st.VG is not None else st.V, st.G, x)
     u, rep = pcg(fun, pre, B, problem.eps, problem.tol_stop,
                  problem.kmax if kmax is None else kmax)
     if with_true_residual:                                   # O11

@@ -67,8 +67,9 @@ def spectral_cp(lams, kind: int, alpha: float, beta: float, eps: float,
                 rank: int | None = None, spd_guard: bool = False, info: dict | None = None) -> CP:
     """O5: CP of D = F(lambda-sum): HOSVD at eps, then T2C (cut (eps/2) or top `rank`).
 
-    SPD guard (reading A7): when `spd_guard`, the rank is raised until the CP is
-    positive on the whole grid.
+    SPD guard (readings A7/A7'/A7''): when `spd_guard`, the rank is raised (up to 64), then the
+    Tucker tolerance tightened (down to eps/1e4), until the CP is positive on the whole grid;
+    failing that, a constant term 2|min| + 1e-15 sum|w| makes it positive.
     """
     D = coefficient_tensor(lams, kind, alpha, beta)
     core, Z = hosvd(D, eps)
@@ -84,7 +85,8 @@ def spectral_cp(lams, kind: int, alpha: float, beta: float, eps: float,
             # if the Tucker approximation itself is not positive at that accuracy, tighten its
             # tolerance tenfold and repeat (up to eps/1e4)
             e = eps
-            while cp_min_entry(out) <= 0:
+            shift = 0.0
+            while (mn := cp_min_entry(out)) <= 0:
                 if r < min(64, int(np.prod(core.shape))):
                     r += 1
                 elif e > eps * 1e-4:
@@ -92,10 +94,19 @@ def spectral_cp(lams, kind: int, alpha: float, beta: float, eps: float,
                     core, Z = hosvd(D, e)
                     r = rank
                 else:
+                    # reading A7'': still not positive (entries of D spanning many decades keep
+                    # a rounding-level negative lobe): add the constant s (x) 1 (x) 1 (x) 1 with
+                    # s = 2|min| + 1e-15 sum|w|  (sum|w| bounds the largest entry)
+                    shift = 2.0 * abs(mn) + 1e-15 * float(np.sum(np.abs(out.w)))
+                    n1 = [u.shape[0] for u in out.U]
+                    one = [np.full((k, 1), 1.0 / np.sqrt(k)) for k in n1]
+                    out = CP(np.append(out.w, shift * np.sqrt(float(np.prod(n1)))),
+                             [np.hstack([u, o]) for u, o in zip(out.U, one)])
                     break
                 out = tucker_to_canonical(core, Z, None, keep=r)
             if info is not None:
                 info["guard_eps"] = e
+                info["guard_shift"] = shift
     if info is not None:
         info["rank"] = out.rank
         diff = np.einsum("k,ik,jk,lk->ijl", out.w, out.U[0], out.U[1], out.U[2]) - D

@@ -15,6 +15,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libfraccontrol.so")
 
 FC_F, FC_G, FC_POW_PLUS, FC_POW_MINUS = 0, 1, 2, 3
+FC_PRECOND_B, FC_PRECOND_A = 0, 1
 FC_MAX_ITERS = 256
 STATUS = {0: "OK", 1: "NOT_CONVERGED", 2: "RANK_CAP_HIT", -1: "INVALID_ARG", -2: "SHAPE",
           -3: "CAPACITY", -4: "NONPOS_COEF", -5: "NOT_SPD", -6: "NAN", -7: "EIG_NOCONV",
@@ -30,7 +31,7 @@ class fc_params(C.Structure):
     _fields_ = [("alpha", C.c_double), ("beta", C.c_double), ("eps", C.c_double),
                 ("tol_stop", C.c_double), ("eps_D", C.c_double), ("kmax", C.c_int),
                 ("precond_rank", C.c_int), ("op_rank", C.c_int), ("rank_cap", C.c_int),
-                ("boundary", C.c_int)]
+                ("boundary", C.c_int), ("precond_case", C.c_int)]
 
 
 class fc_trunc_info(C.Structure):
@@ -68,7 +69,7 @@ ENTRY_POINTS = ["fc_create", "fc_destroy", "fc_last_error", "fc_set_stream", "sl
                 "sl_set_eigen", "op_get_spectral_cp", "op_set_spectral_cp", "op_spectral_rank",
                 "fracop_apply", "precond_apply", "cp_dot", "cp_axpy", "cp_truncate", "pcg_solve",
                 "fc_dgemm", "fc_last_kernel_stats", "fc_kernel_launches", "fracop_apply_truncate", "fc_orthonormalize",
-                "fc_profile_gemm", "fc_syev"]
+                "fc_profile_gemm", "fc_syev", "op_get_precond_basis", "op_set_precond_basis"]
 
 
 def load_library(path: str = LIB_PATH) -> C.CDLL:
@@ -98,6 +99,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "fc_profile_gemm": ([P, I, C.POINTER(D), C.POINTER(D), C.POINTER(C.c_longlong)], I),
         "fc_syev": ([P, I, C.POINTER(I), C.POINTER(P), C.POINTER(I), C.POINTER(P), C.POINTER(P), C.POINTER(I),
                      C.POINTER(I)], I),
+        "op_get_precond_basis": ([P, I, P, P], I), "op_set_precond_basis": ([P, I, P, P], I),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -107,8 +109,9 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
 
 
 def make_params(alpha, beta, eps, tol_stop=0.0, eps_D=0.0, kmax=0, precond_rank=0, op_rank=0,
-                rank_cap=0, boundary=0) -> fc_params:
-    return fc_params(alpha, beta, eps, tol_stop, eps_D, kmax, precond_rank, op_rank, rank_cap, boundary)
+                rank_cap=0, boundary=0, precond_case=FC_PRECOND_B) -> fc_params:
+    return fc_params(alpha, beta, eps, tol_stop, eps_D, kmax, precond_rank, op_rank, rank_cap, boundary,
+                     precond_case)
 
 
 class DeviceCP:
@@ -195,6 +198,19 @@ class Context:
         Vt = torch.empty(self.n, self.n, dtype=torch.float64, device="cuda")   # (col, row) = V^T row-major
         self._check(self.lib.sl_get_eigen(self.h, mode, lam.data_ptr(), Vt.data_ptr()))
         return lam, Vt.T
+
+    def op_get_precond_basis(self, mode):
+        import torch
+        lam = torch.empty(self.n, dtype=torch.float64, device="cuda")
+        Vt = torch.empty(self.n, self.n, dtype=torch.float64, device="cuda")
+        self._check(self.lib.op_get_precond_basis(self.h, mode, lam.data_ptr(), Vt.data_ptr()))
+        return lam, Vt.T
+
+    def op_set_precond_basis(self, mode, lam, V):
+        import torch
+        lam_t = torch.as_tensor(np.asarray(lam, dtype=np.float64), device="cuda").contiguous()
+        Vt = torch.as_tensor(np.ascontiguousarray(np.asarray(V, dtype=np.float64).T), device="cuda")
+        self._check(self.lib.op_set_precond_basis(self.h, mode, lam_t.data_ptr(), Vt.data_ptr()))
 
     def sl_set_eigen(self, n, mode, lam, V, params: fc_params | None = None):
         import torch

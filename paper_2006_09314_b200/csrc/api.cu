@@ -62,7 +62,7 @@ void apply_plain(fc_ctx c, const SpecCP& sp, const fc_cp& x, fc_cp& y) {
   f.transA = 1;
   f.nbatch = 3;
   for (int l = 0; l < 3; ++l)
-    f.b[l] = GemmBatch{n, R, n, c->V_l(l), n, x.U[l], x.ld[l], What + (size_t)l * n * R, n, nullptr, 0, nullptr};
+    f.b[l] = GemmBatch{n, R, n, c->Vsp(sp, l), n, x.U[l], x.ld[l], What + (size_t)l * n * R, n, nullptr, 0, nullptr};
   gemm(f, st);
 
   // S8 (moved ahead): column norms of u_k (.) w_j; ||V y|| = ||y|| since V is orthogonal
@@ -91,7 +91,7 @@ void apply_plain(fc_ctx c, const SpecCP& sp, const fc_cp& x, fc_cp& y) {
   iv.nbatch = 3;
   iv.krR = R;
   for (int l = 0; l < 3; ++l)
-    iv.b[l] = GemmBatch{n, r * R, n, c->V_l(l), n, What + (size_t)l * n * R, n, y.U[l], y.ld[l],
+    iv.b[l] = GemmBatch{n, r * R, n, c->Vsp(sp, l), n, What + (size_t)l * n * R, n, y.U[l], y.ld[l],
                         sp.Ul(n, l), n, csp[l]};
   // wave balance: with one 128x128 CTA per SM, split K until the grid covers >= 3 waves
   const long long tiles = 3LL * cdiv(n, 128) * cdiv((long long)r * R, 128);
@@ -342,16 +342,51 @@ int sl_set_eigen(fc_ctx c, int n, int mode, const double* lam, const double* V, 
       c->lam.ensure((size_t)3 * n);
       c->V.ensure((size_t)3 * n * n);
       for (auto& h : c->have_eig) h = false;
-      for (auto& s : c->spec) s.valid = false;
+      for (auto& h : c->have_A) h = false;
+      for (auto& s : c->spec) {
+        s.valid = false;
+        s.basis = nullptr;
+      }
     }
     if (p) {
       c->p = *p;
       c->have_params = true;
+      if (p->precond_case == FC_PRECOND_B) c->spec[FC_G].basis = nullptr;
     }
     FC_CUDA_TRY(cudaMemcpyAsync(c->lam_l(mode), lam, (size_t)n * 8, cudaMemcpyDeviceToDevice, c->st));
     FC_CUDA_TRY(cudaMemcpyAsync(c->V_l(mode), V, (size_t)n * n * 8, cudaMemcpyDeviceToDevice, c->st));
     FC_CUDA_TRY(cudaStreamSynchronize(c->st));
     c->have_eig[mode] = true;
+    return FC_OK;
+  });
+}
+
+int op_get_precond_basis(fc_ctx c, int mode, double* lam, double* V) {
+  return guard(c, [&]() {
+    require(mode >= 0 && mode < 3, FC_ERR_INVALID_ARG, "mode");
+    require(c->n > 0 && c->have_A[mode], FC_ERR_NOT_READY, "no case-(A) preconditioner basis");
+    const size_t n = c->n;
+    if (lam)
+      FC_CUDA_TRY(cudaMemcpyAsync(lam, c->lamA.p + (size_t)mode * n, n * 8, cudaMemcpyDeviceToDevice, c->st));
+    if (V)
+      FC_CUDA_TRY(cudaMemcpyAsync(V, c->VA.p + (size_t)mode * n * n, n * n * 8, cudaMemcpyDeviceToDevice, c->st));
+    FC_CUDA_TRY(cudaStreamSynchronize(c->st));
+    return FC_OK;
+  });
+}
+
+int op_set_precond_basis(fc_ctx c, int mode, const double* lam, const double* V) {
+  return guard(c, [&]() {
+    require(mode >= 0 && mode < 3 && lam && V, FC_ERR_INVALID_ARG, "op_set_precond_basis args");
+    require(c->n > 0, FC_ERR_NOT_READY, "set the eigenpairs (n) first");
+    const size_t n = c->n;
+    c->lamA.ensure(3 * n);
+    c->VA.ensure(3 * n * n);
+    FC_CUDA_TRY(cudaMemcpyAsync(c->lamA.p + (size_t)mode * n, lam, n * 8, cudaMemcpyDeviceToDevice, c->st));
+    FC_CUDA_TRY(cudaMemcpyAsync(c->VA.p + (size_t)mode * n * n, V, n * n * 8, cudaMemcpyDeviceToDevice, c->st));
+    FC_CUDA_TRY(cudaStreamSynchronize(c->st));
+    c->have_A[mode] = true;
+    if (c->have_A[0] && c->have_A[1] && c->have_A[2]) c->spec[FC_G].basis = c->VA.p;
     return FC_OK;
   });
 }

@@ -14,6 +14,9 @@ struct SpecCP {
   bool valid = false;
   bool has_basis = false;
   int tucker_rank[3] = {0, 0, 0};
+  // eigenbasis the CP is diagonal in (3 x n x n, mode-major); nullptr: the context's SL basis V.
+  // The case-(A) preconditioner (FC_PRECOND_A) lives in the DST-I basis of the b0-Laplacian.
+  const double* basis = nullptr;
   double* Ul(int n, int l) const { return U.p + (size_t)l * n * r; }
 };
 
@@ -26,6 +29,9 @@ struct fc_ctx_s {
   fc::DBuf lam;       // 3 x n
   fc::DBuf V;         // 3 x n x n (mode-major, each column-major)
   bool have_eig[3] = {false, false, false};
+  fc::DBuf lamA;      // case-(A) preconditioner: b0-scaled Laplacian eigenvalues, 3 x n
+  fc::DBuf VA;        // ... and the DST-I basis, 3 x n x n
+  bool have_A[3] = {false, false, false};
   SpecCP spec[4];
   std::string err;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -33,4 +39,6 @@ struct fc_ctx_s {
   int k_launches = 0;
   double* lam_l(int l) const { return lam.p + (size_t)l * n; }
   double* V_l(int l) const { return V.p + (size_t)l * n * n; }
+  // the eigenbasis a spectral CP is applied in
+  const double* Vsp(const SpecCP& sp, int l) const { return sp.basis ? sp.basis + (size_t)l * n * n : V_l(l); }
 };

@@ -143,7 +143,7 @@ TT apply_truncate_tt(fc_ctx c, SpecCP& sp, const TT& x, double eps, int rank_cap
   for (int l = 0; l < 3; ++l) {
     Zh[l] = p;
     p += (size_t)n * x.q[l];
-    fwd.b[l] = GemmBatch{n, x.q[l], n, c->V_l(l), n, x.Q[l], n, Zh[l], n, nullptr, 0, nullptr};
+    fwd.b[l] = GemmBatch{n, x.q[l], n, c->Vsp(sp, l), n, x.Q[l], n, Zh[l], n, nullptr, 0, nullptr};
   }
   gemm(fwd, st);
   StructuredS ss;
@@ -172,7 +172,7 @@ TT apply_truncate_tt(fc_ctx c, SpecCP& sp, const TT& x, double eps, int rank_cap
   for (int l = 0; l < 3; ++l) {
     if (out.R == 0) break;
     newQ.emplace_back((size_t)n * out.q[l] * 8, st);
-    inv.b[inv.nbatch++] = GemmBatch{n, out.q[l], n, c->V_l(l), n, out.Q[l], n, newQ.back().d(), n, nullptr, 0, nullptr};
+    inv.b[inv.nbatch++] = GemmBatch{n, out.q[l], n, c->Vsp(sp, l), n, out.Q[l], n, newQ.back().d(), n, nullptr, 0, nullptr};
   }
   if (inv.nbatch) {
     gemm(inv, st);

@@ -105,7 +105,8 @@ __device__ __forceinline__ double key_to_double(unsigned long long k) {
 }
 
 // min over the full n^3 grid of sum_t w_t U1[i,t] U2[j,t] U3[k,t]; thread per (i, j)
-constexpr int kGuardMaxR = 64;
+constexpr int kGuardMaxR = 64;        // rank search limit of the SPD guard (A7)
+constexpr int kCpMinMaxR = kGuardMaxR + 1;   // + the A7'' constant term
 __global__ void cp_min_kernel(int n, int r, const double* __restrict__ w, const double* __restrict__ U1,
                               const double* __restrict__ U2, const double* __restrict__ U3,
                               unsigned long long* out) {
@@ -113,7 +114,7 @@ __global__ void cp_min_kernel(int n, int r, const double* __restrict__ w, const 
   double mn = 1e300;
   if (ij < (long long)n * n) {
     int i = (int)(ij % n), j = (int)(ij / n);
-    double a[kGuardMaxR];
+    double a[kCpMinMaxR];
 #pragma unroll 8
     for (int t = 0; t < r; ++t) a[t] = w[t] * U1[i + (size_t)t * n] * U2[j + (size_t)t * n];
     for (int k = 0; k < n; ++k) {
@@ -141,9 +142,10 @@ struct CoreResult {
   double* Z[3] = {nullptr, nullptr, nullptr};
 };
 
-CoreResult spectral_tucker(fc_ctx c, int kind, double alpha, double beta, double eps) {
+CoreResult spectral_tucker(fc_ctx c, int kind, double alpha, double beta, double eps, const double* lam3) {
   cudaStream_t st = c->st;
   const int n = c->n;
+  auto lam_l = [&](int l) { return lam3 + (size_t)l * n; };
   Scratch s(st);
   const int p = std::min(kSamples, n);
   int q[3];
@@ -152,7 +154,7 @@ CoreResult spectral_tucker(fc_ctx c, int kind, double alpha, double beta, double
   for (int l = 0; l < 3; ++l) {
     const int la = (l == 0) ? 1 : 0, lb = (l == 2) ? 1 : 2;
     double* Phi = s.alloc<double>((size_t)n * p);
-    sample_fibres_kernel<<<nblk((long long)n * p), 256, 0, st>>>(n, p, c->lam_l(l), c->lam_l(la), c->lam_l(lb), kind,
+    sample_fibres_kernel<<<nblk((long long)n * p), 256, 0, st>>>(n, p, lam_l(l), lam_l(la), lam_l(lb), kind,
                                                                  alpha, beta, Phi);
     FC_CHECK_LAUNCH();
     // orthonormal basis of range(Phi) by column-pivoted MGS (rank revealing, no squaring):
@@ -177,9 +179,9 @@ CoreResult spectral_tucker(fc_ctx c, int kind, double alpha, double beta, double
     g.gen.kind = kind;
     g.gen.alpha = alpha;
     g.gen.beta = beta;
-    g.gen.l1 = c->lam_l(0);
-    g.gen.l2 = c->lam_l(1);
-    g.gen.l3 = c->lam_l(2);
+    g.gen.l1 = lam_l(0);
+    g.gen.l2 = lam_l(1);
+    g.gen.l3 = lam_l(2);
     g.gen.n1 = n;
     g.nbatch = 1;
     g.b[0] = GemmBatch{(int)nn, q[2], n, nullptr, (int)nn, Q[2], n, T3, (int)nn, nullptr, 0, nullptr};
@@ -257,7 +259,7 @@ CoreResult spectral_tucker(fc_ctx c, int kind, double alpha, double beta, double
 double cp_min_entry(fc_ctx c, const TT& x) {
   cudaStream_t st = c->st;
   const int n = c->n, r = x.R;
-  require(r <= kGuardMaxR, FC_ERR_CAPACITY, "SPD guard supports ranks <= 64");
+  require(r <= kCpMinMaxR, FC_ERR_CAPACITY, "SPD guard supports ranks <= 64 (+1 shift term)");
   Scratch s(st);
   double* U = s.alloc<double>((size_t)3 * n * r);
   double* w = s.alloc<double>(r);
@@ -305,9 +307,13 @@ void store_spec(fc_ctx c, SpecCP& sp, const TT& x, const int tucker[3]) {
 
 }  // namespace
 
-void build_spectral_cp(fc_ctx c, int which, double alpha, double beta, double eps, int keep, bool spd_guard) {
-  CoreResult cr = spectral_tucker(c, which, alpha, beta, eps);
+// spectral CP of f(lam1 + lam2 + lam3) over the eigenvalues lam3 (3 x n; the context's SL
+// eigenvalues, or the case-(A) Laplacian ones), applied in `basis` (nullptr: the SL basis)
+void build_spectral_cp(fc_ctx c, int which, double alpha, double beta, double eps, int keep, bool spd_guard,
+                       const double* lam3, const double* basis) {
+  CoreResult cr = spectral_tucker(c, which, alpha, beta, eps, lam3);
   int k = keep;
+  bool shifted = false;
   TT x = tucker_to_canonical(c, cr.core2, cr.s, cr.Z, c->n, eps, k, 0, nullptr);
   if (spd_guard) {
     // reading A7': raise the T2C rank (<= 64) until the CP is positive on the full grid; if the
@@ -320,16 +326,79 @@ void build_spectral_cp(fc_ctx c, int which, double alpha, double beta, double ep
         ++k;
       } else if (e > eps * 1e-4 * 1.0000001) {
         e /= 10.0;
-        cr = spectral_tucker(c, which, alpha, beta, e);
+        cr = spectral_tucker(c, which, alpha, beta, e, lam3);
         k = keep;
       } else {
-        throw Error(FC_ERR_NOT_SPD, "preconditioner CP not positive on the grid (min " + std::to_string(mn) +
-                                        ") at rank <= 64 and Tucker tolerance eps/1e4");
+        // reading A7'': add the constant s (x) 1 (x) 1 (x) 1, s = 2|min| + 1e-15 sum|w|
+        const int n = c->n;
+        std::vector<double> hw(x.R);
+        FC_CUDA_TRY(cudaMemcpyAsync(hw.data(), x.w, (size_t)x.R * 8, cudaMemcpyDeviceToHost, c->st));
+        FC_CUDA_TRY(cudaStreamSynchronize(c->st));
+        double sw = 0.0;
+        for (double v : hw) sw += std::fabs(v);
+        const double shift = 2.0 * std::fabs(mn) + 1e-15 * sw;
+        std::vector<double> h1((size_t)n + 1, 1.0 / std::sqrt((double)n));
+        h1[n] = shift * std::pow((double)n, 1.5);
+        Scratch s1(c->st);
+        double* d1 = s1.alloc<double>((size_t)n + 1);
+        FC_CUDA_TRY(cudaMemcpyAsync(d1, h1.data(), ((size_t)n + 1) * 8, cudaMemcpyHostToDevice, c->st));
+        double* ones[3] = {d1, d1, d1};
+        const int ld1[3] = {n, n, n};
+        TT one = tt_from_cp(c->st, n, 1, d1 + n, ones, ld1);
+        x = tt_axpy(c->st, x, 1.0, one);
+        FC_CUDA_TRY(cudaStreamSynchronize(c->st));
+        mn = cp_min_entry(c, x);
+        require(mn > 0.0, FC_ERR_NOT_SPD, "preconditioner CP not positive on the grid after the A7'' shift");
+        shifted = true;
+        break;
       }
       x = tucker_to_canonical(c, cr.core2, cr.s, cr.Z, c->n, e, k, 0, nullptr);
     }
   }
   store_spec(c, c->spec[which], x, cr.s);
+  if (shifted) c->spec[which].has_basis = false;   // the appended term: recompute W, E (pmgs)
+  c->spec[which].basis = basis;
+}
+
+// case-(A) preconditioner basis [P:772-785, P:842-849]: b0_l = (max a~_l + min a~_l)/2 over the
+// midpoint values the operator uses (A2); lam_k = b0_l 4/h^2 sin^2(k pi h/2), k = 1..n (ascending),
+// V[i, k] = sqrt(2h) sin(i k pi h) (DST-I, orthonormal), i, k = 1..n
+__global__ void laplace_basis_kernel(int n, double b0a, double b0b, double b0c, double* lam, double* V) {
+  const double h = 1.0 / (n + 1), pi = 3.141592653589793;
+  const double b0[3] = {b0a, b0b, b0c};
+  const int l = blockIdx.y;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < (long long)n * n;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(idx % n), k = (int)(idx / n);
+    // sin(i k pi h) with the argument reduced exactly: (i k) mod 2(n+1) keeps it in [0, 2 pi)
+    const long long m = ((long long)(i + 1) * (k + 1)) % (2LL * (n + 1));
+    V[(size_t)l * n * n + idx] = sqrt(2.0 * h) * sin((double)m * pi * h);
+    if (i == 0) {
+      const double sk = sin((k + 1) * pi * h / 2.0);
+      lam[(size_t)l * n + k] = b0[l] * 4.0 / (h * h) * sk * sk;
+    }
+  }
+}
+
+void precond_basis_A(fc_ctx c, const double* a_mid, int boundary) {
+  const int n = c->n;
+  double b0[3];
+  for (int l = 0; l < 3; ++l) {
+    const double* a = a_mid + (size_t)l * (n + 1);
+    // effective midpoints (A2): boundary = 0 replaces the two end values by their neighbours
+    const int i0 = boundary == 0 ? 1 : 0, i1 = boundary == 0 ? n - 1 : n;
+    double mx = a[i0], mn = a[i0];
+    for (int i = i0; i <= i1; ++i) {
+      mx = std::max(mx, a[i]);
+      mn = std::min(mn, a[i]);
+    }
+    b0[l] = 0.5 * (mx + mn);
+  }
+  c->lamA.ensure((size_t)3 * n);
+  c->VA.ensure((size_t)3 * n * n);
+  laplace_basis_kernel<<<dim3(nblk((long long)n * n), 3), 256, 0, c->st>>>(n, b0[0], b0[1], b0[2], c->lamA.p, c->VA.p);
+  FC_CHECK_LAUNCH();
+  for (auto& h : c->have_A) h = true;
 }
 
 }  // namespace fc
@@ -365,8 +434,18 @@ extern "C" int sl_setup(fc_ctx c, int n, const double* a_mid, const fc_params* p
     require(hs == 0, hs, "coefficient check failed on the device");
     for (auto& h : c->have_eig) h = true;
     const double epsD = p->eps_D > 0 ? p->eps_D : p->eps;
-    build_spectral_cp(c, FC_F, p->alpha, p->beta, epsD, p->op_rank > 0 ? p->op_rank : 0, false);
-    build_spectral_cp(c, FC_G, p->alpha, p->beta, epsD, p->precond_rank > 0 ? p->precond_rank : 6, true);
+    require(p->precond_case == FC_PRECOND_B || p->precond_case == FC_PRECOND_A, FC_ERR_INVALID_ARG,
+            "precond_case must be FC_PRECOND_B or FC_PRECOND_A");
+    build_spectral_cp(c, FC_F, p->alpha, p->beta, epsD, p->op_rank > 0 ? p->op_rank : 0, false, c->lam.p, nullptr);
+    for (auto& h : c->have_A) h = false;
+    if (p->precond_case == FC_PRECOND_A) {
+      precond_basis_A(c, a_mid, p->boundary);
+      build_spectral_cp(c, FC_G, p->alpha, p->beta, epsD, p->precond_rank > 0 ? p->precond_rank : 6, true,
+                        c->lamA.p, c->VA.p);
+    } else {
+      build_spectral_cp(c, FC_G, p->alpha, p->beta, epsD, p->precond_rank > 0 ? p->precond_rank : 6, true,
+                        c->lam.p, nullptr);
+    }
     return FC_OK;
   } catch (const Error& e) {
     c->err = e.msg;

@@ -106,6 +106,7 @@ class Problem:
     kmax: int = 100
     precond_rank: int = 6
     boundary: int = 0          # 0 = paper rule [P:517-518], 1 = standard
+    precond: str = "B"         # preconditioner case (A) or (B) [P:758-768]; B = default (A6)
 
 
 CONFIGS = {
@@ -122,8 +123,9 @@ CONFIGS = {
 
 
 def make_problem(name: str, n: int | None = None, eps: float | None = None,
-                 alpha: float | None = None, beta: float | None = None) -> Problem:
-    """Build config `name` (optionally at another n / eps, e.g. C4's eps sweep)."""
+                 alpha: float | None = None, beta: float | None = None, precond: str = "B") -> Problem:
+    """Build config `name` (optionally at another n / eps, e.g. C4's eps sweep; precond "A"
+    selects the case-(A) anisotropic-Laplacian preconditioner)."""
     cfg = CONFIGS[name]
     n = cfg["n"] if n is None else n
     eps = cfg["eps"] if eps is None else eps
@@ -132,7 +134,7 @@ def make_problem(name: str, n: int | None = None, eps: float | None = None,
     return Problem(name=name, n=n, a_mid=np.ascontiguousarray(a_mid),
                    alpha=cfg["alpha"] if alpha is None else alpha,
                    beta=cfg["beta"] if beta is None else beta,
-                   eps=eps, tol_stop=10.0 * eps, b_w=w, b_U=U)
+                   eps=eps, tol_stop=10.0 * eps, b_w=w, b_U=U, precond=precond)
 
 
 # C5 operator-apply sweep grid [BJ configs[4]]
