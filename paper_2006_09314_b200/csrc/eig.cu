@@ -342,6 +342,7 @@ __global__ void ns_matrix_kernel(int n, double* G) {
 constexpr int kTriThreads = 512;
 constexpr int kSmemMaxN = 150;   // (N^2 + 18 N) * 8 <= 202 KB in shared memory, else global (L2)
 constexpr int kPackedMaxN = 230; // packed lower triangle in shared memory up to this size
+constexpr int kClusterMinN = 96; // above this the cluster kernels take over (FC_NO_CLUSTER: 230)
 constexpr size_t kTriSmemMax = 220 * 1024;
 
 __device__ double block_sum(double v, double* red) {
@@ -460,13 +461,13 @@ __global__ void __launch_bounds__(kTriThreads) tridiag_kernel(const __grid_const
 // (N(N+1)/2 doubles: N <= 230 fits in 216 KB), 1024 threads, matvec partials by shared-memory
 // atomics.  Column j is contiguous at off(j) = j N - j(j-1)/2; element (i, j), i >= j, at
 // off(j) + i - j.
-__global__ void __launch_bounds__(1024) tridiag_packed_kernel(const __grid_constant__ SyevBatch B) {
+__global__ void __launch_bounds__(1024) tridiag_packed_kernel(const __grid_constant__ SyevBatch B, int maxN) {
   extern __shared__ double sm[];
   __shared__ double red[33];
   __shared__ double alpha_s;
   const SyevEntry& E = B.e[blockIdx.x];
   const int N = E.N;
-  if (N <= 0 || N > kPackedMaxN) return;
+  if (N <= 0 || N > maxN) return;
   const int tid = threadIdx.x, nt = blockDim.x, warp = tid >> 5, ln = tid & 31, NW = nt >> 5;
   const size_t P = (size_t)N * (N + 1) / 2;
   double* L = sm;
@@ -553,7 +554,7 @@ constexpr int kCl16MaxN = 840;   // ... with 16 CTAs (non-portable cluster size)
 
 template <int CS>
 __host__ __device__ constexpr bool cluster_class(int N) {
-  return CS == 8 ? (N > kPackedMaxN && N <= kCl8MaxN) : (N > kCl8MaxN && N <= kCl16MaxN);
+  return CS == 8 ? (N > kClusterMinN && N <= kCl8MaxN) : (N > kCl8MaxN && N <= kCl16MaxN);
 }
 
 template <int CS>
@@ -826,59 +827,62 @@ __global__ void __launch_bounds__(1024) orth_backtransform_kernel(const __grid_c
     for (int k = tid; k < N; k += nt) yi[k] *= inv;
     __syncthreads();
   }
-  if (E.A == nullptr) return;   // orthonormalisation only
-  // back-transform: for k = N-3 .. 0: y[k+1:] -= 2 u_k (u_k . y[k+1:]); warp per vector.
-  // For N <= 512 the warp keeps its vector in registers (element ln + 32 c in slot c), so the
-  // only memory traffic is the (L2-resident) Householder vectors, all loads independent.
-  const int w = tid >> 5, ln = tid & 31;
-  if (N <= 512) {
-    constexpr int MC = 16;
-    for (int i = w; i < r; i += nt / 32) {
-      double* yi = Y + (size_t)i * ldy;
-      double yv[MC];
+}
+
+// back-transform z = H_0 H_1 ... H_{N-3} y of the leading r eigenvectors with the Householder
+// vectors stored in A (column k, rows k+1..): warp per vector, many CTAs (grid.x covers the
+// vectors, grid.y the batch entries).  For N <= 32*MC the warp keeps its vector in registers
+// (element ln + 32 c in slot c): the only memory traffic is the L2-resident reflectors.
+template <int MC>
+__global__ void __launch_bounds__(512) backtransform_kernel(const __grid_constant__ SyevBatch B) {
+  const SyevEntry& E = B.e[blockIdx.y];
+  const int N = E.N;
+  const int r = min(*E.r, N);
+  const int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), ln = threadIdx.x & 31;
+  if (w >= r || E.A == nullptr) return;
+  double* yi = E.Y + (size_t)w * E.ldy;
+  if (N <= 32 * MC) {
+    double yv[MC];
+#pragma unroll
+    for (int c = 0; c < MC; ++c) {
+      const int idx = ln + 32 * c;
+      yv[c] = idx < N ? yi[idx] : 0.0;
+    }
+    for (int k = N - 3; k >= 0; --k) {
+      const double* u = E.A + (size_t)k * E.lda;   // u_k[idx] at A[idx, k] for idx > k
+      const int c0 = (k + 1) >> 5;                 // slots below c0 hold idx <= k: skip them
+      double s = 0.0;
 #pragma unroll
       for (int c = 0; c < MC; ++c) {
         const int idx = ln + 32 * c;
-        yv[c] = idx < N ? yi[idx] : 0.0;
+        if (c >= c0 && idx > k && idx < N) s = fma(u[idx], yv[c], s);
       }
-      for (int k = N - 3; k >= 0; --k) {
-        const double* u = E.A + (size_t)k * E.lda;   // u_k[idx] at A[idx, k] for idx > k
-        double s = 0.0;
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (s != 0.0) {
+        const double t2 = 2.0 * s;
 #pragma unroll
         for (int c = 0; c < MC; ++c) {
           const int idx = ln + 32 * c;
-          if (idx > k && idx < N) s += u[idx] * yv[c];
-        }
-        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-        if (s != 0.0) {
-          const double t2 = 2.0 * s;
-#pragma unroll
-          for (int c = 0; c < MC; ++c) {
-            const int idx = ln + 32 * c;
-            if (idx > k && idx < N) yv[c] -= t2 * u[idx];
-          }
+          if (c >= c0 && idx > k && idx < N) yv[c] -= t2 * u[idx];
         }
       }
+    }
 #pragma unroll
-      for (int c = 0; c < MC; ++c) {
-        const int idx = ln + 32 * c;
-        if (idx < N) yi[idx] = yv[c];
-      }
+    for (int c = 0; c < MC; ++c) {
+      const int idx = ln + 32 * c;
+      if (idx < N) yi[idx] = yv[c];
     }
     return;
   }
-  for (int i = w; i < r; i += nt / 32) {
-    double* yi = Y + (size_t)i * ldy;
-    for (int k = N - 3; k >= 0; --k) {
-      const double* u = E.A + (k + 1) + (size_t)k * E.lda;
-      const int m = N - k - 1;
-      double s = 0.0;
-      for (int t = ln; t < m; t += 32) s += u[t] * yi[k + 1 + t];
-      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-      if (s != 0.0)
-        for (int t = ln; t < m; t += 32) yi[k + 1 + t] -= 2.0 * s * u[t];
-      __syncwarp();
-    }
+  for (int k = N - 3; k >= 0; --k) {
+    const double* u = E.A + (k + 1) + (size_t)k * E.lda;
+    const int m = N - k - 1;
+    double s = 0.0;
+    for (int t = ln; t < m; t += 32) s += u[t] * yi[k + 1 + t];
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (s != 0.0)
+      for (int t = ln; t < m; t += 32) yi[k + 1 + t] -= 2.0 * s * u[t];
+    __syncwarp();
   }
 }
 
@@ -1441,6 +1445,7 @@ void syev_values(const SyevBatch& b, cudaStream_t st) {
   if (b.nb == 0) return;
   static const bool no_cluster = getenv("FC_NO_CLUSTER") != nullptr;
   const int minG = no_cluster ? kPackedMaxN : kCl16MaxN;   // sizes above go to the global kernel
+  const int maxP = no_cluster ? kPackedMaxN : kClusterMinN; // sizes up to this: packed single CTA
   int maxN = 0;
   size_t smem_g = 0, smem_p = 0, smem_8 = 0, smem_16 = 0;
   bool any_g = false, any_p = false;
@@ -1449,7 +1454,7 @@ void syev_values(const SyevBatch& b, cudaStream_t st) {
     const int N = b.e[i].N;
     maxN = std::max(maxN, N);
     if (N <= 0) continue;
-    if (N <= kPackedMaxN) {
+    if (N <= maxP) {
       any_p = true;
       smem_p = std::max(smem_p, ((size_t)N * (N + 1) / 2 + 2 * (size_t)N) * 8);
     } else if (N > minG) {
@@ -1472,7 +1477,7 @@ void syev_values(const SyevBatch& b, cudaStream_t st) {
     attr = true;
   }
   if (any_p) {
-    tridiag_packed_kernel<<<b.nb, 1024, smem_p, st>>>(b);
+    tridiag_packed_kernel<<<b.nb, 1024, smem_p, st>>>(b, maxP);
     FC_CHECK_LAUNCH();
   }
   if (any_g) {
@@ -1487,7 +1492,16 @@ void syev_vectors(const SyevBatch& b, int maxN, cudaStream_t st) {
   if (b.nb == 0 || maxN == 0) return;
   tri_invit_kernel<<<dim3(cdiv(maxN, 64), b.nb), 64, 0, st>>>(b);
   FC_CHECK_LAUNCH();
-  orth_backtransform_kernel<<<b.nb, 1024, (size_t)maxN * 8, st>>>(b);
+  // CGS2 of the inverse-iteration vectors (tridiagonal coordinates), one CTA per matrix
+  SyevBatch ob = b;
+  for (int i = 0; i < ob.nb; ++i) ob.e[i].A = nullptr;
+  orth_backtransform_kernel<<<b.nb, 1024, (size_t)maxN * 8, st>>>(ob);
+  FC_CHECK_LAUNCH();
+  // back-transformation, warp per vector over many CTAs
+  const dim3 grid(cdiv(maxN, 16), b.nb);
+  if (maxN <= 512) backtransform_kernel<16><<<grid, 512, 0, st>>>(b);
+  else if (maxN <= 1024) backtransform_kernel<32><<<grid, 512, 0, st>>>(b);
+  else backtransform_kernel<1><<<grid, 512, 0, st>>>(b);
   FC_CHECK_LAUNCH();
 }
 
