@@ -1562,6 +1562,15 @@ void bcgs_cluster_setup() {
   attr = true;
 }
 
+// split-K for the two skinny GEMMs of a block projection, P = Q^T A_blk (k x W x n) and
+// A_blk -= Q P (n x W x k): enough CTAs for ~2 waves of 148 SMs (64 x 64 tiles), at least 64 of
+// the reduction dimension per split (atomic epilogue; both GEMMs accumulate into beta = 1 targets)
+void split_skinny(GemmArgs& p, GemmArgs& u, int n, int k, int w, int nb) {
+  const int tp = cdiv(k, 64) * cdiv(w, 64) * nb, tu = cdiv(n, 64) * cdiv(w, 64) * nb;
+  p.splitk = std::max(1, std::min(cdiv(n, 64), cdiv(2 * 148, tp)));
+  u.splitk = std::max(1, std::min(cdiv(k, 64), cdiv(2 * 148, tu)));
+}
+
 void bcgs(const BcgsBatch& bin, cudaStream_t st) {
   if (bin.nb == 0) return;
   constexpr int W = kBcgsW;
@@ -1626,7 +1635,7 @@ void bcgs(const BcgsBatch& bin, cudaStream_t st) {
         ++nb;
       }
       p.nbatch = u.nbatch = nb;
-      p.splitk = std::max(1, std::min(cdiv(b.e[0].n, 256), 8));
+      split_skinny(p, u, b.e[0].n, std::min(j0, b.e[0].kcap), W, nb);
       gemm(p, st);
       gemm(u, st);
     }
@@ -1649,7 +1658,7 @@ void bcgs(const BcgsBatch& bin, cudaStream_t st) {
         ++nb;
       }
       p.nbatch = u.nbatch = nb;
-      p.splitk = std::max(1, std::min(cdiv(b.e[0].n, 256), 8));
+      split_skinny(p, u, b.e[0].n, std::min(j0, b.e[0].kcap), W, nb);
       gemm(p, st);
       gemm(u, st);
     }

@@ -10,6 +10,9 @@
 // mma.sync.m8n8k4.f64 (SASS: DMMA.8x8x4).  Tiles: CTA 64x64, BK = 16, 4 warps each owning a
 // 32x32 sub-tile (4x4 DMMA fragments, 32 fp64 accumulators per thread), operands staged
 // global -> shared with cp.async in a 3-stage ring (zero-filled at ragged edges).
+#include <algorithm>
+#include <cstdlib>
+#include <map>
 #include "common.cuh"
 
 namespace fc {
@@ -417,6 +420,7 @@ struct GemmProf {
   bool on = false;
   std::vector<cudaEvent_t> ev;   // pairs
   std::vector<double> flops;
+  std::vector<std::string> shape;   // FC_GEMM_TRACE: per-launch shape key
   size_t used = 0;
 };
 GemmProf& gprof() {
@@ -435,13 +439,26 @@ void gemm_profile(bool enable, double* ms, double* flops, long long* launches) {
   }
   P.on = false;
   double t = 0, f = 0;
+  std::map<std::string, std::pair<double, int>> hist;
   for (size_t i = 0; i < P.used; ++i) {
     float x = 0;
     FC_CUDA_TRY(cudaEventSynchronize(P.ev[2 * i + 1]));
     FC_CUDA_TRY(cudaEventElapsedTime(&x, P.ev[2 * i], P.ev[2 * i + 1]));
     t += x;
     f += P.flops[i];
+    if (i < P.shape.size()) {
+      auto& h = hist[P.shape[i]];
+      h.first += x;
+      h.second += 1;
+    }
   }
+  if (!hist.empty()) {   // FC_GEMM_TRACE: time by launch shape, largest first
+    std::vector<std::pair<double, std::string>> v;
+    for (auto& kv : hist) v.push_back({kv.second.first, kv.first + " x" + std::to_string(kv.second.second)});
+    std::sort(v.rbegin(), v.rend());
+    for (size_t i = 0; i < v.size() && i < 40; ++i) fprintf(stderr, "[fc gemm] %8.2f ms  %s\n", v[i].first, v[i].second.c_str());
+  }
+  P.shape.clear();
   if (ms) *ms = t;
   if (flops) *flops = f;
   if (launches) *launches = (long long)P.used;
@@ -461,6 +478,14 @@ void gemm(const GemmArgs& a, cudaStream_t st) {
   }
   double f = 0;
   for (int i = 0; i < a.nbatch; ++i) f += 2.0 * a.rep * a.b[i].M * (double)a.b[i].N * a.b[i].K;
+  static const bool trace = getenv("FC_GEMM_TRACE") != nullptr;
+  if (trace) {
+    char key[160];
+    snprintf(key, sizeof key, "t%d%d M%d N%d K%d nb%d rep%d sk%d%s", a.transA, a.transB, a.b[0].M, a.b[0].N, a.b[0].K,
+             a.nbatch, a.rep, a.splitk, a.krR ? " KR" : (a.gen.kind >= 0 ? " GEN" : ""));
+    P.shape.resize(P.used);
+    P.shape.push_back(key);
+  }
   FC_CUDA_TRY(cudaEventRecord(P.ev[2 * P.used], st));
   gemm_dispatch(a, st);
   FC_CUDA_TRY(cudaEventRecord(P.ev[2 * P.used + 1], st));
