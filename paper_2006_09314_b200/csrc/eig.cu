@@ -87,7 +87,8 @@ __global__ void gk_bisect_kernel(int n, const double* __restrict__ s_all, double
 
 // ---- tridiagonal inverse iteration (shared by (a) and (b)) ---------------------------
 // T = tridiag(e, d, e) of size N.  Scratch arrays strided by `stride` (coalesced across
-// threads): 5 arrays of N entries.  Writes the unit vector into v[k*vstride].
+// threads): 5 arrays of N entries (u0 holds the reciprocal pivots).  Writes the unit vector into
+// v[k*vstride].
 __device__ void tri_invit(int N, const double* __restrict__ d, const double* __restrict__ e, double lam,
                           double tnorm, double* scr, size_t stride, double* v, size_t vstride, unsigned seed) {
   double* u0 = scr;
@@ -109,20 +110,20 @@ __device__ void tri_invit(int N, const double* __restrict__ d, const double* __r
     double as = (k + 1 < N - 1) ? e[k + 1] : 0.0;
     if (fabs(sub) > fabs(cd)) {
       double m = cd / sub;
-      S(u0, k) = sub; S(u1, k) = ad; S(u2, k) = as;
+      S(u0, k) = 1.0 / sub; S(u1, k) = ad; S(u2, k) = as;
       S(lm, k) = m; S(pv, k) = 1.0;
       double nd = cs - m * ad, ns = cs2 - m * as;
       cd = nd; cs = ns; cs2 = 0.0;
     } else {
       if (fabs(cd) < tiny) cd = (cd >= 0 ? tiny : -tiny);
       double m = sub / cd;
-      S(u0, k) = cd; S(u1, k) = cs; S(u2, k) = cs2;
+      S(u0, k) = 1.0 / cd; S(u1, k) = cs; S(u2, k) = cs2;
       S(lm, k) = m; S(pv, k) = 0.0;
       cd = ad - m * cs; cs = as; cs2 = 0.0;
     }
   }
   if (fabs(cd) < tiny) cd = (cd >= 0 ? tiny : -tiny);
-  S(u0, N - 1) = cd; S(u1, N - 1) = 0.0; S(u2, N - 1) = 0.0;
+  S(u0, N - 1) = 1.0 / cd; S(u1, N - 1) = 0.0; S(u2, N - 1) = 0.0;
   // start vector: deterministic hash in [0.5, 1.5)
   for (int k = 0; k < N; ++k) {
     unsigned h = (unsigned)k * 2654435761u ^ (seed * 2246822519u + 0x9E3779B9u);
@@ -130,18 +131,21 @@ __device__ void tri_invit(int N, const double* __restrict__ d, const double* __r
     v[(size_t)k * vstride] = 0.5 + (h & 0xFFFFFF) / 16777216.0;
   }
   for (int it = 0; it < 3; ++it) {
-    // forward: apply P and L
+    // forward: apply P and L (the running entry carried in a register; every load below is
+    // independent of the recurrence, so the loop is an FMA chain)
+    double carry = v[0];
     for (int k = 0; k < N - 1; ++k) {
-      double bk = v[(size_t)k * vstride], bk1 = v[(size_t)(k + 1) * vstride];
+      double bk = carry, bk1 = v[(size_t)(k + 1) * vstride];
       if (S(pv, k) != 0.0) { double t = bk; bk = bk1; bk1 = t; }
       bk1 -= S(lm, k) * bk;
       v[(size_t)k * vstride] = bk;
-      v[(size_t)(k + 1) * vstride] = bk1;
+      carry = bk1;
     }
-    // backward with U (3 diagonals)
+    v[(size_t)(N - 1) * vstride] = carry;
+    // backward with U (3 diagonals; u0 holds the reciprocal pivots)
     double x2 = 0.0, x1 = 0.0, nrm = 0.0;
     for (int k = N - 1; k >= 0; --k) {
-      double x = (v[(size_t)k * vstride] - S(u1, k) * x1 - S(u2, k) * x2) / S(u0, k);
+      double x = (v[(size_t)k * vstride] - S(u1, k) * x1 - S(u2, k) * x2) * S(u0, k);
       v[(size_t)k * vstride] = x;
       x2 = x1; x1 = x;
       nrm = fmax(nrm, fabs(x));
@@ -165,16 +169,18 @@ __device__ void tri_lu_solve(int N, const double* scr, size_t stride, double* v)
   const double* lm = scr + (size_t)3 * N * stride;
   const double* pv = scr + (size_t)4 * N * stride;
 #define S(a, k) a[(size_t)(k) * stride]
+  double carry = v[0];
   for (int k = 0; k < N - 1; ++k) {
-    double bk = v[k], bk1 = v[k + 1];
+    double bk = carry, bk1 = v[k + 1];
     if (S(pv, k) != 0.0) { double t = bk; bk = bk1; bk1 = t; }
     bk1 -= S(lm, k) * bk;
     v[k] = bk;
-    v[k + 1] = bk1;
+    carry = bk1;
   }
+  v[N - 1] = carry;
   double x2 = 0.0, x1 = 0.0;
   for (int k = N - 1; k >= 0; --k) {
-    double x = (v[k] - S(u1, k) * x1 - S(u2, k) * x2) / S(u0, k);
+    double x = (v[k] - S(u1, k) * x1 - S(u2, k) * x2) * S(u0, k);   // u0: reciprocal pivots
     v[k] = x;
     x2 = x1; x1 = x;
   }
@@ -1340,17 +1346,25 @@ __global__ void col_norms_kernel(const __grid_constant__ BcgsBatch B) {
   if (ln == 0) E.norm0[c] = sqrt(s);
 }
 
-__global__ void rank_cut_kernel(int count, const double* __restrict__ s2, double factor,
-                                const double* __restrict__ energy, int* r_out, double* margin_out) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+constexpr int kCutStage = 6144;   // small-end values staged in shared memory (48 KB)
+__global__ void __launch_bounds__(256) rank_cut_kernel(int count, const double* __restrict__ s2, double factor,
+                                                       const double* __restrict__ energy, int* r_out,
+                                                       double* margin_out) {
+  __shared__ double tail[kCutStage];
+  // stage the small end s2[count - m .. count) (coalesced, whole block); the sum itself stays
+  // sequential from the small end (the oracle's order)
+  const int m = min(count, kCutStage), base = count - m;
+  for (int i = threadIdx.x; i < m; i += blockDim.x) tail[i] = s2[base + i];
+  __syncthreads();
+  if (threadIdx.x != 0) return;
   const double thr = factor * (*energy);
   // tails from the small end: tail(r) = sum_{k >= r} s2[k]
   double acc = 0.0;
   int r = count;                 // default: keep everything
   double margin = 1e300;
   for (int k = count - 1; k >= 1; --k) {
-    acc += s2[k];   // not clamped: eigenvalues of a PSD Gram at the noise floor are +-eps||M||,
-                    // clamping would bias the tail upward by (#noise) * eps ||M||
+    acc += k >= base ? tail[k - base] : s2[k];   // not clamped: eigenvalues of a PSD Gram at the
+                    // noise floor are +-eps||M||; clamping would bias the tail by (#noise) eps ||M||
     double m = fabs(acc - thr) / (thr > 0 ? thr : 1.0);
     if (acc <= thr) {
       r = k;                    // tail beyond index k-1 fits: keep k values
@@ -1668,7 +1682,7 @@ void bcgs(const BcgsBatch& bin, cudaStream_t st) {
 
 void rank_cut_device(int count, const double* s2, double factor, const double* energy, int* r_out,
                      double* margin_out, cudaStream_t st) {
-  rank_cut_kernel<<<1, 32, 0, st>>>(count, s2, factor, energy, r_out, margin_out);
+  rank_cut_kernel<<<1, 256, 0, st>>>(count, s2, factor, energy, r_out, margin_out);
   FC_CHECK_LAUNCH();
 }
 
