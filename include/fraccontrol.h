@@ -175,6 +175,14 @@ int cp_truncate(fc_ctx ctx, const fc_cp* x, double eps, fc_cp* y, fc_trunc_info*
 int fracop_apply_truncate(fc_ctx ctx, int which, const fc_cp* x, double eps, fc_cp* y, fc_trunc_info* info);
 
 /* ---- the solver: S14 ------------------------------------------------------------------ */
+/* state_recover  [P:287-289, P:969-972]: the state y = beta_paper A^-alpha u of the control problem;
+ *   with reading A5 (beta_paper = 1, gamma = beta) y = A^-alpha u, truncated at eps (RHOSVD + T2C,
+ *   as cp_truncate; fused apply -> truncate in eigen coordinates).  The spectral CP of lam^-alpha
+ *   (FC_POW_MINUS) is built on first use at eps_D (or injected by op_set_spectral_cp).
+ *   u, y: caller-owned device CPs (y.cap >= result rank else CAPACITY, info->required_rank set).
+ *   Errors: NOT_READY (no sl_setup / params), INVALID_ARG, SHAPE, CAPACITY, CUDA. */
+int state_recover(fc_ctx ctx, const fc_cp* u, double eps, fc_cp* y, fc_trunc_info* info);
+
 /* pcg_solve: Algorithm 1 [P:1825-1872] with fun = fracop_apply(FC_F), precond =
  * fracop_apply(FC_G), trunc = cp_truncate(eps); X0 = 0 (A14), R0 = B untruncated (A15).
  * Returns FC_OK, FC_NOT_CONVERGED, or an error; u (device CP, cap >= final rank, else

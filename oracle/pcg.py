@@ -16,7 +16,7 @@ import numpy as np
 from . import cp as cpm
 from .cp import CP
 from .sturm import dst1_basis, effective_midpoints, eigenpairs, laplace_eigenvalues
-from .spectral import FC_F, FC_G, spectral_cp
+from .spectral import FC_F, FC_G, FC_POW_MINUS, spectral_cp
 from .truncate import truncate
 
 
@@ -125,3 +125,16 @@ def solve(problem, st: Setup | None = None, kmax=None, with_true_residual=False)
         from .measure import diff_norm
         rep["true_residual"] = diff_norm(fun(u), B) / cpm.norm(B)
     return u, rep, st
+
+
+def state_cp(problem, st: Setup, eps_D=None) -> CP:
+    """Spectral CP of lam^-alpha (FC_POW_MINUS) on the SL eigenvalues, eps_D-driven (O5)."""
+    eps_D = problem.eps if eps_D is None else eps_D
+    return spectral_cp(st.lams, FC_POW_MINUS, problem.alpha, problem.beta, eps_D)
+
+
+def state(problem, st: Setup, u: CP, Pm: CP | None = None) -> CP:
+    """State recovery [P:287-289, P:969-972]: y = beta_paper A^-alpha u; with reading A5
+    (beta_paper = 1) y = A^-alpha u, truncated at eps (O6 apply, O9 truncate)."""
+    Pm = state_cp(problem, st) if Pm is None else Pm
+    return truncate(cpm.apply(st.V, Pm, u), problem.eps)

@@ -69,7 +69,7 @@ ENTRY_POINTS = ["fc_create", "fc_destroy", "fc_last_error", "fc_set_stream", "sl
                 "sl_set_eigen", "op_get_spectral_cp", "op_set_spectral_cp", "op_spectral_rank",
                 "fracop_apply", "precond_apply", "cp_dot", "cp_axpy", "cp_truncate", "pcg_solve",
                 "fc_dgemm", "fc_last_kernel_stats", "fc_kernel_launches", "fracop_apply_truncate", "fc_orthonormalize",
-                "fc_profile_gemm", "fc_syev", "op_get_precond_basis", "op_set_precond_basis"]
+                "fc_profile_gemm", "fc_syev", "op_get_precond_basis", "op_set_precond_basis", "state_recover"]
 
 
 def load_library(path: str = LIB_PATH) -> C.CDLL:
@@ -100,6 +100,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "fc_syev": ([P, I, C.POINTER(I), C.POINTER(P), C.POINTER(I), C.POINTER(P), C.POINTER(P), C.POINTER(I),
                      C.POINTER(I)], I),
         "op_get_precond_basis": ([P, I, P, P], I), "op_set_precond_basis": ([P, I, P, P], I),
+        "state_recover": ([P, cpp, D, cpp, C.POINTER(fc_trunc_info)], I),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -287,6 +288,21 @@ class Context:
             xs, ys = x.struct(), y.struct()
             rc = self.lib.fracop_apply_truncate(self.h, which, C.byref(xs), C.c_double(eps), C.byref(ys),
                                                 C.byref(info))
+            if rc == -3 and info.required_rank > cap:
+                cap = info.required_rank
+                continue
+            self._check(rc)
+            y.rank = ys.rank
+            return y, info
+
+    def state_recover(self, u: DeviceCP, eps: float, cap: int | None = None):
+        """y = A^-alpha u truncated at eps (state_recover)."""
+        cap = cap if cap is not None else max(4 * u.rank, 64)
+        while True:
+            y = DeviceCP(self.n, cap)
+            info = fc_trunc_info()
+            us, ys = u.struct(), y.struct()
+            rc = self.lib.state_recover(self.h, C.byref(us), C.c_double(eps), C.byref(ys), C.byref(info))
             if rc == -3 and info.required_rank > cap:
                 cap = info.required_rank
                 continue

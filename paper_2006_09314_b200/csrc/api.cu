@@ -416,6 +416,7 @@ int op_set_spectral_cp(fc_ctx c, int which, const fc_cp* in) {
 int op_get_spectral_cp(fc_ctx c, int which, fc_cp* out) {
   return guard(c, [&]() {
     require(which >= 0 && which < 4, FC_ERR_INVALID_ARG, "which");
+    ensure_spectral(c, which);
     SpecCP& s = c->spec[which];
     require(s.valid, FC_ERR_NOT_READY, "spectral CP not set");
     check_cp(c, out, "out");
@@ -438,6 +439,7 @@ int op_get_spectral_cp(fc_ctx c, int which, fc_cp* out) {
 int op_spectral_rank(fc_ctx c, int which, int* rank, int* tucker) {
   return guard(c, [&]() {
     require(which >= 0 && which < 4, FC_ERR_INVALID_ARG, "which");
+    ensure_spectral(c, which);
     SpecCP& s = c->spec[which];
     require(s.valid, FC_ERR_NOT_READY, "spectral CP not set");
     if (rank) *rank = s.r;
@@ -453,6 +455,7 @@ int fracop_apply(fc_ctx c, int which, const fc_cp* x, fc_cp* y) {
     check_cp(c, x, "x");
     check_cp(c, y, "y");
     require(c->have_eig[0] && c->have_eig[1] && c->have_eig[2], FC_ERR_NOT_READY, "eigenpairs missing");
+    ensure_spectral(c, which);
     const SpecCP& s = c->spec[which];
     require(s.valid, FC_ERR_NOT_READY, "spectral CP not set");
     long long need = (long long)s.r * x->rank;

@@ -267,6 +267,7 @@ int fracop_apply_truncate(fc_ctx c, int which, const fc_cp* x, double eps, fc_cp
     check_cp2(c, y, "y");
     require(eps > 0 && std::isfinite(eps), FC_ERR_INVALID_ARG, "eps must be > 0");
     require(c->have_eig[0] && c->have_eig[1] && c->have_eig[2], FC_ERR_NOT_READY, "eigenpairs missing");
+    ensure_spectral(c, which);
     SpecCP& sp = c->spec[which];
     require(sp.valid, FC_ERR_NOT_READY, "spectral CP not set");
     TruncStats S;
@@ -284,6 +285,10 @@ int fracop_apply_truncate(fc_ctx c, int which, const fc_cp* x, double eps, fc_cp
     store_tt(c, out, y);
     return FC_OK;
   });
+}
+
+int state_recover(fc_ctx c, const fc_cp* u, double eps, fc_cp* y, fc_trunc_info* info) {
+  return fracop_apply_truncate(c, FC_POW_MINUS, u, eps, y, info);
 }
 
 int pcg_solve(fc_ctx c, const fc_cp* b, const fc_params* prm, fc_cp* u, fc_pcg_report* rep) {

@@ -360,6 +360,16 @@ void build_spectral_cp(fc_ctx c, int which, double alpha, double beta, double ep
   c->spec[which].basis = basis;
 }
 
+void ensure_spectral(fc_ctx c, int which) {
+  SpecCP& sp = c->spec[which];
+  if (sp.valid || (which != FC_POW_PLUS && which != FC_POW_MINUS)) return;
+  require(c->have_params, FC_ERR_NOT_READY, "spectral CP of A^+-alpha needs alpha: call sl_setup or pass params");
+  require(c->n > 0 && c->have_eig[0] && c->have_eig[1] && c->have_eig[2], FC_ERR_NOT_READY, "eigenpairs missing");
+  const double epsD = c->p.eps_D > 0 ? c->p.eps_D : c->p.eps;
+  build_spectral_cp(c, which, c->p.alpha, c->p.beta, epsD, c->p.op_rank > 0 ? c->p.op_rank : 0, false, c->lam.p,
+                    nullptr);
+}
+
 // case-(A) preconditioner basis [P:772-785, P:842-849]: b0_l = (max a~_l + min a~_l)/2 over the
 // midpoint values the operator uses (A2); lam_k = b0_l 4/h^2 sin^2(k pi h/2), k = 1..n (ascending),
 // V[i, k] = sqrt(2h) sin(i k pi h) (DST-I, orthonormal), i, k = 1..n
