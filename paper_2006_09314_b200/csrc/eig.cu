@@ -1115,16 +1115,17 @@ __global__ void __launch_bounds__(1024) bcgs_finalize_kernel(const __grid_consta
 //   the tau ||x|| decision level) -> at most 2 cluster barriers per column;
 //   finalisation: dots with the earlier block vectors and the norm in one all-reduce (1 barrier).
 constexpr int kBcgsClusterThreads = 512;
-constexpr int kBcgsRB = 128;               // rows per CTA: n <= 8*128 with 8 CTAs, <= 16*128 with 16
-constexpr int kBcgsLd = kBcgsRB + 4;
 
+// cluster configurations: (CS CTAs, block width W, rows per CTA RB), n <= CS * RB; see bcgs()
+template <int W, int RB>
 struct BcgsClusterSmem {
-  double X[kBcgsLd * kBcgsW];
-  double Yb[kBcgsLd * kBcgsW];
-  double part[2][kBcgsW + 2];     // partial dots (+ norm), double-buffered (read remotely)
-  double coef[kBcgsW + 2];
+  static constexpr int LD = RB + 4;   // conflict-free row-parallel access
+  double X[LD * W];
+  double Yb[LD * W];
+  double part[2][W + 2];          // partial dots (+ norm), double-buffered (read remotely)
+  double coef[W + 2];
   double red[kBcgsClusterThreads / 32];
-  int alive[kBcgsW];
+  int alive[W];
 };
 
 // all-reduce of buf[0..cnt) (per-CTA partials, read remotely) into out[0..cnt); every CTA sums
@@ -1145,6 +1146,7 @@ __device__ __forceinline__ void cluster_allreduce(cooperative_groups::cluster_gr
 
 // partial dots part[a] = sum_{i < nr} V[i, a] x[i] for a < na (4 independent dots per warp)
 // and, if want_norm, part[na] = sum x[i]^2
+template <int LD>
 __device__ __forceinline__ void block_dots(const double* V, const double* x, int nr, int na, bool want_norm,
                                            double* part, double* red) {
   const int tid = threadIdx.x, warp = tid >> 5, ln = tid & 31, NW = blockDim.x >> 5;
@@ -1152,10 +1154,10 @@ __device__ __forceinline__ void block_dots(const double* V, const double* x, int
     double s0 = 0, s1 = 0, s2 = 0, s3 = 0;
     for (int i = ln; i < nr; i += 32) {
       const double xi = x[i];
-      s0 = fma(V[i + (size_t)a0 * kBcgsLd], xi, s0);
-      if (a0 + 1 < na) s1 = fma(V[i + (size_t)(a0 + 1) * kBcgsLd], xi, s1);
-      if (a0 + 2 < na) s2 = fma(V[i + (size_t)(a0 + 2) * kBcgsLd], xi, s2);
-      if (a0 + 3 < na) s3 = fma(V[i + (size_t)(a0 + 3) * kBcgsLd], xi, s3);
+      s0 = fma(V[i + (size_t)a0 * LD], xi, s0);
+      if (a0 + 1 < na) s1 = fma(V[i + (size_t)(a0 + 1) * LD], xi, s1);
+      if (a0 + 2 < na) s2 = fma(V[i + (size_t)(a0 + 2) * LD], xi, s2);
+      if (a0 + 3 < na) s3 = fma(V[i + (size_t)(a0 + 3) * LD], xi, s3);
     }
     for (int o = 16; o > 0; o >>= 1) {
       s0 += __shfl_xor_sync(0xffffffffu, s0, o);
@@ -1185,25 +1187,28 @@ __device__ __forceinline__ void block_dots(const double* V, const double* x, int
 }
 
 // x[i] -= sum_{a < na} coef[a] V[i, a]  (4 threads per row)
+template <int LD, int RB>
 __device__ __forceinline__ void block_update(const double* V, double* x, int nr, int na, const double* coef) {
   const int tid = threadIdx.x, nt = blockDim.x;
-  for (int base = 0; base < kBcgsRB * 4; base += nt) {
+  for (int base = 0; base < RB * 4; base += nt) {
     const int idx = base + tid, i = idx >> 2, qd = idx & 3;
     double v = 0.0;
     if (i < nr)
-      for (int a = qd; a < na; a += 4) v = fma(coef[a], V[i + (size_t)a * kBcgsLd], v);
+      for (int a = qd; a < na; a += 4) v = fma(coef[a], V[i + (size_t)a * LD], v);
     v += __shfl_xor_sync(0xffffffffu, v, 1);
     v += __shfl_xor_sync(0xffffffffu, v, 2);
     if (qd == 0 && i < nr) x[i] -= v;
   }
 }
 
-template <int CS>
+template <int CS, int W, int RBM>
 __global__ void __launch_bounds__(kBcgsClusterThreads, 1)
     bcgs_block_cluster_kernel(const __grid_constant__ BcgsBatch B, int j0, int w) {
   namespace cg = cooperative_groups;
   extern __shared__ __align__(16) unsigned char smraw[];
-  BcgsClusterSmem& S = *reinterpret_cast<BcgsClusterSmem*>(smraw);
+  using Smem = BcgsClusterSmem<W, RBM>;
+  constexpr int LD = Smem::LD;
+  Smem& S = *reinterpret_cast<Smem*>(smraw);
   cg::cluster_group cl = cg::this_cluster();
   const BcgsEntry& E = B.e[blockIdx.y];
   if (j0 >= E.p) return;                                   // uniform over the cluster
@@ -1213,7 +1218,7 @@ __global__ void __launch_bounds__(kBcgsClusterThreads, 1)
   const int tid = threadIdx.x, nt = blockDim.x, warp = tid >> 5, ln = tid & 31, NW = nt >> 5;
   for (int idx = tid; idx < RB * wb; idx += nt) {
     const int i = idx % RB, c = idx / RB;
-    S.X[i + (size_t)c * kBcgsLd] = i < nr ? E.A[(size_t)(r0 + i) + (size_t)(j0 + c) * E.lda] : 0.0;
+    S.X[i + (size_t)c * LD] = i < nr ? E.A[(size_t)(r0 + i) + (size_t)(j0 + c) * E.lda] : 0.0;
   }
   double mx = 0.0;
   for (int c = tid; c < E.p; c += nt) mx = fmax(mx, E.norm0[c]);
@@ -1227,7 +1232,7 @@ __global__ void __launch_bounds__(kBcgsClusterThreads, 1)
   __syncthreads();
   // ---- pre-filter: all block column norms in one all-reduce ----
   for (int c = warp; c < wb; c += NW) {
-    const double* x = S.X + (size_t)c * kBcgsLd;
+    const double* x = S.X + (size_t)c * LD;
     double q = 0.0;
     for (int i = ln; i < nr; i += 32) q = fma(x[i], x[i], q);
     for (int o = 16; o > 0; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
@@ -1244,28 +1249,28 @@ __global__ void __launch_bounds__(kBcgsClusterThreads, 1)
   int na = 0, ph = 1;                                      // ph: partial buffer of the next phase
   for (int c = 0; c < wb; ++c) {
     if (!S.alive[c]) continue;
-    double* x = S.X + (size_t)c * kBcgsLd;
+    double* x = S.X + (size_t)c * LD;
     double s2;
     if (na == 0) {
-      block_dots(S.Yb, x, nr, 0, true, S.part[ph], S.red);
+      block_dots<LD>(S.Yb, x, nr, 0, true, S.part[ph], S.red);
       cl.sync();
       cluster_allreduce<CS>(cl, S.part[ph], 1, S.coef);
       __syncthreads();
       s2 = S.coef[0];
       ph ^= 1;
     } else {
-      block_dots(S.Yb, x, nr, na, false, S.part[ph], S.red);
+      block_dots<LD>(S.Yb, x, nr, na, false, S.part[ph], S.red);
       cl.sync();
       cluster_allreduce<CS>(cl, S.part[ph], na, S.coef);
       __syncthreads();
-      block_update(S.Yb, x, nr, na, S.coef);
+      block_update<LD, RBM>(S.Yb, x, nr, na, S.coef);
       __syncthreads();
       ph ^= 1;
-      block_dots(S.Yb, x, nr, na, true, S.part[ph], S.red);
+      block_dots<LD>(S.Yb, x, nr, na, true, S.part[ph], S.red);
       cl.sync();
       cluster_allreduce<CS>(cl, S.part[ph], na + 1, S.coef);
       __syncthreads();
-      block_update(S.Yb, x, nr, na, S.coef);
+      block_update<LD, RBM>(S.Yb, x, nr, na, S.coef);
       double c2 = 0.0;
       for (int a = 0; a < na; ++a) c2 = fma(S.coef[a], S.coef[a], c2);
       s2 = S.coef[na] - c2;
@@ -1275,15 +1280,15 @@ __global__ void __launch_bounds__(kBcgsClusterThreads, 1)
     const double lim = E.tau * fmax(E.norm0[j0 + c], nmax);
     if (s2 > lim * lim && k0 + na < E.kcap) {
       const double inv = 1.0 / sqrt(s2);
-      double* y = S.Yb + (size_t)na * kBcgsLd;
+      double* y = S.Yb + (size_t)na * LD;
       for (int i = tid; i < RB; i += nt) y[i] = i < nr ? x[i] * inv : 0.0;
       ++na;
     }
     __syncthreads();
   }
-  for (int idx = tid; idx < nr * kBcgsW; idx += nt) {      // unused block columns stay 0
+  for (int idx = tid; idx < nr * W; idx += nt) {           // unused block columns stay 0
     const int i = idx % nr, a = idx / nr;
-    E.Y[(size_t)(r0 + i) + (size_t)a * n] = a < na ? S.Yb[i + (size_t)a * kBcgsLd] : 0.0;
+    E.Y[(size_t)(r0 + i) + (size_t)a * n] = a < na ? S.Yb[i + (size_t)a * LD] : 0.0;
   }
   if (r == 0 && tid == 0) *E.nacc = na;
   cl.sync();                                                 // smem stays alive for readers
@@ -1292,12 +1297,14 @@ __global__ void __launch_bounds__(kBcgsClusterThreads, 1)
 // BCGS2 second pass, in-block part, on the cluster: Y[:, :nacc] (re-projected against Q) are
 // re-orthonormalised among themselves (one MGS pass, dots and norm in one all-reduce) and
 // appended to Q at k.
-template <int CS>
+template <int CS, int W, int RBM>
 __global__ void __launch_bounds__(kBcgsClusterThreads, 1)
     bcgs_finalize_cluster_kernel(const __grid_constant__ BcgsBatch B, int j0) {
   namespace cg = cooperative_groups;
   extern __shared__ __align__(16) unsigned char smraw[];
-  BcgsClusterSmem& S = *reinterpret_cast<BcgsClusterSmem*>(smraw);
+  using Smem = BcgsClusterSmem<W, RBM>;
+  constexpr int LD = Smem::LD;
+  Smem& S = *reinterpret_cast<Smem*>(smraw);
   cg::cluster_group cl = cg::this_cluster();
   const BcgsEntry& E = B.e[blockIdx.y];
   if (j0 >= E.p) return;
@@ -1307,17 +1314,17 @@ __global__ void __launch_bounds__(kBcgsClusterThreads, 1)
   const int tid = threadIdx.x, nt = blockDim.x;
   for (int idx = tid; idx < RB * na; idx += nt) {
     const int i = idx % RB, c = idx / RB;
-    S.Yb[i + (size_t)c * kBcgsLd] = i < nr ? E.Y[(size_t)(r0 + i) + (size_t)c * n] : 0.0;
+    S.Yb[i + (size_t)c * LD] = i < nr ? E.Y[(size_t)(r0 + i) + (size_t)c * n] : 0.0;
   }
   __syncthreads();
   for (int c = 0; c < na; ++c) {
-    double* y = S.Yb + (size_t)c * kBcgsLd;
+    double* y = S.Yb + (size_t)c * LD;
     double* part = S.part[c & 1];
-    block_dots(S.Yb, y, nr, c, true, part, S.red);
+    block_dots<LD>(S.Yb, y, nr, c, true, part, S.red);
     cl.sync();
     cluster_allreduce<CS>(cl, part, c + 1, S.coef);
     __syncthreads();
-    if (c > 0) block_update(S.Yb, y, nr, c, S.coef);
+    if (c > 0) block_update<LD, RBM>(S.Yb, y, nr, c, S.coef);
     double c2 = 0.0;
     for (int a = 0; a < c; ++a) c2 = fma(S.coef[a], S.coef[a], c2);
     const double s2 = S.coef[c] - c2;
@@ -1562,18 +1569,33 @@ void launch_cluster(K kern, int CS, int nb, size_t smem, cudaStream_t st, const 
   FC_CHECK_LAUNCH();
 }
 
-template <int CS>
+template <int CS, int W, int RB>
 void bcgs_cluster_setup() {
   static bool attr = false;
   if (attr) return;
-  const int smem = (int)sizeof(BcgsClusterSmem);
-  FC_CUDA_TRY(cudaFuncSetAttribute(bcgs_block_cluster_kernel<CS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  FC_CUDA_TRY(cudaFuncSetAttribute(bcgs_finalize_cluster_kernel<CS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  const int smem = (int)sizeof(BcgsClusterSmem<W, RB>);
+  FC_CUDA_TRY(cudaFuncSetAttribute(bcgs_block_cluster_kernel<CS, W, RB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  FC_CUDA_TRY(cudaFuncSetAttribute(bcgs_finalize_cluster_kernel<CS, W, RB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   smem));
   if (CS > 8) {
-    FC_CUDA_TRY(cudaFuncSetAttribute(bcgs_block_cluster_kernel<CS>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    FC_CUDA_TRY(cudaFuncSetAttribute(bcgs_finalize_cluster_kernel<CS>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    FC_CUDA_TRY(cudaFuncSetAttribute(bcgs_block_cluster_kernel<CS, W, RB>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    FC_CUDA_TRY(cudaFuncSetAttribute(bcgs_finalize_cluster_kernel<CS, W, RB>, cudaFuncAttributeNonPortableClusterSizeAllowed,
+                                     1));
   }
   attr = true;
+}
+
+template <int CS, int W, int RB>
+void bcgs_cluster_block(const BcgsBatch& bb, int j0, cudaStream_t st) {
+  bcgs_cluster_setup<CS, W, RB>();
+  launch_cluster(bcgs_block_cluster_kernel<CS, W, RB>, CS, bb.nb, sizeof(BcgsClusterSmem<W, RB>), st, bb, j0, W, true);
+}
+
+template <int CS, int W, int RB>
+void bcgs_cluster_finalize(const BcgsBatch& bb, int j0, cudaStream_t st) {
+  bcgs_cluster_setup<CS, W, RB>();
+  launch_cluster(bcgs_finalize_cluster_kernel<CS, W, RB>, CS, bb.nb, sizeof(BcgsClusterSmem<W, RB>), st, bb, j0, 0,
+                 false);
 }
 
 // split-K for the two skinny GEMMs of a block projection, P = Q^T A_blk (k x W x n) and
@@ -1587,28 +1609,32 @@ void split_skinny(GemmArgs& p, GemmArgs& u, int n, int k, int w, int nb) {
 
 void bcgs(const BcgsBatch& bin, cudaStream_t st) {
   if (bin.nb == 0) return;
-  constexpr int W = kBcgsW;
   static const bool no_cluster = getenv("FC_NO_CLUSTER") != nullptr;
+  static const int wenv = getenv("FC_BCGS_W") ? atoi(getenv("FC_BCGS_W")) : 64;
   int maxn = 0;
   for (int i = 0; i < bin.nb; ++i) maxn = std::max(maxn, bin.e[i].n);
-  const int CS = no_cluster || maxn > 16 * kBcgsRB ? 0 : (maxn <= 8 * kBcgsRB ? 8 : 16);
-  if (CS == 8) bcgs_cluster_setup<8>();
-  if (CS == 16) bcgs_cluster_setup<16>();
+  // 3: 8 CTAs x 128 rows, W = 64 (n <= 1024, default);  1: 16 x 64, W = 128 (n <= 1024,
+  // FC_BCGS_W=128: half the projection GEMMs, but slower in-block steps: 521 vs 479 ms per C4
+  // solve);  2: 16 x 128, W = 64 (n <= 2048);  0: one CTA per matrix (W = 64)
+  int cfg = 0;
+  if (!no_cluster) {
+    if (maxn <= 1024) cfg = wenv == 128 ? 1 : 3;
+    else if (maxn <= 2048) cfg = 2;
+  }
+  const int W = cfg == 1 ? 128 : 64;
   auto block_step = [&](const BcgsBatch& bb, int j0) {
-    if (CS == 8)
-      launch_cluster(bcgs_block_cluster_kernel<8>, 8, bb.nb, sizeof(BcgsClusterSmem), st, bb, j0, W, true);
-    else if (CS == 16)
-      launch_cluster(bcgs_block_cluster_kernel<16>, 16, bb.nb, sizeof(BcgsClusterSmem), st, bb, j0, W, true);
+    if (cfg == 1) bcgs_cluster_block<16, 128, 64>(bb, j0, st);
+    else if (cfg == 2) bcgs_cluster_block<16, 64, 128>(bb, j0, st);
+    else if (cfg == 3) bcgs_cluster_block<8, 64, 128>(bb, j0, st);
     else {
       bcgs_block_kernel<<<bb.nb, 1024, (size_t)bb.e[0].n * 8, st>>>(bb, j0, W);
       FC_CHECK_LAUNCH();
     }
   };
   auto finalize_step = [&](const BcgsBatch& bb, int j0) {
-    if (CS == 8)
-      launch_cluster(bcgs_finalize_cluster_kernel<8>, 8, bb.nb, sizeof(BcgsClusterSmem), st, bb, j0, 0, false);
-    else if (CS == 16)
-      launch_cluster(bcgs_finalize_cluster_kernel<16>, 16, bb.nb, sizeof(BcgsClusterSmem), st, bb, j0, 0, false);
+    if (cfg == 1) bcgs_cluster_finalize<16, 128, 64>(bb, j0, st);
+    else if (cfg == 2) bcgs_cluster_finalize<16, 64, 128>(bb, j0, st);
+    else if (cfg == 3) bcgs_cluster_finalize<8, 64, 128>(bb, j0, st);
     else {
       bcgs_finalize_kernel<<<bb.nb, 1024, (size_t)bb.e[0].n * 8, st>>>(bb, j0);
       FC_CHECK_LAUNCH();
@@ -1617,7 +1643,7 @@ void bcgs(const BcgsBatch& bin, cudaStream_t st) {
   BcgsBatch b = bin;
   Scratch scr(st);
   for (int i = 0; i < b.nb; ++i) {
-    b.e[i].Y = scr.alloc<double>((size_t)b.e[i].n * W);
+    b.e[i].Y = scr.alloc<double>((size_t)b.e[i].n * kBcgsW);
     b.e[i].nacc = scr.alloc<int>(1);
   }
   int maxp = 0;

@@ -54,7 +54,7 @@ void pmgs(const PmgsBatch& b, cudaStream_t st);
 // the accepted basis with DMMA GEMMs (twice), then orthogonalised in-block by one CTA; a column
 // is accepted when its residual exceeds tau * its original norm.  A (n x p) is overwritten;
 // Q (n x kcap) receives the basis, *k (device) its size; P is kcap x 32 scratch, norm0 p.
-constexpr int kBcgsW = 64;   // block width of the blocked Gram-Schmidt (P scratch: kcap x kBcgsW)
+constexpr int kBcgsW = 128;  // max block width of the blocked Gram-Schmidt (P scratch: kcap x kBcgsW)
 struct BcgsEntry {
   int n, p;
   double* A; int lda;
