@@ -176,6 +176,7 @@ void copy_cp_block(cudaStream_t st, int n, const fc_cp& src, fc_cp& dst, int col
 
 namespace fc {
 std::atomic<long long> g_launches{0};
+thread_local cudaStream_t tl_stream = nullptr;
 }
 
 // ======================================================================================
@@ -303,8 +304,14 @@ int fc_create(fc_ctx* ctx, void* cuda_stream) {
 int fc_destroy(fc_ctx c) {
   if (!c) return FC_OK;
   cudaStreamSynchronize(c->st);
+  if (c->st2) {
+    cudaStreamSynchronize(c->st2);
+    cudaStreamDestroy(c->st2);
+  }
   c->lam.release();
   c->V.release();
+  c->lamA.release();
+  c->VA.release();
   for (auto& s : c->spec) {
     s.w.release(); s.U.release(); s.W.release(); s.E.release();
   }

@@ -22,6 +22,7 @@ struct SpecCP {
 
 struct fc_ctx_s {
   cudaStream_t st = nullptr;
+  cudaStream_t st2 = nullptr;   // side stream of pcg_solve (the X update runs concurrently)
   int dev = 0;
   int n = 0;
   fc_params p{};
@@ -42,3 +43,9 @@ struct fc_ctx_s {
   // the eigenbasis a spectral CP is applied in
   const double* Vsp(const SpecCP& sp, int l) const { return sp.basis ? sp.basis + (size_t)l * n * n : V_l(l); }
 };
+
+namespace fc {
+// stream override of the calling host thread (pcg_solve's side thread truncates X on st2)
+extern thread_local cudaStream_t tl_stream;
+inline cudaStream_t stream_of(const fc_ctx_s* c) { return tl_stream ? tl_stream : c->st; }
+}  // namespace fc

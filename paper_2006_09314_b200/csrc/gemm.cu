@@ -13,6 +13,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <map>
+#include <mutex>
 #include "common.cuh"
 
 namespace fc {
@@ -417,6 +418,7 @@ void launch_big(const GemmArgs& a, dim3 grid, cudaStream_t st) {
 // the algorithmic flop count 2 M N K per batch entry ------------------------------------
 namespace {
 struct GemmProf {
+  std::mutex mu;                    // pcg_solve launches from two host threads
   bool on = false;
   std::vector<cudaEvent_t> ev;   // pairs
   std::vector<double> flops;
@@ -469,6 +471,7 @@ static void gemm_dispatch(const GemmArgs& a, cudaStream_t st);
 void gemm(const GemmArgs& a, cudaStream_t st) {
   GemmProf& P = gprof();
   if (!P.on) return gemm_dispatch(a, st);
+  std::lock_guard<std::mutex> lock(P.mu);
   if (P.ev.size() < 2 * (P.used + 1)) {
     for (int i = 0; i < 256; ++i) {
       cudaEvent_t e;

@@ -13,6 +13,8 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <exception>
+#include <thread>
 #include "cpops.cuh"
 #include "eig.cuh"
 #include "solver.cuh"
@@ -68,7 +70,7 @@ int nblocks(long long tot) { return (int)std::min<long long>(std::max<long long>
 // Reduced basis of the spectral CP: U_l = W_l E_l with W_l orthonormal (n x s_l).
 void ensure_spec_basis(fc_ctx c, SpecCP& sp) {
   if (sp.has_basis) return;
-  cudaStream_t st = c->st;
+  cudaStream_t st = stream_of(c);
   const int n = c->n, r = sp.r;
   Scratch s(st);
   int sdim[3];
@@ -106,7 +108,7 @@ void ensure_spec_basis(fc_ctx c, SpecCP& sp) {
 
 // S = trunc(F x) for a TT iterate x (physical coordinates, orthonormal bases).
 TT apply_truncate_tt(fc_ctx c, SpecCP& sp, const TT& x, double eps, int rank_cap, TruncStats* stats) {
-  cudaStream_t st = c->st;
+  cudaStream_t st = stream_of(c);
   const int n = c->n, r = sp.r, R = x.R;
   if (R == 0) {
     TT z;
@@ -234,6 +236,56 @@ void store_tt(fc_ctx c, const TT& x, fc_cp* y) {
 }
 }  // namespace
 
+// Algorithm 1 lines 10-11 (X <- trunc(X + a P)) on the context's side stream from a helper
+// thread: X is read again only by the next iteration's X update, so its truncation overlaps the
+// R, Z and P work of lines 12-21 (the truncation syncs its own stream to read ranks, hence the
+// second host thread).  Events order the streams both ways; the result's memory is re-homed on
+// the main stream.  The destructor joins on every path (also when the main thread throws).
+struct XJob {
+  fc_ctx c;
+  cudaStream_t st;
+  TT XP, out;
+  TruncStats stats;
+  std::exception_ptr err;
+  std::thread th;
+  bool joined = false;
+  XJob(fc_ctx c_, cudaStream_t st_, const TT& X, const TT& P, double a, double eps, int cap) : c(c_), st(st_) {
+    XP = tt_axpy(st, X, a, P);
+    cudaEvent_t ev;
+    FC_CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    FC_CUDA_TRY(cudaEventRecord(ev, st));
+    FC_CUDA_TRY(cudaStreamWaitEvent(c->st2, ev, 0));
+    FC_CUDA_TRY(cudaEventDestroy(ev));
+    th = std::thread([this, eps, cap]() {
+      tl_stream = c->st2;
+      try {
+        out = truncate_tt(c, XP, eps, cap, &stats);
+      } catch (...) {
+        err = std::current_exception();
+      }
+      tl_stream = nullptr;
+    });
+  }
+  void finish() {
+    if (joined) return;
+    joined = true;
+    th.join();
+    cudaEvent_t ev;
+    cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+    cudaEventRecord(ev, c->st2);
+    cudaStreamWaitEvent(st, ev, 0);   // main stream after the side stream's work (uses and frees)
+    cudaEventDestroy(ev);
+    for (auto& m : out.mem) m.st = st;
+  }
+  TT join(TruncStats* s) {
+    finish();
+    if (err) std::rethrow_exception(err);
+    *s = stats;
+    return std::move(out);
+  }
+  ~XJob() { finish(); }
+};
+
 extern "C" {
 
 int cp_truncate(fc_ctx c, const fc_cp* x, double eps, fc_cp* y, fc_trunc_info* info) {
@@ -302,7 +354,8 @@ int pcg_solve(fc_ctx c, const fc_cp* b, const fc_params* prm, fc_cp* u, fc_pcg_r
     const int kmax = std::min(prm->kmax > 0 ? prm->kmax : 100, FC_MAX_ITERS);  // A17
     const int cap = prm->rank_cap > 0 ? prm->rank_cap : (1 << 20);
     require(c->spec[FC_F].valid && c->spec[FC_G].valid, FC_ERR_NOT_READY, "spectral CPs missing");
-    cudaStream_t st = c->st;
+    cudaStream_t st = stream_of(c);
+    if (!c->st2) FC_CUDA_TRY(cudaStreamCreateWithFlags(&c->st2, cudaStreamNonBlocking));
     fc_pcg_report local{};
     fc_pcg_report& RP = rep ? *rep : local;
     RP = fc_pcg_report{};
@@ -351,10 +404,7 @@ int pcg_solve(fc_ctx c, const fc_cp* b, const fc_params* prm, fc_cp* u, fc_pcg_r
       if (!std::isfinite(ps)) { cudaEventDestroy(loop0); throw Error(FC_ERR_NAN, "<P,S> is not finite"); }
       if (ps <= 0) { cudaEventDestroy(loop0); throw Error(FC_ERR_NOT_SPD, "<P,S> <= 0"); }
       const double a_k = rz / ps;                                   // line 9
-      {
-        TT XP = tt_axpy(st, X, a_k, P);                             // lines 10-11
-        X = truncate_tt(c, XP, eps, cap, &sX);
-      }
+      XJob xjob(c, st, X, P, a_k, eps, cap);                        // lines 10-11 (side stream)
       {
         TT RS = tt_axpy(st, R, -a_k, S);                            // lines 12-13
         R = truncate_tt(c, RS, eps, cap, &sR);
@@ -363,12 +413,13 @@ int pcg_solve(fc_ctx c, const fc_cp* b, const fc_params* prm, fc_cp* u, fc_pcg_r
       const double rel = std::sqrt(std::max(rr, 0.0)) / normB;      // line 14 (A13)
       RP.rel_res[k] = rel;
       RP.rank_S[k] = S.R;
-      RP.rank_X[k] = X.R;
       RP.rank_R[k] = R.R;
       RP.tucker_S[k] = std::max(sS.tucker[0], std::max(sS.tucker[1], sS.tucker[2]));
       RP.iters = k + 1;
       if (!std::isfinite(rel)) { cudaEventDestroy(loop0); throw Error(FC_ERR_NAN, "residual is not finite"); }
       if (rel <= tol) {
+        X = xjob.join(&sX);
+        RP.rank_X[k] = X.R;
         RP.rank_Z[k] = Z.R;
         RP.rank_P[k] = P.R;
         FC_CUDA_TRY(cudaEventRecord(ti1, st));
@@ -388,6 +439,8 @@ int pcg_solve(fc_ctx c, const fc_cp* b, const fc_params* prm, fc_cp* u, fc_pcg_r
         P = truncate_tt(c, ZP, eps, cap, &sP);
       }
       rz = rz_new;
+      X = xjob.join(&sX);
+      RP.rank_X[k] = X.R;
       RP.rank_Z[k] = Z.R;
       RP.rank_P[k] = P.R;
       FC_CUDA_TRY(cudaEventRecord(ti1, st));

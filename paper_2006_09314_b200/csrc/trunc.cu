@@ -458,7 +458,7 @@ int read_int(const int* d, cudaStream_t st) {
 // ---------------------------------------------------------------------------------------
 TT tucker_to_canonical(fc_ctx c, const double* core, const int r[3], double* const Z[3], int n, double eps,
                        int keep, int rank_cap, TruncStats* stats) {
-  cudaStream_t st = c->st;
+  cudaStream_t st = stream_of(c);
   int mc = 0;
   for (int l = 1; l < 3; ++l)
     if (r[l] < r[mc]) mc = l;                       // ties -> lowest mode
@@ -588,7 +588,7 @@ int struct_chunk(const StructuredS* ss) {
 }
 
 TT truncate_tt(fc_ctx c, const TT& xin, double eps, int rank_cap, TruncStats* stats, const StructuredS* ss) {
-  cudaStream_t st = c->st;
+  cudaStream_t st = stream_of(c);
   const int n = xin.n, R = xin.R;
   TruncStats local;
   TruncStats& S = stats ? *stats : local;
@@ -965,7 +965,7 @@ TT tt_axpy(cudaStream_t st, const TT& x, double a, const TT& y) {
 
 double tt_dot(fc_ctx c, const TT& x, const TT& y) {
   if (x.R == 0 || y.R == 0) return 0.0;
-  cudaStream_t st = c->st;
+  cudaStream_t st = stream_of(c);
   Scratch s(st);
   double* H = s.alloc<double>((size_t)3 * x.R * y.R + 1);
   for (int l = 0; l < 3; ++l) {
