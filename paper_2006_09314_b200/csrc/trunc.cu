@@ -178,6 +178,9 @@ __global__ void extract_slices_kernel(const double* __restrict__ core, int r0, i
 constexpr int kSliceMax = 512;
 __device__ int g_slice_sweeps_max = 0;   // diagnostics (FC_TRACE): most Jacobi sweeps of a slice
 constexpr size_t kSliceSmem = 200 * 1024;
+// SMEM: the working set lives in shared memory (the compiler then emits LDS/STS; with a pointer
+// that may be global it emits generic loads); else in the per-slice global workspace gws.
+template <bool SMEM>
 __global__ void __launch_bounds__(512) slice_svd_kernel(int ra, int rb, const double* __restrict__ S, double* s_out,
                                                         double* Ua, double* Vb, double* gws) {
   extern __shared__ double sm[];
@@ -185,10 +188,9 @@ __global__ void __launch_bounds__(512) slice_svd_kernel(int ra, int rb, const do
   const bool tr = ra < rb;                     // work on S^T when wide
   const int rows = tr ? rb : ra, cols = tr ? ra : rb;
   const int k = cols;                          // = min(ra, rb)
-  const bool in_smem = gws == nullptr;
-  double* A = in_smem ? sm : gws + (size_t)nu * ((size_t)rows * cols + (size_t)cols * cols);   // rows x cols
+  double* A = SMEM ? sm : gws + (size_t)nu * ((size_t)rows * cols + (size_t)cols * cols);   // rows x cols
   double* W = A + rows * cols;                 // cols x cols rotations
-  double* nrm = in_smem ? W + cols * cols : sm;  // cols
+  double* nrm = SMEM ? W + cols * cols : sm;   // cols
   int* order = (int*)(nrm + cols);             // cols
   const double* src = S + (size_t)nu * ra * rb;
   const int tid = threadIdx.x, nt = blockDim.x, warp = tid >> 5, ln = tid & 31, nw = nt >> 5;
@@ -237,28 +239,34 @@ __global__ void __launch_bounds__(512) slice_svd_kernel(int ra, int rb, const do
   int G = 32;
   while (G > 4 && nt / G < p / 2) G >>= 1;
   const int gid = tid / G, gl = tid % G, ng = nt / G;
-  const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << ((ln / G) * G));
   for (int sweep = 0; sweep < 40; ++sweep) {
     if (tid == 0) changed = 0;
     __syncthreads();
     for (int rd = 0; rd < p - 1; ++rd) {
-      for (int pi = gid; pi < p / 2; pi += ng) {
-        int a, b;
-        if (pi == 0) { a = rd % (p - 1); b = p - 1; }
-        else { a = (rd + pi) % (p - 1); b = (rd - pi + p - 1) % (p - 1); }
-        if (a > b) { int t = a; a = b; b = t; }
-        if (b >= cols) continue;
+      // uniform trip count over the block: every lane reaches the shuffles (full mask, no
+      // divergent shuffle handling); groups without a pair reduce zeros
+      for (int pi0 = 0; pi0 < p / 2; pi0 += ng) {
+        const int pi = pi0 + gid;
+        int a = 0, b = 0;
+        bool act = pi < p / 2;
+        if (act) {
+          if (pi == 0) { a = rd % (p - 1); b = p - 1; }
+          else { a = (rd + pi) % (p - 1); b = (rd - pi + p - 1) % (p - 1); }
+          if (a > b) { int t = a; a = b; b = t; }
+          act = b < cols;
+        }
         double al = 0, be = 0, ga = 0;
-        for (int i = gl; i < rows; i += G) {
-          double x = A[i + a * rows], y = A[i + b * rows];
-          al = fma(x, x, al); be = fma(y, y, be); ga = fma(x, y, ga);
-        }
+        if (act)
+          for (int i = gl; i < rows; i += G) {
+            double x = A[i + a * rows], y = A[i + b * rows];
+            al = fma(x, x, al); be = fma(y, y, be); ga = fma(x, y, ga);
+          }
         for (int o = G >> 1; o > 0; o >>= 1) {
-          al += __shfl_xor_sync(gmask, al, o);
-          be += __shfl_xor_sync(gmask, be, o);
-          ga += __shfl_xor_sync(gmask, ga, o);
+          al += __shfl_xor_sync(0xffffffffu, al, o);
+          be += __shfl_xor_sync(0xffffffffu, be, o);
+          ga += __shfl_xor_sync(0xffffffffu, ga, o);
         }
-        if (ga == 0.0 || ga * ga <= tol2 * (al * be) || al <= neg2 || be <= neg2) continue;
+        if (!act || ga == 0.0 || ga * ga <= tol2 * (al * be) || al <= neg2 || be <= neg2) continue;
         // Rutishauser's rotation, zeta = (be - al) / (2 ga), t = sign(zeta) / (|zeta| + sqrt(1 + zeta^2)),
         // written with one square root and one division
         const double dd = be - al, g2 = 2.0 * ga;
@@ -487,10 +495,12 @@ TT tucker_to_canonical(fc_ctx c, const double* core, const int r[3], double* con
   }
   static bool attr = false;
   if (!attr) {
-    FC_CUDA_TRY(cudaFuncSetAttribute(slice_svd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSliceSmem));
+    FC_CUDA_TRY(cudaFuncSetAttribute(slice_svd_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)kSliceSmem));
     attr = true;
   }
-  slice_svd_kernel<<<rc, 512, smem, st>>>(ra, rb, S, sv, Ua, Vb, gws);
+  if (gws) slice_svd_kernel<false><<<rc, 512, smem, st>>>(ra, rb, S, sv, Ua, Vb, gws);
+  else slice_svd_kernel<true><<<rc, 512, smem, st>>>(ra, rb, S, sv, Ua, Vb, nullptr);
   FC_CHECK_LAUNCH();
   if (getenv("FC_TRACE")) {
     int sw = 0, zero = 0;
