@@ -142,6 +142,14 @@ int op_spectral_rank(fc_ctx ctx, int which, int* rank, int* tucker_rank /* [3] o
  * set (shared-input parity): copies; once all 3 modes are set the FC_G spectral CP is applied
  * in this basis (its CP must then be built on these lam, op_set_spectral_cp). */
 int op_get_precond_basis(fc_ctx ctx, int mode, double* lam, double* V);
+/* Sinc-quadrature construction of a spectral CP [P:325-351, P:725-752]:
+ * lam^-alpha = 1/Gamma(alpha) int_0^inf t^(alpha-1) e^(-t lam) dt ~ sum_k c_k prod_l e^(-t_k lam_l)
+ * (rank 2M+1 = O(|log eps| log(lam_max/lam_min)), positive factors, pointwise relative accuracy
+ * ~eps).  which = FC_POW_MINUS (the rule itself, untruncated), FC_POW_PLUS (lam-sum (.)
+ * lam^(alpha-1), truncated at eps) or FC_F (beta lam^alpha + lam^-alpha, truncated at eps); the
+ * result replaces that spectral CP of the context.  Needs the eigenpairs and alpha, beta
+ * (sl_setup, or sl_set_eigen with params).  Errors: NOT_READY, INVALID_ARG, CUDA. */
+int op_build_spectral_sinc(fc_ctx ctx, int which, double eps);
 int op_set_precond_basis(fc_ctx ctx, int mode, const double* lam, const double* V);
 
 /* ---- the operator: S5..S8 -------------------------------------------------------------- */

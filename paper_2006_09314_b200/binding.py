@@ -69,7 +69,7 @@ ENTRY_POINTS = ["fc_create", "fc_destroy", "fc_last_error", "fc_set_stream", "sl
                 "sl_set_eigen", "op_get_spectral_cp", "op_set_spectral_cp", "op_spectral_rank",
                 "fracop_apply", "precond_apply", "cp_dot", "cp_axpy", "cp_truncate", "pcg_solve",
                 "fc_dgemm", "fc_last_kernel_stats", "fc_kernel_launches", "fracop_apply_truncate", "fc_orthonormalize",
-                "fc_profile_gemm", "fc_syev", "op_get_precond_basis", "op_set_precond_basis", "state_recover"]
+                "fc_profile_gemm", "fc_syev", "op_get_precond_basis", "op_set_precond_basis", "state_recover", "op_build_spectral_sinc"]
 
 
 def load_library(path: str = LIB_PATH) -> C.CDLL:
@@ -101,6 +101,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
                      C.POINTER(I)], I),
         "op_get_precond_basis": ([P, I, P, P], I), "op_set_precond_basis": ([P, I, P, P], I),
         "state_recover": ([P, cpp, D, cpp, C.POINTER(fc_trunc_info)], I),
+        "op_build_spectral_sinc": ([P, I, D], I),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -294,6 +295,9 @@ class Context:
             self._check(rc)
             y.rank = ys.rank
             return y, info
+
+    def op_build_spectral_sinc(self, which, eps):
+        self._check(self.lib.op_build_spectral_sinc(self.h, which, C.c_double(eps)))
 
     def state_recover(self, u: DeviceCP, eps: float, cap: int | None = None):
         """y = A^-alpha u truncated at eps (state_recover)."""

@@ -368,6 +368,13 @@ int sl_set_eigen(fc_ctx c, int n, int mode, const double* lam, const double* V, 
   });
 }
 
+int op_build_spectral_sinc(fc_ctx c, int which, double eps) {
+  return guard(c, [&]() {
+    build_spectral_sinc(c, which, eps);
+    return FC_OK;
+  });
+}
+
 int op_get_precond_basis(fc_ctx c, int mode, double* lam, double* V) {
   return guard(c, [&]() {
     require(mode >= 0 && mode < 3, FC_ERR_INVALID_ARG, "mode");

@@ -12,4 +12,5 @@ void build_spectral_cp(fc_ctx c, int which, double alpha, double beta, double ep
                        const double* lam3, const double* basis);
 // FC_POW_PLUS / FC_POW_MINUS spectral CPs are built on first use (eps_D-driven, SL basis)
 void ensure_spectral(fc_ctx c, int which);
+void build_spectral_sinc(fc_ctx c, int which, double eps);
 }  // namespace fc

@@ -14,6 +14,7 @@
 #include <cfloat>
 #include <cstring>
 #include <cmath>
+#include <vector>
 #include "cpops.cuh"
 #include "eig.cuh"
 #include "solver.cuh"
@@ -358,6 +359,171 @@ void build_spectral_cp(fc_ctx c, int which, double alpha, double beta, double ep
   store_spec(c, c->spec[which], x, cr.s);
   if (shifted) c->spec[which].has_basis = false;   // the appended term: recompute W, E (pmgs)
   c->spec[which].basis = basis;
+}
+
+// ---- sinc-quadrature construction [P:325-351, P:725-752] ------------
+// lam^-a = 1/Gamma(a) int_R exp(a x - lam e^x) dx ~ sum_k c_k exp(-t_k lam), t_k = e^(x_k),
+// c_k = h e^(a x_k) / Gamma(a), h = 2 pi d / ln(1/eps) with the strip half-width d = pi/3 (the
+// error constant grows towards d = pi/2); [x_lo, x_hi] drops the tails below
+// eps Gamma(a) lam^-a on [lam_min, lam_max] (lower: e^(a x_lo)/a; upper: L^a e^-L, L = lam_min e^x_hi)
+void sinc_nodes_host(double a, double lam_min, double lam_max, double eps, std::vector<double>& t,
+                     std::vector<double>& c) {
+  const double g = std::tgamma(a), h = 2.0 * M_PI * (M_PI / 3.0) / std::log(1.0 / eps);
+  const double x_lo = (std::log(eps * a * g) - a * std::log(lam_max)) / a;
+  double L = std::log(1.0 / (eps * g));
+  for (int i = 0; i < 20; ++i) L = std::log(1.0 / (eps * g)) + a * std::log(std::max(L, 1.0));
+  const double x_hi = std::log(L / lam_min);
+  const int m = (int)std::ceil((x_hi - x_lo) / h);
+  t.resize(m + 1);
+  c.resize(m + 1);
+  for (int k = 0; k <= m; ++k) {
+    const double x = x_lo + h * k;
+    t[k] = std::exp(x);
+    c[k] = h * std::exp(a * x) / g;
+  }
+}
+
+// column k of mode l (block (k, l)): U = exp(-t_k lam_l) / norm, nrm[l*R + k] = norm
+__global__ void sinc_factor_kernel(int n, int R, const double* __restrict__ lam3, const double* __restrict__ t,
+                                   double* U, double* nrm) {
+  __shared__ double red[32];
+  const int k = blockIdx.x, l = blockIdx.y;
+  const double* lam = lam3 + (size_t)l * n;
+  double* u = U + (size_t)l * n * R + (size_t)k * n;
+  double part = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const double v = exp(-t[k] * lam[i]);
+    u[i] = v;
+    part = fma(v, v, part);
+  }
+  for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = part;
+  __syncthreads();
+  double s2 = 0.0;
+  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s2 += red[w];
+  const double nr = sqrt(s2), inv = nr > 0 ? 1.0 / nr : 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) u[i] *= inv;
+  if (threadIdx.x == 0) nrm[(size_t)l * R + k] = nr;
+}
+
+// D (.) Q: term m*R + k, mode l factor (l == m ? lam_l : 1) .* Q_l[:, k]  (D = lam-sum, rank 3)
+__global__ void lam_hadamard_kernel(int n, int R, const double* __restrict__ lam3, const double* __restrict__ Q,
+                                    double* out) {
+  const long long tot = 3LL * 3 * R * n;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < tot;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(idx % n);
+    const int term = (int)((idx / n) % (3 * R));
+    const int l = (int)(idx / ((long long)n * 3 * R));
+    const int m = term / R, k = term % R;
+    const double q = Q[(size_t)l * n * R + (size_t)k * n + i];
+    out[idx] = (l == m ? lam3[(size_t)l * n + i] : 1.0) * q;
+  }
+}
+
+namespace {
+// CP of lam^-a over the context's lam-sums by the sinc rule, as a (plain, rank 2M+1) TT
+TT sinc_pow_minus_tt(fc_ctx c, double a, double eps) {
+  cudaStream_t st = c->st;
+  const int n = c->n;
+  double lo = 0.0, hi = 0.0;
+  for (int l = 0; l < 3; ++l) {
+    double e[2];
+    FC_CUDA_TRY(cudaMemcpyAsync(e, c->lam_l(l), 8, cudaMemcpyDeviceToHost, st));
+    FC_CUDA_TRY(cudaMemcpyAsync(e + 1, c->lam_l(l) + n - 1, 8, cudaMemcpyDeviceToHost, st));
+    FC_CUDA_TRY(cudaStreamSynchronize(st));
+    lo += e[0];
+    hi += e[1];
+  }
+  std::vector<double> t, cw;
+  sinc_nodes_host(a, lo, hi, eps, t, cw);
+  const int R = (int)t.size();
+  Scratch s(st);
+  double* td = s.alloc<double>(R);
+  double* U = s.alloc<double>((size_t)3 * n * R);
+  double* nrm = s.alloc<double>((size_t)3 * R);
+  FC_CUDA_TRY(cudaMemcpyAsync(td, t.data(), (size_t)R * 8, cudaMemcpyHostToDevice, st));
+  sinc_factor_kernel<<<dim3(R, 3), 256, 0, st>>>(n, R, c->lam.p, td, U, nrm);
+  FC_CHECK_LAUNCH();
+  std::vector<double> hn((size_t)3 * R);
+  FC_CUDA_TRY(cudaMemcpyAsync(hn.data(), nrm, hn.size() * 8, cudaMemcpyDeviceToHost, st));
+  FC_CUDA_TRY(cudaStreamSynchronize(st));
+  for (int k = 0; k < R; ++k) cw[k] *= hn[k] * hn[R + k] * hn[2 * R + k];
+  double* wd = s.alloc<double>(R);
+  FC_CUDA_TRY(cudaMemcpyAsync(wd, cw.data(), (size_t)R * 8, cudaMemcpyHostToDevice, st));
+  double* Up[3] = {U, U + (size_t)n * R, U + (size_t)2 * n * R};
+  const int ld[3] = {n, n, n};
+  TT x = tt_from_cp(st, n, R, wd, Up, ld);
+  FC_CUDA_TRY(cudaStreamSynchronize(st));
+  return x;
+}
+
+// lam^a = lam-sum (.) lam^(a-1), truncated at eps (a = 1: the rank-3 lam-sum itself)
+TT sinc_pow_plus_tt(fc_ctx c, double a, double eps) {
+  cudaStream_t st = c->st;
+  const int n = c->n;
+  Scratch s(st);
+  int R;
+  std::vector<double> hw;
+  double* Q;
+  if (a >= 1.0) {   // the lam-sum: Q = one unit constant column per mode, weight sqrt(n)^2 ... via R = 1
+    R = 1;
+    std::vector<double> h1((size_t)3 * n, 1.0 / std::sqrt((double)n));
+    Q = s.alloc<double>((size_t)3 * n);
+    FC_CUDA_TRY(cudaMemcpyAsync(Q, h1.data(), h1.size() * 8, cudaMemcpyHostToDevice, st));
+    hw.assign(1, std::pow((double)n, 1.5));
+  } else {
+    TT q = sinc_pow_minus_tt(c, 1.0 - a, eps);
+    R = q.R;
+    Q = s.alloc<double>((size_t)3 * n * R);
+    double* Qp[3] = {Q, Q + (size_t)n * R, Q + (size_t)2 * n * R};
+    const int ld[3] = {n, n, n};
+    double* qw = s.alloc<double>(R);
+    tt_expand(st, q, Qp, ld, qw);
+    hw.resize(R);
+    FC_CUDA_TRY(cudaMemcpyAsync(hw.data(), qw, (size_t)R * 8, cudaMemcpyDeviceToHost, st));
+    FC_CUDA_TRY(cudaStreamSynchronize(st));
+  }
+  double* H = s.alloc<double>((size_t)3 * n * 3 * R);
+  lam_hadamard_kernel<<<nblk(9LL * R * n), 256, 0, st>>>(n, R, c->lam.p, Q, H);
+  FC_CHECK_LAUNCH();
+  std::vector<double> w3((size_t)3 * R);
+  for (int m = 0; m < 3; ++m)
+    for (int k = 0; k < R; ++k) w3[(size_t)m * R + k] = hw[k];
+  double* wd = s.alloc<double>((size_t)3 * R);
+  FC_CUDA_TRY(cudaMemcpyAsync(wd, w3.data(), w3.size() * 8, cudaMemcpyHostToDevice, st));
+  double* Hp[3] = {H, H + (size_t)n * 3 * R, H + (size_t)2 * n * 3 * R};
+  const int ld[3] = {n, n, n};
+  TT x = tt_from_cp(st, n, 3 * R, wd, Hp, ld);
+  return truncate_tt(c, x, eps, 0, nullptr);
+}
+}  // namespace
+
+// op_build_spectral_sinc: spectral CP of `which` (FC_POW_MINUS: the sinc rule itself, rank 2M+1,
+// untruncated; FC_POW_PLUS: lam-sum (.) lam^(alpha-1), truncated; FC_F: beta lam^alpha + lam^-alpha,
+// truncated) over the context's SL eigenvalues
+void build_spectral_sinc(fc_ctx c, int which, double eps) {
+  require(c->have_params, FC_ERR_NOT_READY, "alpha/beta unknown: call sl_setup (or sl_set_eigen with params)");
+  require(c->n > 0 && c->have_eig[0] && c->have_eig[1] && c->have_eig[2], FC_ERR_NOT_READY, "eigenpairs missing");
+  require(which == FC_POW_MINUS || which == FC_POW_PLUS || which == FC_F, FC_ERR_INVALID_ARG,
+          "sinc construction: FC_POW_MINUS, FC_POW_PLUS or FC_F");
+  require(eps > 0 && eps < 1, FC_ERR_INVALID_ARG, "eps in (0, 1)");
+  const double a = c->p.alpha, b = c->p.beta;
+  TT x;
+  if (which == FC_POW_MINUS) {
+    x = sinc_pow_minus_tt(c, a, eps);
+  } else if (which == FC_POW_PLUS) {
+    x = sinc_pow_plus_tt(c, a, eps);
+  } else {
+    TT pm = sinc_pow_minus_tt(c, a, eps);
+    TT pp = sinc_pow_plus_tt(c, a, eps);
+    TT sum = tt_axpy(c->st, pm, b, pp);
+    x = truncate_tt(c, sum, eps, 0, nullptr);
+  }
+  const int tk[3] = {x.q[0], x.q[1], x.q[2]};
+  store_spec(c, c->spec[which], x, tk);
+  c->spec[which].basis = nullptr;
+  if (which == FC_POW_MINUS) c->spec[which].has_basis = false;   // plain CP: recompute W, E
 }
 
 void ensure_spectral(fc_ctx c, int which) {
