@@ -46,8 +46,9 @@ inline void* dev_alloc(size_t bytes, cudaStream_t st) {
   const cudaError_t e = cudaMallocAsync(&p, bytes, st);
   if (e != cudaSuccess) {
     cudaGetLastError();
-    throw Error(FC_ERR_CUDA, "device allocation of " + std::to_string(bytes >> 20) + " MiB failed: " +
-                                 cudaGetErrorString(e));
+    // out of device memory = the problem's ranks exceed what the device holds (reading A22: CAPACITY)
+    throw Error(e == cudaErrorMemoryAllocation ? FC_ERR_CAPACITY : FC_ERR_CUDA,
+                "device allocation of " + std::to_string(bytes >> 20) + " MiB failed: " + cudaGetErrorString(e));
   }
   return p;
 }

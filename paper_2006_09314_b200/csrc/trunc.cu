@@ -76,6 +76,21 @@ __global__ void struct_scale_kernel(int t, int R, int Rx, const double* __restri
   }
 }
 
+// s2[i] += sum_j C[i, j]^2 over this block's column range (rows x cols, ld rows): threads over
+// rows (coalesced), blocks over column ranges, atomic accumulation of the partial sums
+__global__ void row_sumsq_kernel(int rows, int cols, const double* __restrict__ C, double* s2) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= rows) return;
+  const int per = (cols + gridDim.y - 1) / gridDim.y;
+  const int j0 = blockIdx.y * per, j1 = min(cols, j0 + per);
+  double acc = 0.0;
+  for (int j = j0; j < j1; ++j) {
+    const double v = C[i + (size_t)j * rows];
+    acc = fma(v, v, acc);
+  }
+  atomicAdd(s2 + i, acc);
+}
+
 // out[:, c] = in[:, c] * d[c]   (rows x cols, ld rows)
 __global__ void scale_cols_kernel(int rows, int cols, const double* __restrict__ in, const double* __restrict__ d,
                                   double* out) {
@@ -175,7 +190,7 @@ __global__ void extract_slices_kernel(const double* __restrict__ core, int r0, i
 // Ua[nu*ra*k + m*ra + x], Vb[nu*rb*k + m*rb + y].
 // Slices whose working set exceeds the shared-memory budget run the same algorithm in a
 // per-slice global (L2-resident) workspace `gws` of (rows*cols + cols*cols) doubles.
-constexpr int kSliceMax = 512;
+constexpr int kSliceMax = 1024;
 __device__ int g_slice_sweeps_max = 0;   // diagnostics (FC_TRACE): most Jacobi sweeps of a slice
 constexpr size_t kSliceSmem = 200 * 1024;
 // SMEM: the working set lives in shared memory (the compiler then emits LDS/STS; with a pointer
@@ -473,7 +488,7 @@ TT tucker_to_canonical(fc_ctx c, const double* core, const int r[3], double* con
   int ma = (mc == 0) ? 1 : 0, mb = (mc == 2) ? 1 : 2;
   const int ra = r[ma], rb = r[mb], rc = r[mc];
   const int k = std::min(ra, rb);
-  require(std::max(ra, rb) <= kSliceMax, FC_ERR_CAPACITY, "Tucker rank above the T2C slice limit (512)");
+  require(std::max(ra, rb) <= kSliceMax, FC_ERR_CAPACITY, "Tucker rank above the T2C slice limit (1024)");
   const int K = rc * k;
   Scratch s(st);
   double* S = s.alloc<double>((size_t)ra * rb * rc);
@@ -588,6 +603,8 @@ void tt_compute_core(cudaStream_t st, TT& x) {
 // ~2 kBasisTol ||A|| sigma_cut, i.e. <= 4e-4 of the threshold (eps/2)^2 ||A||^2 at eps = 1e-6,
 // well inside the A23 noise band; it shrinks the eigenproblem (and its N^3 cost) notably.
 constexpr double kBasisTol = 1e-10;
+// Gram eigenvalue noise per direction, in units of eps_mach * lam_max (refined cut below it)
+constexpr double kNoise = 1.0;
 
 // spectral terms per chunk of the structured norm / Gram pass: t x (Rx * chunk) <= 2^27 doubles
 constexpr size_t kStructChunk = (size_t)1 << 27;
@@ -753,8 +770,9 @@ TT truncate_tt(fc_ctx c, const TT& xin, double eps, int rank_cap, TruncStats* st
                                           inv[2], energy);
   FC_CHECK_LAUNCH();
   // ---- 3. side matrix in the basis: B_l = C_l D_l (q x R); M_l = B_l B_l^T -------------
-  double* Bm[3];
+  double* Bm[3] = {nullptr, nullptr, nullptr};
   double* M[3];
+  const bool sgram_used = ss != nullptr;
   if (ss) {
     // M_l = sum_kk Rm_kk H_kk Rm_kk^T,  H_kk = W_kk W_kk^T,  W_kk = Cx diag(d_l[kk*Rx + .])
     // (t x t per spectral term, W chunked over kk): G_kk = Rm_kk H_kk, then
@@ -840,13 +858,86 @@ TT truncate_tt(fc_ctx c, const TT& xin, double eps, int rank_cap, TruncStats* st
   }
   syev_values(eb, st);
   for (int l = 0; l < 3; ++l) rank_cut_device(q[l], lam[l], 0.25 * eps * eps, energy, rl + l, margins + l, st);
-  syev_vectors(eb, maxq, st);
   int r[3];
-  double hm[3];
+  double hm[3], lam0[3];
   FC_CUDA_TRY(cudaMemcpyAsync(r, rl, 3 * sizeof(int), cudaMemcpyDeviceToHost, st));
   FC_CUDA_TRY(cudaMemcpyAsync(hm, margins, 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
   FC_CUDA_TRY(cudaMemcpyAsync(&S.energy, energy, sizeof(double), cudaMemcpyDeviceToHost, st));
+  for (int l = 0; l < 3; ++l) FC_CUDA_TRY(cudaMemcpyAsync(lam0 + l, lam[l], sizeof(double), cudaMemcpyDeviceToHost, st));
   FC_CUDA_TRY(cudaStreamSynchronize(st));
+  // Noise-limited cuts (small eps, large bases): the Gram's eigenvalues carry ~eps_mach lam_max
+  // each as rounding noise, so when the threshold (eps/2)^2 E is below k * kNoise * eps_mach lam_max
+  // the eigenvalue tails cannot decide the cut.  Then all eigenvectors are computed and the tails
+  // are taken from the data instead: s2_i = ||y_i^T B||^2 (B the side matrix in the basis; errors
+  // ~eps_mach ||B|| sigma_i, not eps_mach ||B||^2; the y_i are orthonormal to ~1e-15, and mixing
+  // across the cut leaks only ~(eps_mach ||M||)^2 / lam_r of energy) — reading A11', DESIGN.md.
+  bool refine[3] = {false, false, false}, any_refine = false;
+  for (int l = 0; l < 3; ++l) {
+    refine[l] = 0.25 * eps * eps * S.energy < kNoise * q[l] * 2.220446049250313e-16 * lam0[l] && q[l] > 1;
+    any_refine |= refine[l];
+  }
+  if (any_refine) {
+    int hr[3] = {r[0], r[1], r[2]};
+    for (int l = 0; l < 3; ++l)
+      if (refine[l]) hr[l] = q[l];
+    FC_CUDA_TRY(cudaMemcpyAsync(rl, hr, 3 * sizeof(int), cudaMemcpyHostToDevice, st));
+  }
+  syev_vectors(eb, maxq, st);
+  if (any_refine) {
+    for (int l = 0; l < 3; ++l) {
+      if (!refine[l]) continue;
+      const int ql = q[l];
+      double* s2r = s.zeros<double>(ql);
+      if (!sgram_used) {
+        // C = Y^T Bm (ql x R), row sums of squares
+        const size_t chunk = std::max<size_t>(1, ((size_t)1 << 27) / std::max(ql, 1));
+        double* Cb = s.alloc<double>((size_t)ql * std::min<size_t>(chunk, (size_t)R));
+        for (size_t c0 = 0; c0 < (size_t)R; c0 += chunk) {
+          const int m = (int)std::min(chunk, (size_t)R - c0);
+          dgemm(st, 1, 0, ql, m, ql, 1.0, Y[l], ql, Bm[l] + c0 * ql, ql, 0.0, Cb, ql);
+          row_sumsq_kernel<<<dim3(cdiv(ql, 128), std::min(cdiv(m, 256), 512)), 128, 0, st>>>(ql, m, Cb, s2r);
+          FC_CHECK_LAUNCH();
+        }
+      } else {
+        // structured: (Y^T Rm_kk) (Cx D_kk) per spectral term kk, chunked
+        const int t = ss->t[l], rr = ss->r, Rx = ss->Rx;
+        double* YR = s.alloc<double>((size_t)ql * t * rr);
+        dgemm(st, 1, 0, ql, t * rr, ql, 1.0, Y[l], ql, RmE[l], ql, 0.0, YR, ql);
+        const int kc = std::max(1, (int)std::min<size_t>((size_t)rr, ((size_t)1 << 26) /
+                                                                   std::max<size_t>((size_t)ql * Rx, 1)));
+        double* Wc = s.alloc<double>((size_t)t * Rx * kc);
+        double* Cb = s.alloc<double>((size_t)ql * Rx * kc);
+        for (int k0 = 0; k0 < rr; k0 += kc) {
+          const int nk = std::min(kc, rr - k0);
+          struct_scale_kernel<<<blocks_for((long long)t * Rx * nk), 256, 0, st>>>(t, nk * Rx, Rx, ss->Cx[l],
+                                                                                   dl[l] + (size_t)k0 * Rx, Wc);
+          FC_CHECK_LAUNCH();
+          GemmArgs g;
+          g.nbatch = 1;
+          g.rep = nk;
+          g.b[0] = GemmBatch{ql, Rx, t, YR + (size_t)k0 * ql * t, ql, Wc, t, Cb, ql, nullptr, 0, nullptr};
+          g.b[0].sA = (long long)ql * t;
+          g.b[0].sB = (long long)t * Rx;
+          g.b[0].sC = (long long)ql * Rx;
+          gemm(g, st);
+          row_sumsq_kernel<<<dim3(cdiv(ql, 128), std::min(cdiv(nk * Rx, 256), 512)), 128, 0, st>>>(ql, nk * Rx, Cb,
+                                                                                                  s2r);
+          FC_CHECK_LAUNCH();
+        }
+      }
+      rank_cut_device(ql, s2r, 0.25 * eps * eps, energy, rl + l, margins + l, st);
+    }
+    int r_gram[3] = {r[0], r[1], r[2]};
+    FC_CUDA_TRY(cudaMemcpyAsync(r, rl, 3 * sizeof(int), cudaMemcpyDeviceToHost, st));
+    FC_CUDA_TRY(cudaMemcpyAsync(hm, margins, 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
+    FC_CUDA_TRY(cudaStreamSynchronize(st));
+    S.refined = true;
+    if (getenv("FC_TRACE"))
+      fprintf(stderr, "[fc trunc] refined cut: modes (%d,%d,%d) gram r=(%d,%d,%d) -> r=(%d,%d,%d) thr/lam0=(%.2e,%.2e,%.2e)\n",
+              refine[0], refine[1], refine[2], r_gram[0], r_gram[1], r_gram[2], r[0], r[1], r[2],
+              0.25 * eps * eps * S.energy / lam0[0], 0.25 * eps * eps * S.energy / lam0[1],
+              0.25 * eps * eps * S.energy / lam0[2]);
+  }
   for (int l = 0; l < 3; ++l) {
     S.tucker[l] = r[l];
     S.min_margin = std::min(S.min_margin, hm[l]);
@@ -873,6 +964,10 @@ TT truncate_tt(fc_ctx c, const TT& xin, double eps, int rank_cap, TruncStats* st
   }
   // ---- 6. core beta = x x_l Z_l^T (r0 x r1 x r2) ---------------------------------------------
   const size_t r12 = (size_t)r[0] * r[1];
+  // reading A22: the Tucker stage is run while r1 r2 r3 <= 2^28 (2 GB), else CAPACITY
+  require(r12 * r[2] <= ((size_t)1 << 28), FC_ERR_CAPACITY,
+          "Tucker core of " + std::to_string(r[0]) + " x " + std::to_string(r[1]) + " x " + std::to_string(r[2]) +
+              " above 2^28 entries (A22)");
   double* core = s.zeros<double>(r12 * r[2]);
   if (ss) {
     // Tucker route: beta = sum_kk wF[kk] core_x x_1 H1_kk x_2 H2_kk x_3 H3_kk,

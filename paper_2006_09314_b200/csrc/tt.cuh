@@ -63,6 +63,7 @@ struct TruncStats {
   int basis[3] = {0, 0, 0};
   int in_rank = 0, out_rank = 0, t2c_mode = 0;
   double energy = 0.0, min_margin = 1e300;
+  bool refined = false;   // a noise-limited cut was decided from data-based tails (A11')
 };
 
 // RHOSVD -> core -> T2C (S11-S13).  Output: orthonormal Q (n x r_l), orthogonal CP terms.

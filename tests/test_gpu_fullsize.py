@@ -45,12 +45,14 @@ def test_fullsize_solve_properties(lib, name, n, max_iters):
     assert rc == 0 and rep["converged"]
     assert rep["iters"] <= max_iters
     assert rep["rel_res"][-1] <= p.tol_stop
-    # true residual through the public API: F(u) by the fused apply+truncate at 1e-10 (the
-    # untruncated product has r_F * rank(u) terms, ~1e6 at C3), r = b - F(u), truncated at 1e-10
+    # true residual through the public API: F(u) by the fused apply+truncate at et (the
+    # untruncated product has r_F * rank(u) terms, ~1e6 at C3), r = b - F(u), truncated at et
     # to an orthogonal CP so that ||r||^2 = sum w^2 without cancellation; both truncations move
-    # ||r|| by <= ~1e-10 ||b||, far below the bound
-    Fu, _ = ctx.fracop_apply_truncate(FC_F, u, 1e-10)
-    r, _ = ctx.cp_truncate(ctx.cp_axpy(b, -1.0, Fu), 1e-10)
+    # ||r|| by <= ~et ||b|| with et = min(1e-7, tol_stop / 100), two orders below the residual
+    # (a tighter et makes r's truncation keep rank ~n: the energy it is relative to is ~||b||^2)
+    et = min(1e-7, p.tol_stop / 100)
+    Fu, _ = ctx.fracop_apply_truncate(FC_F, u, et)
+    r, _ = ctx.cp_truncate(ctx.cp_axpy(b, -1.0, Fu), et)
     rw = r.w[:r.rank].cpu().numpy()
     true_rel = math.sqrt(float(np.sum(rw ** 2)) / ctx.cp_dot(b, b))
     kappa = kappa_F(ctx, p)

@@ -60,7 +60,7 @@ def test_state_lazy_build_independent(lib):
 
 def test_state_fullsize(lib):
     """C4, n = 1024: the state of the solved control, y = A^-alpha u (state_recover, fused
-    apply -> truncate at 1e-10), equals the untruncated apply of the lambda^-alpha CP to the
+    apply -> truncate at 1e-8), equals the untruncated apply of the lambda^-alpha CP to the
     truncation accuracy (measured with the cancellation floor of cp_dot, ~1e-6).  A check of
     b - y - beta A^alpha u against b - F(u) is NOT used: the eps_D spectral CPs are Frobenius-
     accurate, and on the lowest frequencies (where a smooth u lives) lambda^alpha's CP is off by up
@@ -72,9 +72,9 @@ def test_state_fullsize(lib):
     ctx.sl_setup(p.n, p.a_mid, prm)
     u, rep, rc = ctx.pcg_solve(DeviceCP.from_numpy(p.b_w, p.b_U), prm)
     assert rc == 0
-    y, info = ctx.state_recover(u, 1e-10)
+    y, info = ctx.state_recover(u, 1e-8)
     yu = ctx.fracop_apply(FC_POW_MINUS, u)
     d = ctx.cp_axpy(y, -1.0, yu)
     rel = math.sqrt(max(ctx.cp_dot(d, d), 0.0) / ctx.cp_dot(yu, yu))
     print(f"C4 n=1024 state: rank {y.rank} (untruncated {yu.rank}), ||y - A^-a u|| / ||A^-a u|| = {rel:.2e}")
-    assert rel <= 1e-6
+    assert rel <= 2e-8

@@ -1,3 +1,5 @@
 mkdir -p gpurun_out
-FC_PRECISE_GRAM=1 FC_POOL_RESERVE_MB=60000 timeout 1500 python tools/eps_sweep.py > gpurun_out/eps_sweep_precise.jsonl 2>&1
-cat gpurun_out/eps_sweep_precise.jsonl | tail -4
+timeout 1500 python -m pytest tests/test_gpu_fullsize.py tests/test_gpu_caseA.py tests/test_gpu_state.py -q -s --tb=short > gpurun_out/pytest_gpu.log 2>&1
+tail -1 gpurun_out/pytest_gpu.log
+timeout 1200 python tools/eps_sweep.py > gpurun_out/eps_sweep.jsonl 2>&1
+cat gpurun_out/eps_sweep.jsonl | tail -4
