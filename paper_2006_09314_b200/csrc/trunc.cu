@@ -76,21 +76,6 @@ __global__ void struct_scale_kernel(int t, int R, int Rx, const double* __restri
   }
 }
 
-// s2[i] += sum_j C[i, j]^2 over this block's column range (rows x cols, ld rows): threads over
-// rows (coalesced), blocks over column ranges, atomic accumulation of the partial sums
-__global__ void row_sumsq_kernel(int rows, int cols, const double* __restrict__ C, double* s2) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= rows) return;
-  const int per = (cols + gridDim.y - 1) / gridDim.y;
-  const int j0 = blockIdx.y * per, j1 = min(cols, j0 + per);
-  double acc = 0.0;
-  for (int j = j0; j < j1; ++j) {
-    const double v = C[i + (size_t)j * rows];
-    acc = fma(v, v, acc);
-  }
-  atomicAdd(s2 + i, acc);
-}
-
 // out[:, c] = in[:, c] * d[c]   (rows x cols, ld rows)
 __global__ void scale_cols_kernel(int rows, int cols, const double* __restrict__ in, const double* __restrict__ d,
                                   double* out) {
@@ -867,10 +852,10 @@ TT truncate_tt(fc_ctx c, const TT& xin, double eps, int rank_cap, TruncStats* st
   FC_CUDA_TRY(cudaStreamSynchronize(st));
   // Noise-limited cuts (small eps, large bases): the Gram's eigenvalues carry ~eps_mach lam_max
   // each as rounding noise, so when the threshold (eps/2)^2 E is below k * kNoise * eps_mach lam_max
-  // the eigenvalue tails cannot decide the cut.  Then all eigenvectors are computed and the tails
-  // are taken from the data instead: s2_i = ||y_i^T B||^2 (B the side matrix in the basis; errors
-  // ~eps_mach ||B|| sigma_i, not eps_mach ||B||^2; the y_i are orthonormal to ~1e-15, and mixing
-  // across the cut leaks only ~(eps_mach ||M||)^2 / lam_r of energy) — reading A11', DESIGN.md.
+  // the eigenvalue tails cannot decide the cut (reading A11').  Then all eigenvectors
+  // are computed; the eigenvalues above the noise level are kept, and the noise subspace Y_ns is
+  // re-diagonalised from the data: G_ns = C C^T with C = Y_ns^T B formed explicitly (its rounding
+  // is ~eps_mach ||C||^2, ~1e-32 of the energy), its eigenpairs replace the noisy ones.
   bool refine[3] = {false, false, false}, any_refine = false;
   for (int l = 0; l < 3; ++l) {
     refine[l] = 0.25 * eps * eps * S.energy < kNoise * q[l] * 2.220446049250313e-16 * lam0[l] && q[l] > 1;
@@ -887,26 +872,39 @@ TT truncate_tt(fc_ctx c, const TT& xin, double eps, int rank_cap, TruncStats* st
     for (int l = 0; l < 3; ++l) {
       if (!refine[l]) continue;
       const int ql = q[l];
-      double* s2r = s.zeros<double>(ql);
+      // split: the p eigenvalues above the noise level are trusted; the noise subspace Y_ns
+      // (ql x m) is re-diagonalised from the data: G_ns = C C^T with C = Y_ns^T B computed
+      // explicitly (rounding ~ eps_mach ||C||^2, i.e. ~1e-32 of the energy instead of 1e-16)
+      std::vector<double> hl(ql);
+      FC_CUDA_TRY(cudaMemcpyAsync(hl.data(), lam[l], (size_t)ql * 8, cudaMemcpyDeviceToHost, st));
+      FC_CUDA_TRY(cudaStreamSynchronize(st));
+      const double noise = kNoise * ql * 2.220446049250313e-16 * lam0[l];
+      int pk = 0;
+      while (pk < ql && hl[pk] > noise) ++pk;
+      const int m = ql - pk;
+      if (m == 0) {
+        rank_cut_device(ql, lam[l], 0.25 * eps * eps, energy, rl + l, margins + l, st);
+        continue;
+      }
+      double* Yns = Y[l] + (size_t)pk * ql;
+      double* G = s.zeros<double>((size_t)m * m);
       if (!sgram_used) {
-        // C = Y^T Bm (ql x R), row sums of squares
-        const size_t chunk = std::max<size_t>(1, ((size_t)1 << 27) / std::max(ql, 1));
-        double* Cb = s.alloc<double>((size_t)ql * std::min<size_t>(chunk, (size_t)R));
+        const size_t chunk = std::max<size_t>(1, ((size_t)1 << 27) / std::max(m, 1));
+        double* Cb = s.alloc<double>((size_t)m * std::min<size_t>(chunk, (size_t)R));
         for (size_t c0 = 0; c0 < (size_t)R; c0 += chunk) {
-          const int m = (int)std::min(chunk, (size_t)R - c0);
-          dgemm(st, 1, 0, ql, m, ql, 1.0, Y[l], ql, Bm[l] + c0 * ql, ql, 0.0, Cb, ql);
-          row_sumsq_kernel<<<dim3(cdiv(ql, 128), std::min(cdiv(m, 256), 512)), 128, 0, st>>>(ql, m, Cb, s2r);
-          FC_CHECK_LAUNCH();
+          const int mc = (int)std::min(chunk, (size_t)R - c0);
+          dgemm(st, 1, 0, m, mc, ql, 1.0, Yns, ql, Bm[l] + c0 * ql, ql, 0.0, Cb, m);
+          dgemm(st, 0, 1, m, m, mc, 1.0, Cb, m, Cb, m, 1.0, G, m);
         }
       } else {
-        // structured: (Y^T Rm_kk) (Cx D_kk) per spectral term kk, chunked
+        // structured: C_kk = (Y_ns^T Rm_kk)(Cx D_kk), spectral terms chunked; G += C C^T per chunk
         const int t = ss->t[l], rr = ss->r, Rx = ss->Rx;
-        double* YR = s.alloc<double>((size_t)ql * t * rr);
-        dgemm(st, 1, 0, ql, t * rr, ql, 1.0, Y[l], ql, RmE[l], ql, 0.0, YR, ql);
+        double* YR = s.alloc<double>((size_t)m * t * rr);
+        dgemm(st, 1, 0, m, t * rr, ql, 1.0, Yns, ql, RmE[l], ql, 0.0, YR, m);
         const int kc = std::max(1, (int)std::min<size_t>((size_t)rr, ((size_t)1 << 26) /
-                                                                   std::max<size_t>((size_t)ql * Rx, 1)));
+                                                                   std::max<size_t>((size_t)std::max(m, t) * Rx, 1)));
         double* Wc = s.alloc<double>((size_t)t * Rx * kc);
-        double* Cb = s.alloc<double>((size_t)ql * Rx * kc);
+        double* Cb = s.alloc<double>((size_t)m * Rx * kc);
         for (int k0 = 0; k0 < rr; k0 += kc) {
           const int nk = std::min(kc, rr - k0);
           struct_scale_kernel<<<blocks_for((long long)t * Rx * nk), 256, 0, st>>>(t, nk * Rx, Rx, ss->Cx[l],
@@ -915,16 +913,31 @@ TT truncate_tt(fc_ctx c, const TT& xin, double eps, int rank_cap, TruncStats* st
           GemmArgs g;
           g.nbatch = 1;
           g.rep = nk;
-          g.b[0] = GemmBatch{ql, Rx, t, YR + (size_t)k0 * ql * t, ql, Wc, t, Cb, ql, nullptr, 0, nullptr};
-          g.b[0].sA = (long long)ql * t;
+          g.b[0] = GemmBatch{m, Rx, t, YR + (size_t)k0 * m * t, m, Wc, t, Cb, m, nullptr, 0, nullptr};
+          g.b[0].sA = (long long)m * t;
           g.b[0].sB = (long long)t * Rx;
-          g.b[0].sC = (long long)ql * Rx;
+          g.b[0].sC = (long long)m * Rx;
           gemm(g, st);
-          row_sumsq_kernel<<<dim3(cdiv(ql, 128), std::min(cdiv(nk * Rx, 256), 512)), 128, 0, st>>>(ql, nk * Rx, Cb,
-                                                                                                  s2r);
-          FC_CHECK_LAUNCH();
+          dgemm(st, 0, 1, m, m, nk * Rx, 1.0, Cb, m, Cb, m, 1.0, G, m);
         }
       }
+      // eigen of G_ns (all vectors): mu descending, V_ns
+      SyevBatch gb;
+      double* mu = s.alloc<double>(m);
+      double* Vn = s.alloc<double>((size_t)m * m);
+      int* rm = s.alloc<int>(1);
+      FC_CUDA_TRY(cudaMemcpyAsync(rm, &m, sizeof(int), cudaMemcpyHostToDevice, st));
+      gb.e[gb.nb++] = SyevEntry{m, G, m, s.alloc<double>(m), s.alloc<double>(m), mu, Vn, m, rm,
+                                s.alloc<double>((size_t)5 * m * m)};
+      syev_values(gb, st);
+      syev_vectors(gb, m, st);
+      // s2 = [trusted eigenvalues ; mu], the noise-subspace vectors rotated: Y_ns <- Y_ns V_ns
+      double* s2r = s.alloc<double>(ql);
+      FC_CUDA_TRY(cudaMemcpyAsync(s2r, lam[l], (size_t)pk * 8, cudaMemcpyDeviceToDevice, st));
+      FC_CUDA_TRY(cudaMemcpyAsync(s2r + pk, mu, (size_t)m * 8, cudaMemcpyDeviceToDevice, st));
+      double* Yr = s.alloc<double>((size_t)ql * m);
+      dgemm(st, 0, 0, ql, m, m, 1.0, Yns, ql, Vn, m, 0.0, Yr, ql);
+      FC_CUDA_TRY(cudaMemcpyAsync(Yns, Yr, (size_t)ql * m * 8, cudaMemcpyDeviceToDevice, st));
       rank_cut_device(ql, s2r, 0.25 * eps * eps, energy, rl + l, margins + l, st);
     }
     int r_gram[3] = {r[0], r[1], r[2]};

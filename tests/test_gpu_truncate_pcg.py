@@ -178,3 +178,23 @@ def check_rank_history(rep, rep_ref):
         assert abs(rep["iters"] - rep_ref["iters"]) <= 1
     else:
         assert rep["iters"] == rep_ref["iters"]
+
+
+@pytest.mark.parametrize("n,R,eps", [(48, 5, 1e-8), (40, 4, 1e-9), (64, 3, 1e-8)])
+def test_truncate_small_eps_refined_cut(lib, n, R, eps):
+    """Cuts below the Gram noise level ((eps/2)^2 E < k eps_mach lam_max), reading A11': the
+    eigenvalues above the noise level are kept, the noise subspace Y_ns is re-diagonalised from
+    the data (Gram of C = Y_ns^T B, rounding ~1e-32 of the energy).  Tucker ranks as the oracle's
+    exact SVD cut (+-1 in the A23 band), result within 2 eps."""
+    from paper_2006_09314_b200.binding import DeviceCP
+    p = make_problem("C1", n=n)
+    ctx = lib.context()
+    st = _shared(ctx, p)
+    w, U = random_cp(n, R, 17)
+    x = cpm.apply(st.V, st.F, cpm.CP(np.linspace(1, 2, R), U))
+    info_o = {}
+    ref = truncate(x, eps, info_o)
+    y, info = ctx.cp_truncate(DeviceCP.from_numpy(x.w, x.U), eps)
+    for l in range(3):
+        assert abs(info.tucker_rank[l] - info_o["tucker_rank"][l]) <= 1
+    assert reldiff(_cp(y), ref) <= 2 * eps
