@@ -251,6 +251,16 @@ struct XJob {
   bool joined = false;
   XJob(fc_ctx c_, cudaStream_t st_, const TT& X, const TT& P, double a, double eps, int cap) : c(c_), st(st_) {
     XP = tt_axpy(st, X, a, P);
+    static const bool inline_x = getenv("FC_NO_OVERLAP") != nullptr;   // diagnostics: no side stream
+    if (inline_x) {
+      try {
+        out = truncate_tt(c, XP, eps, cap, &stats);
+      } catch (...) {
+        err = std::current_exception();
+      }
+      joined = true;
+      return;
+    }
     cudaEvent_t ev;
     FC_CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
     FC_CUDA_TRY(cudaEventRecord(ev, st));
