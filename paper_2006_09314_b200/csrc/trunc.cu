@@ -325,6 +325,218 @@ __global__ void __launch_bounds__(512) slice_svd_kernel(int ra, int rb, const do
   for (int m = tid; m < k; m += nt) s_out[(size_t)nu * k + m] = nrm[order[m]];
 }
 
+// T2C slice SVD with QR preconditioning (Drmac-Veselic): A P = Q R by Householder QR with column
+// pivoting, then one-sided Jacobi on the columns of R^T (graded, nearly diagonal: a few sweeps
+// instead of ~16 on the slice itself).  R^T W = U' Sigma gives A = (Q W) Sigma (P U')^T: the tall-
+// side vectors are Q W (reflectors applied to W), the short-side vectors P U'.  Same outputs and
+// convergence test as slice_svd_kernel; shared memory: rows*cols + 2 cols^2 + 3 cols doubles.
+size_t slice_qrj_smem(int rows, int cols) {
+  return ((size_t)rows * cols + 2 * (size_t)cols * cols + 3 * (size_t)cols) * 8 + (size_t)cols * 8 + 64;
+}
+
+__global__ void __launch_bounds__(512) slice_svd_qrj_kernel(int ra, int rb, const double* __restrict__ S,
+                                                            double* s_out, double* Ua, double* Vb) {
+  extern __shared__ double sm[];
+  const int nu = blockIdx.x;
+  const bool tr = ra < rb;
+  const int rows = tr ? rb : ra, cols = tr ? ra : rb, k = cols;
+  double* A = sm;                                   // rows x cols: R above, reflectors below
+  double* X = A + (size_t)rows * cols;              // cols x cols: R^T, rotated by Jacobi
+  double* W = X + (size_t)cols * cols;              // cols x cols rotations
+  double* cn = W + (size_t)cols * cols;             // cols: column norms^2 / singular values
+  double* tau = cn + cols;                          // cols
+  double* red = tau + cols;                         // cols (reduction scratch)
+  int* perm = (int*)(red + cols);                   // cols
+  int* order = perm + cols;                         // cols
+  __shared__ int piv_s;
+  __shared__ double sval;
+  __shared__ int changed;
+  const double* src = S + (size_t)nu * ra * rb;
+  const int tid = threadIdx.x, nt = blockDim.x, warp = tid >> 5, ln = tid & 31, nw = nt >> 5;
+  for (int idx = tid; idx < rows * cols; idx += nt) {
+    const int i = idx % rows, j = idx / rows;
+    A[idx] = tr ? src[j + (size_t)i * ra] : src[i + (size_t)j * ra];
+  }
+  for (int j = tid; j < cols; j += nt) perm[j] = j;
+  __syncthreads();
+  double fro2 = 0.0;
+  // ---- Householder QR with column pivoting ----
+  for (int i = 0; i < cols; ++i) {
+    // trailing column norms (exact each step), pivot = largest (lowest index on ties)
+    for (int j = i + warp; j < cols; j += nw) {
+      const double* a = A + (size_t)j * rows;
+      double s2 = 0.0;
+      for (int t = i + ln; t < rows; t += 32) s2 = fma(a[t], a[t], s2);
+      for (int o = 16; o > 0; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+      if (ln == 0) cn[j] = s2;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      int pj = i;
+      for (int j = i + 1; j < cols; ++j)
+        if (cn[j] > cn[pj]) pj = j;
+      piv_s = pj;
+      if (i == 0) {
+        double f = 0.0;
+        for (int j = 0; j < cols; ++j) f += cn[j];
+        sval = f;
+      }
+    }
+    __syncthreads();
+    if (i == 0) fro2 = sval;
+    const int pj = piv_s;
+    if (pj != i) {
+      for (int t = tid; t < rows; t += nt) {
+        const double x = A[t + (size_t)i * rows];
+        A[t + (size_t)i * rows] = A[t + (size_t)pj * rows];
+        A[t + (size_t)pj * rows] = x;
+      }
+      if (tid == 0) {
+        const int q = perm[i]; perm[i] = perm[pj]; perm[pj] = q;
+        const double c = cn[i]; cn[i] = cn[pj]; cn[pj] = c;
+      }
+      __syncthreads();
+    }
+    // reflector for column i (rows i..): v = x - alpha e1, stored normalised with v0 = 1
+    double* ai = A + (size_t)i * rows;
+    const double x0 = ai[i];
+    const double sig = cn[i] - x0 * x0;          // sum of squares below the diagonal
+    double alpha = x0, tv = 0.0;
+    if (sig > 0.0 || x0 < 0.0) {
+      const double nrm = sqrt(fmax(cn[i], 0.0));
+      alpha = -copysign(nrm, x0);
+      const double v0 = x0 - alpha;
+      tv = (alpha - x0) / alpha;                  // tau = (alpha - x0) / alpha, v scaled by 1/v0
+      const double inv = 1.0 / v0;
+      for (int t = i + 1 + tid; t < rows; t += nt) ai[t] *= inv;
+    }
+    __syncthreads();
+    // apply H = I - tau v v^T to the trailing columns (warp per column)
+    if (tv != 0.0)
+      for (int j = i + 1 + warp; j < cols; j += nw) {
+        double* a = A + (size_t)j * rows;
+        double d = (ln == 0) ? a[i] : 0.0;
+        for (int t = i + 1 + ln; t < rows; t += 32) d = fma(ai[t], a[t], d);
+        for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+        const double f = tv * d;
+        if (ln == 0) a[i] -= f;
+        for (int t = i + 1 + ln; t < rows; t += 32) a[t] -= f * ai[t];
+      }
+    if (tid == 0) {
+      tau[i] = tv;
+      red[i] = alpha;                            // R[i, i]
+    }
+    __syncthreads();
+  }
+  // X = R^T (cols x cols, lower triangular), W = I
+  for (int idx = tid; idx < cols * cols; idx += nt) {
+    const int r = idx % cols, c = idx / cols;    // X[r, c] = R[c, r]
+    X[idx] = (r > c) ? A[c + (size_t)r * rows] : (r == c ? red[r] : 0.0);
+    W[idx] = (r == c) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  // ---- one-sided Jacobi on the columns of X ----
+  const double neg2 = 1e-24 * fro2;
+  const int p = cols + (cols & 1);
+  const double tol = 2.0 * sqrt((double)cols) * 2.220446049250313e-16, tol2 = tol * tol;
+  int G = 32;
+  while (G > 4 && nt / G < p / 2) G >>= 1;
+  const int gid = tid / G, gl = tid % G, ng = nt / G;
+  for (int sweep = 0; sweep < 40; ++sweep) {
+    if (tid == 0) changed = 0;
+    __syncthreads();
+    for (int rd = 0; rd < p - 1; ++rd) {
+      for (int pi0 = 0; pi0 < p / 2; pi0 += ng) {
+        const int pi = pi0 + gid;
+        int a = 0, b = 0;
+        bool act = pi < p / 2;
+        if (act) {
+          if (pi == 0) { a = rd % (p - 1); b = p - 1; }
+          else { a = (rd + pi) % (p - 1); b = (rd - pi + p - 1) % (p - 1); }
+          if (a > b) { int t = a; a = b; b = t; }
+          act = b < cols;
+        }
+        double al = 0, be = 0, ga = 0;
+        if (act)
+          for (int i = gl; i < cols; i += G) {
+            const double x = X[i + a * cols], y = X[i + b * cols];
+            al = fma(x, x, al); be = fma(y, y, be); ga = fma(x, y, ga);
+          }
+        for (int o = G >> 1; o > 0; o >>= 1) {
+          al += __shfl_xor_sync(0xffffffffu, al, o);
+          be += __shfl_xor_sync(0xffffffffu, be, o);
+          ga += __shfl_xor_sync(0xffffffffu, ga, o);
+        }
+        if (!act || ga == 0.0 || ga * ga <= tol2 * (al * be) || al <= neg2 || be <= neg2) continue;
+        const double dd = be - al, g2 = 2.0 * ga;
+        const double t = copysign(1.0, dd) * g2 / (fabs(dd) + sqrt(fma(dd, dd, g2 * g2)));
+        const double c = rsqrt(fma(t, t, 1.0)), sn = c * t;
+        for (int i = gl; i < cols; i += G) {
+          double x = X[i + a * cols], y = X[i + b * cols];
+          X[i + a * cols] = c * x - sn * y;
+          X[i + b * cols] = sn * x + c * y;
+          x = W[i + a * cols];
+          y = W[i + b * cols];
+          W[i + a * cols] = c * x - sn * y;
+          W[i + b * cols] = sn * x + c * y;
+        }
+        if (gl == 0) changed = 1;
+      }
+      __syncthreads();
+    }
+    if (!changed) {
+      if (tid == 0) atomicMax(&g_slice_sweeps_max, sweep + 1);
+      break;
+    }
+    __syncthreads();
+  }
+  // singular values, order
+  for (int j = warp; j < cols; j += nw) {
+    double s2 = 0;
+    for (int i = ln; i < cols; i += 32) s2 = fma(X[i + j * cols], X[i + j * cols], s2);
+    for (int o = 16; o > 0; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+    if (ln == 0) cn[j] = sqrt(s2);
+  }
+  __syncthreads();
+  for (int j = tid; j < cols; j += nt) {
+    int rk = 0;
+    for (int i = 0; i < cols; ++i) rk += (cn[i] > cn[j]) || (cn[i] == cn[j] && i < j);
+    order[rk] = j;
+  }
+  __syncthreads();
+  // tall-side vectors: Q w_j = H_0 (H_1 ... (H_{c-1} [w_j; 0])), warp per vector, in place in a
+  // rows-length scratch: reuse X's column?  No: build in global output directly (warp-private)
+  for (int m = warp; m < k; m += nw) {
+    const int j = order[m];
+    double* out = tr ? (Vb + (size_t)nu * rb * k + (size_t)m * rb) : (Ua + (size_t)nu * ra * k + (size_t)m * ra);
+    for (int t = ln; t < rows; t += 32) out[t] = t < cols ? W[t + (size_t)j * cols] : 0.0;
+    __syncwarp();
+    for (int i = cols - 1; i >= 0; --i) {
+      const double tv = tau[i];
+      if (tv == 0.0) continue;
+      const double* v = A + (size_t)i * rows;   // v_i[i] = 1, v_i[t] = A[t, i] for t > i
+      double d = (ln == 0) ? out[i] : 0.0;
+      for (int t = i + 1 + ln; t < rows; t += 32) d = fma(v[t], out[t], d);
+      for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+      const double f = tv * d;
+      __syncwarp();
+      if (ln == 0) out[i] -= f;
+      for (int t = i + 1 + ln; t < rows; t += 32) out[t] -= f * v[t];
+      __syncwarp();
+    }
+  }
+  // short-side vectors: P u'_j (u'_j = x_j / sigma_j), row perm[i] <- entry i
+  for (int idx = tid; idx < k * cols; idx += nt) {
+    const int m = idx / cols, i = idx % cols;
+    const int j = order[m];
+    const double sj = cn[j];
+    const double v = sj > 0 ? X[i + (size_t)j * cols] / sj : 0.0;
+    if (tr) Ua[(size_t)nu * ra * k + (size_t)m * ra + perm[i]] = v;
+    else Vb[(size_t)nu * rb * k + (size_t)m * rb + perm[i]] = v;
+  }
+  for (int m = tid; m < k; m += nt) s_out[(size_t)nu * k + m] = cn[order[m]];
+}
+
 // pool all (s, nu, m), sort by s desc, ties (nu, m) asc: rank of each element by counting
 // (thread per element, candidates staged through shared-memory tiles); s2 sorted and keys
 __global__ void __launch_bounds__(256) pool_rank_kernel(int K, const double* __restrict__ s, double* s2_sorted,
@@ -499,8 +711,21 @@ TT tucker_to_canonical(fc_ctx c, const double* core, const int r[3], double* con
                                      (int)kSliceSmem));
     attr = true;
   }
-  if (gws) slice_svd_kernel<false><<<rc, 512, smem, st>>>(ra, rb, S, sv, Ua, Vb, gws);
-  else slice_svd_kernel<true><<<rc, 512, smem, st>>>(ra, rb, S, sv, Ua, Vb, nullptr);
+  static const bool no_qr = getenv("FC_SLICE_NO_QR") != nullptr;
+  const size_t qsm = slice_qrj_smem(rows, cols);
+  if (!no_qr && qsm <= kSliceSmem) {
+    static bool qattr = false;
+    if (!qattr) {
+      FC_CUDA_TRY(cudaFuncSetAttribute(slice_svd_qrj_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)kSliceSmem));
+      qattr = true;
+    }
+    slice_svd_qrj_kernel<<<rc, 512, qsm, st>>>(ra, rb, S, sv, Ua, Vb);
+  } else if (gws) {
+    slice_svd_kernel<false><<<rc, 512, smem, st>>>(ra, rb, S, sv, Ua, Vb, gws);
+  } else {
+    slice_svd_kernel<true><<<rc, 512, smem, st>>>(ra, rb, S, sv, Ua, Vb, nullptr);
+  }
   FC_CHECK_LAUNCH();
   if (getenv("FC_TRACE")) {
     int sw = 0, zero = 0;
