@@ -1294,12 +1294,116 @@ __global__ void __launch_bounds__(kBcgsClusterThreads, 1)
   cl.sync();                                                 // smem stays alive for readers
 }
 
+// Polar (Newton-Schulz) re-orthonormalisation of the na block vectors held row-distributed in
+// S.Yb (rows [0, RB) of this CTA): G = Yb^T Yb all-reduced through DSMEM (reduce-scatter of the
+// partials in rank order, then all-gather: every CTA holds the same G), D = diag(G)^-1/2 and
+// Yb <- Yb D (3I - D G D) / 2.  The error e = max|D G D - I| squares per step (0.75 e^2): one
+// step when e < 1e-8 (the usual case: two in-block passes plus the second projection leave
+// e ~ 1e-13), up to 4 otherwise.  Replaces na sequential MGS steps (one cluster barrier each) by
+// one Gram all-reduce; the order of the vectors inside the block is irrelevant to the basis
+// (coefficients are formed as Q^T K afterwards).  Shared scratch: S.X (partials, then H; and the
+// reduced Gram), which needs LD * W >= 2 W^2.
+template <int CS, int W, int RBM>
+__device__ void bcgs_polar(cooperative_groups::cluster_group& cl, BcgsClusterSmem<W, RBM>& S, int na, int RB) {
+  constexpr int LD = BcgsClusterSmem<W, RBM>::LD;
+  constexpr int G = kBcgsClusterThreads / RBM, CPG = W / G;   // apply: column groups x columns
+  static_assert(LD >= 2 * W && kBcgsClusterThreads % RBM == 0 && W % G == 0, "polar layout");
+  double* P = S.X;
+  double* R = S.X + W * W;
+  const int tid = threadIdx.x, warp = tid >> 5, ln = tid & 31, NW = blockDim.x >> 5, nt = blockDim.x;
+  const int cnt = na * na, ch = (cnt + CS - 1) / CS, r = (int)cl.block_rank(), nt4 = (na + 3) / 4;
+  for (int it = 0; it < 4; ++it) {
+    // partial Gram over this CTA's rows: 4 x 4 upper tiles per warp, lanes over rows
+    for (int t = warp; t < nt4 * nt4; t += NW) {
+      const int ta = t / nt4, tb = t % nt4;
+      if (ta > tb) continue;
+      double acc[4][4] = {};
+      for (int i = ln; i < RB; i += 32) {
+        double ya[4], yb[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          ya[q] = 4 * ta + q < na ? S.Yb[i + (size_t)(4 * ta + q) * LD] : 0.0;
+          yb[q] = 4 * tb + q < na ? S.Yb[i + (size_t)(4 * tb + q) * LD] : 0.0;
+        }
+#pragma unroll
+        for (int p = 0; p < 4; ++p)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) acc[p][q] = fma(ya[p], yb[q], acc[p][q]);
+      }
+#pragma unroll
+      for (int p = 0; p < 4; ++p)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          double v = acc[p][q];
+          for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+          const int a = 4 * ta + p, b = 4 * tb + q;
+          if (ln == 0 && a < na && b < na) {
+            P[a * na + b] = v;
+            P[b * na + a] = v;
+          }
+        }
+    }
+    cl.sync();
+    for (int e = r * ch + tid; e < min(cnt, (r + 1) * ch); e += nt) {   // reduce own chunk
+      double v = 0.0;
+      for (int s = 0; s < CS; ++s) v += cl.map_shared_rank(P, s)[e];
+      R[e] = v;
+    }
+    cl.sync();
+    for (int e = tid; e < cnt; e += nt) {                               // gather the others
+      const int own = e / ch;
+      if (own != r) R[e] = cl.map_shared_rank(R, own)[e];
+    }
+    __syncthreads();
+    for (int a = tid; a < na; a += nt) {
+      const double g = R[a * na + a];
+      S.coef[a] = g > 0.0 ? 1.0 / sqrt(g) : 0.0;
+    }
+    __syncthreads();
+    double err = 0.0;
+    for (int e = tid; e < cnt; e += nt) {
+      const int a = e / na, b = e % na;
+      const double gt = S.coef[a] * R[e] * S.coef[b];
+      err = fmax(err, fabs(gt - (a == b ? 1.0 : 0.0)));
+      P[e] = S.coef[a] * ((a == b ? 1.5 : 0.0) - 0.5 * gt);         // H = D (3I - DGD) / 2
+    }
+    for (int o = 16; o > 0; o >>= 1) err = fmax(err, __shfl_xor_sync(0xffffffffu, err, o));
+    if (ln == 0) S.red[warp] = err;
+    __syncthreads();
+    err = 0.0;
+    for (int w = 0; w < NW; ++w) err = fmax(err, S.red[w]);
+    if (it > 0 && err < 1e-13) break;                                   // uniform: same G everywhere
+    // Yb <- Yb H: thread = (row i, group of CPG columns); H reads are warp broadcasts
+    const int i = tid % RBM, b0 = (tid / RBM) * CPG;
+    double acc[CPG];
+#pragma unroll
+    for (int q = 0; q < CPG; ++q) acc[q] = 0.0;
+    if (i < RB && b0 < na)
+      for (int a = 0; a < na; ++a) {
+        const double y = S.Yb[i + (size_t)a * LD];
+        const double* h = P + a * na + b0;
+#pragma unroll
+        for (int q = 0; q < CPG; ++q)
+          if (b0 + q < na) acc[q] = fma(y, h[q], acc[q]);
+      }
+    __syncthreads();
+    if (i < RB)
+#pragma unroll
+      for (int q = 0; q < CPG; ++q)
+        if (b0 + q < na) S.Yb[i + (size_t)(b0 + q) * LD] = acc[q];
+    __syncthreads();
+    if (err < 1e-8) break;
+  }
+  cl.sync();                                                            // others may still gather R
+}
+
 // BCGS2 second pass, in-block part, on the cluster: Y[:, :nacc] (re-projected against Q) are
-// re-orthonormalised among themselves (one MGS pass, dots and norm in one all-reduce) and
-// appended to Q at k.
+// re-orthonormalised among themselves and appended to Q at k: polar step above (default), or
+// one MGS pass with dots and norm in one all-reduce (FC_BCGS_MGS_FINAL, or layouts without the
+// polar scratch).
 template <int CS, int W, int RBM>
 __global__ void __launch_bounds__(kBcgsClusterThreads, 1)
-    bcgs_finalize_cluster_kernel(const __grid_constant__ BcgsBatch B, int j0) {
+    bcgs_finalize_cluster_kernel(const __grid_constant__ BcgsBatch B, int j0, int mgs) {
   namespace cg = cooperative_groups;
   extern __shared__ __align__(16) unsigned char smraw[];
   using Smem = BcgsClusterSmem<W, RBM>;
@@ -1317,6 +1421,17 @@ __global__ void __launch_bounds__(kBcgsClusterThreads, 1)
     S.Yb[i + (size_t)c * LD] = i < nr ? E.Y[(size_t)(r0 + i) + (size_t)c * n] : 0.0;
   }
   __syncthreads();
+  if constexpr (RBM + 4 >= 2 * W) if (!mgs) {
+    bcgs_polar<CS, W, RBM>(cl, S, na, RB);
+    for (int idx = tid; idx < nr * na; idx += nt) {
+      const int i = idx % nr, c = idx / nr;
+      const double v = S.Yb[i + (size_t)c * LD];
+      E.Y[(size_t)(r0 + i) + (size_t)c * n] = v;
+      E.Q[(size_t)(r0 + i) + (size_t)(k0 + c) * E.ldq] = v;
+    }
+    if (r == 0 && tid == 0) *E.k = k0 + na;
+    return;
+  }
   for (int c = 0; c < na; ++c) {
     double* y = S.Yb + (size_t)c * LD;
     double* part = S.part[c & 1];
@@ -1594,8 +1709,9 @@ void bcgs_cluster_block(const BcgsBatch& bb, int j0, cudaStream_t st) {
 template <int CS, int W, int RB>
 void bcgs_cluster_finalize(const BcgsBatch& bb, int j0, cudaStream_t st) {
   bcgs_cluster_setup<CS, W, RB>();
-  launch_cluster(bcgs_finalize_cluster_kernel<CS, W, RB>, CS, bb.nb, sizeof(BcgsClusterSmem<W, RB>), st, bb, j0, 0,
-                 false);
+  static const int mgs = getenv("FC_BCGS_MGS_FINAL") != nullptr;   // diagnostic: sequential MGS
+  launch_cluster(bcgs_finalize_cluster_kernel<CS, W, RB>, CS, bb.nb, sizeof(BcgsClusterSmem<W, RB>), st, bb, j0, mgs,
+                 true);
 }
 
 // split-K for the two skinny GEMMs of a block projection, P = Q^T A_blk (k x W x n) and

@@ -1,9 +1,5 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_truncate_pcg.py tests/test_gpu_caseA.py -q --tb=short -x > gpurun_out/pytest_gpu.log 2>&1
-tail -1 gpurun_out/pytest_gpu.log
-FC_TRACE=1 python tools/one_solve.py > gpurun_out/trace.log 2>&1
-grep "fc t2c" gpurun_out/trace.log | sort | uniq -c | sort -rn | head -4
-timeout 600 python bench.py --steps 5 --no-cpu-baseline > gpurun_out/bench.jsonl 2> gpurun_out/bench.err
-python -c "
-import json;d=json.loads(open('gpurun_out/bench.jsonl').read().strip().splitlines()[-1])
-print(round(d['value'],2), d['step_ms'], round(d['e2e']['value'],2), d['iters_per_solve'])"
+timeout 600 python -m pytest tests/test_gpu_truncate_pcg.py tests/test_gpu_caseA.py -x -q -m gpu > gpurun_out/pytest_gpu.log 2>&1 || { tail -30 gpurun_out/pytest_gpu.log; exit 1; }
+tail -2 gpurun_out/pytest_gpu.log
+for i in 1 2; do timeout 300 python bench.py --steps 5 --warmup 3 2>gpurun_out/bench.err | tee -a gpurun_out/bench.jsonl | python -c "import json,sys; d=json.loads(sys.stdin.readline()); print(d['value'], d['ms_per_step'], d['e2e']['value'], d['roofline']['frac'])"; done
+FC_BCGS_MGS_FINAL=1 timeout 300 python bench.py --steps 5 --warmup 3 2>>gpurun_out/bench.err | python -c "import json,sys; d=json.loads(sys.stdin.readline()); print('mgs', d['value'], d['ms_per_step'])"
