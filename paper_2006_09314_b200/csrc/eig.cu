@@ -10,6 +10,7 @@
 //     iteration for the leading r vectors, CGS2 re-orthonormalisation, back-transformation.
 #include <cfloat>
 #include <cstdlib>
+#include <cstdio>
 #include <cooperative_groups.h>
 #include "eig.cuh"
 
@@ -1105,16 +1106,27 @@ __global__ void __launch_bounds__(1024) bcgs_finalize_kernel(const __grid_consta
 // ---- cluster versions of the two in-block steps --------------------------------------------
 // CTA r of a CS-CTA cluster owns rows [r RB, (r+1) RB) of the n x W block (RB = n / CS <= 128)
 // and keeps them in shared memory: the block X and the accepted unit vectors Yb (leading
-// dimension RB + 4: conflict-free row-parallel access).  Every dot product and norm is a partial
-// over the CTA's rows, all-reduced through DSMEM in a fixed order (the same value in every CTA,
-// so the accept decisions agree).
-//   in-block step: one all-reduce of all block column norms first (columns already below the
-//   threshold after the GEMM projection cannot be accepted later: skipped); then per remaining
-//   column: pass 1 (dots, all-reduce, update), pass 2 fused with the norm (dots and ||x'||^2 in
-//   one all-reduce, ||x''||^2 = ||x'||^2 - ||c2||^2: c2 = O(eps ||x||) after pass 1, far below
-//   the tau ||x|| decision level) -> at most 2 cluster barriers per column;
-//   finalisation: dots with the earlier block vectors and the norm in one all-reduce (1 barrier).
+// dimension RB + 4: conflict-free row-parallel access).  Every dot product, norm and Gram entry
+// is a partial over the CTA's rows, all-reduced through DSMEM in a fixed order (the same value in
+// every CTA, so every accept decision agrees).
+//   in-block step (default): the block Gram G = X^T X in one cluster reduction; a replicated
+//   in-order Cholesky of G accepts the columns that are clearly independent of the earlier
+//   accepted ones (Schur residual s_c > max(theta^2 G_cc, 1.01 lim^2), theta = 1e-4: s_c is
+//   accurate to ~m eps G_cc, i.e. to 1e-6 relative at the theta level, so the decision is safe),
+//   rejects those with theta^2 G_cc < s_c < 0.99 lim^2 (below lim against a subset of the final
+//   basis already) and defers the rest; the accepted columns are orthonormalised by CholQR (Y = X L^-T) followed
+//   by the polar step (= CholQR2; a block whose CholQR orthogonality loss exceeds 1e-4 is redone
+//   on the per-column path; below it the span error eps kappa ~ 1e-10 is far under the
+//   truncation tolerances); the deferred
+//   columns (about 10 % of those alive in the C4 solve) go through the exact per-column path:
+//   pass 1 (dots, all-reduce, update), pass 2 fused with the norm (dots and ||x'||^2 in one
+//   all-reduce, ||x''||^2 = ||x'||^2 - ||c2||^2: c2 = O(eps ||x||) after pass 1, far below the
+//   tau ||x|| decision level) -> 2 cluster barriers per deferred column.  FC_BCGS_SEQ: every
+//   alive column through the per-column path (the previous design).
+//   finalisation: polar step on the re-projected block (one Gram all-reduce).
 constexpr int kBcgsClusterThreads = 512;
+constexpr double kBcgsTheta2 = 1e-8;    // theta^2: clear-acceptance level of the Gram Cholesky
+constexpr double kBcgsCholFail = 1e-4;  // orthogonality loss above which bcgs_polar takes a Cholesky step
 
 // cluster configurations: (CS CTAs, block width W, rows per CTA RB), n <= CS * RB; see bcgs()
 template <int W, int RB>
@@ -1122,11 +1134,20 @@ struct BcgsClusterSmem {
   static constexpr int LD = RB + 4;   // conflict-free row-parallel access
   double X[LD * W];
   double Yb[LD * W];
+  double gram[2 * W * W];         // Gram partials (read remotely) / Cholesky factor / H; reduced Gram
   double part[2][W + 2];          // partial dots (+ norm), double-buffered (read remotely)
   double coef[W + 2];
   double red[kBcgsClusterThreads / 32];
+  double pn2[W];                  // squared column norms after the GEMM projection
   int alive[W];
+  int cidx[W], uidx[W];           // Cholesky-accepted / deferred columns
 };
+
+// diagnostics (FC_TRACE): in-block residual ratios ||x''|| / ||x_proj|| of the columns that pass
+// the pre-filter, by decade (bin d: ratio in [10^-(d+1), 10^-d)), [18] pre-filtered, [19] blocks,
+// [20] deferred by the Gram Cholesky, [22] rejected by it, [21] blocks redone on the per-column
+// path
+__device__ unsigned long long g_bcgs_hist[23];
 
 // all-reduce of buf[0..cnt) (per-CTA partials, read remotely) into out[0..cnt); every CTA sums
 // the CS partials in rank order (shuffle tree over groups of CS lanes)
@@ -1201,9 +1222,224 @@ __device__ __forceinline__ void block_update(const double* V, double* x, int nr,
   }
 }
 
+// G = M^T M for the m columns of M (this CTA's rows [0, RB), ld LD) over the whole cluster:
+// 4 x 4 upper tiles per warp with lanes over rows (conflict-free) into the partials S.gram[0..m^2),
+// reduce-scatter in rank order into S.gram[W^2 + .], all-gather of the other CTAs' chunks: on
+// return every CTA holds the identical G (ld m) at S.gram + W^2.  The partials may be reused
+// after return; the reduced copy is read remotely until the next cluster barrier.
+template <int CS, int W, int RBM>
+__device__ void cluster_gram(cooperative_groups::cluster_group& cl, BcgsClusterSmem<W, RBM>& S, const double* M,
+                             int m, int RB) {
+  constexpr int LD = BcgsClusterSmem<W, RBM>::LD;
+  double* P = S.gram;
+  double* R = S.gram + W * W;
+  const int tid = threadIdx.x, warp = tid >> 5, ln = tid & 31, NW = blockDim.x >> 5, nt = blockDim.x;
+  const int cnt = m * m, ch = (cnt + CS - 1) / CS, r = (int)cl.block_rank(), nt4 = (m + 3) / 4;
+  for (int t = warp; t < nt4 * nt4; t += NW) {
+    const int ta = t / nt4, tb = t % nt4;
+    if (ta > tb) continue;
+    double acc[4][4] = {};
+    for (int i = ln; i < RB; i += 32) {
+      double ya[4], yb[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        ya[q] = 4 * ta + q < m ? M[i + (size_t)(4 * ta + q) * LD] : 0.0;
+        yb[q] = 4 * tb + q < m ? M[i + (size_t)(4 * tb + q) * LD] : 0.0;
+      }
+#pragma unroll
+      for (int p = 0; p < 4; ++p)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[p][q] = fma(ya[p], yb[q], acc[p][q]);
+    }
+#pragma unroll
+    for (int p = 0; p < 4; ++p)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        double v = acc[p][q];
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        const int a = 4 * ta + p, b = 4 * tb + q;
+        if (ln == 0 && a < m && b < m) {
+          P[a * m + b] = v;
+          P[b * m + a] = v;
+        }
+      }
+  }
+  cl.sync();
+  for (int e = r * ch + tid; e < min(cnt, (r + 1) * ch); e += nt) {   // reduce own chunk
+    double v = 0.0;
+    for (int s = 0; s < CS; ++s) v += cl.map_shared_rank(P, s)[e];
+    R[e] = v;
+  }
+  cl.sync();
+  for (int e = tid; e < cnt; e += nt) {                               // gather the others
+    const int own = e / ch;
+    if (own != r) R[e] = cl.map_shared_rank(R, own)[e];
+  }
+  __syncthreads();
+}
+
+// Polar (Newton-Schulz) re-orthonormalisation of the na block vectors held row-distributed in
+// S.Yb (rows [0, RB) of this CTA): G = Yb^T Yb (cluster_gram), D = diag(G)^-1/2 and
+// Yb <- Yb D (3I - D G D) / 2.  The error e = max|D G D - I| squares per step (0.75 e^2): one
+// step when e < 1e-8 (the usual case), more otherwise.  When e > kBcgsCholFail (a CholQR input
+// with kappa > ~1e6) the step is a Cholesky one instead, Yb <- Yb L^-T with G = L L^T (CholQR2:
+// valid up to kappa ~ 1e8), computed redundantly in every CTA from the identical G; returns
+// false (Yb unusable, caller redoes the block) if that Cholesky breaks down or does not bring e
+// down.  Replaces na sequential MGS steps (one cluster barrier each) by one Gram all-reduce; the
+// order of the vectors inside the block is irrelevant to the basis (coefficients are formed as
+// Q^T K afterwards).
+template <int CS, int W, int RBM>
+__device__ bool bcgs_polar(cooperative_groups::cluster_group& cl, BcgsClusterSmem<W, RBM>& S, int na, int RB) {
+  constexpr int LD = BcgsClusterSmem<W, RBM>::LD;
+  constexpr int G = kBcgsClusterThreads / RBM, CPG = W / G;   // apply: column groups x columns
+  static_assert(kBcgsClusterThreads % RBM == 0 && W % G == 0, "polar layout");
+  double* H = S.gram;
+  const double* R = S.gram + W * W;
+  const int tid = threadIdx.x, warp = tid >> 5, ln = tid & 31, NW = blockDim.x >> 5, nt = blockDim.x;
+  const int cnt = na * na;
+  int chol = 0;
+  for (int it = 0; it < 6; ++it) {
+    if (it > 0) cl.sync();            // everyone has gathered the previous reduced Gram
+    cluster_gram<CS, W, RBM>(cl, S, S.Yb, na, RB);
+    for (int a = tid; a < na; a += nt) {
+      const double g = R[a * na + a];
+      S.coef[a] = g > 0.0 ? 1.0 / sqrt(g) : 0.0;
+    }
+    __syncthreads();
+    double err = 0.0;
+    for (int e = tid; e < cnt; e += nt) {
+      const int a = e / na, b = e % na;
+      const double gt = S.coef[a] * R[e] * S.coef[b];
+      err = fmax(err, fabs(gt - (a == b ? 1.0 : 0.0)));
+      H[e] = S.coef[a] * ((a == b ? 1.5 : 0.0) - 0.5 * gt);         // H = D (3I - DGD) / 2
+    }
+    for (int o = 16; o > 0; o >>= 1) err = fmax(err, __shfl_xor_sync(0xffffffffu, err, o));
+    if (ln == 0) S.red[warp] = err;
+    __syncthreads();
+    err = 0.0;
+    for (int w = 0; w < NW; ++w) err = fmax(err, S.red[w]);         // uniform: same G everywhere
+    if (it > 0 && err < 1e-13) break;
+    if (err > kBcgsCholFail) {
+      if (chol == 2) {
+        cl.sync();
+        return false;
+      }
+      ++chol;
+      // Cholesky step: H <- L with G = L L^T (in-order, replicated), Yb <- Yb L^-T
+      __syncthreads();
+      for (int e = tid; e < cnt; e += nt) H[e] = R[e];
+      __syncthreads();
+      bool ok = true;
+      for (int c = 0; c < na; ++c) {
+        const double piv = H[c + c * na];
+        if (!(piv > 1e-14 * R[c * na + c])) {
+          ok = false;
+          break;
+        }
+        const double d = sqrt(piv), inv = 1.0 / d;
+        for (int j = c + 1 + tid; j < na; j += nt) H[j + c * na] *= inv;
+        __syncthreads();
+        const int t = na - c - 1;
+        for (int idx = tid; idx < t * t; idx += nt) {
+          const int j = c + 1 + idx % t, k = c + 1 + idx / t;
+          H[j + k * na] -= H[j + c * na] * H[k + c * na];
+        }
+        if (tid == 0) H[c + c * na] = d;
+        __syncthreads();
+      }
+      if (!ok) {
+        cl.sync();
+        return false;
+      }
+      for (int i = tid; i < RB; i += nt)
+        for (int m = 0; m < na; ++m) {
+          double v = S.Yb[i + (size_t)m * LD];
+          for (int q = 0; q < m; ++q) v = fma(-S.Yb[i + (size_t)q * LD], H[m + q * na], v);
+          S.Yb[i + (size_t)m * LD] = v / H[m + m * na];
+        }
+      __syncthreads();
+      continue;
+    }
+    // Yb <- Yb H: thread = (row i, group of CPG columns); H reads are warp broadcasts
+    const int i = tid % RBM, b0 = (tid / RBM) * CPG;
+    double acc[CPG];
+#pragma unroll
+    for (int q = 0; q < CPG; ++q) acc[q] = 0.0;
+    if (i < RB && b0 < na)
+      for (int a = 0; a < na; ++a) {
+        const double y = S.Yb[i + (size_t)a * LD];
+        const double* h = H + a * na + b0;
+#pragma unroll
+        for (int q = 0; q < CPG; ++q)
+          if (b0 + q < na) acc[q] = fma(y, h[q], acc[q]);
+      }
+    __syncthreads();
+    if (i < RB)
+#pragma unroll
+      for (int q = 0; q < CPG; ++q)
+        if (b0 + q < na) S.Yb[i + (size_t)(b0 + q) * LD] = acc[q];
+    __syncthreads();
+    if (err < 1e-8) break;
+  }
+  cl.sync();                                                            // others may still gather R
+  return true;
+}
+
+// exact per-column step for block column c against the na accepted in-block vectors: two
+// projection passes (the second fused with the norm), accept test, append.  Returns the new na.
+template <int CS, int W, int RBM>
+__device__ int bcgs_column(cooperative_groups::cluster_group& cl, BcgsClusterSmem<W, RBM>& S, const BcgsEntry& E,
+                           const BcgsBatch& B, int c, int na, int& ph, int j0, int k0, double nmax, int nr, int RB,
+                           int r) {
+  constexpr int LD = BcgsClusterSmem<W, RBM>::LD;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  double* x = S.X + (size_t)c * LD;
+  double s2;
+  if (na == 0) {
+    block_dots<LD>(S.Yb, x, nr, 0, true, S.part[ph], S.red);
+    cl.sync();
+    cluster_allreduce<CS>(cl, S.part[ph], 1, S.coef);
+    __syncthreads();
+    s2 = S.coef[0];
+    ph ^= 1;
+  } else {
+    block_dots<LD>(S.Yb, x, nr, na, false, S.part[ph], S.red);
+    cl.sync();
+    cluster_allreduce<CS>(cl, S.part[ph], na, S.coef);
+    __syncthreads();
+    block_update<LD, RBM>(S.Yb, x, nr, na, S.coef);
+    __syncthreads();
+    ph ^= 1;
+    block_dots<LD>(S.Yb, x, nr, na, true, S.part[ph], S.red);
+    cl.sync();
+    cluster_allreduce<CS>(cl, S.part[ph], na + 1, S.coef);
+    __syncthreads();
+    block_update<LD, RBM>(S.Yb, x, nr, na, S.coef);
+    double c2 = 0.0;
+    for (int a = 0; a < na; ++a) c2 = fma(S.coef[a], S.coef[a], c2);
+    s2 = S.coef[na] - c2;
+    __syncthreads();
+    ph ^= 1;
+  }
+  const double lim = E.tau * fmax(E.norm0[j0 + c], nmax);
+  if (B.trace && r == 0 && tid == 0) {
+    const double ratio = s2 > 0.0 ? sqrt(s2 / S.pn2[c]) : 0.0;
+    const int d = ratio > 0.0 ? min(17, max(0, (int)floor(-log10(ratio)))) : 17;
+    atomicAdd(&g_bcgs_hist[d], 1ull);
+  }
+  if (s2 > lim * lim && k0 + na < E.kcap) {
+    const double inv = 1.0 / sqrt(s2);
+    double* y = S.Yb + (size_t)na * LD;
+    for (int i = tid; i < RB; i += nt) y[i] = i < nr ? x[i] * inv : 0.0;
+    ++na;
+  }
+  __syncthreads();
+  return na;
+}
+
 template <int CS, int W, int RBM>
 __global__ void __launch_bounds__(kBcgsClusterThreads, 1)
-    bcgs_block_cluster_kernel(const __grid_constant__ BcgsBatch B, int j0, int w) {
+    bcgs_block_cluster_kernel(const __grid_constant__ BcgsBatch B, int j0, int w, int seq) {
   namespace cg = cooperative_groups;
   extern __shared__ __align__(16) unsigned char smraw[];
   using Smem = BcgsClusterSmem<W, RBM>;
@@ -1230,61 +1466,103 @@ __global__ void __launch_bounds__(kBcgsClusterThreads, 1)
   for (int i = 0; i < NW; ++i) nmax = fmax(nmax, S.red[i]);
   const int k0 = *E.k;
   __syncthreads();
-  // ---- pre-filter: all block column norms in one all-reduce ----
-  for (int c = warp; c < wb; c += NW) {
-    const double* x = S.X + (size_t)c * LD;
-    double q = 0.0;
-    for (int i = ln; i < nr; i += 32) q = fma(x[i], x[i], q);
-    for (int o = 16; o > 0; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
-    if (ln == 0) S.part[0][c] = q;
-  }
-  cl.sync();
-  cluster_allreduce<CS>(cl, S.part[0], wb, S.coef);
-  __syncthreads();
-  for (int c = tid; c < wb; c += nt) {
-    const double lim = E.tau * fmax(E.norm0[j0 + c], nmax);
-    S.alive[c] = S.coef[c] > lim * lim;
-  }
-  __syncthreads();
   int na = 0, ph = 1;                                      // ph: partial buffer of the next phase
-  for (int c = 0; c < wb; ++c) {
-    if (!S.alive[c]) continue;
-    double* x = S.X + (size_t)c * LD;
-    double s2;
-    if (na == 0) {
-      block_dots<LD>(S.Yb, x, nr, 0, true, S.part[ph], S.red);
-      cl.sync();
-      cluster_allreduce<CS>(cl, S.part[ph], 1, S.coef);
-      __syncthreads();
-      s2 = S.coef[0];
-      ph ^= 1;
-    } else {
-      block_dots<LD>(S.Yb, x, nr, na, false, S.part[ph], S.red);
-      cl.sync();
-      cluster_allreduce<CS>(cl, S.part[ph], na, S.coef);
-      __syncthreads();
-      block_update<LD, RBM>(S.Yb, x, nr, na, S.coef);
-      __syncthreads();
-      ph ^= 1;
-      block_dots<LD>(S.Yb, x, nr, na, true, S.part[ph], S.red);
-      cl.sync();
-      cluster_allreduce<CS>(cl, S.part[ph], na + 1, S.coef);
-      __syncthreads();
-      block_update<LD, RBM>(S.Yb, x, nr, na, S.coef);
-      double c2 = 0.0;
-      for (int a = 0; a < na; ++a) c2 = fma(S.coef[a], S.coef[a], c2);
-      s2 = S.coef[na] - c2;
-      __syncthreads();
-      ph ^= 1;
+  if (seq) {
+    // ---- per-column path: pre-filter (all block column norms in one all-reduce), then every
+    // alive column through bcgs_column ----
+    for (int c = warp; c < wb; c += NW) {
+      const double* x = S.X + (size_t)c * LD;
+      double q = 0.0;
+      for (int i = ln; i < nr; i += 32) q = fma(x[i], x[i], q);
+      for (int o = 16; o > 0; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
+      if (ln == 0) S.part[0][c] = q;
     }
-    const double lim = E.tau * fmax(E.norm0[j0 + c], nmax);
-    if (s2 > lim * lim && k0 + na < E.kcap) {
-      const double inv = 1.0 / sqrt(s2);
-      double* y = S.Yb + (size_t)na * LD;
-      for (int i = tid; i < RB; i += nt) y[i] = i < nr ? x[i] * inv : 0.0;
-      ++na;
+    cl.sync();
+    cluster_allreduce<CS>(cl, S.part[0], wb, S.coef);
+    __syncthreads();
+    for (int c = tid; c < wb; c += nt) {
+      const double lim = E.tau * fmax(E.norm0[j0 + c], nmax);
+      S.alive[c] = S.coef[c] > lim * lim;
+      S.pn2[c] = S.coef[c];
+      if (B.trace && r == 0 && !S.alive[c]) atomicAdd(&g_bcgs_hist[18], 1ull);
+    }
+    if (B.trace && r == 0 && tid == 0) atomicAdd(&g_bcgs_hist[19], 1ull);
+    __syncthreads();
+    for (int c = 0; c < wb; ++c)
+      if (S.alive[c]) na = bcgs_column<CS, W, RBM>(cl, S, E, B, c, na, ph, j0, k0, nmax, nr, RB, r);
+  } else {
+    // ---- Gram path ----
+    cluster_gram<CS, W, RBM>(cl, S, S.X, wb, RB);
+    double* L = S.gram;                                    // Cholesky in place of the partials
+    const double* G = S.gram + W * W;
+    for (int e = tid; e < wb * wb; e += nt) L[e] = G[e];
+    for (int c = tid; c < wb; c += nt) {
+      const double lim = E.tau * fmax(E.norm0[j0 + c], nmax);
+      S.pn2[c] = G[c * wb + c];
+      S.alive[c] = S.pn2[c] > lim * lim;
+      if (B.trace && r == 0 && !S.alive[c]) atomicAdd(&g_bcgs_hist[18], 1ull);
+    }
+    if (B.trace && r == 0 && tid == 0) atomicAdd(&g_bcgs_hist[19], 1ull);
+    __syncthreads();
+    // replicated in-order Cholesky with deferral (identical arithmetic in every CTA)
+    int nC = 0, nU = 0;
+    const int cap = E.kcap - k0;
+    for (int c = 0; c < wb; ++c) {
+      if (!S.alive[c]) continue;
+      const double piv = L[c + c * wb];
+      const double lim = E.tau * fmax(E.norm0[j0 + c], nmax);
+      if (nC < cap && piv > fmax(kBcgsTheta2 * S.pn2[c], 1.01 * lim * lim)) {
+        const double d = sqrt(piv), inv = 1.0 / d;
+        for (int j = c + 1 + tid; j < wb; j += nt) L[j + c * wb] *= inv;
+        __syncthreads();
+        const int t = wb - c - 1;
+        for (int idx = tid; idx < t * t; idx += nt) {
+          const int j = c + 1 + idx % t, k = c + 1 + idx / t;
+          L[j + k * wb] -= L[j + c * wb] * L[k + c * wb];
+        }
+        if (tid == 0) {
+          L[c + c * wb] = d;
+          S.cidx[nC] = c;
+        }
+        if (B.trace && r == 0 && tid == 0) {
+          const int dd = min(17, max(0, (int)floor(-0.5 * log10(piv / S.pn2[c]))));
+          atomicAdd(&g_bcgs_hist[dd], 1ull);
+        }
+        ++nC;
+        __syncthreads();
+      } else if (piv > kBcgsTheta2 * S.pn2[c] && piv < 0.99 * lim * lim) {
+        // residual against the accepted subset already below lim (accurate to ~1e-6 here): the
+        // per-column path, projecting against a superset, would reject it too
+        if (B.trace && r == 0 && tid == 0) atomicAdd(&g_bcgs_hist[22], 1ull);
+      } else if (nC < cap || piv <= kBcgsTheta2 * S.pn2[c]) {
+        if (tid == 0) S.uidx[nU] = c;
+        ++nU;
+      }
     }
     __syncthreads();
+    if (B.trace && r == 0 && tid == 0) atomicAdd(&g_bcgs_hist[20], (unsigned long long)nU);
+    // CholQR: Yb[:, m] = (X[:, c_m] - sum_{q < m} Yb[:, q] L[c_m, c_q]) / L[c_m, c_m]
+    for (int i = tid; i < RB; i += nt) {
+      for (int m = 0; m < nC; ++m) {
+        const int c = S.cidx[m];
+        double v = S.X[i + (size_t)c * LD];
+        for (int q = 0; q < m; ++q) v = fma(-S.Yb[i + (size_t)q * LD], L[c + S.cidx[q] * wb], v);
+        S.Yb[i + (size_t)m * LD] = v / L[c + c * wb];
+      }
+    }
+    __syncthreads();
+    cl.sync();                                             // all gathers of G done before reuse
+    // CholQR loses orthogonality like eps kappa(X_C)^2; the polar routine repairs it with a second
+    // Cholesky step up to kappa ~ 1e8, beyond that the block is redone on the per-column path
+    if (bcgs_polar<CS, W, RBM>(cl, S, nC, RB)) {
+      na = nC;
+      for (int u = 0; u < nU; ++u)
+        na = bcgs_column<CS, W, RBM>(cl, S, E, B, S.uidx[u], na, ph, j0, k0, nmax, nr, RB, r);
+    } else {
+      if (B.trace && r == 0 && tid == 0) atomicAdd(&g_bcgs_hist[21], 1ull);
+      for (int c = 0; c < wb; ++c)
+        if (S.alive[c]) na = bcgs_column<CS, W, RBM>(cl, S, E, B, c, na, ph, j0, k0, nmax, nr, RB, r);
+    }
   }
   for (int idx = tid; idx < nr * W; idx += nt) {           // unused block columns stay 0
     const int i = idx % nr, a = idx / nr;
@@ -1294,116 +1572,12 @@ __global__ void __launch_bounds__(kBcgsClusterThreads, 1)
   cl.sync();                                                 // smem stays alive for readers
 }
 
-// Polar (Newton-Schulz) re-orthonormalisation of the na block vectors held row-distributed in
-// S.Yb (rows [0, RB) of this CTA): G = Yb^T Yb all-reduced through DSMEM (reduce-scatter of the
-// partials in rank order, then all-gather: every CTA holds the same G), D = diag(G)^-1/2 and
-// Yb <- Yb D (3I - D G D) / 2.  The error e = max|D G D - I| squares per step (0.75 e^2): one
-// step when e < 1e-8 (the usual case: two in-block passes plus the second projection leave
-// e ~ 1e-13), up to 4 otherwise.  Replaces na sequential MGS steps (one cluster barrier each) by
-// one Gram all-reduce; the order of the vectors inside the block is irrelevant to the basis
-// (coefficients are formed as Q^T K afterwards).  Shared scratch: S.X (partials, then H; and the
-// reduced Gram), which needs LD * W >= 2 W^2.
-template <int CS, int W, int RBM>
-__device__ void bcgs_polar(cooperative_groups::cluster_group& cl, BcgsClusterSmem<W, RBM>& S, int na, int RB) {
-  constexpr int LD = BcgsClusterSmem<W, RBM>::LD;
-  constexpr int G = kBcgsClusterThreads / RBM, CPG = W / G;   // apply: column groups x columns
-  static_assert(LD >= 2 * W && kBcgsClusterThreads % RBM == 0 && W % G == 0, "polar layout");
-  double* P = S.X;
-  double* R = S.X + W * W;
-  const int tid = threadIdx.x, warp = tid >> 5, ln = tid & 31, NW = blockDim.x >> 5, nt = blockDim.x;
-  const int cnt = na * na, ch = (cnt + CS - 1) / CS, r = (int)cl.block_rank(), nt4 = (na + 3) / 4;
-  for (int it = 0; it < 4; ++it) {
-    // partial Gram over this CTA's rows: 4 x 4 upper tiles per warp, lanes over rows
-    for (int t = warp; t < nt4 * nt4; t += NW) {
-      const int ta = t / nt4, tb = t % nt4;
-      if (ta > tb) continue;
-      double acc[4][4] = {};
-      for (int i = ln; i < RB; i += 32) {
-        double ya[4], yb[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          ya[q] = 4 * ta + q < na ? S.Yb[i + (size_t)(4 * ta + q) * LD] : 0.0;
-          yb[q] = 4 * tb + q < na ? S.Yb[i + (size_t)(4 * tb + q) * LD] : 0.0;
-        }
-#pragma unroll
-        for (int p = 0; p < 4; ++p)
-#pragma unroll
-          for (int q = 0; q < 4; ++q) acc[p][q] = fma(ya[p], yb[q], acc[p][q]);
-      }
-#pragma unroll
-      for (int p = 0; p < 4; ++p)
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          double v = acc[p][q];
-          for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-          const int a = 4 * ta + p, b = 4 * tb + q;
-          if (ln == 0 && a < na && b < na) {
-            P[a * na + b] = v;
-            P[b * na + a] = v;
-          }
-        }
-    }
-    cl.sync();
-    for (int e = r * ch + tid; e < min(cnt, (r + 1) * ch); e += nt) {   // reduce own chunk
-      double v = 0.0;
-      for (int s = 0; s < CS; ++s) v += cl.map_shared_rank(P, s)[e];
-      R[e] = v;
-    }
-    cl.sync();
-    for (int e = tid; e < cnt; e += nt) {                               // gather the others
-      const int own = e / ch;
-      if (own != r) R[e] = cl.map_shared_rank(R, own)[e];
-    }
-    __syncthreads();
-    for (int a = tid; a < na; a += nt) {
-      const double g = R[a * na + a];
-      S.coef[a] = g > 0.0 ? 1.0 / sqrt(g) : 0.0;
-    }
-    __syncthreads();
-    double err = 0.0;
-    for (int e = tid; e < cnt; e += nt) {
-      const int a = e / na, b = e % na;
-      const double gt = S.coef[a] * R[e] * S.coef[b];
-      err = fmax(err, fabs(gt - (a == b ? 1.0 : 0.0)));
-      P[e] = S.coef[a] * ((a == b ? 1.5 : 0.0) - 0.5 * gt);         // H = D (3I - DGD) / 2
-    }
-    for (int o = 16; o > 0; o >>= 1) err = fmax(err, __shfl_xor_sync(0xffffffffu, err, o));
-    if (ln == 0) S.red[warp] = err;
-    __syncthreads();
-    err = 0.0;
-    for (int w = 0; w < NW; ++w) err = fmax(err, S.red[w]);
-    if (it > 0 && err < 1e-13) break;                                   // uniform: same G everywhere
-    // Yb <- Yb H: thread = (row i, group of CPG columns); H reads are warp broadcasts
-    const int i = tid % RBM, b0 = (tid / RBM) * CPG;
-    double acc[CPG];
-#pragma unroll
-    for (int q = 0; q < CPG; ++q) acc[q] = 0.0;
-    if (i < RB && b0 < na)
-      for (int a = 0; a < na; ++a) {
-        const double y = S.Yb[i + (size_t)a * LD];
-        const double* h = P + a * na + b0;
-#pragma unroll
-        for (int q = 0; q < CPG; ++q)
-          if (b0 + q < na) acc[q] = fma(y, h[q], acc[q]);
-      }
-    __syncthreads();
-    if (i < RB)
-#pragma unroll
-      for (int q = 0; q < CPG; ++q)
-        if (b0 + q < na) S.Yb[i + (size_t)(b0 + q) * LD] = acc[q];
-    __syncthreads();
-    if (err < 1e-8) break;
-  }
-  cl.sync();                                                            // others may still gather R
-}
-
 // BCGS2 second pass, in-block part, on the cluster: Y[:, :nacc] (re-projected against Q) are
-// re-orthonormalised among themselves and appended to Q at k: polar step above (default), or
-// one MGS pass with dots and norm in one all-reduce (FC_BCGS_MGS_FINAL, or layouts without the
-// polar scratch).
+// re-orthonormalised among themselves and appended to Q at k: polar step (default), or one MGS
+// pass with dots and norm in one all-reduce (FC_BCGS_MGS_FINAL).
 template <int CS, int W, int RBM>
 __global__ void __launch_bounds__(kBcgsClusterThreads, 1)
-    bcgs_finalize_cluster_kernel(const __grid_constant__ BcgsBatch B, int j0, int mgs) {
+    bcgs_finalize_cluster_kernel(const __grid_constant__ BcgsBatch B, int j0, int w, int mgs) {
   namespace cg = cooperative_groups;
   extern __shared__ __align__(16) unsigned char smraw[];
   using Smem = BcgsClusterSmem<W, RBM>;
@@ -1416,12 +1590,13 @@ __global__ void __launch_bounds__(kBcgsClusterThreads, 1)
   const int r = (int)cl.block_rank(), RB = (n + CS - 1) / CS;
   const int r0 = r * RB, nr = max(0, min(n, r0 + RB) - r0);
   const int tid = threadIdx.x, nt = blockDim.x;
+  (void)w;
   for (int idx = tid; idx < RB * na; idx += nt) {
     const int i = idx % RB, c = idx / RB;
     S.Yb[i + (size_t)c * LD] = i < nr ? E.Y[(size_t)(r0 + i) + (size_t)c * n] : 0.0;
   }
   __syncthreads();
-  if constexpr (RBM + 4 >= 2 * W) if (!mgs) {
+  if (!mgs) {
     bcgs_polar<CS, W, RBM>(cl, S, na, RB);
     for (int idx = tid; idx < nr * na; idx += nt) {
       const int i = idx % nr, c = idx / nr;
@@ -1666,7 +1841,7 @@ void pmgs(const PmgsBatch& b, cudaStream_t st) {
 
 template <typename K>
 void launch_cluster(K kern, int CS, int nb, size_t smem, cudaStream_t st, const BcgsBatch& b, int j0, int w,
-                    bool with_w) {
+                    int flag) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(CS, nb, 1);
   cfg.blockDim = dim3(kBcgsClusterThreads, 1, 1);
@@ -1679,8 +1854,7 @@ void launch_cluster(K kern, int CS, int nb, size_t smem, cudaStream_t st, const 
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  if (with_w) FC_CUDA_TRY(cudaLaunchKernelEx(&cfg, (void (*)(BcgsBatch, int, int))kern, b, j0, w));
-  else FC_CUDA_TRY(cudaLaunchKernelEx(&cfg, (void (*)(BcgsBatch, int))kern, b, j0));
+  FC_CUDA_TRY(cudaLaunchKernelEx(&cfg, (void (*)(BcgsBatch, int, int, int))kern, b, j0, w, flag));
   FC_CHECK_LAUNCH();
 }
 
@@ -1703,15 +1877,15 @@ void bcgs_cluster_setup() {
 template <int CS, int W, int RB>
 void bcgs_cluster_block(const BcgsBatch& bb, int j0, cudaStream_t st) {
   bcgs_cluster_setup<CS, W, RB>();
-  launch_cluster(bcgs_block_cluster_kernel<CS, W, RB>, CS, bb.nb, sizeof(BcgsClusterSmem<W, RB>), st, bb, j0, W, true);
+  static const int seq = getenv("FC_BCGS_SEQ") != nullptr;   // diagnostic: per-column in-block path
+  launch_cluster(bcgs_block_cluster_kernel<CS, W, RB>, CS, bb.nb, sizeof(BcgsClusterSmem<W, RB>), st, bb, j0, W, seq);
 }
 
 template <int CS, int W, int RB>
 void bcgs_cluster_finalize(const BcgsBatch& bb, int j0, cudaStream_t st) {
   bcgs_cluster_setup<CS, W, RB>();
   static const int mgs = getenv("FC_BCGS_MGS_FINAL") != nullptr;   // diagnostic: sequential MGS
-  launch_cluster(bcgs_finalize_cluster_kernel<CS, W, RB>, CS, bb.nb, sizeof(BcgsClusterSmem<W, RB>), st, bb, j0, mgs,
-                 true);
+  launch_cluster(bcgs_finalize_cluster_kernel<CS, W, RB>, CS, bb.nb, sizeof(BcgsClusterSmem<W, RB>), st, bb, j0, W, mgs);
 }
 
 // split-K for the two skinny GEMMs of a block projection, P = Q^T A_blk (k x W x n) and
@@ -1726,21 +1900,18 @@ void split_skinny(GemmArgs& p, GemmArgs& u, int n, int k, int w, int nb) {
 void bcgs(const BcgsBatch& bin, cudaStream_t st) {
   if (bin.nb == 0) return;
   static const bool no_cluster = getenv("FC_NO_CLUSTER") != nullptr;
-  static const int wenv = getenv("FC_BCGS_W") ? atoi(getenv("FC_BCGS_W")) : 64;
   int maxn = 0;
   for (int i = 0; i < bin.nb; ++i) maxn = std::max(maxn, bin.e[i].n);
-  // 3: 8 CTAs x 128 rows, W = 64 (n <= 1024, default);  1: 16 x 64, W = 128 (n <= 1024,
-  // FC_BCGS_W=128: half the projection GEMMs, but slower in-block steps: 521 vs 479 ms per C4
-  // solve);  2: 16 x 128, W = 64 (n <= 2048);  0: one CTA per matrix (W = 64)
+  // 3: 8 CTAs x 128 rows (n <= 1024, default);  2: 16 x 128 (n <= 2048);  0: one CTA per matrix.
+  // W = 64 (a W = 128 cluster variant was slower: 521 vs 479 ms per C4 solve with per-column steps)
   int cfg = 0;
   if (!no_cluster) {
-    if (maxn <= 1024) cfg = wenv == 128 ? 1 : 3;
+    if (maxn <= 1024) cfg = 3;
     else if (maxn <= 2048) cfg = 2;
   }
-  const int W = cfg == 1 ? 128 : 64;
+  const int W = 64;
   auto block_step = [&](const BcgsBatch& bb, int j0) {
-    if (cfg == 1) bcgs_cluster_block<16, 128, 64>(bb, j0, st);
-    else if (cfg == 2) bcgs_cluster_block<16, 64, 128>(bb, j0, st);
+    if (cfg == 2) bcgs_cluster_block<16, 64, 128>(bb, j0, st);
     else if (cfg == 3) bcgs_cluster_block<8, 64, 128>(bb, j0, st);
     else {
       bcgs_block_kernel<<<bb.nb, 1024, (size_t)bb.e[0].n * 8, st>>>(bb, j0, W);
@@ -1748,8 +1919,7 @@ void bcgs(const BcgsBatch& bin, cudaStream_t st) {
     }
   };
   auto finalize_step = [&](const BcgsBatch& bb, int j0) {
-    if (cfg == 1) bcgs_cluster_finalize<16, 128, 64>(bb, j0, st);
-    else if (cfg == 2) bcgs_cluster_finalize<16, 64, 128>(bb, j0, st);
+    if (cfg == 2) bcgs_cluster_finalize<16, 64, 128>(bb, j0, st);
     else if (cfg == 3) bcgs_cluster_finalize<8, 64, 128>(bb, j0, st);
     else {
       bcgs_finalize_kernel<<<bb.nb, 1024, (size_t)bb.e[0].n * 8, st>>>(bb, j0);
@@ -1757,6 +1927,22 @@ void bcgs(const BcgsBatch& bin, cudaStream_t st) {
     }
   };
   BcgsBatch b = bin;
+  static const bool trace = getenv("FC_TRACE") != nullptr;
+  if (trace) {
+    static bool reg = false;
+    if (!reg) {
+      reg = true;
+      std::atexit([] {
+        unsigned long long h[23];
+        if (cudaMemcpyFromSymbol(h, g_bcgs_hist, sizeof(h)) != cudaSuccess) return;
+        fprintf(stderr, "[bcgs] blocks %llu (redone %llu) prefiltered %llu deferred %llu rejected %llu; by decade:",
+                h[19], h[21], h[18], h[20], h[22]);
+        for (int d = 0; d < 18; ++d) fprintf(stderr, " %llu", h[d]);
+        fprintf(stderr, "\n");
+      });
+    }
+  }
+  b.trace = trace;
   Scratch scr(st);
   for (int i = 0; i < b.nb; ++i) {
     b.e[i].Y = scr.alloc<double>((size_t)b.e[i].n * kBcgsW);

@@ -69,6 +69,7 @@ struct BcgsEntry {
 };
 struct BcgsBatch {
   int nb = 0;
+  int trace = 0;   // FC_TRACE diagnostics (in-block residual histogram)
   BcgsEntry e[kMaxSyev];
 };
 void bcgs(const BcgsBatch& b, cudaStream_t st);
