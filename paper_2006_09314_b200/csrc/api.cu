@@ -239,7 +239,7 @@ int fc_syev(fc_ctx c, int nb, const int* N, double* const* A, const int* lda, do
                   lam[i] && (Y[i] || r[i] == 0),
               FC_ERR_INVALID_ARG, "fc_syev entry");
       b.e[i] = SyevEntry{N[i], A[i], lda[i], s.alloc<double>(N[i]), s.alloc<double>(N[i]), lam[i], Y[i], ldy[i],
-                         rd + i, s.alloc<double>((size_t)5 * N[i] * N[i])};
+                         rd + i, s.alloc<double>((size_t)6 * N[i] * N[i])};
       maxN = std::max(maxN, N[i]);
     }
     syev_values(b, c->st);

@@ -88,19 +88,26 @@ __global__ void gk_bisect_kernel(int n, const double* __restrict__ s_all, double
 
 // ---- tridiagonal inverse iteration (shared by (a) and (b)) ---------------------------
 // T = tridiag(e, d, e) of size N.  Scratch arrays strided by `stride` (coalesced across
-// threads): 5 arrays of N entries (u0 holds the reciprocal pivots).  Writes the unit vector into
-// v[k*vstride].
+// threads): 5 arrays of N entries (u0 holds the reciprocal pivots), and with `own_work` a sixth
+// one holding the iterate (coalesced, instead of the caller's column v: the solves then touch
+// only coalesced scratch).  Writes the unit vector into v[k*vstride].  All pointers are
+// restrict-qualified (the arrays are disjoint), so the loads of the recurrences can be issued
+// ahead of the FMA chain.
 __device__ void tri_invit(int N, const double* __restrict__ d, const double* __restrict__ e, double lam,
-                          double tnorm, double* scr, size_t stride, double* v, size_t vstride, unsigned seed) {
-  double* u0 = scr;
-  double* u1 = scr + (size_t)N * stride;
-  double* u2 = scr + (size_t)2 * N * stride;
-  double* lm = scr + (size_t)3 * N * stride;
-  double* pv = scr + (size_t)4 * N * stride;
+                          double tnorm, double* scr, size_t stride, double* v_out, size_t vstride, unsigned seed,
+                          bool own_work = false) {
+  double* __restrict__ u0 = scr;
+  double* __restrict__ u1 = scr + (size_t)N * stride;
+  double* __restrict__ u2 = scr + (size_t)2 * N * stride;
+  double* __restrict__ lm = scr + (size_t)3 * N * stride;
+  double* __restrict__ pv = scr + (size_t)4 * N * stride;
+  double* __restrict__ v = own_work ? scr + (size_t)5 * N * stride : v_out;
+  const size_t vs = own_work ? stride : vstride;
   const double tiny = kEps * tnorm + DBL_MIN;
 #define S(a, k) a[(size_t)(k) * stride]
+#define V(k) v[(size_t)(k) * vs]
   if (N == 1) {
-    v[0] = 1.0;
+    v_out[0] = 1.0;
     return;
   }
   // LU with partial pivoting of T - lam I (rows k, k+1 interact only)
@@ -129,36 +136,39 @@ __device__ void tri_invit(int N, const double* __restrict__ d, const double* __r
   for (int k = 0; k < N; ++k) {
     unsigned h = (unsigned)k * 2654435761u ^ (seed * 2246822519u + 0x9E3779B9u);
     h ^= h >> 15; h *= 2246822519u; h ^= h >> 13;
-    v[(size_t)k * vstride] = 0.5 + (h & 0xFFFFFF) / 16777216.0;
+    V(k) = 0.5 + (h & 0xFFFFFF) / 16777216.0;
   }
+  double scale = 1.0;                       // the previous solve's 1 / max|x|, folded into the next
   for (int it = 0; it < 3; ++it) {
     // forward: apply P and L (the running entry carried in a register; every load below is
     // independent of the recurrence, so the loop is an FMA chain)
-    double carry = v[0];
+    double carry = V(0) * scale;
     for (int k = 0; k < N - 1; ++k) {
-      double bk = carry, bk1 = v[(size_t)(k + 1) * vstride];
+      double bk = carry, bk1 = V(k + 1) * scale;
       if (S(pv, k) != 0.0) { double t = bk; bk = bk1; bk1 = t; }
       bk1 -= S(lm, k) * bk;
-      v[(size_t)k * vstride] = bk;
+      V(k) = bk;
       carry = bk1;
     }
-    v[(size_t)(N - 1) * vstride] = carry;
+    V(N - 1) = carry;
     // backward with U (3 diagonals; u0 holds the reciprocal pivots)
     double x2 = 0.0, x1 = 0.0, nrm = 0.0;
     for (int k = N - 1; k >= 0; --k) {
-      double x = (v[(size_t)k * vstride] - S(u1, k) * x1 - S(u2, k) * x2) * S(u0, k);
-      v[(size_t)k * vstride] = x;
+      double x = (V(k) - S(u1, k) * x1 - S(u2, k) * x2) * S(u0, k);
+      V(k) = x;
       x2 = x1; x1 = x;
       nrm = fmax(nrm, fabs(x));
     }
-    // rescale by the max-abs entry (keeps the next solve in range), then 2-norm at the end
-    double inv = 1.0 / nrm;
-    for (int k = 0; k < N; ++k) v[(size_t)k * vstride] *= inv;
+    scale = 1.0 / nrm;                      // rescale by the max-abs entry (keeps the next solve in range)
   }
   double s2 = 0.0;
-  for (int k = 0; k < N; ++k) { double x = v[(size_t)k * vstride]; s2 += x * x; }
-  double inv = 1.0 / sqrt(s2);
-  for (int k = 0; k < N; ++k) v[(size_t)k * vstride] *= inv;
+  for (int k = 0; k < N; ++k) { double x = V(k) * scale; s2 += x * x; }
+  const double inv = scale / sqrt(s2);
+  if (own_work)
+    for (int k = 0; k < N; ++k) v_out[(size_t)k * vstride] = V(k) * inv;
+  else
+    for (int k = 0; k < N; ++k) V(k) *= inv;                 // v is v_out (only accessed through v)
+#undef V
 #undef S
 }
 
@@ -793,7 +803,8 @@ __global__ void tri_invit_kernel(const __grid_constant__ SyevBatch B) {
   if (i >= r) return;
   double tnorm = 0.0;
   for (int k = 0; k < N; ++k) tnorm = fmax(tnorm, fabs(E.d[k]) + 2.0 * (k < N - 1 ? fabs(E.e[k]) : 0.0));
-  tri_invit(N, E.d, E.e, E.lam[i], tnorm, E.scratch + i, (size_t)N, E.Y + (size_t)i * E.ldy, 1, (unsigned)(i + 17));
+  tri_invit(N, E.d, E.e, E.lam[i], tnorm, E.scratch + i, (size_t)N, E.Y + (size_t)i * E.ldy, 1, (unsigned)(i + 17),
+            true);
 }
 
 // one CTA per matrix: CGS2 orthonormalisation of Y[:, 0..r) in order, then back-transform

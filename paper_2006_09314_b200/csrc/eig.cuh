@@ -22,7 +22,7 @@ struct SyevEntry {
   double* lam;               // N (descending)
   double* Y; int ldy;        // N x (cap) eigenvectors
   int* r;                    // device scalar: number of eigenvectors wanted
-  double* scratch;           // 5*N*N doubles of LU scratch for inverse iteration
+  double* scratch;           // 6*N*N doubles of LU + iterate scratch for inverse iteration
 };
 struct SyevBatch {
   int nb = 0;

@@ -222,7 +222,7 @@ CoreResult spectral_tucker(fc_ctx c, int kind, double alpha, double beta, double
     lamc[l] = s.alloc<double>(q[l]);
     Zt[l] = s.alloc<double>((size_t)q[l] * q[l]);
     eb.e[eb.nb++] = SyevEntry{q[l], Gm[l], q[l], s.alloc<double>(q[l]), s.alloc<double>(q[l]), lamc[l], Zt[l], q[l],
-                              rl + l, s.alloc<double>((size_t)5 * q[l] * q[l])};
+                              rl + l, s.alloc<double>((size_t)6 * q[l] * q[l])};
     maxq = std::max(maxq, q[l]);
   }
   syev_values(eb, st);

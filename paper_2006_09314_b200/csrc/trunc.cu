@@ -1063,7 +1063,7 @@ TT truncate_tt(fc_ctx c, const TT& xin, double eps, int rank_cap, TruncStats* st
     lam[l] = s.alloc<double>(ql);
     Y[l] = s.alloc<double>((size_t)ql * ql);
     eb.e[eb.nb++] = SyevEntry{ql, M[l], ql, s.alloc<double>(ql), s.alloc<double>(ql), lam[l], Y[l], ql, rl + l,
-                              s.alloc<double>((size_t)5 * ql * ql)};
+                              s.alloc<double>((size_t)6 * ql * ql)};
     maxq = std::max(maxq, ql);
   }
   syev_values(eb, st);
@@ -1153,7 +1153,7 @@ TT truncate_tt(fc_ctx c, const TT& xin, double eps, int rank_cap, TruncStats* st
       int* rm = s.alloc<int>(1);
       FC_CUDA_TRY(cudaMemcpyAsync(rm, &m, sizeof(int), cudaMemcpyHostToDevice, st));
       gb.e[gb.nb++] = SyevEntry{m, G, m, s.alloc<double>(m), s.alloc<double>(m), mu, Vn, m, rm,
-                                s.alloc<double>((size_t)5 * m * m)};
+                                s.alloc<double>((size_t)6 * m * m)};
       syev_values(gb, st);
       syev_vectors(gb, m, st);
       // s2 = [trusted eigenvalues ; mu], the noise-subspace vectors rotated: Y_ns <- Y_ns V_ns

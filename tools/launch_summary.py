@@ -1,29 +1,33 @@
-"""Summarise an ncu --metrics gpu__time_duration.sum --csv launch list by kernel."""
+"""Summarise an ncu --csv launch list (gpu__time_duration.sum per launch) by kernel name."""
 import collections
 import csv
 import sys
 
+UNIT = {"nsecond": 1e-6, "ns": 1e-6, "usecond": 1e-3, "us": 1e-3, "msecond": 1.0, "ms": 1.0}
 
-def main(path, top=20):
+
+def main(path, top=24):
     rows = list(csv.reader(open(path)))
-    hi = [i for i, r in enumerate(rows) if "Kernel Name" in r][0]
-    h = rows[hi]
-    ki, mi, ui = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
-    tot, cnt = collections.defaultdict(float), collections.Counter()
-    for r in rows[hi + 1:]:
-        if len(r) <= mi:
+    h, agg = None, collections.defaultdict(lambda: [0, 0.0])
+    for r in rows:
+        if h is None:
+            if "Kernel Name" in r:
+                h = r
             continue
-        v = float(r[mi].replace(",", ""))
-        v *= {"nsecond": 1e-6, "ns": 1e-6, "usecond": 1e-3, "us": 1e-3, "msecond": 1.0, "ms": 1.0,
-              "second": 1e3, "s": 1e3}.get(r[ui], 1.0)
-        name = r[ki].split("(")[0][:72]
-        tot[name] += v
-        cnt[name] += 1
-    T = sum(tot.values())
-    print(f"total {T:.1f} ms over {sum(cnt.values())} launches")
-    for k, v in sorted(tot.items(), key=lambda x: -x[1])[:top]:
-        print(f"{100 * v / T:6.2f}%  {v:10.2f} ms  {cnt[k]:5d}  {k}")
+        if len(r) < len(h):
+            continue
+        d = dict(zip(h, r))
+        if d.get("Metric Name") != "gpu__time_duration.sum":
+            continue
+        v = float(d["Metric Value"].replace(",", "")) * UNIT.get(d["Metric Unit"], 1e-6)
+        k = d["Kernel Name"].split("(")[0].replace("fc::<unnamed>::", "")[:60]
+        agg[k][0] += 1
+        agg[k][1] += v
+    tot = sum(v[1] for v in agg.values())
+    print("total %.1f ms over %d launches" % (tot, sum(v[0] for v in agg.values())))
+    for k, v in sorted(agg.items(), key=lambda x: -x[1][1])[:top]:
+        print("%6.2f%% %8.2f ms %5d %s" % (100 * v[1] / tot, v[1], v[0], k))
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], int(sys.argv[2]) if len(sys.argv) > 2 else 20)
+    main(sys.argv[1], int(sys.argv[2]) if len(sys.argv) > 2 else 24)
