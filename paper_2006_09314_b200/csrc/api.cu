@@ -243,7 +243,7 @@ int fc_syev(fc_ctx c, int nb, const int* N, double* const* A, const int* lda, do
       maxN = std::max(maxN, N[i]);
     }
     syev_values(b, c->st);
-    syev_vectors(b, maxN, c->st);
+    syev_vectors(b, maxN, c->st, r);
     FC_CUDA_TRY(cudaStreamSynchronize(c->st));
     return FC_OK;
   });

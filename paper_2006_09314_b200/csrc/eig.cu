@@ -11,6 +11,9 @@
 #include <cfloat>
 #include <cstdlib>
 #include <cstdio>
+#include <vector>
+#include <cmath>
+#include <algorithm>
 #include <cooperative_groups.h>
 #include "eig.cuh"
 
@@ -372,6 +375,25 @@ __device__ double block_sum(double v, double* red) {
   if (threadIdx.x < 32) {
     t = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
     for (int s = 16; s > 0; s >>= 1) t += __shfl_down_sync(0xffffffffu, t, s);
+    if (threadIdx.x == 0) red[32] = t;
+  }
+  __syncthreads();
+  return red[32];
+}
+
+// NaN-propagating maximum (a NaN anywhere makes the result NaN)
+__device__ __forceinline__ double nan_max(double a, double b) { return (b > a || b != b) ? b : a; }
+
+__device__ double block_max(double v, double* red) {
+  for (int s = 16; s > 0; s >>= 1) v = nan_max(v, __shfl_down_sync(0xffffffffu, v, s));
+  const int w = threadIdx.x >> 5, ln = threadIdx.x & 31;
+  __syncthreads();
+  if (ln == 0) red[w] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (threadIdx.x < 32) {
+    t = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+    for (int s = 16; s > 0; s >>= 1) t = nan_max(t, __shfl_down_sync(0xffffffffu, t, s));
     if (threadIdx.x == 0) red[32] = t;
   }
   __syncthreads();
@@ -809,9 +831,13 @@ __global__ void tri_invit_kernel(const __grid_constant__ SyevBatch B) {
 
 // one CTA per matrix: CGS2 orthonormalisation of Y[:, 0..r) in order, then back-transform
 // with the Householder vectors stored in A: z = H_0 H_1 ... H_{N-3} y.
-__global__ void __launch_bounds__(1024) orth_backtransform_kernel(const __grid_constant__ SyevBatch B) {
+// (flag != nullptr: only the entries with flag[i] != 0 are processed; the polar path below
+// handles the others)
+__global__ void __launch_bounds__(1024) orth_backtransform_kernel(const __grid_constant__ SyevBatch B,
+                                                                  const int* __restrict__ flag) {
   __shared__ double red[33];
   extern __shared__ double coef[];   // r coefficients
+  if (flag && flag[blockIdx.x] == 0) return;
   const SyevEntry& E = B.e[blockIdx.x];
   const int N = E.N;
   const int r = min(*E.r, N);
@@ -844,6 +870,48 @@ __global__ void __launch_bounds__(1024) orth_backtransform_kernel(const __grid_c
     double inv = s2 > 0 ? 1.0 / sqrt(s2) : 0.0;
     for (int k = tid; k < N; k += nt) yi[k] *= inv;
     __syncthreads();
+  }
+}
+
+// Polar orthonormalisation of inverse-iteration vectors (syev_vectors with host-known ranks):
+// Newton-Schulz steps Y <- Y D (3I - D G D) / 2 with G = Y^T Y on batched DMMA GEMMs.  The
+// inverse-iteration vectors are orthogonal to eps ||T|| / gap: in the C4 solve max|G - I| is
+// below 1e-8 in 186 of 198 calls and at most 1.3e-4 (FC_TRACE_ORTH), so two steps reach
+// ~1e-17 (0.75 e^2 per step).  Symmetric (Loewdin) orthogonalisation mixes vectors i, j by
+// ~G_ij ~ eps ||T|| / |lam_i - lam_j|, which moves their residuals by ~eps ||T||: as accurate as
+// Gram-Schmidt, and order-free.  Entries whose first error exceeds kOrthPolarMax keep H = I
+// (bit-exact copies) and are flagged for the CGS2 kernel.
+constexpr double kOrthPolarMax = 1e-4;
+struct PolarBatch {
+  int nb = 0;
+  int r[kMaxSyev];
+  double* G[kMaxSyev];      // r x r Gram, overwritten by H
+  int* flag;                // device, nb entries (zeroed by the caller)
+};
+
+__global__ void __launch_bounds__(1024) ns_polar_kernel(const __grid_constant__ PolarBatch P, int step) {
+  __shared__ double red[33];
+  extern __shared__ double dsc[];   // r scale factors
+  const int e = blockIdx.x, r = P.r[e];
+  double* G = P.G[e];
+  const int tid = threadIdx.x, nt = blockDim.x;
+  for (int a = tid; a < r; a += nt) {
+    const double g = G[a + (size_t)a * r];
+    dsc[a] = g > 0.0 ? 1.0 / sqrt(g) : 0.0;
+  }
+  __syncthreads();
+  double err = 0.0;
+  const size_t cnt = (size_t)r * r;
+  for (size_t i = tid; i < cnt; i += nt) {
+    const int a = (int)(i % r), b = (int)(i / r);
+    err = nan_max(err, fabs(dsc[a] * G[i] * dsc[b] - (a == b ? 1.0 : 0.0)));
+  }
+  err = block_max(err, red);
+  const bool keep = step == 0 ? !(err <= kOrthPolarMax) : P.flag[e] != 0;   // NaN -> keep
+  if (step == 0 && tid == 0 && keep) P.flag[e] = 1;
+  for (size_t i = tid; i < cnt; i += nt) {
+    const int a = (int)(i % r), b = (int)(i / r);
+    G[i] = keep ? (a == b ? 1.0 : 0.0) : dsc[a] * ((a == b ? 1.5 : 0.0) - 0.5 * dsc[a] * G[i] * dsc[b]);
   }
 }
 
@@ -1810,14 +1878,98 @@ void syev_values(const SyevBatch& b, cudaStream_t st) {
   FC_CHECK_LAUNCH();
 }
 
-void syev_vectors(const SyevBatch& b, int maxN, cudaStream_t st) {
+void syev_vectors(const SyevBatch& b, int maxN, cudaStream_t st, const int* r_host) {
   if (b.nb == 0 || maxN == 0) return;
   tri_invit_kernel<<<dim3(cdiv(maxN, 64), b.nb), 64, 0, st>>>(b);
   FC_CHECK_LAUNCH();
-  // CGS2 of the inverse-iteration vectors (tridiagonal coordinates), one CTA per matrix
+  static const bool trace_orth = getenv("FC_TRACE_ORTH") != nullptr;
+  if (trace_orth) {   // diagnostics: orthogonality of the inverse-iteration vectors
+    for (int i = 0; i < b.nb; ++i) {
+      const SyevEntry& E = b.e[i];
+      int r = 0;
+      FC_CUDA_TRY(cudaMemcpyAsync(&r, E.r, sizeof(int), cudaMemcpyDeviceToHost, st));
+      FC_CUDA_TRY(cudaStreamSynchronize(st));
+      r = std::min(r, E.N);
+      if (r <= 0) continue;
+      double* G = nullptr;
+      FC_CUDA_TRY(cudaMalloc(&G, (size_t)r * r * 8));
+      dgemm(st, 1, 0, r, r, E.N, 1.0, E.Y, E.ldy, E.Y, E.ldy, 0.0, G, r);
+      std::vector<double> h((size_t)r * r);
+      FC_CUDA_TRY(cudaMemcpyAsync(h.data(), G, h.size() * 8, cudaMemcpyDeviceToHost, st));
+      FC_CUDA_TRY(cudaStreamSynchronize(st));
+      FC_CUDA_TRY(cudaFree(G));
+      double mx = 0.0;
+      int c2 = 0, c6 = 0, c10 = 0;
+      for (int a = 0; a < r; ++a)
+        for (int c = 0; c < r; ++c) {
+          const double v = std::fabs(h[a + (size_t)c * r] - (a == c ? 1.0 : 0.0));
+          mx = std::max(mx, v);
+          if (a < c) {
+            c2 += v > 1e-2;
+            c6 += v > 1e-6;
+            c10 += v > 1e-10;
+          }
+        }
+      fprintf(stderr, "[fc orth] N=%d r=%d max|G-I|=%.2e pairs>1e-2:%d >1e-6:%d >1e-10:%d\n", E.N, r, mx, c2, c6, c10);
+    }
+  }
+  // orthonormalisation of the inverse-iteration vectors (tridiagonal coordinates): polar steps on
+  // GEMMs when the ranks are known on the host, CGS2 (one CTA per matrix) for the flagged or
+  // all entries otherwise
   SyevBatch ob = b;
   for (int i = 0; i < ob.nb; ++i) ob.e[i].A = nullptr;
-  orth_backtransform_kernel<<<b.nb, 1024, (size_t)maxN * 8, st>>>(ob);
+  static const bool no_polar = getenv("FC_ORTH_CGS2") != nullptr;   // diagnostic
+  const int* flag = nullptr;
+  Scratch s(st);
+  if (r_host && !no_polar) {
+    PolarBatch P;
+    P.nb = b.nb;
+    int* fl = s.zeros<int>(b.nb);
+    P.flag = fl;
+    size_t gsz = 0;
+    int rmax = 1, tiles = 0;
+    for (int i = 0; i < b.nb; ++i) {
+      P.r[i] = std::min(r_host[i], b.e[i].N);
+      gsz += (size_t)P.r[i] * P.r[i];
+      rmax = std::max(rmax, P.r[i]);
+      tiles += cdiv(P.r[i], 64) * cdiv(P.r[i], 64);
+    }
+    double* Gall = s.alloc<double>(std::max<size_t>(gsz, 1));
+    double* Y2[kMaxSyev];
+    size_t off = 0;
+    for (int i = 0; i < b.nb; ++i) {
+      P.G[i] = Gall + off;
+      off += (size_t)P.r[i] * P.r[i];
+      Y2[i] = s.alloc<double>(std::max<size_t>((size_t)b.e[i].N * P.r[i], 1));
+    }
+    for (int step = 0; step < 2; ++step) {
+      GemmArgs g, h;
+      g.transA = 1;
+      g.beta = 1.0;
+      int ng = 0;
+      for (int i = 0; i < b.nb; ++i) {
+        if (P.r[i] == 0) continue;
+        const SyevEntry& E = b.e[i];
+        const double* src = step == 0 ? E.Y : Y2[i];
+        const int lds = step == 0 ? E.ldy : E.N;
+        double* dst = step == 0 ? Y2[i] : E.Y;
+        const int ldd = step == 0 ? E.N : E.ldy;
+        g.b[ng] = GemmBatch{P.r[i], P.r[i], E.N, src, lds, src, lds, P.G[i], P.r[i], nullptr, 0, nullptr};
+        h.b[ng] = GemmBatch{E.N, P.r[i], P.r[i], src, lds, P.G[i], P.r[i], dst, ldd, nullptr, 0, nullptr};
+        ++ng;
+      }
+      if (ng == 0) break;
+      g.nbatch = h.nbatch = ng;
+      g.splitk = std::max(1, std::min(cdiv(maxN, 64), cdiv(2 * 148, std::max(tiles, 1))));
+      FC_CUDA_TRY(cudaMemsetAsync(Gall, 0, gsz * 8, st));
+      gemm(g, st);
+      ns_polar_kernel<<<b.nb, 1024, (size_t)rmax * 8, st>>>(P, step);
+      FC_CHECK_LAUNCH();
+      gemm(h, st);
+    }
+    flag = fl;
+  }
+  orth_backtransform_kernel<<<b.nb, 1024, (size_t)maxN * 8, st>>>(ob, flag);
   FC_CHECK_LAUNCH();
   // back-transformation, warp per vector over many CTAs
   const dim3 grid(cdiv(maxN, 16), b.nb);
@@ -1831,7 +1983,7 @@ void orthonormalize_cols(int N, double* Y, int ldy, int* r_dev, int rmax, cudaSt
   SyevBatch b;
   b.nb = 1;
   b.e[0] = SyevEntry{N, nullptr, 0, nullptr, nullptr, nullptr, Y, ldy, r_dev, nullptr};
-  orth_backtransform_kernel<<<1, 1024, (size_t)std::max(rmax, 1) * 8, st>>>(b);
+  orth_backtransform_kernel<<<1, 1024, (size_t)std::max(rmax, 1) * 8, st>>>(b, nullptr);
   FC_CHECK_LAUNCH();
 }
 

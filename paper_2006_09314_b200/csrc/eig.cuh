@@ -31,8 +31,9 @@ struct SyevBatch {
 // phase 1: Householder tridiagonalisation + bisection for all eigenvalues (descending)
 void syev_values(const SyevBatch& b, cudaStream_t st);
 // phase 2 (after r has been decided on the device): inverse iteration + orthonormalisation +
-// back-transformation of the leading r eigenvectors.
-void syev_vectors(const SyevBatch& b, int maxN, cudaStream_t st);
+// back-transformation of the leading r eigenvectors.  r_host (optional): the same ranks known on
+// the host, which enables the GEMM-based polar orthonormalisation.
+void syev_vectors(const SyevBatch& b, int maxN, cudaStream_t st, const int* r_host = nullptr);
 
 // Column-pivoted modified Gram-Schmidt (rank revealing, no Gram squaring), one CTA per entry:
 // A (n x p, overwritten) -> Q (n x k) orthonormal, every column of A within tau*||a_c|| of

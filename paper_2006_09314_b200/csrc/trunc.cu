@@ -1092,7 +1092,12 @@ TT truncate_tt(fc_ctx c, const TT& xin, double eps, int rank_cap, TruncStats* st
       if (refine[l]) hr[l] = q[l];
     FC_CUDA_TRY(cudaMemcpyAsync(rl, hr, 3 * sizeof(int), cudaMemcpyHostToDevice, st));
   }
-  syev_vectors(eb, maxq, st);
+  {
+    int hr[3] = {r[0], r[1], r[2]};
+    for (int l = 0; l < 3; ++l)
+      if (refine[l]) hr[l] = q[l];
+    syev_vectors(eb, maxq, st, hr);
+  }
   if (any_refine) {
     for (int l = 0; l < 3; ++l) {
       if (!refine[l]) continue;
@@ -1155,7 +1160,7 @@ TT truncate_tt(fc_ctx c, const TT& xin, double eps, int rank_cap, TruncStats* st
       gb.e[gb.nb++] = SyevEntry{m, G, m, s.alloc<double>(m), s.alloc<double>(m), mu, Vn, m, rm,
                                 s.alloc<double>((size_t)6 * m * m)};
       syev_values(gb, st);
-      syev_vectors(gb, m, st);
+      syev_vectors(gb, m, st, &m);
       // s2 = [trusted eigenvalues ; mu], the noise-subspace vectors rotated: Y_ns <- Y_ns V_ns
       double* s2r = s.alloc<double>(ql);
       FC_CUDA_TRY(cudaMemcpyAsync(s2r, lam[l], (size_t)pk * 8, cudaMemcpyDeviceToDevice, st));
