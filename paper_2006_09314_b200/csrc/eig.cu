@@ -588,13 +588,9 @@ __global__ void __launch_bounds__(1024) tridiag_packed_kernel(const __grid_const
 //   of the own columns is fused with the next step's partial matvec.
 // Two cluster barriers per step; the owner of a slice serves only that slice (DSMEM reads are
 // paid by the owner's shared-memory port).
-constexpr int kCl8MaxN = 600;    // packed own columns + 5 N vectors fit 220 KB with 8 CTAs
+constexpr int kCl4MaxN = 440;    // packed own columns + 5 N vectors fit 220 KB with 4 CTAs
+constexpr int kCl8MaxN = 600;    // ... with 8 CTAs
 constexpr int kCl16MaxN = 840;   // ... with 16 CTAs (non-portable cluster size)
-
-template <int CS>
-__host__ __device__ constexpr bool cluster_class(int N) {
-  return CS == 8 ? (N > kClusterMinN && N <= kCl8MaxN) : (N > kCl8MaxN && N <= kCl16MaxN);
-}
 
 template <int CS>
 __host__ __device__ inline size_t cluster_smem_doubles(int N) {
@@ -610,14 +606,15 @@ __device__ __forceinline__ double rank2(double a, double ui, double qi, double u
 }
 
 template <int CS>
-__global__ void __launch_bounds__(1024, 1) tridiag_cluster_kernel(const __grid_constant__ SyevBatch B) {
+__global__ void __launch_bounds__(1024, 1) tridiag_cluster_kernel(const __grid_constant__ SyevBatch B, int nlo,
+                                                                  int nhi) {
   namespace cg = cooperative_groups;
   extern __shared__ double sm[];
   __shared__ double red[33];
   cg::cluster_group cl = cg::this_cluster();
   const SyevEntry& E = B.e[blockIdx.y];
   const int N = E.N;
-  if (!cluster_class<CS>(N)) return;                     // uniform over the cluster
+  if (N <= nlo || N > nhi) return;                       // this launch's size class (uniform)
   const int c = (int)cl.block_rank();
   const int tid = threadIdx.x, nt = blockDim.x, warp = tid >> 5, ln = tid & 31, NW = nt >> 5;
   const int ncol = (N - c + CS - 1) / CS;                // own columns j = c + t CS
@@ -1807,7 +1804,7 @@ void sl_eigen_device(cudaStream_t st, int n, const double* a_mid_dev, int bounda
 }
 
 template <int CS>
-void launch_tridiag_cluster(const SyevBatch& b, size_t smem, cudaStream_t st) {
+void launch_tridiag_cluster(const SyevBatch& b, size_t smem, cudaStream_t st, int nlo, int nhi) {
   auto kern = tridiag_cluster_kernel<CS>;
   static bool attr = false;
   if (!attr) {
@@ -1827,7 +1824,7 @@ void launch_tridiag_cluster(const SyevBatch& b, size_t smem, cudaStream_t st) {
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  FC_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, b));
+  FC_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, b, nlo, nhi));
   FC_CHECK_LAUNCH();
 }
 
@@ -1837,8 +1834,14 @@ void syev_values(const SyevBatch& b, cudaStream_t st) {
   const int minG = no_cluster ? kPackedMaxN : kCl16MaxN;   // sizes above go to the global kernel
   const int maxP = no_cluster ? kPackedMaxN : kClusterMinN; // sizes up to this: packed single CTA
   int maxN = 0;
-  size_t smem_g = 0, smem_p = 0, smem_8 = 0, smem_16 = 0;
+  size_t smem_g = 0, smem_p = 0, smem_4 = 0, smem_8 = 0, smem_16 = 0;
   bool any_g = false, any_p = false;
+  // cluster size classes (N in (lo, hi]): 16 CTAs (non-portable) for 97..840 (the per-step
+  // matvec / rank-2 work per CTA matters more than the DSMEM fan-in: C4 solve 365 ms vs 371 ms
+  // with 8 CTAs up to 600 and 388 ms with 4 CTAs up to 440).  FC_TRI_CS=4|8: those layouts.
+  static const int tri_cs = getenv("FC_TRI_CS") ? atoi(getenv("FC_TRI_CS")) : 16;
+  const int cl4 = tri_cs == 4 ? kCl4MaxN : maxP;
+  const int cl8 = tri_cs == 16 ? maxP : kCl8MaxN;
   constexpr int NW = kTriThreads / 32;
   for (int i = 0; i < b.nb; ++i) {
     const int N = b.e[i].N;
@@ -1850,14 +1853,17 @@ void syev_values(const SyevBatch& b, cudaStream_t st) {
     } else if (N > minG) {
       any_g = true;
       smem_g = std::max(smem_g, (size_t)(2 + NW) * N * 8);
-    } else if (cluster_class<8>(N)) {
+    } else if (N <= cl4) {
+      smem_4 = std::max(smem_4, cluster_smem_doubles<4>(N) * 8);
+    } else if (N <= cl8) {
       smem_8 = std::max(smem_8, cluster_smem_doubles<8>(N) * 8);
     } else {
       smem_16 = std::max(smem_16, cluster_smem_doubles<16>(N) * 8);
     }
   }
-  if (smem_8) launch_tridiag_cluster<8>(b, smem_8, st);
-  if (smem_16) launch_tridiag_cluster<16>(b, smem_16, st);
+  if (smem_4) launch_tridiag_cluster<4>(b, smem_4, st, maxP, cl4);
+  if (smem_8) launch_tridiag_cluster<8>(b, smem_8, st, cl4, cl8);
+  if (smem_16) launch_tridiag_cluster<16>(b, smem_16, st, cl8, kCl16MaxN);
   if (maxN == 0) return;
   require(smem_g <= kTriSmemMax, FC_ERR_CAPACITY, "symmetric eigensolver: matrix dimension above 1500");
   static bool attr = false;
