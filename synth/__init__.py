@@ -8,4 +8,5 @@ fixed seeds (NumPy PCG64 `default_rng`).  Both the oracle (`oracle/`) and the GP
 """
 from .configs import (  # noqa: F401
     CONFIGS, Problem, grid_points, midpoints, make_problem, random_cp, normalize_cp,
+    CONFIGS2, Problem2, make_problem2,
 )

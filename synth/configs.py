@@ -139,3 +139,60 @@ def make_problem(name: str, n: int | None = None, eps: float | None = None,
 
 # C5 operator-apply sweep grid [BJ configs[4]]
 C5_GRID = [(n, R, r) for n in (256, 1024, 2048) for R in (16, 64, 256) for r in (8, 16, 32)]
+
+
+# ---- 2D variant --------------------------------------------------
+# The paper's 2D tests [P:1068-1225] use a box / H-type design function given only as figures;
+# these seeded stand-ins reuse C1's a1, a2 and rank-2 / rank-8 right-hand sides.
+
+@dataclass
+class Problem2:
+    name: str
+    n: int
+    a_mid: np.ndarray          # (2, n+1) midpoint samples of a1, a2
+    alpha: float
+    beta: float
+    eps: float
+    tol_stop: float
+    b_w: np.ndarray
+    b_U: list = field(default_factory=list)
+    kmax: int = 100
+    precond_rank: int = 6
+    boundary: int = 0
+
+
+def _rhs2_smooth(n):
+    x = grid_points(n)
+    s = np.sin(np.pi * x)
+    g = x * (1.0 - x) * np.exp(x)
+    return normalize_cp(np.ones(2), [np.stack([s, g], axis=1), np.stack([s, g], axis=1)])
+
+
+def _rhs2_bumps(n, R=8, seed=6):
+    x = grid_points(n)
+    rng = np.random.default_rng(seed)
+    c = rng.uniform(0.2, 0.8, size=(2, R))
+    wd = rng.uniform(0.05, 0.2, size=(2, R))
+    U = [np.exp(-((x[:, None] - c[l][None, :]) ** 2) / (2.0 * wd[l][None, :] ** 2)) for l in range(2)]
+    return normalize_cp(np.ones(R), U)
+
+
+CONFIGS2 = {
+    # D1: the paper's 2D n = 64 setting [P:1125-1152] (alpha sweep), smooth rank-2 right-hand side
+    "D1": dict(n=64, alpha=0.5, beta=0.01, eps=1e-6, rhs=_rhs2_smooth),
+    # D2: large 2D grid (the paper's 2D grids reach 2048 [P:1097-1123]), rank-8 bumps
+    "D2": dict(n=1024, alpha=0.5, beta=0.01, eps=1e-6, rhs=_rhs2_bumps),
+}
+
+
+def make_problem2(name: str, n: int | None = None, eps: float | None = None, alpha: float | None = None,
+                  beta: float | None = None) -> Problem2:
+    cfg = CONFIGS2[name]
+    n = cfg["n"] if n is None else n
+    eps = cfg["eps"] if eps is None else eps
+    a_mid = _coef_c1(midpoints(n))[:2]
+    w, U = cfg["rhs"](n)
+    return Problem2(name=name, n=n, a_mid=np.ascontiguousarray(a_mid),
+                    alpha=cfg["alpha"] if alpha is None else alpha,
+                    beta=cfg["beta"] if beta is None else beta,
+                    eps=eps, tol_stop=10.0 * eps, b_w=w, b_U=U)
