@@ -197,6 +197,51 @@ int state_recover(fc_ctx ctx, const fc_cp* u, double eps, fc_cp* y, fc_trunc_inf
  * CAPACITY) receives X; rep (host, may be NULL) the per-iteration history. */
 int pcg_solve(fc_ctx ctx, const fc_cp* b, const fc_params* p, fc_cp* u, fc_pcg_report* rep);
 
+/* ---- the 2D variant ------------------------------------------------
+ * A = T1 (x) I + I (x) T2 [P:449-452 with d = 2]; the same PCG (Algorithm 1, "independent of d"
+ * [P:962-969]) with the reduced-SVD truncation the paper uses for d = 2 [P:973-976].
+ * A low-rank matrix x = sum_k w[k] U[0][:,k] (x) U[1][:,k], i.e. X = U0 diag(w) U1^T [P:585-595],
+ * stored as fc_lr2 with the fc_cp conventions (device pointers, column-major n x cap factors
+ * with leading dimension ld, unit columns, signed weights, rank 0 = zero).  The 2D calls use
+ * the context's mode-0 and mode-1 eigenpairs and their own spectral factorisations. */
+typedef struct {
+    int n[2];        /* mode sizes (both equal to the context's n)                              */
+    int rank;
+    int cap;
+    double* w;       /* device, [cap]                                                           */
+    double* U[2];    /* device, column-major n[l] x cap, leading dimension ld[l]                */
+    int ld[2];
+} fc_lr2;
+
+/* sl_setup_2d [P:443-561 with d = 2]: a_mid HOST, 2 x (n+1) row-major midpoint samples of a1, a2
+ *   (A1, A2).  Eigenpairs of modes 0 and 1 (as sl_setup), then the low-rank factorisations of
+ *   D2[i,j] = F(lam1_i + lam2_j) [P:693 with d = 2]: FC_F by truncated SVD at eps_D (reading 2D-S:
+ *   sum of the dropped s^2 <= eps_D^2 ||D2||_F^2) and FC_G = 1/F with rank precond_rank raised
+ *   until positive on the grid (A7'/A7'' as in 3D).  Errors: INVALID_ARG, NONPOS_COEF, NOT_SPD,
+ *   CAPACITY, CUDA. */
+int sl_setup_2d(fc_ctx ctx, int n, const double* a_mid, const fc_params* p);
+/* get / set (shared-input parity) the 2D factorisation of `which` (FC_F or FC_G).  get: out->cap
+ * must be >= its rank (else CAPACITY with out->rank = required).  set: copies; needs the mode-0/1
+ * eigenpairs (sl_setup_2d or sl_set_eigen) and params for alpha, beta. */
+int op_get_spectral_2d(fc_ctx ctx, int which, fc_lr2* out);
+int op_set_spectral_2d(fc_ctx ctx, int which, const fc_lr2* in);
+/* fracop_apply_2d [P:597-611]: y = F(A) x = sum_k sum_j V0(a_k . V0^T x0_j) (x) V1(b_k . V1^T x1_j),
+ *   term order t = k*x.rank + j (A19), untruncated (y.rank = r_which * x.rank, else CAPACITY),
+ *   columns normalised.  x and y must not alias. */
+int fracop_apply_2d(fc_ctx ctx, int which, const fc_lr2* x, fc_lr2* y);
+/* cp_dot_2d [P:1748-1755 with d = 2]: *out_host = sum_{k,m} w_k v_m <x0_k, y0_m> <x1_k, y1_m>. */
+int cp_dot_2d(fc_ctx ctx, const fc_lr2* x, const fc_lr2* y, double* out_host);
+/* cp_truncate_2d [P:973-976]: reduced SVD — orthonormal bases Q_l of span(U_l) (rank-revealing
+ *   block Gram-Schmidt), core K = C0 diag(w) C1^T with C_l = Q_l^T U_l, SVD of K, smallest r with
+ *   sum_{k>r} s_k^2 <= eps^2 sum s_k^2 (reading 2D-T; ties and zeros as A23), y = (Q0 Uk_r, Q1 Vk_r,
+ *   s_r) with orthonormal factors.  out_rank (host, may be NULL) receives r; y.cap < r -> CAPACITY
+ *   (out_rank = required).  x and y must not alias; ranks of the bases <= 1024. */
+int cp_truncate_2d(fc_ctx ctx, const fc_lr2* x, double eps, fc_lr2* y, int* out_rank);
+/* pcg_solve_2d: Algorithm 1 [P:1825-1872] with fun = F (FC_F factorisation), precond = G (FC_G),
+ *   trunc = cp_truncate_2d(eps) fused with the apply in eigen coordinates (V_l orthogonal: only the
+ *   surviving columns are transformed back); readings A13-A17 as pcg_solve.  Same returns. */
+int pcg_solve_2d(fc_ctx ctx, const fc_lr2* b, const fc_params* p, fc_lr2* u, fc_pcg_report* rep);
+
 /* ---- raw kernels exposed for tests/bench (same ABI rules) ------------------------------- */
 /* C = alpha*op(A)*op(B) + beta*C, FP64, column-major, DMMA tiles; all pointers device.   */
 int fc_dgemm(fc_ctx ctx, int transA, int transB, int M, int N, int K, double alpha,

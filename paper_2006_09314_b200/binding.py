@@ -27,6 +27,11 @@ class fc_cp(C.Structure):
                 ("U", C.c_void_p * 3), ("ld", C.c_int * 3)]
 
 
+class fc_lr2(C.Structure):
+    _fields_ = [("n", C.c_int * 2), ("rank", C.c_int), ("cap", C.c_int), ("w", C.c_void_p),
+                ("U", C.c_void_p * 2), ("ld", C.c_int * 2)]
+
+
 class fc_params(C.Structure):
     _fields_ = [("alpha", C.c_double), ("beta", C.c_double), ("eps", C.c_double),
                 ("tol_stop", C.c_double), ("eps_D", C.c_double), ("kmax", C.c_int),
@@ -69,7 +74,9 @@ ENTRY_POINTS = ["fc_create", "fc_destroy", "fc_last_error", "fc_set_stream", "sl
                 "sl_set_eigen", "op_get_spectral_cp", "op_set_spectral_cp", "op_spectral_rank",
                 "fracop_apply", "precond_apply", "cp_dot", "cp_axpy", "cp_truncate", "pcg_solve",
                 "fc_dgemm", "fc_last_kernel_stats", "fc_kernel_launches", "fracop_apply_truncate", "fc_orthonormalize",
-                "fc_profile_gemm", "fc_syev", "op_get_precond_basis", "op_set_precond_basis", "state_recover", "op_build_spectral_sinc"]
+                "fc_profile_gemm", "fc_syev", "op_get_precond_basis", "op_set_precond_basis", "state_recover", "op_build_spectral_sinc",
+                "sl_setup_2d", "op_get_spectral_2d", "op_set_spectral_2d", "fracop_apply_2d", "cp_dot_2d",
+                "cp_truncate_2d", "pcg_solve_2d"]
 
 
 def load_library(path: str = LIB_PATH) -> C.CDLL:
@@ -102,6 +109,12 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "op_get_precond_basis": ([P, I, P, P], I), "op_set_precond_basis": ([P, I, P, P], I),
         "state_recover": ([P, cpp, D, cpp, C.POINTER(fc_trunc_info)], I),
         "op_build_spectral_sinc": ([P, I, D], I),
+        "sl_setup_2d": ([P, I, P, C.POINTER(fc_params)], I),
+        "op_get_spectral_2d": ([P, I, C.POINTER(fc_lr2)], I), "op_set_spectral_2d": ([P, I, C.POINTER(fc_lr2)], I),
+        "fracop_apply_2d": ([P, I, C.POINTER(fc_lr2), C.POINTER(fc_lr2)], I),
+        "cp_dot_2d": ([P, C.POINTER(fc_lr2), C.POINTER(fc_lr2), C.POINTER(D)], I),
+        "cp_truncate_2d": ([P, C.POINTER(fc_lr2), D, C.POINTER(fc_lr2), C.POINTER(I)], I),
+        "pcg_solve_2d": ([P, C.POINTER(fc_lr2), C.POINTER(fc_params), C.POINTER(fc_lr2), C.POINTER(fc_pcg_report)], I),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -144,6 +157,41 @@ class DeviceCP:
     def struct(self) -> fc_cp:
         s = fc_cp()
         for l in range(3):
+            s.n[l] = self.n
+            s.U[l] = self.U[l].data_ptr()
+            s.ld[l] = self.n
+        s.rank, s.cap, s.w = self.rank, self.cap, self.w.data_ptr()
+        return s
+
+
+class DeviceLR2:
+    """A 2D low-rank matrix in device memory (fc_lr2): w (cap,), U[l] stored (cap, n) row-major =
+    n x cap column-major with ld = n."""
+
+    def __init__(self, n: int, cap: int, rank: int = 0, device="cuda"):
+        import torch
+        self.n, self.cap, self.rank = n, max(cap, 1), rank
+        self.w = torch.zeros(self.cap, dtype=torch.float64, device=device)
+        self.U = [torch.zeros(self.cap, n, dtype=torch.float64, device=device) for _ in range(2)]
+
+    @classmethod
+    def from_numpy(cls, w, U, cap=None, device="cuda"):
+        import torch
+        R = int(np.asarray(w).size)
+        n = U[0].shape[0]
+        x = cls(n, cap if cap is not None else R, R, device)
+        x.w[:R] = torch.as_tensor(np.asarray(w, dtype=np.float64), device=device)
+        for l in range(2):
+            x.U[l][:R] = torch.as_tensor(np.ascontiguousarray(np.asarray(U[l], dtype=np.float64).T), device=device)
+        return x
+
+    def to_numpy(self):
+        R = self.rank
+        return (self.w[:R].cpu().numpy().copy(), [self.U[l][:R].cpu().numpy().T.copy() for l in range(2)])
+
+    def struct(self) -> fc_lr2:
+        s = fc_lr2()
+        for l in range(2):
             s.n[l] = self.n
             s.U[l] = self.U[l].data_ptr()
             s.ld[l] = self.n
@@ -322,6 +370,75 @@ class Context:
             bs, us = b.struct(), u.struct()
             rc = self.lib.pcg_solve(self.h, C.byref(bs), C.byref(params), C.byref(us), C.byref(rep))
             if rc == -3 and us.rank > u.cap:        # the solution's rank exceeds u.cap: re-run
+                cap = us.rank
+                continue
+            self._check(rc, ok=(0, 1, 2))
+            u.rank = us.rank
+            return u, rep.as_dict(), rc
+
+    # ---- 2D variant ----
+    def sl_setup_2d(self, n, a_mid, params: fc_params):
+        a = np.ascontiguousarray(np.asarray(a_mid, dtype=np.float64).reshape(2, n + 1))
+        self._check(self.lib.sl_setup_2d(self.h, n, a.ctypes.data, C.byref(params)))
+        self.n = n
+
+    def op_get_spectral_2d(self, which, cap: int = 128) -> DeviceLR2:
+        while True:
+            y = DeviceLR2(self.n, cap)
+            s = y.struct()
+            rc = self.lib.op_get_spectral_2d(self.h, which, C.byref(s))
+            if rc == -3 and s.rank > cap:
+                cap = s.rank
+                continue
+            self._check(rc)
+            y.rank = s.rank
+            return y
+
+    def op_set_spectral_2d(self, which, x: DeviceLR2):
+        s = x.struct()
+        self._check(self.lib.op_set_spectral_2d(self.h, which, C.byref(s)))
+
+    def fracop_apply_2d(self, which, x: DeviceLR2, cap: int | None = None) -> DeviceLR2:
+        cap = cap if cap is not None else 64 * max(x.rank, 1)
+        while True:
+            y = DeviceLR2(self.n, cap)
+            xs, ys = x.struct(), y.struct()
+            rc = self.lib.fracop_apply_2d(self.h, which, C.byref(xs), C.byref(ys))
+            if rc == -3 and ys.rank > cap:
+                cap = ys.rank
+                continue
+            self._check(rc)
+            y.rank = ys.rank
+            return y
+
+    def cp_dot_2d(self, x: DeviceLR2, y: DeviceLR2) -> float:
+        out = C.c_double()
+        xs, ys = x.struct(), y.struct()
+        self._check(self.lib.cp_dot_2d(self.h, C.byref(xs), C.byref(ys), C.byref(out)))
+        return out.value
+
+    def cp_truncate_2d(self, x: DeviceLR2, eps: float, cap: int | None = None):
+        cap = cap if cap is not None else max(x.rank, 16)
+        while True:
+            y = DeviceLR2(self.n, cap)
+            r = C.c_int()
+            xs, ys = x.struct(), y.struct()
+            rc = self.lib.cp_truncate_2d(self.h, C.byref(xs), C.c_double(eps), C.byref(ys), C.byref(r))
+            if rc == -3 and r.value > cap:
+                cap = r.value
+                continue
+            self._check(rc)
+            y.rank = ys.rank
+            return y
+
+    def pcg_solve_2d(self, b: DeviceLR2, params: fc_params, cap: int = 1024, u: DeviceLR2 | None = None):
+        while True:
+            if u is None or u.cap < cap:
+                u = DeviceLR2(self.n, cap)
+            rep = fc_pcg_report()
+            bs, us = b.struct(), u.struct()
+            rc = self.lib.pcg_solve_2d(self.h, C.byref(bs), C.byref(params), C.byref(us), C.byref(rep))
+            if rc == -3 and us.rank > u.cap:
                 cap = us.rank
                 continue
             self._check(rc, ok=(0, 1, 2))

@@ -315,6 +315,9 @@ int fc_destroy(fc_ctx c) {
   for (auto& s : c->spec) {
     s.w.release(); s.U.release(); s.W.release(); s.E.release();
   }
+  for (auto& s : c->spec2) {
+    s.w.release(); s.U.release();
+  }
   if (c->e0) cudaEventDestroy(c->e0);
   if (c->e1) cudaEventDestroy(c->e1);
   delete c;

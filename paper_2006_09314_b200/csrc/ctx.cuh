@@ -20,6 +20,16 @@ struct SpecCP {
   double* Ul(int n, int l) const { return U.p + (size_t)l * n * r; }
 };
 
+// 2D variant: low-rank factorisation D2 ~ sum_k w_k a_k b_k^T of
+// D2[i, j] = f(lam1_i + lam2_j) over the context's mode-0 / mode-1 eigenvalues
+struct Spec2 {
+  int r = 0;
+  fc::DBuf w;         // [r]
+  fc::DBuf U;         // 2 blocks n x r (mode l at U.p + l*n*r), unit columns
+  bool valid = false;
+  double* Ul(int n, int l) const { return U.p + (size_t)l * n * r; }
+};
+
 struct fc_ctx_s {
   cudaStream_t st = nullptr;
   cudaStream_t st2 = nullptr;   // side stream of pcg_solve (the X update runs concurrently)
@@ -34,6 +44,7 @@ struct fc_ctx_s {
   fc::DBuf VA;        // ... and the DST-I basis, 3 x n x n
   bool have_A[3] = {false, false, false};
   SpecCP spec[4];
+  Spec2 spec2[2];     // 2D: FC_F, FC_G
   std::string err;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   double k_flops = 0, k_bytes = 0;

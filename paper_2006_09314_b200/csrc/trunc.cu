@@ -676,6 +676,53 @@ int read_int(const int* d, cudaStream_t st) {
 }  // namespace
 
 // ---------------------------------------------------------------------------------------
+// Batched SVD of ns column-major ra x rb matrices (S + nu*ra*rb): k = min(ra, rb) triples per
+// matrix sorted by s descending (s[nu*k + m], Ua[nu*ra*k + m*ra + x], Vb[nu*rb*k + m*rb + y]).
+// QR-preconditioned one-sided Jacobi when the working set fits shared memory, else the plain
+// one-sided Jacobi (shared memory, or a per-matrix global workspace).
+void small_svd(cudaStream_t st, int ra, int rb, int ns, const double* S, double* sv, double* Ua, double* Vb) {
+  require(std::max(ra, rb) <= kSliceMax, FC_ERR_CAPACITY, "small SVD: dimension above 1024");
+  if (ns == 0 || ra == 0 || rb == 0) return;
+  const int k = std::min(ra, rb);
+  Scratch s(st);
+  const int rows = std::max(ra, rb), cols = k;
+  size_t smem = ((size_t)rows * cols + (size_t)cols * cols + cols) * 8 + (size_t)cols * 4 + 16;
+  double* gws = nullptr;
+  if (smem > kSliceSmem) {
+    gws = s.alloc<double>((size_t)ns * ((size_t)rows * cols + (size_t)cols * cols));
+    smem = (size_t)cols * 12 + 16;
+  }
+  static bool attr = false;
+  if (!attr) {
+    FC_CUDA_TRY(cudaFuncSetAttribute(slice_svd_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)kSliceSmem));
+    attr = true;
+  }
+  static const bool no_qr = getenv("FC_SLICE_NO_QR") != nullptr;
+  const size_t qsm = slice_qrj_smem(rows, cols);
+  if (!no_qr && qsm <= kSliceSmem) {
+    static bool qattr = false;
+    if (!qattr) {
+      FC_CUDA_TRY(cudaFuncSetAttribute(slice_svd_qrj_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)kSliceSmem));
+      qattr = true;
+    }
+    slice_svd_qrj_kernel<<<ns, 512, qsm, st>>>(ra, rb, S, sv, Ua, Vb);
+  } else if (gws) {
+    slice_svd_kernel<false><<<ns, 512, smem, st>>>(ra, rb, S, sv, Ua, Vb, gws);
+  } else {
+    slice_svd_kernel<true><<<ns, 512, smem, st>>>(ra, rb, S, sv, Ua, Vb, nullptr);
+  }
+  FC_CHECK_LAUNCH();
+  if (getenv("FC_TRACE")) {
+    int sw = 0, zero = 0;
+    FC_CUDA_TRY(cudaMemcpyFromSymbolAsync(&sw, g_slice_sweeps_max, sizeof(int), 0, cudaMemcpyDeviceToHost, st));
+    FC_CUDA_TRY(cudaMemcpyToSymbolAsync(g_slice_sweeps_max, &zero, sizeof(int), 0, cudaMemcpyHostToDevice, st));
+    FC_CUDA_TRY(cudaStreamSynchronize(st));
+    fprintf(stderr, "[fc svd] %d matrices of %d x %d: max sweeps %d\n", ns, ra, rb, sw);
+  }
+}
+
 TT tucker_to_canonical(fc_ctx c, const double* core, const int r[3], double* const Z[3], int n, double eps,
                        int keep, int rank_cap, TruncStats* stats) {
   cudaStream_t st = stream_of(c);
@@ -698,42 +745,7 @@ TT tucker_to_canonical(fc_ctx c, const double* core, const int r[3], double* con
   int* rdev = s.alloc<int>(2);
   extract_slices_kernel<<<blocks_for((long long)ra * rb * rc), 256, 0, st>>>(core, r[0], r[1], r[2], ma, mb, mc, S);
   FC_CHECK_LAUNCH();
-  const int rows = std::max(ra, rb), cols = k;
-  size_t smem = ((size_t)rows * cols + (size_t)cols * cols + cols) * 8 + (size_t)cols * 4 + 16;
-  double* gws = nullptr;
-  if (smem > kSliceSmem) {
-    gws = s.alloc<double>((size_t)rc * ((size_t)rows * cols + (size_t)cols * cols));
-    smem = (size_t)cols * 12 + 16;
-  }
-  static bool attr = false;
-  if (!attr) {
-    FC_CUDA_TRY(cudaFuncSetAttribute(slice_svd_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)kSliceSmem));
-    attr = true;
-  }
-  static const bool no_qr = getenv("FC_SLICE_NO_QR") != nullptr;
-  const size_t qsm = slice_qrj_smem(rows, cols);
-  if (!no_qr && qsm <= kSliceSmem) {
-    static bool qattr = false;
-    if (!qattr) {
-      FC_CUDA_TRY(cudaFuncSetAttribute(slice_svd_qrj_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)kSliceSmem));
-      qattr = true;
-    }
-    slice_svd_qrj_kernel<<<rc, 512, qsm, st>>>(ra, rb, S, sv, Ua, Vb);
-  } else if (gws) {
-    slice_svd_kernel<false><<<rc, 512, smem, st>>>(ra, rb, S, sv, Ua, Vb, gws);
-  } else {
-    slice_svd_kernel<true><<<rc, 512, smem, st>>>(ra, rb, S, sv, Ua, Vb, nullptr);
-  }
-  FC_CHECK_LAUNCH();
-  if (getenv("FC_TRACE")) {
-    int sw = 0, zero = 0;
-    FC_CUDA_TRY(cudaMemcpyFromSymbolAsync(&sw, g_slice_sweeps_max, sizeof(int), 0, cudaMemcpyDeviceToHost, st));
-    FC_CUDA_TRY(cudaMemcpyToSymbolAsync(g_slice_sweeps_max, &zero, sizeof(int), 0, cudaMemcpyHostToDevice, st));
-    FC_CUDA_TRY(cudaStreamSynchronize(st));
-    fprintf(stderr, "[fc t2c] slices %d of %d x %d: max sweeps %d\n", rc, ra, rb, sw);
-  }
+  small_svd(st, ra, rb, rc, S, sv, Ua, Vb);
   pool_rank_kernel<<<cdiv(K, 256), 256, 0, st>>>(K, sv, s2s, keys);
   FC_CHECK_LAUNCH();
   pool_energy_kernel<<<1, 1024, 0, st>>>(K, sv, energy);

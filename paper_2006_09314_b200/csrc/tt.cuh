@@ -76,6 +76,9 @@ void tt_compute_core(cudaStream_t st, TT& x);
 // eps-cut (keep <= 0) or top-`keep` triples.  Used by the truncation and the spectral CP.
 TT tucker_to_canonical(fc_ctx c, const double* core, const int r[3], double* const Z[3], int n, double eps,
                        int keep, int rank_cap, TruncStats* stats);
+// batched SVD of ns column-major ra x rb matrices (max(ra, rb) <= 1024): k = min(ra, rb) triples
+// per matrix sorted by s descending: s[nu*k + m], Ua[nu*ra*k + m*ra + x], Vb[nu*rb*k + m*rb + y]
+void small_svd(cudaStream_t st, int ra, int rb, int ns, const double* S, double* sv, double* Ua, double* Vb);
 // x + a*y (concatenation; bases concatenated, coefficients block-diagonal)
 TT tt_axpy(cudaStream_t st, const TT& x, double a, const TT& y);
 // <x, y>  (result in device scalar `out`, and returned on the host when sync)
