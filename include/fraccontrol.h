@@ -174,6 +174,14 @@ int cp_axpy(fc_ctx ctx, const fc_cp* x, double a, const fc_cp* y, fc_cp* z);
  * info may be NULL.  x and y must not alias. */
 int cp_truncate(fc_ctx ctx, const fc_cp* x, double eps, fc_cp* y, fc_trunc_info* info);
 
+/* cp_truncate_als: cp_truncate with the canonical-to-Tucker ALS refinement
+ * [P:1060, P:1792-1803] (the algorithm of the cited C2T): after the RHOSVD (ranks r_l by the
+ * (eps/2)^2 rule) `sweeps` HOOI sweeps over the modes (ranks fixed) replace each basis Z_l by the
+ * leading r_l left singular vectors of the mode-l unfolding of x x_{m != l} Z_m^T, then core and
+ * T2C as cp_truncate (reading ALS).  sweeps = 0 is cp_truncate.  Same output / info /
+ * CAPACITY rules; the projected unfolding must stay below 2^28 entries (else CAPACITY). */
+int cp_truncate_als(fc_ctx ctx, const fc_cp* x, double eps, int sweeps, fc_cp* y, fc_trunc_info* info);
+
 /* fracop_apply_truncate: y = trunc(F(A) x, eps) fused (S5-S13): the
  * Khatri-Rao Hadamard product is formed in the eigenbasis on a reduced basis
  * [w_a (.) V^T q_b] (w_a: basis of the spectral CP's factors, q_b: of x's), the RHOSVD runs

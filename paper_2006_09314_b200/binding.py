@@ -76,7 +76,7 @@ ENTRY_POINTS = ["fc_create", "fc_destroy", "fc_last_error", "fc_set_stream", "sl
                 "fc_dgemm", "fc_last_kernel_stats", "fc_kernel_launches", "fracop_apply_truncate", "fc_orthonormalize",
                 "fc_profile_gemm", "fc_syev", "op_get_precond_basis", "op_set_precond_basis", "state_recover", "op_build_spectral_sinc",
                 "sl_setup_2d", "op_get_spectral_2d", "op_set_spectral_2d", "fracop_apply_2d", "cp_dot_2d",
-                "cp_truncate_2d", "pcg_solve_2d"]
+                "cp_truncate_2d", "pcg_solve_2d", "cp_truncate_als"]
 
 
 def load_library(path: str = LIB_PATH) -> C.CDLL:
@@ -109,6 +109,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "op_get_precond_basis": ([P, I, P, P], I), "op_set_precond_basis": ([P, I, P, P], I),
         "state_recover": ([P, cpp, D, cpp, C.POINTER(fc_trunc_info)], I),
         "op_build_spectral_sinc": ([P, I, D], I),
+        "cp_truncate_als": ([P, cpp, D, I, cpp, C.POINTER(fc_trunc_info)], I),
         "sl_setup_2d": ([P, I, P, C.POINTER(fc_params)], I),
         "op_get_spectral_2d": ([P, I, C.POINTER(fc_lr2)], I), "op_set_spectral_2d": ([P, I, C.POINTER(fc_lr2)], I),
         "fracop_apply_2d": ([P, I, C.POINTER(fc_lr2), C.POINTER(fc_lr2)], I),
@@ -322,6 +323,20 @@ class Context:
             info = fc_trunc_info()
             xs, ys = x.struct(), y.struct()
             rc = self.lib.cp_truncate(self.h, C.byref(xs), C.c_double(eps), C.byref(ys), C.byref(info))
+            if rc == -3 and info.required_rank > cap:
+                cap = info.required_rank
+                continue
+            self._check(rc)
+            y.rank = ys.rank
+            return y, info
+
+    def cp_truncate_als(self, x: DeviceCP, eps: float, sweeps: int = 2, cap: int | None = None):
+        cap = cap if cap is not None else max(4 * x.rank, 64)
+        while True:
+            y = DeviceCP(self.n, cap)
+            info = fc_trunc_info()
+            xs, ys = x.struct(), y.struct()
+            rc = self.lib.cp_truncate_als(self.h, C.byref(xs), C.c_double(eps), sweeps, C.byref(ys), C.byref(info))
             if rc == -3 and info.required_rank > cap:
                 cap = info.required_rank
                 continue

@@ -322,6 +322,31 @@ int cp_truncate(fc_ctx c, const fc_cp* x, double eps, fc_cp* y, fc_trunc_info* i
   });
 }
 
+int cp_truncate_als(fc_ctx c, const fc_cp* x, double eps, int sweeps, fc_cp* y, fc_trunc_info* info) {
+  return guard2(c, [&]() {
+    check_cp2(c, x, "x");
+    check_cp2(c, y, "y");
+    require(eps > 0 && std::isfinite(eps), FC_ERR_INVALID_ARG, "eps must be > 0");
+    require(sweeps >= 0 && sweeps <= 100, FC_ERR_INVALID_ARG, "sweeps in [0, 100]");
+    TruncStats S;
+    TT xt = tt_from_cp(c->st, c->n, x->rank, x->w, x->U, x->ld);
+    TT out;
+    try {
+      out = truncate_tt(c, xt, eps, 0, &S, nullptr, sweeps);
+    } catch (const Error& e) {
+      fill_info(info, S);
+      if (info && e.code == FC_ERR_CAPACITY) info->required_rank = S.out_rank;
+      throw;
+    }
+    fill_info(info, S);
+    if (y->cap < out.R) {
+      if (info) info->required_rank = out.R;
+    }
+    store_tt(c, out, y);
+    return FC_OK;
+  });
+}
+
 int fracop_apply_truncate(fc_ctx c, int which, const fc_cp* x, double eps, fc_cp* y, fc_trunc_info* info) {
   return guard2(c, [&]() {
     require(which >= 0 && which < 4, FC_ERR_INVALID_ARG, "which");

@@ -836,7 +836,8 @@ int struct_chunk(const StructuredS* ss) {
   return (int)std::max<size_t>(1, std::min<size_t>((size_t)ss->r, kStructChunk / per));
 }
 
-TT truncate_tt(fc_ctx c, const TT& xin, double eps, int rank_cap, TruncStats* stats, const StructuredS* ss) {
+TT truncate_tt(fc_ctx c, const TT& xin, double eps, int rank_cap, TruncStats* stats, const StructuredS* ss,
+               int als_sweeps) {
   cudaStream_t st = stream_of(c);
   const int n = xin.n, R = xin.R;
   TruncStats local;
@@ -1205,6 +1206,56 @@ TT truncate_tt(fc_ctx c, const TT& xin, double eps, int rank_cap, TruncStats* st
     TT z;
     z.n = n;
     return z;
+  }
+  // ---- 4b. C2T-ALS refinement (oracle/als.py): HOOI sweeps over the modes
+  // with the ranks r_l fixed.  In the basis coordinates the CP is x = sum_t xi_t (x)_l Cs_l[:, t]
+  // with Cs_l = Co_l diag(1/n_l); for mode l, A_m = Y_m^T Cs_m (m != l) and
+  // W_l^T = KR(A_a, A_b) Cs_l^T ((r_a r_b) x q_l; KR weighted by xi, chunked over the terms as the
+  // core below); Y_l <- the top r_l eigenvectors of W_l W_l^T (batched syev).  CP route only.
+  if (als_sweeps > 0 && !ss) {
+    double* Cs[3];
+    for (int l = 0; l < 3; ++l) {
+      Cs[l] = s.alloc<double>((size_t)q[l] * R);
+      scale_cols_kernel<<<blocks_for((long long)q[l] * R), 256, 0, st>>>(q[l], R, Co[l], inv[l], Cs[l]);
+      FC_CHECK_LAUNCH();
+    }
+    for (int sweep = 0; sweep < als_sweeps; ++sweep)
+      for (int l = 0; l < 3; ++l) {
+        const int a = l == 0 ? 1 : 0, b = l == 2 ? 1 : 2;
+        Scratch sa(st);
+        double* A[2];
+        const int ab[2] = {a, b};
+        for (int i = 0; i < 2; ++i) {
+          const int m = ab[i];
+          A[i] = sa.alloc<double>((size_t)r[m] * R);
+          dgemm(st, 1, 0, r[m], R, q[m], 1.0, Y[m], q[m], Cs[m], q[m], 0.0, A[i], r[m]);
+        }
+        const size_t rab = (size_t)r[a] * r[b];
+        require(rab * q[l] <= ((size_t)1 << 28), FC_ERR_CAPACITY, "C2T-ALS: projected unfolding above 2^28 entries");
+        double* Wt = sa.zeros<double>(rab * q[l]);
+        const int chunk = (int)std::max<size_t>(1, std::min<size_t>((size_t)R, (size_t)(1 << 27) / std::max<size_t>(rab, 1)));
+        double* KR = sa.alloc<double>(rab * chunk);
+        for (int t0 = 0; t0 < R; t0 += chunk) {
+          const int m = std::min(chunk, R - t0);
+          kr12_kernel<<<blocks_for((long long)rab * m), 256, 0, st>>>(r[a], r[b], m, xi + t0, A[0] + (size_t)t0 * r[a],
+                                                                       A[1] + (size_t)t0 * r[b], KR);
+          FC_CHECK_LAUNCH();
+          const int tiles = cdiv((long long)rab, 64) * cdiv(q[l], 64);
+          dgemm(st, 0, 1, (int)rab, q[l], m, 1.0, KR, (int)rab, Cs[l] + (size_t)t0 * q[l], q[l], 1.0, Wt, (int)rab,
+                std::max(1, std::min(cdiv(m, 64), std::max(1, 296 / std::max(tiles, 1)))));
+        }
+        double* Gw = sa.zeros<double>((size_t)q[l] * q[l]);
+        dgemm(st, 1, 0, q[l], q[l], (int)rab, 1.0, Wt, (int)rab, Wt, (int)rab, 1.0, Gw, q[l],
+              std::max(1, std::min(cdiv((long long)rab, 256), 16)));
+        SyevBatch gb;
+        double* mu = sa.alloc<double>(q[l]);
+        int* rd = sa.alloc<int>(1);
+        FC_CUDA_TRY(cudaMemcpyAsync(rd, &r[l], sizeof(int), cudaMemcpyHostToDevice, st));
+        gb.e[gb.nb++] = SyevEntry{q[l], Gw, q[l], sa.alloc<double>(q[l]), sa.alloc<double>(q[l]), mu, Y[l], q[l], rd,
+                                  sa.alloc<double>((size_t)6 * q[l] * q[l])};
+        syev_values(gb, st);
+        syev_vectors(gb, q[l], st, &r[l]);
+      }
   }
   // ---- 5. Z_l = Qo_l Y_r -----------------------------------------------------------------
   double* Z[3];

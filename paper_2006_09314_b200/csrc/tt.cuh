@@ -68,8 +68,9 @@ struct TruncStats {
 
 // RHOSVD -> core -> T2C (S11-S13).  Output: orthonormal Q (n x r_l), orthogonal CP terms.
 // rank_cap > 0: output rank limit (FC_ERR_CAPACITY with stats.out_rank = required).
+// als_sweeps > 0: C2T-ALS refinement (HOOI sweeps with the RHOSVD ranks) before the core (CP route).
 TT truncate_tt(fc_ctx c, const TT& x, double eps, int rank_cap, TruncStats* stats,
-               const StructuredS* ss = nullptr);
+               const StructuredS* ss = nullptr, int als_sweeps = 0);
 // Tucker core of a TT from its CP coefficients (sum_t w_t (x)_l C_l[:, t]), chunked over terms
 void tt_compute_core(cudaStream_t st, TT& x);
 // T2C of a dense core (r1 x r2 x r3, column-major) with bases Z (n x r_l, orthonormal):
