@@ -661,6 +661,20 @@ __global__ void accumulate_core_kernel(int nb, int r0, int r1, int r2, const dou
   }
 }
 
+// B^T: out[j + i*cols] = in[i + j*rows]   (in rows x cols, column-major)
+__global__ void transpose_kernel(int rows, int cols, const double* __restrict__ in, double* out) {
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < (long long)rows * cols;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(idx % rows), j = (int)(idx / rows);
+    out[j + (size_t)i * cols] = in[idx];
+  }
+}
+
+__global__ void square_into_kernel(int k, const double* __restrict__ s, double* s2) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < k) s2[i] = s[i] * s[i];
+}
+
 int blocks_for(long long total) {
   long long b = (total + 255) / 256;
   return (int)std::min<long long>(std::max<long long>(b, 1), 148 * 8);
@@ -827,6 +841,9 @@ void tt_compute_core(cudaStream_t st, TT& x) {
 constexpr double kBasisTol = 1e-10;
 // Gram eigenvalue noise per direction, in units of eps_mach * lam_max (refined cut below it)
 constexpr double kNoise = 1.0;
+// K13: below this eps the CP route takes the SVD of the side matrix itself (FC_TRUNC_QR=0/1)
+constexpr double kQrEps = 1e-6;
+constexpr double kQrBasisTol = 1e-14;
 
 // spectral terms per chunk of the structured norm / Gram pass: t x (Rx * chunk) <= 2^27 doubles
 constexpr size_t kStructChunk = (size_t)1 << 27;
@@ -1065,16 +1082,68 @@ TT truncate_tt(fc_ctx c, const TT& xin, double eps, int rank_cap, TruncStats* st
     gemm(m, st);
   }
   // ---- 4. eigen of M: s^2 descending, rank cut (tails from the small end), leading vectors ----
-  SyevBatch eb;
+  // K13 (eps < kQrEps on the CP route): the SVD of the side matrix B_l itself
+  // instead of the eigen-decomposition of B_l B_l^T, so the singular values carry ~eps_mach
+  // relative error instead of ~eps_mach * s_max^2 (no squaring floor).  B_l^T (R x q) gets a
+  // rank-revealing orthonormal basis Qb (blocked Gram-Schmidt, the QR step), Cb = Qb^T B_l^T
+  // (qb x q) its one-sided Jacobi SVD (QR-preconditioned): B_l = Vc S (Qb Uc)^T, so s^2 and the
+  // left vectors Vc take the place of the Gram's eigenpairs.  R <= q: the SVD of B_l directly.
   double* lam[3];
   double* Y[3];
   int* rl = s.alloc<int>(4);
   double* margins = s.alloc<double>(3);
-  int maxq = 0;
+  static const int qr_env = getenv("FC_TRUNC_QR") ? atoi(getenv("FC_TRUNC_QR")) : -1;
+  bool qr[3] = {false, false, false};
   for (int l = 0; l < 3; ++l) {
     const int ql = q[l];
     lam[l] = s.alloc<double>(ql);
     Y[l] = s.alloc<double>((size_t)ql * ql);
+    qr[l] = !ss && ql <= kSliceMax && (qr_env == 1 || (qr_env != 0 && eps < kQrEps)) &&
+            (R <= ql || R <= 2048);   // the transposed side matrix stays on the cluster BCGS
+  }
+  for (int l = 0; l < 3; ++l) {
+    if (!qr[l]) continue;
+    const int ql = q[l];
+    Scratch sq(st);
+    FC_CUDA_TRY(cudaMemsetAsync(Y[l], 0, (size_t)ql * ql * 8, st));
+    FC_CUDA_TRY(cudaMemsetAsync(lam[l], 0, (size_t)ql * 8, st));
+    double* sv;
+    int k;
+    if (R <= ql) {
+      k = R;
+      sv = sq.alloc<double>(k);
+      double* Vb = sq.alloc<double>((size_t)R * k);
+      small_svd(st, ql, R, 1, Bm[l], sv, Y[l], Vb);                   // left vectors straight into Y
+    } else {
+      double* Bt = sq.alloc<double>((size_t)R * ql);
+      transpose_kernel<<<blocks_for((long long)R * ql), 256, 0, st>>>(ql, R, Bm[l], Bt);
+      FC_CHECK_LAUNCH();
+      double* Bt2 = sq.alloc<double>((size_t)R * ql);
+      FC_CUDA_TRY(cudaMemcpyAsync(Bt2, Bt, (size_t)R * ql * 8, cudaMemcpyDeviceToDevice, st));
+      BcgsBatch pb;
+      int* kd = sq.zeros<int>(1);
+      double* Qb = sq.alloc<double>((size_t)R * ql);
+      pb.e[pb.nb++] = BcgsEntry{R, ql, Bt2, R, Qb, R, ql, kd, sq.alloc<double>(ql),
+                                sq.alloc<double>((size_t)ql * kBcgsW), kQrBasisTol};
+      bcgs(pb, st);
+      const int qb = std::max(read_int(kd, st), 1);
+      double* Cb = sq.zeros<double>((size_t)qb * ql);
+      dgemm(st, 1, 0, qb, ql, R, 1.0, Qb, R, Bt, R, 1.0, Cb, qb, std::max(1, std::min(cdiv(R, 256), 16)));
+      k = std::min(qb, ql);
+      sv = sq.alloc<double>(k);
+      double* Uc = sq.alloc<double>((size_t)qb * k);
+      small_svd(st, qb, ql, 1, Cb, sv, Uc, Y[l]);                      // B's left vectors = Vc
+    }
+    square_into_kernel<<<cdiv(k, 256), 256, 0, st>>>(k, sv, lam[l]);
+    FC_CHECK_LAUNCH();
+  }
+  SyevBatch eb;
+  int ebmap[3] = {-1, -1, -1};
+  int maxq = 0;
+  for (int l = 0; l < 3; ++l) {
+    if (qr[l]) continue;
+    const int ql = q[l];
+    ebmap[l] = eb.nb;
     eb.e[eb.nb++] = SyevEntry{ql, M[l], ql, s.alloc<double>(ql), s.alloc<double>(ql), lam[l], Y[l], ql, rl + l,
                               s.alloc<double>((size_t)6 * ql * ql)};
     maxq = std::max(maxq, ql);
@@ -1093,10 +1162,11 @@ TT truncate_tt(fc_ctx c, const TT& xin, double eps, int rank_cap, TruncStats* st
   // the eigenvalue tails cannot decide the cut (reading A11').  Then all eigenvectors
   // are computed; the eigenvalues above the noise level are kept, and the noise subspace Y_ns is
   // re-diagonalised from the data: G_ns = C C^T with C = Y_ns^T B formed explicitly (its rounding
-  // is ~eps_mach ||C||^2, ~1e-32 of the energy), its eigenpairs replace the noisy ones.
+  // is ~eps_mach ||C||^2, ~1e-32 of the energy), its eigenpairs replace the noisy ones.  (Modes on
+  // the K13 path have no such floor.)
   bool refine[3] = {false, false, false}, any_refine = false;
   for (int l = 0; l < 3; ++l) {
-    refine[l] = 0.25 * eps * eps * S.energy < kNoise * q[l] * 2.220446049250313e-16 * lam0[l] && q[l] > 1;
+    refine[l] = !qr[l] && 0.25 * eps * eps * S.energy < kNoise * q[l] * 2.220446049250313e-16 * lam0[l] && q[l] > 1;
     any_refine |= refine[l];
   }
   if (any_refine) {
@@ -1105,10 +1175,10 @@ TT truncate_tt(fc_ctx c, const TT& xin, double eps, int rank_cap, TruncStats* st
       if (refine[l]) hr[l] = q[l];
     FC_CUDA_TRY(cudaMemcpyAsync(rl, hr, 3 * sizeof(int), cudaMemcpyHostToDevice, st));
   }
-  {
-    int hr[3] = {r[0], r[1], r[2]};
+  if (eb.nb) {
+    int hr[3] = {0, 0, 0};
     for (int l = 0; l < 3; ++l)
-      if (refine[l]) hr[l] = q[l];
+      if (ebmap[l] >= 0) hr[ebmap[l]] = refine[l] ? q[l] : r[l];
     syev_vectors(eb, maxq, st, hr);
   }
   if (any_refine) {

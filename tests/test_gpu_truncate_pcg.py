@@ -182,9 +182,10 @@ def check_rank_history(rep, rep_ref):
 
 @pytest.mark.parametrize("n,R,eps", [(48, 5, 1e-8), (40, 4, 1e-9), (64, 3, 1e-8)])
 def test_truncate_small_eps_refined_cut(lib, n, R, eps):
-    """Cuts below the Gram noise level ((eps/2)^2 E < k eps_mach lam_max), reading A11': the
-    eigenvalues above the noise level are kept, the noise subspace Y_ns is re-diagonalised from
-    the data (Gram of C = Y_ns^T B, rounding ~1e-32 of the energy).  Tucker ranks as the oracle's
+    """Cuts below the Gram noise level ((eps/2)^2 E < k eps_mach lam_max): cp_truncate (CP route)
+    takes the K13 path for eps < 1e-6 (SVD of the side matrix itself: rank-revealing basis of
+    B^T + QR-preconditioned Jacobi, no squaring floor); apply outputs (structured route) take
+    reading A11' (noise subspace re-diagonalised from the data).  Tucker ranks as the oracle's
     exact SVD cut (+-1 in the A23 band), result within 2 eps."""
     from paper_2006_09314_b200.binding import DeviceCP
     p = make_problem("C1", n=n)
@@ -197,4 +198,28 @@ def test_truncate_small_eps_refined_cut(lib, n, R, eps):
     y, info = ctx.cp_truncate(DeviceCP.from_numpy(x.w, x.U), eps)
     for l in range(3):
         assert abs(info.tucker_rank[l] - info_o["tucker_rank"][l]) <= 1
+    assert reldiff(_cp(y), ref) <= 2 * eps
+
+
+@pytest.mark.parametrize("eps", [1e-9, 1e-10])
+def test_truncate_k13_below_gram_floor(lib, eps):
+    """K13 (SVD of the side matrix, no squaring): a CP whose mode spectra decay geometrically
+    over 14 decades, cut at eps where the Gram eigenvalues (noise ~eps_mach s_max^2, i.e. a floor
+    of ~1e-8 relative in s) cannot see the cut.  Tucker ranks equal the oracle's exact-SVD cut
+    unless that cut is inside the A23 noise band; result within 2 eps."""
+    from paper_2006_09314_b200.binding import DeviceCP, make_params
+    n, R = 64, 48
+    rng = np.random.default_rng(21)
+    Q = [np.linalg.qr(rng.standard_normal((n, R)))[0] for _ in range(3)]
+    decay = 10.0 ** (-np.linspace(0, 14, R))
+    U = [Q[l] @ (np.diag(decay) @ rng.standard_normal((R, R))) for l in range(3)]
+    x = cpm.normalized(np.ones(R), U)
+    ctx = lib.context()
+    ctx.sl_setup(n, np.ones((3, n + 1)), make_params(0.5, 0.01, 1e-6))
+    info_o = {}
+    ref = truncate(x, eps, info_o)
+    y, info = ctx.cp_truncate(DeviceCP.from_numpy(x.w, x.U), eps)
+    marginal = min(info_o["margins"]) < 5e-3
+    for l in range(3):
+        assert abs(info.tucker_rank[l] - info_o["tucker_rank"][l]) <= (1 if marginal else 0), (l, marginal)
     assert reldiff(_cp(y), ref) <= 2 * eps
