@@ -1814,7 +1814,10 @@ void launch_tridiag_cluster(const SyevBatch& b, size_t smem, cudaStream_t st, in
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(CS, b.nb, 1);
-  cfg.blockDim = dim3(1024, 1, 1);
+  // 512 threads per CTA: the per-step block barriers dominate at these sizes (C4 solve 359 ms vs
+  // 365 ms with 1024; FC_TRI_THREADS overrides for diagnostics)
+  static const int thr = getenv("FC_TRI_THREADS") ? atoi(getenv("FC_TRI_THREADS")) : 512;
+  cfg.blockDim = dim3(thr, 1, 1);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute at[1];
@@ -1873,7 +1876,8 @@ void syev_values(const SyevBatch& b, cudaStream_t st) {
     attr = true;
   }
   if (any_p) {
-    tridiag_packed_kernel<<<b.nb, 1024, smem_p, st>>>(b, maxP);
+    static const int pthr = getenv("FC_TRI_PACKED_THREADS") ? atoi(getenv("FC_TRI_PACKED_THREADS")) : 1024;
+    tridiag_packed_kernel<<<b.nb, pthr, smem_p, st>>>(b, maxP);
     FC_CHECK_LAUNCH();
   }
   if (any_g) {
