@@ -115,6 +115,11 @@ struct GemmBatch {
   const double* colscale;
   // strides between the GemmArgs::rep repetitions of this entry (A, B, C, colscale, krU)
   long long sA = 0, sB = 0, sC = 0, sS = 0, sK = 0;
+  // optional device-side bounds read by the kernel: M_eff = min(M, *dynM), K_eff = min(K, *dynK)
+  // (rows / terms beyond them are known to be zero: the blocked Gram-Schmidt passes the number of
+  // accepted basis columns so that the unused, zero, columns of Q cost nothing)
+  const int* dynM = nullptr;
+  const int* dynK = nullptr;
 };
 // Generated A operand (transA = 0): A(m, k) = f((l1[m % n1] + l2[m / n1]) + l3[k]) with the
 // spectral function f of kind FC_F / FC_G / FC_POW_PLUS / FC_POW_MINUS [P:640-648, P:693].

@@ -2100,6 +2100,8 @@ void bcgs(const BcgsBatch& bin, cudaStream_t st) {
     }
   };
   BcgsBatch b = bin;
+  // projection GEMMs bounded by the device count of accepted columns (FC_BCGS_NO_DYNK: full j0)
+  static const bool dyn_k = getenv("FC_BCGS_NO_DYNK") == nullptr;
   static const bool trace = getenv("FC_TRACE") != nullptr;
   if (trace) {
     static bool reg = false;
@@ -2147,6 +2149,10 @@ void bcgs(const BcgsBatch& bin, cudaStream_t st) {
         FC_CUDA_TRY(cudaMemsetAsync(E.P, 0, (size_t)kup * W * 8, st));
         p.b[nb] = GemmBatch{kup, wb, E.n, E.Q, E.ldq, E.A + (size_t)j0 * E.lda, E.lda, E.P, kup, nullptr, 0, nullptr};
         u.b[nb] = GemmBatch{E.n, wb, kup, E.Q, E.ldq, E.P, kup, E.A + (size_t)j0 * E.lda, E.lda, nullptr, 0, nullptr};
+        if (dyn_k) {               // only the first *E.k columns of Q are nonzero
+          p.b[nb].dynM = E.k;
+          u.b[nb].dynK = E.k;
+        }
         ++nb;
       }
       p.nbatch = u.nbatch = nb;
@@ -2170,6 +2176,10 @@ void bcgs(const BcgsBatch& bin, cudaStream_t st) {
         FC_CUDA_TRY(cudaMemsetAsync(E.P, 0, (size_t)kup * W * 8, st));
         p.b[nb] = GemmBatch{kup, W, E.n, E.Q, E.ldq, E.Y, E.n, E.P, kup, nullptr, 0, nullptr};
         u.b[nb] = GemmBatch{E.n, W, kup, E.Q, E.ldq, E.P, kup, E.Y, E.n, nullptr, 0, nullptr};
+        if (dyn_k) {
+          p.b[nb].dynM = E.k;
+          u.b[nb].dynK = E.k;
+        }
         ++nb;
       }
       p.nbatch = u.nbatch = nb;

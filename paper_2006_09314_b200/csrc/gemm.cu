@@ -131,11 +131,14 @@ __global__ void __launch_bounds__(NT) dgemm_dmma_kernel(const __grid_constant__ 
   double* gC = g.C + (size_t)ri * g.sC;
   const double* gS = g.colscale ? g.colscale + (size_t)ri * g.sS : nullptr;
   const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
-  if (m0 >= g.M || n0 >= g.N) return;
+  const int Meff = g.dynM ? min(g.M, *g.dynM) : g.M;
+  const int Keff = g.dynK ? min(g.K, *g.dynK) : g.K;
+  if (m0 >= Meff || n0 >= g.N) return;
 
-  int kchunk = ((g.K + args.splitk - 1) / args.splitk + BK - 1) / BK * BK;
+  int kchunk = ((Keff + args.splitk - 1) / args.splitk + BK - 1) / BK * BK;
   const int kbeg = ks * kchunk;
-  const int kend = min(g.K, kbeg + kchunk);
+  const int kend = min(Keff, kbeg + kchunk);
+  if (args.splitk > 1 && kend <= kbeg) return;   // empty split: nothing to accumulate
   const int nk = kend > kbeg ? (kend - kbeg + BK - 1) / BK : 0;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -480,7 +483,18 @@ void gemm(const GemmArgs& a, cudaStream_t st) {
     }
   }
   double f = 0;
-  for (int i = 0; i < a.nbatch; ++i) f += 2.0 * a.rep * a.b[i].M * (double)a.b[i].N * a.b[i].K;
+  for (int i = 0; i < a.nbatch; ++i) {
+    // algorithmic flops of the work actually done: device-side bounds are read back (profiling only)
+    int M = a.b[i].M, K = a.b[i].K;
+    if (a.b[i].dynM || a.b[i].dynK) {
+      int d = 0;
+      FC_CUDA_TRY(cudaMemcpyAsync(&d, a.b[i].dynM ? a.b[i].dynM : a.b[i].dynK, sizeof(int), cudaMemcpyDeviceToHost, st));
+      FC_CUDA_TRY(cudaStreamSynchronize(st));
+      if (a.b[i].dynM) M = std::min(M, d);
+      else K = std::min(K, d);
+    }
+    f += 2.0 * a.rep * M * (double)a.b[i].N * K;
+  }
   static const bool trace = getenv("FC_GEMM_TRACE") != nullptr;
   if (trace) {
     char key[160];
@@ -510,7 +524,9 @@ static void gemm_dispatch(const GemmArgs& a, cudaStream_t st) {
     work += (long long)a.rep * a.b[i].M * a.b[i].N * a.b[i].K;
     minK = std::min(minK, a.b[i].K);
   }
-  if (a.gen.kind < 0 && maxM >= 256 && maxN >= 256 && minK >= 64 && work >= (1LL << 27)) {
+  bool dyn = false;
+  for (int i = 0; i < a.nbatch; ++i) dyn |= a.b[i].dynM != nullptr || a.b[i].dynK != nullptr;
+  if (!dyn && a.gen.kind < 0 && maxM >= 256 && maxN >= 256 && minK >= 64 && work >= (1LL << 27)) {
     dim3 grid(cdiv(maxM, big::BM), cdiv(maxN, big::BN), a.nbatch * a.rep * a.splitk);
     require(grid.y <= 65535 && grid.z <= 65535, FC_ERR_INVALID_ARG, "gemm grid too large");
     if (a.krR > 0) big::launch_big<0, 0, true>(a, grid, st);

@@ -661,6 +661,30 @@ __global__ void accumulate_core_kernel(int nb, int r0, int r1, int r2, const dou
   }
 }
 
+// fixed-order dot of two arrays: per-block partials, then one thread sums them in block order
+__global__ void core_dot_kernel(long long tot, const double* __restrict__ a, const double* __restrict__ b,
+                                double* part) {
+  __shared__ double red[32];
+  double s = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < tot; i += (long long)gridDim.x * blockDim.x)
+    s = fma(a[i], b[i], s);
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+    part[blockIdx.x] = t;
+  }
+}
+
+__global__ void core_dot_final_kernel(int nb, const double* __restrict__ part, double* out) {
+  if (threadIdx.x != 0) return;
+  double t = 0.0;
+  for (int i = 0; i < nb; ++i) t += part[i];
+  *out = t;
+}
+
 // B^T: out[j + i*cols] = in[i + j*rows]   (in rows x cols, column-major)
 __global__ void transpose_kernel(int rows, int cols, const double* __restrict__ in, double* out) {
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < (long long)rows * cols;
@@ -1448,6 +1472,52 @@ double tt_dot(fc_ctx c, const TT& x, const TT& y) {
   if (x.R == 0 || y.R == 0) return 0.0;
   cudaStream_t st = stream_of(c);
   Scratch s(st);
+  static const bool no_core_dot = getenv("FC_NO_CORE_DOT") != nullptr;   // diagnostic
+  if (x.core && y.core && !no_core_dot) {
+    // both carry their Tucker cores (x = core_x x_l Q_x,l): <x, y> = <core_x, core_y x_l G_l>,
+    // G_l = Q_x,l^T Q_y,l — r^3-sized contractions instead of the R_x x R_y term Hadamard
+    const int* a = x.q;
+    const int* b = y.q;
+    double* G[3];
+    GemmArgs gg;
+    gg.transA = 1;
+    gg.beta = 1.0;
+    gg.nbatch = 3;
+    int tiles = 0;
+    for (int l = 0; l < 3; ++l) {
+      G[l] = s.zeros<double>((size_t)a[l] * b[l]);
+      gg.b[l] = GemmBatch{a[l], b[l], x.n, x.Q[l], x.n, y.Q[l], y.n, G[l], a[l], nullptr, 0, nullptr};
+      tiles += cdiv(a[l], 64) * cdiv(b[l], 64);
+    }
+    gg.splitk = std::max(1, std::min(cdiv(x.n, 64), cdiv(2 * 148, std::max(tiles, 1))));
+    gemm(gg, st);
+    // T1 = G0 core_y(1)  (a0 x b1 b2);  T2 = T1 (a0 b1 x b2) G2^T  (a0 b1 x a2);
+    // T3[:, :, k] = T2[:, :, k] (a0 x b1) G1^T  (a0 x a1), k < a2
+    double* T1 = s.alloc<double>((size_t)a[0] * b[1] * b[2]);
+    dgemm(st, 0, 0, a[0], b[1] * b[2], b[0], 1.0, G[0], a[0], y.core, b[0], 0.0, T1, a[0]);
+    double* T2 = s.alloc<double>((size_t)a[0] * b[1] * a[2]);
+    dgemm(st, 0, 1, a[0] * b[1], a[2], b[2], 1.0, T1, a[0] * b[1], G[2], a[2], 0.0, T2, a[0] * b[1]);
+    double* T3 = s.alloc<double>((size_t)a[0] * a[1] * a[2]);
+    GemmArgs g3;
+    g3.transB = 1;
+    g3.nbatch = 1;
+    g3.rep = a[2];
+    g3.b[0] = GemmBatch{a[0], a[1], b[1], T2, a[0], G[1], a[1], T3, a[0], nullptr, 0, nullptr};
+    g3.b[0].sA = (long long)a[0] * b[1];
+    g3.b[0].sC = (long long)a[0] * a[1];
+    gemm(g3, st);
+    const long long tot = (long long)a[0] * a[1] * a[2];
+    constexpr int NB = 148;
+    double* part = s.alloc<double>(NB + 1);
+    core_dot_kernel<<<NB, 256, 0, st>>>(tot, x.core, T3, part);
+    FC_CHECK_LAUNCH();
+    core_dot_final_kernel<<<1, 32, 0, st>>>(NB, part, part + NB);
+    FC_CHECK_LAUNCH();
+    double h = 0;
+    FC_CUDA_TRY(cudaMemcpyAsync(&h, part + NB, sizeof(double), cudaMemcpyDeviceToHost, st));
+    FC_CUDA_TRY(cudaStreamSynchronize(st));
+    return h;
+  }
   double* H = s.alloc<double>((size_t)3 * x.R * y.R + 1);
   for (int l = 0; l < 3; ++l) {
     // G = Q_x^T Q_y (qx x qy), T = G C_y (qx x Ry), H_l = C_x^T T (Rx x Ry)
