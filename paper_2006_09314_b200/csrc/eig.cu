@@ -1734,19 +1734,19 @@ __global__ void __launch_bounds__(256) rank_cut_kernel(int count, const double* 
   // tails from the small end: tail(r) = sum_{k >= r} s2[k]
   double acc = 0.0;
   int r = count;                 // default: keep everything
-  double margin = 1e300;
+  double dmin = 1e300;           // min |tail - thr| over the visited tails (divided once below:
+                                 // division by thr > 0 is monotone, so the margin is unchanged)
   for (int k = count - 1; k >= 1; --k) {
     acc += k >= base ? tail[k - base] : s2[k];   // not clamped: eigenvalues of a PSD Gram at the
                     // noise floor are +-eps||M||; clamping would bias the tail by (#noise) eps ||M||
-    double m = fabs(acc - thr) / (thr > 0 ? thr : 1.0);
+    dmin = fmin(dmin, fabs(acc - thr));
     if (acc <= thr) {
       r = k;                    // tail beyond index k-1 fits: keep k values
-      margin = fmin(margin, m);
     } else {
-      margin = fmin(margin, m);
       break;
     }
   }
+  const double margin = dmin >= 1e300 ? 1e300 : dmin / (thr > 0 ? thr : 1.0);
   if (count >= 1 && r < 1) r = 1;
   while (r > 0 && r < count && s2[r] == s2[r - 1] && s2[r] > 0) ++r;   // ties kept together (A23)
   *r_out = count == 0 ? 0 : r;
