@@ -969,6 +969,93 @@ __global__ void __launch_bounds__(512) backtransform_kernel(const __grid_constan
   }
 }
 
+// Same back-transformation with the reflectors staged through shared memory: the CTA's 16 warps
+// (16 vectors) share every reflector, so the whole CTA copies chunks of KB reflector columns
+// (N doubles each, 8-byte cp.async) into a double buffer one chunk ahead, and each warp applies
+// them from shared memory to its register-resident vector (same arithmetic and order as
+// backtransform_kernel: the per-reflector critical path no longer includes an L2 round trip).
+__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src));
+}
+__device__ __forceinline__ void cp_async_commit_bt() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int NPEND>
+__device__ __forceinline__ void cp_async_wait_bt() { asm volatile("cp.async.wait_group %0;\n" ::"n"(NPEND)); }
+
+template <int MC, int KB>
+__global__ void __launch_bounds__(512) backtransform_smem_kernel(const __grid_constant__ SyevBatch B) {
+  extern __shared__ double su[];                    // 2 buffers x KB reflectors x (32 MC)
+  constexpr int NP = 32 * MC;
+  const SyevEntry& E = B.e[blockIdx.y];
+  const int N = E.N;
+  const int r = min(*E.r, N);
+  const int nw = blockDim.x >> 5;
+  if ((int)blockIdx.x * nw >= r || E.A == nullptr || N > NP || N < 3) return;   // uniform per CTA
+  const int w = blockIdx.x * nw + (threadIdx.x >> 5), ln = threadIdx.x & 31, tid = threadIdx.x;
+  const bool active = w < r;
+  double* yi = E.Y + (size_t)(active ? w : 0) * E.ldy;
+  double yv[MC];
+#pragma unroll
+  for (int c = 0; c < MC; ++c) {
+    const int idx = ln + 32 * c;
+    yv[c] = (active && idx < N) ? yi[idx] : 0.0;
+  }
+  const int nk = N - 2;                              // reflectors k = N-3 .. 0
+  const int nchunks = (nk + KB - 1) / KB;
+  auto issue = [&](int ci) {
+    double* buf = su + (size_t)(ci & 1) * KB * NP;
+    const int kb0 = ci * KB, cnt = min(KB, nk - kb0);
+    for (int idx = tid; idx < cnt * N; idx += blockDim.x) {
+      const int kk = idx / N, i = idx - kk * N;
+      const int k = N - 3 - (kb0 + kk);
+      cp_async8(buf + kk * NP + i, E.A + (size_t)k * E.lda + i);
+    }
+    cp_async_commit_bt();
+  };
+  issue(0);
+  for (int ci = 0; ci < nchunks; ++ci) {
+    if (ci + 1 < nchunks) {
+      issue(ci + 1);
+      cp_async_wait_bt<1>();
+    } else {
+      cp_async_wait_bt<0>();
+    }
+    __syncthreads();
+    if (active) {
+      const double* buf = su + (size_t)(ci & 1) * KB * NP;
+      const int kb0 = ci * KB, cnt = min(KB, nk - kb0);
+      for (int kk = 0; kk < cnt; ++kk) {
+        const int k = N - 3 - (kb0 + kk);
+        const double* u = buf + kk * NP;             // u_k[idx] for idx > k
+        const int c0 = (k + 1) >> 5;
+        double s = 0.0;
+#pragma unroll
+        for (int c = 0; c < MC; ++c) {
+          const int idx = ln + 32 * c;
+          if (c >= c0 && idx > k && idx < N) s = fma(u[idx], yv[c], s);
+        }
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (s != 0.0) {
+          const double t2 = 2.0 * s;
+#pragma unroll
+          for (int c = 0; c < MC; ++c) {
+            const int idx = ln + 32 * c;
+            if (c >= c0 && idx > k && idx < N) yv[c] -= t2 * u[idx];
+          }
+        }
+      }
+    }
+    __syncthreads();                                 // buffer (ci & 1) is refilled by issue(ci + 2)
+  }
+  if (active) {
+#pragma unroll
+    for (int c = 0; c < MC; ++c) {
+      const int idx = ln + 32 * c;
+      if (idx < N) yi[idx] = yv[c];
+    }
+  }
+}
+
 // Column-pivoted modified Gram-Schmidt (rank revealing, no Gram squaring), one CTA per matrix.
 // A (n x p, column-major, overwritten with residuals) -> Q (n x k, orthonormal, k <= p) with
 // every column of A within tau * ||a_c|| of span(Q).  Pivot: largest residual norm among the
@@ -1981,9 +2068,22 @@ void syev_vectors(const SyevBatch& b, int maxN, cudaStream_t st, const int* r_ho
   }
   orth_backtransform_kernel<<<b.nb, 1024, (size_t)maxN * 8, st>>>(ob, flag);
   FC_CHECK_LAUNCH();
-  // back-transformation, warp per vector over many CTAs
+  // back-transformation, warp per vector over many CTAs; reflectors staged through shared memory
+  // (FC_BT_GLOBAL: the global-memory kernel)
   const dim3 grid(cdiv(maxN, 16), b.nb);
-  if (maxN <= 512) backtransform_kernel<16><<<grid, 512, 0, st>>>(b);
+  static const bool bt_global = getenv("FC_BT_GLOBAL") != nullptr;
+  constexpr size_t kBtSmem = 128 * 1024;
+  static bool bt_attr = false;
+  if (!bt_attr) {
+    FC_CUDA_TRY(cudaFuncSetAttribute(backtransform_smem_kernel<16, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)kBtSmem));
+    FC_CUDA_TRY(cudaFuncSetAttribute(backtransform_smem_kernel<32, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)kBtSmem));
+    bt_attr = true;
+  }
+  if (!bt_global && maxN <= 512) backtransform_smem_kernel<16, 16><<<grid, 512, kBtSmem, st>>>(b);
+  else if (!bt_global && maxN <= 1024) backtransform_smem_kernel<32, 8><<<grid, 512, kBtSmem, st>>>(b);
+  else if (maxN <= 512) backtransform_kernel<16><<<grid, 512, 0, st>>>(b);
   else if (maxN <= 1024) backtransform_kernel<32><<<grid, 512, 0, st>>>(b);
   else backtransform_kernel<1><<<grid, 512, 0, st>>>(b);
   FC_CHECK_LAUNCH();
