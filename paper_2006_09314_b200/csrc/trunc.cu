@@ -361,25 +361,34 @@ __global__ void __launch_bounds__(512) slice_svd_qrj_kernel(int ra, int rb, cons
   __syncthreads();
   double fro2 = 0.0;
   // ---- Householder QR with column pivoting ----
+  // trailing column norms: exact sums over rows >= i; computed once here and then accumulated in
+  // the same pass (and order) that applies each reflector
+  for (int j = warp; j < cols; j += nw) {
+    const double* a = A + (size_t)j * rows;
+    double s2 = 0.0;
+    for (int t = ln; t < rows; t += 32) s2 = fma(a[t], a[t], s2);
+    for (int o = 16; o > 0; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+    if (ln == 0) cn[j] = s2;
+  }
+  __syncthreads();
   for (int i = 0; i < cols; ++i) {
-    // trailing column norms (exact each step), pivot = largest (lowest index on ties)
-    for (int j = i + warp; j < cols; j += nw) {
-      const double* a = A + (size_t)j * rows;
-      double s2 = 0.0;
-      for (int t = i + ln; t < rows; t += 32) s2 = fma(a[t], a[t], s2);
-      for (int o = 16; o > 0; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
-      if (ln == 0) cn[j] = s2;
-    }
-    __syncthreads();
-    if (tid == 0) {
-      int pj = i;
-      for (int j = i + 1; j < cols; ++j)
-        if (cn[j] > cn[pj]) pj = j;
-      piv_s = pj;
+    // pivot = largest trailing norm (lowest index on ties): one warp
+    if (warp == 0) {
+      double bv = -1.0;
+      int bj = cols;
+      for (int j = i + ln; j < cols; j += 32)
+        if (cn[j] > bv) { bv = cn[j]; bj = j; }
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int oj = __shfl_xor_sync(0xffffffffu, bj, o);
+        if (ov > bv || (ov == bv && oj < bj)) { bv = ov; bj = oj; }
+      }
+      if (ln == 0) piv_s = bj < cols ? bj : i;
       if (i == 0) {
         double f = 0.0;
-        for (int j = 0; j < cols; ++j) f += cn[j];
-        sval = f;
+        for (int j = ln; j < cols; j += 32) f += cn[j];
+        for (int o = 16; o > 0; o >>= 1) f += __shfl_xor_sync(0xffffffffu, f, o);
+        if (ln == 0) sval = f;
       }
     }
     __syncthreads();
@@ -411,17 +420,28 @@ __global__ void __launch_bounds__(512) slice_svd_qrj_kernel(int ra, int rb, cons
       for (int t = i + 1 + tid; t < rows; t += nt) ai[t] *= inv;
     }
     __syncthreads();
-    // apply H = I - tau v v^T to the trailing columns (warp per column)
-    if (tv != 0.0)
-      for (int j = i + 1 + warp; j < cols; j += nw) {
-        double* a = A + (size_t)j * rows;
+    // apply H = I - tau v v^T to the trailing columns (warp per column); the same pass leaves
+    // the next step's trailing norm (rows >= i+1) in cn[j]
+    for (int j = i + 1 + warp; j < cols; j += nw) {
+      double* a = A + (size_t)j * rows;
+      double s2 = 0.0;
+      if (tv != 0.0) {
         double d = (ln == 0) ? a[i] : 0.0;
         for (int t = i + 1 + ln; t < rows; t += 32) d = fma(ai[t], a[t], d);
         for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
         const double f = tv * d;
         if (ln == 0) a[i] -= f;
-        for (int t = i + 1 + ln; t < rows; t += 32) a[t] -= f * ai[t];
+        for (int t = i + 1 + ln; t < rows; t += 32) {
+          const double v = a[t] - f * ai[t];
+          a[t] = v;
+          s2 = fma(v, v, s2);
+        }
+      } else {
+        for (int t = i + 1 + ln; t < rows; t += 32) s2 = fma(a[t], a[t], s2);
       }
+      for (int o = 16; o > 0; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+      if (ln == 0) cn[j] = s2;
+    }
     if (tid == 0) {
       tau[i] = tv;
       red[i] = alpha;                            // R[i, i]

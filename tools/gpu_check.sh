@@ -1,5 +1,3 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_linalg.py tests/test_gpu_truncate_pcg.py tests/test_gpu_setup.py -q -m gpu -x 2>&1 | tail -2
-python tools/one_solve.py > /dev/null 2>&1 || exit 1
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --cache-control none --csv --log-file gpurun_out/l_solve_warm.csv python tools/one_solve.py > /dev/null 2>&1
-echo done
+timeout 900 python -m pytest tests/test_gpu_truncate_pcg.py tests/test_gpu_caseA.py tests/test_gpu_lr2d.py tests/test_gpu_als.py tests/test_gpu_linalg.py tests/test_gpu_setup.py -q -m gpu -x > gpurun_out/pt.log 2>&1; tail -2 gpurun_out/pt.log
+for i in 1 2; do timeout 300 python bench.py --steps 5 --warmup 3 2>>gpurun_out/bench.err | python -c "import json,sys; d=json.loads(sys.stdin.readline()); print(d['value'], d['ms_per_step'], d['final_rel_res'])"; done
