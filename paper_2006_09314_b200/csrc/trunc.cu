@@ -88,10 +88,10 @@ __global__ void scale_cols_kernel(int rows, int cols, const double* __restrict__
 // xi_t, d_l[t] = xi_t / n_l[t], inv_n_l[t] = 1/n_l[t], energy += xi^2 (single block reduction)
 __global__ void term_weights_kernel(int R, const double* __restrict__ w, const double* n2a, const double* n2b,
                                     const double* n2c, double* xi, double* da, double* db, double* dc,
-                                    double* ia, double* ib, double* ic, double* energy) {
+                                    double* ia, double* ib, double* ic, double* part) {
   __shared__ double red[32];
   double acc = 0.0;
-  for (int t = threadIdx.x; t < R; t += blockDim.x) {
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < R; t += gridDim.x * blockDim.x) {
     double na = sqrt(n2a[t]), nb = sqrt(n2b[t]), nc = sqrt(n2c[t]);
     double x = w[t] * na * nb * nc;
     bool zero = (x == 0.0);
@@ -110,8 +110,16 @@ __global__ void term_weights_kernel(int R, const double* __restrict__ w, const d
   if (threadIdx.x < 32) {
     double v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
     for (int s = 16; s > 0; s >>= 1) v += __shfl_down_sync(0xffffffffu, v, s);
-    if (threadIdx.x == 0) *energy = v;
+    if (threadIdx.x == 0) part[blockIdx.x] = v;
   }
+}
+
+// energy = sum of the per-block partials in block order (deterministic)
+__global__ void sum_parts_kernel(int nb, const double* __restrict__ part, double* out) {
+  if (threadIdx.x != 0) return;
+  double v = 0.0;
+  for (int b = 0; b < nb; ++b) v += part[b];
+  *out = v;
 }
 
 // F = Lam^1/2 U^T from the (descending) eigenpairs of K^T K.  Eigenvalues below the
@@ -1050,9 +1058,15 @@ TT truncate_tt(fc_ctx c, const TT& xin, double eps, int rank_cap, TruncStats* st
       FC_CHECK_LAUNCH();
     }
   }
-  term_weights_kernel<<<1, 1024, 0, st>>>(R, xin.w, n2[0], n2[1], n2[2], xi, dl[0], dl[1], dl[2], inv[0], inv[1],
-                                          inv[2], energy);
-  FC_CHECK_LAUNCH();
+  {
+    const int nbw = std::max(1, std::min(148, cdiv(R, 1024)));
+    double* part = s.alloc<double>(nbw);
+    term_weights_kernel<<<nbw, 1024, 0, st>>>(R, xin.w, n2[0], n2[1], n2[2], xi, dl[0], dl[1], dl[2], inv[0], inv[1],
+                                              inv[2], part);
+    FC_CHECK_LAUNCH();
+    sum_parts_kernel<<<1, 32, 0, st>>>(nbw, part, energy);
+    FC_CHECK_LAUNCH();
+  }
   // ---- 3. side matrix in the basis: B_l = C_l D_l (q x R); M_l = B_l B_l^T -------------
   double* Bm[3] = {nullptr, nullptr, nullptr};
   double* M[3];
