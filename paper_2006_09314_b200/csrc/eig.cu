@@ -1795,6 +1795,8 @@ __global__ void __launch_bounds__(kBcgsClusterThreads, 1)
   if (r == 0 && tid == 0) *E.k = k0 + na;
 }
 
+__global__ void set_int_kernel(int* p, int v) { *p = v; }
+
 __global__ void col_norms_kernel(const __grid_constant__ BcgsBatch B) {
   const BcgsEntry& E = B.e[blockIdx.y];
   const int c = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5), ln = threadIdx.x & 31;
@@ -2165,9 +2167,10 @@ void bcgs_cluster_finalize(const BcgsBatch& bb, int j0, cudaStream_t st) {
 // A_blk -= Q P (n x W x k): enough CTAs for ~2 waves of 148 SMs (64 x 64 tiles), at least 64 of
 // the reduction dimension per split (atomic epilogue; both GEMMs accumulate into beta = 1 targets)
 void split_skinny(GemmArgs& p, GemmArgs& u, int n, int k, int w, int nb) {
+  static const int waves = getenv("FC_SKINNY_WAVES") ? atoi(getenv("FC_SKINNY_WAVES")) : 2;
   const int tp = cdiv(k, 64) * cdiv(w, 64) * nb, tu = cdiv(n, 64) * cdiv(w, 64) * nb;
-  p.splitk = std::max(1, std::min(cdiv(n, 64), cdiv(2 * 148, tp)));
-  u.splitk = std::max(1, std::min(cdiv(k, 64), cdiv(2 * 148, tu)));
+  p.splitk = std::max(1, std::min(cdiv(n, 64), cdiv(waves * 148, tp)));
+  u.splitk = std::max(1, std::min(cdiv(k, 64), cdiv(waves * 148, tu)));
 }
 
 void bcgs(const BcgsBatch& bin, cudaStream_t st) {
@@ -2225,27 +2228,40 @@ void bcgs(const BcgsBatch& bin, cudaStream_t st) {
   }
   int maxp = 0;
   for (int i = 0; i < b.nb; ++i) {
-    const BcgsEntry& E = b.e[i];
-    maxp = std::max(maxp, E.p);
+    BcgsEntry& E = b.e[i];
     FC_CUDA_TRY(cudaMemsetAsync(E.Q, 0, (size_t)E.ldq * E.kcap * 8, st));
-    FC_CUDA_TRY(cudaMemsetAsync(E.k, 0, sizeof(int), st));
+    const int kb = std::min(std::max(E.k_base, 0), std::min(E.p, E.kcap));
+    E.k_base = kb;
+    set_int_kernel<<<1, 1, 0, st>>>(E.k, kb);
+    FC_CHECK_LAUNCH();
+    if (kb > 0) {   // orthonormal prefix: into Q as it is; the rest is processed against it
+      FC_CUDA_TRY(cudaMemcpy2DAsync(E.Q, (size_t)E.ldq * 8, E.A, (size_t)E.lda * 8, (size_t)E.n * 8, kb,
+                                    cudaMemcpyDeviceToDevice, st));
+      E.A += (size_t)kb * E.lda;
+      E.p -= kb;
+    }
+    maxp = std::max(maxp, E.p);
   }
   col_norms_kernel<<<dim3(cdiv(maxp, 8), b.nb), 256, 0, st>>>(b);
   FC_CHECK_LAUNCH();
   for (int j0 = 0; j0 < maxp; j0 += W) {
     // project the block against every column accepted so far (<= j0; unused Q columns are 0)
     // one projection pass (BCGS2: the accepted vectors get a second one below)
-    for (int pass = 0; pass < 1 && j0 > 0; ++pass) {
+    bool any_base = false;
+    for (int i = 0; i < b.nb; ++i) any_base |= b.e[i].k_base > 0;
+    for (int pass = 0; pass < 1 && (j0 > 0 || any_base); ++pass) {
       GemmArgs p, u;
       p.transA = 1;
       p.beta = 1.0;
       u.alpha = -1.0;
       u.beta = 1.0;
-      int nb = 0;
+      int nb = 0, kmx = 0;
       for (int i = 0; i < b.nb; ++i) {
         const BcgsEntry& E = b.e[i];
         if (j0 >= E.p) continue;
-        const int wb = std::min(W, E.p - j0), kup = std::min(j0, E.kcap);
+        const int wb = std::min(W, E.p - j0), kup = std::min(E.k_base + j0, E.kcap);
+        if (kup == 0) continue;
+        kmx = std::max(kmx, kup);
         FC_CUDA_TRY(cudaMemsetAsync(E.P, 0, (size_t)kup * W * 8, st));
         p.b[nb] = GemmBatch{kup, wb, E.n, E.Q, E.ldq, E.A + (size_t)j0 * E.lda, E.lda, E.P, kup, nullptr, 0, nullptr};
         u.b[nb] = GemmBatch{E.n, wb, kup, E.Q, E.ldq, E.P, kup, E.A + (size_t)j0 * E.lda, E.lda, nullptr, 0, nullptr};
@@ -2256,23 +2272,27 @@ void bcgs(const BcgsBatch& bin, cudaStream_t st) {
         ++nb;
       }
       p.nbatch = u.nbatch = nb;
-      split_skinny(p, u, b.e[0].n, std::min(j0, b.e[0].kcap), W, nb);
-      gemm(p, st);
-      gemm(u, st);
+      if (nb) {
+        split_skinny(p, u, b.e[0].n, kmx, W, nb);
+        gemm(p, st);
+        gemm(u, st);
+      }
     }
     block_step(b, j0);
     // BCGS2: re-project the accepted (unit) block vectors against the previous basis
-    if (j0 > 0) {
+    if (j0 > 0 || any_base) {
       GemmArgs p, u;
       p.transA = 1;
       p.beta = 1.0;
       u.alpha = -1.0;
       u.beta = 1.0;
-      int nb = 0;
+      int nb = 0, kmx = 0;
       for (int i = 0; i < b.nb; ++i) {
         const BcgsEntry& E = b.e[i];
         if (j0 >= E.p) continue;
-        const int kup = std::min(j0, E.kcap);
+        const int kup = std::min(E.k_base + j0, E.kcap);
+        if (kup == 0) continue;
+        kmx = std::max(kmx, kup);
         FC_CUDA_TRY(cudaMemsetAsync(E.P, 0, (size_t)kup * W * 8, st));
         p.b[nb] = GemmBatch{kup, W, E.n, E.Q, E.ldq, E.Y, E.n, E.P, kup, nullptr, 0, nullptr};
         u.b[nb] = GemmBatch{E.n, W, kup, E.Q, E.ldq, E.P, kup, E.Y, E.n, nullptr, 0, nullptr};
@@ -2283,9 +2303,11 @@ void bcgs(const BcgsBatch& bin, cudaStream_t st) {
         ++nb;
       }
       p.nbatch = u.nbatch = nb;
-      split_skinny(p, u, b.e[0].n, std::min(j0, b.e[0].kcap), W, nb);
-      gemm(p, st);
-      gemm(u, st);
+      if (nb) {
+        split_skinny(p, u, b.e[0].n, kmx, W, nb);
+        gemm(p, st);
+        gemm(u, st);
+      }
     }
     finalize_step(b, j0);
   }

@@ -67,6 +67,7 @@ struct BcgsEntry {
   double tau;
   double* Y = nullptr;   // n x 32 block buffer (allocated by bcgs)
   int* nacc = nullptr;   // accepted count of the current block (allocated by bcgs)
+  int k_base = 0;        // the first k_base columns of A are orthonormal: taken into Q as they are
 };
 struct BcgsBatch {
   int nb = 0;

@@ -14,6 +14,7 @@
 #include <chrono>
 #include <cmath>
 #include <exception>
+#include <memory>
 #include <thread>
 #include "cpops.cuh"
 #include "eig.cuh"
@@ -116,6 +117,7 @@ TT apply_truncate_tt(fc_ctx c, SpecCP& sp, const TT& x, double eps, int rank_cap
     return z;
   }
   ensure_spec_basis(c, sp);
+  auto pm0 = std::make_unique<PhaseMarks>(st);
   // x's Tucker core (T2C outputs carry it; otherwise form it once from the CP coefficients)
   TT xc;
   const double* core_x = x.core;
@@ -166,7 +168,10 @@ TT apply_truncate_tt(fc_ctx c, SpecCP& sp, const TT& x, double eps, int rank_cap
     FC_CHECK_LAUNCH();
     y.orth[l] = false;
   }
+  pm0->mark("0 apply: fwd + KR basis");
+  pm0.reset();
   TT out = truncate_tt(c, y, eps, rank_cap, stats, &ss);
+  PhaseMarks pm1(st);
   // S7: back to physical coordinates, only the surviving basis columns
   GemmArgs inv;
   inv.nbatch = 0;
@@ -181,6 +186,7 @@ TT apply_truncate_tt(fc_ctx c, SpecCP& sp, const TT& x, double eps, int rank_cap
     for (int l = 0; l < 3; ++l)
       FC_CUDA_TRY(cudaMemcpyAsync(out.Q[l], newQ[l].d(), (size_t)n * out.q[l] * 8, cudaMemcpyDeviceToDevice, st));
   }
+  pm1.mark("9 back-transform");
   return out;
 }
 

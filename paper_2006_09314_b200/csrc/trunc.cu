@@ -13,6 +13,8 @@
 //   core beta = sum_t xi_t Chat_1[:,t] (x) Chat_2[:,t] (x) Chat_3[:,t]                (S12)
 //   T2C: slice SVDs along the min-rank mode, pooled cut at (eps/2)^2 ||beta||^2        (S13)
 #include <algorithm>
+#include <map>
+#include <mutex>
 #include <cmath>
 #include "cpops.cuh"
 #include "eig.cuh"
@@ -741,6 +743,58 @@ int read_int(const int* d, cudaStream_t st) {
 
 }  // namespace
 
+// ---- FC_PHASES: real-run time per truncation phase (CUDA events between phase marks; host
+// waits included, i.e. what the stream actually spends), printed at exit --------------------
+struct PhaseProf {
+  std::mutex mu;
+  std::map<std::string, std::pair<double, long>> acc;
+  ~PhaseProf() {
+    if (acc.empty()) return;
+    std::vector<std::pair<double, std::string>> v;
+    double tot = 0.0;
+    for (auto& kv : acc) {
+      v.push_back({kv.second.first, kv.first});
+      tot += kv.second.first;
+    }
+    std::sort(v.rbegin(), v.rend());
+    fprintf(stderr, "[fc phases] total %.1f ms\n", tot);
+    for (auto& x : v)
+      fprintf(stderr, "[fc phases] %8.2f ms %5.1f%%  %-28s x%ld\n", x.first, 100.0 * x.first / tot, x.second.c_str(),
+              acc[x.second].second);
+  }
+};
+PhaseProf& phase_prof() {
+  static PhaseProf p;
+  return p;
+}
+PhaseMarks::PhaseMarks(cudaStream_t s) : st(s) {
+  static const bool enabled = getenv("FC_PHASES") != nullptr;
+  on = enabled;
+  mark("start");
+}
+void PhaseMarks::mark(const char* name) {
+  if (!on) return;
+  cudaEvent_t e;
+  if (cudaEventCreate(&e) != cudaSuccess) return;
+  cudaEventRecord(e, st);
+  m.push_back({name, e});
+}
+PhaseMarks::~PhaseMarks() {
+  if (!on) return;
+  if (m.size() >= 2 && cudaEventSynchronize(m.back().second) == cudaSuccess) {
+    PhaseProf& P = phase_prof();
+    std::lock_guard<std::mutex> lock(P.mu);
+    for (size_t i = 1; i < m.size(); ++i) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, m[i - 1].second, m[i].second);
+      auto& a = P.acc[m[i].first];
+      a.first += ms;
+      a.second += 1;
+    }
+  }
+  for (auto& x : m) cudaEventDestroy(x.second);
+}
+
 // ---------------------------------------------------------------------------------------
 // Batched SVD of ns column-major ra x rb matrices (S + nu*ra*rb): k = min(ra, rb) triples per
 // matrix sorted by s descending (s[nu*k + m], Ua[nu*ra*k + m*ra + x], Vb[nu*rb*k + m*rb + y]).
@@ -809,9 +863,11 @@ TT tucker_to_canonical(fc_ctx c, const double* core, const int r[3], double* con
   int* keys = s.alloc<int>((size_t)K);
   double* energy = s.alloc<double>(2);
   int* rdev = s.alloc<int>(2);
+  PhaseMarks pm(st);
   extract_slices_kernel<<<blocks_for((long long)ra * rb * rc), 256, 0, st>>>(core, r[0], r[1], r[2], ma, mb, mc, S);
   FC_CHECK_LAUNCH();
   small_svd(st, ra, rb, rc, S, sv, Ua, Vb);
+  pm.mark("7 T2C slice SVDs");
   pool_rank_kernel<<<cdiv(K, 256), 256, 0, st>>>(K, sv, s2s, keys);
   FC_CHECK_LAUNCH();
   pool_energy_kernel<<<1, 1024, 0, st>>>(K, sv, energy);
@@ -823,6 +879,7 @@ TT tucker_to_canonical(fc_ctx c, const double* core, const int r[3], double* con
     rank_cut_device(K, s2s, 0.25 * eps * eps, energy, rdev, energy + 1, st);
     R = read_int(rdev, st);
   }
+  pm.mark("8 T2C pooled cut");
   if (stats) {
     stats->t2c_mode = mc;
     stats->out_rank = R;
@@ -918,6 +975,7 @@ TT truncate_tt(fc_ctx c, const TT& xin, double eps, int rank_cap, TruncStats* st
     return z;
   }
   Scratch s(st);
+  PhaseMarks pm(st);
   // ---- 1. orthonormal basis per mode: K = Q_l (n x q) -> pivoted MGS -> Qo (n x k), then
   //         the coefficients in that basis Co = (Qo^T K) C.  Rank revealing without forming
   //         K^T K (no squaring): every column of K is kept to 1e-13 of its norm.
@@ -941,6 +999,8 @@ TT truncate_tt(fc_ctx c, const TT& xin, double eps, int rank_cap, TruncStats* st
       map[l] = pb.nb;
       pb.e[pb.nb++] = BcgsEntry{n, xin.q[l], Kc, n, Qn, n, kcap, kdev + l, s.alloc<double>(xin.q[l]),
                                 s.alloc<double>((size_t)kcap * kBcgsW), kBasisTol};
+      static const bool no_prefix = getenv("FC_NO_ORTH_PREFIX") != nullptr;   // diagnostic
+      if (!no_prefix) pb.e[pb.nb - 1].k_base = std::min(xin.orth_prefix[l], kcap);
     }
     bcgs(pb, st);
     int kh[4] = {0, 0, 0, 0};
@@ -1003,6 +1063,7 @@ TT truncate_tt(fc_ctx c, const TT& xin, double eps, int rank_cap, TruncStats* st
     S.basis[l] = q[l];
     require(q[l] >= 1 && q[l] <= 2048, FC_ERR_CAPACITY, "side-matrix basis dimension above 2048");
   }
+  pm.mark(ss ? "1 basis (structured)" : "1 basis (cp)");
   // ---- 2. term norms n_l[t] = ||C_l[:, t]|| (orthonormal basis), xi_t, d_l[t] = xi_t/n_l[t] ----
   double* n2[3];
   double* dl[3];
@@ -1067,6 +1128,7 @@ TT truncate_tt(fc_ctx c, const TT& xin, double eps, int rank_cap, TruncStats* st
     sum_parts_kernel<<<1, 32, 0, st>>>(nbw, part, energy);
     FC_CHECK_LAUNCH();
   }
+  pm.mark("2 term norms");
   // ---- 3. side matrix in the basis: B_l = C_l D_l (q x R); M_l = B_l B_l^T -------------
   double* Bm[3] = {nullptr, nullptr, nullptr};
   double* M[3];
@@ -1139,6 +1201,7 @@ TT truncate_tt(fc_ctx c, const TT& xin, double eps, int rank_cap, TruncStats* st
     m.splitk = std::max(1, std::min(cdiv(R, 128), std::max(1, 148 * 3 / std::max(tiles, 1))));
     gemm(m, st);
   }
+  pm.mark("3 side Gram");
   // ---- 4. eigen of M: s^2 descending, rank cut (tails from the small end), leading vectors ----
   // K13 (eps < kQrEps on the CP route): the SVD of the side matrix B_l itself
   // instead of the eigen-decomposition of B_l B_l^T, so the singular values carry ~eps_mach
@@ -1207,6 +1270,7 @@ TT truncate_tt(fc_ctx c, const TT& xin, double eps, int rank_cap, TruncStats* st
     maxq = std::max(maxq, ql);
   }
   syev_values(eb, st);
+  pm.mark("4a eig values (+K13)");
   for (int l = 0; l < 3; ++l) rank_cut_device(q[l], lam[l], 0.25 * eps * eps, energy, rl + l, margins + l, st);
   int r[3];
   double hm[3], lam0[3];
@@ -1335,6 +1399,7 @@ TT truncate_tt(fc_ctx c, const TT& xin, double eps, int rank_cap, TruncStats* st
     z.n = n;
     return z;
   }
+  pm.mark("4b cut + eig vectors");
   // ---- 4b. C2T-ALS refinement (oracle/als.py): HOOI sweeps over the modes
   // with the ranks r_l fixed.  In the basis coordinates the CP is x = sum_t xi_t (x)_l Cs_l[:, t]
   // with Cs_l = Co_l diag(1/n_l); for mode l, A_m = Y_m^T Cs_m (m != l) and
@@ -1396,6 +1461,7 @@ TT truncate_tt(fc_ctx c, const TT& xin, double eps, int rank_cap, TruncStats* st
     }
     gemm(gz, st);
   }
+  pm.mark("5 Z");
   // ---- 6. core beta = x x_l Z_l^T (r0 x r1 x r2) ---------------------------------------------
   const size_t r12 = (size_t)r[0] * r[1];
   // reading A22: the Tucker stage is run while r1 r2 r3 <= 2^28 (2 GB), else CAPACITY
@@ -1467,6 +1533,7 @@ TT truncate_tt(fc_ctx c, const TT& xin, double eps, int rank_cap, TruncStats* st
             std::max(1, std::min(cdiv(m, 64), std::max(1, 296 / std::max(tiles, 1)))));
     }
   }
+  pm.mark(ss ? "6 core (structured)" : "6 core (cp)");
   return tucker_to_canonical(c, core, r, Z, n, eps, 0, rank_cap, &S);
 }
 
@@ -1498,6 +1565,7 @@ TT tt_axpy(cudaStream_t st, const TT& x, double a, const TT& y) {
                                                                             z.C[l]);
     FC_CHECK_LAUNCH();
     z.orth[l] = (x.R == 0 && y.orth[l]) || (y.R == 0 && x.orth[l]);
+    z.orth_prefix[l] = x.orth[l] ? x.q[l] : x.orth_prefix[l];
   }
   return z;
 }
@@ -1505,6 +1573,11 @@ TT tt_axpy(cudaStream_t st, const TT& x, double a, const TT& y) {
 double tt_dot(fc_ctx c, const TT& x, const TT& y) {
   if (x.R == 0 || y.R == 0) return 0.0;
   cudaStream_t st = stream_of(c);
+  PhaseMarks pm(st);
+  struct MarkAtExit {
+    PhaseMarks& p;
+    ~MarkAtExit() { p.mark("dot"); }
+  } mark_at_exit{pm};
   Scratch s(st);
   static const bool no_core_dot = getenv("FC_NO_CORE_DOT") != nullptr;   // diagnostic
   if (x.core && y.core && !no_core_dot) {
@@ -1631,6 +1704,7 @@ TT tt_copy(cudaStream_t st, const TT& x) {
   for (int l = 0; l < 3; ++l) {
     y.q[l] = x.q[l];
     y.orth[l] = x.orth[l];
+    y.orth_prefix[l] = x.orth_prefix[l];
     y.Q[l] = p;
     p += (size_t)x.n * x.q[l];
     y.C[l] = p;

@@ -42,6 +42,9 @@ struct TT {
   double* C[3] = {nullptr, nullptr, nullptr};
   double* w = nullptr;
   bool orth[3] = {false, false, false};
+  // the first orth_prefix[l] columns of Q_l are orthonormal (the x part of x + a*y when x is a
+  // truncation output): the basis stage seeds its Gram-Schmidt with them
+  int orth_prefix[3] = {0, 0, 0};
   double* core = nullptr;     // optional Tucker core q0 x q1 x q2 (x = core x_l Q_l), column-major
   std::vector<DevMem> mem;    // owned storage (may be empty for views)
 };
@@ -56,6 +59,16 @@ struct StructuredS {
   const double* Cx[3];        // t_l x Rx
   const double* wF;           // r
   const double* core_x;       // t0 x t1 x t2 (x's Tucker core in its basis)
+};
+
+// FC_PHASES diagnostics: CUDA events at phase boundaries, elapsed time accumulated per phase
+struct PhaseMarks {
+  cudaStream_t st;
+  bool on = false;
+  std::vector<std::pair<const char*, cudaEvent_t>> m;
+  explicit PhaseMarks(cudaStream_t s);
+  void mark(const char* name);
+  ~PhaseMarks();
 };
 
 struct TruncStats {
