@@ -98,7 +98,7 @@ __global__ void gk_bisect_kernel(int n, const double* __restrict__ s_all, double
 // ahead of the FMA chain.
 __device__ void tri_invit(int N, const double* __restrict__ d, const double* __restrict__ e, double lam,
                           double tnorm, double* scr, size_t stride, double* v_out, size_t vstride, unsigned seed,
-                          bool own_work = false) {
+                          bool own_work = false, int nsolve = 3) {
   double* __restrict__ u0 = scr;
   double* __restrict__ u1 = scr + (size_t)N * stride;
   double* __restrict__ u2 = scr + (size_t)2 * N * stride;
@@ -142,7 +142,7 @@ __device__ void tri_invit(int N, const double* __restrict__ d, const double* __r
     V(k) = 0.5 + (h & 0xFFFFFF) / 16777216.0;
   }
   double scale = 1.0;                       // the previous solve's 1 / max|x|, folded into the next
-  for (int it = 0; it < 3; ++it) {
+  for (int it = 0; it < nsolve; ++it) {
     // forward: apply P and L (the running entry carried in a register; every load below is
     // independent of the recurrence, so the loop is an FMA chain)
     double carry = V(0) * scale;
@@ -814,7 +814,7 @@ __global__ void tri_bisect_kernel(const __grid_constant__ SyevBatch B) {
 }
 
 // thread per wanted vector (i < r): inverse iteration on (d, e) into Y[:, i]
-__global__ void tri_invit_kernel(const __grid_constant__ SyevBatch B) {
+__global__ void tri_invit_kernel(const __grid_constant__ SyevBatch B, int nsolve) {
   const SyevEntry& E = B.e[blockIdx.y];
   const int N = E.N;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -823,7 +823,7 @@ __global__ void tri_invit_kernel(const __grid_constant__ SyevBatch B) {
   double tnorm = 0.0;
   for (int k = 0; k < N; ++k) tnorm = fmax(tnorm, fabs(E.d[k]) + 2.0 * (k < N - 1 ? fabs(E.e[k]) : 0.0));
   tri_invit(N, E.d, E.e, E.lam[i], tnorm, E.scratch + i, (size_t)N, E.Y + (size_t)i * E.ldy, 1, (unsigned)(i + 17),
-            true);
+            true, nsolve);
 }
 
 // one CTA per matrix: CGS2 orthonormalisation of Y[:, 0..r) in order, then back-transform
@@ -1979,7 +1979,9 @@ void syev_values(const SyevBatch& b, cudaStream_t st) {
 
 void syev_vectors(const SyevBatch& b, int maxN, cudaStream_t st, const int* r_host) {
   if (b.nb == 0 || maxN == 0) return;
-  tri_invit_kernel<<<dim3(cdiv(maxN, 64), b.nb), 64, 0, st>>>(b);
+  // inverse-iteration solves per vector (FC_INVIT_SOLVES, default 3)
+  static const int nsolve = getenv("FC_INVIT_SOLVES") ? atoi(getenv("FC_INVIT_SOLVES")) : 3;
+  tri_invit_kernel<<<dim3(cdiv(maxN, 64), b.nb), 64, 0, st>>>(b, nsolve);
   FC_CHECK_LAUNCH();
   static const bool trace_orth = getenv("FC_TRACE_ORTH") != nullptr;
   if (trace_orth) {   // diagnostics: orthogonality of the inverse-iteration vectors
