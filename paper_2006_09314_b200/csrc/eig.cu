@@ -1294,7 +1294,7 @@ constexpr double kBcgsCholFail = 1e-4;  // orthogonality loss above which bcgs_p
 // cluster configurations: (CS CTAs, block width W, rows per CTA RB), n <= CS * RB; see bcgs()
 template <int W, int RB>
 struct BcgsClusterSmem {
-  static constexpr int LD = RB + 4;   // conflict-free row-parallel access
+  static constexpr int LD = RB + 1;   // odd: conflict-free both row-parallel and column-parallel
   double X[LD * W];
   double Yb[LD * W];
   double gram[2 * W * W];         // Gram partials (read remotely) / Cholesky factor / H; reduced Gram
@@ -1302,6 +1302,7 @@ struct BcgsClusterSmem {
   double coef[W + 2];
   double red[kBcgsClusterThreads / 32];
   double pn2[W];                  // squared column norms after the GEMM projection
+  double lim2[W];                 // (tau max(norm0_c, nmax))^2, the acceptance level of column c
   int alive[W];
   int cidx[W], uidx[W];           // Cholesky-accepted / deferred columns
 };
@@ -1311,6 +1312,10 @@ struct BcgsClusterSmem {
 // [20] deferred by the Gram Cholesky, [22] rejected by it, [21] blocks redone on the per-column
 // path
 __device__ unsigned long long g_bcgs_hist[23];
+// FC_TRACE: cycles of the in-block Gram path stages (cluster rank 0): Gram + Cholesky, CholQR,
+// polar step, deferred columns
+__device__ unsigned long long g_bcgs_cyc[10];
+__device__ int g_bcgs_timing = 0;
 
 // all-reduce of buf[0..cnt) (per-CTA partials, read remotely) into out[0..cnt); every CTA sums
 // the CS partials in rank order (shuffle tree over groups of CS lanes)
@@ -1398,47 +1403,92 @@ __device__ void cluster_gram(cooperative_groups::cluster_group& cl, BcgsClusterS
   double* R = S.gram + W * W;
   const int tid = threadIdx.x, warp = tid >> 5, ln = tid & 31, NW = blockDim.x >> 5, nt = blockDim.x;
   const int cnt = m * m, ch = (cnt + CS - 1) / CS, r = (int)cl.block_rank(), nt4 = (m + 3) / 4;
-  for (int t = warp; t < nt4 * nt4; t += NW) {
-    const int ta = t / nt4, tb = t % nt4;
-    if (ta > tb) continue;
+  const bool tm = g_bcgs_timing && r == 0 && tid == 0;
+  long long t0 = tm ? clock64() : 0;
+  // 4 x 4 register tiles over strided column groups {t, t+h, t+2h, t+3h} (h = ceil(m/4)): a tile
+  // per thread pair (even / odd rows, combined by one shuffle), consecutive pairs on consecutive
+  // a-groups (odd LD: distinct banks), the b-group values are broadcasts; half the shared-memory
+  // loads per FMA of a thread-per-entry layout, no reduction trees
+  const int h4 = (m + 3) / 4, ntile = h4 * h4;
+  // warp-uniform loop (the pair shuffle below needs every lane of the warp): lanes past the end
+  // run with empty tiles
+  for (int ub = tid - ln; ub < 2 * ntile; ub += nt) {
+    const int u = ub + ln;
+    const bool valid = u < 2 * ntile;
+    const int tile = valid ? u >> 1 : 0, part = u & 1;
+    const int ta = tile % h4, tb = tile / h4;
+    const double* ya[4];
+    const double* yb[4];
+    bool va[4], vb[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int a = ta + q * h4, b = tb + q * h4;
+      va[q] = a < m;
+      vb[q] = b < m;
+      ya[q] = M + (size_t)(va[q] ? a : 0) * LD;
+      yb[q] = M + (size_t)(vb[q] ? b : 0) * LD;
+    }
     double acc[4][4] = {};
-    for (int i = ln; i < RB; i += 32) {
-      double ya[4], yb[4];
+    for (int i = part; valid && i < RB; i += 2) {
+      double xa[4], xb[4];
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        ya[q] = 4 * ta + q < m ? M[i + (size_t)(4 * ta + q) * LD] : 0.0;
-        yb[q] = 4 * tb + q < m ? M[i + (size_t)(4 * tb + q) * LD] : 0.0;
+        xa[q] = ya[q][i];
+        xb[q] = yb[q][i];
       }
 #pragma unroll
       for (int p = 0; p < 4; ++p)
 #pragma unroll
-        for (int q = 0; q < 4; ++q) acc[p][q] = fma(ya[p], yb[q], acc[p][q]);
+        for (int q = 0; q < 4; ++q) acc[p][q] = fma(xa[p], xb[q], acc[p][q]);
     }
 #pragma unroll
     for (int p = 0; p < 4; ++p)
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        double v = acc[p][q];
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        const int a = 4 * ta + p, b = 4 * tb + q;
-        if (ln == 0 && a < m && b < m) {
-          P[a * m + b] = v;
-          P[b * m + a] = v;
-        }
+        const double v = acc[p][q] + __shfl_xor_sync(0xffffffffu, acc[p][q], 1);
+        if (valid && part == 0 && va[p] && vb[q]) P[(ta + p * h4) * m + (tb + q * h4)] = v;
       }
   }
+  long long t1 = tm ? clock64() : 0;
   cl.sync();
-  for (int e = r * ch + tid; e < min(cnt, (r + 1) * ch); e += nt) {   // reduce own chunk
+  long long t2 = tm ? clock64() : 0;
+  // reduce own chunk: the CS remote partials are loaded into registers first (independent DSMEM
+  // loads in flight together), then summed in rank order
+  for (int e = r * ch + tid; e < min(cnt, (r + 1) * ch); e += nt) {
+    double pv[CS];
+#pragma unroll
+    for (int s = 0; s < CS; ++s) pv[s] = cl.map_shared_rank(P, s)[e];
     double v = 0.0;
-    for (int s = 0; s < CS; ++s) v += cl.map_shared_rank(P, s)[e];
+#pragma unroll
+    for (int s = 0; s < CS; ++s) v += pv[s];
     R[e] = v;
   }
+  long long t3 = tm ? clock64() : 0;
   cl.sync();
-  for (int e = tid; e < cnt; e += nt) {                               // gather the others
+  long long t4 = tm ? clock64() : 0;
+  // gather the other chunks: all of this thread's remote loads issued before any local store
+  constexpr int kGatherMax = (W * W + kBcgsClusterThreads - 1) / kBcgsClusterThreads;
+  double gv[kGatherMax];
+#pragma unroll
+  for (int it = 0; it < kGatherMax; ++it) {
+    const int e = tid + it * nt;
     const int own = e / ch;
-    if (own != r) R[e] = cl.map_shared_rank(R, own)[e];
+    gv[it] = (e < cnt && own != r) ? cl.map_shared_rank(R, own)[e] : 0.0;
+  }
+#pragma unroll
+  for (int it = 0; it < kGatherMax; ++it) {
+    const int e = tid + it * nt;
+    if (e < cnt && e / ch != r) R[e] = gv[it];
   }
   __syncthreads();
+  if (tm) {
+    const long long t5 = clock64();
+    atomicAdd(&g_bcgs_cyc[5], (unsigned long long)(t1 - t0));
+    atomicAdd(&g_bcgs_cyc[6], (unsigned long long)(t2 - t1));
+    atomicAdd(&g_bcgs_cyc[7], (unsigned long long)(t3 - t2));
+    atomicAdd(&g_bcgs_cyc[8], (unsigned long long)(t4 - t3));
+    atomicAdd(&g_bcgs_cyc[9], (unsigned long long)(t5 - t4));
+  }
 }
 
 // Polar (Newton-Schulz) re-orthonormalisation of the na block vectors held row-distributed in
@@ -1655,13 +1705,16 @@ __global__ void __launch_bounds__(kBcgsClusterThreads, 1)
       if (S.alive[c]) na = bcgs_column<CS, W, RBM>(cl, S, E, B, c, na, ph, j0, k0, nmax, nr, RB, r);
   } else {
     // ---- Gram path ----
+    long long tc0 = B.trace ? clock64() : 0;
     cluster_gram<CS, W, RBM>(cl, S, S.X, wb, RB);
+    if (B.trace && r == 0 && tid == 0) atomicAdd(&g_bcgs_cyc[4], (unsigned long long)(clock64() - tc0));
     double* L = S.gram;                                    // Cholesky in place of the partials
     const double* G = S.gram + W * W;
     for (int e = tid; e < wb * wb; e += nt) L[e] = G[e];
     for (int c = tid; c < wb; c += nt) {
       const double lim = E.tau * fmax(E.norm0[j0 + c], nmax);
       S.pn2[c] = G[c * wb + c];
+      S.lim2[c] = lim * lim;
       S.alive[c] = S.pn2[c] > lim * lim;
       if (B.trace && r == 0 && !S.alive[c]) atomicAdd(&g_bcgs_hist[18], 1ull);
     }
@@ -1673,27 +1726,24 @@ __global__ void __launch_bounds__(kBcgsClusterThreads, 1)
     for (int c = 0; c < wb; ++c) {
       if (!S.alive[c]) continue;
       const double piv = L[c + c * wb];
-      const double lim = E.tau * fmax(E.norm0[j0 + c], nmax);
-      if (nC < cap && piv > fmax(kBcgsTheta2 * S.pn2[c], 1.01 * lim * lim)) {
-        const double d = sqrt(piv), inv = 1.0 / d;
-        for (int j = c + 1 + tid; j < wb; j += nt) L[j + c * wb] *= inv;
-        __syncthreads();
-        const int t = wb - c - 1;
-        for (int idx = tid; idx < t * t; idx += nt) {
-          const int j = c + 1 + idx % t, k = c + 1 + idx / t;
-          L[j + k * wb] -= L[j + c * wb] * L[k + c * wb];
+      const double lim2 = S.lim2[c];
+      if (nC < cap && piv > fmax(kBcgsTheta2 * S.pn2[c], 1.01 * lim2)) {
+        // right-looking step on the lower triangle with the raw pivot column (l_jc l_kc =
+        // a_jc a_kc / piv): a warp per trailing column k, lanes over rows j >= k; the pivot
+        // column itself is scaled after the loop (one barrier per accepted column)
+        const double ipiv = 1.0 / piv;
+        for (int k = c + 1 + warp; k < wb; k += NW) {
+          const double akc = L[k + c * wb] * ipiv;
+          for (int j = k + ln; j < wb; j += 32) L[j + k * wb] -= L[j + c * wb] * akc;
         }
-        if (tid == 0) {
-          L[c + c * wb] = d;
-          S.cidx[nC] = c;
-        }
+        if (tid == 0) S.cidx[nC] = c;
         if (B.trace && r == 0 && tid == 0) {
           const int dd = min(17, max(0, (int)floor(-0.5 * log10(piv / S.pn2[c]))));
           atomicAdd(&g_bcgs_hist[dd], 1ull);
         }
         ++nC;
         __syncthreads();
-      } else if (piv > kBcgsTheta2 * S.pn2[c] && piv < 0.99 * lim * lim) {
+      } else if (piv > kBcgsTheta2 * S.pn2[c] && piv < 0.99 * lim2) {
         // residual against the accepted subset already below lim (accurate to ~1e-6 here): the
         // per-column path, projecting against a superset, would reject it too
         if (B.trace && r == 0 && tid == 0) atomicAdd(&g_bcgs_hist[22], 1ull);
@@ -1703,7 +1753,16 @@ __global__ void __launch_bounds__(kBcgsClusterThreads, 1)
       }
     }
     __syncthreads();
+    // finish the factor: L[c, c] = sqrt(piv_c), L[j, c] = a_jc / sqrt(piv_c) for the accepted c
+    for (int m = warp; m < nC; m += NW) {
+      const int c = S.cidx[m];
+      const double d = sqrt(L[c + c * wb]), inv = 1.0 / d;
+      for (int j = c + 1 + ln; j < wb; j += 32) L[j + c * wb] *= inv;
+      if (ln == 0) L[c + c * wb] = d;
+    }
+    __syncthreads();
     if (B.trace && r == 0 && tid == 0) atomicAdd(&g_bcgs_hist[20], (unsigned long long)nU);
+    long long tc1 = B.trace ? clock64() : 0;
     // CholQR: Yb[:, m] = (X[:, c_m] - sum_{q < m} Yb[:, q] L[c_m, c_q]) / L[c_m, c_m]
     for (int i = tid; i < RB; i += nt) {
       for (int m = 0; m < nC; ++m) {
@@ -1717,10 +1776,19 @@ __global__ void __launch_bounds__(kBcgsClusterThreads, 1)
     cl.sync();                                             // all gathers of G done before reuse
     // CholQR loses orthogonality like eps kappa(X_C)^2; the polar routine repairs it with a second
     // Cholesky step up to kappa ~ 1e8, beyond that the block is redone on the per-column path
+    long long tc2 = B.trace ? clock64() : 0;
     if (bcgs_polar<CS, W, RBM>(cl, S, nC, RB)) {
+      long long tc3 = B.trace ? clock64() : 0;
       na = nC;
       for (int u = 0; u < nU; ++u)
         na = bcgs_column<CS, W, RBM>(cl, S, E, B, S.uidx[u], na, ph, j0, k0, nmax, nr, RB, r);
+      if (B.trace && r == 0 && tid == 0) {
+        const long long tc4 = clock64();
+        atomicAdd(&g_bcgs_cyc[0], (unsigned long long)(tc1 - tc0));
+        atomicAdd(&g_bcgs_cyc[1], (unsigned long long)(tc2 - tc1));
+        atomicAdd(&g_bcgs_cyc[2], (unsigned long long)(tc3 - tc2));
+        atomicAdd(&g_bcgs_cyc[3], (unsigned long long)(tc4 - tc3));
+      }
     } else {
       if (B.trace && r == 0 && tid == 0) atomicAdd(&g_bcgs_hist[21], 1ull);
       for (int c = 0; c < wb; ++c)
@@ -2219,10 +2287,25 @@ void bcgs(const BcgsBatch& bin, cudaStream_t st) {
                 h[19], h[21], h[18], h[20], h[22]);
         for (int d = 0; d < 18; ++d) fprintf(stderr, " %llu", h[d]);
         fprintf(stderr, "\n");
+        unsigned long long cy[10];
+        if (cudaMemcpyFromSymbol(cy, g_bcgs_cyc, sizeof(cy)) == cudaSuccess) {
+          fprintf(stderr, "[bcgs] in-block Mcycles: gram+cholesky %.1f (gram %.1f) cholqr %.1f polar %.1f deferred %.1f\n",
+                  cy[0] * 1e-6, cy[4] * 1e-6, cy[1] * 1e-6, cy[2] * 1e-6, cy[3] * 1e-6);
+          fprintf(stderr, "[bcgs] cluster_gram Mcycles: partials %.1f sync1 %.1f reduce %.1f sync2 %.1f gather %.1f\n",
+                  cy[5] * 1e-6, cy[6] * 1e-6, cy[7] * 1e-6, cy[8] * 1e-6, cy[9] * 1e-6);
+        }
       });
     }
   }
   b.trace = trace;
+  if (trace) {
+    static bool tset = false;
+    if (!tset) {
+      int one = 1;
+      FC_CUDA_TRY(cudaMemcpyToSymbol(g_bcgs_timing, &one, sizeof(int)));
+      tset = true;
+    }
+  }
   Scratch scr(st);
   for (int i = 0; i < b.nb; ++i) {
     b.e[i].Y = scr.alloc<double>((size_t)b.e[i].n * kBcgsW);
