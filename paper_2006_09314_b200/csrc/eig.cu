@@ -771,11 +771,34 @@ __device__ int tri_count(int N, const double* __restrict__ d, const double* __re
   return cnt;
 }
 
+// Sturm count from shared-memory copies of d and e^2, with the correctly rounded reciprocal
+// instead of the (longer) division sequence: q <- (d_k - x) - e_{k-1}^2 * rcp(q)
+__device__ __forceinline__ int tri_count_s(int N, const double* __restrict__ d, const double* __restrict__ e2,
+                                           double x, double pivmin) {
+  double q = d[0] - x;
+  int cnt = q < 0.0;
+  for (int k = 1; k < N; ++k) {
+    if (fabs(q) < pivmin) q = -pivmin;
+    q = fma(-e2[k - 1], __drcp_rn(q), d[k] - x);
+    cnt += (q < 0.0);
+  }
+  return cnt;
+}
+
 // warp per eigenvalue (multisection); lam[i] = i-th largest.  Each round the 32 lanes count
 // the eigenvalues below 32 equispaced interior points of [lo, hi]; the interval shrinks 33x.
+// d and e^2 are staged in shared memory (2 N doubles) for the Sturm counts.
 __global__ void tri_bisect_kernel(const __grid_constant__ SyevBatch B) {
+  extern __shared__ double sde[];
   const SyevEntry& E = B.e[blockIdx.y];
   const int N = E.N;
+  double* ds = sde;
+  double* e2s = sde + N;
+  for (int k = threadIdx.x; k < N; k += blockDim.x) {
+    ds[k] = E.d[k];
+    e2s[k] = k < N - 1 ? E.e[k] * E.e[k] : 0.0;
+  }
+  __syncthreads();
   const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int ln = threadIdx.x & 31;
   if (i >= N) return;
@@ -800,7 +823,7 @@ __global__ void tri_bisect_kernel(const __grid_constant__ SyevBatch B) {
   for (int it = 0; it < 60; ++it) {
     if (hi - lo <= fmax(atol, 2.0 * kEps * fmax(fabs(lo), fabs(hi)))) break;
     const double x = lo + (hi - lo) * ((double)(ln + 1) / 33.0);
-    const bool ge = (x > lo && x < hi) ? tri_count(N, E.d, E.e, x, pivmin) >= target : (x >= hi);
+    const bool ge = (x > lo && x < hi) ? tri_count_s(N, ds, e2s, x, pivmin) >= target : (x >= hi);
     const unsigned m = __ballot_sync(0xffffffffu, ge);
     // first lane whose point has >= target eigenvalues below it: new interval (x_{j-1}, x_j]
     const int j = m ? __ffs(m) - 1 : 32;
@@ -2041,7 +2064,7 @@ void syev_values(const SyevBatch& b, cudaStream_t st) {
     tridiag_kernel<<<b.nb, kTriThreads, smem_g, st>>>(b, minG);
     FC_CHECK_LAUNCH();
   }
-  tri_bisect_kernel<<<dim3(cdiv(maxN, 8), b.nb), 256, 0, st>>>(b);
+  tri_bisect_kernel<<<dim3(cdiv(maxN, 8), b.nb), 256, (size_t)2 * maxN * 8, st>>>(b);
   FC_CHECK_LAUNCH();
 }
 
