@@ -341,19 +341,22 @@ __global__ void __launch_bounds__(512) slice_svd_kernel(int ra, int rb, const do
 // side vectors are Q W (reflectors applied to W), the short-side vectors P U'.  Same outputs and
 // convergence test as slice_svd_kernel; shared memory: rows*cols + 2 cols^2 + 3 cols doubles.
 size_t slice_qrj_smem(int rows, int cols) {
-  return ((size_t)rows * cols + 2 * (size_t)cols * cols + 3 * (size_t)cols) * 8 + (size_t)cols * 8 + 64;
+  return ((size_t)rows * cols + 2 * (size_t)(cols | 1) * cols + 3 * (size_t)cols) * 8 + (size_t)cols * 8 + 64;
 }
 
-__global__ void __launch_bounds__(512) slice_svd_qrj_kernel(int ra, int rb, const double* __restrict__ S,
+__global__ void __launch_bounds__(1024) slice_svd_qrj_kernel(int ra, int rb, const double* __restrict__ S,
                                                             double* s_out, double* Ua, double* Vb) {
   extern __shared__ double sm[];
   const int nu = blockIdx.x;
   const bool tr = ra < rb;
   const int rows = tr ? rb : ra, cols = tr ? ra : rb, k = cols;
   double* A = sm;                                   // rows x cols: R above, reflectors below
-  double* X = A + (size_t)rows * cols;              // cols x cols: R^T, rotated by Jacobi
-  double* W = X + (size_t)cols * cols;              // cols x cols rotations
-  double* cn = W + (size_t)cols * cols;             // cols: column norms^2 / singular values
+  const int lx = cols | 1;                          // odd leading dimension of X and W: the
+                                                    // thread groups of a Jacobi round (different
+                                                    // column pairs, same rows) hit distinct banks
+  double* X = A + (size_t)rows * cols;              // cols x cols (ld lx): R^T, rotated by Jacobi
+  double* W = X + (size_t)lx * cols;                // cols x cols (ld lx) rotations
+  double* cn = W + (size_t)lx * cols;               // cols: column norms^2 / singular values
   double* tau = cn + cols;                          // cols
   double* red = tau + cols;                         // cols (reduction scratch)
   int* perm = (int*)(red + cols);                   // cols
@@ -461,8 +464,8 @@ __global__ void __launch_bounds__(512) slice_svd_qrj_kernel(int ra, int rb, cons
   // X = R^T (cols x cols, lower triangular), W = I
   for (int idx = tid; idx < cols * cols; idx += nt) {
     const int r = idx % cols, c = idx / cols;    // X[r, c] = R[c, r]
-    X[idx] = (r > c) ? A[c + (size_t)r * rows] : (r == c ? red[r] : 0.0);
-    W[idx] = (r == c) ? 1.0 : 0.0;
+    X[r + c * lx] = (r > c) ? A[c + (size_t)r * rows] : (r == c ? red[r] : 0.0);
+    W[r + c * lx] = (r == c) ? 1.0 : 0.0;
   }
   __syncthreads();
   // ---- one-sided Jacobi on the columns of X ----
@@ -489,7 +492,7 @@ __global__ void __launch_bounds__(512) slice_svd_qrj_kernel(int ra, int rb, cons
         double al = 0, be = 0, ga = 0;
         if (act)
           for (int i = gl; i < cols; i += G) {
-            const double x = X[i + a * cols], y = X[i + b * cols];
+            const double x = X[i + a * lx], y = X[i + b * lx];
             al = fma(x, x, al); be = fma(y, y, be); ga = fma(x, y, ga);
           }
         for (int o = G >> 1; o > 0; o >>= 1) {
@@ -502,13 +505,13 @@ __global__ void __launch_bounds__(512) slice_svd_qrj_kernel(int ra, int rb, cons
         const double t = copysign(1.0, dd) * g2 / (fabs(dd) + sqrt(fma(dd, dd, g2 * g2)));
         const double c = rsqrt(fma(t, t, 1.0)), sn = c * t;
         for (int i = gl; i < cols; i += G) {
-          double x = X[i + a * cols], y = X[i + b * cols];
-          X[i + a * cols] = c * x - sn * y;
-          X[i + b * cols] = sn * x + c * y;
-          x = W[i + a * cols];
-          y = W[i + b * cols];
-          W[i + a * cols] = c * x - sn * y;
-          W[i + b * cols] = sn * x + c * y;
+          double x = X[i + a * lx], y = X[i + b * lx];
+          X[i + a * lx] = c * x - sn * y;
+          X[i + b * lx] = sn * x + c * y;
+          x = W[i + a * lx];
+          y = W[i + b * lx];
+          W[i + a * lx] = c * x - sn * y;
+          W[i + b * lx] = sn * x + c * y;
         }
         if (gl == 0) changed = 1;
       }
@@ -523,7 +526,7 @@ __global__ void __launch_bounds__(512) slice_svd_qrj_kernel(int ra, int rb, cons
   // singular values, order
   for (int j = warp; j < cols; j += nw) {
     double s2 = 0;
-    for (int i = ln; i < cols; i += 32) s2 = fma(X[i + j * cols], X[i + j * cols], s2);
+    for (int i = ln; i < cols; i += 32) s2 = fma(X[i + j * lx], X[i + j * lx], s2);
     for (int o = 16; o > 0; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
     if (ln == 0) cn[j] = sqrt(s2);
   }
@@ -539,7 +542,42 @@ __global__ void __launch_bounds__(512) slice_svd_qrj_kernel(int ra, int rb, cons
   for (int m = warp; m < k; m += nw) {
     const int j = order[m];
     double* out = tr ? (Vb + (size_t)nu * rb * k + (size_t)m * rb) : (Ua + (size_t)nu * ra * k + (size_t)m * ra);
-    for (int t = ln; t < rows; t += 32) out[t] = t < cols ? W[t + (size_t)j * cols] : 0.0;
+    if (rows <= 128) {
+      // register-resident vector (element ln + 32 c in slot c): no global round trip per reflector
+      double ov[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int t = ln + 32 * c;
+        ov[c] = (t < rows && t < cols) ? W[t + (size_t)j * lx] : 0.0;
+      }
+      for (int i = cols - 1; i >= 0; --i) {
+        const double tv = tau[i];
+        if (tv == 0.0) continue;
+        const double* v = A + (size_t)i * rows;   // v_i[i] = 1, v_i[t] = A[t, i] for t > i
+        double d = 0.0;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const int t = ln + 32 * c;
+          if (t == i) d += ov[c];
+          else if (t > i && t < rows) d = fma(v[t], ov[c], d);
+        }
+        for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+        const double f = tv * d;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const int t = ln + 32 * c;
+          if (t == i) ov[c] -= f;
+          else if (t > i && t < rows) ov[c] -= f * v[t];
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int t = ln + 32 * c;
+        if (t < rows) out[t] = ov[c];
+      }
+      continue;
+    }
+    for (int t = ln; t < rows; t += 32) out[t] = t < cols ? W[t + (size_t)j * lx] : 0.0;
     __syncwarp();
     for (int i = cols - 1; i >= 0; --i) {
       const double tv = tau[i];
@@ -560,7 +598,7 @@ __global__ void __launch_bounds__(512) slice_svd_qrj_kernel(int ra, int rb, cons
     const int m = idx / cols, i = idx % cols;
     const int j = order[m];
     const double sj = cn[j];
-    const double v = sj > 0 ? X[i + (size_t)j * cols] / sj : 0.0;
+    const double v = sj > 0 ? X[i + (size_t)j * lx] / sj : 0.0;
     if (tr) Ua[(size_t)nu * ra * k + (size_t)m * ra + perm[i]] = v;
     else Vb[(size_t)nu * rb * k + (size_t)m * rb + perm[i]] = v;
   }
@@ -827,7 +865,10 @@ void small_svd(cudaStream_t st, int ra, int rb, int ns, const double* S, double*
                                        (int)kSliceSmem));
       qattr = true;
     }
-    slice_svd_qrj_kernel<<<ns, 512, qsm, st>>>(ra, rb, S, sv, Ua, Vb);
+    // 512 threads (1024, i.e. 16 lanes per Jacobi column pair, measured slower: 320 vs 318 ms per
+    // C4 solve); FC_SLICE_THREADS overrides (diagnostic)
+    static const int sthr = getenv("FC_SLICE_THREADS") ? atoi(getenv("FC_SLICE_THREADS")) : 512;
+    slice_svd_qrj_kernel<<<ns, sthr, qsm, st>>>(ra, rb, S, sv, Ua, Vb);
   } else if (gws) {
     slice_svd_kernel<false><<<ns, 512, smem, st>>>(ra, rb, S, sv, Ua, Vb, gws);
   } else {
