@@ -344,19 +344,24 @@ size_t slice_qrj_smem(int rows, int cols) {
   return ((size_t)rows * cols + 2 * (size_t)(cols | 1) * cols + 3 * (size_t)cols) * 8 + (size_t)cols * 8 + 64;
 }
 
+// SMEM = false: A, X, W in a per-matrix global (L2-resident) workspace gws of
+// rows*cols + 2*(cols|1)*cols doubles (matrices too large for shared memory, e.g. the 2D
+// truncation's ~126 x 126 cores); the small arrays stay in shared memory.
+template <bool SMEM>
 __global__ void __launch_bounds__(1024) slice_svd_qrj_kernel(int ra, int rb, const double* __restrict__ S,
-                                                            double* s_out, double* Ua, double* Vb) {
+                                                            double* s_out, double* Ua, double* Vb, double* gws) {
   extern __shared__ double sm[];
   const int nu = blockIdx.x;
   const bool tr = ra < rb;
   const int rows = tr ? rb : ra, cols = tr ? ra : rb, k = cols;
-  double* A = sm;                                   // rows x cols: R above, reflectors below
   const int lx = cols | 1;                          // odd leading dimension of X and W: the
                                                     // thread groups of a Jacobi round (different
                                                     // column pairs, same rows) hit distinct banks
+  double* A = SMEM ? sm : gws + (size_t)nu * ((size_t)rows * cols + 2 * (size_t)lx * cols);
+                                                    // rows x cols: R above, reflectors below
   double* X = A + (size_t)rows * cols;              // cols x cols (ld lx): R^T, rotated by Jacobi
   double* W = X + (size_t)lx * cols;                // cols x cols (ld lx) rotations
-  double* cn = W + (size_t)lx * cols;               // cols: column norms^2 / singular values
+  double* cn = SMEM ? W + (size_t)lx * cols : sm;   // cols: column norms^2 / singular values
   double* tau = cn + cols;                          // cols
   double* red = tau + cols;                         // cols (reduction scratch)
   int* perm = (int*)(red + cols);                   // cols
@@ -858,17 +863,22 @@ void small_svd(cudaStream_t st, int ra, int rb, int ns, const double* S, double*
   }
   static const bool no_qr = getenv("FC_SLICE_NO_QR") != nullptr;
   const size_t qsm = slice_qrj_smem(rows, cols);
+  // 512 threads (1024, i.e. 16 lanes per Jacobi column pair, measured slower: 320 vs 318 ms per
+  // C4 solve); FC_SLICE_THREADS overrides (diagnostic)
+  static const int sthr = getenv("FC_SLICE_THREADS") ? atoi(getenv("FC_SLICE_THREADS")) : 512;
+  static bool qattr = false;
+  if (!qattr) {
+    FC_CUDA_TRY(cudaFuncSetAttribute(slice_svd_qrj_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)kSliceSmem));
+    qattr = true;
+  }
   if (!no_qr && qsm <= kSliceSmem) {
-    static bool qattr = false;
-    if (!qattr) {
-      FC_CUDA_TRY(cudaFuncSetAttribute(slice_svd_qrj_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)kSliceSmem));
-      qattr = true;
-    }
-    // 512 threads (1024, i.e. 16 lanes per Jacobi column pair, measured slower: 320 vs 318 ms per
-    // C4 solve); FC_SLICE_THREADS overrides (diagnostic)
-    static const int sthr = getenv("FC_SLICE_THREADS") ? atoi(getenv("FC_SLICE_THREADS")) : 512;
-    slice_svd_qrj_kernel<<<ns, sthr, qsm, st>>>(ra, rb, S, sv, Ua, Vb);
+    slice_svd_qrj_kernel<true><<<ns, sthr, qsm, st>>>(ra, rb, S, sv, Ua, Vb, nullptr);
+  } else if (!no_qr) {
+    // QR-preconditioned Jacobi with the matrices in an L2-resident global workspace
+    double* qws = s.alloc<double>((size_t)ns * ((size_t)rows * cols + 2 * (size_t)(cols | 1) * cols));
+    const size_t small = (5 * (size_t)cols) * 8 + 64;
+    slice_svd_qrj_kernel<false><<<ns, sthr, small, st>>>(ra, rb, S, sv, Ua, Vb, qws);
   } else if (gws) {
     slice_svd_kernel<false><<<ns, 512, smem, st>>>(ra, rb, S, sv, Ua, Vb, gws);
   } else {
