@@ -381,6 +381,23 @@ __device__ double block_sum(double v, double* red) {
   return red[32];
 }
 
+// block_sum without the leading barrier: only for call sites where every earlier reader of `red`
+// is separated from this call by another block-wide barrier
+__device__ double block_sum_nl(double v, double* red) {
+  for (int s = 16; s > 0; s >>= 1) v += __shfl_down_sync(0xffffffffu, v, s);
+  const int w = threadIdx.x >> 5, ln = threadIdx.x & 31;
+  if (ln == 0) red[w] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (threadIdx.x < 32) {
+    t = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+    for (int s = 16; s > 0; s >>= 1) t += __shfl_down_sync(0xffffffffu, t, s);
+    if (threadIdx.x == 0) red[32] = t;
+  }
+  __syncthreads();
+  return red[32];
+}
+
 // NaN-propagating maximum (a NaN anywhere makes the result NaN)
 __device__ __forceinline__ double nan_max(double a, double b) { return (b > a || b != b) ? b : a; }
 
@@ -522,7 +539,7 @@ __global__ void __launch_bounds__(1024) tridiag_packed_kernel(const __grid_const
     const double x0 = colk[0];
     double part = 0.0;
     for (int i = tid + 1; i < m; i += nt) part += colk[i] * colk[i];
-    const double sig = block_sum(part, red);
+    const double sig = block_sum_nl(part, red);   // previous use: >= 3 barriers back
     const bool skip = (sig == 0.0);
     double alpha = x0;
     if (!skip) {
@@ -551,7 +568,7 @@ __global__ void __launch_bounds__(1024) tridiag_packed_kernel(const __grid_const
       __syncthreads();
       double kp = 0.0;
       for (int i = tid; i < m; i += nt) kp += u[i] * p[i];
-      const double K = block_sum(kp, red);
+      const double K = block_sum_nl(kp, red);    // previous use: >= 2 barriers back
       for (int i = tid; i < m; i += nt) p[i] -= K * u[i];
       __syncthreads();
       for (int jj = warp; jj < m; jj += NW) {
@@ -645,7 +662,7 @@ __global__ void __launch_bounds__(1024, 1) tridiag_cluster_kernel(const __grid_c
     const double x0 = col[s + 1];
     double part = 0.0;
     for (int i = s + 2 + tid; i < N; i += nt) part += col[i] * col[i];
-    const double sig = block_sum(part, red);
+    const double sig = block_sum_nl(part, red);   // previous use (phase 4) is >= 2 barriers back
     double alpha = x0;
     if (sig == 0.0) {
       for (int i = s + 1 + tid; i < N; i += nt) uu[i] = 0.0;
@@ -726,10 +743,11 @@ __global__ void __launch_bounds__(1024, 1) tridiag_cluster_kernel(const __grid_c
       q[i] = cl.map_shared_rank(ps, o)[i - o * SL];
       col[i] = cl.map_shared_rank(ncs, o)[i - o * SL];
     }
-    __syncthreads();
+    // no barrier: this thread's u . q partial reads only the q[i] it just gathered (and u from
+    // the previous step, already behind barriers); the barrier inside block_sum_nl orders the rest
     double kp = 0.0;
     for (int i = s + 1 + tid; i < N; i += nt) kp += u[i] * q[i];
-    const double K = block_sum(kp, red);
+    const double K = block_sum_nl(kp, red);
     for (int i = s + 1 + tid; i < N; i += nt) q[i] -= K * u[i];
     __syncthreads();
     {
