@@ -1416,18 +1416,20 @@ __device__ __forceinline__ void block_dots(const double* V, const double* x, int
   }
 }
 
-// x[i] -= sum_{a < na} coef[a] V[i, a]  (4 threads per row)
+// x[i] -= sum_{a < na} coef[a] V[i, a]: 2 threads per row — lanes 0-15 and 16-31 of a warp take
+// the same 16 consecutive rows, the even / odd columns, combined by one shuffle (with the odd
+// leading dimension every bank is hit exactly twice per load: conflict-free)
 template <int LD, int RB>
 __device__ __forceinline__ void block_update(const double* V, double* x, int nr, int na, const double* coef) {
   const int tid = threadIdx.x, nt = blockDim.x;
-  for (int base = 0; base < RB * 4; base += nt) {
-    const int idx = base + tid, i = idx >> 2, qd = idx & 3;
+  for (int base = 0; base < RB * 2; base += nt) {
+    const int idx = base + tid, ln = idx & 31;
+    const int i = (idx >> 5) * 16 + (ln & 15), half = ln >> 4;
     double v = 0.0;
     if (i < nr)
-      for (int a = qd; a < na; a += 4) v = fma(coef[a], V[i + (size_t)a * LD], v);
-    v += __shfl_xor_sync(0xffffffffu, v, 1);
-    v += __shfl_xor_sync(0xffffffffu, v, 2);
-    if (qd == 0 && i < nr) x[i] -= v;
+      for (int a = half; a < na; a += 2) v = fma(coef[a], V[i + (size_t)a * LD], v);
+    v += __shfl_xor_sync(0xffffffffu, v, 16);
+    if (half == 0 && i < nr) x[i] -= v;
   }
 }
 
