@@ -1580,8 +1580,11 @@ TT truncate_tt(fc_ctx c, const TT& xin, double eps, int rank_cap, TruncStats* st
                                                                    Chat[1] + (size_t)tt0 * r[1], KR);
       FC_CHECK_LAUNCH();
       int tiles = cdiv((long long)r12, 64) * cdiv(r[2], 64);
+      // split-K sized for ~8 waves of 148 SMs (1-2 waves of 64x64 tiles left a half-empty last wave;
+      // C4 solve 311 ms vs 313 ms with 2 or 4 waves)
+      static const int core_waves = getenv("FC_CORE_WAVES") ? atoi(getenv("FC_CORE_WAVES")) : 8;
       dgemm(st, 0, 1, (int)r12, r[2], m, 1.0, KR, (int)r12, Chat[2] + (size_t)tt0 * r[2], r[2], 1.0, core, (int)r12,
-            std::max(1, std::min(cdiv(m, 64), std::max(1, 296 / std::max(tiles, 1)))));
+            std::max(1, std::min(cdiv(m, 64), std::max(1, cdiv(core_waves * 148, std::max(tiles, 1))))));
     }
   }
   pm.mark(ss ? "6 core (structured)" : "6 core (cp)");
