@@ -1007,6 +1007,12 @@ constexpr double kQrBasisTol = 1e-14;
 
 // spectral terms per chunk of the structured norm / Gram pass: t x (Rx * chunk) <= 2^27 doubles
 constexpr size_t kStructChunk = (size_t)1 << 27;
+// split-K target of the side-Gram GEMMs, in waves of 148 SMs (FC_GRAM_WAVES)
+int gram_waves() {
+  static const int w = getenv("FC_GRAM_WAVES") ? atoi(getenv("FC_GRAM_WAVES")) : 8;   // 8: 312 ms vs 316 ms (3)
+  return w;
+}
+
 int struct_chunk(const StructuredS* ss) {
   const int tmax = std::max(ss->t[0], std::max(ss->t[1], ss->t[2]));
   const size_t per = (size_t)std::max(tmax, 1) * std::max(ss->Rx, 1);
@@ -1231,7 +1237,7 @@ TT truncate_tt(fc_ctx c, const TT& xin, double eps, int rank_cap, TruncStats* st
     }
     gemm(gq, st);
     m.beta = 1.0;
-    m.splitk = std::max(1, std::min(cdiv(minkd, 128), std::max(1, 148 * 3 / std::max(tiles, 1))));
+    m.splitk = std::max(1, std::min(cdiv(minkd, 128), std::max(1, cdiv(gram_waves() * 148, std::max(tiles, 1)))));
     gemm(m, st);
   } else {
     for (int l = 0; l < 3; ++l) {
@@ -1249,7 +1255,7 @@ TT truncate_tt(fc_ctx c, const TT& xin, double eps, int rank_cap, TruncStats* st
       m.b[l] = GemmBatch{q[l], q[l], R, Bm[l], q[l], Bm[l], q[l], M[l], q[l], nullptr, 0, nullptr};
       tiles += cdiv(q[l], 64) * cdiv(q[l], 64);
     }
-    m.splitk = std::max(1, std::min(cdiv(R, 128), std::max(1, 148 * 3 / std::max(tiles, 1))));
+    m.splitk = std::max(1, std::min(cdiv(R, 128), std::max(1, cdiv(gram_waves() * 148, std::max(tiles, 1)))));
     gemm(m, st);
   }
   pm.mark("3 side Gram");
