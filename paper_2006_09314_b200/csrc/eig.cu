@@ -1843,6 +1843,10 @@ __global__ void __launch_bounds__(kBcgsClusterThreads, 1)
     E.Y[(size_t)(r0 + i) + (size_t)a * n] = a < na ? S.Yb[i + (size_t)a * LD] : 0.0;
   }
   if (r == 0 && tid == 0) *E.nacc = na;
+  {   // zero the projection scratch P for this block's BCGS2 pass (replaces a host memset)
+    const int kup = min(E.k_base + j0, E.kcap);
+    for (long long idx = (long long)r * nt + tid; idx < (long long)kup * W; idx += (long long)CS * nt) E.P[idx] = 0.0;
+  }
   cl.sync();                                                 // smem stays alive for readers
 }
 
@@ -1879,6 +1883,10 @@ __global__ void __launch_bounds__(kBcgsClusterThreads, 1)
       E.Q[(size_t)(r0 + i) + (size_t)(k0 + c) * E.ldq] = v;
     }
     if (r == 0 && tid == 0) *E.k = k0 + na;
+    {   // zero the projection scratch P for the next block's first pass (replaces a host memset)
+      const int kup = min(E.k_base + j0 + W, E.kcap);
+      for (long long idx = (long long)r * nt + tid; idx < (long long)kup * W; idx += (long long)CS * nt) E.P[idx] = 0.0;
+    }
     return;
   }
   for (int c = 0; c < na; ++c) {
@@ -1904,6 +1912,10 @@ __global__ void __launch_bounds__(kBcgsClusterThreads, 1)
   }
   cl.sync();
   if (r == 0 && tid == 0) *E.k = k0 + na;
+  {
+    const int kup = min(E.k_base + j0 + W, E.kcap);
+    for (long long idx = (long long)r * nt + tid; idx < (long long)kup * W; idx += (long long)CS * nt) E.P[idx] = 0.0;
+  }
 }
 
 __global__ void set_int_kernel(int* p, int v) { *p = v; }
@@ -2358,6 +2370,7 @@ void bcgs(const BcgsBatch& bin, cudaStream_t st) {
   for (int i = 0; i < b.nb; ++i) {
     BcgsEntry& E = b.e[i];
     FC_CUDA_TRY(cudaMemsetAsync(E.Q, 0, (size_t)E.ldq * E.kcap * 8, st));
+    FC_CUDA_TRY(cudaMemsetAsync(E.P, 0, (size_t)E.kcap * kBcgsW * 8, st));   // the cluster kernels re-zero it
     const int kb = std::min(std::max(E.k_base, 0), std::min(E.p, E.kcap));
     E.k_base = kb;
     set_int_kernel<<<1, 1, 0, st>>>(E.k, kb);
@@ -2390,7 +2403,7 @@ void bcgs(const BcgsBatch& bin, cudaStream_t st) {
         const int wb = std::min(W, E.p - j0), kup = std::min(E.k_base + j0, E.kcap);
         if (kup == 0) continue;
         kmx = std::max(kmx, kup);
-        FC_CUDA_TRY(cudaMemsetAsync(E.P, 0, (size_t)kup * W * 8, st));
+        if (cfg == 0) FC_CUDA_TRY(cudaMemsetAsync(E.P, 0, (size_t)kup * W * 8, st));
         p.b[nb] = GemmBatch{kup, wb, E.n, E.Q, E.ldq, E.A + (size_t)j0 * E.lda, E.lda, E.P, kup, nullptr, 0, nullptr};
         u.b[nb] = GemmBatch{E.n, wb, kup, E.Q, E.ldq, E.P, kup, E.A + (size_t)j0 * E.lda, E.lda, nullptr, 0, nullptr};
         if (dyn_k) {               // only the first *E.k columns of Q are nonzero
@@ -2421,7 +2434,7 @@ void bcgs(const BcgsBatch& bin, cudaStream_t st) {
         const int kup = std::min(E.k_base + j0, E.kcap);
         if (kup == 0) continue;
         kmx = std::max(kmx, kup);
-        FC_CUDA_TRY(cudaMemsetAsync(E.P, 0, (size_t)kup * W * 8, st));
+        if (cfg == 0) FC_CUDA_TRY(cudaMemsetAsync(E.P, 0, (size_t)kup * W * 8, st));
         p.b[nb] = GemmBatch{kup, W, E.n, E.Q, E.ldq, E.Y, E.n, E.P, kup, nullptr, 0, nullptr};
         u.b[nb] = GemmBatch{E.n, W, kup, E.Q, E.ldq, E.P, kup, E.Y, E.n, nullptr, 0, nullptr};
         if (dyn_k) {
