@@ -1530,9 +1530,20 @@ TT truncate_tt(fc_ctx c, const TT& xin, double eps, int rank_cap, TruncStats* st
     // Tucker route: beta = sum_kk wF[kk] core_x x_1 H1_kk x_2 H2_kk x_3 H3_kk,
     // H_l,kk = Z_l^T diag(u_l,kk) xhat_l = Y_r^T Rm_kk (r_l x t_l): Hall_l = Y_r^T RmE_l
     double* Hall[3];
-    for (int l = 0; l < 3; ++l) {
-      Hall[l] = s.alloc<double>((size_t)r[l] * ss->t[l] * ss->r);
-      dgemm(st, 1, 0, r[l], ss->t[l] * ss->r, q[l], 1.0, Y[l], q[l], RmE[l], q[l], 0.0, Hall[l], r[l]);
+    {   // the three modes in one batched launch (split-K over the basis dimension)
+      GemmArgs gh;
+      gh.transA = 1;
+      gh.beta = 1.0;
+      gh.nbatch = 3;
+      int tiles = 0, minq = INT32_MAX;
+      for (int l = 0; l < 3; ++l) {
+        Hall[l] = s.zeros<double>((size_t)r[l] * ss->t[l] * ss->r);
+        gh.b[l] = GemmBatch{r[l], ss->t[l] * ss->r, q[l], Y[l], q[l], RmE[l], q[l], Hall[l], r[l], nullptr, 0, nullptr};
+        tiles += cdiv(r[l], 64) * cdiv((long long)ss->t[l] * ss->r, 64);
+        minq = std::min(minq, q[l]);
+      }
+      gh.splitk = std::max(1, std::min(cdiv(minq, 64), cdiv(gram_waves() * 148, std::max(tiles, 1))));
+      gemm(gh, st);
     }
     const int t0 = ss->t[0], t1 = ss->t[1], t2 = ss->t[2], r0 = r[0], r1 = r[1], r2 = r[2];
     const int NB = kMaxBatch;
