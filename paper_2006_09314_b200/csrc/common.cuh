@@ -144,6 +144,20 @@ struct GemmArgs {
 void gemm(const GemmArgs& a, cudaStream_t st);
 // fc_profile_gemm: enable -> start recording; disable -> totals of the recorded launches
 void gemm_profile(bool enable, double* ms, double* flops, long long* launches);
+// split-K factor giving ~`waves` waves of 64 x 64 tiles on 148 SMs (at least 64 of K per split);
+// the caller zeroes C and sets beta = 1 (atomic epilogue)
+inline int waves_splitk(const GemmArgs& a, int waves) {
+  long long tiles = 0;
+  int minK = 1 << 30;
+  for (int i = 0; i < a.nbatch; ++i) {
+    tiles += (long long)a.rep * ((a.b[i].M + 63) / 64) * ((a.b[i].N + 63) / 64);
+    minK = a.b[i].K < minK ? a.b[i].K : minK;
+  }
+  const long long want = (waves * 148LL + (tiles > 0 ? tiles : 1) - 1) / (tiles > 0 ? tiles : 1);
+  const long long kmax = (minK + 63) / 64;
+  const long long sk = want < kmax ? want : kmax;
+  return sk > 1 ? (int)sk : 1;
+}
 // convenience single GEMM
 void dgemm(cudaStream_t st, int transA, int transB, int M, int N, int K, double alpha,
            const double* A, int lda, const double* B, int ldb, double beta, double* C, int ldc,

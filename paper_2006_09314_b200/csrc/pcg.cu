@@ -149,6 +149,10 @@ TT apply_truncate_tt(fc_ctx c, SpecCP& sp, const TT& x, double eps, int rank_cap
     p += (size_t)n * x.q[l];
     fwd.b[l] = GemmBatch{n, x.q[l], n, c->Vsp(sp, l), n, x.Q[l], n, Zh[l], n, nullptr, 0, nullptr};
   }
+  // ~100 output tiles for 148 SMs with K = n: split-K (zeroed output, beta = 1)
+  FC_CUDA_TRY(cudaMemsetAsync(Zh[0], 0, (size_t)n * (x.q[0] + x.q[1] + x.q[2]) * 8, st));
+  fwd.beta = 1.0;
+  fwd.splitk = waves_splitk(fwd, 8);
   gemm(fwd, st);
   StructuredS ss;
   ss.r = r;
@@ -175,16 +179,22 @@ TT apply_truncate_tt(fc_ctx c, SpecCP& sp, const TT& x, double eps, int rank_cap
   // S7: back to physical coordinates, only the surviving basis columns
   GemmArgs inv;
   inv.nbatch = 0;
-  std::vector<DevMem> newQ;
-  for (int l = 0; l < 3; ++l) {
-    if (out.R == 0) break;
-    newQ.emplace_back((size_t)n * out.q[l] * 8, st);
-    inv.b[inv.nbatch++] = GemmBatch{n, out.q[l], n, c->Vsp(sp, l), n, out.Q[l], n, newQ.back().d(), n, nullptr, 0, nullptr};
-  }
-  if (inv.nbatch) {
+  if (out.R > 0) {
+    const size_t tot = (size_t)n * (out.q[0] + out.q[1] + out.q[2]);
+    DevMem newQ(tot * 8, st);
+    FC_CUDA_TRY(cudaMemsetAsync(newQ.d(), 0, tot * 8, st));
+    double* nq[3];
+    size_t off = 0;
+    for (int l = 0; l < 3; ++l) {
+      nq[l] = newQ.d() + off;
+      off += (size_t)n * out.q[l];
+      inv.b[inv.nbatch++] = GemmBatch{n, out.q[l], n, c->Vsp(sp, l), n, out.Q[l], n, nq[l], n, nullptr, 0, nullptr};
+    }
+    inv.beta = 1.0;
+    inv.splitk = waves_splitk(inv, 8);
     gemm(inv, st);
     for (int l = 0; l < 3; ++l)
-      FC_CUDA_TRY(cudaMemcpyAsync(out.Q[l], newQ[l].d(), (size_t)n * out.q[l] * 8, cudaMemcpyDeviceToDevice, st));
+      FC_CUDA_TRY(cudaMemcpyAsync(out.Q[l], nq[l], (size_t)n * out.q[l] * 8, cudaMemcpyDeviceToDevice, st));
   }
   pm1.mark("9 back-transform");
   return out;

@@ -1512,10 +1512,12 @@ TT truncate_tt(fc_ctx c, const TT& xin, double eps, int rank_cap, TruncStats* st
   {
     GemmArgs gz;
     gz.nbatch = 3;
+    gz.beta = 1.0;
     for (int l = 0; l < 3; ++l) {
-      Z[l] = s.alloc<double>((size_t)n * r[l]);
+      Z[l] = s.zeros<double>((size_t)n * r[l]);
       gz.b[l] = GemmBatch{n, r[l], q[l], Qo[l], n, Y[l], q[l], Z[l], n, nullptr, 0, nullptr};
     }
+    gz.splitk = waves_splitk(gz, 8);   // ~100 tiles for 148 SMs: split over the basis dimension
     gemm(gz, st);
   }
   pm.mark("5 Z");
