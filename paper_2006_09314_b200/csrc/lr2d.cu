@@ -325,11 +325,13 @@ LR2 lr2_truncate(cudaStream_t st, const LR2& x, double eps, int rank_cap, int* r
   double* C[2];
   GemmArgs g;
   g.transA = 1;
+  g.beta = 1.0;
   g.nbatch = 2;
   for (int l = 0; l < 2; ++l) {
-    C[l] = s.alloc<double>((size_t)q[l] * R);
+    C[l] = s.zeros<double>((size_t)q[l] * R);
     g.b[l] = GemmBatch{q[l], R, n, Q[l], n, x.U[l], n, C[l], q[l], nullptr, 0, nullptr};
   }
+  g.splitk = waves_splitk(g, 8);   // few output tiles, K = n
   gemm(g, st);
   scale_cols2_kernel<<<nblk2((long long)q[0] * R), 256, 0, st>>>(q[0], R, x.w, C[0]);
   FC_CHECK_LAUNCH();
@@ -359,8 +361,11 @@ LR2 lr2_truncate(cudaStream_t st, const LR2& x, double eps, int rank_cap, int* r
   FC_CUDA_TRY(cudaMemcpyAsync(y.w, sv, (size_t)r * 8, cudaMemcpyDeviceToDevice, st));
   GemmArgs z;
   z.nbatch = 2;
+  z.beta = 1.0;
+  FC_CUDA_TRY(cudaMemsetAsync(y.U[0], 0, (size_t)2 * n * r * 8, st));   // U[0], U[1] contiguous
   z.b[0] = GemmBatch{n, r, q[0], Q[0], n, Ua, q[0], y.U[0], n, nullptr, 0, nullptr};
   z.b[1] = GemmBatch{n, r, q[1], Q[1], n, Vb, q[1], y.U[1], n, nullptr, 0, nullptr};
+  z.splitk = waves_splitk(z, 8);
   gemm(z, st);
   return y;
 }
@@ -375,9 +380,12 @@ LR2 lr2_apply_hat(fc_ctx c, const Spec2& sp, const LR2& x) {
   double* Xh = s.alloc<double>((size_t)2 * n * R);
   GemmArgs f;                                                      // forward transform
   f.transA = 1;
+  f.beta = 1.0;
   f.nbatch = 2;
+  FC_CUDA_TRY(cudaMemsetAsync(Xh, 0, (size_t)2 * n * R * 8, st));
   for (int l = 0; l < 2; ++l)
     f.b[l] = GemmBatch{n, R, n, c->V_l(l), n, x.U[l], n, Xh + (size_t)l * n * R, n, nullptr, 0, nullptr};
+  f.splitk = waves_splitk(f, 8);
   gemm(f, st);
   for (int l = 0; l < 2; ++l) {
     hadamard2_kernel<<<nblk2((long long)n * r * R), 256, 0, st>>>(n, r, sp.Ul(n, l), n, R, Xh + (size_t)l * n * R, n,
@@ -394,11 +402,13 @@ void lr2_inverse(fc_ctx c, LR2& y) {
   if (y.R == 0) return;
   cudaStream_t st = c->st;
   Scratch s(st);
-  double* T = s.alloc<double>((size_t)2 * y.n * y.R);
+  double* T = s.zeros<double>((size_t)2 * y.n * y.R);
   GemmArgs g;
   g.nbatch = 2;
+  g.beta = 1.0;
   for (int l = 0; l < 2; ++l)
     g.b[l] = GemmBatch{y.n, y.R, y.n, c->V_l(l), y.n, y.U[l], y.n, T + (size_t)l * y.n * y.R, y.n, nullptr, 0, nullptr};
+  g.splitk = waves_splitk(g, 8);
   gemm(g, st);
   for (int l = 0; l < 2; ++l)
     FC_CUDA_TRY(cudaMemcpyAsync(y.U[l], T + (size_t)l * y.n * y.R, (size_t)y.n * y.R * 8, cudaMemcpyDeviceToDevice,
