@@ -767,6 +767,12 @@ __global__ void transpose_kernel(int rows, int cols, const double* __restrict__ 
   }
 }
 
+// A[i + j q] = (i == j) for a q x q block (A pre-zeroed)
+__global__ void eye_kernel(int q, double* A) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < q) A[i + (size_t)i * q] = 1.0;
+}
+
 __global__ void square_into_kernel(int k, const double* __restrict__ s, double* s2) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < k) s2[i] = s[i] * s[i];
@@ -1354,11 +1360,54 @@ TT truncate_tt(fc_ctx c, const TT& xin, double eps, int rank_cap, TruncStats* st
       if (refine[l]) hr[l] = q[l];
     FC_CUDA_TRY(cudaMemcpyAsync(rl, hr, 3 * sizeof(int), cudaMemcpyHostToDevice, st));
   }
+  // refined modes: only the pk eigenvectors above the noise level are computed by inverse iteration
+  // (the noise subspace needs just an orthonormal basis: it is re-diagonalised from the data below;
+  // FC_REFINE_ALL_VECTORS: inverse iteration for all q vectors, the previous design)
+  static const bool refine_all = getenv("FC_REFINE_ALL_VECTORS") != nullptr;
+  int pkv[3] = {0, 0, 0};
+  for (int l = 0; l < 3; ++l) {
+    if (!refine[l]) continue;
+    std::vector<double> hl(q[l]);
+    FC_CUDA_TRY(cudaMemcpyAsync(hl.data(), lam[l], (size_t)q[l] * 8, cudaMemcpyDeviceToHost, st));
+    FC_CUDA_TRY(cudaStreamSynchronize(st));
+    const double noise = kNoise * q[l] * 2.220446049250313e-16 * lam0[l];
+    while (pkv[l] < q[l] && hl[pkv[l]] > noise) ++pkv[l];
+  }
   if (eb.nb) {
     int hr[3] = {0, 0, 0};
     for (int l = 0; l < 3; ++l)
-      if (ebmap[l] >= 0) hr[ebmap[l]] = refine[l] ? q[l] : r[l];
+      if (ebmap[l] >= 0) hr[ebmap[l]] = refine[l] ? (refine_all ? q[l] : std::max(pkv[l], 1)) : r[l];
+    if (any_refine) {   // the device-side counts must match
+      int hd[3] = {r[0], r[1], r[2]};
+      for (int l = 0; l < 3; ++l)
+        if (refine[l]) hd[l] = refine_all ? q[l] : std::max(pkv[l], 1);
+      FC_CUDA_TRY(cudaMemcpyAsync(rl, hd, 3 * sizeof(int), cudaMemcpyHostToDevice, st));
+    }
     syev_vectors(eb, maxq, st, hr);
+  }
+  if (any_refine && !refine_all) {
+    // orthonormal basis of the complement of the trusted vectors: blocked Gram-Schmidt of
+    // [Y_t | I_q] seeded with the orthonormal Y_t (k_base = pk) -> columns pk..q-1 of Y
+    for (int l = 0; l < 3; ++l) {
+      if (!refine[l] || pkv[l] >= q[l]) continue;
+      const int ql = q[l], pk = pkv[l];
+      Scratch sc(st);
+      double* A = sc.zeros<double>((size_t)ql * (pk + ql));
+      if (pk > 0) FC_CUDA_TRY(cudaMemcpyAsync(A, Y[l], (size_t)ql * pk * 8, cudaMemcpyDeviceToDevice, st));
+      eye_kernel<<<blocks_for(ql), 256, 0, st>>>(ql, A + (size_t)ql * pk);
+      FC_CHECK_LAUNCH();
+      BcgsBatch cb;
+      int* kd = sc.zeros<int>(1);
+      double* Qc = sc.alloc<double>((size_t)ql * ql);
+      cb.e[cb.nb++] = BcgsEntry{ql, pk + ql, A, ql, Qc, ql, ql, kd, sc.alloc<double>(pk + ql),
+                                sc.alloc<double>((size_t)ql * kBcgsW), kBasisTol};
+      cb.e[0].k_base = pk;
+      bcgs(cb, st);
+      const int kc = read_int(kd, st);
+      require(kc == ql, FC_ERR_CUDA, "noise-subspace complement basis incomplete");
+      FC_CUDA_TRY(cudaMemcpyAsync(Y[l] + (size_t)pk * ql, Qc + (size_t)pk * ql, (size_t)ql * (ql - pk) * 8,
+                                  cudaMemcpyDeviceToDevice, st));
+    }
   }
   if (any_refine) {
     for (int l = 0; l < 3; ++l) {
@@ -1422,15 +1471,22 @@ TT truncate_tt(fc_ctx c, const TT& xin, double eps, int rank_cap, TruncStats* st
       gb.e[gb.nb++] = SyevEntry{m, G, m, s.alloc<double>(m), s.alloc<double>(m), mu, Vn, m, rm,
                                 s.alloc<double>((size_t)6 * m * m)};
       syev_values(gb, st);
-      syev_vectors(gb, m, st, &m);
-      // s2 = [trusted eigenvalues ; mu], the noise-subspace vectors rotated: Y_ns <- Y_ns V_ns
+      // s2 = [trusted eigenvalues ; mu] and the cut; then only the (r - pk) leading eigenvectors of
+      // G_ns are computed and the noise-subspace vectors rotated: Y_ns[:, :r-pk] <- Y_ns V_ns
       double* s2r = s.alloc<double>(ql);
       FC_CUDA_TRY(cudaMemcpyAsync(s2r, lam[l], (size_t)pk * 8, cudaMemcpyDeviceToDevice, st));
       FC_CUDA_TRY(cudaMemcpyAsync(s2r + pk, mu, (size_t)m * 8, cudaMemcpyDeviceToDevice, st));
-      double* Yr = s.alloc<double>((size_t)ql * m);
-      dgemm(st, 0, 0, ql, m, m, 1.0, Yns, ql, Vn, m, 0.0, Yr, ql);
-      FC_CUDA_TRY(cudaMemcpyAsync(Yns, Yr, (size_t)ql * m * 8, cudaMemcpyDeviceToDevice, st));
       rank_cut_device(ql, s2r, 0.25 * eps * eps, energy, rl + l, margins + l, st);
+      const int rcut = read_int(rl + l, st);
+      const int nv = refine_all ? m : std::max(0, std::min(rcut, ql) - pk);
+      if (nv > 0) {
+        FC_CUDA_TRY(cudaMemcpyAsync(rm, &nv, sizeof(int), cudaMemcpyHostToDevice, st));
+        int nvh = nv;
+        syev_vectors(gb, m, st, &nvh);
+        double* Yr = s.alloc<double>((size_t)ql * nv);
+        dgemm(st, 0, 0, ql, nv, m, 1.0, Yns, ql, Vn, m, 0.0, Yr, ql);
+        FC_CUDA_TRY(cudaMemcpyAsync(Yns, Yr, (size_t)ql * nv * 8, cudaMemcpyDeviceToDevice, st));
+      }
     }
     int r_gram[3] = {r[0], r[1], r[2]};
     FC_CUDA_TRY(cudaMemcpyAsync(r, rl, 3 * sizeof(int), cudaMemcpyDeviceToHost, st));
