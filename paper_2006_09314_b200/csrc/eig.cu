@@ -2184,7 +2184,9 @@ void syev_vectors(const SyevBatch& b, int maxN, cudaStream_t st, const int* r_ho
       }
       if (ng == 0) break;
       g.nbatch = h.nbatch = ng;
-      g.splitk = std::max(1, std::min(cdiv(maxN, 64), cdiv(2 * 148, std::max(tiles, 1))));
+      // split-K for ~`pw` waves of 148 SMs (FC_POLAR_WAVES overrides; diagnostics)
+      static const int pw = getenv("FC_POLAR_WAVES") ? atoi(getenv("FC_POLAR_WAVES")) : 2;
+      g.splitk = std::max(1, std::min(cdiv(maxN, 64), cdiv(pw * 148, std::max(tiles, 1))));
       FC_CUDA_TRY(cudaMemsetAsync(Gall, 0, gsz * 8, st));
       gemm(g, st);
       ns_polar_kernel<<<b.nb, 1024, (size_t)rmax * 8, st>>>(P, step);

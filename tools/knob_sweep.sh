@@ -1,6 +1,7 @@
 # Knob sweep on the C4 bench: one bench line per environment setting (diagnostics only).
+# usage: bash tools/knob_sweep.sh "BASE=1" "FC_POLAR_WAVES=4" ...
 mkdir -p gpurun_out
-for kv in "BASE=1" "FC_TRI_THREADS=256" "FC_TRI_THREADS=384" "FC_TRI_PACKED_THREADS=512" "FC_SKINNY_WAVES=1" "FC_SKINNY_WAVES=4" "BASE=2"; do
+for kv in "$@"; do
   env $kv timeout 240 python bench.py --steps 5 --warmup 3 > gpurun_out/ks.log 2>&1
   python - "$kv" <<'PY'
 import json, sys
