@@ -319,7 +319,19 @@ def apply_roofline(ctx, L, n, R=64, r=16, reps=10):
             "cell": {"n": n, "R": R, "r": r}, "bound": "tensor", "achieved": ach,
             "peak": FP64_DMMA_TFLOPS, "unit": "TFLOP/s", "frac": ach / FP64_DMMA_TFLOPS,
             "peak_source": "measured DMMA m8n8k4 FP64 peak (tools/peak_fp64.cu); MEASURED_PEAKS.json has no FP64 entry",
-            "traffic": None, "ms": t}
+            "traffic": kr_traffic(n, R, r), "ms": t}
+
+
+def kr_traffic(n, R, r):
+    """DRAM bytes (read + write) of one fused KR inverse-transform launch at this C5 cell, from the
+    committed `ncu --set full` capture (profiles/r01h_kr_traffic.json), or None."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "r01h_kr_traffic.json")))
+    except (OSError, ValueError):
+        return None
+    if (d.get("n"), d.get("R"), d.get("r")) != (n, R, r):
+        return None
+    return d["dram_bytes"]
 
 
 if __name__ == "__main__":
