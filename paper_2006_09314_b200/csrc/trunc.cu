@@ -869,9 +869,9 @@ void small_svd(cudaStream_t st, int ra, int rb, int ns, const double* S, double*
   }
   static const bool no_qr = getenv("FC_SLICE_NO_QR") != nullptr;
   const size_t qsm = slice_qrj_smem(rows, cols);
-  // 512 threads (1024, i.e. 16 lanes per Jacobi column pair, measured slower: 320 vs 318 ms per
-  // C4 solve); FC_SLICE_THREADS overrides (diagnostic)
-  static const int sthr = getenv("FC_SLICE_THREADS") ? atoi(getenv("FC_SLICE_THREADS")) : 512;
+  // 768 threads: C4 44.0 iters/s vs 43.4 with 512, 43.9 with 640 and 43.3 with 1024
+  // (profiles/r01h_knob_sweep_slice.txt); FC_SLICE_THREADS overrides (diagnostic)
+  static const int sthr = getenv("FC_SLICE_THREADS") ? atoi(getenv("FC_SLICE_THREADS")) : 768;
   static bool qattr = false;
   if (!qattr) {
     FC_CUDA_TRY(cudaFuncSetAttribute(slice_svd_qrj_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
