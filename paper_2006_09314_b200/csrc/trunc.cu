@@ -871,7 +871,10 @@ void small_svd(cudaStream_t st, int ra, int rb, int ns, const double* S, double*
   const size_t qsm = slice_qrj_smem(rows, cols);
   // 768 threads: C4 44.0 iters/s vs 43.4 with 512, 43.9 with 640 and 43.3 with 1024
   // (profiles/r01h_knob_sweep_slice.txt); FC_SLICE_THREADS overrides (diagnostic)
-  static const int sthr = getenv("FC_SLICE_THREADS") ? atoi(getenv("FC_SLICE_THREADS")) : 768;
+  static const int sthr_env = getenv("FC_SLICE_THREADS") ? atoi(getenv("FC_SLICE_THREADS")) : 768;
+  // FC_SLICE_THREADS=0 (diagnostic): 16 lanes per Jacobi column pair, every pair in one pass
+  const int sthr = sthr_env > 0 ? sthr_env
+                                : std::min(1024, std::max(256, ((16 * ((std::min(ra, rb) + 1) / 2)) + 31) / 32 * 32));
   static bool qattr = false;
   if (!qattr) {
     FC_CUDA_TRY(cudaFuncSetAttribute(slice_svd_qrj_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
