@@ -254,6 +254,14 @@ int pcg_solve_2d(fc_ctx ctx, const fc_lr2* b, const fc_params* p, fc_lr2* u, fc_
 /* C = alpha*op(A)*op(B) + beta*C, FP64, column-major, DMMA tiles; all pointers device.   */
 int fc_dgemm(fc_ctx ctx, int transA, int transB, int M, int N, int K, double alpha,
              const double* A, int lda, const double* B, int ldb, double beta, double* C, int ldc);
+/* fc_dgemm with the K range split over `splitk` CTAs per output tile (splitk >= 1; clamped to 8 on
+ * the 128x128-tile path and to 64 otherwise).  The partial tiles are summed in a fixed split order
+ * (thread-block-cluster DSMEM reduction up to 16 splits, a global workspace above), so the result
+ * is bit-identical from run to run for the same arguments; C is not read when beta == 0.
+ * splitk < 1 -> FC_ERR_INVALID_ARG. */
+int fc_dgemm_splitk(fc_ctx ctx, int transA, int transB, int M, int N, int K, double alpha,
+                    const double* A, int lda, const double* B, int ldb, double beta, double* C, int ldc,
+                    int splitk);
 /* Milliseconds of the last launch of the dominant kernel of the last API call (events on
  * the context stream) and its algorithmic flop and byte counts (for the roofline line). */
 int fc_last_kernel_stats(fc_ctx ctx, double* ms, double* flops, double* bytes, int* launches);

@@ -529,6 +529,21 @@ int fc_dgemm(fc_ctx c, int transA, int transB, int M, int N, int K, double alpha
   });
 }
 
+int fc_dgemm_splitk(fc_ctx c, int transA, int transB, int M, int N, int K, double alpha, const double* A, int lda,
+                    const double* B, int ldb, double beta, double* C, int ldc, int splitk) {
+  return guard(c, [&]() {
+    require(M >= 0 && N >= 0 && K >= 0, FC_ERR_INVALID_ARG, "dims");
+    require(splitk >= 1, FC_ERR_INVALID_ARG, "splitk >= 1");
+    FC_CUDA_TRY(cudaEventRecord(c->e0, c->st));
+    dgemm(c->st, transA, transB, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, splitk);
+    FC_CUDA_TRY(cudaEventRecord(c->e1, c->st));
+    c->k_flops = 2.0 * M * (double)N * K;
+    c->k_bytes = 8.0 * ((double)M * K + (double)K * N + (double)M * N * (beta != 0 ? 2 : 1));
+    c->k_launches = 1;
+    return FC_OK;
+  });
+}
+
 int fc_last_kernel_stats(fc_ctx c, double* ms, double* flops, double* bytes, int* launches) {
   return guard(c, [&]() {
     float t = 0;

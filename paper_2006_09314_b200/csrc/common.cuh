@@ -135,17 +135,25 @@ struct GemmArgs {
   int transA = 0, transB = 0;
   GenA gen;
   int krR = 0;           // > 0 enables the Khatri-Rao B operand
-  int splitk = 1;        // > 1: atomicAdd epilogue (beta must be 1, C pre-initialised)
+  // > 1: the K range is split over `splitk` CTAs per output tile and the partial tiles are
+  // reduced in a FIXED order (split 0, 1, ...): through distributed shared memory inside a
+  // (1, 1, splitk) thread-block cluster for splitk <= 16 (the 128x128 tiles clamp to 8), else
+  // through a global workspace by the last-arriving CTA (clamped to 64).  Deterministic (bit-identical run to run); C = alpha op(A) op(B) + beta C
+  // for every splitk.
+  int splitk = 1;
   double alpha = 1.0, beta = 0.0;
   int nbatch = 0;
   int rep = 1;           // every entry is repeated rep times with its strides (strided batch)
   GemmBatch b[kMaxBatch];
+  // set by the dispatcher (gemm.cu): split-K reduction mode and its workspace
+  int kmode = 0;             // 0 direct, 1 cluster (DSMEM), 2 workspace
+  double* ws = nullptr;      // kmode 2: partial tiles
+  int* cnt = nullptr;        // kmode 2: per-tile arrival counters (self-resetting)
 };
 void gemm(const GemmArgs& a, cudaStream_t st);
 // fc_profile_gemm: enable -> start recording; disable -> totals of the recorded launches
 void gemm_profile(bool enable, double* ms, double* flops, long long* launches);
-// split-K factor giving ~`waves` waves of 64 x 64 tiles on 148 SMs (at least 64 of K per split);
-// the caller zeroes C and sets beta = 1 (atomic epilogue)
+// split-K factor giving ~`waves` waves of 64 x 64 tiles on 148 SMs (at least 64 of K per split)
 inline int waves_splitk(const GemmArgs& a, int waves) {
   long long tiles = 0;
   int minK = 1 << 30;

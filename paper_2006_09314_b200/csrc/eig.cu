@@ -553,17 +553,16 @@ __global__ void __launch_bounds__(1024) tridiag_packed_kernel(const __grid_const
     }
     __syncthreads();
     if (!skip) {
-      for (int jj = warp; jj < m; jj += NW) {
-        const double* cj = L + off(k + 1 + jj);   // element (k+1+ii, k+1+jj) at cj[ii - jj]
-        const double uj = u[jj];
+      // p = A u, one warp per row in a fixed summation order (deterministic; the lower triangle
+      // holds element (k+1+ii, k+1+jj), ii >= jj, at L[off(k+1+jj) + ii - jj])
+      for (int ii = warp; ii < m; ii += NW) {
         double dot = 0.0;
-        for (int ii = jj + ln; ii < m; ii += 32) {
-          const double a = cj[ii - jj];
-          atomicAdd(p + ii, a * uj);
-          if (ii > jj) dot += a * u[ii];
+        for (int jj = ln; jj < m; jj += 32) {
+          const double a = jj <= ii ? L[off(k + 1 + jj) + (ii - jj)] : L[off(k + 1 + ii) + (jj - ii)];
+          dot = fma(a, u[jj], dot);
         }
         for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
-        if (ln == 0) atomicAdd(p + jj, dot);
+        if (ln == 0) p[ii] = dot;
       }
       __syncthreads();
       double kp = 0.0;
@@ -2292,7 +2291,8 @@ void bcgs_cluster_finalize(const BcgsBatch& bb, int j0, cudaStream_t st) {
 
 // split-K for the two skinny GEMMs of a block projection, P = Q^T A_blk (k x W x n) and
 // A_blk -= Q P (n x W x k): enough CTAs for ~2 waves of 148 SMs (64 x 64 tiles), at least 64 of
-// the reduction dimension per split (atomic epilogue; both GEMMs accumulate into beta = 1 targets)
+// the reduction dimension per split (deterministic split-K; P is written with beta = 0, A updated
+// with beta = 1)
 void split_skinny(GemmArgs& p, GemmArgs& u, int n, int k, int w, int nb) {
   static const int waves = getenv("FC_SKINNY_WAVES") ? atoi(getenv("FC_SKINNY_WAVES")) : 2;
   const int tp = cdiv(k, 64) * cdiv(w, 64) * nb, tu = cdiv(n, 64) * cdiv(w, 64) * nb;
@@ -2388,14 +2388,20 @@ void bcgs(const BcgsBatch& bin, cudaStream_t st) {
   col_norms_kernel<<<dim3(cdiv(maxp, 8), b.nb), 256, 0, st>>>(b);
   FC_CHECK_LAUNCH();
   for (int j0 = 0; j0 < maxp; j0 += W) {
-    // project the block against every column accepted so far (<= j0; unused Q columns are 0)
-    // one projection pass (BCGS2: the accepted vectors get a second one below)
+    // project the block against every column accepted so far (<= j0; unused Q columns are 0),
+    // TWICE before the in-block step: after a single classical projection a column that lies
+    // almost in span(Q) (residual ~1e-10 of its norm, still above the acceptance level) keeps a
+    // Q-component of the order of its residual, the accept decision is taken on that noise and
+    // the basis loses orthogonality completely (observed on the eigen-coordinate Khatri-Rao bases
+    // of C4 at eps = 1e-8: |Q^T Q - I| = 1).  "Twice is enough" makes the residual accurate; the
+    // accepted vectors then get the BCGS2 re-projection below.
     bool any_base = false;
     for (int i = 0; i < b.nb; ++i) any_base |= b.e[i].k_base > 0;
-    for (int pass = 0; pass < 1 && (j0 > 0 || any_base); ++pass) {
+    static const int npre = getenv("FC_BCGS_PREPASS") ? atoi(getenv("FC_BCGS_PREPASS")) : 2;   // diagnostic
+    for (int pass = 0; pass < npre && (j0 > 0 || any_base); ++pass) {
       GemmArgs p, u;
       p.transA = 1;
-      p.beta = 1.0;
+      p.beta = 0.0;   // P = Q^T A (rows beyond the accepted count are never read: dynK below)
       u.alpha = -1.0;
       u.beta = 1.0;
       int nb = 0, kmx = 0;
@@ -2405,7 +2411,6 @@ void bcgs(const BcgsBatch& bin, cudaStream_t st) {
         const int wb = std::min(W, E.p - j0), kup = std::min(E.k_base + j0, E.kcap);
         if (kup == 0) continue;
         kmx = std::max(kmx, kup);
-        if (cfg == 0) FC_CUDA_TRY(cudaMemsetAsync(E.P, 0, (size_t)kup * W * 8, st));
         p.b[nb] = GemmBatch{kup, wb, E.n, E.Q, E.ldq, E.A + (size_t)j0 * E.lda, E.lda, E.P, kup, nullptr, 0, nullptr};
         u.b[nb] = GemmBatch{E.n, wb, kup, E.Q, E.ldq, E.P, kup, E.A + (size_t)j0 * E.lda, E.lda, nullptr, 0, nullptr};
         if (dyn_k) {               // only the first *E.k columns of Q are nonzero
@@ -2426,7 +2431,7 @@ void bcgs(const BcgsBatch& bin, cudaStream_t st) {
     if (j0 > 0 || any_base) {
       GemmArgs p, u;
       p.transA = 1;
-      p.beta = 1.0;
+      p.beta = 0.0;
       u.alpha = -1.0;
       u.beta = 1.0;
       int nb = 0, kmx = 0;
@@ -2436,7 +2441,6 @@ void bcgs(const BcgsBatch& bin, cudaStream_t st) {
         const int kup = std::min(E.k_base + j0, E.kcap);
         if (kup == 0) continue;
         kmx = std::max(kmx, kup);
-        if (cfg == 0) FC_CUDA_TRY(cudaMemsetAsync(E.P, 0, (size_t)kup * W * 8, st));
         p.b[nb] = GemmBatch{kup, W, E.n, E.Q, E.ldq, E.Y, E.n, E.P, kup, nullptr, 0, nullptr};
         u.b[nb] = GemmBatch{E.n, W, kup, E.Q, E.ldq, E.P, kup, E.Y, E.n, nullptr, 0, nullptr};
         if (dyn_k) {

@@ -10,7 +10,13 @@
 // mma.sync.m8n8k4.f64 (SASS: DMMA.8x8x4).  Tiles: CTA 64x64, BK = 16, 4 warps each owning a
 // 32x32 sub-tile (4x4 DMMA fragments, 32 fp64 accumulators per thread), operands staged
 // global -> shared with cp.async in a 3-stage ring (zero-filled at ragged edges).
+//
+// Split-K is deterministic: the partial tiles of one output tile are summed in split order,
+// either through distributed shared memory inside a (1, 1, splitk) cluster (splitk <= 8) or
+// through a global workspace by the last CTA to arrive (splitk > 8).  No atomics touch C, so
+// repeated runs are bit-identical and C needs no pre-zeroing.
 #include <algorithm>
+#include <cooperative_groups.h>
 #include <cstdlib>
 #include <map>
 #include <mutex>
@@ -19,8 +25,11 @@
 namespace fc {
 namespace {
 
-constexpr int BM = 64, BN = 64, BK = 16, PAD = 8, STAGES = 3, NT = 128;
-constexpr int LDS = BM + PAD;  // 72 doubles: k-rows land on alternating bank halves
+constexpr int BM = 64, BN = 64, BK = 16, PAD = 4, STAGES = 3, NT = 128;
+// 68 doubles = 4 (mod 16): a fragment load (lanes fr = 0..7 along m, fc4 = 0..3 along k) then
+// touches 16 distinct 8-byte bank pairs per half-warp (72 = 8 (mod 16) put fc4 and fc4 + 2 on
+// the same banks: a 2-way conflict on every A and B fragment load)
+constexpr int LDS = BM + PAD;
 constexpr int STAGE_ELEMS = BK * LDS;
 
 __device__ __forceinline__ void cp_async8(double* smem, const double* gmem, bool pred) {
@@ -113,6 +122,97 @@ __device__ __forceinline__ void load_tile_B(double* Bs, double* Ks, const GemmBa
   }
 }
 
+// ---- epilogue shared by both kernels ---------------------------------------------------
+// Fragment element (i, j, e) of a thread lives at row wm + i*8 + fr, col wn + j*8 + 2*fc4 + e of
+// the CTA tile; slot s = (i*4 + j)*2 + e.  WM = warps along m.
+template <int WM>
+__device__ __forceinline__ void slot_rc(int tid, int s, int& r, int& c) {
+  const int lane = tid & 31, warp = tid >> 5;
+  const int i = s >> 3, j = (s >> 1) & 3, e = s & 1;
+  r = (warp % WM) * 32 + i * 8 + (lane >> 2);
+  c = (warp / WM) * 32 + j * 8 + 2 * (lane & 3) + e;
+}
+
+__device__ __forceinline__ void put_elem(const GemmArgs& args, const GemmBatch& g, int ri, int r, int c, double v) {
+  if (r >= g.M || c >= g.N) return;
+  const double cs = g.colscale ? g.colscale[c + (size_t)ri * g.sS] : 1.0;
+  const double val = args.alpha * cs * v;
+  double* dst = g.C + (size_t)ri * g.sC + (size_t)r + (size_t)c * g.ldc;
+  if (args.beta == 0.0) *dst = val;
+  else *dst = val + args.beta * *dst;
+}
+
+// NTH threads, WM warps along m; `red` = the CTA's (now idle) pipeline shared memory, at least
+// 32 * NTH doubles.  ks = this CTA's split, tile = linear output-tile index (workspace mode).
+template <int NTH, int WM>
+__device__ __forceinline__ void tile_epilogue(const double (&acc)[4][4][2], const GemmArgs& args, const GemmBatch& g,
+                                              int ri, int m0, int n0, int ks, long long tile, double* red) {
+  const int tid = threadIdx.x;
+  if (args.kmode == 0) {
+#pragma unroll
+    for (int s = 0; s < 32; ++s) {
+      int r, c;
+      slot_rc<WM>(tid, s, r, c);
+      put_elem(args, g, ri, m0 + r, n0 + c, acc[s >> 3][(s >> 1) & 3][s & 1]);
+    }
+    return;
+  }
+  const int S = args.splitk;
+  if (args.kmode == 1) {
+    // cluster (1, 1, S): rank q holds split q.  Every CTA parks its partial tile in its own
+    // shared memory; CTA q then sums slots q, q + S, ... over ranks 0..S-1 in that order.
+    namespace cg = cooperative_groups;
+    cg::cluster_group cl = cg::this_cluster();
+#pragma unroll
+    for (int s = 0; s < 32; ++s) red[s * NTH + tid] = acc[s >> 3][(s >> 1) & 3][s & 1];
+    cl.sync();
+    for (int s = ks; s < 32; s += S) {
+      // all S remote loads in flight at once (~200-cycle DSMEM latency each), then the sum in
+      // split order
+      double pv[16];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) pv[q] = q < S ? cl.map_shared_rank(red, q)[s * NTH + tid] : 0.0;
+      double v = 0.0;
+#pragma unroll
+      for (int q = 0; q < 16; ++q)
+        if (q < S) v += pv[q];
+      int r, c;
+      slot_rc<WM>(tid, s, r, c);
+      put_elem(args, g, ri, m0 + r, n0 + c, v);
+    }
+    cl.sync();   // peers may still read this CTA's partial
+    return;
+  }
+  // workspace: partial (tile, ks) at ws[((tile * S + ks) * 32 + s) * NTH + tid]; the last CTA to
+  // arrive sums splits 0..S-1 in order and resets the tile's counter
+  __shared__ int last_s;
+  double* wp = args.ws + ((size_t)tile * S + ks) * 32 * NTH;
+#pragma unroll
+  for (int s = 0; s < 32; ++s) wp[s * NTH + tid] = acc[s >> 3][(s >> 1) & 3][s & 1];
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) last_s = atomicAdd(args.cnt + tile, 1) == S - 1;
+  __syncthreads();
+  if (!last_s) return;
+  __threadfence();
+  const double* w0 = args.ws + (size_t)tile * S * 32 * NTH;
+  for (int s = 0; s < 32; ++s) {
+    double v = 0.0;
+    for (int q0 = 0; q0 < S; q0 += 16) {   // 16 loads in flight, summed in split order
+      double pv[16];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) pv[q] = q0 + q < S ? __ldcg(w0 + ((size_t)(q0 + q) * 32 + s) * NTH + tid) : 0.0;
+#pragma unroll
+      for (int q = 0; q < 16; ++q)
+        if (q0 + q < S) v += pv[q];
+    }
+    int r, c;
+    slot_rc<WM>(tid, s, r, c);
+    put_elem(args, g, ri, m0 + r, n0 + c, v);
+  }
+  if (tid == 0) args.cnt[tile] = 0;
+}
+
 template <bool KR, bool GEN>
 __global__ void __launch_bounds__(NT) dgemm_dmma_kernel(const __grid_constant__ GemmArgs args) {
   extern __shared__ __align__(16) double smem[];
@@ -128,18 +228,16 @@ __global__ void __launch_bounds__(NT) dgemm_dmma_kernel(const __grid_constant__ 
   const double* gA = g.A + (size_t)ri * g.sA;
   const double* gB = g.B + (size_t)ri * g.sB;
   const double* gK = g.krU + (size_t)ri * g.sK;
-  double* gC = g.C + (size_t)ri * g.sC;
-  const double* gS = g.colscale ? g.colscale + (size_t)ri * g.sS : nullptr;
   const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
   const int Meff = g.dynM ? min(g.M, *g.dynM) : g.M;
   const int Keff = g.dynK ? min(g.K, *g.dynK) : g.K;
+  // uniform over the splits of a tile (same cluster / same counter): all leave together
   if (m0 >= Meff || n0 >= g.N) return;
 
   int kchunk = ((Keff + args.splitk - 1) / args.splitk + BK - 1) / BK * BK;
   const int kbeg = ks * kchunk;
   const int kend = min(Keff, kbeg + kchunk);
-  if (args.splitk > 1 && kend <= kbeg) return;   // empty split: nothing to accumulate
-  const int nk = kend > kbeg ? (kend - kbeg + BK - 1) / BK : 0;
+  const int nk = kend > kbeg ? (kend - kbeg + BK - 1) / BK : 0;   // an empty split adds zeros
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = (warp & 1) * 32, wn = (warp >> 1) * 32;
@@ -199,27 +297,29 @@ __global__ void __launch_bounds__(NT) dgemm_dmma_kernel(const __grid_constant__ 
     }
   }
   cp_async_wait<0>();
+  __syncthreads();   // the pipeline buffers become the reduction buffer
+  const long long tile = ((long long)bi * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+  tile_epilogue<NT, 2>(acc, args, g, ri, m0, n0, ks, tile, smem);
+}
 
-  // epilogue: fragment (i, j) element e -> row wm+i*8+fr, col wn+j*8+2*fc4+e
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-#pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      int c = n0 + wn + j * 8 + 2 * fc4 + e;
-      if (c >= g.N) continue;
-      double cs = gS ? gS[c] : 1.0;
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        int r = m0 + wm + i * 8 + fr;
-        if (r >= g.M) continue;
-        double v = args.alpha * cs * acc[i][j][e];
-        double* dst = gC + (size_t)r + (size_t)c * g.ldc;
-        if (args.splitk > 1) atomicAdd(dst, v);
-        else if (args.beta == 0.0) *dst = v;
-        else *dst = v + args.beta * *dst;
-      }
-    }
+// launch with the split-K reduction mode's cluster shape (kmode 1: (1, 1, splitk))
+void launch_gemm_kernel(void (*kern)(GemmArgs), const GemmArgs& a, dim3 grid, int nt, int smem, cudaStream_t st) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(nt, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  if (a.kmode == 1) {
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 1;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = a.splitk;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
   }
+  FC_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, a));
+  FC_CHECK_LAUNCH();
 }
 
 // ---------------------------------------------------------------------------------------
@@ -230,9 +330,11 @@ __global__ void __launch_bounds__(NT) dgemm_dmma_kernel(const __grid_constant__ 
 // K-contiguous operands and every fragment load is at most 2-way banked.
 namespace big {
 constexpr int BM = 128, BN = 128, BK = 16, NT = 512, STAGES = 3;
-constexpr int LDK = BM + 8;        // k-major row length (136)
+constexpr int LDK = BM + 4;        // k-major row length 132 = 4 (mod 16): conflict-free fragment
+                                   // loads (136 = 8 (mod 16) was 2-way conflicted, fc4 vs fc4 + 2)
 constexpr int LDM = BK + 4;        // m/n-major row length (20)
 constexpr int TILE = BM * LDM > BK * LDK ? BM * LDM : BK * LDK;   // 2560 doubles
+constexpr int RED = 32 * NT;       // split-K reduction buffer (doubles), aliases the pipeline
 
 __device__ __forceinline__ void cp_async16(double* smem, const double* gmem, int bytes) {
   unsigned s = (unsigned)__cvta_generic_to_shared(smem);
@@ -314,7 +416,7 @@ __global__ void __launch_bounds__(NT, 1) dgemm_big_kernel(const __grid_constant_
   const double* gB = g.B + (size_t)ri * g.sB;
   const double* gK = g.krU + (size_t)ri * g.sK;
   const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
-  if (m0 >= g.M || n0 >= g.N) return;
+  if (m0 >= g.M || n0 >= g.N) return;   // uniform over the splits of a tile
   const int kchunk = ((g.K + args.splitk - 1) / args.splitk + BK - 1) / BK * BK;
   const int kbeg = ks * kchunk, kend = min(g.K, kbeg + kchunk);
   const int nk = kend > kbeg ? (kend - kbeg + BK - 1) / BK : 0;
@@ -381,37 +483,20 @@ __global__ void __launch_bounds__(NT, 1) dgemm_big_kernel(const __grid_constant_
     }
   }
   cp_async_wait<0>();
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-#pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      const int c = n0 + wn + j * 8 + 2 * fc4 + e;
-      if (c >= g.N) continue;
-      const double cs = g.colscale ? g.colscale[c + (size_t)ri * g.sS] : 1.0;
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int r = m0 + wm + i * 8 + fr;
-        if (r >= g.M) continue;
-        const double v = args.alpha * cs * acc[i][j][e];
-        double* dst = g.C + (size_t)ri * g.sC + (size_t)r + (size_t)c * g.ldc;
-        if (args.splitk > 1) atomicAdd(dst, v);
-        else if (args.beta == 0.0) *dst = v;
-        else *dst = v + args.beta * *dst;
-      }
-    }
-  }
+  __syncthreads();
+  const long long tile = ((long long)bi * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+  tile_epilogue<NT, 4>(acc, args, g, ri, m0, n0, ks, tile, smem);
 }
 
 template <int TA, int TB, bool KR>
 void launch_big(const GemmArgs& a, dim3 grid, cudaStream_t st) {
-  const int smem = (KR ? 3 : 2) * STAGES * TILE * (int)sizeof(double);
+  const int smem = std::max((KR ? 3 : 2) * STAGES * TILE, RED) * (int)sizeof(double);
   static bool attr = false;
   if (!attr) {
     FC_CUDA_TRY(cudaFuncSetAttribute(dgemm_big_kernel<TA, TB, KR>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr = true;
   }
-  dgemm_big_kernel<TA, TB, KR><<<grid, NT, smem, st>>>(a);
-  FC_CHECK_LAUNCH();
+  launch_gemm_kernel(dgemm_big_kernel<TA, TB, KR>, a, grid, NT, smem, st);
 }
 }  // namespace big
 
@@ -510,8 +595,58 @@ void gemm(const GemmArgs& a, cudaStream_t st) {
   ++P.used;
 }
 
-static void gemm_dispatch(const GemmArgs& a, cudaStream_t st) {
-  if (a.nbatch <= 0) return;
+// ---- split-K workspace (kmode 2), one per stream: launches on a stream run in order, so the
+// partial tiles and the self-resetting counters are never shared by two running launches --------
+namespace {
+struct SplitWs {
+  double* ws = nullptr;
+  size_t wsn = 0;
+  int* cnt = nullptr;
+  size_t cntn = 0;
+};
+std::mutex g_ws_mu;
+std::map<cudaStream_t, SplitWs> g_ws;
+
+void split_workspace(cudaStream_t st, size_t doubles, size_t tiles, double** ws, int** cnt) {
+  std::lock_guard<std::mutex> lock(g_ws_mu);
+  SplitWs& w = g_ws[st];
+  if (w.wsn < doubles) {
+    if (w.ws) FC_CUDA_TRY(cudaFreeAsync(w.ws, st));
+    w.wsn = std::max(doubles, (size_t)1 << 20);
+    w.ws = (double*)dev_alloc(w.wsn * sizeof(double), st);
+  }
+  if (w.cntn < tiles) {
+    if (w.cnt) FC_CUDA_TRY(cudaFreeAsync(w.cnt, st));
+    w.cntn = std::max(tiles, (size_t)4096);
+    w.cnt = (int*)dev_alloc(w.cntn * sizeof(int), st);
+    FC_CUDA_TRY(cudaMemsetAsync(w.cnt, 0, w.cntn * sizeof(int), st));
+  }
+  *ws = w.ws;
+  *cnt = w.cnt;
+}
+
+// split-K reduction: inside a cluster for up to kClusterSplit splits (16: non-portable cluster size,
+// the 64x64-tile kernel fits 2-4 CTAs per SM; 8 for the 1-CTA-per-SM 128x128 kernel), through the
+// global workspace above, up to 64 splits (last CTA to arrive; FC_GEMM_MAX_SPLIT sets the cap)
+constexpr int kClusterSplit = 16, kBigClusterSplit = 8;
+int max_split() {
+  // 64: C4 303 ms vs 375 ms with the cap at 16 (GEMMs with few output tiles and long K)
+  static const int v = getenv("FC_GEMM_MAX_SPLIT") ? atoi(getenv("FC_GEMM_MAX_SPLIT")) : 64;
+  return std::max(1, std::min(v, 64));
+}
+
+void set_kmode(GemmArgs& a, dim3 grid, int nthreads, cudaStream_t st) {
+  a.kmode = a.splitk <= 1 ? 0 : (a.splitk <= kClusterSplit ? 1 : 2);
+  if (a.kmode == 2) {
+    const size_t tiles = (size_t)grid.x * grid.y * (grid.z / a.splitk);
+    split_workspace(st, tiles * a.splitk * 32 * nthreads, tiles, &a.ws, &a.cnt);
+  }
+}
+}  // namespace
+
+static void gemm_dispatch(const GemmArgs& a_in, cudaStream_t st) {
+  if (a_in.nbatch <= 0) return;
+  GemmArgs a = a_in;
   int maxM = 0, maxN = 0;
   for (int i = 0; i < a.nbatch; ++i) {
     maxM = std::max(maxM, a.b[i].M);
@@ -526,9 +661,12 @@ static void gemm_dispatch(const GemmArgs& a, cudaStream_t st) {
   }
   bool dyn = false;
   for (int i = 0; i < a.nbatch; ++i) dyn |= a.b[i].dynM != nullptr || a.b[i].dynK != nullptr;
+  a.splitk = std::max(1, a.splitk);
   if (!dyn && a.gen.kind < 0 && maxM >= 256 && maxN >= 256 && minK >= 64 && work >= (1LL << 27)) {
+    a.splitk = std::min(a.splitk, kBigClusterSplit);   // big tiles: cluster reduction only
     dim3 grid(cdiv(maxM, big::BM), cdiv(maxN, big::BN), a.nbatch * a.rep * a.splitk);
     require(grid.y <= 65535 && grid.z <= 65535, FC_ERR_INVALID_ARG, "gemm grid too large");
+    set_kmode(a, grid, big::NT, st);
     if (a.krR > 0) big::launch_big<0, 0, true>(a, grid, st);
     else if (!a.transA && !a.transB) big::launch_big<0, 0, false>(a, grid, st);
     else if (a.transA && !a.transB) big::launch_big<1, 0, false>(a, grid, st);
@@ -539,18 +677,23 @@ static void gemm_dispatch(const GemmArgs& a, cudaStream_t st) {
   static bool attr = false;
   const int smem2 = 2 * STAGES * STAGE_ELEMS * (int)sizeof(double);
   const int smem3 = 3 * STAGES * STAGE_ELEMS * (int)sizeof(double);
+  static_assert(2 * STAGES * STAGE_ELEMS >= 32 * NT, "split-K reduction buffer aliases the pipeline");
   if (!attr) {
     FC_CUDA_TRY(cudaFuncSetAttribute(dgemm_dmma_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2));
     FC_CUDA_TRY(cudaFuncSetAttribute(dgemm_dmma_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem3));
     FC_CUDA_TRY(cudaFuncSetAttribute(dgemm_dmma_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2));
+    FC_CUDA_TRY(cudaFuncSetAttribute(dgemm_dmma_kernel<false, false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    FC_CUDA_TRY(cudaFuncSetAttribute(dgemm_dmma_kernel<true, false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    FC_CUDA_TRY(cudaFuncSetAttribute(dgemm_dmma_kernel<false, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     attr = true;
   }
+  a.splitk = std::min(a.splitk, max_split());
   dim3 grid(cdiv(maxM, BM), cdiv(maxN, BN), a.nbatch * a.rep * a.splitk);
   require(grid.y <= 65535 && grid.z <= 65535, FC_ERR_INVALID_ARG, "gemm grid too large");
-  if (a.gen.kind >= 0) dgemm_dmma_kernel<false, true><<<grid, NT, smem2, st>>>(a);
-  else if (a.krR > 0) dgemm_dmma_kernel<true, false><<<grid, NT, smem3, st>>>(a);
-  else dgemm_dmma_kernel<false, false><<<grid, NT, smem2, st>>>(a);
-  FC_CHECK_LAUNCH();
+  set_kmode(a, grid, NT, st);
+  if (a.gen.kind >= 0) launch_gemm_kernel(dgemm_dmma_kernel<false, true>, a, grid, NT, smem2, st);
+  else if (a.krR > 0) launch_gemm_kernel(dgemm_dmma_kernel<true, false>, a, grid, NT, smem3, st);
+  else launch_gemm_kernel(dgemm_dmma_kernel<false, false>, a, grid, NT, smem2, st);
 }
 
 void dgemm(cudaStream_t st, int transA, int transB, int M, int N, int K, double alpha, const double* A,

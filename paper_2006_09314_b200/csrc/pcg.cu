@@ -200,6 +200,41 @@ TT apply_truncate_tt(fc_ctx c, SpecCP& sp, const TT& x, double eps, int rank_cap
   return out;
 }
 
+// FC_TRACE_PCG diagnostics: orthonormality of a TT iterate's bases and ||core||^2 vs sum w^2
+// (equal for the orthogonal-CP outputs of a truncation)
+void tt_check(cudaStream_t st, const TT& x, const char* name) {
+  if (x.R == 0) return;
+  double orth = 0.0;
+  for (int l = 0; l < 3; ++l) {
+    const int q = x.q[l];
+    Scratch s(st);
+    double* G = s.alloc<double>((size_t)q * q);
+    dgemm(st, 1, 0, q, q, x.n, 1.0, x.Q[l], x.n, x.Q[l], x.n, 0.0, G, q);
+    std::vector<double> h((size_t)q * q);
+    FC_CUDA_TRY(cudaMemcpyAsync(h.data(), G, h.size() * 8, cudaMemcpyDeviceToHost, st));
+    FC_CUDA_TRY(cudaStreamSynchronize(st));
+    for (int i = 0; i < q; ++i)
+      for (int j = 0; j < q; ++j) orth = std::max(orth, std::fabs(h[i + (size_t)j * q] - (i == j ? 1.0 : 0.0)));
+  }
+  std::vector<double> w(x.R);
+  FC_CUDA_TRY(cudaMemcpyAsync(w.data(), x.w, (size_t)x.R * 8, cudaMemcpyDeviceToHost, st));
+  double c2 = -1.0;
+  std::vector<double> core;
+  if (x.core) {
+    core.resize((size_t)x.q[0] * x.q[1] * x.q[2]);
+    FC_CUDA_TRY(cudaMemcpyAsync(core.data(), x.core, core.size() * 8, cudaMemcpyDeviceToHost, st));
+  }
+  FC_CUDA_TRY(cudaStreamSynchronize(st));
+  double w2 = 0.0;
+  for (double v : w) w2 += v * v;
+  if (x.core) {
+    c2 = 0.0;
+    for (double v : core) c2 += v * v;
+  }
+  fprintf(stderr, "[fc pcg]   %s: R %d q (%d,%d,%d) orth_err %.2e  sum w^2 %.6e  ||core||^2 %.6e\n", name, x.R, x.q[0],
+          x.q[1], x.q[2], orth, w2, c2);
+}
+
 }  // namespace fc
 
 using namespace fc;
@@ -455,6 +490,14 @@ int pcg_solve(fc_ctx c, const fc_cp* b, const fc_params* prm, fc_cp* u, fc_pcg_r
       if (!std::isfinite(ps)) { cudaEventDestroy(loop0); throw Error(FC_ERR_NAN, "<P,S> is not finite"); }
       if (ps <= 0) { cudaEventDestroy(loop0); throw Error(FC_ERR_NOT_SPD, "<P,S> <= 0"); }
       const double a_k = rz / ps;                                   // line 9
+      static const bool tr_pcg = getenv("FC_TRACE_PCG") != nullptr;
+      if (tr_pcg) {
+        fprintf(stderr, "[fc pcg] k=%d <R,Z>=%.10e <P,S>=%.10e a=%.10e  S: tucker (%d,%d,%d) energy %.6e refined %d\n", k,
+                rz, ps, a_k, sS.tucker[0], sS.tucker[1], sS.tucker[2], sS.energy, (int)sS.refined);
+        tt_check(st, P, "P");
+        tt_check(st, S, "S");
+        tt_check(st, R, "R");
+      }
       XJob xjob(c, st, X, P, a_k, eps, cap);                        // lines 10-11 (side stream)
       {
         TT RS = tt_axpy(st, R, -a_k, S);                            // lines 12-13
@@ -485,6 +528,13 @@ int pcg_solve(fc_ctx c, const fc_cp* b, const fc_params* prm, fc_cp* u, fc_pcg_r
       Z = apply_truncate_tt(c, G, R, eps, cap, &sZ2);               // lines 17-18
       const double rz_new = tt_dot(c, R, Z);
       const double b_k = rz_new / rz;                               // line 19 (A16)
+      if (tr_pcg) {
+        fprintf(stderr, "[fc pcg] k=%d rel=%.6e <R',Z'>=%.10e b=%.10e  R: tucker (%d,%d,%d) energy %.6e refined %d  Z: tucker (%d,%d,%d) refined %d\n",
+                k, rel, rz_new, b_k, sR.tucker[0], sR.tucker[1], sR.tucker[2], sR.energy, (int)sR.refined, sZ2.tucker[0],
+                sZ2.tucker[1], sZ2.tucker[2], (int)sZ2.refined);
+        tt_check(st, R, "R'");
+        tt_check(st, Z, "Z'");
+      }
       {
         TT ZP = tt_axpy(st, Z, b_k, P);                             // lines 20-21
         P = truncate_tt(c, ZP, eps, cap, &sP);

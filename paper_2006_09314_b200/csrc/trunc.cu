@@ -783,6 +783,21 @@ int blocks_for(long long total) {
   return (int)std::min<long long>(std::max<long long>(b, 1), 148 * 8);
 }
 
+// FC_TRACE_ORTH_Y diagnostics: max |A^T A - I| of a rows x cols column-major block
+double dbg_orth(cudaStream_t st, const double* A, int rows, int cols, int ld) {
+  if (cols <= 0) return 0.0;
+  Scratch s(st);
+  double* G = s.alloc<double>((size_t)cols * cols);
+  dgemm(st, 1, 0, cols, cols, rows, 1.0, A, ld, A, ld, 0.0, G, cols);
+  std::vector<double> h((size_t)cols * cols);
+  FC_CUDA_TRY(cudaMemcpyAsync(h.data(), G, h.size() * 8, cudaMemcpyDeviceToHost, st));
+  FC_CUDA_TRY(cudaStreamSynchronize(st));
+  double e = 0.0;
+  for (int i = 0; i < cols; ++i)
+    for (int j = 0; j < cols; ++j) e = std::max(e, std::fabs(h[i + (size_t)j * cols] - (i == j ? 1.0 : 0.0)));
+  return e;
+}
+
 int read_int(const int* d, cudaStream_t st) {
   int h = 0;
   FC_CUDA_TRY(cudaMemcpyAsync(&h, d, sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -1567,6 +1582,12 @@ TT truncate_tt(fc_ctx c, const TT& xin, double eps, int rank_cap, TruncStats* st
       }
   }
   // ---- 5. Z_l = Qo_l Y_r -----------------------------------------------------------------
+  static const bool tr_orth_y = getenv("FC_TRACE_ORTH_Y") != nullptr;
+  if (tr_orth_y)
+    for (int l = 0; l < 3; ++l)
+      fprintf(stderr, "[fc orthY] %s mode %d q %d r %d refine %d pk %d qr %d: |Qo^T Qo - I| %.2e |Y_r^T Y_r - I| %.2e\n",
+              ss ? "struct" : "cp", l, q[l], r[l], (int)refine[l], pkv[l], (int)qr[l], dbg_orth(st, Qo[l], n, q[l], n),
+              dbg_orth(st, Y[l], q[l], r[l], q[l]));
   double* Z[3];
   {
     GemmArgs gz;

@@ -58,6 +58,40 @@ def test_dgemm(lib, tA, tB, M, N, K):
     assert np.max(np.abs(got - ref)) <= 1e-13 * max(1.0, np.max(np.abs(ref))) * np.sqrt(K)
 
 
+@pytest.mark.parametrize("tA,tB,M,N,K,splitk", [
+    (0, 0, 64, 64, 1024, 2), (1, 0, 100, 70, 3000, 5), (1, 0, 37, 129, 200, 8),   # cluster (DSMEM) reduction
+    (0, 1, 130, 33, 4000, 9), (1, 0, 64, 64, 1024, 16), (0, 0, 90, 90, 7000, 32),  # workspace reduction
+    (0, 0, 50, 40, 100, 64),                                 # more splits than K tiles: empty splits add zeros
+    (0, 0, 1000, 700, 1300, 4), (1, 0, 513, 1030, 2570, 8),  # 128 x 128 tiles, cluster reduction
+    (0, 1, 700, 900, 1330, 16)])                             # ... clamped to 8 splits
+def test_dgemm_splitk_deterministic(lib, tA, tB, M, N, K, splitk):
+    """Split-K GEMM: the partial tiles are reduced in a fixed order (no atomics), so the result
+    matches NumPy to the FP64 accumulation bound and two launches are bit-identical; beta = 0 never
+    reads C (NaN-filled here)."""
+    import torch
+    ctx = lib.context()
+    rng = np.random.default_rng(M * 7 + N + splitk)
+    A = rng.standard_normal((K, M) if tA == 0 else (M, K))
+    B = rng.standard_normal((N, K) if tB == 0 else (K, N))
+    At, Bt = (torch.tensor(v, device="cuda") for v in (A, B))
+    opA = A.T if tA == 0 else A
+    opB = B.T if tB == 0 else B
+    ref = opA @ opB
+    outs = []
+    for _ in range(2):
+        Ct = torch.full((N, M), float("nan"), dtype=torch.float64, device="cuda")
+        ctx.dgemm(tA, tB, M, N, K, 1.0, At, A.shape[1], Bt, B.shape[1], 0.0, Ct, M, splitk=splitk)
+        outs.append(Ct.cpu().numpy().T)
+    assert np.array_equal(outs[0], outs[1])
+    assert np.max(np.abs(outs[0] - ref)) <= 1e-13 * max(1.0, np.max(np.abs(ref))) * np.sqrt(K)
+    # beta != 0 with split-K: C = alpha AB + beta C
+    Cm = rng.standard_normal((N, M))
+    Ct = torch.tensor(Cm, device="cuda")
+    ctx.dgemm(tA, tB, M, N, K, 0.5, At, A.shape[1], Bt, B.shape[1], 0.25, Ct, M, splitk=splitk)
+    ref2 = 0.5 * ref + 0.25 * Cm.T
+    assert np.max(np.abs(Ct.cpu().numpy().T - ref2)) <= 1e-13 * max(1.0, np.max(np.abs(ref2))) * np.sqrt(K)
+
+
 @pytest.mark.parametrize("n,R", [(32, 5), (37, 1), (64, 13)])
 def test_fracop_apply_parity(lib, n, R):
     from paper_2006_09314_b200.binding import DeviceCP, FC_F, FC_G
