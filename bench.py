@@ -8,8 +8,10 @@ eigenpairs + spectral CPs) runs once before the timed region and is reported as 
 value = PCG iterations / second over the timed steps (all ranks); time_to_eps_ms = median
 per-step solve time.  L2 is flushed (a 512 MiB write) between timed steps, outside the events.
 
---impl reference: the oracle (oracle/, NumPy/SciPy FP64) on the host cores, on a bounded
-sample of the same workload (C4 at n = 64: the oracle's dense setup is infeasible at n = 1024).
+--impl reference / cpu_baseline: the oracle (oracle/, NumPy/SciPy FP64, as it stands) on the host
+cores, on the same workload (C4, n = 1024): Z0 + the first PCG iteration per step, with the
+device-built eigenpairs and spectral CPs injected (the oracle's own setup materialises n^3
+entries); cpu_baseline also keeps the n = 64 own-setup figure as an extra key.
 Multi-GPU: replicas only (independent solves per rank, no collective).
 """
 from __future__ import annotations
@@ -39,7 +41,7 @@ def _peaks():
         return {}
 
 
-FP64_DMMA_TFLOPS = 37.16   # measured on this pool's B200 (tools/peak_fp64.cu, profiles/r01_peaks.md)
+FP64_DMMA_TFLOPS = 37.16   # measured on this pool's B200 (tools/peak_fp64.cu, profiles/r01_peak_fp64.jsonl)
 
 
 class Clocks:
@@ -112,7 +114,7 @@ def aggregate_over_ranks(t_seconds: float, iters: int, world: int, device: str):
 
 
 def oracle_sample(n=64, iters_cap=3):
-    """Oracle PCG on the C4 workload at n = 64 (bounded): returns (iters, loop seconds)."""
+    """Oracle PCG on the C4 workload at n = 64 with its own setup (bounded): (iters, loop s)."""
     from oracle import cp as cpm
     from oracle import pcg as P
     from synth import make_problem
@@ -126,28 +128,67 @@ def oracle_sample(n=64, iters_cap=3):
     return rep["iters"], dt
 
 
+def device_setup_for_oracle(ctx, p, prm):
+    """The oracle's PCG needs only (lambda, V) per mode and the spectral CPs F, G; its own setup
+    materialises n^3 entries of D (infeasible at n = 1024), so the device-built setup is exported
+    through the C-ABI (sl_get_eigen, op_get_spectral_cp) - outside every timed region."""
+    from oracle import cp as cpm
+    from oracle import pcg as P
+    from paper_2006_09314_b200.binding import FC_F, FC_G
+    ctx.sl_setup(p.n, p.a_mid, prm)
+    lams, V = [], []
+    for l in range(3):
+        lam, Vl = ctx.sl_get_eigen(l)
+        lams.append(lam.cpu().numpy())
+        V.append(Vl.cpu().numpy())
+    Fw, FU = ctx.op_get_spectral_cp(FC_F).to_numpy()
+    Gw, GU = ctx.op_get_spectral_cp(FC_G).to_numpy()
+    return P.Setup(lams, V, cpm.CP(Fw, FU), cpm.CP(Gw, GU))
+
+
+def oracle_c4_step(p, st, kmax=1):
+    """One bounded step of the oracle on the headline workload (C4, n = 1024): Algorithm 1 as it
+    stands (oracle/pcg.py: Z0 = trunc(G B), then kmax iterations), timed on the host cores."""
+    from oracle import cp as cpm
+    from oracle import pcg as P
+    B = cpm.normalized(p.b_w, p.b_U)
+    t0 = time.perf_counter()
+    _, rep = P.pcg(lambda x: cpm.apply(st.V, st.F, x), lambda x: cpm.apply(st.V, st.G, x), B, p.eps,
+                   p.tol_stop, kmax=kmax)
+    return rep["iters"], time.perf_counter() - t0, rep
+
+
+ORACLE_SAMPLE = ("oracle (NumPy/SciPy FP64, oracle/pcg.py as it stands) on the headline workload C4 n=1024 "
+                 "eps=1e-6 with the device-built eigenpairs and spectral CPs injected: Z0 + the first PCG "
+                 "iteration per step (the cheapest iteration: later ones grow with the ranks)")
+
+
 def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    per = []
-    iters_tot = 0
+    import torch
+    from paper_2006_09314_b200.binding import Library, make_params
+    from synth import make_problem
+    torch.cuda.set_device(0)
+    p = make_problem("C4", n=args.n, eps=args.eps)
+    ctx = Library().context()
+    st = device_setup_for_oracle(ctx, p, make_params(p.alpha, p.beta, p.eps, p.tol_stop))
     for _ in range(args.warmup):
-        oracle_sample(iters_cap=1)
-    t_all = 0.0
+        oracle_sample(n=16, iters_cap=1)          # the oracle has nothing to warm up: tiny runs
+    per, iters_tot = [], 0
     for _ in range(args.steps):
-        it, dt = oracle_sample(iters_cap=2)
+        it, dt, _ = oracle_c4_step(p, st, kmax=1)
         iters_tot += it
-        t_all += dt
         per.append(dt)
-    v = iters_tot / t_all
+    v = iters_tot / sum(per)
     cores = os.cpu_count()
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * float(np.mean(per)),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": {"workload": WORKLOAD, "sample": "C4 workload at n=64, 2 PCG iterations per step"},
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
-                             "sample": "oracle (NumPy/SciPy) PCG loop, C4 workload at n=64, 2 iterations per step"},
+            "data": "synthetic", "config": {"workload": WORKLOAD, "n": p.n, "eps": p.eps,
+                                            "sample": "Z0 + 1 PCG iteration per step"},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": ORACLE_SAMPLE},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -199,7 +240,9 @@ def main():
         torch.cuda.synchronize()
 
     # ---- device-timed region: K solves from HBM-resident b ------------------------------
-    times, iters, reps = [], 0, []
+    times, iters, reps, rcs = [], 0, [], []
+    ucap = 4096                                 # the solution buffer is allocated once, outside
+    u = DeviceCP(p.n, ucap)                     # the timed region (pcg_solve grows it if needed)
     l0 = kernel_launches(L)
     barrier()
     with Clocks(local) as clk:
@@ -207,12 +250,13 @@ def main():
             flush.fill_(1.0)                    # L2 flush (outside the events)
             s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             s0.record(stream)
-            u, rep, rc = ctx.pcg_solve(b, prm)
+            u, rep, rc = ctx.pcg_solve(b, prm, cap=u.cap, u=u)
             s1.record(stream)
             s1.synchronize()
             times.append(s0.elapsed_time(s1))
             iters += rep["iters"]
             reps.append(rep)
+            rcs.append(rc)
     barrier()
     launches = (kernel_launches(L) - l0) // max(args.steps, 1)
     t_total, iters = aggregate_over_ranks(sum(times) / 1e3, iters, world, "cuda")
@@ -221,9 +265,9 @@ def main():
     # ---- end to end through the public API with HOST buffers ----------------------------
     hw = torch.tensor(p.b_w, dtype=torch.float64).pin_memory()
     hU = [torch.tensor(np.ascontiguousarray(p.b_U[l].T), dtype=torch.float64).pin_memory() for l in range(3)]
-    cap_out = max(r["rank_X"][-1] for r in reps) if reps else 1
-    hu_w = torch.empty(4096, dtype=torch.float64).pin_memory()
-    hu_U = [torch.empty(4096, p.n, dtype=torch.float64).pin_memory() for _ in range(3)]
+    cap_out = max(u.cap, max(r["rank_X"][-1] for r in reps) if reps else 1)
+    hu_w = torch.empty(cap_out, dtype=torch.float64).pin_memory()
+    hu_U = [torch.empty(cap_out, p.n, dtype=torch.float64).pin_memory() for _ in range(3)]
     e2e_times, e2e_iters, h2d, d2h = [], 0, 0, 0
     barrier()
     for _ in range(args.steps):
@@ -235,7 +279,8 @@ def main():
         bd.w[:bd.rank].copy_(hw, non_blocking=True)
         for l in range(3):
             bd.U[l][:bd.rank].copy_(hU[l], non_blocking=True)
-        u, rep, rc = ctx.pcg_solve(bd, prm)
+        u, rep, rc = ctx.pcg_solve(bd, prm, cap=u.cap, u=u)
+        rcs.append(rc)
         R = u.rank
         hu_w[:R].copy_(u.w[:R], non_blocking=True)
         for l in range(3):
@@ -252,6 +297,7 @@ def main():
     # ---- dominant kernel class of the step: the DMMA GEMMs (one extra, untimed solve with every
     # GEMM launch bracketed by events on the library stream; algorithmic flops 2MNK) ----------
     ctx.profile_gemm(True)
+    ctx.profile_kernel(1, True)
     flush.fill_(1.0)
     _, rep_p, _ = ctx.pcg_solve(b, prm)
     gp = ctx.profile_gemm(False)
@@ -263,6 +309,10 @@ def main():
             "peak_source": "measured DMMA m8n8k4 FP64 peak (tools/peak_fp64.cu); MEASURED_PEAKS.json has no FP64 entry",
             "launches_per_step": gp["launches"], "gemm_ms_per_step": gp["ms"],
             "share_of_step": gp["ms"] / step_ms if step_ms > 0 else None}
+    # the HBM-class kernels: the eigen-coordinate Khatri-Rao basis over the
+    # same profiled solve, and cp_dot's Hadamard-of-Grams reduction at C4-iterate ranks
+    kr = ctx.profile_kernel(1, False)
+    roof_hbm = hbm_roofline(ctx, p.n, kr)
     # the north-star's mode-transform kernel at a C5 cell (fused Khatri-Rao inverse transform)
     roof_apply = apply_roofline(ctx, L, p.n)
     if rank != 0:
@@ -274,7 +324,10 @@ def main():
         "config": {"workload": WORKLOAD, "n": p.n, "eps": p.eps, "tol_stop": p.tol_stop,
                    "l2": "flushed (512 MiB write) between timed steps", "parallelism": "replicas",
                    "setup_ms": setup_ms},
-        "time_to_eps_ms": float(np.median(times)),
+        # every timed solve must have converged (rc 0, A13) for a time-to-eps to exist
+        "rc": sorted(set(int(r) for r in rcs)),
+        "converged_all": all(r == 0 for r in rcs),
+        "time_to_eps_ms": float(np.median(times)) if all(r == 0 for r in rcs) else None,
         "step_ms": [round(t, 2) for t in times],
         "slowest_step_iter_ms": [round(t, 1) for t in reps[int(np.argmax(times))]["t_iter_ms"]] if reps else [],
         "fastest_step_iter_ms": [round(t, 1) for t in reps[int(np.argmin(times))]["t_iter_ms"]] if reps else [],
@@ -285,13 +338,57 @@ def main():
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
         "roofline": roof,
         "roofline_apply": roof_apply,
+        "roofline_hbm": roof_hbm,
         "clocks": clk.summary(),
     }
-    if not args.no_cpu_baseline and world == 1 or (not args.no_cpu_baseline and rank == 0):
-        it, dt = oracle_sample(iters_cap=2)
+    if not args.no_cpu_baseline and world == 1:
+        st_o = device_setup_for_oracle(ctx, p, prm)
+        it, dt, rep_o = oracle_c4_step(p, st_o, kmax=1)
+        # same inputs, same first iteration: the oracle's residual and ranks are the device's
+        same = (abs(rep_o["rel_res"][0] - reps[-1]["rel_res"][0]) <= 1e-5 * reps[-1]["rel_res"][0]
+                and rep_o["rank_S"][0] == reps[-1]["rank_S"][0] and rep_o["rank_R"][0] == reps[-1]["rank_R"][0])
+        it64, dt64 = oracle_sample(iters_cap=2)
         line["cpu_baseline"] = {"value": it / dt, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle",
-                                "sample": "oracle PCG loop, C4 workload at n=64 (dense oracle setup infeasible at n=1024), 2 iterations"}
+                                "sample": ORACLE_SAMPLE, "seconds": dt, "iters": it,
+                                "first_iteration_matches_device": bool(same),
+                                "n64_own_setup": {"value": it64 / dt64, "unit": UNIT, "iters": it64, "seconds": dt64}}
     print(json.dumps(line), flush=True)
+
+
+def hbm_peak():
+    pk = _peaks()
+    for k in ("hbm_gbs", "hbm_copy_gbs", "hbm_GBps"):
+        if isinstance(pk.get(k), (int, float)):
+            return float(pk[k]), f"MEASURED_PEAKS.json {k}"
+    return 6536.0, "MEASURED_PEAKS.json hbm_gbs (6536) not readable: fallback"
+
+
+def hbm_roofline(ctx, n, kr, R=4096, reps=5):
+    """K9 (dot_reduce: sum_{k,m} wx wy G0 G1 G2, 24 B per entry) timed inside cp_dot of two
+    rank-R CPs at mode size n (C4 iterates reach R ~ 4000-6000), and K6 (Khatri-Rao basis of the
+    fused apply) over one profiled C4 solve (kr).  achieved = algorithmic bytes / event time."""
+    from paper_2006_09314_b200.binding import DeviceCP
+    from synth import random_cp
+    peak, src = hbm_peak()
+    w, U = random_cp(n, R, 41)
+    x = DeviceCP.from_numpy(w, U)
+    w, U = random_cp(n, R, 42)
+    y = DeviceCP.from_numpy(w, U)
+    ctx.cp_dot(x, y)
+    ctx.profile_kernel(0, True)
+    for _ in range(reps):
+        ctx.cp_dot(x, y)
+    d = ctx.profile_kernel(0, False)
+    ach = d["bytes"] / (d["ms"] * 1e-3) / 1e9 if d["ms"] > 0 else 0.0
+    kra = kr["bytes"] / (kr["ms"] * 1e-3) / 1e9 if kr["ms"] > 0 else 0.0
+    return {"dot_reduce": {"kernel": "dot_reduce_kernel (K9, cp_dot Hadamard-of-Grams reduction)",
+                           "bound": "hbm", "cell": {"n": n, "R1": R, "R2": R}, "achieved": ach, "peak": peak,
+                           "unit": "GB/s", "frac": ach / peak, "bytes_per_launch": d["bytes"] / max(d["launches"], 1),
+                           "ms_per_launch": d["ms"] / max(d["launches"], 1), "traffic": None, "peak_source": src},
+            "kr_basis": {"kernel": "hadamard_basis_kernel (K6, eigen-coordinate Khatri-Rao basis, one C4 solve)",
+                         "bound": "hbm", "achieved": kra, "peak": peak, "unit": "GB/s", "frac": kra / peak,
+                         "launches": kr["launches"], "bytes_per_launch": kr["bytes"] / max(kr["launches"], 1),
+                         "ms_per_launch": kr["ms"] / max(kr["launches"], 1), "traffic": None, "peak_source": src}}
 
 
 def apply_roofline(ctx, L, n, R=64, r=16, reps=10):

@@ -70,7 +70,9 @@ typedef struct {
     int kmax;            /* max PCG iterations (A17); <= 0 -> 100                           */
     int precond_rank;    /* rank r_G of the preconditioner CP (A7); <= 0 -> 6    [P:990]    */
     int op_rank;         /* > 0: fixed rank of the operator CP (C5 sweep); 0: eps_D-driven  */
-    int rank_cap;        /* max CP rank of any iterate (capacity); <= 0 -> 2^20             */
+    int rank_cap;        /* max CP rank of any iterate: a truncation whose eps-cut keeps more  */
+                         /* T2C triples keeps the top rank_cap (warning FC_RANK_CAP_HIT);    */
+                         /* <= 0 -> 2^20 (no cap)                                            */
     int boundary;        /* 0: paper boundary rule [P:517-518] (A2); 1: standard            */
     int precond_case;    /* FC_PRECOND_B (0, default, A6) or FC_PRECOND_A (1)   [P:758-868] */
 } fc_params;
@@ -105,6 +107,8 @@ typedef struct {
     double t_total_ms;              /* whole pcg_solve (device events)                       */
     double t_loop_ms;               /* loop only: iterations/s = iters / t_loop_ms * 1e3     */
     double normB;
+    int cap_hits;                   /* truncations clipped at params.rank_cap (their top      */
+                                    /* rank_cap T2C triples kept); > 0 -> FC_RANK_CAP_HIT     */
 } fc_pcg_report;
 
 /* ---- context -------------------------------------------------------------------------- */
@@ -201,8 +205,10 @@ int state_recover(fc_ctx ctx, const fc_cp* u, double eps, fc_cp* y, fc_trunc_inf
 
 /* pcg_solve: Algorithm 1 [P:1825-1872] with fun = fracop_apply(FC_F), precond =
  * fracop_apply(FC_G), trunc = cp_truncate(eps); X0 = 0 (A14), R0 = B untruncated (A15).
- * Returns FC_OK, FC_NOT_CONVERGED, or an error; u (device CP, cap >= final rank, else
- * CAPACITY) receives X; rep (host, may be NULL) the per-iteration history. */
+ * Returns FC_OK; FC_NOT_CONVERGED (kmax reached); FC_RANK_CAP_HIT (converged, but at least one
+ * truncation kept only the top p->rank_cap T2C triples: rep->cap_hits counts them; the
+ * eps-bound of those truncations does not hold); or an error.  u (device CP, cap >= final
+ * rank, else CAPACITY) receives X; rep (host, may be NULL) the per-iteration history. */
 int pcg_solve(fc_ctx ctx, const fc_cp* b, const fc_params* p, fc_cp* u, fc_pcg_report* rep);
 
 /* ---- the 2D variant ------------------------------------------------
@@ -280,6 +286,15 @@ int fc_syev(fc_ctx ctx, int nb, const int* N, double* const* A, const int* lda, 
  * roofline line).  enable=1 starts recording; enable=0 stops and returns the summed device
  * time (ms), the summed algorithmic flops (2 M N K per batch entry) and the launch count. */
 int fc_profile_gemm(fc_ctx ctx, int enable, double* ms, double* flops, long long* launches);
+/* Opt-in accounting of one HBM-class kernel (events around each launch on
+ * its stream): kernel = FC_KP_DOT_REDUCE (the Hadamard-of-Grams reduction of cp_dot, 24 bytes per
+ * (k, m) entry [P:1748-1755]) or FC_KP_KR_BASIS (the eigen-coordinate Khatri-Rao basis
+ * K = [w_a (.) V^T q_b] of fracop_apply_truncate, 8 bytes per written entry plus its inputs
+ * [P:1756-1763]).  enable=1 starts recording; enable=0 stops and returns the summed device time
+ * (ms), the summed algorithmic bytes and the launch count.  Errors: INVALID_ARG (kernel id). */
+#define FC_KP_DOT_REDUCE 0
+#define FC_KP_KR_BASIS   1
+int fc_profile_kernel(fc_ctx ctx, int kernel, int enable, double* ms, double* bytes, long long* launches);
 /* Process-wide count of CUDA kernels this library has launched (host-side counter). */
 int fc_kernel_launches(long long* count);
 

@@ -69,15 +69,20 @@ class NotSPD(RuntimeError):
     pass
 
 
-def pcg(fun, precond, B: CP, eps: float, tol_stop: float, kmax: int = 100, trunc=None):
-    """Algorithm 1.  fun/precond: CP -> CP (untruncated applies); trunc(x, eps) -> CP."""
+def pcg(fun, precond, B: CP, eps: float, tol_stop: float, kmax: int = 100, trunc=None,
+        rank_cap: int | None = None):
+    """Algorithm 1.  fun/precond: CP -> CP (untruncated applies); trunc(x, eps) -> CP.
+    rank_cap (A26): every truncation keeps at most rank_cap T2C triples; rep["cap_hits"] counts
+    the truncations that were clipped."""
     rep = {"rel_res": [], "rank_X": [], "rank_R": [], "rank_Z": [], "rank_P": [],
-           "rank_S": [], "t_iter": [], "converged": False, "iters": 0, "margins": []}
+           "rank_S": [], "t_iter": [], "converged": False, "iters": 0, "margins": [],
+           "cap_hits": 0}
     if trunc is None:
         def trunc(x, e):                                      # logs the cut margins (A23)
             info = {}
-            y = truncate(x, e, info)
+            y = truncate(x, e, info, rank_cap=rank_cap)
             rep["margins"].append(min(info.get("margins", [np.inf]) or [np.inf]))
+            rep["cap_hits"] += int(info.get("clipped", False))
             return y
     normB = cpm.norm(B)
     X = cpm.zeros(B.shape)                                   # X^(0) = 0          (A14)
@@ -113,14 +118,14 @@ def pcg(fun, precond, B: CP, eps: float, tol_stop: float, kmax: int = 100, trunc
     return X, rep
 
 
-def solve(problem, st: Setup | None = None, kmax=None, with_true_residual=False):
+def solve(problem, st: Setup | None = None, kmax=None, with_true_residual=False, rank_cap=None):
     """pcg_solve for a synth.Problem: returns (u, report, setup)."""
     st = setup(problem) if st is None else st
     B = cpm.normalized(problem.b_w, problem.b_U)
     fun = lambda x: cpm.apply(st.V, st.F, x)
     pre = lambda x: cpm.apply(st.VG if st.VG is not None else st.V, st.G, x)
     u, rep = pcg(fun, pre, B, problem.eps, problem.tol_stop,
-                 problem.kmax if kmax is None else kmax)
+                 problem.kmax if kmax is None else kmax, rank_cap=rank_cap)
     if with_true_residual:                                   # O11
         from .measure import diff_norm
         rep["true_residual"] = diff_norm(fun(u), B) / cpm.norm(B)

@@ -51,13 +51,15 @@ def rank_cut(s2: np.ndarray, thr: float, rmin: int = 1, margins: list | None = N
 
 
 def tucker_to_canonical(core: np.ndarray, Z: list, eps: float | None, keep: int | None = None,
-                        info: dict | None = None) -> CP:
+                        info: dict | None = None, rank_cap: int | None = None) -> CP:
     """T2C of the Tucker tensor core x_1 Z1 x_2 Z2 x_3 Z3 [P:1804-1812] (reading A10).
 
     Slice along the min-rank mode c (ties -> lowest mode); a < b are the other modes.
     SVD of every slice core(:,:,nu) (r_a x r_b); pool (s, nu, m); sort by s descending,
     ties by (nu, m); keep the smallest R with sum_{dropped} s^2 <= (eps/2)^2 ||core||_F^2
     (or the top `keep` triples).  Output factors Z_a a_m, Z_b b_m, Z_c[:, nu], weight s.
+    rank_cap (reading A26, the rank cap of Algorithm 1's iterates): R = min(R, rank_cap), i.e.
+    the top rank_cap triples of the pooled order; info["clipped"] records it.
     """
     r = core.shape
     c = int(np.argmin(r))
@@ -78,7 +80,11 @@ def tucker_to_canonical(core: np.ndarray, Z: list, eps: float | None, keep: int 
         R = min(keep, len(trip))
     else:
         R = rank_cut(s_all ** 2, (eps / 2.0) ** 2 * nb2, margins=margins)
+    clipped = rank_cap is not None and R > rank_cap
+    if clipped:
+        R = rank_cap
     if info is not None:
+        info["clipped"] = clipped
         info["t2c_mode"] = c
         info["t2c_candidates"] = len(trip)
         info["out_rank"] = R
@@ -89,8 +95,8 @@ def tucker_to_canonical(core: np.ndarray, Z: list, eps: float | None, keep: int 
     return CP(s_all[:R].copy(), U)
 
 
-def truncate(x: CP, eps: float, info: dict | None = None) -> CP:
-    """O9 steps 1-5 (RHOSVD -> core -> T2C)."""
+def truncate(x: CP, eps: float, info: dict | None = None, rank_cap: int | None = None) -> CP:
+    """O9 steps 1-5 (RHOSVD -> core -> T2C); rank_cap: see tucker_to_canonical (A26)."""
     # 1. drop terms with zero weight or a zero column
     keep = x.w != 0
     for l in range(3):
@@ -113,4 +119,4 @@ def truncate(x: CP, eps: float, info: dict | None = None) -> CP:
     core = np.einsum("t,at,bt,ct->abc", w, C[0], C[1], C[2])   # 4. beta
     if info is not None:
         info["tucker_rank"] = ranks
-    return tucker_to_canonical(core, Z, eps, info=info)        # 5. T2C
+    return tucker_to_canonical(core, Z, eps, info=info, rank_cap=rank_cap)   # 5. T2C

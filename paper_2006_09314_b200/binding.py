@@ -16,6 +16,7 @@ LIB_PATH = os.path.join(HERE, "libfraccontrol.so")
 
 FC_F, FC_G, FC_POW_PLUS, FC_POW_MINUS = 0, 1, 2, 3
 FC_PRECOND_B, FC_PRECOND_A = 0, 1
+FC_KP_DOT_REDUCE, FC_KP_KR_BASIS = 0, 1
 FC_MAX_ITERS = 256
 STATUS = {0: "OK", 1: "NOT_CONVERGED", 2: "RANK_CAP_HIT", -1: "INVALID_ARG", -2: "SHAPE",
           -3: "CAPACITY", -4: "NONPOS_COEF", -5: "NOT_SPD", -6: "NAN", -7: "EIG_NOCONV",
@@ -52,7 +53,7 @@ class fc_pcg_report(C.Structure):
                 ("rank_Z", C.c_int * FC_MAX_ITERS), ("rank_P", C.c_int * FC_MAX_ITERS),
                 ("rank_S", C.c_int * FC_MAX_ITERS), ("tucker_S", C.c_int * FC_MAX_ITERS),
                 ("t_iter_ms", C.c_double * FC_MAX_ITERS), ("t_total_ms", C.c_double),
-                ("t_loop_ms", C.c_double), ("normB", C.c_double)]
+                ("t_loop_ms", C.c_double), ("normB", C.c_double), ("cap_hits", C.c_int)]
 
     def as_dict(self):
         k = self.iters
@@ -61,7 +62,8 @@ class fc_pcg_report(C.Structure):
                 "rank_R": list(self.rank_R[:k]), "rank_Z": list(self.rank_Z[:k]),
                 "rank_P": list(self.rank_P[:k]), "rank_S": list(self.rank_S[:k]),
                 "tucker_S": list(self.tucker_S[:k]), "t_iter_ms": list(self.t_iter_ms[:k]),
-                "t_total_ms": self.t_total_ms, "t_loop_ms": self.t_loop_ms, "normB": self.normB}
+                "t_total_ms": self.t_total_ms, "t_loop_ms": self.t_loop_ms, "normB": self.normB,
+                "cap_hits": self.cap_hits}
 
 
 class FCError(RuntimeError):
@@ -74,7 +76,7 @@ ENTRY_POINTS = ["fc_create", "fc_destroy", "fc_last_error", "fc_set_stream", "sl
                 "sl_set_eigen", "op_get_spectral_cp", "op_set_spectral_cp", "op_spectral_rank",
                 "fracop_apply", "precond_apply", "cp_dot", "cp_axpy", "cp_truncate", "pcg_solve",
                 "fc_dgemm", "fc_dgemm_splitk", "fc_last_kernel_stats", "fc_kernel_launches", "fracop_apply_truncate", "fc_orthonormalize",
-                "fc_profile_gemm", "fc_syev", "op_get_precond_basis", "op_set_precond_basis", "state_recover", "op_build_spectral_sinc",
+                "fc_profile_gemm", "fc_profile_kernel", "fc_syev", "op_get_precond_basis", "op_set_precond_basis", "state_recover", "op_build_spectral_sinc",
                 "sl_setup_2d", "op_get_spectral_2d", "op_set_spectral_2d", "fracop_apply_2d", "cp_dot_2d",
                 "cp_truncate_2d", "pcg_solve_2d", "cp_truncate_als"]
 
@@ -105,6 +107,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "fc_kernel_launches": ([C.POINTER(C.c_longlong)], I),
         "fc_orthonormalize": ([P, I, I, P, P, D, C.POINTER(I)], I),
         "fc_profile_gemm": ([P, I, C.POINTER(D), C.POINTER(D), C.POINTER(C.c_longlong)], I),
+        "fc_profile_kernel": ([P, I, I, C.POINTER(D), C.POINTER(D), C.POINTER(C.c_longlong)], I),
         "fc_syev": ([P, I, C.POINTER(I), C.POINTER(P), C.POINTER(I), C.POINTER(P), C.POINTER(P), C.POINTER(I),
                      C.POINTER(I)], I),
         "op_get_precond_basis": ([P, I, P, P], I), "op_set_precond_basis": ([P, I, P, P], I),
@@ -466,6 +469,12 @@ class Context:
         ms, fl, nl = C.c_double(), C.c_double(), C.c_longlong()
         self._check(self.lib.fc_profile_gemm(self.h, 1 if enable else 0, C.byref(ms), C.byref(fl), C.byref(nl)))
         return {"ms": ms.value, "flops": fl.value, "launches": nl.value}
+
+    def profile_kernel(self, kernel: int, enable: bool):
+        ms, b, nl = C.c_double(), C.c_double(), C.c_longlong()
+        self._check(self.lib.fc_profile_kernel(self.h, kernel, 1 if enable else 0, C.byref(ms), C.byref(b),
+                                               C.byref(nl)))
+        return {"ms": ms.value, "bytes": b.value, "launches": nl.value}
 
     def orthonormalize(self, A, tau=1e-13):
         """A: torch (p, n) row-major == n x p column-major (overwritten).  Returns Q (k, n)."""

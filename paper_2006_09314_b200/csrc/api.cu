@@ -256,6 +256,13 @@ int fc_profile_gemm(fc_ctx c, int enable, double* ms, double* flops, long long* 
   });
 }
 
+int fc_profile_kernel(fc_ctx c, int kernel, int enable, double* ms, double* bytes, long long* launches) {
+  return guard(c, [&]() {
+    kprof_read(kernel, enable != 0, ms, bytes, launches);
+    return FC_OK;
+  });
+}
+
 int fc_kernel_launches(long long* count) {
   if (!count) return FC_ERR_INVALID_ARG;
   *count = fc::g_launches.load();

@@ -153,6 +153,18 @@ struct GemmArgs {
 void gemm(const GemmArgs& a, cudaStream_t st);
 // fc_profile_gemm: enable -> start recording; disable -> totals of the recorded launches
 void gemm_profile(bool enable, double* ms, double* flops, long long* launches);
+// fc_profile_kernel: opt-in accounting of the HBM-class kernels (events around each launch on
+// its stream, algorithmic bytes per launch), one record per kernel id
+enum KProfId { KP_DOT_REDUCE = 0, KP_KR_BASIS = 1, KP_COUNT = 2 };
+struct KProfScope {
+  int id;
+  cudaStream_t st;
+  double bytes;
+  bool on;
+  KProfScope(int id_, cudaStream_t st_, double bytes_);
+  ~KProfScope();
+};
+void kprof_read(int id, bool enable, double* ms, double* bytes, long long* launches);
 // split-K factor giving ~`waves` waves of 64 x 64 tiles on 148 SMs (at least 64 of K per split)
 inline int waves_splitk(const GemmArgs& a, int waves) {
   long long tiles = 0;

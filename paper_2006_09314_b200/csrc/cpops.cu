@@ -1,5 +1,7 @@
 // Elementwise / reduction kernels of the CP algebra (S6 weights, S8 normalisation, S9 axpy,
 // S10 cp_dot) [P:1748-1763].  All FP64, coalesced column-major access.
+#include <mutex>
+#include <vector>
 #include "cpops.cuh"
 
 namespace fc {
@@ -34,17 +36,46 @@ __global__ void apply_weights_kernel(int r, int R, const double* wF, const doubl
 }
 
 // out[blockIdx.x] = partial of sum_{k,m} wx[k] wy[m] G0[k,m] G1[k,m] G2[k,m]  (grid-stride,
-// deterministic: a fixed grid and a second single-block pass over the partials)
-__global__ void dot_reduce_kernel(int R1, int R2, const double* wx, const double* wy, const double* G0,
-                                  const double* G1, const double* G2, int ld, double* out) {
+// deterministic: a fixed grid and a second single-block pass over the partials).  HBM-bound
+// (K9, 24 bytes per (k, m) entry): contiguous Grams (ld == R1) are streamed as 16-byte double2
+// loads, two per operand in flight per thread; strided Grams take the scalar loop.
+__global__ void dot_reduce_kernel(int R1, int R2, const double* __restrict__ wx, const double* __restrict__ wy,
+                                  const double* __restrict__ G0, const double* __restrict__ G1,
+                                  const double* __restrict__ G2, int ld, double* out) {
   __shared__ double red[32];
   double acc = 0.0;
   const long long total = (long long)R1 * R2;
-  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
-       idx += (long long)gridDim.x * blockDim.x) {
-    int k = (int)(idx % R1), m = (int)(idx / R1);
-    size_t o = (size_t)k + (size_t)m * ld;
-    acc += wx[k] * wy[m] * (G0[o] * G1[o] * G2[o]);
+  const long long nth = (long long)gridDim.x * blockDim.x, t0 = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (ld == R1 && ((reinterpret_cast<size_t>(G0) | reinterpret_cast<size_t>(G1) | reinterpret_cast<size_t>(G2)) & 15) == 0) {
+    const long long npair = total >> 1;
+    const double2* A = reinterpret_cast<const double2*>(G0);
+    const double2* B = reinterpret_cast<const double2*>(G1);
+    const double2* Cc = reinterpret_cast<const double2*>(G2);
+    auto term = [&](long long idx, double g) {
+      const long long m = idx / R1, k = idx - m * R1;
+      return wx[k] * wy[m] * g;
+    };
+    long long p = t0;
+    for (; p + nth < npair; p += 2 * nth) {   // two pairs per operand in flight
+      const double2 a0 = __ldcs(A + p), b0 = __ldcs(B + p), c0 = __ldcs(Cc + p);
+      const double2 a1 = __ldcs(A + p + nth), b1 = __ldcs(B + p + nth), c1 = __ldcs(Cc + p + nth);
+      acc += term(2 * p, a0.x * b0.x * c0.x);
+      acc += term(2 * p + 1, a0.y * b0.y * c0.y);
+      acc += term(2 * (p + nth), a1.x * b1.x * c1.x);
+      acc += term(2 * (p + nth) + 1, a1.y * b1.y * c1.y);
+    }
+    for (; p < npair; p += nth) {
+      const double2 a0 = __ldcs(A + p), b0 = __ldcs(B + p), c0 = __ldcs(Cc + p);
+      acc += term(2 * p, a0.x * b0.x * c0.x);
+      acc += term(2 * p + 1, a0.y * b0.y * c0.y);
+    }
+    if ((total & 1) && t0 == 0) acc += term(total - 1, G0[total - 1] * G1[total - 1] * G2[total - 1]);
+  } else {
+    for (long long idx = t0; idx < total; idx += nth) {
+      int k = (int)(idx % R1), m = (int)(idx / R1);
+      size_t o = (size_t)k + (size_t)m * ld;
+      acc += wx[k] * wy[m] * (G0[o] * G1[o] * G2[o]);
+    }
   }
   for (int s = 16; s > 0; s >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, s);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
@@ -114,14 +145,80 @@ void apply_weights(int r, int R, const double* wF, const double* wx, const doubl
 void dot_reduce(int R1, int R2, const double* wx, const double* wy, const double* const G[3], int ld,
                 double* out_dev, cudaStream_t st) {
   const long long total = (long long)R1 * R2;
-  const int nb = (int)std::min<long long>(std::max<long long>((total + 8191) / 8192, 1), 296);
+  // up to 8 CTAs of 256 threads per SM (148 SMs), ~4 entries per thread and pass at least
+  const int nb = (int)std::min<long long>(std::max<long long>((total + 4095) / 4096, 1), 148 * 8);
   double* part = nullptr;
   FC_CUDA_TRY(cudaMallocAsync(&part, (size_t)nb * sizeof(double), st));
-  dot_reduce_kernel<<<nb, 512, 0, st>>>(R1, R2, wx, wy, G[0], G[1], G[2], ld, part);
-  FC_CHECK_LAUNCH();
+  {
+    KProfScope kp(KP_DOT_REDUCE, st, 24.0 * (double)total + 8.0 * (R1 + R2));
+    dot_reduce_kernel<<<nb, 256, 0, st>>>(R1, R2, wx, wy, G[0], G[1], G[2], ld, part);
+    FC_CHECK_LAUNCH();
+  }
   sum_kernel<<<1, 512, 0, st>>>(nb, part, out_dev);
   FC_CHECK_LAUNCH();
   FC_CUDA_TRY(cudaFreeAsync(part, st));
+}
+
+// ---- fc_profile_kernel: per-kernel events + algorithmic bytes (opt-in; see common.cuh) ----
+namespace {
+struct KProf {
+  std::mutex mu;
+  bool on = false;
+  std::vector<cudaEvent_t> ev;   // pairs, recycled
+  std::vector<double> bytes;
+  size_t used = 0;
+};
+KProf& kprof(int id) {
+  static KProf p[KP_COUNT];
+  return p[id];
+}
+}  // namespace
+
+KProfScope::KProfScope(int id_, cudaStream_t st_, double bytes_) : id(id_), st(st_), bytes(bytes_) {
+  KProf& P = kprof(id);
+  on = P.on;
+  if (!on) return;
+  std::lock_guard<std::mutex> lock(P.mu);
+  if (P.ev.size() < 2 * (P.used + 1))
+    for (int i = 0; i < 64; ++i) {
+      cudaEvent_t e;
+      FC_CUDA_TRY(cudaEventCreate(&e));
+      P.ev.push_back(e);
+    }
+  FC_CUDA_TRY(cudaEventRecord(P.ev[2 * P.used], st));
+}
+
+KProfScope::~KProfScope() {
+  if (!on) return;
+  KProf& P = kprof(id);
+  std::lock_guard<std::mutex> lock(P.mu);
+  cudaEventRecord(P.ev[2 * P.used + 1], st);
+  P.bytes.push_back(bytes);
+  ++P.used;
+}
+
+void kprof_read(int id, bool enable, double* ms, double* bytes, long long* launches) {
+  require(id >= 0 && id < KP_COUNT, FC_ERR_INVALID_ARG, "kernel id");
+  KProf& P = kprof(id);
+  std::lock_guard<std::mutex> lock(P.mu);
+  if (enable) {
+    P.on = true;
+    P.used = 0;
+    P.bytes.clear();
+    return;
+  }
+  P.on = false;
+  double t = 0, b = 0;
+  for (size_t i = 0; i < P.used; ++i) {
+    float x = 0;
+    FC_CUDA_TRY(cudaEventSynchronize(P.ev[2 * i + 1]));
+    FC_CUDA_TRY(cudaEventElapsedTime(&x, P.ev[2 * i], P.ev[2 * i + 1]));
+    t += x;
+    b += P.bytes[i];
+  }
+  if (ms) *ms = t;
+  if (bytes) *bytes = b;
+  if (launches) *launches = (long long)P.used;
 }
 
 void copy_cols3(const Mat3& src, const Mat3& dst, double scale, cudaStream_t st) {

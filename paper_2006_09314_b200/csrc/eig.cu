@@ -608,20 +608,25 @@ constexpr int kCl4MaxN = 440;    // packed own columns + 5 N vectors fit 220 KB 
 constexpr int kCl8MaxN = 600;    // ... with 8 CTAs
 constexpr int kCl16MaxN = 840;   // ... with 16 CTAs (non-portable cluster size)
 
-template <int CS>
+template <int CS, bool GL = false>
 __host__ __device__ inline size_t cluster_smem_doubles(int N) {
   const int ncol0 = (N + CS - 1) / CS;                                 // CTA 0 owns the most
-  const size_t P = (size_t)ncol0 * N - (size_t)CS * ncol0 * (ncol0 - 1) / 2;
+  const size_t P = GL ? 0 : (size_t)ncol0 * N - (size_t)CS * ncol0 * (ncol0 - 1) / 2;
   const int SL = (N + CS - 1) / CS;
   return P + 4 * (size_t)N + (size_t)CS * SL + 2 * (size_t)SL;
 }
+constexpr int kClGlobalMaxN = 2048;   // GL cluster path (own columns in L2) up to this size
 
 // a - 2 (ui qj + qi uj) with explicit roundings (identical wherever it is evaluated)
 __device__ __forceinline__ double rank2(double a, double ui, double qi, double uj, double qj) {
   return __fma_rn(-2.0, __fma_rn(ui, qj, __dmul_rn(qi, uj)), a);
 }
 
-template <int CS>
+// GL (N > kCl16MaxN): the own columns do not fit shared memory; each CTA keeps them in a
+// private slice of E.scratch (L2-resident: the whole triangle is <= 16 MB at N = 2048) and the
+// next pivot column is fetched from the owner's slice with L1-bypassing loads (ld.global.cg:
+// the owner updates it between fetches); the vectors stay in shared memory (DSMEM as above).
+template <int CS, bool GL>
 __global__ void __launch_bounds__(1024, 1) tridiag_cluster_kernel(const __grid_constant__ SyevBatch B, int nlo,
                                                                   int nhi) {
   namespace cg = cooperative_groups;
@@ -639,8 +644,8 @@ __global__ void __launch_bounds__(1024, 1) tridiag_cluster_kernel(const __grid_c
   // the same layout in every CTA (CTA 0 owns the most entries): map_shared_rank(ptr, r) maps
   // to the same offset in CTA r
   const size_t P = loff_of(0, SL);
-  double* L = sm;
-  double* u = L + P;          // Householder vector of the current step (absolute row index)
+  double* L = GL ? E.scratch + (size_t)c * P : sm;
+  double* u = GL ? sm : L + P;   // Householder vector of the current step (absolute row index)
   double* u1 = u + N;         // ... of the next step
   double* col = u1 + N;       // current pivot column (absolute row index)
   double* Y = col + N;        // partial matvec (read remotely)
@@ -724,8 +729,13 @@ __global__ void __launch_bounds__(1024, 1) tridiag_cluster_kernel(const __grid_c
     }
     {
       const int jn = s + 1, o = jn % CS, tn = jn / CS;
-      const double* Lo = cl.map_shared_rank(L, o) + loff_of(o, tn);
-      for (int i = i0 + tid; i < i1; i += nt) ncs[i - c * SL] = Lo[i - jn];
+      if (GL) {
+        const double* Lo = E.scratch + (size_t)o * P + loff_of(o, tn);
+        for (int i = i0 + tid; i < i1; i += nt) ncs[i - c * SL] = __ldcg(Lo + (i - jn));
+      } else {
+        const double* Lo = cl.map_shared_rank(L, o) + loff_of(o, tn);
+        for (int i = i0 + tid; i < i1; i += nt) ncs[i - c * SL] = Lo[i - jn];
+      }
     }
     if (c == 0)   // the Householder vector of step s into column s of A (all initial reads are done)
       for (int i = s + 1 + tid; i < N; i += nt) E.A[i + (size_t)s * E.lda] = u[i];
@@ -2014,9 +2024,9 @@ void sl_eigen_device(cudaStream_t st, int n, const double* a_mid_dev, int bounda
   }
 }
 
-template <int CS>
+template <int CS, bool GL = false>
 void launch_tridiag_cluster(const SyevBatch& b, size_t smem, cudaStream_t st, int nlo, int nhi) {
-  auto kern = tridiag_cluster_kernel<CS>;
+  auto kern = tridiag_cluster_kernel<CS, GL>;
   static bool attr = false;
   if (!attr) {
     FC_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
@@ -2048,7 +2058,9 @@ void syev_values(const SyevBatch& b, cudaStream_t st) {
   const int minG = no_cluster ? kPackedMaxN : kCl16MaxN;   // sizes above go to the global kernel
   const int maxP = no_cluster ? kPackedMaxN : kClusterMinN; // sizes up to this: packed single CTA
   int maxN = 0;
-  size_t smem_g = 0, smem_p = 0, smem_4 = 0, smem_8 = 0, smem_16 = 0;
+  size_t smem_g = 0, smem_p = 0, smem_4 = 0, smem_8 = 0, smem_16 = 0, smem_gl = 0;
+  static const bool no_gl = getenv("FC_NO_CLUSTER_GL") != nullptr;   // diagnostics: single-CTA kernel
+  const int maxGL = (no_cluster || no_gl) ? minG : kClGlobalMaxN;
   bool any_g = false, any_p = false;
   // cluster size classes (N in (lo, hi]): 16 CTAs (non-portable) for 97..840 (the per-step
   // matvec / rank-2 work per CTA matters more than the DSMEM fan-in: C4 solve 365 ms vs 371 ms
@@ -2064,9 +2076,11 @@ void syev_values(const SyevBatch& b, cudaStream_t st) {
     if (N <= maxP) {
       any_p = true;
       smem_p = std::max(smem_p, ((size_t)N * (N + 1) / 2 + 2 * (size_t)N) * 8);
-    } else if (N > minG) {
+    } else if (N > maxGL) {
       any_g = true;
       smem_g = std::max(smem_g, (size_t)(2 + NW) * N * 8);
+    } else if (N > minG) {
+      smem_gl = std::max(smem_gl, cluster_smem_doubles<16, true>(N) * 8);
     } else if (N <= cl4) {
       smem_4 = std::max(smem_4, cluster_smem_doubles<4>(N) * 8);
     } else if (N <= cl8) {
@@ -2078,6 +2092,7 @@ void syev_values(const SyevBatch& b, cudaStream_t st) {
   if (smem_4) launch_tridiag_cluster<4>(b, smem_4, st, maxP, cl4);
   if (smem_8) launch_tridiag_cluster<8>(b, smem_8, st, cl4, cl8);
   if (smem_16) launch_tridiag_cluster<16>(b, smem_16, st, cl8, kCl16MaxN);
+  if (smem_gl) launch_tridiag_cluster<16, true>(b, smem_gl, st, minG, maxGL);
   if (maxN == 0) return;
   require(smem_g <= kTriSmemMax, FC_ERR_CAPACITY, "symmetric eigensolver: matrix dimension above 1500");
   static bool attr = false;
@@ -2092,7 +2107,7 @@ void syev_values(const SyevBatch& b, cudaStream_t st) {
     FC_CHECK_LAUNCH();
   }
   if (any_g) {
-    tridiag_kernel<<<b.nb, kTriThreads, smem_g, st>>>(b, minG);
+    tridiag_kernel<<<b.nb, kTriThreads, smem_g, st>>>(b, maxGL);
     FC_CHECK_LAUNCH();
   }
   tri_bisect_kernel<<<dim3(cdiv(maxN, 8), b.nb), 256, (size_t)2 * maxN * 8, st>>>(b);

@@ -24,9 +24,27 @@
 namespace fc {
 namespace {
 
+// K6 (S6) in eigen coordinates: K[:, a*q + b] = W[:, a] (.) Zh[:, b] (n x s*q, written once:
+// HBM-write-bound; reads W (n x s) and Zh (n x q) from L2).  One CTA row per output column
+// block, 16-byte double2 stores along the (even) mode size.
 __global__ void hadamard_basis_kernel(int n, int s, const double* __restrict__ W, int q,
                                       const double* __restrict__ Zh, double* K) {
-  const long long tot = (long long)n * s * q;
+  const int cols = s * q;
+  const size_t al = reinterpret_cast<size_t>(W) | reinterpret_cast<size_t>(Zh) | reinterpret_cast<size_t>(K);
+  if ((n & 1) == 0 && (al & 15) == 0) {
+    const int n2 = n >> 1;
+    const long long tot = (long long)n2 * cols;
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < tot;
+         idx += (long long)gridDim.x * blockDim.x) {
+      const int col = (int)(idx / n2), i2 = (int)(idx - (long long)col * n2);
+      const int a = col / q, b = col - a * q;
+      const double2 w = __ldg(reinterpret_cast<const double2*>(W + (size_t)a * n) + i2);
+      const double2 z = __ldg(reinterpret_cast<const double2*>(Zh + (size_t)b * n) + i2);
+      __stcs(reinterpret_cast<double2*>(K + (size_t)col * n) + i2, make_double2(w.x * z.x, w.y * z.y));
+    }
+    return;
+  }
+  const long long tot = (long long)n * cols;
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < tot;
        idx += (long long)gridDim.x * blockDim.x) {
     int i = (int)(idx % n);
@@ -129,7 +147,7 @@ TT apply_truncate_tt(fc_ctx c, SpecCP& sp, const TT& x, double eps, int rank_cap
   TT y;   // eigen-coordinate Hadamard tensor: basis K_l, weights kron(w_F, w_x); no coefficients
   y.n = n;
   y.R = r * R;
-  size_t need = (size_t)y.R;
+  size_t need = (size_t)y.R + 1;
   for (int l = 0; l < 3; ++l) {
     y.q[l] = sp.s[l] * x.q[l];
     need += (size_t)n * x.q[l] + (size_t)n * y.q[l];
@@ -137,7 +155,7 @@ TT apply_truncate_tt(fc_ctx c, SpecCP& sp, const TT& x, double eps, int rank_cap
   y.mem.emplace_back(need * 8, st);
   double* p = y.mem.back().d();
   y.w = p;
-  p += y.R;
+  p += y.R + (y.R & 1);   // keep the basis blocks 16-byte aligned (double2 access)
   kron_w_kernel<<<cdiv(y.R, 256), 256, 0, st>>>(r, sp.w.p, R, x.w, y.w);
   FC_CHECK_LAUNCH();
   GemmArgs fwd;   // S5: Zhat_l = V_l^T Q_l
@@ -168,8 +186,12 @@ TT apply_truncate_tt(fc_ctx c, SpecCP& sp, const TT& x, double eps, int rank_cap
     y.Q[l] = p;
     p += (size_t)n * y.q[l];
     y.C[l] = nullptr;
-    hadamard_basis_kernel<<<nblocks((long long)n * y.q[l]), 256, 0, st>>>(n, sp.s[l], Wl, x.q[l], Zh[l], y.Q[l]);
-    FC_CHECK_LAUNCH();
+    {
+      KProfScope kp(KP_KR_BASIS, st, 8.0 * ((double)n * y.q[l] + (double)n * (sp.s[l] + x.q[l])));
+      hadamard_basis_kernel<<<nblocks((long long)n * y.q[l] / 2 + 1), 256, 0, st>>>(n, sp.s[l], Wl, x.q[l], Zh[l],
+                                                                                    y.Q[l]);
+      FC_CHECK_LAUNCH();
+    }
     y.orth[l] = false;
   }
   pm0->mark("0 apply: fwd + KR basis");
@@ -478,6 +500,7 @@ int pcg_solve(fc_ctx c, const fc_cp* b, const fc_params* prm, fc_cp* u, fc_pcg_r
     TT Z = apply_truncate_tt(c, G, R, eps, cap, &sZ);
     TT P = tt_copy(st, Z);
     double rz = tt_dot(c, R, Z);
+    RP.cap_hits = sZ.clipped;
     int status = FC_NOT_CONVERGED;
     cudaEvent_t loop0;
     FC_CUDA_TRY(cudaEventCreate(&loop0));
@@ -510,9 +533,11 @@ int pcg_solve(fc_ctx c, const fc_cp* b, const fc_params* prm, fc_cp* u, fc_pcg_r
       RP.rank_R[k] = R.R;
       RP.tucker_S[k] = std::max(sS.tucker[0], std::max(sS.tucker[1], sS.tucker[2]));
       RP.iters = k + 1;
+      RP.cap_hits += sS.clipped + sR.clipped;
       if (!std::isfinite(rel)) { cudaEventDestroy(loop0); throw Error(FC_ERR_NAN, "residual is not finite"); }
       if (rel <= tol) {
         X = xjob.join(&sX);
+        RP.cap_hits += sX.clipped;
         RP.rank_X[k] = X.R;
         RP.rank_Z[k] = Z.R;
         RP.rank_P[k] = P.R;
@@ -541,6 +566,7 @@ int pcg_solve(fc_ctx c, const fc_cp* b, const fc_params* prm, fc_cp* u, fc_pcg_r
       }
       rz = rz_new;
       X = xjob.join(&sX);
+      RP.cap_hits += sX.clipped + sZ2.clipped + sP.clipped;
       RP.rank_X[k] = X.R;
       RP.rank_Z[k] = Z.R;
       RP.rank_P[k] = P.R;
@@ -559,6 +585,7 @@ int pcg_solve(fc_ctx c, const fc_cp* b, const fc_params* prm, fc_cp* u, fc_pcg_r
     RP.t_loop_ms = tl;
     RP.t_total_ms = tt;
     RP.converged = status == FC_OK;
+    if (status == FC_OK && RP.cap_hits > 0) status = FC_RANK_CAP_HIT;   // converged, but clipped
     RP.status = status;
     store_tt(c, X, u);
     return status;

@@ -78,6 +78,157 @@ __global__ void struct_scale_kernel(int t, int R, int Rx, const double* __restri
   }
 }
 
+// ---- accurate factor of the per-term side Grams (A11' on the structured route) --------------
+// The structured side matrix of mode l is B = [Rm_1 W_1 | ... | Rm_r W_r], W_k = Cx diag(d_k)
+// (t x Rx per spectral term k).  B B^T = sum_k Rm_k L_k L_k^T Rm_k^T for ANY L_k with
+// L_k L_k^T = W_k W_k^T, so B's singular values are those of the explicit q x (r t) matrix
+// B~ = [Rm_k L_k]_k.  L_k is computed WITHOUT the Gram's squaring floor: H_k = W_k W_k^T is
+// accumulated in double-double (TwoProduct by FMA + TwoSum, ~1e-32 relative), factored by a
+// diagonally pivoted Cholesky in double-double, and only the factor is rounded to double.  A
+// rounding of L (or of Rm, or of a later product with B~) perturbs v^T B B^T v by
+// ~2 ||B^T v|| eps_mach ||B|| — linear in the small singular values, not eps_mach ||B||^2.
+constexpr int kFactorMaxT = 96;        // t (x's Tucker rank) handled by the factor kernel
+constexpr int kFactorThreads = 512;
+constexpr int kFactorJC = 32;          // W columns staged per chunk
+constexpr int kFactorEnt = (kFactorMaxT * (kFactorMaxT + 1) / 2 + kFactorThreads - 1) / kFactorThreads;
+
+struct dd { double hi, lo; };
+__device__ __forceinline__ dd dd_fast2sum(double a, double b) {
+  const double s = a + b;
+  return {s, b - (s - a)};
+}
+__device__ __forceinline__ dd dd_add(dd a, dd b) {           // (hi, lo) + (hi, lo), TwoSum on hi
+  const double s = a.hi + b.hi, bb = s - a.hi;
+  const double err = (a.hi - (s - bb)) + (b.hi - bb);
+  return dd_fast2sum(s, err + a.lo + b.lo);
+}
+__device__ __forceinline__ dd dd_mul(dd a, dd b) {
+  const double p = a.hi * b.hi;
+  const double e = fma(a.hi, b.hi, -p) + (a.hi * b.lo + a.lo * b.hi);
+  return dd_fast2sum(p, e);
+}
+__device__ __forceinline__ dd dd_div(dd a, dd b) {
+  const double q1 = a.hi / b.hi;
+  const dd r = dd_add(a, dd_mul({-q1, 0.0}, b));
+  return dd_fast2sum(q1, r.hi / b.hi);
+}
+__device__ __forceinline__ dd dd_sqrt(dd a) {
+  if (a.hi <= 0.0) return {0.0, 0.0};
+  const double s = sqrt(a.hi);
+  const double e = (fma(-s, s, a.hi) + a.lo) / (2.0 * s);
+  return dd_fast2sum(s, e);
+}
+
+// one CTA per spectral term k: L_k (t x t, column-major, ld t; columns beyond the numerical rank
+// are zero) with L_k L_k^T = W_k W_k^T, W_k[a, j] = Cx[a + j t] d[k Rx + j]
+__global__ void __launch_bounds__(kFactorThreads) struct_factor_kernel(int t, int Rx, const double* __restrict__ Cx,
+                                                                       const double* __restrict__ d, double* Lout) {
+  extern __shared__ double fsm[];
+  const int k = blockIdx.x, tid = threadIdx.x;
+  const int ne = t * (t + 1) / 2;
+  double* Wc = fsm;                                  // t x kFactorJC chunk of W_k
+  double* Hh = fsm + (size_t)t * kFactorJC;          // t x t (hi), later the Schur complement
+  double* Hl = Hh + (size_t)t * t;                   // t x t (lo)
+  double* Lc = Hl + (size_t)t * t;                   // current column (hi, lo): 2 t
+  double* piv = Lc + 2 * t;                          // used flags: t
+  // entry e -> (a, b), a >= b, row-major over the lower triangle
+  int ea[kFactorEnt], eb[kFactorEnt];
+  dd acc[kFactorEnt];
+#pragma unroll
+  for (int q = 0; q < kFactorEnt; ++q) {
+    const int e = tid + q * kFactorThreads;
+    int a = 0, b = 0;
+    if (e < ne) {
+      a = (int)((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
+      while ((a + 1) * (a + 2) / 2 <= e) ++a;
+      while (a * (a + 1) / 2 > e) --a;
+      b = e - a * (a + 1) / 2;
+    }
+    ea[q] = a;
+    eb[q] = b;
+    acc[q] = {0.0, 0.0};
+  }
+  const double* dk = d + (size_t)k * Rx;
+  for (int j0 = 0; j0 < Rx; j0 += kFactorJC) {
+    const int jc = min(kFactorJC, Rx - j0);
+    __syncthreads();
+    for (int idx = tid; idx < t * jc; idx += kFactorThreads) {
+      const int a = idx % t, jj = idx / t;
+      Wc[a + jj * t] = Cx[a + (size_t)(j0 + jj) * t] * dk[j0 + jj];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < kFactorEnt; ++q) {
+      if (tid + q * kFactorThreads >= ne) break;
+      const int a = ea[q], b = eb[q];
+      double hi = acc[q].hi, lo = acc[q].lo;
+      for (int jj = 0; jj < jc; ++jj) {
+        const double x = Wc[a + jj * t], y = Wc[b + jj * t];
+        const double p = x * y, pe = fma(x, y, -p);
+        const double s = hi + p, bb = s - hi;
+        lo += ((hi - (s - bb)) + (p - bb)) + pe;
+        hi = s;
+      }
+      acc[q] = dd_fast2sum(hi, lo);
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < kFactorEnt; ++q) {
+    if (tid + q * kFactorThreads >= ne) break;
+    const int a = ea[q], b = eb[q];
+    Hh[a + b * t] = Hh[b + a * t] = acc[q].hi;
+    Hl[a + b * t] = Hl[b + a * t] = acc[q].lo;
+  }
+  for (int i = tid; i < t; i += kFactorThreads) piv[i] = 0.0;
+  double* L = Lout + (size_t)k * t * t;
+  for (int i = tid; i < t * t; i += kFactorThreads) L[i] = 0.0;
+  __syncthreads();
+  __shared__ double s_tr;
+  __shared__ int s_p;
+  if (tid == 0) {
+    double tr = 0.0;
+    for (int i = 0; i < t; ++i) tr += Hh[i + i * t];
+    s_tr = tr;
+  }
+  __syncthreads();
+  const double stop = 1e-30 * s_tr;
+  for (int c = 0; c < t; ++c) {
+    if (tid == 0) {                                   // diagonal pivot: the largest Schur diagonal
+      int p = -1;
+      double best = stop;
+      for (int i = 0; i < t; ++i)
+        if (piv[i] == 0.0 && Hh[i + i * t] > best) {
+          best = Hh[i + i * t];
+          p = i;
+        }
+      s_p = p;
+      if (p >= 0) piv[p] = 1.0;
+    }
+    __syncthreads();
+    const int p = s_p;
+    if (p < 0) break;                                 // the rest of H is below 1e-30 of its trace
+    const dd sp = dd_sqrt({Hh[p + p * t], Hl[p + p * t]});
+    for (int i = tid; i < t; i += kFactorThreads) {
+      dd v = {0.0, 0.0};
+      if (i == p) v = sp;
+      else if (piv[i] == 0.0) v = dd_div({Hh[i + p * t], Hl[i + p * t]}, sp);
+      Lc[2 * i] = v.hi;
+      Lc[2 * i + 1] = v.lo;
+      L[i + (size_t)c * t] = v.hi + v.lo;
+    }
+    __syncthreads();
+    for (int idx = tid; idx < t * t; idx += kFactorThreads) {   // Schur complement (unpivoted rows)
+      const int i = idx % t, j = idx / t;
+      if (piv[i] != 0.0 || piv[j] != 0.0 || j > i) continue;
+      const dd v = dd_add({Hh[idx], Hl[idx]}, dd_mul({-Lc[2 * i], -Lc[2 * i + 1]}, {Lc[2 * j], Lc[2 * j + 1]}));
+      Hh[idx] = Hh[j + i * t] = v.hi;
+      Hl[idx] = Hl[j + i * t] = v.lo;
+    }
+    __syncthreads();
+  }
+}
+
 // out[:, c] = in[:, c] * d[c]   (rows x cols, ld rows)
 __global__ void scale_cols_kernel(int rows, int cols, const double* __restrict__ in, const double* __restrict__ d,
                                   double* out) {
@@ -959,7 +1110,13 @@ TT tucker_to_canonical(fc_ctx c, const double* core, const int r[3], double* con
     stats->t2c_mode = mc;
     stats->out_rank = R;
   }
-  if (rank_cap > 0 && R > rank_cap) throw Error(FC_ERR_CAPACITY, "truncation output rank above the rank cap");
+  if (rank_cap > 0 && R > rank_cap) {   // clip to the top rank_cap triples (a prefix of the pooled order)
+    R = rank_cap;
+    if (stats) {
+      stats->clipped = true;
+      stats->out_rank = R;
+    }
+  }
   TT out;
   out.n = n;
   out.R = R;
@@ -1403,6 +1560,7 @@ TT truncate_tt(fc_ctx c, const TT& xin, double eps, int rank_cap, TruncStats* st
     }
     syev_vectors(eb, maxq, st, hr);
   }
+  if (any_refine) pm.mark("4b1 refine: trusted vectors");
   if (any_refine && !refine_all) {
     // orthonormal basis of the complement of the trusted vectors: blocked Gram-Schmidt of
     // [Y_t | I_q] seeded with the orthonormal Y_t (k_base = pk) -> columns pk..q-1 of Y
@@ -1426,6 +1584,7 @@ TT truncate_tt(fc_ctx c, const TT& xin, double eps, int rank_cap, TruncStats* st
       FC_CUDA_TRY(cudaMemcpyAsync(Y[l] + (size_t)pk * ql, Qc + (size_t)pk * ql, (size_t)ql * (ql - pk) * 8,
                                   cudaMemcpyDeviceToDevice, st));
     }
+    pm.mark("4b2 refine: complement basis");
   }
   if (any_refine) {
     for (int l = 0; l < 3; ++l) {
@@ -1460,6 +1619,38 @@ TT truncate_tt(fc_ctx c, const TT& xin, double eps, int rank_cap, TruncStats* st
         const int t = ss->t[l], rr = ss->r, Rx = ss->Rx;
         double* YR = s.alloc<double>((size_t)m * t * rr);
         dgemm(st, 1, 0, m, t * rr, ql, 1.0, Yns, ql, RmE[l], ql, 0.0, YR, m);
+        static const bool no_factor = getenv("FC_NO_STRUCT_FACTOR") != nullptr;   // diagnostics
+        if (t <= kFactorMaxT && !no_factor) {
+          // G_ns = sum_kk (YR_kk L_kk)(YR_kk L_kk)^T with L_kk L_kk^T = W_kk W_kk^T (the accurate
+          // factor above): an m x (t r) product instead of m x (Rx r) (Rx = x's CP rank)
+          double* Lf = s.alloc<double>((size_t)t * t * rr);
+          const size_t fsmem = ((size_t)t * kFactorJC + 2 * (size_t)t * t + 3 * (size_t)t) * 8;
+          static bool fattr = false;
+          if (!fattr) {
+            FC_CUDA_TRY(cudaFuncSetAttribute(struct_factor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)(((size_t)kFactorMaxT * kFactorJC + 2 * (size_t)kFactorMaxT * kFactorMaxT +
+                                                    3 * (size_t)kFactorMaxT) * 8)));
+            fattr = true;
+          }
+          struct_factor_kernel<<<rr, kFactorThreads, fsmem, st>>>(t, Rx, ss->Cx[l], dl[l], Lf);
+          FC_CHECK_LAUNCH();
+          double* Ct = s.alloc<double>((size_t)m * t * rr);
+          GemmArgs g;
+          g.nbatch = 1;
+          g.rep = rr;
+          g.b[0] = GemmBatch{m, t, t, YR, m, Lf, t, Ct, m, nullptr, 0, nullptr};
+          g.b[0].sA = (long long)m * t;
+          g.b[0].sB = (long long)t * t;
+          g.b[0].sC = (long long)m * t;
+          gemm(g, st);
+          GemmArgs gg;
+          gg.transB = 1;
+          gg.nbatch = 1;
+          gg.beta = 1.0;
+          gg.b[0] = GemmBatch{m, m, t * rr, Ct, m, Ct, m, G, m, nullptr, 0, nullptr};
+          gg.splitk = waves_splitk(gg, 4);
+          gemm(gg, st);
+        } else {
         const int kc = std::max(1, (int)std::min<size_t>((size_t)rr, ((size_t)1 << 26) /
                                                                    std::max<size_t>((size_t)std::max(m, t) * Rx, 1)));
         double* Wc = s.alloc<double>((size_t)t * Rx * kc);
@@ -1479,7 +1670,9 @@ TT truncate_tt(fc_ctx c, const TT& xin, double eps, int rank_cap, TruncStats* st
           gemm(g, st);
           dgemm(st, 0, 1, m, m, nk * Rx, 1.0, Cb, m, Cb, m, 1.0, G, m);
         }
+        }
       }
+      pm.mark("4b3 refine: noise Gram");
       // eigen of G_ns (all vectors): mu descending, V_ns
       SyevBatch gb;
       double* mu = s.alloc<double>(m);
@@ -1505,6 +1698,7 @@ TT truncate_tt(fc_ctx c, const TT& xin, double eps, int rank_cap, TruncStats* st
         dgemm(st, 0, 0, ql, nv, m, 1.0, Yns, ql, Vn, m, 0.0, Yr, ql);
         FC_CUDA_TRY(cudaMemcpyAsync(Yns, Yr, (size_t)ql * nv * 8, cudaMemcpyDeviceToDevice, st));
       }
+      pm.mark("4b4 refine: noise eig");
     }
     int r_gram[3] = {r[0], r[1], r[2]};
     FC_CUDA_TRY(cudaMemcpyAsync(r, rl, 3 * sizeof(int), cudaMemcpyDeviceToHost, st));

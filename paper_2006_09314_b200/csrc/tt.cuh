@@ -77,10 +77,12 @@ struct TruncStats {
   int in_rank = 0, out_rank = 0, t2c_mode = 0;
   double energy = 0.0, min_margin = 1e300;
   bool refined = false;   // a noise-limited cut was decided from data-based tails (A11')
+  bool clipped = false;   // the T2C output was clipped to the rank cap (FC_RANK_CAP_HIT)
 };
 
 // RHOSVD -> core -> T2C (S11-S13).  Output: orthonormal Q (n x r_l), orthogonal CP terms.
-// rank_cap > 0: output rank limit (FC_ERR_CAPACITY with stats.out_rank = required).
+// rank_cap > 0: output rank limit: the T2C keeps its top rank_cap triples (pooled order) and
+// sets stats.clipped (pcg_solve then returns FC_RANK_CAP_HIT).
 // als_sweeps > 0: C2T-ALS refinement (HOOI sweeps with the RHOSVD ranks) before the core (CP route).
 TT truncate_tt(fc_ctx c, const TT& x, double eps, int rank_cap, TruncStats* stats,
                const StructuredS* ss = nullptr, int als_sweeps = 0);

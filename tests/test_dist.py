@@ -64,8 +64,9 @@ def test_reference_arm_other_ranks_exit_silently():
     assert out.stdout.strip() == ""
 
 
-@pytest.mark.slow
+@pytest.mark.gpu
 def test_reference_arm_rank0_line():
+    """The reference arm (the oracle on C4 n = 1024) takes the device-built setup: GPU box only."""
     env = dict(os.environ, RANK="0", WORLD_SIZE="1", LOCAL_RANK="0")
     out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference",
                           "--steps", "1", "--warmup", "0"], env=env, capture_output=True, text=True, timeout=600)

@@ -54,7 +54,7 @@ def test_caseA_pcg_shared(lib, name, n, alpha, beta):
     """Shared inputs: the oracle's SL eigenpairs, F, the DST basis and G_A injected; ranks and
     iterations as the oracle's (marginal cuts excepted), u within max(10 eps, 1e-9)."""
     from paper_2006_09314_b200.binding import FC_F, FC_G, DeviceCP, make_params
-    from test_gpu_truncate_pcg import check_rank_history
+    from _parity import check_rank_history
     p = make_problem(name, n=n, alpha=alpha, beta=beta, precond="A")
     st = P.setup(p)
     ctx = lib.context()

@@ -31,11 +31,12 @@ def _graded_psd(N, seed, decay=16.0):
     return 0.5 * (M + M.T)
 
 
-@pytest.mark.parametrize("sizes", [[200, 400, 700], [231, 600, 601, 840], [1000], [17, 841], [96, 97, 440, 441]])
+@pytest.mark.parametrize("sizes", [[200, 400, 700], [231, 600, 601, 840], [1000], [17, 841], [96, 97, 440, 441],
+                                   [1400, 900], [1500]])
 def test_syev_paths(lib, sizes):
     """fc_syev (the truncation's Gram eigensolver) on every tridiagonalisation path: packed
     shared memory (N <= 96), 16-CTA cluster (97..840; FC_TRI_CS=8 / 4: 8-CTA up to 600 / 4-CTA
-    up to 440), global (> 840), mixed in one batch; the eigenvectors through the polar
+    up to 440), 16-CTA cluster with the columns in L2 (841..2048), mixed in one batch; the eigenvectors through the polar
     orthonormalisation (host-known ranks).  Eigenvalues within 20 eps ||M|| of LAPACK; the leading 64 eigenvectors
     orthonormal with residual <= 1e-13 ||M||."""
     import torch
