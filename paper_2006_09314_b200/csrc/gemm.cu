@@ -387,18 +387,47 @@ __device__ __forceinline__ void load_op(double* T, const double* base, int ld, i
   }
 }
 
-// Khatri-Rao operand tile (K contiguous): column c -> W[:, c % R] and U[:, c / R]
-__device__ __forceinline__ void load_kr(double* T, double* TK, const GemmBatch& g, const double* gB, const double* gK,
-                                        int krR, int n0, int k0, int kend, int tid) {
+// Khatri-Rao operand tile (K contiguous): column c -> W[:, c % R] and U[:, c / R].  The two
+// column base pointers of each of a thread's chunk rows are fixed for the whole K loop, so they
+// are formed once (no division per tile); 16-byte cp.async when both operands allow it.
+struct KRRows {
+  const double* b[2];
+  const double* k[2];
+  bool ok[2];
+};
+__device__ __forceinline__ KRRows kr_rows(const GemmBatch& g, const double* gB, const double* gK, int krR, int n0,
+                                          int tid) {
+  KRRows p;
 #pragma unroll
-  for (int i = 0; i < 2048 / NT; ++i) {
-    const int idx = tid + i * NT;
-    const int rr = idx >> 4, kk = idx & 15;
-    const int c = n0 + rr, k = k0 + kk;
-    const bool ok = (c < g.N) && (k < kend);
-    const int kf = ok ? c / krR : 0, j = ok ? c - kf * krR : 0;
-    cp_async8(T + rr * LDM + kk, ok ? gB + (size_t)k + (size_t)j * g.ldb : gB, ok);
-    cp_async8(TK + rr * LDM + kk, ok ? gK + (size_t)k + (size_t)kf * g.ldkr : gK, ok);
+  for (int i = 0; i < 2; ++i) {
+    const int c = n0 + (tid >> 3) + i * (NT >> 3);
+    p.ok[i] = c < g.N;
+    const int kf = p.ok[i] ? c / krR : 0, j = p.ok[i] ? c - kf * krR : 0;
+    p.b[i] = gB + (size_t)j * g.ldb;
+    p.k[i] = gK + (size_t)kf * g.ldkr;
+  }
+  return p;
+}
+__device__ __forceinline__ void load_kr(double* T, double* TK, const KRRows& p, const double* gB, const double* gK,
+                                        int k0, int kend, int tid, bool vec) {
+  const int kk = (tid & 7) * 2, k = k0 + kk;
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const int rr = (tid >> 3) + i * (NT >> 3);
+    double* dB = T + rr * LDM + kk;
+    double* dK = TK + rr * LDM + kk;
+    if (vec) {
+      const int nk = p.ok[i] ? max(0, min(2, kend - k)) : 0;
+      cp_async16(dB, nk > 0 ? p.b[i] + k : gB, nk * 8);
+      cp_async16(dK, nk > 0 ? p.k[i] + k : gK, nk * 8);
+    } else {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const bool ok = p.ok[i] && (k + e < kend);
+        cp_async8(dB + e, ok ? p.b[i] + k + e : gB, ok);
+        cp_async8(dK + e, ok ? p.k[i] + k + e : gK, ok);
+      }
+    }
   }
 }
 
@@ -435,10 +464,16 @@ __global__ void __launch_bounds__(NT, 1) dgemm_big_kernel(const __grid_constant_
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
+  KRRows krp{};
+  bool vecKR = false;
+  if (KR) {
+    krp = kr_rows(g, gB, gK, args.krR, n0, tid);
+    vecKR = ((g.ldb & 1) == 0) && ((g.ldkr & 1) == 0) && (((uintptr_t)gB & 15) == 0) && (((uintptr_t)gK & 15) == 0);
+  }
   auto issue = [&](int s, int kt) {
     const int k0 = kbeg + kt * BK;
     load_op<AK>(As + s * TILE, gA, g.lda, m0, g.M, k0, kend, tid, vecA);
-    if (KR) load_kr(Bs + s * TILE, Ks + s * TILE, g, gB, gK, args.krR, n0, k0, kend, tid);
+    if (KR) load_kr(Bs + s * TILE, Ks + s * TILE, krp, gB, gK, k0, kend, tid, vecKR);
     else load_op<BKc>(Bs + s * TILE, gB, g.ldb, n0, g.N, k0, kend, tid, vecB);
   };
 #pragma unroll

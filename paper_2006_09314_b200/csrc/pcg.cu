@@ -24,11 +24,20 @@
 namespace fc {
 namespace {
 
-// K6 (S6) in eigen coordinates: K[:, a*q + b] = W[:, a] (.) Zh[:, b] (n x s*q, written once:
-// HBM-write-bound; reads W (n x s) and Zh (n x q) from L2).  One CTA row per output column
-// block, 16-byte double2 stores along the (even) mode size.
-__global__ void hadamard_basis_kernel(int n, int s, const double* __restrict__ W, int q,
-                                      const double* __restrict__ Zh, double* K) {
+// K6 (S6) in eigen coordinates, the 3 modes in one launch (blockIdx.y = mode):
+// K_l[:, a*q + b] = W_l[:, a] (.) Zh_l[:, b] (n x s_l q_l, written once: HBM-write-bound; W and
+// Zh are re-read from L2), 16-byte double2 loads / streaming stores along the (even) mode size.
+struct KRBasisArgs {
+  int n, s[3], q[3];
+  const double* W[3];
+  const double* Zh[3];
+  double* K[3];
+};
+__global__ void hadamard_basis_kernel(const __grid_constant__ KRBasisArgs A) {
+  const int l = blockIdx.y, n = A.n, s = A.s[l], q = A.q[l];
+  const double* __restrict__ W = A.W[l];
+  const double* __restrict__ Zh = A.Zh[l];
+  double* K = A.K[l];
   const int cols = s * q;
   const size_t al = reinterpret_cast<size_t>(W) | reinterpret_cast<size_t>(Zh) | reinterpret_cast<size_t>(K);
   if ((n & 1) == 0 && (al & 15) == 0) {
@@ -177,6 +186,10 @@ TT apply_truncate_tt(fc_ctx c, SpecCP& sp, const TT& x, double eps, int rank_cap
   ss.Rx = R;
   ss.wF = sp.w.p;
   ss.core_x = core_x;
+  KRBasisArgs kra;
+  kra.n = n;
+  double kr_bytes = 0.0;
+  long long kr_max = 0;
   for (int l = 0; l < 3; ++l) {   // S6: the Khatri-Rao basis [w_a (.) xhat_b]
     const double* Wl = sp.W.p + (size_t)l * n * sp.smax;
     ss.s[l] = sp.s[l];
@@ -186,13 +199,21 @@ TT apply_truncate_tt(fc_ctx c, SpecCP& sp, const TT& x, double eps, int rank_cap
     y.Q[l] = p;
     p += (size_t)n * y.q[l];
     y.C[l] = nullptr;
-    {
-      KProfScope kp(KP_KR_BASIS, st, 8.0 * ((double)n * y.q[l] + (double)n * (sp.s[l] + x.q[l])));
-      hadamard_basis_kernel<<<nblocks((long long)n * y.q[l] / 2 + 1), 256, 0, st>>>(n, sp.s[l], Wl, x.q[l], Zh[l],
-                                                                                    y.Q[l]);
-      FC_CHECK_LAUNCH();
-    }
+    kra.s[l] = sp.s[l];
+    kra.q[l] = x.q[l];
+    kra.W[l] = Wl;
+    kra.Zh[l] = Zh[l];
+    kra.K[l] = y.Q[l];
+    kr_bytes += 8.0 * ((double)n * y.q[l] + (double)n * (sp.s[l] + x.q[l]));
+    kr_max = std::max(kr_max, (long long)n * y.q[l]);
     y.orth[l] = false;
+  }
+  {
+    KProfScope kp(KP_KR_BASIS, st, kr_bytes);
+    // ~8 resident 256-thread CTAs per SM over the 3 modes, 16 bytes per thread and pass
+    const int gx = (int)std::max<long long>(1, std::min<long long>((kr_max / 2 + 255) / 256, 148 * 8 / 3 + 1));
+    hadamard_basis_kernel<<<dim3(gx, 3), 256, 0, st>>>(kra);
+    FC_CHECK_LAUNCH();
   }
   pm0->mark("0 apply: fwd + KR basis");
   pm0.reset();

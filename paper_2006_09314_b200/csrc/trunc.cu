@@ -1563,43 +1563,55 @@ TT truncate_tt(fc_ctx c, const TT& xin, double eps, int rank_cap, TruncStats* st
   if (any_refine) pm.mark("4b1 refine: trusted vectors");
   if (any_refine && !refine_all) {
     // orthonormal basis of the complement of the trusted vectors: blocked Gram-Schmidt of
-    // [Y_t | I_q] seeded with the orthonormal Y_t (k_base = pk) -> columns pk..q-1 of Y
+    // [Y_t | I_q] seeded with the orthonormal Y_t (k_base = pk) -> columns pk..q-1 of Y; the
+    // refined modes share one batched Gram-Schmidt
+    BcgsBatch cb;
+    int* kd = s.zeros<int>(4);
+    int cmap[3] = {-1, -1, -1};
+    double* Qc[3] = {nullptr, nullptr, nullptr};
     for (int l = 0; l < 3; ++l) {
       if (!refine[l] || pkv[l] >= q[l]) continue;
       const int ql = q[l], pk = pkv[l];
-      Scratch sc(st);
-      double* A = sc.zeros<double>((size_t)ql * (pk + ql));
+      double* A = s.zeros<double>((size_t)ql * (pk + ql));
       if (pk > 0) FC_CUDA_TRY(cudaMemcpyAsync(A, Y[l], (size_t)ql * pk * 8, cudaMemcpyDeviceToDevice, st));
       eye_kernel<<<blocks_for(ql), 256, 0, st>>>(ql, A + (size_t)ql * pk);
       FC_CHECK_LAUNCH();
-      BcgsBatch cb;
-      int* kd = sc.zeros<int>(1);
-      double* Qc = sc.alloc<double>((size_t)ql * ql);
-      cb.e[cb.nb++] = BcgsEntry{ql, pk + ql, A, ql, Qc, ql, ql, kd, sc.alloc<double>(pk + ql),
-                                sc.alloc<double>((size_t)ql * kBcgsW), kBasisTol};
-      cb.e[0].k_base = pk;
+      Qc[l] = s.alloc<double>((size_t)ql * ql);
+      cmap[l] = cb.nb;
+      cb.e[cb.nb++] = BcgsEntry{ql, pk + ql, A, ql, Qc[l], ql, ql, kd + l, s.alloc<double>(pk + ql),
+                                s.alloc<double>((size_t)ql * kBcgsW), kBasisTol};
+      cb.e[cb.nb - 1].k_base = pk;
+    }
+    if (cb.nb) {
       bcgs(cb, st);
-      const int kc = read_int(kd, st);
-      require(kc == ql, FC_ERR_CUDA, "noise-subspace complement basis incomplete");
-      FC_CUDA_TRY(cudaMemcpyAsync(Y[l] + (size_t)pk * ql, Qc + (size_t)pk * ql, (size_t)ql * (ql - pk) * 8,
-                                  cudaMemcpyDeviceToDevice, st));
+      int kh[4] = {0, 0, 0, 0};
+      FC_CUDA_TRY(cudaMemcpyAsync(kh, kd, 3 * sizeof(int), cudaMemcpyDeviceToHost, st));
+      FC_CUDA_TRY(cudaStreamSynchronize(st));
+      for (int l = 0; l < 3; ++l) {
+        if (cmap[l] < 0) continue;
+        const int ql = q[l], pk = pkv[l];
+        require(kh[l] == ql, FC_ERR_CUDA, "noise-subspace complement basis incomplete");
+        FC_CUDA_TRY(cudaMemcpyAsync(Y[l] + (size_t)pk * ql, Qc[l] + (size_t)pk * ql, (size_t)ql * (ql - pk) * 8,
+                                    cudaMemcpyDeviceToDevice, st));
+      }
     }
     pm.mark("4b2 refine: complement basis");
   }
   if (any_refine) {
+    // split: the pk eigenvalues above the noise level are trusted; the noise subspace Y_ns
+    // (ql x m) is re-diagonalised from the data: G_ns = C C^T with C = Y_ns^T B computed
+    // explicitly (rounding ~ eps_mach ||C||^2, i.e. ~1e-32 of the energy instead of 1e-16).
+    // The refined modes' G_ns go through one batched eigensolver.
+    SyevBatch gb;
+    int gmap[3] = {-1, -1, -1}, mm[3] = {0, 0, 0};
+    double* mu[3] = {nullptr, nullptr, nullptr};
+    double* Vn[3] = {nullptr, nullptr, nullptr};
+    int* rm = s.alloc<int>(4);
     for (int l = 0; l < 3; ++l) {
       if (!refine[l]) continue;
-      const int ql = q[l];
-      // split: the p eigenvalues above the noise level are trusted; the noise subspace Y_ns
-      // (ql x m) is re-diagonalised from the data: G_ns = C C^T with C = Y_ns^T B computed
-      // explicitly (rounding ~ eps_mach ||C||^2, i.e. ~1e-32 of the energy instead of 1e-16)
-      std::vector<double> hl(ql);
-      FC_CUDA_TRY(cudaMemcpyAsync(hl.data(), lam[l], (size_t)ql * 8, cudaMemcpyDeviceToHost, st));
-      FC_CUDA_TRY(cudaStreamSynchronize(st));
-      const double noise = kNoise * ql * 2.220446049250313e-16 * lam0[l];
-      int pk = 0;
-      while (pk < ql && hl[pk] > noise) ++pk;
+      const int ql = q[l], pk = pkv[l];
       const int m = ql - pk;
+      mm[l] = m;
       if (m == 0) {
         rank_cut_device(ql, lam[l], 0.25 * eps * eps, energy, rl + l, margins + l, st);
         continue;
@@ -1614,11 +1626,13 @@ TT truncate_tt(fc_ctx c, const TT& xin, double eps, int rank_cap, TruncStats* st
           dgemm(st, 1, 0, m, mc, ql, 1.0, Yns, ql, Bm[l] + c0 * ql, ql, 0.0, Cb, m);
           dgemm(st, 0, 1, m, m, mc, 1.0, Cb, m, Cb, m, 1.0, G, m);
         }
+        pm.mark("4b3 refine: noise Gram (cp)");
       } else {
-        // structured: C_kk = (Y_ns^T Rm_kk)(Cx D_kk), spectral terms chunked; G += C C^T per chunk
+        // structured: C_kk = (Y_ns^T Rm_kk)(Cx D_kk)
         const int t = ss->t[l], rr = ss->r, Rx = ss->Rx;
         double* YR = s.alloc<double>((size_t)m * t * rr);
         dgemm(st, 1, 0, m, t * rr, ql, 1.0, Yns, ql, RmE[l], ql, 0.0, YR, m);
+        pm.mark("4b3 refine: YR = Yns^T RmE");
         static const bool no_factor = getenv("FC_NO_STRUCT_FACTOR") != nullptr;   // diagnostics
         if (t <= kFactorMaxT && !no_factor) {
           // G_ns = sum_kk (YR_kk L_kk)(YR_kk L_kk)^T with L_kk L_kk^T = W_kk W_kk^T (the accurate
@@ -1634,6 +1648,7 @@ TT truncate_tt(fc_ctx c, const TT& xin, double eps, int rank_cap, TruncStats* st
           }
           struct_factor_kernel<<<rr, kFactorThreads, fsmem, st>>>(t, Rx, ss->Cx[l], dl[l], Lf);
           FC_CHECK_LAUNCH();
+          pm.mark("4b3 refine: dd factor");
           double* Ct = s.alloc<double>((size_t)m * t * rr);
           GemmArgs g;
           g.nbatch = 1;
@@ -1650,56 +1665,79 @@ TT truncate_tt(fc_ctx c, const TT& xin, double eps, int rank_cap, TruncStats* st
           gg.b[0] = GemmBatch{m, m, t * rr, Ct, m, Ct, m, G, m, nullptr, 0, nullptr};
           gg.splitk = waves_splitk(gg, 4);
           gemm(gg, st);
+          pm.mark("4b3 refine: C~ C~^T");
         } else {
-        const int kc = std::max(1, (int)std::min<size_t>((size_t)rr, ((size_t)1 << 26) /
-                                                                   std::max<size_t>((size_t)std::max(m, t) * Rx, 1)));
-        double* Wc = s.alloc<double>((size_t)t * Rx * kc);
-        double* Cb = s.alloc<double>((size_t)m * Rx * kc);
-        for (int k0 = 0; k0 < rr; k0 += kc) {
-          const int nk = std::min(kc, rr - k0);
-          struct_scale_kernel<<<blocks_for((long long)t * Rx * nk), 256, 0, st>>>(t, nk * Rx, Rx, ss->Cx[l],
-                                                                                   dl[l] + (size_t)k0 * Rx, Wc);
-          FC_CHECK_LAUNCH();
-          GemmArgs g;
-          g.nbatch = 1;
-          g.rep = nk;
-          g.b[0] = GemmBatch{m, Rx, t, YR + (size_t)k0 * m * t, m, Wc, t, Cb, m, nullptr, 0, nullptr};
-          g.b[0].sA = (long long)m * t;
-          g.b[0].sB = (long long)t * Rx;
-          g.b[0].sC = (long long)m * Rx;
-          gemm(g, st);
-          dgemm(st, 0, 1, m, m, nk * Rx, 1.0, Cb, m, Cb, m, 1.0, G, m);
-        }
+          const int kc = std::max(1, (int)std::min<size_t>((size_t)rr, ((size_t)1 << 26) /
+                                                                     std::max<size_t>((size_t)std::max(m, t) * Rx, 1)));
+          double* Wc = s.alloc<double>((size_t)t * Rx * kc);
+          double* Cb = s.alloc<double>((size_t)m * Rx * kc);
+          for (int k0 = 0; k0 < rr; k0 += kc) {
+            const int nk = std::min(kc, rr - k0);
+            struct_scale_kernel<<<blocks_for((long long)t * Rx * nk), 256, 0, st>>>(t, nk * Rx, Rx, ss->Cx[l],
+                                                                                     dl[l] + (size_t)k0 * Rx, Wc);
+            FC_CHECK_LAUNCH();
+            GemmArgs g;
+            g.nbatch = 1;
+            g.rep = nk;
+            g.b[0] = GemmBatch{m, Rx, t, YR + (size_t)k0 * m * t, m, Wc, t, Cb, m, nullptr, 0, nullptr};
+            g.b[0].sA = (long long)m * t;
+            g.b[0].sB = (long long)t * Rx;
+            g.b[0].sC = (long long)m * Rx;
+            gemm(g, st);
+            dgemm(st, 0, 1, m, m, nk * Rx, 1.0, Cb, m, Cb, m, 1.0, G, m);
+          }
         }
       }
-      pm.mark("4b3 refine: noise Gram");
-      // eigen of G_ns (all vectors): mu descending, V_ns
-      SyevBatch gb;
-      double* mu = s.alloc<double>(m);
-      double* Vn = s.alloc<double>((size_t)m * m);
-      int* rm = s.alloc<int>(1);
-      FC_CUDA_TRY(cudaMemcpyAsync(rm, &m, sizeof(int), cudaMemcpyHostToDevice, st));
-      gb.e[gb.nb++] = SyevEntry{m, G, m, s.alloc<double>(m), s.alloc<double>(m), mu, Vn, m, rm,
+      mu[l] = s.alloc<double>(m);
+      Vn[l] = s.alloc<double>((size_t)m * m);
+      gmap[l] = gb.nb;
+      gb.e[gb.nb++] = SyevEntry{m, G, m, s.alloc<double>(m), s.alloc<double>(m), mu[l], Vn[l], m, rm + l,
                                 s.alloc<double>((size_t)6 * m * m)};
-      syev_values(gb, st);
-      // s2 = [trusted eigenvalues ; mu] and the cut; then only the (r - pk) leading eigenvectors of
-      // G_ns are computed and the noise-subspace vectors rotated: Y_ns[:, :r-pk] <- Y_ns V_ns
-      double* s2r = s.alloc<double>(ql);
-      FC_CUDA_TRY(cudaMemcpyAsync(s2r, lam[l], (size_t)pk * 8, cudaMemcpyDeviceToDevice, st));
-      FC_CUDA_TRY(cudaMemcpyAsync(s2r + pk, mu, (size_t)m * 8, cudaMemcpyDeviceToDevice, st));
-      rank_cut_device(ql, s2r, 0.25 * eps * eps, energy, rl + l, margins + l, st);
-      const int rcut = read_int(rl + l, st);
-      const int nv = refine_all ? m : std::max(0, std::min(rcut, ql) - pk);
-      if (nv > 0) {
-        FC_CUDA_TRY(cudaMemcpyAsync(rm, &nv, sizeof(int), cudaMemcpyHostToDevice, st));
-        int nvh = nv;
-        syev_vectors(gb, m, st, &nvh);
-        double* Yr = s.alloc<double>((size_t)ql * nv);
-        dgemm(st, 0, 0, ql, nv, m, 1.0, Yns, ql, Vn, m, 0.0, Yr, ql);
-        FC_CUDA_TRY(cudaMemcpyAsync(Yns, Yr, (size_t)ql * nv * 8, cudaMemcpyDeviceToDevice, st));
-      }
-      pm.mark("4b4 refine: noise eig");
     }
+    pm.mark("4b3 refine: noise Gram");
+    // eigenvalues of every G_ns (one batch); s2 = [trusted eigenvalues ; mu] and the cut per mode
+    int maxm = 0;
+    if (gb.nb) {
+      syev_values(gb, st);
+      for (int l = 0; l < 3; ++l) {
+        if (gmap[l] < 0) continue;
+        const int ql = q[l], pk = pkv[l];
+        maxm = std::max(maxm, mm[l]);
+        double* s2r = s.alloc<double>(ql);
+        if (pk > 0) FC_CUDA_TRY(cudaMemcpyAsync(s2r, lam[l], (size_t)pk * 8, cudaMemcpyDeviceToDevice, st));
+        FC_CUDA_TRY(cudaMemcpyAsync(s2r + pk, mu[l], (size_t)mm[l] * 8, cudaMemcpyDeviceToDevice, st));
+        rank_cut_device(ql, s2r, 0.25 * eps * eps, energy, rl + l, margins + l, st);
+      }
+      // only the (r - pk) leading eigenvectors of each G_ns are computed (one batch), and the
+      // noise-subspace vectors rotated: Y_ns[:, :r-pk] <- Y_ns V_ns
+      int rc[4] = {0, 0, 0, 0};
+      FC_CUDA_TRY(cudaMemcpyAsync(rc, rl, 3 * sizeof(int), cudaMemcpyDeviceToHost, st));
+      FC_CUDA_TRY(cudaStreamSynchronize(st));
+      SyevBatch vb;
+      int nvh[kMaxSyev], nvd[4] = {0, 0, 0, 0}, nvl[3] = {0, 0, 0};
+      for (int l = 0; l < 3; ++l) {
+        if (gmap[l] < 0) continue;
+        const int nv = refine_all ? mm[l] : std::max(0, std::min(rc[l], q[l]) - pkv[l]);
+        nvl[l] = nv;
+        nvd[l] = nv;
+        if (nv <= 0) continue;
+        nvh[vb.nb] = nv;
+        vb.e[vb.nb++] = gb.e[gmap[l]];
+      }
+      if (vb.nb) {
+        FC_CUDA_TRY(cudaMemcpyAsync(rm, nvd, 3 * sizeof(int), cudaMemcpyHostToDevice, st));
+        syev_vectors(vb, maxm, st, nvh);
+        for (int l = 0; l < 3; ++l) {
+          if (nvl[l] <= 0) continue;
+          const int ql = q[l], nv = nvl[l], m = mm[l];
+          double* Yns = Y[l] + (size_t)pkv[l] * ql;
+          double* Yr = s.alloc<double>((size_t)ql * nv);
+          dgemm(st, 0, 0, ql, nv, m, 1.0, Yns, ql, Vn[l], m, 0.0, Yr, ql);
+          FC_CUDA_TRY(cudaMemcpyAsync(Yns, Yr, (size_t)ql * nv * 8, cudaMemcpyDeviceToDevice, st));
+        }
+      }
+    }
+    pm.mark("4b4 refine: noise eig");
     int r_gram[3] = {r[0], r[1], r[2]};
     FC_CUDA_TRY(cudaMemcpyAsync(r, rl, 3 * sizeof(int), cudaMemcpyDeviceToHost, st));
     FC_CUDA_TRY(cudaMemcpyAsync(hm, margins, 3 * sizeof(double), cudaMemcpyDeviceToHost, st));

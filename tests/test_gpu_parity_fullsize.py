@@ -44,12 +44,13 @@ def test_pcg_parity_fullsize(lib, name, n, kmax):
     assert d <= max(10 * p.eps, 1e-9)
 
 
-@pytest.mark.parametrize("name", ["C3a", "C3b"])
-def test_first_operator_steps_c3(lib, name):
+@pytest.mark.parametrize("name,with_s0", [("C3a", True), ("C3b", False)])
+def test_first_operator_steps_c3(lib, name, with_s0):
     """C3a/C3b at n = 512 (rough coefficients 1 + 0.9 sin, alpha = 0.25 / 0.75): Algorithm 1's
     lines 2-3 and 7-8 of the first iteration, Z0 = trunc(G B) and S0 = trunc(F Z0), against the
     oracle (the oracle's full PCG iteration at C3 takes > 10 min on the host cores: its
-    untruncated r x R products reach ~10^5 terms)."""
+    untruncated r x R products reach ~10^5 terms; C3b's S0 alone, a 3594-term input, takes the
+    oracle ~8 min, so C3b stops at Z0)."""
     from paper_2006_09314_b200.binding import DeviceCP, make_params, FC_F, FC_G
     p = make_problem(name, n=512)
     prm = make_params(p.alpha, p.beta, p.eps, p.tol_stop)
@@ -66,6 +67,8 @@ def test_first_operator_steps_c3(lib, name):
     if marg >= 5e-3:
         assert list(info.tucker_rank) == info_o["tucker_rank"] and z.rank == z_ref.rank
     assert d <= tol
+    if not with_s0:
+        return
     # S0 on the SAME input (the oracle's Z0) on both sides
     zo = DeviceCP.from_numpy(z_ref.w, z_ref.U)
     s_dev, info = ctx.fracop_apply_truncate(FC_F, zo, p.eps)
