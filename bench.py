@@ -313,7 +313,10 @@ def main():
     # same profiled solve, and cp_dot's Hadamard-of-Grams reduction at C4-iterate ranks
     kr = ctx.profile_kernel(1, False)
     roof_hbm = hbm_roofline(ctx, p.n, kr)
-    # the north-star's mode-transform kernel at a C5 cell (fused Khatri-Rao inverse transform)
+    # variant (not the headline): the same solve with the preconditioner CP at rank r_G = 24
+    # instead of the paper's 6 [P:990] (DESIGN.md §7 iteration counts): time-to-eps it reaches
+    variant = rg_variant(L, p, stream)
+    # the north-star's mode-transform kernel at a C5 cell (inverse transform + Khatri-Rao operand)
     roof_apply = apply_roofline(ctx, L, p.n)
     if rank != 0:
         return
@@ -339,6 +342,7 @@ def main():
         "roofline": roof,
         "roofline_apply": roof_apply,
         "roofline_hbm": roof_hbm,
+        "variant_rG24": variant,
         "clocks": clk.summary(),
     }
     if not args.no_cpu_baseline and world == 1:
@@ -353,6 +357,32 @@ def main():
                                 "first_iteration_matches_device": bool(same),
                                 "n64_own_setup": {"value": it64 / dt64, "unit": UNIT, "iters": it64, "seconds": dt64}}
     print(json.dumps(line), flush=True)
+
+
+def rg_variant(L, p, stream, rG=24, reps=3):
+    """C4 with params.precond_rank = rG (everything else as the headline): median device time of
+    `reps` solves after one warm-up, iterations, iters/s, final rel_res."""
+    import torch
+    from paper_2006_09314_b200.binding import DeviceCP, make_params
+    ctx = L.context(stream.cuda_stream)
+    prm = make_params(p.alpha, p.beta, p.eps, p.tol_stop, precond_rank=rG)
+    ctx.sl_setup(p.n, p.a_mid, prm)
+    b = DeviceCP.from_numpy(p.b_w, p.b_U)
+    u, rep, rc = ctx.pcg_solve(b, prm)
+    ts, its, rcs = [], [], []
+    for _ in range(reps):
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record(stream)
+        u, rep, rc = ctx.pcg_solve(b, prm, cap=u.cap, u=u)
+        s1.record(stream)
+        s1.synchronize()
+        ts.append(s0.elapsed_time(s1))
+        its.append(rep["iters"])
+        rcs.append(rc)
+    t = float(np.median(ts))
+    return {"precond_rank": rG, "time_to_eps_ms": t if all(r == 0 for r in rcs) else None, "iters": its[-1],
+            "iters_per_s": sum(its) / (sum(ts) * 1e-3), "rel_res": rep["rel_res"][-1], "rc": sorted(set(rcs)),
+            "note": "variant, not the headline: the paper fixes r_G = 6 [P:990]"}
 
 
 def hbm_peak():
@@ -406,24 +436,32 @@ def apply_roofline(ctx, L, n, R=64, r=16, reps=10):
     for _ in range(3):
         ctx.fracop_apply(FC_F, x, y)
     ms = []
+    ctx.profile_kernel(2, True)
     for _ in range(reps):
         ctx.fracop_apply(FC_F, x, y)
         ms.append(ctx.last_kernel_stats()["ms"])
+    kp = ctx.profile_kernel(2, False)
     st = ctx.last_kernel_stats()
     t = float(np.median(ms))
     ach = st["flops"] / (t * 1e-3) / 1e12
-    return {"kernel": "dgemm_dmma_kernel<KR> (fused Khatri-Rao inverse mode transform, S6+S7)",
+    peak_hbm, _ = hbm_peak()
+    kr_gbs = kp["bytes"] / (kp["ms"] * 1e-3) / 1e9 if kp["ms"] > 0 else 0.0
+    return {"kernel": "dgemm_big_kernel (inverse mode transform Y_l = V_l Yhat_l, S7; Yhat = u_F (.) V^T x by kr_product_kernel, K6)",
             "cell": {"n": n, "R": R, "r": r}, "bound": "tensor", "achieved": ach,
             "peak": FP64_DMMA_TFLOPS, "unit": "TFLOP/s", "frac": ach / FP64_DMMA_TFLOPS,
             "peak_source": "measured DMMA m8n8k4 FP64 peak (tools/peak_fp64.cu); MEASURED_PEAKS.json has no FP64 entry",
-            "traffic": kr_traffic(n, R, r), "ms": t}
+            "traffic": kr_traffic(n, R, r), "ms": t,
+            "kr_product": {"kernel": "kr_product_kernel (K6, Yhat = u_F (.) V^T x, 3 modes per launch)", "bound": "hbm",
+                           "achieved": kr_gbs, "peak": peak_hbm, "unit": "GB/s", "frac": kr_gbs / peak_hbm,
+                           "ms_per_launch": kp["ms"] / max(kp["launches"], 1),
+                           "bytes_per_launch": kp["bytes"] / max(kp["launches"], 1)}}
 
 
 def kr_traffic(n, R, r):
-    """DRAM bytes (read + write) of one fused KR inverse-transform launch at this C5 cell, from the
-    committed `ncu --set full` capture (profiles/r01h_kr_traffic.json), or None."""
+    """DRAM bytes (read + write) of one inverse-transform launch at this C5 cell, from the committed
+    `ncu --set full` capture of the current kernel (profiles/r02_inv_traffic.json), or None."""
     try:
-        d = json.load(open(os.path.join(ROOT, "profiles", "r01h_kr_traffic.json")))
+        d = json.load(open(os.path.join(ROOT, "profiles", "r02_inv_traffic.json")))
     except (OSError, ValueError):
         return None
     if (d.get("n"), d.get("R"), d.get("r")) != (n, R, r):

@@ -294,6 +294,7 @@ int fc_profile_gemm(fc_ctx ctx, int enable, double* ms, double* flops, long long
  * (ms), the summed algorithmic bytes and the launch count.  Errors: INVALID_ARG (kernel id). */
 #define FC_KP_DOT_REDUCE 0
 #define FC_KP_KR_BASIS   1
+#define FC_KP_KR_PRODUCT 2   /* fracop_apply's Khatri-Rao operand u_k (.) V^T x_j (K6), 8 B per entry */
 int fc_profile_kernel(fc_ctx ctx, int kernel, int enable, double* ms, double* bytes, long long* launches);
 /* Process-wide count of CUDA kernels this library has launched (host-side counter). */
 int fc_kernel_launches(long long* count);

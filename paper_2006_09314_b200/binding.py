@@ -16,7 +16,7 @@ LIB_PATH = os.path.join(HERE, "libfraccontrol.so")
 
 FC_F, FC_G, FC_POW_PLUS, FC_POW_MINUS = 0, 1, 2, 3
 FC_PRECOND_B, FC_PRECOND_A = 0, 1
-FC_KP_DOT_REDUCE, FC_KP_KR_BASIS = 0, 1
+FC_KP_DOT_REDUCE, FC_KP_KR_BASIS, FC_KP_KR_PRODUCT = 0, 1, 2
 FC_MAX_ITERS = 256
 STATUS = {0: "OK", 1: "NOT_CONVERGED", 2: "RANK_CAP_HIT", -1: "INVALID_ARG", -2: "SHAPE",
           -3: "CAPACITY", -4: "NONPOS_COEF", -5: "NOT_SPD", -6: "NAN", -7: "EIG_NOCONV",

@@ -86,23 +86,38 @@ void apply_plain(fc_ctx c, const SpecCP& sp, const fc_cp& x, fc_cp& y) {
   double* csp[3] = {cs, cs + (size_t)r * R, cs + (size_t)2 * r * R};
   apply_weights(r, R, sp.w.p, x.w, N2p, y.w, csp, st);
 
-  // S6+S7 inverse transform with the Khatri-Rao operand fused: Y_l = V_l [u_k (.) w_j]_t
+  // S6: the Khatri-Rao / Hadamard operand Yhat_l[:, k R + j] = u_k (.) w_j, written once (K6,
+  // HBM-write-bound, 3 modes in one launch), then S7: Y_l = V_l Yhat_l as a plain GEMM (B
+  // contiguous along K: 16-byte cp.async, no product in the MMA loop).  FC_KR_FUSED=1: the
+  // product formed at fragment-load time inside the GEMM instead (diagnostic; its per-fragment
+  // DMULs were 25 % of the kernel's stall samples, r02 ncu).
+  static const bool kr_fused = getenv("FC_KR_FUSED") != nullptr;
   GemmArgs iv;
   iv.nbatch = 3;
-  iv.krR = R;
+  double* Yhat = nullptr;
+  if (kr_fused) {
+    iv.krR = R;
+  } else {
+    Yhat = s.alloc<double>((size_t)3 * n * r * R);
+    const double* Uf[3] = {sp.Ul(n, 0), sp.Ul(n, 1), sp.Ul(n, 2)};
+    const double* Wh[3] = {What, What + (size_t)n * R, What + (size_t)2 * n * R};
+    double* Yh[3] = {Yhat, Yhat + (size_t)n * r * R, Yhat + (size_t)2 * n * r * R};
+    kr_product3(n, r, R, Uf, Wh, Yh, st);
+  }
   for (int l = 0; l < 3; ++l)
-    iv.b[l] = GemmBatch{n, r * R, n, c->Vsp(sp, l), n, What + (size_t)l * n * R, n, y.U[l], y.ld[l],
-                        sp.Ul(n, l), n, csp[l]};
-  // wave balance: with one 128x128 CTA per SM, split K until the grid covers >= 3 waves
+    iv.b[l] = kr_fused ? GemmBatch{n, r * R, n, c->Vsp(sp, l), n, What + (size_t)l * n * R, n, y.U[l], y.ld[l],
+                                   sp.Ul(n, l), n, csp[l]}
+                       : GemmBatch{n, r * R, n, c->Vsp(sp, l), n, Yhat + (size_t)l * n * r * R, n, y.U[l], y.ld[l],
+                                   nullptr, 0, csp[l]};
+  // wave balance (one 128x128 CTA per SM): no split-K once the tiles fill >= 2 waves of 148 SMs
+  // (the split reduction costs more than the last wave's fill: r02 sweep, sk = 1 best at 384+
+  // tiles), else the smallest power of two reaching 2 waves (>= 128 of K per split, <= 8)
   const long long tiles = 3LL * cdiv(n, 128) * cdiv((long long)r * R, 128);
   int sk = 1;
-  while (tiles * sk < 3LL * 148 && n / (sk * 2) >= 256 && sk < 4) sk *= 2;
-  if (sk > 1) {
-    iv.splitk = sk;
-    iv.beta = 1.0;
-    for (int l = 0; l < 3; ++l)
-      FC_CUDA_TRY(cudaMemset2DAsync(y.U[l], (size_t)y.ld[l] * 8, 0, (size_t)n * 8, (size_t)r * R, st));
-  }
+  while (tiles * sk < 2LL * 148 && sk < 8 && n / (2 * sk) >= 128) sk *= 2;
+  static const int sk_env = getenv("FC_APPLY_SPLITK") ? atoi(getenv("FC_APPLY_SPLITK")) : 0;   // diagnostic
+  if (sk_env > 0) sk = sk_env;
+  iv.splitk = sk;   // deterministic split-K reduction: C needs no pre-zeroing (beta = 0)
   FC_CUDA_TRY(cudaEventRecord(c->e0, st));
   gemm(iv, st);
   FC_CUDA_TRY(cudaEventRecord(c->e1, st));

@@ -155,7 +155,7 @@ void gemm(const GemmArgs& a, cudaStream_t st);
 void gemm_profile(bool enable, double* ms, double* flops, long long* launches);
 // fc_profile_kernel: opt-in accounting of the HBM-class kernels (events around each launch on
 // its stream, algorithmic bytes per launch), one record per kernel id
-enum KProfId { KP_DOT_REDUCE = 0, KP_KR_BASIS = 1, KP_COUNT = 2 };
+enum KProfId { KP_DOT_REDUCE = 0, KP_KR_BASIS = 1, KP_KR_PRODUCT = 2, KP_COUNT = 3 };
 struct KProfScope {
   int id;
   cudaStream_t st;

@@ -87,6 +87,38 @@ __global__ void dot_reduce_kernel(int R1, int R2, const double* __restrict__ wx,
   }
 }
 
+// K6 (S6) [P:604-605, P:1756-1763]: Y_l[:, k R + j] = U_l[:, k] (.) W_l[:, j] (n x r R per
+// mode, blockIdx.y = mode), 16-byte loads / streaming stores along n when n is even and the
+// blocks are 16-byte aligned; HBM-write-bound (U and W are re-read from L2)
+__global__ void kr_product_kernel(int n, int r, int R, Cmat3 U, Cmat3 W, Mat3 Y) {
+  const int l = blockIdx.y;
+  const double* __restrict__ u = U.p[l];
+  const double* __restrict__ w = W.p[l];
+  double* y = Y.p[l];
+  const long long cols = (long long)r * R;
+  const size_t al = reinterpret_cast<size_t>(u) | reinterpret_cast<size_t>(w) | reinterpret_cast<size_t>(y);
+  if ((n & 1) == 0 && (al & 15) == 0) {
+    const int n2 = n >> 1;
+    const long long tot = (long long)n2 * cols;
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < tot;
+         idx += (long long)gridDim.x * blockDim.x) {
+      const long long c = idx / n2;
+      const int i2 = (int)(idx - c * n2), k = (int)(c / R), j = (int)(c - (long long)k * R);
+      const double2 a = __ldg(reinterpret_cast<const double2*>(u + (size_t)k * n) + i2);
+      const double2 b = __ldg(reinterpret_cast<const double2*>(w + (size_t)j * n) + i2);
+      __stcs(reinterpret_cast<double2*>(y + (size_t)c * n) + i2, make_double2(a.x * b.x, a.y * b.y));
+    }
+    return;
+  }
+  const long long tot = (long long)n * cols;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < tot;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const long long c = idx / n;
+    const int i = (int)(idx - c * n), k = (int)(c / R), j = (int)(c - (long long)k * R);
+    y[idx] = u[i + (size_t)k * n] * w[i + (size_t)j * n];
+  }
+}
+
 __global__ void sum_kernel(int n, const double* __restrict__ x, double* out) {
   __shared__ double red[32];
   double acc = 0.0;
@@ -139,6 +171,23 @@ void apply_weights(int r, int R, const double* wF, const double* wx, const doubl
   if (total == 0) return;
   apply_weights_kernel<<<cdiv(total, 256), 256, 0, st>>>(r, R, wF, wx, N2[0], N2[1], N2[2], wout, cs[0], cs[1],
                                                          cs[2]);
+  FC_CHECK_LAUNCH();
+}
+
+void kr_product3(int n, int r, int R, const double* const U[3], const double* const W[3], double* const Y[3],
+                 cudaStream_t st) {
+  const long long tot = (long long)n * r * R;
+  if (tot == 0) return;
+  Cmat3 u{}, w{};
+  Mat3 y{};
+  for (int l = 0; l < 3; ++l) {
+    u.p[l] = U[l];
+    w.p[l] = W[l];
+    y.p[l] = Y[l];
+  }
+  const int gx = (int)std::max<long long>(1, std::min<long long>((tot / 2 + 255) / 256, 148 * 8 / 3 + 1));
+  KProfScope kp(KP_KR_PRODUCT, st, 3.0 * 8.0 * ((double)tot + (double)n * (r + R)));
+  kr_product_kernel<<<dim3(gx, 3), 256, 0, st>>>(n, r, R, u, w, y);
   FC_CHECK_LAUNCH();
 }
 

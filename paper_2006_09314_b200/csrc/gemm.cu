@@ -508,7 +508,7 @@ __global__ void __launch_bounds__(NT, 1) dgemm_big_kernel(const __grid_constant_
           const int o = nn * LDM + k;
           bf[j] = b_s[o] * k_s[o];
         } else {
-          bf[j] = (BKc || KR) ? b_s[nn * LDM + k] : b_s[k * LDK + nn];
+          bf[j] = BKc ? b_s[nn * LDM + k] : b_s[k * LDK + nn];
         }
       }
 #pragma unroll

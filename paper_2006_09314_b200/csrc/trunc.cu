@@ -87,10 +87,11 @@ __global__ void struct_scale_kernel(int t, int R, int Rx, const double* __restri
 // diagonally pivoted Cholesky in double-double, and only the factor is rounded to double.  A
 // rounding of L (or of Rm, or of a later product with B~) perturbs v^T B B^T v by
 // ~2 ||B^T v|| eps_mach ||B|| — linear in the small singular values, not eps_mach ||B||^2.
-constexpr int kFactorMaxT = 96;        // t (x's Tucker rank) handled by the factor kernel
+constexpr int kFactorMaxT = 512;       // t (x's Tucker rank) handled by the factor kernel
+constexpr int kFactorSmemT = 96;       // up to this t the dd Gram lives in shared memory
 constexpr int kFactorThreads = 512;
 constexpr int kFactorJC = 32;          // W columns staged per chunk
-constexpr int kFactorEnt = (kFactorMaxT * (kFactorMaxT + 1) / 2 + kFactorThreads - 1) / kFactorThreads;
+constexpr int kFactorEnt = 10;         // Gram entries per thread and pass over W
 
 struct dd { double hi, lo; };
 __device__ __forceinline__ dd dd_fast2sum(double a, double b) {
@@ -120,66 +121,72 @@ __device__ __forceinline__ dd dd_sqrt(dd a) {
 }
 
 // one CTA per spectral term k: L_k (t x t, column-major, ld t; columns beyond the numerical rank
-// are zero) with L_k L_k^T = W_k W_k^T, W_k[a, j] = Cx[a + j t] d[k Rx + j]
+// are zero) with L_k L_k^T = W_k W_k^T, W_k[a, j] = Cx[a + j t] d[k Rx + j].  The dd Gram (hi, lo)
+// is in shared memory for t <= kFactorSmemT, else in this CTA's slice of Hg (2 t^2 doubles per
+// CTA, L2-resident); Gram entries are accumulated kFactorEnt per thread per pass over W.
 __global__ void __launch_bounds__(kFactorThreads) struct_factor_kernel(int t, int Rx, const double* __restrict__ Cx,
-                                                                       const double* __restrict__ d, double* Lout) {
+                                                                       const double* __restrict__ d, double* Lout,
+                                                                       double* Hg) {
   extern __shared__ double fsm[];
   const int k = blockIdx.x, tid = threadIdx.x;
   const int ne = t * (t + 1) / 2;
+  const bool gl = t > kFactorSmemT;
   double* Wc = fsm;                                  // t x kFactorJC chunk of W_k
-  double* Hh = fsm + (size_t)t * kFactorJC;          // t x t (hi), later the Schur complement
-  double* Hl = Hh + (size_t)t * t;                   // t x t (lo)
-  double* Lc = Hl + (size_t)t * t;                   // current column (hi, lo): 2 t
+  double* Lc = fsm + (size_t)t * kFactorJC;          // current column (hi, lo): 2 t
   double* piv = Lc + 2 * t;                          // used flags: t
-  // entry e -> (a, b), a >= b, row-major over the lower triangle
-  int ea[kFactorEnt], eb[kFactorEnt];
-  dd acc[kFactorEnt];
-#pragma unroll
-  for (int q = 0; q < kFactorEnt; ++q) {
-    const int e = tid + q * kFactorThreads;
-    int a = 0, b = 0;
-    if (e < ne) {
-      a = (int)((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
-      while ((a + 1) * (a + 2) / 2 <= e) ++a;
-      while (a * (a + 1) / 2 > e) --a;
-      b = e - a * (a + 1) / 2;
-    }
-    ea[q] = a;
-    eb[q] = b;
-    acc[q] = {0.0, 0.0};
-  }
+  double* Hh = gl ? Hg + (size_t)k * 2 * t * t : piv + t;   // t x t (hi), later the Schur complement
+  double* Hl = Hh + (size_t)t * t;                   // t x t (lo)
   const double* dk = d + (size_t)k * Rx;
-  for (int j0 = 0; j0 < Rx; j0 += kFactorJC) {
-    const int jc = min(kFactorJC, Rx - j0);
-    __syncthreads();
-    for (int idx = tid; idx < t * jc; idx += kFactorThreads) {
-      const int a = idx % t, jj = idx / t;
-      Wc[a + jj * t] = Cx[a + (size_t)(j0 + jj) * t] * dk[j0 + jj];
-    }
-    __syncthreads();
+  for (int e0 = 0; e0 < ne; e0 += kFactorEnt * kFactorThreads) {
+    // entry e -> (a, b), a >= b, row-major over the lower triangle
+    int ea[kFactorEnt], eb[kFactorEnt];
+    dd acc[kFactorEnt];
 #pragma unroll
     for (int q = 0; q < kFactorEnt; ++q) {
-      if (tid + q * kFactorThreads >= ne) break;
-      const int a = ea[q], b = eb[q];
-      double hi = acc[q].hi, lo = acc[q].lo;
-      for (int jj = 0; jj < jc; ++jj) {
-        const double x = Wc[a + jj * t], y = Wc[b + jj * t];
-        const double p = x * y, pe = fma(x, y, -p);
-        const double s = hi + p, bb = s - hi;
-        lo += ((hi - (s - bb)) + (p - bb)) + pe;
-        hi = s;
+      const int e = e0 + tid + q * kFactorThreads;
+      int a = 0, b = 0;
+      if (e < ne) {
+        a = (int)((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
+        while ((a + 1) * (a + 2) / 2 <= e) ++a;
+        while (a * (a + 1) / 2 > e) --a;
+        b = e - a * (a + 1) / 2;
       }
-      acc[q] = dd_fast2sum(hi, lo);
+      ea[q] = a;
+      eb[q] = b;
+      acc[q] = {0.0, 0.0};
+    }
+    for (int j0 = 0; j0 < Rx; j0 += kFactorJC) {
+      const int jc = min(kFactorJC, Rx - j0);
+      __syncthreads();
+      for (int idx = tid; idx < t * jc; idx += kFactorThreads) {
+        const int a = idx % t, jj = idx / t;
+        Wc[a + jj * t] = Cx[a + (size_t)(j0 + jj) * t] * dk[j0 + jj];
+      }
+      __syncthreads();
+#pragma unroll
+      for (int q = 0; q < kFactorEnt; ++q) {
+        if (e0 + tid + q * kFactorThreads >= ne) break;
+        const int a = ea[q], b = eb[q];
+        double hi = acc[q].hi, lo = acc[q].lo;
+        for (int jj = 0; jj < jc; ++jj) {
+          const double x = Wc[a + jj * t], y = Wc[b + jj * t];
+          const double p = x * y, pe = fma(x, y, -p);
+          const double s = hi + p, bb = s - hi;
+          lo += ((hi - (s - bb)) + (p - bb)) + pe;
+          hi = s;
+        }
+        acc[q] = dd_fast2sum(hi, lo);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < kFactorEnt; ++q) {
+      if (e0 + tid + q * kFactorThreads >= ne) break;
+      const int a = ea[q], b = eb[q];
+      Hh[a + b * t] = Hh[b + a * t] = acc[q].hi;
+      Hl[a + b * t] = Hl[b + a * t] = acc[q].lo;
     }
   }
   __syncthreads();
-#pragma unroll
-  for (int q = 0; q < kFactorEnt; ++q) {
-    if (tid + q * kFactorThreads >= ne) break;
-    const int a = ea[q], b = eb[q];
-    Hh[a + b * t] = Hh[b + a * t] = acc[q].hi;
-    Hl[a + b * t] = Hl[b + a * t] = acc[q].lo;
-  }
   for (int i = tid; i < t; i += kFactorThreads) piv[i] = 0.0;
   double* L = Lout + (size_t)k * t * t;
   for (int i = tid; i < t * t; i += kFactorThreads) L[i] = 0.0;
@@ -1638,15 +1645,18 @@ TT truncate_tt(fc_ctx c, const TT& xin, double eps, int rank_cap, TruncStats* st
           // G_ns = sum_kk (YR_kk L_kk)(YR_kk L_kk)^T with L_kk L_kk^T = W_kk W_kk^T (the accurate
           // factor above): an m x (t r) product instead of m x (Rx r) (Rx = x's CP rank)
           double* Lf = s.alloc<double>((size_t)t * t * rr);
-          const size_t fsmem = ((size_t)t * kFactorJC + 2 * (size_t)t * t + 3 * (size_t)t) * 8;
+          const bool fgl = t > kFactorSmemT;
+          double* Hg = fgl ? s.alloc<double>((size_t)2 * t * t * rr) : nullptr;
+          const size_t fsmem = ((size_t)t * kFactorJC + 3 * (size_t)t + (fgl ? 0 : 2 * (size_t)t * t)) * 8;
           static bool fattr = false;
           if (!fattr) {
-            FC_CUDA_TRY(cudaFuncSetAttribute(struct_factor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)(((size_t)kFactorMaxT * kFactorJC + 2 * (size_t)kFactorMaxT * kFactorMaxT +
-                                                    3 * (size_t)kFactorMaxT) * 8)));
+            const size_t fmax = std::max(((size_t)kFactorMaxT * kFactorJC + 3 * (size_t)kFactorMaxT) * 8,
+                                         ((size_t)kFactorSmemT * kFactorJC + 3 * (size_t)kFactorSmemT +
+                                          2 * (size_t)kFactorSmemT * kFactorSmemT) * 8);
+            FC_CUDA_TRY(cudaFuncSetAttribute(struct_factor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fmax));
             fattr = true;
           }
-          struct_factor_kernel<<<rr, kFactorThreads, fsmem, st>>>(t, Rx, ss->Cx[l], dl[l], Lf);
+          struct_factor_kernel<<<rr, kFactorThreads, fsmem, st>>>(t, Rx, ss->Cx[l], dl[l], Lf, Hg);
           FC_CHECK_LAUNCH();
           pm.mark("4b3 refine: dd factor");
           double* Ct = s.alloc<double>((size_t)m * t * rr);
