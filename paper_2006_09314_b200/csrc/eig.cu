@@ -615,6 +615,19 @@ __host__ __device__ inline size_t cluster_smem_doubles(int N) {
   const int SL = (N + CS - 1) / CS;
   return P + 4 * (size_t)N + (size_t)CS * SL + 2 * (size_t)SL;
 }
+// GL hybrid: the number of leading own columns that fit shared memory (220 KB) next to the
+// vectors (CTA 0's packed sizes, the largest), and the resulting dynamic shared memory
+inline int cluster_gl_tsm(int N, size_t* smem_bytes) {
+  constexpr int CS = 16;
+  const size_t vec = cluster_smem_doubles<CS, true>(N);
+  const size_t cap = 220 * 1024 / 8;
+  const int SL = (N + CS - 1) / CS;
+  int t = 0;
+  auto loff0 = [N](int tt) { return (size_t)tt * N - (size_t)CS * tt * (tt - 1) / 2; };
+  while (t < SL && vec + loff0(t + 1) <= cap) ++t;
+  *smem_bytes = (vec + loff0(t)) * 8;
+  return t;
+}
 constexpr int kClGlobalMaxN = 2048;   // GL cluster path (own columns in L2) up to this size
 
 // a - 2 (ui qj + qi uj) with explicit roundings (identical wherever it is evaluated)
@@ -626,9 +639,11 @@ __device__ __forceinline__ double rank2(double a, double ui, double qi, double u
 // private slice of E.scratch (L2-resident: the whole triangle is <= 16 MB at N = 2048) and the
 // next pivot column is fetched from the owner's slice with L1-bypassing loads (ld.global.cg:
 // the owner updates it between fetches); the vectors stay in shared memory (DSMEM as above).
+//   Hybrid: the first `tsm` own columns stay in shared memory (as many as fit next to the vectors,
+//   DSMEM pivot fetches), the rest in the L2 slice; tsm >= ncol is the all-shared-memory layout.
 template <int CS, bool GL>
 __global__ void __launch_bounds__(1024, 1) tridiag_cluster_kernel(const __grid_constant__ SyevBatch B, int nlo,
-                                                                  int nhi) {
+                                                                  int nhi, int tsm_arg) {
   namespace cg = cooperative_groups;
   extern __shared__ double sm[];
   __shared__ double red[33];
@@ -644,8 +659,13 @@ __global__ void __launch_bounds__(1024, 1) tridiag_cluster_kernel(const __grid_c
   // the same layout in every CTA (CTA 0 owns the most entries): map_shared_rank(ptr, r) maps
   // to the same offset in CTA r
   const size_t P = loff_of(0, SL);
-  double* L = GL ? E.scratch + (size_t)c * P : sm;
-  double* u = GL ? sm : L + P;   // Householder vector of the current step (absolute row index)
+  const int tsm = GL ? tsm_arg : SL;                     // own columns t < tsm in shared memory
+  const size_t Psm = loff_of(0, min(tsm, SL));           // their (largest, CTA 0) packed size
+  double* L = sm;                                        // shared-memory part (columns t < tsm)
+  // L2 part (columns t >= tsm): column t at Lg + loff_of(c, t) (offsets below loff_of(c, tsm) unused)
+  double* Lg = GL ? E.scratch + (size_t)c * P - loff_of(c, min(tsm, ncol)) : nullptr;
+  auto colp = [&](int t) -> double* { return (GL && t >= tsm ? Lg : L) + loff_of(c, t); };
+  double* u = sm + Psm;       // Householder vector of the current step (absolute row index)
   double* u1 = u + N;         // ... of the next step
   double* col = u1 + N;       // current pivot column (absolute row index)
   double* Y = col + N;        // partial matvec (read remotely)
@@ -655,7 +675,7 @@ __global__ void __launch_bounds__(1024, 1) tridiag_cluster_kernel(const __grid_c
 
   for (int t = warp; t < ncol; t += NW) {
     const int j = c + t * CS;
-    double* dst = L + loff_of(c, t);
+    double* dst = colp(t);
     for (int i = j + ln; i < N; i += 32) dst[i - j] = E.A[i + (size_t)j * E.lda];
   }
   for (int i = tid; i < N; i += nt) col[i] = E.A[i];
@@ -689,8 +709,8 @@ __global__ void __launch_bounds__(1024, 1) tridiag_cluster_kernel(const __grid_c
       double acc = 0.0;
       int t = max(0, (lo - c + CS - 1) / CS);
       size_t off = loff_of(c, t);
-      for (int j = c + t * CS; j <= i; j += CS) {
-        double* a = L + off + (i - j);
+      for (int j = c + t * CS; j <= i; j += CS, ++t) {
+        double* a = (GL && t >= tsm ? Lg : L) + off + (i - j);
         double v = *a;
         if (upd && j >= jupd) {
           v = rank2(v, ui, qi, u[j], q[j]);
@@ -704,7 +724,7 @@ __global__ void __launch_bounds__(1024, 1) tridiag_cluster_kernel(const __grid_c
     __syncthreads();
     for (int t = max(0, (jsym - c + CS - 1) / CS) + warp; t < ncol; t += NW) {
       const int j = c + t * CS;
-      const double* a = L + loff_of(c, t);
+      const double* a = colp(t);
       double dot = 0.0;
       for (int i = j + 1 + ln; i < N; i += 32) dot = fma(a[i - j], w[i], dot);
       for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
@@ -729,8 +749,9 @@ __global__ void __launch_bounds__(1024, 1) tridiag_cluster_kernel(const __grid_c
     }
     {
       const int jn = s + 1, o = jn % CS, tn = jn / CS;
-      if (GL) {
-        const double* Lo = E.scratch + (size_t)o * P + loff_of(o, tn);
+      if (GL && tn >= tsm) {
+        const int ncol_o = (N - o + CS - 1) / CS;
+        const double* Lo = E.scratch + (size_t)o * P - loff_of(o, min(tsm, ncol_o)) + loff_of(o, tn);
         for (int i = i0 + tid; i < i1; i += nt) ncs[i - c * SL] = __ldcg(Lo + (i - jn));
       } else {
         const double* Lo = cl.map_shared_rank(L, o) + loff_of(o, tn);
@@ -782,7 +803,7 @@ __global__ void __launch_bounds__(1024, 1) tridiag_cluster_kernel(const __grid_c
     u = u1;
     u1 = tmp;
   }
-  if (tid == 0 && (N - 1) % CS == c) E.d[N - 1] = L[loff_of(c, (N - 1) / CS)];
+  if (tid == 0 && (N - 1) % CS == c) E.d[N - 1] = *colp((N - 1) / CS);
   cl.sync();                                                             // smem stays alive for readers
 }
 
@@ -2025,7 +2046,7 @@ void sl_eigen_device(cudaStream_t st, int n, const double* a_mid_dev, int bounda
 }
 
 template <int CS, bool GL = false>
-void launch_tridiag_cluster(const SyevBatch& b, size_t smem, cudaStream_t st, int nlo, int nhi) {
+void launch_tridiag_cluster(const SyevBatch& b, size_t smem, cudaStream_t st, int nlo, int nhi, int tsm = 0) {
   auto kern = tridiag_cluster_kernel<CS, GL>;
   static bool attr = false;
   if (!attr) {
@@ -2048,7 +2069,7 @@ void launch_tridiag_cluster(const SyevBatch& b, size_t smem, cudaStream_t st, in
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  FC_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, b, nlo, nhi));
+  FC_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, b, nlo, nhi, tsm));
   FC_CHECK_LAUNCH();
 }
 
@@ -2058,7 +2079,8 @@ void syev_values(const SyevBatch& b, cudaStream_t st) {
   const int minG = no_cluster ? kPackedMaxN : kCl16MaxN;   // sizes above go to the global kernel
   const int maxP = no_cluster ? kPackedMaxN : kClusterMinN; // sizes up to this: packed single CTA
   int maxN = 0;
-  size_t smem_g = 0, smem_p = 0, smem_4 = 0, smem_8 = 0, smem_16 = 0, smem_gl = 0;
+  size_t smem_g = 0, smem_p = 0, smem_4 = 0, smem_8 = 0, smem_16 = 0;
+  int gl_n = 0;
   static const bool no_gl = getenv("FC_NO_CLUSTER_GL") != nullptr;   // diagnostics: single-CTA kernel
   const int maxGL = (no_cluster || no_gl) ? minG : kClGlobalMaxN;
   bool any_g = false, any_p = false;
@@ -2080,7 +2102,7 @@ void syev_values(const SyevBatch& b, cudaStream_t st) {
       any_g = true;
       smem_g = std::max(smem_g, (size_t)(2 + NW) * N * 8);
     } else if (N > minG) {
-      smem_gl = std::max(smem_gl, cluster_smem_doubles<16, true>(N) * 8);
+      gl_n = std::max(gl_n, N);
     } else if (N <= cl4) {
       smem_4 = std::max(smem_4, cluster_smem_doubles<4>(N) * 8);
     } else if (N <= cl8) {
@@ -2092,7 +2114,18 @@ void syev_values(const SyevBatch& b, cudaStream_t st) {
   if (smem_4) launch_tridiag_cluster<4>(b, smem_4, st, maxP, cl4);
   if (smem_8) launch_tridiag_cluster<8>(b, smem_8, st, cl4, cl8);
   if (smem_16) launch_tridiag_cluster<16>(b, smem_16, st, cl8, kCl16MaxN);
-  if (smem_gl) launch_tridiag_cluster<16, true>(b, smem_gl, st, minG, maxGL);
+  if (gl_n) {
+    // one shared-memory head size for the launch, from its largest entry (smaller entries have
+    // shorter columns: the same head fits)
+    static const bool gl_all_l2 = getenv("FC_GL_NO_SMEM_HEAD") != nullptr;   // diagnostic
+    size_t smem_gl = 0;
+    int tsm = cluster_gl_tsm(gl_n, &smem_gl);
+    if (gl_all_l2) {
+      tsm = 0;
+      smem_gl = cluster_smem_doubles<16, true>(gl_n) * 8;
+    }
+    launch_tridiag_cluster<16, true>(b, smem_gl, st, minG, maxGL, tsm);
+  }
   if (maxN == 0) return;
   require(smem_g <= kTriSmemMax, FC_ERR_CAPACITY, "symmetric eigensolver: matrix dimension above 1500");
   static bool attr = false;

@@ -168,3 +168,34 @@ def test_cp_dot_parity(lib, n, R1, R2):
     zw, zU = z.to_numpy()
     ref = cpm.axpy(x, -0.3, y)
     assert np.array_equal(zw, ref.w) and all(np.array_equal(zU[l], ref.U[l]) for l in range(3))
+
+
+@pytest.mark.parametrize("n,R,r", [(256, 16, 8), (256, 8, 4)])
+def test_c5_truncation_parity(lib, n, R, r):
+    """BASELINE.json configs[4]: the truncation of the r R product back to eps = 1e-6
+    (fracop_apply_truncate, reading A22's cells where the Tucker core stays small) against the
+    oracle's trunc(apply(x)): C5 recipe (N(0,1) normalised factors, seed 5; random rank-r spectral
+    CP), C1 coefficients' eigenpairs shared.  Ranks equal, result within the derived bar."""
+    from paper_2006_09314_b200.binding import DeviceCP, FC_F
+    from oracle.measure import reldiff
+    from oracle.truncate import truncate
+    import sys, os
+    sys.path.insert(0, os.path.dirname(__file__))
+    from _parity import trunc_tolerance
+    p = make_problem("C1", n=n)
+    ctx = lib.context()
+    lams, V, F, G = _shared_setup(ctx, p, r_fixed=r)
+    w, U = random_cp(n, R, 5)
+    x = cpm.CP(w, U)
+    eps = 1e-6
+    info_o = {}
+    ref = truncate(cpm.apply(V, F, x), eps, info_o)
+    y, info = ctx.fracop_apply_truncate(FC_F, DeviceCP.from_numpy(w, U), eps)
+    tol, marg = trunc_tolerance(info_o, eps)
+    wy, Uy = y.to_numpy()
+    d = reldiff(cpm.CP(wy, Uy), ref)
+    print(f"C5 n={n} R={R} r={r}: tucker {list(info.tucker_rank)}/{info_o['tucker_rank']} rank {y.rank}/{ref.rank} "
+          f"reldiff {d:.2e} (tol {tol:g}, margin {marg:.2e})")
+    if marg >= 5e-3:
+        assert list(info.tucker_rank) == info_o["tucker_rank"] and y.rank == ref.rank
+    assert d <= tol
