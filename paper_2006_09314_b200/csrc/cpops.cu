@@ -95,18 +95,23 @@ __global__ void kr_product_kernel(int n, int r, int R, Cmat3 U, Cmat3 W, Mat3 Y)
   const double* __restrict__ u = U.p[l];
   const double* __restrict__ w = W.p[l];
   double* y = Y.p[l];
-  const long long cols = (long long)r * R;
+  const int cols = r * R;
   const size_t al = reinterpret_cast<size_t>(u) | reinterpret_cast<size_t>(w) | reinterpret_cast<size_t>(y);
   if ((n & 1) == 0 && (al & 15) == 0) {
-    const int n2 = n >> 1;
-    const long long tot = (long long)n2 * cols;
-    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < tot;
-         idx += (long long)gridDim.x * blockDim.x) {
-      const long long c = idx / n2;
-      const int i2 = (int)(idx - c * n2), k = (int)(c / R), j = (int)(c - (long long)k * R);
-      const double2 a = __ldg(reinterpret_cast<const double2*>(u + (size_t)k * n) + i2);
-      const double2 b = __ldg(reinterpret_cast<const double2*>(w + (size_t)j * n) + i2);
-      __stcs(reinterpret_cast<double2*>(y + (size_t)c * n) + i2, make_double2(a.x * b.x, a.y * b.y));
+    // a warp per output column at a time: column index math once per column, 16-byte
+    // coalesced loads of u_k, w_j (L2) and streaming stores of y_c along n
+    const int n2 = n >> 1, lane = threadIdx.x & 31;
+    const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+    for (int c = wid; c < cols; c += nw) {
+      const int k = c / R, j = c - k * R;
+      const double2* a = reinterpret_cast<const double2*>(u + (size_t)k * n);
+      const double2* b = reinterpret_cast<const double2*>(w + (size_t)j * n);
+      double2* o = reinterpret_cast<double2*>(y + (size_t)c * n);
+#pragma unroll 4
+      for (int i2 = lane; i2 < n2; i2 += 32) {
+        const double2 x = __ldg(a + i2), z = __ldg(b + i2);
+        __stcs(o + i2, make_double2(x.x * z.x, x.y * z.y));
+      }
     }
     return;
   }
@@ -185,7 +190,9 @@ void kr_product3(int n, int r, int R, const double* const U[3], const double* co
     w.p[l] = W[l];
     y.p[l] = Y[l];
   }
-  const int gx = (int)std::max<long long>(1, std::min<long long>((tot / 2 + 255) / 256, 148 * 8 / 3 + 1));
+  // a warp per column, 8 warps per CTA; ~8 resident CTAs per SM over the 3 modes
+  const long long cols = (long long)r * R;
+  const int gx = (int)std::max<long long>(1, std::min<long long>((cols + 7) / 8, 148 * 8 / 3 + 1));
   KProfScope kp(KP_KR_PRODUCT, st, 3.0 * 8.0 * ((double)tot + (double)n * (r + R)));
   kr_product_kernel<<<dim3(gx, 3), 256, 0, st>>>(n, r, R, u, w, y);
   FC_CHECK_LAUNCH();

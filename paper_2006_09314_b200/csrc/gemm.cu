@@ -47,8 +47,32 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
                : "d"(a), "d"(b));
 }
 
+__device__ __forceinline__ void cp_async16s(double* smem, const double* gmem, int bytes) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(bytes));
+}
+
+// a BK x 64 tile contiguous along its 64-wide dimension (A not transposed, B transposed), k-major
+// in shared memory: 16-byte chunks (pairs along the contiguous dimension; ragged edges
+// zero-filled by the transfer size)
+__device__ __forceinline__ void load_tile_vec(double* T, const double* base, int ld, int r0, int rmax, int k0,
+                                              int kend, int tid) {
+#pragma unroll
+  for (int i = 0; i < (BK * BM) / (2 * NT); ++i) {
+    const int c = tid + i * NT;
+    const int rr = (c % (BM / 2)) * 2, kk = c / (BM / 2);
+    const int r = r0 + rr, k = k0 + kk;
+    const int nr = (k < kend) ? max(0, min(2, rmax - r)) : 0;
+    cp_async16s(T + kk * LDS + rr, nr > 0 ? base + (size_t)r + (size_t)k * ld : base, nr * 8);
+  }
+}
+
 __device__ __forceinline__ void load_tile_A(double* As, const GemmBatch& g, const double* gA, int transA, int m0,
-                                            int k0, int kend, int tid) {
+                                            int k0, int kend, int tid, bool vec = false) {
+  if (!transA && vec) {
+    load_tile_vec(As, gA, g.lda, m0, g.M, k0, kend, tid);
+    return;
+  }
 #pragma unroll
   for (int i = 0; i < (BK * BM) / NT; ++i) {
     int idx = tid + i * NT;
@@ -91,7 +115,11 @@ __device__ __forceinline__ void gen_tile_A(double* As, const GemmBatch& g, const
 
 __device__ __forceinline__ void load_tile_B(double* Bs, double* Ks, const GemmBatch& g, const double* gB,
                                             const double* gK, int transB, int krR, int n0, int k0, int kend,
-                                            int tid) {
+                                            int tid, bool vec = false) {
+  if (krR == 0 && transB && vec) {
+    load_tile_vec(Bs, gB, g.ldb, n0, g.N, k0, kend, tid);
+    return;
+  }
   if (krR > 0) {
     // Khatri-Rao operand: column c = k_F * R + j  ->  u_F[:, k_F] (.) W[:, j].  Both factors are
     // gathered by cp.async into two tiles; the product is formed at fragment-load time.
@@ -238,6 +266,9 @@ __global__ void __launch_bounds__(NT) dgemm_dmma_kernel(const __grid_constant__ 
   const int kbeg = ks * kchunk;
   const int kend = min(Keff, kbeg + kchunk);
   const int nk = kend > kbeg ? (kend - kbeg + BK - 1) / BK : 0;   // an empty split adds zeros
+  // 16-byte staging needs an even leading dimension and a 16-byte aligned base
+  const bool vecA = ((g.lda & 1) == 0) && (((uintptr_t)gA & 15) == 0);
+  const bool vecB = ((g.ldb & 1) == 0) && (((uintptr_t)gB & 15) == 0);
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = (warp & 1) * 32, wn = (warp >> 1) * 32;
@@ -254,9 +285,9 @@ __global__ void __launch_bounds__(NT) dgemm_dmma_kernel(const __grid_constant__ 
   for (int s = 0; s < STAGES - 1; ++s) {
     if (s < nk) {
       if (GEN) gen_tile_A(As + s * STAGE_ELEMS, g, args.gen, m0, kbeg + s * BK, kend, tid);
-      else load_tile_A(As + s * STAGE_ELEMS, g, gA, args.transA, m0, kbeg + s * BK, kend, tid);
+      else load_tile_A(As + s * STAGE_ELEMS, g, gA, args.transA, m0, kbeg + s * BK, kend, tid, vecA);
       load_tile_B(Bs + s * STAGE_ELEMS, Ks + s * STAGE_ELEMS, g, gB, gK, args.transB, KR ? args.krR : 0, n0,
-                  kbeg + s * BK, kend, tid);
+                  kbeg + s * BK, kend, tid, vecB);
     }
     cp_async_commit();
   }
@@ -271,9 +302,9 @@ __global__ void __launch_bounds__(NT) dgemm_dmma_kernel(const __grid_constant__ 
       if (nt < nk) {
         int sl = nt % STAGES;
         if (GEN) gen_tile_A(As + sl * STAGE_ELEMS, g, args.gen, m0, kbeg + nt * BK, kend, tid);
-        else load_tile_A(As + sl * STAGE_ELEMS, g, gA, args.transA, m0, kbeg + nt * BK, kend, tid);
+        else load_tile_A(As + sl * STAGE_ELEMS, g, gA, args.transA, m0, kbeg + nt * BK, kend, tid, vecA);
         load_tile_B(Bs + sl * STAGE_ELEMS, Ks + sl * STAGE_ELEMS, g, gB, gK, args.transB, KR ? args.krR : 0, n0,
-                    kbeg + nt * BK, kend, tid);
+                    kbeg + nt * BK, kend, tid, vecB);
       }
       cp_async_commit();
     }

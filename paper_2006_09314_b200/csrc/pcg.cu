@@ -41,15 +41,20 @@ __global__ void hadamard_basis_kernel(const __grid_constant__ KRBasisArgs A) {
   const int cols = s * q;
   const size_t al = reinterpret_cast<size_t>(W) | reinterpret_cast<size_t>(Zh) | reinterpret_cast<size_t>(K);
   if ((n & 1) == 0 && (al & 15) == 0) {
-    const int n2 = n >> 1;
-    const long long tot = (long long)n2 * cols;
-    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < tot;
-         idx += (long long)gridDim.x * blockDim.x) {
-      const int col = (int)(idx / n2), i2 = (int)(idx - (long long)col * n2);
+    // a warp per output column at a time (index math once per column), 16-byte coalesced
+    // loads from L2 and streaming stores along n
+    const int n2 = n >> 1, lane = threadIdx.x & 31;
+    const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+    for (int col = wid; col < cols; col += nw) {
       const int a = col / q, b = col - a * q;
-      const double2 w = __ldg(reinterpret_cast<const double2*>(W + (size_t)a * n) + i2);
-      const double2 z = __ldg(reinterpret_cast<const double2*>(Zh + (size_t)b * n) + i2);
-      __stcs(reinterpret_cast<double2*>(K + (size_t)col * n) + i2, make_double2(w.x * z.x, w.y * z.y));
+      const double2* wa = reinterpret_cast<const double2*>(W + (size_t)a * n);
+      const double2* zb = reinterpret_cast<const double2*>(Zh + (size_t)b * n);
+      double2* o = reinterpret_cast<double2*>(K + (size_t)col * n);
+#pragma unroll 4
+      for (int i2 = lane; i2 < n2; i2 += 32) {
+        const double2 w = __ldg(wa + i2), z = __ldg(zb + i2);
+        __stcs(o + i2, make_double2(w.x * z.x, w.y * z.y));
+      }
     }
     return;
   }
@@ -211,7 +216,7 @@ TT apply_truncate_tt(fc_ctx c, SpecCP& sp, const TT& x, double eps, int rank_cap
   {
     KProfScope kp(KP_KR_BASIS, st, kr_bytes);
     // ~8 resident 256-thread CTAs per SM over the 3 modes, 16 bytes per thread and pass
-    const int gx = (int)std::max<long long>(1, std::min<long long>((kr_max / 2 + 255) / 256, 148 * 8 / 3 + 1));
+    const int gx = (int)std::max<long long>(1, std::min<long long>((kr_max / n + 7) / 8, 148 * 8 / 3 + 1));
     hadamard_basis_kernel<<<dim3(gx, 3), 256, 0, st>>>(kra);
     FC_CHECK_LAUNCH();
   }

@@ -124,6 +124,7 @@ __device__ __forceinline__ dd dd_sqrt(dd a) {
 // are zero) with L_k L_k^T = W_k W_k^T, W_k[a, j] = Cx[a + j t] d[k Rx + j].  The dd Gram (hi, lo)
 // is in shared memory for t <= kFactorSmemT, else in this CTA's slice of Hg (2 t^2 doubles per
 // CTA, L2-resident); Gram entries are accumulated kFactorEnt per thread per pass over W.
+template <int ENT>
 __global__ void __launch_bounds__(kFactorThreads) struct_factor_kernel(int t, int Rx, const double* __restrict__ Cx,
                                                                        const double* __restrict__ d, double* Lout,
                                                                        double* Hg) {
@@ -134,15 +135,16 @@ __global__ void __launch_bounds__(kFactorThreads) struct_factor_kernel(int t, in
   double* Wc = fsm;                                  // t x kFactorJC chunk of W_k
   double* Lc = fsm + (size_t)t * kFactorJC;          // current column (hi, lo): 2 t
   double* piv = Lc + 2 * t;                          // used flags: t
-  double* Hh = gl ? Hg + (size_t)k * 2 * t * t : piv + t;   // t x t (hi), later the Schur complement
+  int* rem = reinterpret_cast<int*>(piv + t);        // unpivoted indices (t ints in t doubles)
+  double* Hh = gl ? Hg + (size_t)k * 2 * t * t : piv + 2 * t;   // t x t (hi), later the Schur complement
   double* Hl = Hh + (size_t)t * t;                   // t x t (lo)
   const double* dk = d + (size_t)k * Rx;
-  for (int e0 = 0; e0 < ne; e0 += kFactorEnt * kFactorThreads) {
+  for (int e0 = 0; e0 < ne; e0 += ENT * kFactorThreads) {
     // entry e -> (a, b), a >= b, row-major over the lower triangle
-    int ea[kFactorEnt], eb[kFactorEnt];
-    dd acc[kFactorEnt];
+    int ea[ENT], eb[ENT];
+    dd acc[ENT];
 #pragma unroll
-    for (int q = 0; q < kFactorEnt; ++q) {
+    for (int q = 0; q < ENT; ++q) {
       const int e = e0 + tid + q * kFactorThreads;
       int a = 0, b = 0;
       if (e < ne) {
@@ -164,7 +166,7 @@ __global__ void __launch_bounds__(kFactorThreads) struct_factor_kernel(int t, in
       }
       __syncthreads();
 #pragma unroll
-      for (int q = 0; q < kFactorEnt; ++q) {
+      for (int q = 0; q < ENT; ++q) {
         if (e0 + tid + q * kFactorThreads >= ne) break;
         const int a = ea[q], b = eb[q];
         double hi = acc[q].hi, lo = acc[q].lo;
@@ -175,11 +177,14 @@ __global__ void __launch_bounds__(kFactorThreads) struct_factor_kernel(int t, in
           lo += ((hi - (s - bb)) + (p - bb)) + pe;
           hi = s;
         }
-        acc[q] = dd_fast2sum(hi, lo);
+        acc[q].hi = hi;
+        acc[q].lo = lo;
       }
+#pragma unroll
+      for (int q = 0; q < ENT; ++q) acc[q] = dd_fast2sum(acc[q].hi, acc[q].lo);
     }
 #pragma unroll
-    for (int q = 0; q < kFactorEnt; ++q) {
+    for (int q = 0; q < ENT; ++q) {
       if (e0 + tid + q * kFactorThreads >= ne) break;
       const int a = ea[q], b = eb[q];
       Hh[a + b * t] = Hh[b + a * t] = acc[q].hi;
@@ -192,25 +197,62 @@ __global__ void __launch_bounds__(kFactorThreads) struct_factor_kernel(int t, in
   for (int i = tid; i < t * t; i += kFactorThreads) L[i] = 0.0;
   __syncthreads();
   __shared__ double s_tr;
-  __shared__ int s_p;
+  __shared__ int s_p, s_nrem;
+  __shared__ double w_best[kFactorThreads / 32];
+  __shared__ int w_idx[kFactorThreads / 32];
   if (tid == 0) {
     double tr = 0.0;
     for (int i = 0; i < t; ++i) tr += Hh[i + i * t];
     s_tr = tr;
+    s_nrem = t;
   }
+  for (int i = tid; i < t; i += kFactorThreads) rem[i] = i;
   __syncthreads();
   const double stop = 1e-30 * s_tr;
+  const int warp = tid >> 5, lane = tid & 31;
   for (int c = 0; c < t; ++c) {
-    if (tid == 0) {                                   // diagonal pivot: the largest Schur diagonal
+    const int nrem = s_nrem;
+    // diagonal pivot: the largest Schur diagonal among the unpivoted indices (ties -> the
+    // smallest index), block-wide argmax
+    double best = stop;
+    int bi = -1;
+    for (int q = tid; q < nrem; q += kFactorThreads) {
+      const int i = rem[q];
+      const double v = Hh[i + i * t];
+      if (v > best || (v == best && bi >= 0 && i < bi)) {
+        best = v;
+        bi = i;
+      }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (oi >= 0 && (bi < 0 || ov > best || (ov == best && oi < bi))) {
+        best = ov;
+        bi = oi;
+      }
+    }
+    if (lane == 0) {
+      w_best[warp] = best;
+      w_idx[warp] = bi;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double b = stop;
       int p = -1;
-      double best = stop;
-      for (int i = 0; i < t; ++i)
-        if (piv[i] == 0.0 && Hh[i + i * t] > best) {
-          best = Hh[i + i * t];
-          p = i;
+      for (int w = 0; w < kFactorThreads / 32; ++w)
+        if (w_idx[w] >= 0 && (p < 0 || w_best[w] > b || (w_best[w] == b && w_idx[w] < p))) {
+          b = w_best[w];
+          p = w_idx[w];
         }
       s_p = p;
-      if (p >= 0) piv[p] = 1.0;
+      if (p >= 0) {
+        piv[p] = 1.0;
+        int q = 0;                                    // remove p from the unpivoted list
+        while (rem[q] != p) ++q;
+        rem[q] = rem[nrem - 1];
+        s_nrem = nrem - 1;
+      }
     }
     __syncthreads();
     const int p = s_p;
@@ -225,12 +267,19 @@ __global__ void __launch_bounds__(kFactorThreads) struct_factor_kernel(int t, in
       L[i + (size_t)c * t] = v.hi + v.lo;
     }
     __syncthreads();
-    for (int idx = tid; idx < t * t; idx += kFactorThreads) {   // Schur complement (unpivoted rows)
-      const int i = idx % t, j = idx / t;
-      if (piv[i] != 0.0 || piv[j] != 0.0 || j > i) continue;
-      const dd v = dd_add({Hh[idx], Hl[idx]}, dd_mul({-Lc[2 * i], -Lc[2 * i + 1]}, {Lc[2 * j], Lc[2 * j + 1]}));
-      Hh[idx] = Hh[j + i * t] = v.hi;
-      Hl[idx] = Hl[j + i * t] = v.lo;
+    // Schur complement on the unpivoted lower triangle: pairs (qa >= qb) of the remaining list
+    const int nr = nrem - 1;
+    const int np = nr * (nr + 1) / 2;
+    for (int e = tid; e < np; e += kFactorThreads) {
+      int qa = (int)((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
+      while ((qa + 1) * (qa + 2) / 2 <= e) ++qa;
+      while (qa * (qa + 1) / 2 > e) --qa;
+      const int qb = e - qa * (qa + 1) / 2;
+      const int i = rem[qa], j = rem[qb];
+      const size_t ij = (size_t)i + (size_t)j * t;
+      const dd v = dd_add({Hh[ij], Hl[ij]}, dd_mul({-Lc[2 * i], -Lc[2 * i + 1]}, {Lc[2 * j], Lc[2 * j + 1]}));
+      Hh[ij] = Hh[j + (size_t)i * t] = v.hi;
+      Hl[ij] = Hl[j + (size_t)i * t] = v.lo;
     }
     __syncthreads();
   }
@@ -1647,16 +1696,27 @@ TT truncate_tt(fc_ctx c, const TT& xin, double eps, int rank_cap, TruncStats* st
           double* Lf = s.alloc<double>((size_t)t * t * rr);
           const bool fgl = t > kFactorSmemT;
           double* Hg = fgl ? s.alloc<double>((size_t)2 * t * t * rr) : nullptr;
-          const size_t fsmem = ((size_t)t * kFactorJC + 3 * (size_t)t + (fgl ? 0 : 2 * (size_t)t * t)) * 8;
+          const size_t fsmem = ((size_t)t * kFactorJC + 4 * (size_t)t + (fgl ? 0 : 2 * (size_t)t * t)) * 8;
           static bool fattr = false;
           if (!fattr) {
-            const size_t fmax = std::max(((size_t)kFactorMaxT * kFactorJC + 3 * (size_t)kFactorMaxT) * 8,
-                                         ((size_t)kFactorSmemT * kFactorJC + 3 * (size_t)kFactorSmemT +
+            const size_t fmax = std::max(((size_t)kFactorMaxT * kFactorJC + 4 * (size_t)kFactorMaxT) * 8,
+                                         ((size_t)kFactorSmemT * kFactorJC + 4 * (size_t)kFactorSmemT +
                                           2 * (size_t)kFactorSmemT * kFactorSmemT) * 8);
-            FC_CUDA_TRY(cudaFuncSetAttribute(struct_factor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fmax));
+            FC_CUDA_TRY(cudaFuncSetAttribute(struct_factor_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fmax));
+            FC_CUDA_TRY(cudaFuncSetAttribute(struct_factor_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fmax));
+            FC_CUDA_TRY(cudaFuncSetAttribute(struct_factor_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fmax));
+            FC_CUDA_TRY(cudaFuncSetAttribute(struct_factor_kernel<kFactorEnt>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)fmax));
             fattr = true;
           }
-          struct_factor_kernel<<<rr, kFactorThreads, fsmem, st>>>(t, Rx, ss->Cx[l], dl[l], Lf, Hg);
+          // Gram entries per thread and pass: the smallest of 1, 2, 4, 10 that covers t(t+1)/2 in one
+          // pass (the entries are independent accumulation chains; idle slots would cost issue slots)
+          const int ne = t * (t + 1) / 2;
+          const int ept = cdiv(ne, kFactorThreads);
+          if (ept <= 1) struct_factor_kernel<1><<<rr, kFactorThreads, fsmem, st>>>(t, Rx, ss->Cx[l], dl[l], Lf, Hg);
+          else if (ept <= 2) struct_factor_kernel<2><<<rr, kFactorThreads, fsmem, st>>>(t, Rx, ss->Cx[l], dl[l], Lf, Hg);
+          else if (ept <= 4) struct_factor_kernel<4><<<rr, kFactorThreads, fsmem, st>>>(t, Rx, ss->Cx[l], dl[l], Lf, Hg);
+          else struct_factor_kernel<kFactorEnt><<<rr, kFactorThreads, fsmem, st>>>(t, Rx, ss->Cx[l], dl[l], Lf, Hg);
           FC_CHECK_LAUNCH();
           pm.mark("4b3 refine: dd factor");
           double* Ct = s.alloc<double>((size_t)m * t * rr);
