@@ -753,6 +753,22 @@ static void gemm_dispatch(const GemmArgs& a_in, cudaStream_t st) {
     FC_CUDA_TRY(cudaFuncSetAttribute(dgemm_dmma_kernel<false, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     attr = true;
   }
+  // auto split-K for callers that left splitk at 1: a 64 x 64 output tile with a long K is one
+  // SM's work (~16 us per 4 MFLOP at the per-SM DMMA rate), so grids below two waves of 148 SMs
+  // split K (>= 128 per split, <= 16: the cluster reduction) until they reach two waves
+  static const bool auto_split = getenv("FC_GEMM_NO_AUTO_SPLIT") == nullptr;   // diagnostic
+  if (auto_split && a.splitk <= 1 && a.gen.kind < 0 && a.krR == 0) {
+    long long tiles = 0;
+    int kmin = INT32_MAX;
+    for (int i = 0; i < a.nbatch; ++i) {
+      tiles += (long long)a.rep * cdiv(a.b[i].M, BM) * cdiv(a.b[i].N, BN);
+      kmin = std::min(kmin, a.b[i].K);
+    }
+    if (tiles > 0 && tiles < 2 * 148 && kmin >= 256) {
+      const long long want = (2 * 148 + tiles - 1) / tiles;
+      a.splitk = (int)std::max<long long>(1, std::min<long long>({want, (long long)(kmin / 128), 16LL}));
+    }
+  }
   a.splitk = std::min(a.splitk, max_split());
   dim3 grid(cdiv(maxM, BM), cdiv(maxN, BN), a.nbatch * a.rep * a.splitk);
   require(grid.y <= 65535 && grid.z <= 65535, FC_ERR_INVALID_ARG, "gemm grid too large");
