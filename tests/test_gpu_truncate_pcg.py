@@ -122,7 +122,7 @@ def test_pcg_parity_shared(lib, name, n):
     prm = make_params(p.alpha, p.beta, p.eps, p.tol_stop)
     u, rep, rc = ctx.pcg_solve(b, prm)
     assert rc == 0 and rep["converged"]
-    check_rank_history(rep, rep_ref, f"{name} n={n}")
+    check_rank_history(rep, rep_ref, f"{name} n={n}", floor_rank=0.95 * n * n)
     d = reldiff(_cp(u), u_ref)
     assert d <= max(10 * p.eps, 1e-9)
     # true residual ||B - F(u)||/||B|| (O11) on both sides: the two differ by at most
