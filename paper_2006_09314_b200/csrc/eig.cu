@@ -1252,7 +1252,9 @@ __global__ void __launch_bounds__(1024) bcgs_block_kernel(const __grid_constant_
     nacc_s = 0;
     k0_s = *E.k;
     double mx = 0.0;
-    for (int c = 0; c < E.p; ++c) mx = fmax(mx, E.norm0[c]);
+    if (E.nmax) mx = *E.nmax;
+    else
+      for (int c = 0; c < E.p; ++c) mx = fmax(mx, E.norm0[c]);
     nmax_s = mx;
   }
   for (int i = tid; i < n * kBcgsW; i += nt) E.Y[i] = 0.0;   // block buffer (n x W, ld n)
@@ -1743,7 +1745,9 @@ __global__ void __launch_bounds__(kBcgsClusterThreads, 1)
     S.X[i + (size_t)c * LD] = i < nr ? E.A[(size_t)(r0 + i) + (size_t)(j0 + c) * E.lda] : 0.0;
   }
   double mx = 0.0;
-  for (int c = tid; c < E.p; c += nt) mx = fmax(mx, E.norm0[c]);
+  if (E.nmax) mx = *E.nmax;
+  else
+    for (int c = tid; c < E.p; c += nt) mx = fmax(mx, E.norm0[c]);
   for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
   __syncthreads();
   if (ln == 0) S.red[warp] = mx;
@@ -1949,6 +1953,103 @@ __global__ void __launch_bounds__(kBcgsClusterThreads, 1)
 }
 
 __global__ void set_int_kernel(int* p, int v) { *p = v; }
+
+// largest original column norm of every entry (fixed for the whole Gram-Schmidt: the acceptance
+// level tau max(norm0_c, nmax) must not change when columns are pruned)
+__global__ void bcgs_nmax_kernel(const __grid_constant__ BcgsBatch B) {
+  const BcgsEntry& E = B.e[blockIdx.x];
+  double mx = 0.0;
+  for (int c = threadIdx.x; c < E.p; c += blockDim.x) mx = fmax(mx, E.norm0[c]);
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  __shared__ double red[32];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) mx = fmax(mx, red[i]);
+    *E.nmax = mx;
+  }
+}
+
+// bulk pruning (bcgs): the columns [j0, p) of every entry were just projected against the accepted
+// basis; a column whose residual is within its acceptance level tau max(norm0_c, nmax) would be
+// rejected when its block is reached (the basis only grows) -> flag 0
+struct PruneArgs {
+  int j0[kMaxSyev];
+  int* flag[kMaxSyev];
+  int* idx[kMaxSyev];
+  int* cnt;
+  double* tmpA[kMaxSyev];
+  double* tmpN[kMaxSyev];
+};
+__global__ void bcgs_prune_flag_kernel(const __grid_constant__ BcgsBatch B, const __grid_constant__ PruneArgs P) {
+  const BcgsEntry& E = B.e[blockIdx.y];
+  const int c = P.j0[blockIdx.y] + blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), ln = threadIdx.x & 31;
+  if (c >= E.p) return;
+  const double* a = E.A + (size_t)c * E.lda;
+  double s = 0.0;
+  for (int i = ln; i < E.n; i += 32) s = fma(a[i], a[i], s);
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (ln == 0) {
+    const double lim = E.tau * fmax(E.norm0[c], *E.nmax);
+    P.flag[blockIdx.y][c - P.j0[blockIdx.y]] = s > lim * lim ? 1 : 0;
+  }
+}
+// ordered compaction of the surviving columns (one CTA per entry)
+__global__ void __launch_bounds__(1024) bcgs_prune_compact_kernel(const __grid_constant__ BcgsBatch B,
+                                                                  const __grid_constant__ PruneArgs P) {
+  const int e = blockIdx.x;
+  const BcgsEntry& E = B.e[e];
+  const int m = max(0, E.p - P.j0[e]);
+  __shared__ int wsum[32];
+  __shared__ int base;
+  if (threadIdx.x == 0) base = 0;
+  __syncthreads();
+  const int ln = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int c0 = 0; c0 < m; c0 += blockDim.x) {
+    const int c = c0 + threadIdx.x;
+    const int f = c < m ? P.flag[e][c] : 0;
+    const unsigned msk = __ballot_sync(0xffffffffu, f);
+    if (ln == 0) wsum[w] = __popc(msk);
+    __syncthreads();
+    int off = base;
+    for (int i = 0; i < w; ++i) off += wsum[i];
+    if (f) P.idx[e][off + __popc(msk & ((1u << ln) - 1u))] = c;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int t = 0;
+      for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += wsum[i];
+      base += t;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) P.cnt[e] = base;
+}
+// survivors gathered in order into the scratch copies (columns and their original norms)
+__global__ void bcgs_prune_gather_kernel(const __grid_constant__ BcgsBatch B, const __grid_constant__ PruneArgs P) {
+  const int e = blockIdx.y;
+  const BcgsEntry& E = B.e[e];
+  const int cnt = P.cnt[e], n = E.n;
+  const double* src = E.A + (size_t)P.j0[e] * E.lda;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < (long long)n * cnt;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int r = (int)(i % n), j = (int)(i / n), c = P.idx[e][j];
+    P.tmpA[e][i] = src[(size_t)r + (size_t)c * E.lda];
+    if (r == 0) P.tmpN[e][j] = E.norm0[P.j0[e] + c];
+  }
+}
+// ... and written back over columns [j0, j0 + cnt)
+__global__ void bcgs_prune_scatter_kernel(const __grid_constant__ BcgsBatch B, const __grid_constant__ PruneArgs P) {
+  const int e = blockIdx.y;
+  const BcgsEntry& E = B.e[e];
+  const int cnt = P.cnt[e], n = E.n;
+  double* dst = E.A + (size_t)P.j0[e] * E.lda;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < (long long)n * cnt;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int r = (int)(i % n), j = (int)(i / n);
+    dst[(size_t)r + (size_t)j * E.lda] = P.tmpA[e][i];
+    if (r == 0) E.norm0[P.j0[e] + j] = P.tmpN[e][j];
+  }
+}
 
 __global__ void col_norms_kernel(const __grid_constant__ BcgsBatch B) {
   const BcgsEntry& E = B.e[blockIdx.y];
@@ -2435,7 +2536,90 @@ void bcgs(const BcgsBatch& bin, cudaStream_t st) {
   }
   col_norms_kernel<<<dim3(cdiv(maxp, 8), b.nb), 256, 0, st>>>(b);
   FC_CHECK_LAUNCH();
+  for (int i = 0; i < b.nb; ++i) b.e[i].nmax = scr.alloc<double>(1);
+  bcgs_nmax_kernel<<<b.nb, 256, 0, st>>>(b);
+  FC_CHECK_LAUNCH();
+  // bulk pruning (FC_BCGS_PRUNE=0 disables): before every second block from block 2 on the
+  // remaining columns are projected against the accepted basis in one GEMM
+  // pair and those whose residual is already within their acceptance level are dropped (the
+  // greedy Gram-Schmidt would reject them when their block is reached); the survivors keep
+  // their order.  On Khatri-Rao bases (numerical rank ~ p/4) most blocks are skipped this way.
+  static const int prune_on = getenv("FC_BCGS_PRUNE") ? atoi(getenv("FC_BCGS_PRUNE")) : 1;
+  // schedule (diagnostic knobs FC_BCGS_PRUNE_FIRST / _GAP / _INC, in blocks)
+  static const int pr_first = getenv("FC_BCGS_PRUNE_FIRST") ? atoi(getenv("FC_BCGS_PRUNE_FIRST")) : 2;
+  static const int pr_gap = getenv("FC_BCGS_PRUNE_GAP") ? atoi(getenv("FC_BCGS_PRUNE_GAP")) : 2;
+  static const int pr_inc = getenv("FC_BCGS_PRUNE_INC") ? atoi(getenv("FC_BCGS_PRUNE_INC")) : 0;
+  int next_prune = pr_first * W, prune_gap = std::max(1, pr_gap) * W;
+  long long pruned_total = 0;
   for (int j0 = 0; j0 < maxp; j0 += W) {
+    if (prune_on && j0 == next_prune) {
+      next_prune += prune_gap;
+      prune_gap += pr_inc * W;
+      PruneArgs pa{};
+      GemmArgs gp, gu;
+      gp.transA = 1;
+      gp.beta = 0.0;
+      gu.alpha = -1.0;
+      gu.beta = 1.0;
+      int nb = 0, pmx = 0;
+      bool any = false;
+      for (int i = 0; i < b.nb; ++i) {
+        const BcgsEntry& E = b.e[i];
+        pa.j0[i] = j0;
+        const int rem = E.p - j0;
+        if (rem < 2 * W) continue;   // too few columns left to gain
+        any = true;
+        const int kup = std::min(E.k_base + j0, E.kcap);
+        double* Pb = scr.alloc<double>((size_t)kup * rem);
+        gp.b[nb] = GemmBatch{kup, rem, E.n, E.Q, E.ldq, E.A + (size_t)j0 * E.lda, E.lda, Pb, kup, nullptr, 0, nullptr};
+        gp.b[nb].dynM = E.k;
+        gu.b[nb] = GemmBatch{E.n, rem, kup, E.Q, E.ldq, Pb, kup, E.A + (size_t)j0 * E.lda, E.lda, nullptr, 0, nullptr};
+        gu.b[nb].dynK = E.k;
+        ++nb;
+        pmx = std::max(pmx, rem);
+      }
+      if (any) {
+        gp.nbatch = gu.nbatch = nb;
+        gemm(gp, st);
+        gemm(gu, st);
+        pa.cnt = scr.alloc<int>(kMaxSyev);
+        FC_CUDA_TRY(cudaMemsetAsync(pa.cnt, 0, kMaxSyev * sizeof(int), st));
+        for (int i = 0; i < b.nb; ++i) {
+          const BcgsEntry& E = b.e[i];
+          const int rem = std::max(E.p - j0, 0);
+          if (rem < 2 * W) {
+            pa.j0[i] = E.p;   // untouched: nothing flagged, nothing moved
+            continue;
+          }
+          pa.flag[i] = scr.alloc<int>(rem);
+          pa.idx[i] = scr.alloc<int>(rem);
+          pa.tmpA[i] = scr.alloc<double>((size_t)E.n * rem);
+          pa.tmpN[i] = scr.alloc<double>(rem);
+        }
+        bcgs_prune_flag_kernel<<<dim3(cdiv(pmx, 8), b.nb), 256, 0, st>>>(b, pa);
+        FC_CHECK_LAUNCH();
+        bcgs_prune_compact_kernel<<<b.nb, 1024, 0, st>>>(b, pa);
+        FC_CHECK_LAUNCH();
+        const int gx = std::max(1, std::min(cdiv((long long)b.e[0].n * pmx, 256), 148 * 4 / std::max(b.nb, 1) + 1));
+        bcgs_prune_gather_kernel<<<dim3(gx, b.nb), 256, 0, st>>>(b, pa);
+        FC_CHECK_LAUNCH();
+        bcgs_prune_scatter_kernel<<<dim3(gx, b.nb), 256, 0, st>>>(b, pa);
+        FC_CHECK_LAUNCH();
+        int cnt[kMaxSyev];
+        FC_CUDA_TRY(cudaMemcpyAsync(cnt, pa.cnt, b.nb * sizeof(int), cudaMemcpyDeviceToHost, st));
+        FC_CUDA_TRY(cudaStreamSynchronize(st));
+        maxp = 0;
+        for (int i = 0; i < b.nb; ++i) {
+          BcgsEntry& E = b.e[i];
+          if (pa.j0[i] == j0) {
+            pruned_total += E.p - (j0 + cnt[i]);
+            E.p = j0 + cnt[i];
+          }
+          maxp = std::max(maxp, E.p);
+        }
+        if (j0 >= maxp) break;
+      }
+    }
     // project the block against every column accepted so far (<= j0; unused Q columns are 0),
     // TWICE before the in-block step: after a single classical projection a column that lies
     // almost in span(Q) (residual ~1e-10 of its norm, still above the acceptance level) keeps a
@@ -2506,6 +2690,7 @@ void bcgs(const BcgsBatch& bin, cudaStream_t st) {
     }
     finalize_step(b, j0);
   }
+  if (trace && pruned_total) fprintf(stderr, "[bcgs] pruned %lld columns\n", pruned_total);
 }
 
 void rank_cut_device(int count, const double* s2, double factor, const double* energy, int* r_out,

@@ -68,6 +68,7 @@ struct BcgsEntry {
   double* Y = nullptr;   // n x 32 block buffer (allocated by bcgs)
   int* nacc = nullptr;   // accepted count of the current block (allocated by bcgs)
   int k_base = 0;        // the first k_base columns of A are orthonormal: taken into Q as they are
+  double* nmax = nullptr; // largest original column norm (set by bcgs: fixed when columns are pruned)
 };
 struct BcgsBatch {
   int nb = 0;
