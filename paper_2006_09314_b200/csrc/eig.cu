@@ -897,6 +897,99 @@ __global__ void tri_invit_kernel(const __grid_constant__ SyevBatch B, int nsolve
             true, nsolve);
 }
 
+// tri_invit_kernel with each vector's LU factors and iterate in shared memory, interleaved by
+// thread ([k T + t]: conflict-free), and d, e staged once per CTA: the sequential recurrences
+// (LU, forward, backward) then read operands at shared-memory latency, independent of the
+// recurrence and so prefetchable, instead of an L2 round trip per step.  Same operations in the
+// same order as tri_invit (bit-identical vectors).
+__global__ void tri_invit_smem_kernel(const __grid_constant__ SyevBatch B, int nsolve) {
+  extern __shared__ double ism[];
+  const SyevEntry& E = B.e[blockIdx.y];
+  const int N = E.N, T = blockDim.x, t = threadIdx.x;
+  const int r = min(*E.r, N);
+  const int i0 = blockIdx.x * T;
+  if (i0 >= r) return;   // uniform over the CTA
+  double* __restrict__ ds = ism;
+  double* __restrict__ es = ism + N;
+  double* __restrict__ u0 = ism + 2 * (size_t)N;
+  double* __restrict__ u1 = u0 + (size_t)N * T;
+  double* __restrict__ u2 = u1 + (size_t)N * T;
+  double* __restrict__ lm = u2 + (size_t)N * T;
+  double* __restrict__ v = lm + (size_t)N * T;
+  unsigned char* __restrict__ pv = reinterpret_cast<unsigned char*>(v + (size_t)N * T);
+  for (int k = t; k < N; k += T) {
+    ds[k] = E.d[k];
+    es[k] = k < N - 1 ? E.e[k] : 0.0;
+  }
+  __syncthreads();
+  const int i = i0 + t;
+  if (i >= r) return;
+  double tnorm = 0.0;
+  for (int k = 0; k < N; ++k) tnorm = fmax(tnorm, fabs(ds[k]) + 2.0 * (k < N - 1 ? fabs(es[k]) : 0.0));
+  const double lam = E.lam[i];
+  double* vout = E.Y + (size_t)i * E.ldy;
+  if (N == 1) {
+    vout[0] = 1.0;
+    return;
+  }
+  const double tiny = kEps * tnorm + DBL_MIN;
+#define S(a, k) a[(size_t)(k) * T + t]
+  double cd = ds[0] - lam, cs = es[0], cs2 = 0.0;
+  for (int k = 0; k < N - 1; ++k) {
+    double sub = es[k];
+    double ad = ds[k + 1] - lam;
+    double as = (k + 1 < N - 1) ? es[k + 1] : 0.0;
+    if (fabs(sub) > fabs(cd)) {
+      double m = cd / sub;
+      S(u0, k) = 1.0 / sub; S(u1, k) = ad; S(u2, k) = as;
+      S(lm, k) = m; S(pv, k) = 1;
+      double nd = cs - m * ad, ns = cs2 - m * as;
+      cd = nd; cs = ns; cs2 = 0.0;
+    } else {
+      if (fabs(cd) < tiny) cd = (cd >= 0 ? tiny : -tiny);
+      double m = sub / cd;
+      S(u0, k) = 1.0 / cd; S(u1, k) = cs; S(u2, k) = cs2;
+      S(lm, k) = m; S(pv, k) = 0;
+      cd = ad - m * cs; cs = as; cs2 = 0.0;
+    }
+  }
+  if (fabs(cd) < tiny) cd = (cd >= 0 ? tiny : -tiny);
+  S(u0, N - 1) = 1.0 / cd; S(u1, N - 1) = 0.0; S(u2, N - 1) = 0.0;
+  const unsigned seed = (unsigned)(i + 17);
+  for (int k = 0; k < N; ++k) {
+    unsigned h = (unsigned)k * 2654435761u ^ (seed * 2246822519u + 0x9E3779B9u);
+    h ^= h >> 15; h *= 2246822519u; h ^= h >> 13;
+    S(v, k) = 0.5 + (h & 0xFFFFFF) / 16777216.0;
+  }
+  double scale = 1.0;
+  for (int it = 0; it < nsolve; ++it) {
+    double carry = S(v, 0) * scale;
+#pragma unroll 4
+    for (int k = 0; k < N - 1; ++k) {
+      double bk = carry, bk1 = S(v, k + 1) * scale;
+      if (S(pv, k) != 0) { double tt = bk; bk = bk1; bk1 = tt; }
+      bk1 -= S(lm, k) * bk;
+      S(v, k) = bk;
+      carry = bk1;
+    }
+    S(v, N - 1) = carry;
+    double x2 = 0.0, x1 = 0.0, nrm = 0.0;
+#pragma unroll 4
+    for (int k = N - 1; k >= 0; --k) {
+      double x = (S(v, k) - S(u1, k) * x1 - S(u2, k) * x2) * S(u0, k);
+      S(v, k) = x;
+      x2 = x1; x1 = x;
+      nrm = fmax(nrm, fabs(x));
+    }
+    scale = 1.0 / nrm;
+  }
+  double s2 = 0.0;
+  for (int k = 0; k < N; ++k) { double x = S(v, k) * scale; s2 += x * x; }
+  const double inv = scale / sqrt(s2);
+  for (int k = 0; k < N; ++k) vout[k] = S(v, k) * inv;
+#undef S
+}
+
 // one CTA per matrix: CGS2 orthonormalisation of Y[:, 0..r) in order, then back-transform
 // with the Householder vectors stored in A: z = H_0 H_1 ... H_{N-3} y.
 // (flag != nullptr: only the entries with flag[i] != 0 are processed; the polar path below
@@ -2252,7 +2345,31 @@ void syev_vectors(const SyevBatch& b, int maxN, cudaStream_t st, const int* r_ho
   if (b.nb == 0 || maxN == 0) return;
   // inverse-iteration solves per vector (FC_INVIT_SOLVES, default 3)
   static const int nsolve = getenv("FC_INVIT_SOLVES") ? atoi(getenv("FC_INVIT_SOLVES")) : 3;
-  tri_invit_kernel<<<dim3(cdiv(maxN, 64), b.nb), 64, 0, st>>>(b, nsolve);
+  // shared-memory variant: T vectors per CTA, T sized for ~2 CTAs per SM over the batch and
+  // the 227 KB limit (FC_INVIT_GLOBAL=1: the global-scratch kernel)
+  static const bool inv_global = getenv("FC_INVIT_GLOBAL") != nullptr;
+  int rmax = 0;
+  long long tot = 0;
+  for (int i = 0; i < b.nb; ++i) {
+    const int ri = r_host ? std::min(r_host[i], b.e[i].N) : b.e[i].N;
+    rmax = std::max(rmax, ri);
+    tot += ri;
+  }
+  const size_t per_t = (size_t)maxN * (5 * 8 + 1), fixed = (size_t)2 * maxN * 8;
+  const int tmax = (int)std::min<size_t>(32, (200u * 1024 - fixed) / std::max<size_t>(per_t, 1));
+  if (!inv_global && tmax >= 1 && rmax > 0) {
+    int T = (int)std::max<long long>(1, (tot + 2 * 148 - 1) / (2 * 148));
+    T = std::min(T, tmax);
+    const size_t smem = fixed + (size_t)T * per_t + 16;
+    static size_t attr = 0;
+    if (smem > 48 * 1024 && smem > attr) {
+      FC_CUDA_TRY(cudaFuncSetAttribute(tri_invit_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      attr = smem;
+    }
+    tri_invit_smem_kernel<<<dim3(cdiv(rmax, T), b.nb), T, smem, st>>>(b, nsolve);
+  } else {
+    tri_invit_kernel<<<dim3(cdiv(maxN, 64), b.nb), 64, 0, st>>>(b, nsolve);
+  }
   FC_CHECK_LAUNCH();
   static const bool trace_orth = getenv("FC_TRACE_ORTH") != nullptr;
   if (trace_orth) {   // diagnostics: orthogonality of the inverse-iteration vectors

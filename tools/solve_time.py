@@ -31,7 +31,7 @@ def main():
         e1.record()
         torch.cuda.synchronize()
         ts.append(e0.elapsed_time(e1))
-    print(f"n={n} eps={eps} rc={rc} iters={rep['iters']} rel_res={rep['rel_res'][-1]:.6e} rank={u.rank} "
+    print(f"n={n} eps={eps} rc={rc} iters={rep['iters']} rel_res={rep['rel_res'][-1]!r} ranks={sum(rep['rank_R'])}/{sum(rep['rank_S'])}/{sum(rep['rank_Z'])} rank={u.rank} "
           f"ms={' '.join(f'{t:.1f}' for t in ts)} env={ {k: v for k, v in os.environ.items() if k.startswith('FC_')} }")
 
 
