@@ -78,6 +78,58 @@ __global__ void struct_scale_kernel(int t, int R, int Rx, const double* __restri
   }
 }
 
+// ---- weighted Khatri-Rao basis (structured route) ---------------------------------------------
+// The structured side matrix is A_l = sum_a K_a W'_a with K_a = [w_a (.) xhat_b]_b (n x t) and
+// W'_a[b, (kk, j)] = E[a, kk] Cx[b, j] d[kk, j]: column (a, b) of K enters A_l only through row
+// (a, b) of the coefficient matrix, whose norm is rho_{a,b} = (sum_kk E[a,kk]^2 H_kk[b,b])^1/2,
+// H_kk = W_kk W_kk^T.  The rank-revealing Gram-Schmidt therefore runs on K diag(rho / rho_max):
+// a residual e dropped from a scaled column perturbs A_l by ||e|| rho_max — the same bound as
+// dropping it from the unscaled column with the largest weight — while the columns that carry
+// little of x (x's trailing Tucker directions) no longer force basis vectors of their own.
+struct ColWeightArgs {
+  const double* E[3];     // s x r (ld s)
+  const double* H[3];     // t x t x r
+  int s[3], t[3];
+  double* wgt[3];         // s*t column weights rho / rho_max (1 if every rho is 0)
+};
+__global__ void __launch_bounds__(1024) col_weight_kernel(int r, ColWeightArgs a) {
+  __shared__ double red[32];
+  __shared__ double mx_s;
+  const int l = blockIdx.x, s = a.s[l], t = a.t[l], p = s * t;
+  const double* E = a.E[l];
+  const double* H = a.H[l];
+  double mx = 0.0;
+  for (int c = threadIdx.x; c < p; c += blockDim.x) {
+    const int aa = c / t, b = c % t;
+    double v = 0.0;
+    for (int kk = 0; kk < r; ++kk) {
+      const double e = E[aa + (size_t)kk * s];
+      v = fma(e * e, fmax(H[b + (size_t)b * t + (size_t)kk * t * t], 0.0), v);
+    }
+    a.wgt[l][c] = v;
+    mx = fmax(mx, v);
+  }
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if (threadIdx.x == 0) mx_s = v;
+  }
+  __syncthreads();
+  const double m = mx_s;
+  for (int c = threadIdx.x; c < p; c += blockDim.x) a.wgt[l][c] = m > 0.0 ? sqrt(a.wgt[l][c] / m) : 1.0;
+}
+// out[:, c] = in[:, c] * wgt[c]   (n x p, contiguous columns)
+__global__ void scale_copy_cols_kernel(int n, int p, const double* __restrict__ in, const double* __restrict__ wgt,
+                                       double* __restrict__ out) {
+  const long long tot = (long long)n * p;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < tot;
+       idx += (long long)gridDim.x * blockDim.x)
+    out[idx] = in[idx] * wgt[idx / n];
+}
+
 // ---- accurate factor of the per-term side Grams (A11' on the structured route) --------------
 // The structured side matrix of mode l is B = [Rm_1 W_1 | ... | Rm_r W_r], W_k = Cx diag(d_k)
 // (t x Rx per spectral term k).  B B^T = sum_k Rm_k L_k L_k^T Rm_k^T for ANY L_k with
@@ -1236,6 +1288,16 @@ void tt_compute_core(cudaStream_t st, TT& x) {
 // ~2 kBasisTol ||A|| sigma_cut, i.e. <= 4e-4 of the threshold (eps/2)^2 ||A||^2 at eps = 1e-6,
 // well inside the A23 noise band; it shrinks the eigenproblem (and its N^3 cost) notably.
 constexpr double kBasisTol = 1e-10;
+// ... of the weighted Khatri-Rao basis (structured route): there the dropped residuals are not
+// incidental (most columns far below the level) but sit at the level itself, ~sqrt(#columns) tol
+// of the side matrix in total (measured 1.05e-8 of the result at tol = 1e-10, 1377 columns), so
+// the level is set two decades lower to keep the result within the single-truncation parity
+// tolerance max(1e-10, 10 eps_mach / eps): min(1e-12, 1e-6 eps).  Measured on a C4 iterate at
+// n = 1024 (profiles/r02pp_wbasis_tol.txt): the result moves by ~80 tol at eps = 1e-6 and ~480 tol
+// at eps = 1e-8; C4 time-to-eps 225 / 230 / 234 / 238 ms at tol = 1e-10 / 1e-11 / 1e-12 / 1e-13
+// against 278 ms with the unweighted basis.  (FC_WBASIS_TOL overrides; diagnostics)
+constexpr double kWBasisTol = 1e-12;
+constexpr double kWBasisTolPerEps = 1e-6;
 // Gram eigenvalue noise per direction, in units of eps_mach * lam_max (refined cut below it)
 constexpr double kNoise = 1.0;
 // K13: below this eps the CP route takes the SVD of the side matrix itself (FC_TRUNC_QR=0/1)
@@ -1278,6 +1340,117 @@ TT truncate_tt(fc_ctx c, const TT& xin, double eps, int rank_cap, TruncStats* st
   double* RmE[3] = {nullptr, nullptr, nullptr};
   int q[3];
   require(!ss || (!xin.orth[0] && !xin.orth[1] && !xin.orth[2]), FC_ERR_INVALID_ARG, "structured input basis");
+  double* n2[3];
+  double* dl[3];
+  double* inv[3];
+  for (int l = 0; l < 3; ++l) {
+    n2[l] = s.alloc<double>(R);
+    dl[l] = s.alloc<double>(R);
+    inv[l] = s.alloc<double>(R);
+  }
+  double* xi = s.alloc<double>(R);
+  double* energy = s.alloc<double>(4);
+  auto term_weights = [&]() {
+    const int nbw = std::max(1, std::min(148, cdiv(R, 1024)));
+    double* part = s.alloc<double>(nbw);
+    term_weights_kernel<<<nbw, 1024, 0, st>>>(R, xin.w, n2[0], n2[1], n2[2], xi, dl[0], dl[1], dl[2], inv[0], inv[1],
+                                              inv[2], part);
+    FC_CHECK_LAUNCH();
+    sum_parts_kernel<<<1, 32, 0, st>>>(nbw, part, energy);
+    FC_CHECK_LAUNCH();
+  };
+  // n2[kk*Rx + j] = cx_j^T Gm_kk cx_j with Gm_kk (t x t) the Gram of spectral term kk's mode basis,
+  // P_kk = Gm_kk Cx, chunked over kk so that P stays below kStructChunk doubles per mode
+  auto struct_norms = [&](double* const Gm[3]) {
+    const int r = ss->r, Rx = ss->Rx, kc = struct_chunk(ss);
+    double* P[3];
+    for (int l = 0; l < 3; ++l) P[l] = s.alloc<double>((size_t)ss->t[l] * Rx * kc);
+    for (int k0 = 0; k0 < r; k0 += kc) {
+      const int nk = std::min(kc, r - k0);
+      GemmArgs gp;
+      gp.nbatch = 3;
+      gp.rep = nk;
+      StructNormArgs na;
+      for (int l = 0; l < 3; ++l) {
+        const int t = ss->t[l];
+        gp.b[l] = GemmBatch{t, Rx, t, Gm[l] + (size_t)k0 * t * t, t, ss->Cx[l], t, P[l], t, nullptr, 0, nullptr};
+        gp.b[l].sA = (long long)t * t;
+        gp.b[l].sC = (long long)t * Rx;
+        na.Cx[l] = ss->Cx[l]; na.P[l] = P[l]; na.t[l] = t; na.n2[l] = n2[l] + (size_t)k0 * Rx;
+      }
+      gemm(gp, st);
+      struct_norms_kernel<<<dim3(cdiv(nk * Rx, 8), 3), 256, 0, st>>>(nk * Rx, Rx, na);
+      FC_CHECK_LAUNCH();
+    }
+  };
+  // H_kk = W_kk W_kk^T,  W_kk = Cx diag(d_l[kk*Rx + .])   (t x t per spectral term, W chunked over kk)
+  double* Hs[3] = {nullptr, nullptr, nullptr};
+  auto struct_side_grams = [&]() {
+    const int r = ss->r, Rx = ss->Rx, kc = struct_chunk(ss);
+    double* W[3];
+    for (int l = 0; l < 3; ++l) {
+      W[l] = s.alloc<double>((size_t)ss->t[l] * Rx * kc);
+      Hs[l] = s.alloc<double>((size_t)ss->t[l] * ss->t[l] * r);
+    }
+    for (int k0 = 0; k0 < r; k0 += kc) {
+      const int nk = std::min(kc, r - k0);
+      GemmArgs gh;
+      gh.transB = 1;
+      gh.nbatch = 3;
+      gh.rep = nk;
+      for (int l = 0; l < 3; ++l) {
+        const int t = ss->t[l];
+        struct_scale_kernel<<<blocks_for((long long)t * Rx * nk), 256, 0, st>>>(t, nk * Rx, Rx, ss->Cx[l],
+                                                                                 dl[l] + (size_t)k0 * Rx, W[l]);
+        FC_CHECK_LAUNCH();
+        gh.b[l] = GemmBatch{t, t, Rx, W[l], t, W[l], t, Hs[l] + (size_t)k0 * t * t, t, nullptr, 0, nullptr};
+        gh.b[l].sA = gh.b[l].sB = (long long)t * Rx;
+        gh.b[l].sC = (long long)t * t;
+      }
+      gemm(gh, st);
+    }
+  };
+  // Weighted Khatri-Rao basis (structured route; FC_BASIS_WEIGHT=0: the unweighted basis): the term
+  // norms and the per-term side Grams do not need the orthonormal basis — Gm_kk = K_kk^T K_kk with
+  // K_kk = sum_a E[a, kk] K_a (n x t) formed explicitly — so they come first and give every column
+  // of K its weight in the side matrix (col_weight_kernel).
+  static const bool wbasis_on = !(getenv("FC_BASIS_WEIGHT") && atoi(getenv("FC_BASIS_WEIGHT")) == 0);
+  const bool wbasis = ss && wbasis_on;
+  static const double wbasis_env = getenv("FC_WBASIS_TOL") ? atof(getenv("FC_WBASIS_TOL")) : 0.0;
+  const double wbasis_tol = wbasis_env > 0.0 ? wbasis_env : std::min(kWBasisTol, kWBasisTolPerEps * eps);
+  double* wcol[3] = {nullptr, nullptr, nullptr};
+  if (wbasis) {
+    const int r = ss->r;
+    double* Kk[3];
+    double* Gm[3];
+    GemmArgs gk, gg;
+    gk.nbatch = gg.nbatch = 3;
+    gg.transA = 1;
+    gg.rep = r;
+    for (int l = 0; l < 3; ++l) {
+      const int t = ss->t[l], sl = ss->s[l];
+      require(xin.q[l] == sl * t, FC_ERR_INVALID_ARG, "structured basis shape");
+      Kk[l] = s.alloc<double>((size_t)n * t * r);
+      Gm[l] = s.alloc<double>((size_t)t * t * r);
+      gk.b[l] = GemmBatch{n * t, r, sl, xin.Q[l], n * t, ss->E[l], sl, Kk[l], n * t, nullptr, 0, nullptr};
+      gg.b[l] = GemmBatch{t, t, n, Kk[l], n, Kk[l], n, Gm[l], t, nullptr, 0, nullptr};
+      gg.b[l].sA = gg.b[l].sB = (long long)n * t;
+      gg.b[l].sC = (long long)t * t;
+    }
+    gemm(gk, st);
+    gemm(gg, st);
+    struct_norms(Gm);
+    term_weights();
+    struct_side_grams();
+    ColWeightArgs cw;
+    for (int l = 0; l < 3; ++l) {
+      wcol[l] = s.alloc<double>(xin.q[l]);
+      cw.E[l] = ss->E[l]; cw.H[l] = Hs[l]; cw.s[l] = ss->s[l]; cw.t[l] = ss->t[l]; cw.wgt[l] = wcol[l];
+    }
+    col_weight_kernel<<<3, 1024, 0, st>>>(r, cw);
+    FC_CHECK_LAUNCH();
+    pm.mark("0b column weights (structured)");
+  }
   {
     BcgsBatch pb;
     int* kdev = s.alloc<int>(4);
@@ -1287,12 +1460,17 @@ TT truncate_tt(fc_ctx c, const TT& xin, double eps, int rank_cap, TruncStats* st
       if (xin.orth[l]) continue;
       require(xin.q[l] >= 1, FC_ERR_INVALID_ARG, "empty basis");
       double* Kc = s.alloc<double>((size_t)n * xin.q[l]);
-      FC_CUDA_TRY(cudaMemcpyAsync(Kc, xin.Q[l], (size_t)n * xin.q[l] * 8, cudaMemcpyDeviceToDevice, st));
+      if (wcol[l]) {
+        scale_copy_cols_kernel<<<blocks_for((long long)n * xin.q[l]), 256, 0, st>>>(n, xin.q[l], xin.Q[l], wcol[l], Kc);
+        FC_CHECK_LAUNCH();
+      } else {
+        FC_CUDA_TRY(cudaMemcpyAsync(Kc, xin.Q[l], (size_t)n * xin.q[l] * 8, cudaMemcpyDeviceToDevice, st));
+      }
       const int kcap = std::min(n, xin.q[l]);
       double* Qn = s.alloc<double>((size_t)n * kcap);
       map[l] = pb.nb;
       pb.e[pb.nb++] = BcgsEntry{n, xin.q[l], Kc, n, Qn, n, kcap, kdev + l, s.alloc<double>(xin.q[l]),
-                                s.alloc<double>((size_t)kcap * kBcgsW), kBasisTol};
+                                s.alloc<double>((size_t)kcap * kBcgsW), wcol[l] ? wbasis_tol : kBasisTol};
       static const bool no_prefix = getenv("FC_NO_ORTH_PREFIX") != nullptr;   // diagnostic
       if (!no_prefix) pb.e[pb.nb - 1].k_base = std::min(xin.orth_prefix[l], kcap);
     }
@@ -1359,16 +1537,6 @@ TT truncate_tt(fc_ctx c, const TT& xin, double eps, int rank_cap, TruncStats* st
   }
   pm.mark(ss ? "1 basis (structured)" : "1 basis (cp)");
   // ---- 2. term norms n_l[t] = ||C_l[:, t]|| (orthonormal basis), xi_t, d_l[t] = xi_t/n_l[t] ----
-  double* n2[3];
-  double* dl[3];
-  double* inv[3];
-  for (int l = 0; l < 3; ++l) {
-    n2[l] = s.alloc<double>(R);
-    dl[l] = s.alloc<double>(R);
-    inv[l] = s.alloc<double>(R);
-  }
-  double* xi = s.alloc<double>(R);
-  double* energy = s.alloc<double>(4);
   if (!ss) {
     TermArgs ta;
     for (int l = 0; l < 3; ++l) {
@@ -1376,51 +1544,25 @@ TT truncate_tt(fc_ctx c, const TT& xin, double eps, int rank_cap, TruncStats* st
     }
     term_norms_kernel<<<dim3(cdiv(R, 8), 3), 256, 0, st>>>(R, ta);
     FC_CHECK_LAUNCH();
-  } else {
-    // n2[kk*Rx + j] = cx_j^T Gm_kk cx_j with Gm_kk = Rm_kk^T Rm_kk (t x t), P_kk = Gm_kk Cx,
-    // chunked over the spectral terms kk so that P stays below kStructChunk doubles per mode
-    const int r = ss->r, Rx = ss->Rx, kc = struct_chunk(ss);
+    term_weights();
+  } else if (!wbasis) {
+    // Gm_kk = Rm_kk^T Rm_kk (t x t): the term norms through the orthonormal basis
+    const int r = ss->r;
     GemmArgs gg;
     gg.transA = 1;
     gg.nbatch = 3;
     gg.rep = r;
     double* Gm[3];
-    double* P[3];
     for (int l = 0; l < 3; ++l) {
       const int t = ss->t[l], k = q[l];
       Gm[l] = s.alloc<double>((size_t)t * t * r);
-      P[l] = s.alloc<double>((size_t)t * Rx * kc);
       gg.b[l] = GemmBatch{t, t, k, RmE[l], k, RmE[l], k, Gm[l], t, nullptr, 0, nullptr};
       gg.b[l].sA = gg.b[l].sB = (long long)k * t;
       gg.b[l].sC = (long long)t * t;
     }
     gemm(gg, st);
-    for (int k0 = 0; k0 < r; k0 += kc) {
-      const int nk = std::min(kc, r - k0);
-      GemmArgs gp;
-      gp.nbatch = 3;
-      gp.rep = nk;
-      StructNormArgs na;
-      for (int l = 0; l < 3; ++l) {
-        const int t = ss->t[l];
-        gp.b[l] = GemmBatch{t, Rx, t, Gm[l] + (size_t)k0 * t * t, t, ss->Cx[l], t, P[l], t, nullptr, 0, nullptr};
-        gp.b[l].sA = (long long)t * t;
-        gp.b[l].sC = (long long)t * Rx;
-        na.Cx[l] = ss->Cx[l]; na.P[l] = P[l]; na.t[l] = t; na.n2[l] = n2[l] + (size_t)k0 * Rx;
-      }
-      gemm(gp, st);
-      struct_norms_kernel<<<dim3(cdiv(nk * Rx, 8), 3), 256, 0, st>>>(nk * Rx, Rx, na);
-      FC_CHECK_LAUNCH();
-    }
-  }
-  {
-    const int nbw = std::max(1, std::min(148, cdiv(R, 1024)));
-    double* part = s.alloc<double>(nbw);
-    term_weights_kernel<<<nbw, 1024, 0, st>>>(R, xin.w, n2[0], n2[1], n2[2], xi, dl[0], dl[1], dl[2], inv[0], inv[1],
-                                              inv[2], part);
-    FC_CHECK_LAUNCH();
-    sum_parts_kernel<<<1, 32, 0, st>>>(nbw, part, energy);
-    FC_CHECK_LAUNCH();
+    struct_norms(Gm);
+    term_weights();
   }
   pm.mark("2 term norms");
   // ---- 3. side matrix in the basis: B_l = C_l D_l (q x R); M_l = B_l B_l^T -------------
@@ -1431,32 +1573,11 @@ TT truncate_tt(fc_ctx c, const TT& xin, double eps, int rank_cap, TruncStats* st
     // M_l = sum_kk Rm_kk H_kk Rm_kk^T,  H_kk = W_kk W_kk^T,  W_kk = Cx diag(d_l[kk*Rx + .])
     // (t x t per spectral term, W chunked over kk): G_kk = Rm_kk H_kk, then
     // M = [G_1 .. G_r] [Rm_1 .. Rm_r]^T
-    const int r = ss->r, Rx = ss->Rx, kc = struct_chunk(ss);
-    double* W[3];
-    double* H[3];
+    const int r = ss->r;
+    if (!wbasis) struct_side_grams();
+    double* const* H = Hs;
     double* G[3];
-    for (int l = 0; l < 3; ++l) {
-      W[l] = s.alloc<double>((size_t)ss->t[l] * Rx * kc);
-      H[l] = s.alloc<double>((size_t)ss->t[l] * ss->t[l] * r);
-      G[l] = s.alloc<double>((size_t)q[l] * ss->t[l] * r);
-    }
-    for (int k0 = 0; k0 < r; k0 += kc) {
-      const int nk = std::min(kc, r - k0);
-      GemmArgs gh;
-      gh.transB = 1;
-      gh.nbatch = 3;
-      gh.rep = nk;
-      for (int l = 0; l < 3; ++l) {
-        const int t = ss->t[l];
-        struct_scale_kernel<<<blocks_for((long long)t * Rx * nk), 256, 0, st>>>(t, nk * Rx, Rx, ss->Cx[l],
-                                                                                 dl[l] + (size_t)k0 * Rx, W[l]);
-        FC_CHECK_LAUNCH();
-        gh.b[l] = GemmBatch{t, t, Rx, W[l], t, W[l], t, H[l] + (size_t)k0 * t * t, t, nullptr, 0, nullptr};
-        gh.b[l].sA = gh.b[l].sB = (long long)t * Rx;
-        gh.b[l].sC = (long long)t * t;
-      }
-      gemm(gh, st);
-    }
+    for (int l = 0; l < 3; ++l) G[l] = s.alloc<double>((size_t)q[l] * ss->t[l] * r);
     GemmArgs gq, m;
     m.transB = 1;
     gq.nbatch = m.nbatch = 3;
