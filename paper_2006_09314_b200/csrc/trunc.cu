@@ -445,7 +445,9 @@ __global__ void extract_slices_kernel(const double* __restrict__ core, int r0, i
 // Slices whose working set exceeds the shared-memory budget run the same algorithm in a
 // per-slice global (L2-resident) workspace `gws` of (rows*cols + cols*cols) doubles.
 constexpr int kSliceMax = 1024;
+constexpr double kJacobiQuad = 1e-8;   // see slice_svd_qrj_kernel
 __device__ int g_slice_sweeps_max = 0;   // diagnostics (FC_TRACE): most Jacobi sweeps of a slice
+__device__ unsigned long long g_slice_cyc[4] = {0, 0, 0, 0};   // ... slice 0's cycles in QR / X setup / Jacobi / outputs
 constexpr size_t kSliceSmem = 200 * 1024;
 // SMEM: the working set lives in shared memory (the compiler then emits LDS/STS; with a pointer
 // that may be global it emits generic loads); else in the per-slice global workspace gws.
@@ -608,7 +610,8 @@ size_t slice_qrj_smem(int rows, int cols) {
 // truncation's ~126 x 126 cores); the small arrays stay in shared memory.
 template <bool SMEM>
 __global__ void __launch_bounds__(1024) slice_svd_qrj_kernel(int ra, int rb, const double* __restrict__ S,
-                                                            double* s_out, double* Ua, double* Vb, double* gws) {
+                                                            double* s_out, double* Ua, double* Vb, double* gws,
+                                                            double jacobi_quad) {
   extern __shared__ double sm[];
   const int nu = blockIdx.x;
   const bool tr = ra < rb;
@@ -627,7 +630,7 @@ __global__ void __launch_bounds__(1024) slice_svd_qrj_kernel(int ra, int rb, con
   int* order = perm + cols;                         // cols
   __shared__ int piv_s;
   __shared__ double sval;
-  __shared__ int changed;
+  __shared__ int changed, big;
   const double* src = S + (size_t)nu * ra * rb;
   const int tid = threadIdx.x, nt = blockDim.x, warp = tid >> 5, ln = tid & 31, nw = nt >> 5;
   for (int idx = tid; idx < rows * cols; idx += nt) {
@@ -637,6 +640,8 @@ __global__ void __launch_bounds__(1024) slice_svd_qrj_kernel(int ra, int rb, con
   for (int j = tid; j < cols; j += nt) perm[j] = j;
   __syncthreads();
   double fro2 = 0.0;
+  const bool timing = (nu == 0 && tid == 0);
+  long long tc0 = timing ? clock64() : 0;
   // ---- Householder QR with column pivoting ----
   // trailing column norms: exact sums over rows >= i; computed once here and then accumulated in
   // the same pass (and order) that applies each reflector
@@ -725,6 +730,7 @@ __global__ void __launch_bounds__(1024) slice_svd_qrj_kernel(int ra, int rb, con
     }
     __syncthreads();
   }
+  if (timing) { const long long t = clock64(); atomicAdd(&g_slice_cyc[0], (unsigned long long)(t - tc0)); tc0 = t; }
   // X = R^T (cols x cols, lower triangular), W = I
   for (int idx = tid; idx < cols * cols; idx += nt) {
     const int r = idx % cols, c = idx / cols;    // X[r, c] = R[c, r]
@@ -732,15 +738,20 @@ __global__ void __launch_bounds__(1024) slice_svd_qrj_kernel(int ra, int rb, con
     W[r + c * lx] = (r == c) ? 1.0 : 0.0;
   }
   __syncthreads();
+  if (timing) { const long long t = clock64(); atomicAdd(&g_slice_cyc[1], (unsigned long long)(t - tc0)); tc0 = t; }
   // ---- one-sided Jacobi on the columns of X ----
   const double neg2 = 1e-24 * fro2;
   const int p = cols + (cols & 1);
   const double tol = 2.0 * sqrt((double)cols) * 2.220446049250313e-16, tol2 = tol * tol;
+  const double quad2 = jacobi_quad * jacobi_quad;
   int G = 32;
   while (G > 4 && nt / G < p / 2) G >>= 1;
   const int gid = tid / G, gl = tid % G, ng = nt / G;
+  // A sweep whose rotations all had cosines <= kJacobiQuad leaves cosines of their square's order
+  // (quadratic convergence of the cyclic method): it is the last one, the all-quiet confirming
+  // sweep is not run.
   for (int sweep = 0; sweep < 40; ++sweep) {
-    if (tid == 0) changed = 0;
+    if (tid == 0) changed = big = 0;
     __syncthreads();
     for (int rd = 0; rd < p - 1; ++rd) {
       for (int pi0 = 0; pi0 < p / 2; pi0 += ng) {
@@ -748,8 +759,12 @@ __global__ void __launch_bounds__(1024) slice_svd_qrj_kernel(int ra, int rb, con
         int a = 0, b = 0;
         bool act = pi < p / 2;
         if (act) {
-          if (pi == 0) { a = rd % (p - 1); b = p - 1; }
-          else { a = (rd + pi) % (p - 1); b = (rd - pi + p - 1) % (p - 1); }
+          // round-robin pairing; rd, pi < p - 1: one conditional subtraction replaces the modulo
+          if (pi == 0) { a = rd; b = p - 1; }
+          else {
+            a = rd + pi; if (a >= p - 1) a -= p - 1;
+            b = rd - pi; if (b < 0) b += p - 1;
+          }
           if (a > b) { int t = a; a = b; b = t; }
           act = b < cols;
         }
@@ -777,16 +792,20 @@ __global__ void __launch_bounds__(1024) slice_svd_qrj_kernel(int ra, int rb, con
           W[i + a * lx] = c * x - sn * y;
           W[i + b * lx] = sn * x + c * y;
         }
-        if (gl == 0) changed = 1;
+        if (gl == 0) {
+          changed = 1;
+          if (ga * ga > quad2 * (al * be)) big = 1;
+        }
       }
       __syncthreads();
     }
-    if (!changed) {
+    if (!changed || !big) {
       if (tid == 0) atomicMax(&g_slice_sweeps_max, sweep + 1);
       break;
     }
     __syncthreads();
   }
+  if (timing) { const long long t = clock64(); atomicAdd(&g_slice_cyc[2], (unsigned long long)(t - tc0)); tc0 = t; }
   // singular values, order
   for (int j = warp; j < cols; j += nw) {
     double s2 = 0;
@@ -867,6 +886,7 @@ __global__ void __launch_bounds__(1024) slice_svd_qrj_kernel(int ra, int rb, con
     else Vb[(size_t)nu * rb * k + (size_t)m * rb + perm[i]] = v;
   }
   for (int m = tid; m < k; m += nt) s_out[(size_t)nu * k + m] = cn[order[m]];
+  if (timing) atomicAdd(&g_slice_cyc[3], (unsigned long long)(clock64() - tc0));
 }
 
 // pool all (s, nu, m), sort by s desc, ties (nu, m) asc: rank of each element by counting
@@ -1155,13 +1175,15 @@ void small_svd(cudaStream_t st, int ra, int rb, int ns, const double* S, double*
                                      (int)kSliceSmem));
     qattr = true;
   }
+  // FC_JACOBI_QUAD: cosine level below which a sweep is taken as the last (0: always confirm)
+  static const double jquad = getenv("FC_JACOBI_QUAD") ? atof(getenv("FC_JACOBI_QUAD")) : kJacobiQuad;
   if (!no_qr && qsm <= kSliceSmem) {
-    slice_svd_qrj_kernel<true><<<ns, sthr, qsm, st>>>(ra, rb, S, sv, Ua, Vb, nullptr);
+    slice_svd_qrj_kernel<true><<<ns, sthr, qsm, st>>>(ra, rb, S, sv, Ua, Vb, nullptr, jquad);
   } else if (!no_qr) {
     // QR-preconditioned Jacobi with the matrices in an L2-resident global workspace
     double* qws = s.alloc<double>((size_t)ns * ((size_t)rows * cols + 2 * (size_t)(cols | 1) * cols));
     const size_t small = (5 * (size_t)cols) * 8 + 64;
-    slice_svd_qrj_kernel<false><<<ns, sthr, small, st>>>(ra, rb, S, sv, Ua, Vb, qws);
+    slice_svd_qrj_kernel<false><<<ns, sthr, small, st>>>(ra, rb, S, sv, Ua, Vb, qws, jquad);
   } else if (gws) {
     slice_svd_kernel<false><<<ns, 512, smem, st>>>(ra, rb, S, sv, Ua, Vb, gws);
   } else {
@@ -1173,7 +1195,11 @@ void small_svd(cudaStream_t st, int ra, int rb, int ns, const double* S, double*
     FC_CUDA_TRY(cudaMemcpyFromSymbolAsync(&sw, g_slice_sweeps_max, sizeof(int), 0, cudaMemcpyDeviceToHost, st));
     FC_CUDA_TRY(cudaMemcpyToSymbolAsync(g_slice_sweeps_max, &zero, sizeof(int), 0, cudaMemcpyHostToDevice, st));
     FC_CUDA_TRY(cudaStreamSynchronize(st));
-    fprintf(stderr, "[fc svd] %d matrices of %d x %d: max sweeps %d\n", ns, ra, rb, sw);
+    unsigned long long cy[4], zc[4] = {0, 0, 0, 0};
+    FC_CUDA_TRY(cudaMemcpyFromSymbol(cy, g_slice_cyc, sizeof(cy)));
+    FC_CUDA_TRY(cudaMemcpyToSymbol(g_slice_cyc, zc, sizeof(zc)));
+    fprintf(stderr, "[fc svd] %d matrices of %d x %d: max sweeps %d; slice 0 kcycles: QR %.0f, X %.0f, Jacobi %.0f, out %.0f\n",
+            ns, ra, rb, sw, cy[0] * 1e-3, cy[1] * 1e-3, cy[2] * 1e-3, cy[3] * 1e-3);
   }
 }
 

@@ -32,7 +32,7 @@ def _graded_psd(N, seed, decay=16.0):
 
 
 @pytest.mark.parametrize("sizes", [[200, 400, 700], [231, 600, 601, 840], [1000], [17, 841], [96, 97, 440, 441],
-                                   [1400, 900], [1500]])
+                                   [1400, 900], [1500], [3, 4, 5, 31, 32, 33, 64, 65], [100, 150, 215, 216, 217]])
 def test_syev_paths(lib, sizes):
     """fc_syev (the truncation's Gram eigensolver) on every tridiagonalisation path: packed
     shared memory (N <= 96), 16-CTA cluster (97..840; FC_TRI_CS=8 / 4: 8-CTA up to 600 / 4-CTA

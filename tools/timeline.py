@@ -72,6 +72,20 @@ def main():
     print(f"sum of kernel durations {tot/1e3:.2f} ms")
     for k, (t, c) in sorted(agg.items(), key=lambda kv: -kv[1][0])[:45]:
         print(f"{100*t/tot:6.2f}% {t/1e3:8.2f} ms {c:6d}  {t/max(c,1):8.1f} us/launch  {k}")
+    # duration distribution of the GEMM launches (many skinny projections vs few long contractions)
+    edges = [5, 10, 15, 20, 30, 50, 100, 200, 500, 1e9]
+    dist = [[0, 0.0] for _ in edges]
+    for s, e, nm in ks:
+        if "dgemm_dmma_kernel" not in nm:
+            continue
+        d = e - s
+        for i, hi in enumerate(edges):
+            if d < hi:
+                dist[i][0] += 1
+                dist[i][1] += d
+                break
+    print("dgemm_dmma_kernel durations (us bucket upper edge: launches, total ms):",
+          {("%g" % hi): (c, round(t / 1e3, 2)) for hi, (c, t) in zip(edges, dist)})
     hist = collections.Counter()
     for g in gaps:
         hist[min(int(g // 5) * 5, 100)] += 1
