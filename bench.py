@@ -446,7 +446,7 @@ def apply_roofline(ctx, L, n, R=64, r=16, reps=10):
     ach = st["flops"] / (t * 1e-3) / 1e12
     peak_hbm, _ = hbm_peak()
     kr_gbs = kp["bytes"] / (kp["ms"] * 1e-3) / 1e9 if kp["ms"] > 0 else 0.0
-    return {"kernel": "dgemm_big_kernel (inverse mode transform Y_l = V_l Yhat_l, S7; Yhat = u_F (.) V^T x by kr_product_kernel, K6)",
+    return {"kernel": "dgemm_big_streamk_kernel (inverse mode transform Y_l = V_l Yhat_l, S7, stream-K over the SMs; Yhat = u_F (.) V^T x by kr_product_kernel, K6)",
             "cell": {"n": n, "R": R, "r": r}, "bound": "tensor", "achieved": ach,
             "peak": FP64_DMMA_TFLOPS, "unit": "TFLOP/s", "frac": ach / FP64_DMMA_TFLOPS,
             "peak_source": "measured DMMA m8n8k4 FP64 peak (tools/peak_fp64.cu); MEASURED_PEAKS.json has no FP64 entry",
@@ -459,9 +459,9 @@ def apply_roofline(ctx, L, n, R=64, r=16, reps=10):
 
 def kr_traffic(n, R, r):
     """DRAM bytes (read + write) of one inverse-transform launch at this C5 cell, from the committed
-    `ncu --set full` capture of the current kernel (profiles/r02_inv_traffic.json), or None."""
+    `ncu --set full` capture of the current kernel (profiles/r02c_inv_traffic.json), or None."""
     try:
-        d = json.load(open(os.path.join(ROOT, "profiles", "r02_inv_traffic.json")))
+        d = json.load(open(os.path.join(ROOT, "profiles", "r02c_inv_traffic.json")))
     except (OSError, ValueError):
         return None
     if (d.get("n"), d.get("R"), d.get("r")) != (n, R, r):

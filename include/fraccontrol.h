@@ -268,6 +268,14 @@ int fc_dgemm(fc_ctx ctx, int transA, int transB, int M, int N, int K, double alp
 int fc_dgemm_splitk(fc_ctx ctx, int transA, int transB, int M, int N, int K, double alpha,
                     const double* A, int lda, const double* B, int ldb, double beta, double* C, int ldc,
                     int splitk);
+/* fc_dgemm with the stream-K request the inverse mode transform of fracop_apply makes [P:597-628:
+ * Y_l = V_l Yhat_l, the dense contraction of the factored matvec]: when M, N >= 128, K >= 64,
+ * 2 M N K >= 2^28 and the launch has >= 8 k-steps of 16 per SM, one persistent CTA per SM gets an equal contiguous range of the launch's
+ * (tile, k-step) iterations; partial tiles go through a device workspace and are added by the
+ * tile's owner CTA in CTA order (bit-identical run to run).  Otherwise identical to fc_dgemm.
+ * Same arguments, layout and errors as fc_dgemm. */
+int fc_dgemm_streamk(fc_ctx ctx, int transA, int transB, int M, int N, int K, double alpha,
+                     const double* A, int lda, const double* B, int ldb, double beta, double* C, int ldc);
 /* Milliseconds of the last launch of the dominant kernel of the last API call (events on
  * the context stream) and its algorithmic flop and byte counts (for the roofline line). */
 int fc_last_kernel_stats(fc_ctx ctx, double* ms, double* flops, double* bytes, int* launches);

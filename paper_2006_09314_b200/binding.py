@@ -75,7 +75,7 @@ class FCError(RuntimeError):
 ENTRY_POINTS = ["fc_create", "fc_destroy", "fc_last_error", "fc_set_stream", "sl_setup", "sl_get_eigen",
                 "sl_set_eigen", "op_get_spectral_cp", "op_set_spectral_cp", "op_spectral_rank",
                 "fracop_apply", "precond_apply", "cp_dot", "cp_axpy", "cp_truncate", "pcg_solve",
-                "fc_dgemm", "fc_dgemm_splitk", "fc_last_kernel_stats", "fc_kernel_launches", "fracop_apply_truncate", "fc_orthonormalize",
+                "fc_dgemm", "fc_dgemm_splitk", "fc_dgemm_streamk", "fc_last_kernel_stats", "fc_kernel_launches", "fracop_apply_truncate", "fc_orthonormalize",
                 "fc_profile_gemm", "fc_profile_kernel", "fc_syev", "op_get_precond_basis", "op_set_precond_basis", "state_recover", "op_build_spectral_sinc",
                 "sl_setup_2d", "op_get_spectral_2d", "op_set_spectral_2d", "fracop_apply_2d", "cp_dot_2d",
                 "cp_truncate_2d", "pcg_solve_2d", "cp_truncate_als"]
@@ -103,6 +103,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "pcg_solve": ([P, cpp, C.POINTER(fc_params), cpp, C.POINTER(fc_pcg_report)], I),
         "fc_dgemm": ([P, I, I, I, I, I, D, P, I, P, I, D, P, I], I),
         "fc_dgemm_splitk": ([P, I, I, I, I, I, D, P, I, P, I, D, P, I, I], I),
+        "fc_dgemm_streamk": ([P, I, I, I, I, I, D, P, I, P, I, D, P, I], I),
         "fc_last_kernel_stats": ([P, C.POINTER(D), C.POINTER(D), C.POINTER(D), C.POINTER(I)], I),
         "fc_kernel_launches": ([C.POINTER(C.c_longlong)], I),
         "fc_orthonormalize": ([P, I, I, P, P, D, C.POINTER(I)], I),
@@ -501,8 +502,11 @@ class Context:
                                      IA(*Ns), IA(*rs)))
         return [(lam, Y[:r]) for lam, Y, r in zip(lams, Ys, rs)]
 
-    def dgemm(self, transA, transB, M, N, K, alpha, A, lda, B, ldb, beta, Cm, ldc, splitk=None):
-        if splitk is None:
+    def dgemm(self, transA, transB, M, N, K, alpha, A, lda, B, ldb, beta, Cm, ldc, splitk=None, streamk=False):
+        if streamk:
+            self._check(self.lib.fc_dgemm_streamk(self.h, transA, transB, M, N, K, alpha, A.data_ptr(), lda,
+                                                  B.data_ptr(), ldb, beta, Cm.data_ptr(), ldc))
+        elif splitk is None:
             self._check(self.lib.fc_dgemm(self.h, transA, transB, M, N, K, alpha, A.data_ptr(), lda,
                                           B.data_ptr(), ldb, beta, Cm.data_ptr(), ldc))
         else:

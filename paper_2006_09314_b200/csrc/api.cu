@@ -63,6 +63,7 @@ void apply_plain(fc_ctx c, const SpecCP& sp, const fc_cp& x, fc_cp& y) {
   f.nbatch = 3;
   for (int l = 0; l < 3; ++l)
     f.b[l] = GemmBatch{n, R, n, c->Vsp(sp, l), n, x.U[l], x.ld[l], What + (size_t)l * n * R, n, nullptr, 0, nullptr};
+  f.streamk = 1;   // R >= 128: k-step-balanced 128 x 128 tiles (gemm.cu); below, the 64 x 64 kernel
   gemm(f, st);
 
   // S8 (moved ahead): column norms of u_k (.) w_j; ||V y|| = ||y|| since V is orthogonal
@@ -118,6 +119,7 @@ void apply_plain(fc_ctx c, const SpecCP& sp, const fc_cp& x, fc_cp& y) {
   static const int sk_env = getenv("FC_APPLY_SPLITK") ? atoi(getenv("FC_APPLY_SPLITK")) : 0;   // diagnostic
   if (sk_env > 0) sk = sk_env;
   iv.splitk = sk;   // deterministic split-K reduction: C needs no pre-zeroing (beta = 0)
+  iv.streamk = 1;   // ... or, when whole tiles fill the last wave badly, k-step-balanced (stream-K)
   FC_CUDA_TRY(cudaEventRecord(c->e0, st));
   gemm(iv, st);
   FC_CUDA_TRY(cudaEventRecord(c->e1, st));
@@ -543,6 +545,28 @@ int fc_dgemm(fc_ctx c, int transA, int transB, int M, int N, int K, double alpha
     require(M >= 0 && N >= 0 && K >= 0, FC_ERR_INVALID_ARG, "dims");
     FC_CUDA_TRY(cudaEventRecord(c->e0, c->st));
     dgemm(c->st, transA, transB, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+    FC_CUDA_TRY(cudaEventRecord(c->e1, c->st));
+    c->k_flops = 2.0 * M * (double)N * K;
+    c->k_bytes = 8.0 * ((double)M * K + (double)K * N + (double)M * N * (beta != 0 ? 2 : 1));
+    c->k_launches = 1;
+    return FC_OK;
+  });
+}
+
+int fc_dgemm_streamk(fc_ctx c, int transA, int transB, int M, int N, int K, double alpha, const double* A, int lda,
+                     const double* B, int ldb, double beta, double* C, int ldc) {
+  return guard(c, [&]() {
+    require(M >= 0 && N >= 0 && K >= 0, FC_ERR_INVALID_ARG, "dims");
+    GemmArgs a;
+    a.transA = transA;
+    a.transB = transB;
+    a.alpha = alpha;
+    a.beta = beta;
+    a.streamk = 1;
+    a.nbatch = 1;
+    a.b[0] = GemmBatch{M, N, K, A, lda, B, ldb, C, ldc, nullptr, 0, nullptr};
+    FC_CUDA_TRY(cudaEventRecord(c->e0, c->st));
+    gemm(a, c->st);
     FC_CUDA_TRY(cudaEventRecord(c->e1, c->st));
     c->k_flops = 2.0 * M * (double)N * K;
     c->k_bytes = 8.0 * ((double)M * K + (double)K * N + (double)M * N * (beta != 0 ? 2 : 1));

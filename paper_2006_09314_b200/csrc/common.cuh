@@ -146,7 +146,10 @@ struct GemmArgs {
   int rep = 1;           // every entry is repeated rep times with its strides (strided batch)
   GemmBatch b[kMaxBatch];
   // set by the dispatcher (gemm.cu): split-K reduction mode and its workspace
-  int kmode = 0;             // 0 direct, 1 cluster (DSMEM), 2 workspace
+  // request (caller): balance the 128x128-tile kernel's work over the SMs by k-steps instead of
+  // whole tiles (stream-K, gemm.cu) when the tile count leaves the last wave mostly empty
+  int streamk = 0;
+  int kmode = 0;             // 0 direct, 1 cluster (DSMEM), 2 workspace, 3 stream-K
   double* ws = nullptr;      // kmode 2: partial tiles
   int* cnt = nullptr;        // kmode 2: per-tile arrival counters (self-resetting)
 };

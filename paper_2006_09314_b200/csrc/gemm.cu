@@ -554,6 +554,151 @@ __global__ void __launch_bounds__(NT, 1) dgemm_big_kernel(const __grid_constant_
   tile_epilogue<NT, 4>(acc, args, g, ri, m0, n0, ks, tile, smem);
 }
 
+// Stream-K variant of the 128x128 kernel (kmode 3): one persistent CTA per SM; the launch's
+// (tile, k-step) iterations — tiles in (entry, rep, n-tile, m-tile) order, K / 16 steps each,
+// all entries of one shape — are cut into gridDim.x equal contiguous ranges, so every SM gets
+// the same number of k-steps whatever the tile count (192 tiles on 148 SMs: 83 steps per CTA
+// instead of two waves of 64).  A range that starts inside a tile produces a partial tile:
+// written to the CTA's workspace slot and published through its flag.  The CTA whose range holds
+// the tile's first k-step owns the tile: it adds the partials of the following CTAs in CTA order
+// (a fixed order: bit-identical run to run), resets their flags and runs the usual epilogue.
+// A CTA's partial is the FIRST thing it computes and its wait comes LAST, and it only ever waits
+// for CTAs with a higher index, so with any two CTAs resident the chain unwinds: no deadlock.
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+  asm volatile("st.release.gpu.global.s32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
+
+template <int TA, int TB>
+__global__ void __launch_bounds__(NT, 1) dgemm_big_streamk_kernel(const __grid_constant__ GemmArgs args) {
+  extern __shared__ __align__(16) double smem[];
+  double* As = smem;
+  double* Bs = smem + STAGES * TILE;
+  const GemmBatch& g0 = args.b[0];
+  const int tm = (g0.M + BM - 1) / BM, tn = (g0.N + BN - 1) / BN;
+  const int kiters = (g0.K + BK - 1) / BK;
+  const long long ntiles = (long long)args.nbatch * args.rep * tm * tn;
+  const long long total = ntiles * kiters;
+  const int P = gridDim.x, cta = blockIdx.x;
+  auto range_begin = [&](int b) { return total * b / P; };
+  long long it = range_begin(cta);
+  const long long it1 = range_begin(cta + 1);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = (warp & 3) * 32, wn = (warp >> 2) * 32;
+  const int fr = lane >> 2, fc4 = lane & 3;
+  constexpr bool AK = TA == 1;    // A contiguous along k
+  constexpr bool BKc = TB == 0;   // B contiguous along k
+  while (it < it1) {
+    const long long t = it / kiters;
+    const int kb = (int)(it - t * kiters);
+    const int ke = (int)min((long long)kiters, kb + (it1 - it));
+    const int mt = (int)(t % tm), nt_ = (int)((t / tm) % tn);
+    const int bi = (int)(t / ((long long)tm * tn));
+    const int ei = bi / args.rep, ri = bi - ei * args.rep;
+    const GemmBatch& g = args.b[ei];
+    const double* gA = g.A + (size_t)ri * g.sA;
+    const double* gB = g.B + (size_t)ri * g.sB;
+    const int m0 = mt * BM, n0 = nt_ * BN;
+    const int kbeg = kb * BK, kend = min(g.K, ke * BK);
+    const int nk = ke - kb;
+    const bool vecA = ((g.lda & 1) == 0) && (((uintptr_t)gA & 15) == 0);
+    const bool vecB = ((g.ldb & 1) == 0) && (((uintptr_t)gB & 15) == 0);
+    double acc[4][4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    auto issue = [&](int s, int kt) {
+      const int k0 = kbeg + kt * BK;
+      load_op<AK>(As + s * TILE, gA, g.lda, m0, g.M, k0, kend, tid, vecA);
+      load_op<BKc>(Bs + s * TILE, gB, g.ldb, n0, g.N, k0, kend, tid, vecB);
+    };
+#pragma unroll
+    for (int s = 0; s < STAGES - 1; ++s) {
+      if (s < nk) issue(s, s);
+      cp_async_commit();
+    }
+    for (int kt = 0; kt < nk; ++kt) {
+      cp_async_wait<STAGES - 2>();
+      __syncthreads();
+      {
+        const int nx = kt + STAGES - 1;
+        if (nx < nk) issue(nx % STAGES, nx);
+        cp_async_commit();
+      }
+      const int st = kt % STAGES;
+      const double* a_s = As + st * TILE;
+      const double* b_s = Bs + st * TILE;
+#pragma unroll
+      for (int kq = 0; kq < BK; kq += 4) {
+        double af[4], bf[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int m = wm + i * 8 + fr, k = kq + fc4;
+          af[i] = AK ? a_s[m * LDM + k] : a_s[k * LDK + m];
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int nn = wn + j * 8 + fr, k = kq + fc4;
+          bf[j] = BKc ? b_s[nn * LDM + k] : b_s[k * LDK + nn];
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+      }
+    }
+    cp_async_wait<0>();
+    __syncthreads();   // every warp is done with the ring before the next segment refills it
+    if (kb != 0) {
+      // partial tile (the range started inside the tile): slot layout [s][tid], coalesced
+      double* wp = args.ws + (size_t)cta * 32 * NT;
+#pragma unroll
+      for (int s = 0; s < 32; ++s) __stcg(wp + s * NT + tid, acc[s >> 3][(s >> 1) & 3][s & 1]);
+      __threadfence();
+      __syncthreads();
+      if (tid == 0) st_release(args.cnt + cta, 1);
+    } else {
+      // owner: the following CTAs hold the rest of the tile's k-steps, one partial each
+      int covered = ke;
+      for (int c = cta + 1; covered < kiters; ++c) {
+        if (tid == 0)
+          while (ld_acquire(args.cnt + c) == 0) __nanosleep(64);
+        __syncthreads();
+        const double* wp = args.ws + (size_t)c * 32 * NT;
+#pragma unroll
+        for (int s = 0; s < 32; ++s) acc[s >> 3][(s >> 1) & 3][s & 1] += __ldcg(wp + s * NT + tid);
+        __syncthreads();
+        if (tid == 0) args.cnt[c] = 0;   // consumed: ready for the next launch on this stream
+        covered += (int)(min(range_begin(c + 1), (t + 1) * kiters) - range_begin(c));
+      }
+#pragma unroll
+      for (int s = 0; s < 32; ++s) {
+        int r, c;
+        slot_rc<4>(tid, s, r, c);
+        put_elem(args, g, ri, m0 + r, n0 + c, acc[s >> 3][(s >> 1) & 3][s & 1]);
+      }
+    }
+    it += nk;
+  }
+}
+
+template <int TA, int TB>
+void launch_big_streamk(const GemmArgs& a, int ctas, cudaStream_t st) {
+  const int smem = 2 * STAGES * TILE * (int)sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    FC_CUDA_TRY(cudaFuncSetAttribute(dgemm_big_streamk_kernel<TA, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr = true;
+  }
+  dgemm_big_streamk_kernel<TA, TB><<<ctas, NT, smem, st>>>(a);
+  FC_CHECK_LAUNCH();
+}
+
 template <int TA, int TB, bool KR>
 void launch_big(const GemmArgs& a, dim3 grid, cudaStream_t st) {
   const int smem = std::max((KR ? 3 : 2) * STAGES * TILE, RED) * (int)sizeof(double);
@@ -728,6 +873,35 @@ static void gemm_dispatch(const GemmArgs& a_in, cudaStream_t st) {
   bool dyn = false;
   for (int i = 0; i < a.nbatch; ++i) dyn |= a.b[i].dynM != nullptr || a.b[i].dynK != nullptr;
   a.splitk = std::max(1, a.splitk);
+  // stream-K (on request; FC_STREAMK=0 disables): same-shape entries on 128 x 128 tiles with at
+  // least 8 k-steps per SM.  It beat whole-tile launches on every C5 cell it accepts, also where
+  // the tiles fill their waves (n = 2048, R r = 8192: 76.5 -> 81.6 % of the DMMA peak; no launch
+  // tail, the fix-up of one tile overlaps the other CTAs' main loops)
+  if (!dyn && a.gen.kind < 0 && a.krR == 0 && a.streamk && maxM >= 128 && maxN >= 128 && minK >= 64 &&
+      work >= (1LL << 27)) {
+    static const bool sk_on = !(getenv("FC_STREAMK") && atoi(getenv("FC_STREAMK")) == 0);
+    static const int sms = [] {
+      int dev = 0, v = 148;
+      if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+      return std::max(v, 2);
+    }();
+    static const int min_it = getenv("FC_STREAMK_MINIT") ? atoi(getenv("FC_STREAMK_MINIT")) : 8;   // diagnostic
+    bool same = true;
+    for (int i = 1; i < a.nbatch; ++i)
+      same &= a.b[i].M == a.b[0].M && a.b[i].N == a.b[0].N && a.b[i].K == a.b[0].K;
+    const long long tiles = (long long)a.nbatch * a.rep * cdiv(maxM, big::BM) * cdiv(maxN, big::BN);
+    const long long kit = cdiv(a.b[0].K, big::BK);
+    if (sk_on && same && tiles * kit >= (long long)min_it * sms) {
+      a.splitk = 1;
+      a.kmode = 3;
+      split_workspace(st, (size_t)sms * 32 * big::NT, (size_t)sms, &a.ws, &a.cnt);
+      if (!a.transA && !a.transB) big::launch_big_streamk<0, 0>(a, sms, st);
+      else if (a.transA && !a.transB) big::launch_big_streamk<1, 0>(a, sms, st);
+      else if (!a.transA && a.transB) big::launch_big_streamk<0, 1>(a, sms, st);
+      else big::launch_big_streamk<1, 1>(a, sms, st);
+      return;
+    }
+  }
   if (!dyn && a.gen.kind < 0 && maxM >= 256 && maxN >= 256 && minK >= 64 && work >= (1LL << 27)) {
     a.splitk = std::min(a.splitk, kBigClusterSplit);   // big tiles: cluster reduction only
     dim3 grid(cdiv(maxM, big::BM), cdiv(maxN, big::BN), a.nbatch * a.rep * a.splitk);

@@ -92,6 +92,46 @@ def test_dgemm_splitk_deterministic(lib, tA, tB, M, N, K, splitk):
     assert np.max(np.abs(Ct.cpu().numpy().T - ref2)) <= 1e-13 * max(1.0, np.max(np.abs(ref2))) * np.sqrt(K)
 
 
+@pytest.mark.parametrize("tA,tB,M,N,K", [
+    (0, 0, 1500, 1270, 1000),    # 120 tiles on 148 SMs, ragged edges, K not a multiple of 16
+    (1, 0, 1024, 3072, 1024),    # 192 tiles: the C5 cell n = 1024, R r = 1024 (three modes' worth)
+    (0, 1, 2000, 1300, 700), (1, 1, 1100, 1900, 1500),
+    (0, 0, 3000, 2600, 400)])    # 504 tiles: 3.4 waves, contributors and owners in every CTA
+def test_dgemm_streamk_deterministic(lib, tA, tB, M, N, K):
+    """Stream-K 128 x 128 GEMM (the inverse mode transform's balance over the SMs): matches NumPy
+    to the FP64 accumulation bound, two launches are bit-identical (partials added in CTA order),
+    beta = 0 never reads C (NaN-filled), beta != 0 accumulates; a plain launch in between checks
+    that the flags and the workspace are left clean."""
+    import torch
+    ctx = lib.context()
+    rng = np.random.default_rng(M * 7 + N)
+    A = rng.standard_normal((K, M) if tA == 0 else (M, K))
+    B = rng.standard_normal((N, K) if tB == 0 else (K, N))
+    At, Bt = (torch.tensor(v, device="cuda") for v in (A, B))
+    opA = A.T if tA == 0 else A
+    opB = B.T if tB == 0 else B
+    ref = opA @ opB
+    tol = 1e-13 * max(1.0, np.max(np.abs(ref))) * np.sqrt(K)
+    outs = []
+    for rep in range(3):
+        Ct = torch.full((N, M), float("nan"), dtype=torch.float64, device="cuda")
+        ctx.dgemm(tA, tB, M, N, K, 1.0, At, A.shape[1], Bt, B.shape[1], 0.0, Ct, M, streamk=True)
+        outs.append(Ct.cpu().numpy().T)
+        if rep == 0:   # a workspace split-K launch on the same stream shares the counters
+            Xs = torch.tensor(rng.standard_normal((4000, 90)), device="cuda")   # col-major 90 x 4000
+            Cs = torch.full((90, 90), float("nan"), dtype=torch.float64, device="cuda")
+            ctx.dgemm(0, 1, 90, 90, 4000, 1.0, Xs, 90, Xs, 90, 0.0, Cs, 90, splitk=32)
+            Xh = Xs.cpu().numpy().T
+            assert np.max(np.abs(Cs.cpu().numpy().T - Xh @ Xh.T)) <= 1e-11
+    assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
+    assert np.max(np.abs(outs[0] - ref)) <= tol
+    Cm = rng.standard_normal((N, M))
+    Ct = torch.tensor(Cm, device="cuda")
+    ctx.dgemm(tA, tB, M, N, K, 0.5, At, A.shape[1], Bt, B.shape[1], 0.25, Ct, M, streamk=True)
+    ref2 = 0.5 * ref + 0.25 * Cm.T
+    assert np.max(np.abs(Ct.cpu().numpy().T - ref2)) <= 1e-13 * max(1.0, np.max(np.abs(ref2))) * np.sqrt(K)
+
+
 @pytest.mark.parametrize("n,R", [(32, 5), (37, 1), (64, 13)])
 def test_fracop_apply_parity(lib, n, R):
     from paper_2006_09314_b200.binding import DeviceCP, FC_F, FC_G
