@@ -305,7 +305,7 @@ def main():
     ach = gp["flops"] / (gp["ms"] * 1e-3) / 1e12 if gp["ms"] > 0 else 0.0
     roof = {"kernel": "dgemm_dmma_kernel / dgemm_big_kernel (all DMMA GEMM launches of one pcg_solve)",
             "bound": "tensor", "achieved": ach, "peak": FP64_DMMA_TFLOPS, "unit": "TFLOP/s",
-            "frac": ach / FP64_DMMA_TFLOPS, "traffic": None,
+            "frac": ach / FP64_DMMA_TFLOPS, "traffic": gemm_class_traffic(),
             "peak_source": "measured DMMA m8n8k4 FP64 peak (tools/peak_fp64.cu); MEASURED_PEAKS.json has no FP64 entry",
             "launches_per_step": gp["launches"], "gemm_ms_per_step": gp["ms"],
             "share_of_step": gp["ms"] / step_ms if step_ms > 0 else None}
@@ -455,6 +455,16 @@ def apply_roofline(ctx, L, n, R=64, r=16, reps=10):
                            "achieved": kr_gbs, "peak": peak_hbm, "unit": "GB/s", "frac": kr_gbs / peak_hbm,
                            "ms_per_launch": kp["ms"] / max(kp["launches"], 1),
                            "bytes_per_launch": kp["bytes"] / max(kp["launches"], 1)}}
+
+
+def gemm_class_traffic():
+    """DRAM bytes (read + write) per launch of the 64 x 64 DMMA GEMM kernel averaged over one C4
+    setup + solve, from the committed ncu capture (profiles/r02c_gemm_class_traffic.json), or None."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "r02c_gemm_class_traffic.json")))
+        return d["dram_bytes_per_launch"]
+    except (OSError, ValueError, KeyError):
+        return None
 
 
 def kr_traffic(n, R, r):

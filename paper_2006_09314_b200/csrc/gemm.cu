@@ -757,7 +757,7 @@ void gemm_profile(bool enable, double* ms, double* flops, long long* launches) {
     std::vector<std::pair<double, std::string>> v;
     for (auto& kv : hist) v.push_back({kv.second.first, kv.first + " x" + std::to_string(kv.second.second)});
     std::sort(v.rbegin(), v.rend());
-    for (size_t i = 0; i < v.size() && i < 40; ++i) fprintf(stderr, "[fc gemm] %8.2f ms  %s\n", v[i].first, v[i].second.c_str());
+    for (size_t i = 0; i < v.size() && i < 400; ++i) fprintf(stderr, "[fc gemm] %8.2f ms  %s\n", v[i].first, v[i].second.c_str());
   }
   P.shape.clear();
   if (ms) *ms = t;
