@@ -1538,13 +1538,20 @@ TT truncate_tt(fc_ctx c, const TT& xin, double eps, int rank_cap, TruncStats* st
           fclose(f);
         }
       }
-      // Rm = Qo^T K (k x qin) ; Co = Rm C (k x R)
-      double* Rm = s.zeros<double>((size_t)k * xin.q[l]);
-      dgemm(st, 1, 0, k, xin.q[l], n, 1.0, Qo[l], n, xin.Q[l], n, 1.0, Rm, k,
-            std::max(1, std::min(cdiv(n, 256), 16)));
+    }
+    // Rm = Qo^T K (k x qin) ; Co = Rm C (k x R): the modes that got a new basis in one batched
+    // GEMM each (deterministic split-K: no pre-zeroed C)
+    GemmArgs gr, gc;
+    gr.transA = 1;
+    double* Rm[3] = {nullptr, nullptr, nullptr};
+    for (int l = 0; l < 3; ++l) {
+      if (map[l] < 0) continue;
+      const int k = q[l];
+      Rm[l] = s.alloc<double>((size_t)k * xin.q[l]);
+      gr.b[gr.nbatch++] = GemmBatch{k, xin.q[l], n, Qo[l], n, xin.Q[l], n, Rm[l], k, nullptr, 0, nullptr};
       if (!ss) {
         Co[l] = s.alloc<double>((size_t)k * R);
-        dgemm(st, 0, 0, k, R, xin.q[l], 1.0, Rm, k, xin.C[l], xin.q[l], 0.0, Co[l], k);
+        gc.b[gc.nbatch++] = GemmBatch{k, R, xin.q[l], Rm[l], k, xin.C[l], xin.q[l], Co[l], k, nullptr, 0, nullptr};
       } else {
         // structured Hadamard: K columns a*t + b; Rm viewed (k t) x s times E (s x r) gives
         // RmE = [Rm_1 | ... | Rm_r], Rm_kk = sum_a E[a,kk] Rm[:, a*t:(a+1)*t] (k x t);
@@ -1553,8 +1560,12 @@ TT truncate_tt(fc_ctx c, const TT& xin, double eps, int rank_cap, TruncStats* st
         const int t = ss->t[l], sl = ss->s[l], r = ss->r;
         Co[l] = nullptr;
         RmE[l] = s.alloc<double>((size_t)k * t * r);
-        dgemm(st, 0, 0, k * t, r, sl, 1.0, Rm, k * t, ss->E[l], sl, 0.0, RmE[l], k * t);
+        gc.b[gc.nbatch++] = GemmBatch{k * t, r, sl, Rm[l], k * t, ss->E[l], sl, RmE[l], k * t, nullptr, 0, nullptr};
       }
+    }
+    if (gr.nbatch) {
+      gemm(gr, st);
+      gemm(gc, st);
     }
   }
   for (int l = 0; l < 3; ++l) {
