@@ -279,11 +279,6 @@ __global__ void __launch_bounds__(NT) dgemm_dmma_kernel(const __grid_constant__ 
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-  // 8 x 8 fragments of this warp's 32 x 32 sub-tile that reach into the matrix (warp-uniform): a
-  // ragged edge tile (M = 80: a 64-row and a 16-row tile) spends the tensor pipe only on those
-  const int mrem = Meff - (m0 + wm), nrem = g.N - (n0 + wn);
-  const int ni = mrem <= 0 ? 0 : min(4, (mrem + 7) >> 3), nj = nrem <= 0 ? 0 : min(4, (nrem + 7) >> 3);
-  const bool full = ni == 4 && nj == 4;
 
   // prologue
 #pragma unroll
@@ -316,43 +311,20 @@ __global__ void __launch_bounds__(NT) dgemm_dmma_kernel(const __grid_constant__ 
     const double* a_s = As + st * STAGE_ELEMS;
     const double* b_s = Bs + st * STAGE_ELEMS;
     const double* k_s = Ks + st * STAGE_ELEMS;
-    if (full) {
 #pragma unroll
-      for (int kq = 0; kq < BK; kq += 4) {
-        double af[4], bf[4];
+    for (int kq = 0; kq < BK; kq += 4) {
+      double af[4], bf[4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) af[i] = a_s[(kq + fc4) * LDS + wm + i * 8 + fr];
+      for (int i = 0; i < 4; ++i) af[i] = a_s[(kq + fc4) * LDS + wm + i * 8 + fr];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int o = (kq + fc4) * LDS + wn + j * 8 + fr;
-          bf[j] = KR ? b_s[o] * k_s[o] : b_s[o];
-        }
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-          for (int j = 0; j < 4; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+      for (int j = 0; j < 4; ++j) {
+        const int o = (kq + fc4) * LDS + wn + j * 8 + fr;
+        bf[j] = KR ? b_s[o] * k_s[o] : b_s[o];
       }
-    } else if (ni > 0 && nj > 0) {
-      // ragged edge tile: only the 8-row / 8-column fragments that reach into the matrix
 #pragma unroll
-      for (int kq = 0; kq < BK; kq += 4) {
-        double af[4], bf[4];
+      for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int i = 0; i < 4; ++i) af[i] = i < ni ? a_s[(kq + fc4) * LDS + wm + i * 8 + fr] : 0.0;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int o = (kq + fc4) * LDS + wn + j * 8 + fr;
-          bf[j] = j < nj ? (KR ? b_s[o] * k_s[o] : b_s[o]) : 0.0;
-        }
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          if (i < ni) {
-#pragma unroll
-            for (int j = 0; j < 4; ++j)
-              if (j < nj) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
-          }
-        }
-      }
+        for (int j = 0; j < 4; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
     }
   }
   cp_async_wait<0>();
