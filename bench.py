@@ -318,6 +318,9 @@ def main():
     variant = rg_variant(L, p, stream)
     # the north-star's mode-transform kernel at a C5 cell (inverse transform + Khatri-Rao operand)
     roof_apply = apply_roofline(ctx, L, p.n)
+    # the same two kernels at the largest n = 1024 cell of the C5 sweep (R = 256, r = 32: 201 MB
+    # written by the K6 product, 1536 output tiles): launch latency no longer dominates the K6 time
+    roof_apply_large = apply_roofline(ctx, L, p.n, R=256, r=32, reps=5)
     if rank != 0:
         return
     line = {
@@ -341,6 +344,7 @@ def main():
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
         "roofline": roof,
         "roofline_apply": roof_apply,
+        "roofline_apply_large": roof_apply_large,
         "roofline_hbm": roof_hbm,
         "variant_rG24": variant,
         "clocks": clk.summary(),
