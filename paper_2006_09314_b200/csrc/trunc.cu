@@ -172,6 +172,77 @@ __device__ __forceinline__ dd dd_sqrt(dd a) {
   return dd_fast2sum(s, e);
 }
 
+// entry e of the row-major lower triangle -> (a, b), a >= b
+__device__ __forceinline__ void tri_entry(int e, int& a, int& b) {
+  a = (int)((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
+  while ((a + 1) * (a + 2) / 2 <= e) ++a;
+  while (a * (a + 1) / 2 > e) --a;
+  b = e - a * (a + 1) / 2;
+}
+
+// Partial dd Grams over column chunks: CTA (k, sp) accumulates H_k's lower triangle over the W_k
+// columns [sp chunk, (sp + 1) chunk) and writes (hi, lo) to Hp[((k S + sp) 2 + {0, 1}) t^2 + a + b t].
+// One CTA per spectral term left 13 of 148 SMs busy for ~4 ms per launch at eps = 1e-8 (a quarter
+// of that solve); the factor kernel below adds the S partials in split order (dd, fixed order).
+template <int ENT>
+__global__ void __launch_bounds__(kFactorThreads) struct_gram_dd_kernel(int t, int Rx, int chunk,
+                                                                        const double* __restrict__ Cx,
+                                                                        const double* __restrict__ d, double* Hp) {
+  extern __shared__ double fsm[];
+  const int k = blockIdx.x, sp = blockIdx.y, S = gridDim.y, tid = threadIdx.x;
+  const int ne = t * (t + 1) / 2;
+  const int jlo = sp * chunk, jhi = min(Rx, jlo + chunk);
+  double* Wc = fsm;                                  // t x kFactorJC chunk of W_k
+  const double* dk = d + (size_t)k * Rx;
+  double* Ph = Hp + ((size_t)k * S + sp) * 2 * t * t;
+  double* Pl = Ph + (size_t)t * t;
+  for (int e0 = 0; e0 < ne; e0 += ENT * kFactorThreads) {
+    int ea[ENT], eb[ENT];
+    dd acc[ENT];
+#pragma unroll
+    for (int q = 0; q < ENT; ++q) {
+      const int e = e0 + tid + q * kFactorThreads;
+      int a = 0, b = 0;
+      if (e < ne) tri_entry(e, a, b);
+      ea[q] = a;
+      eb[q] = b;
+      acc[q] = {0.0, 0.0};
+    }
+    for (int j0 = jlo; j0 < jhi; j0 += kFactorJC) {
+      const int jc = min(kFactorJC, jhi - j0);
+      __syncthreads();
+      for (int idx = tid; idx < t * jc; idx += kFactorThreads) {
+        const int a = idx % t, jj = idx / t;
+        Wc[a + jj * t] = Cx[a + (size_t)(j0 + jj) * t] * dk[j0 + jj];
+      }
+      __syncthreads();
+#pragma unroll
+      for (int q = 0; q < ENT; ++q) {
+        if (e0 + tid + q * kFactorThreads >= ne) break;
+        const int a = ea[q], b = eb[q];
+        double hi = acc[q].hi, lo = acc[q].lo;
+        for (int jj = 0; jj < jc; ++jj) {
+          const double x = Wc[a + jj * t], y = Wc[b + jj * t];
+          const double p = x * y, pe = fma(x, y, -p);
+          const double s = hi + p, bb = s - hi;
+          lo += ((hi - (s - bb)) + (p - bb)) + pe;
+          hi = s;
+        }
+        acc[q].hi = hi;
+        acc[q].lo = lo;
+      }
+#pragma unroll
+      for (int q = 0; q < ENT; ++q) acc[q] = dd_fast2sum(acc[q].hi, acc[q].lo);
+    }
+#pragma unroll
+    for (int q = 0; q < ENT; ++q) {
+      if (e0 + tid + q * kFactorThreads >= ne) break;
+      Ph[ea[q] + eb[q] * t] = acc[q].hi;
+      Pl[ea[q] + eb[q] * t] = acc[q].lo;
+    }
+  }
+}
+
 // one CTA per spectral term k: L_k (t x t, column-major, ld t; columns beyond the numerical rank
 // are zero) with L_k L_k^T = W_k W_k^T, W_k[a, j] = Cx[a + j t] d[k Rx + j].  The dd Gram (hi, lo)
 // is in shared memory for t <= kFactorSmemT, else in this CTA's slice of Hg (2 t^2 doubles per
@@ -179,7 +250,8 @@ __device__ __forceinline__ dd dd_sqrt(dd a) {
 template <int ENT>
 __global__ void __launch_bounds__(kFactorThreads) struct_factor_kernel(int t, int Rx, const double* __restrict__ Cx,
                                                                        const double* __restrict__ d, double* Lout,
-                                                                       double* Hg) {
+                                                                       double* Hg, const double* __restrict__ Hp,
+                                                                       int S) {
   extern __shared__ double fsm[];
   const int k = blockIdx.x, tid = threadIdx.x;
   const int ne = t * (t + 1) / 2;
@@ -191,7 +263,22 @@ __global__ void __launch_bounds__(kFactorThreads) struct_factor_kernel(int t, in
   double* Hh = gl ? Hg + (size_t)k * 2 * t * t : piv + 2 * t;   // t x t (hi), later the Schur complement
   double* Hl = Hh + (size_t)t * t;                   // t x t (lo)
   const double* dk = d + (size_t)k * Rx;
-  for (int e0 = 0; e0 < ne; e0 += ENT * kFactorThreads) {
+  if (Hp) {
+    // the Gram comes as S partial dd sums over column chunks (struct_gram_dd_kernel): added in
+    // split order
+    for (int e = tid; e < ne; e += kFactorThreads) {
+      int a, b;
+      tri_entry(e, a, b);
+      dd acc = {0.0, 0.0};
+      for (int sp = 0; sp < S; ++sp) {
+        const double* Ph = Hp + ((size_t)k * S + sp) * 2 * t * t;
+        acc = dd_add(acc, {Ph[a + b * t], Ph[(size_t)t * t + a + b * t]});
+      }
+      Hh[a + b * t] = Hh[b + a * t] = acc.hi;
+      Hl[a + b * t] = Hl[b + a * t] = acc.lo;
+    }
+  }
+  for (int e0 = 0; e0 < (Hp ? 0 : ne); e0 += ENT * kFactorThreads) {
     // entry e -> (a, b), a >= b, row-major over the lower triangle
     int ea[ENT], eb[ENT];
     dd acc[ENT];
@@ -1871,10 +1958,37 @@ TT truncate_tt(fc_ctx c, const TT& xin, double eps, int rank_cap, TruncStats* st
           // pass (the entries are independent accumulation chains; idle slots would cost issue slots)
           const int ne = t * (t + 1) / 2;
           const int ept = cdiv(ne, kFactorThreads);
-          if (ept <= 1) struct_factor_kernel<1><<<rr, kFactorThreads, fsmem, st>>>(t, Rx, ss->Cx[l], dl[l], Lf, Hg);
-          else if (ept <= 2) struct_factor_kernel<2><<<rr, kFactorThreads, fsmem, st>>>(t, Rx, ss->Cx[l], dl[l], Lf, Hg);
-          else if (ept <= 4) struct_factor_kernel<4><<<rr, kFactorThreads, fsmem, st>>>(t, Rx, ss->Cx[l], dl[l], Lf, Hg);
-          else struct_factor_kernel<kFactorEnt><<<rr, kFactorThreads, fsmem, st>>>(t, Rx, ss->Cx[l], dl[l], Lf, Hg);
+          // the Gram accumulation split over column chunks (>= 4 staged chunks of W each) so that
+          // the r terms fill two waves of the SMs; FC_FACTOR_SPLIT=0: one CTA per term does both
+          static const bool fsplit_on = !(getenv("FC_FACTOR_SPLIT") && atoi(getenv("FC_FACTOR_SPLIT")) == 0);
+          int S = fsplit_on ? std::min(cdiv(Rx, 4 * kFactorJC), std::max(1, cdiv(2 * 148, rr))) : 1;
+          S = (int)std::min<size_t>((size_t)S, std::max<size_t>(1, ((size_t)1 << 25) / ((size_t)rr * 2 * t * t)));   // partials <= 256 MB
+          double* Hp = nullptr;
+          if (S > 1) {
+            const int chunk = cdiv(cdiv(Rx, S), kFactorJC) * kFactorJC;
+            S = cdiv(Rx, chunk);
+            Hp = s.alloc<double>((size_t)rr * S * 2 * t * t);
+            const size_t gsm = (size_t)t * kFactorJC * 8;
+            static bool gattr = false;
+            if (!gattr) {
+              const int gmax = (int)((size_t)kFactorMaxT * kFactorJC * 8);
+              FC_CUDA_TRY(cudaFuncSetAttribute(struct_gram_dd_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, gmax));
+              FC_CUDA_TRY(cudaFuncSetAttribute(struct_gram_dd_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, gmax));
+              FC_CUDA_TRY(cudaFuncSetAttribute(struct_gram_dd_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, gmax));
+              FC_CUDA_TRY(cudaFuncSetAttribute(struct_gram_dd_kernel<kFactorEnt>, cudaFuncAttributeMaxDynamicSharedMemorySize, gmax));
+              gattr = true;
+            }
+            const dim3 gg(rr, S);
+            if (ept <= 1) struct_gram_dd_kernel<1><<<gg, kFactorThreads, gsm, st>>>(t, Rx, chunk, ss->Cx[l], dl[l], Hp);
+            else if (ept <= 2) struct_gram_dd_kernel<2><<<gg, kFactorThreads, gsm, st>>>(t, Rx, chunk, ss->Cx[l], dl[l], Hp);
+            else if (ept <= 4) struct_gram_dd_kernel<4><<<gg, kFactorThreads, gsm, st>>>(t, Rx, chunk, ss->Cx[l], dl[l], Hp);
+            else struct_gram_dd_kernel<kFactorEnt><<<gg, kFactorThreads, gsm, st>>>(t, Rx, chunk, ss->Cx[l], dl[l], Hp);
+            FC_CHECK_LAUNCH();
+          }
+          if (ept <= 1) struct_factor_kernel<1><<<rr, kFactorThreads, fsmem, st>>>(t, Rx, ss->Cx[l], dl[l], Lf, Hg, Hp, S);
+          else if (ept <= 2) struct_factor_kernel<2><<<rr, kFactorThreads, fsmem, st>>>(t, Rx, ss->Cx[l], dl[l], Lf, Hg, Hp, S);
+          else if (ept <= 4) struct_factor_kernel<4><<<rr, kFactorThreads, fsmem, st>>>(t, Rx, ss->Cx[l], dl[l], Lf, Hg, Hp, S);
+          else struct_factor_kernel<kFactorEnt><<<rr, kFactorThreads, fsmem, st>>>(t, Rx, ss->Cx[l], dl[l], Lf, Hg, Hp, S);
           FC_CHECK_LAUNCH();
           pm.mark("4b3 refine: dd factor");
           double* Ct = s.alloc<double>((size_t)m * t * rr);
