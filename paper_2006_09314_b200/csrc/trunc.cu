@@ -407,18 +407,24 @@ __global__ void __launch_bounds__(kFactorThreads) struct_factor_kernel(int t, in
     }
     __syncthreads();
     // Schur complement on the unpivoted lower triangle: pairs (qa >= qb) of the remaining list
+    // (a warp per row qa of the list, rows dealt from both ends so that every warp gets the same
+    // number of pairs; lanes over qb <= qa: no index decoding per pair)
     const int nr = nrem - 1;
-    const int np = nr * (nr + 1) / 2;
-    for (int e = tid; e < np; e += kFactorThreads) {
-      int qa = (int)((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
-      while ((qa + 1) * (qa + 2) / 2 <= e) ++qa;
-      while (qa * (qa + 1) / 2 > e) --qa;
-      const int qb = e - qa * (qa + 1) / 2;
-      const int i = rem[qa], j = rem[qb];
-      const size_t ij = (size_t)i + (size_t)j * t;
-      const dd v = dd_add({Hh[ij], Hl[ij]}, dd_mul({-Lc[2 * i], -Lc[2 * i + 1]}, {Lc[2 * j], Lc[2 * j + 1]}));
-      Hh[ij] = Hh[j + (size_t)i * t] = v.hi;
-      Hl[ij] = Hl[j + (size_t)i * t] = v.lo;
+    constexpr int NWF = kFactorThreads / 32;
+    for (int h = warp; h < (nr + 1) / 2; h += NWF) {
+      for (int side = 0; side < 2; ++side) {
+        const int qa = side == 0 ? h : nr - 1 - h;
+        if (side == 1 && qa == h) break;              // middle row of an odd count: once
+        const int i = rem[qa];
+        const double lih = -Lc[2 * i], lil = -Lc[2 * i + 1];
+        for (int qb = lane; qb <= qa; qb += 32) {
+          const int j = rem[qb];
+          const size_t ij = (size_t)i + (size_t)j * t, ji = (size_t)j + (size_t)i * t;   // equal entries
+          const dd v = dd_add({Hh[ji], Hl[ji]}, dd_mul({lih, lil}, {Lc[2 * j], Lc[2 * j + 1]}));
+          Hh[ij] = Hh[ji] = v.hi;
+          Hl[ij] = Hl[ji] = v.lo;
+        }
+      }
     }
     __syncthreads();
   }
