@@ -269,9 +269,9 @@ int fc_dgemm_splitk(fc_ctx ctx, int transA, int transB, int M, int N, int K, dou
                     const double* A, int lda, const double* B, int ldb, double beta, double* C, int ldc,
                     int splitk);
 /* fc_dgemm with the stream-K request the inverse mode transform of fracop_apply makes [P:597-628:
- * Y_l = V_l Yhat_l, the dense contraction of the factored matvec]: when M, N >= 128, K >= 64,
- * 2 M N K >= 2^28 and the launch has >= 8 k-steps of 16 per SM, one persistent CTA per SM gets an equal contiguous range of the launch's
- * (tile, k-step) iterations; partial tiles go through a device workspace and are added by the
+ * Y_l = V_l Yhat_l, the dense contraction of the factored matvec]: when M, N > 64, K >= 64,
+ * 2 M N K >= 2^28 and the launch has >= 8 k-steps of 16 per SM, one persistent CTA per SM gets an
+ * equal contiguous range of the launch's (128 x 128 tile, k-step) iterations; partial tiles go through a device workspace and are added by the
  * tile's owner CTA in CTA order (bit-identical run to run).  Otherwise identical to fc_dgemm.
  * Same arguments, layout and errors as fc_dgemm. */
 int fc_dgemm_streamk(fc_ctx ctx, int transA, int transB, int M, int N, int K, double alpha,

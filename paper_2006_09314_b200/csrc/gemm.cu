@@ -873,11 +873,11 @@ static void gemm_dispatch(const GemmArgs& a_in, cudaStream_t st) {
   bool dyn = false;
   for (int i = 0; i < a.nbatch; ++i) dyn |= a.b[i].dynM != nullptr || a.b[i].dynK != nullptr;
   a.splitk = std::max(1, a.splitk);
-  // stream-K (on request; FC_STREAMK=0 disables): same-shape entries on 128 x 128 tiles with at
-  // least 8 k-steps per SM.  It beat whole-tile launches on every C5 cell it accepts, also where
+  // stream-K (on request; FC_STREAMK=0 disables): entries with one tile grid and one K on 128 x 128
+  // tiles (M, N > 64: more than one 64 x 64 tile) with at least 8 k-steps per SM.  It beat whole-tile launches on every C5 cell it accepts, also where
   // the tiles fill their waves (n = 2048, R r = 8192: 76.5 -> 81.6 % of the DMMA peak; no launch
   // tail, the fix-up of one tile overlaps the other CTAs' main loops)
-  if (!dyn && a.gen.kind < 0 && a.krR == 0 && a.streamk && maxM >= 128 && maxN >= 128 && minK >= 64 &&
+  if (!dyn && a.gen.kind < 0 && a.krR == 0 && a.streamk && maxM > 64 && maxN > 64 && minK >= 64 &&
       work >= (1LL << 27)) {
     static const bool sk_on = !(getenv("FC_STREAMK") && atoi(getenv("FC_STREAMK")) == 0);
     static const int sms = [] {
@@ -886,9 +886,10 @@ static void gemm_dispatch(const GemmArgs& a_in, cudaStream_t st) {
       return std::max(v, 2);
     }();
     static const int min_it = getenv("FC_STREAMK_MINIT") ? atoi(getenv("FC_STREAMK_MINIT")) : 8;   // diagnostic
-    bool same = true;
+    bool same = true;   // one tile grid and one K for all entries (M, N may differ inside the last tiles)
     for (int i = 1; i < a.nbatch; ++i)
-      same &= a.b[i].M == a.b[0].M && a.b[i].N == a.b[0].N && a.b[i].K == a.b[0].K;
+      same &= cdiv(a.b[i].M, big::BM) == cdiv(a.b[0].M, big::BM) && cdiv(a.b[i].N, big::BN) == cdiv(a.b[0].N, big::BN) &&
+              a.b[i].K == a.b[0].K;
     const long long tiles = (long long)a.nbatch * a.rep * cdiv(maxM, big::BM) * cdiv(maxN, big::BN);
     const long long kit = cdiv(a.b[0].K, big::BK);
     if (sk_on && same && tiles * kit >= (long long)min_it * sms) {

@@ -1526,6 +1526,8 @@ TT truncate_tt(fc_ctx c, const TT& xin, double eps, int rank_cap, TruncStats* st
         gh.b[l].sA = gh.b[l].sB = (long long)t * Rx;
         gh.b[l].sC = (long long)t * t;
       }
+      static const bool gram_sk = !(getenv("FC_GRAM_STREAMK") && atoi(getenv("FC_GRAM_STREAMK")) == 0);
+      gh.streamk = gram_sk;   // as the Gm Grams above
       gemm(gh, st);
     }
   };
@@ -1556,6 +1558,10 @@ TT truncate_tt(fc_ctx c, const TT& xin, double eps, int rank_cap, TruncStats* st
       gg.b[l].sA = gg.b[l].sB = (long long)n * t;
       gg.b[l].sC = (long long)t * t;
     }
+    // t in (64, 128]: one k-step-balanced 128 x 128 tile per term instead of four 64 x 64 tiles,
+    // three of them ragged (gemm.cu stream-K; FC_GRAM_STREAMK=0: the 64 x 64 kernel)
+    static const bool gram_sk = !(getenv("FC_GRAM_STREAMK") && atoi(getenv("FC_GRAM_STREAMK")) == 0);
+    gg.streamk = gram_sk;
     gemm(gk, st);
     gemm(gg, st);
     struct_norms(Gm);
