@@ -1397,8 +1397,16 @@ void tt_compute_core(cudaStream_t st, TT& x) {
     kr12_kernel<<<blocks_for((long long)r12 * m), 256, 0, st>>>(x.q[0], x.q[1], m, x.w + t0, x.C[0] + (size_t)t0 * x.q[0],
                                                                  x.C[1] + (size_t)t0 * x.q[1], KR);
     FC_CHECK_LAUNCH();
-    dgemm(st, 0, 1, (int)r12, x.q[2], m, 1.0, KR, (int)r12, x.C[2] + (size_t)t0 * x.q[2], x.q[2], 1.0, x.core,
-          (int)r12, std::max(1, std::min(cdiv(m, 64), 8)));
+    // r3 in (64, 128]: k-step-balanced 128 x 128 tiles (stream-K, gemm.cu); else split-K 64 x 64 tiles
+    GemmArgs gk;
+    gk.transB = 1;
+    gk.beta = 1.0;
+    gk.nbatch = 1;
+    gk.b[0] = GemmBatch{(int)r12, x.q[2], m, KR, (int)r12, x.C[2] + (size_t)t0 * x.q[2], x.q[2], x.core, (int)r12,
+                        nullptr, 0, nullptr};
+    gk.splitk = std::max(1, std::min(cdiv(m, 64), 8));
+    gk.streamk = 1;
+    gemm(gk, st);
   }
 }
 
@@ -1497,7 +1505,21 @@ TT truncate_tt(fc_ctx c, const TT& xin, double eps, int rank_cap, TruncStats* st
         gp.b[l].sC = (long long)t * Rx;
         na.Cx[l] = ss->Cx[l]; na.P[l] = P[l]; na.t[l] = t; na.n2[l] = n2[l] + (size_t)k0 * Rx;
       }
-      gemm(gp, st);
+      // t in (64, 128]: a stream-K launch per mode (K = t differs between the modes); else one
+      // batched launch of 64 x 64 tiles
+      static const bool gram_sk = !(getenv("FC_GRAM_STREAMK") && atoi(getenv("FC_GRAM_STREAMK")) == 0);
+      const int tmax = std::max(ss->t[0], std::max(ss->t[1], ss->t[2]));
+      if (gram_sk && tmax > 64 && tmax <= 128) {
+        for (int l = 0; l < 3; ++l) {
+          GemmArgs g1 = gp;
+          g1.nbatch = 1;
+          g1.b[0] = gp.b[l];
+          g1.streamk = 1;
+          gemm(g1, st);
+        }
+      } else {
+        gemm(gp, st);
+      }
       struct_norms_kernel<<<dim3(cdiv(nk * Rx, 8), 3), 256, 0, st>>>(nk * Rx, Rx, na);
       FC_CHECK_LAUNCH();
     }
@@ -2268,8 +2290,16 @@ TT truncate_tt(fc_ctx c, const TT& xin, double eps, int rank_cap, TruncStats* st
       // split-K sized for ~8 waves of 148 SMs (1-2 waves of 64x64 tiles left a half-empty last wave;
       // C4 solve 311 ms vs 313 ms with 2 or 4 waves)
       static const int core_waves = getenv("FC_CORE_WAVES") ? atoi(getenv("FC_CORE_WAVES")) : 8;
-      dgemm(st, 0, 1, (int)r12, r[2], m, 1.0, KR, (int)r12, Chat[2] + (size_t)tt0 * r[2], r[2], 1.0, core, (int)r12,
-            std::max(1, std::min(cdiv(m, 64), std::max(1, cdiv(core_waves * 148, std::max(tiles, 1))))));
+      // (r3 in (64, 128]: the stream-K 128 x 128 kernel instead, one tile column)
+      GemmArgs gz;
+      gz.transB = 1;
+      gz.beta = 1.0;
+      gz.nbatch = 1;
+      gz.b[0] = GemmBatch{(int)r12, r[2], m, KR, (int)r12, Chat[2] + (size_t)tt0 * r[2], r[2], core, (int)r12,
+                          nullptr, 0, nullptr};
+      gz.splitk = std::max(1, std::min(cdiv(m, 64), std::max(1, cdiv(core_waves * 148, std::max(tiles, 1)))));
+      gz.streamk = 1;
+      gemm(gz, st);
     }
   }
   pm.mark(ss ? "6 core (structured)" : "6 core (cp)");
