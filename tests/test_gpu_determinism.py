@@ -93,3 +93,29 @@ def test_pcg_solve_bit_identical(lib, n, eps):
     for k in ("rel_res", "rank_X", "rank_R", "rank_S", "rank_Z", "rank_P", "tucker_S"):
         assert r0[k] == r1[k], k
     assert np.array_equal(u0[0], u1[0])
+
+
+def test_streamk_solve_matches_whole_tile_launches():
+    """The stream-K 128 x 128 GEMM in the truncation (per-term Grams, term-norm products and the
+    core contraction once a Tucker rank exceeds 64, late in the C4 solve) against the same solve
+    with every launch on whole tiles (FC_STREAMK=0, read once per process: two subprocesses):
+    same iteration count, the five rank histories equal up to +-1 at a truncation (a different
+    summation order may flip a marginal cut), residual histories equal to the 6 printed digits."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    reps = []
+    for v in ("1", "0"):
+        env = dict(os.environ, FC_STREAMK=v)
+        out = subprocess.run([sys.executable, os.path.join(root, "tools", "c4_trace.py"), "1e-6", "1024"],
+                             env=env, capture_output=True, text=True, timeout=600)
+        assert out.returncode == 0, out.stderr[-2000:]
+        reps.append(json.loads(next(l for l in out.stdout.splitlines() if l.startswith("{"))))
+    a, b = reps
+    assert a["rc"] == 0 and b["rc"] == 0 and a["iters"] == b["iters"]
+    assert max(a["tucker_S"]) > 64, "the workload no longer reaches the stream-K Gram path"
+    for k in ("rank_X", "rank_R", "rank_S", "rank_Z", "rank_P"):
+        assert all(abs(x - y) <= 1 for x, y in zip(a[k], b[k])), (k, a[k], b[k])
+    assert np.allclose(a["rel_res"], b["rel_res"], rtol=1e-5, atol=0.0)
