@@ -913,46 +913,64 @@ __global__ void __launch_bounds__(1024) slice_svd_qrj_kernel(int ra, int rb, con
     order[rk] = j;
   }
   __syncthreads();
-  // tall-side vectors: Q w_j = H_0 (H_1 ... (H_{c-1} [w_j; 0])), warp per vector, in place in a
-  // rows-length scratch: reuse X's column?  No: build in global output directly (warp-private)
-  for (int m = warp; m < k; m += nw) {
-    const int j = order[m];
-    double* out = tr ? (Vb + (size_t)nu * rb * k + (size_t)m * rb) : (Ua + (size_t)nu * ra * k + (size_t)m * ra);
-    if (rows <= 128) {
-      // register-resident vector (element ln + 32 c in slot c): no global round trip per reflector
-      double ov[4];
+  // tall-side vectors: Q w_j = H_0 (H_1 ... (H_{c-1} [w_j; 0])).  rows <= 128: register-resident
+  // vectors (element ln + 32 c in slot c), two vectors per warp at a time — their reflector
+  // applications (dot, butterfly, update) are independent chains and share the loads of v_i
+  if (rows <= 128) {
+    for (int mb = warp; mb < k; mb += 2 * nw) {
+      const int m1 = mb + nw;
+      const bool two = m1 < k;
+      const int j0 = order[mb], j1 = two ? order[m1] : j0;
+      double o0[4], o1[4];
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         const int t = ln + 32 * c;
-        ov[c] = (t < rows && t < cols) ? W[t + (size_t)j * lx] : 0.0;
+        const bool in = t < rows && t < cols;
+        o0[c] = in ? W[t + (size_t)j0 * lx] : 0.0;
+        o1[c] = (in && two) ? W[t + (size_t)j1 * lx] : 0.0;
       }
       for (int i = cols - 1; i >= 0; --i) {
         const double tv = tau[i];
         if (tv == 0.0) continue;
         const double* v = A + (size_t)i * rows;   // v_i[i] = 1, v_i[t] = A[t, i] for t > i
-        double d = 0.0;
+        double vv[4];
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           const int t = ln + 32 * c;
-          if (t == i) d += ov[c];
-          else if (t > i && t < rows) d = fma(v[t], ov[c], d);
+          vv[c] = t == i ? 1.0 : ((t > i && t < rows) ? v[t] : 0.0);
         }
-        for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
-        const double f = tv * d;
+        double d0 = 0.0, d1 = 0.0;
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
-          const int t = ln + 32 * c;
-          if (t == i) ov[c] -= f;
-          else if (t > i && t < rows) ov[c] -= f * v[t];
+          d0 = fma(vv[c], o0[c], d0);
+          d1 = fma(vv[c], o1[c], d1);
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+          d0 += __shfl_xor_sync(0xffffffffu, d0, o);
+          d1 += __shfl_xor_sync(0xffffffffu, d1, o);
+        }
+        const double f0 = tv * d0, f1 = tv * d1;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          o0[c] = fma(-f0, vv[c], o0[c]);
+          o1[c] = fma(-f1, vv[c], o1[c]);
         }
       }
+      double* out0 = tr ? (Vb + (size_t)nu * rb * k + (size_t)mb * rb) : (Ua + (size_t)nu * ra * k + (size_t)mb * ra);
+      double* out1 = tr ? (Vb + (size_t)nu * rb * k + (size_t)m1 * rb) : (Ua + (size_t)nu * ra * k + (size_t)m1 * ra);
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         const int t = ln + 32 * c;
-        if (t < rows) out[t] = ov[c];
+        if (t < rows) {
+          out0[t] = o0[c];
+          if (two) out1[t] = o1[c];
+        }
       }
-      continue;
     }
+  }
+  for (int m = warp; m < (rows <= 128 ? 0 : k); m += nw) {
+    const int j = order[m];
+    double* out = tr ? (Vb + (size_t)nu * rb * k + (size_t)m * rb) : (Ua + (size_t)nu * ra * k + (size_t)m * ra);
     for (int t = ln; t < rows; t += 32) out[t] = t < cols ? W[t + (size_t)j * lx] : 0.0;
     __syncwarp();
     for (int i = cols - 1; i >= 0; --i) {
